@@ -1,0 +1,138 @@
+/*
+ * mrrr.h -- C ABI of libmrrr.so: k eigenpairs of a real symmetric tridiagonal
+ * matrix T by the mixed-precision MRRR (MR^3) algorithm of arXiv 1401.4950
+ * (Petschow, "MRRR-based Eigensolvers for Multi-core Processors and
+ * Supercomputers"), computed on an NVIDIA B200 (sm_100a).
+ *
+ * Method (PAPER.md lines "P:a-b"):
+ *   Alg. mrrr P:2762-2816 / Alg. mrrr2: root representation
+ *   LDL^T = T - mu I, random relative perturbation, Sturm-count bisection
+ *   (Alg. Bisection, Alg. negcountLDL), classification
+ *   (P:3272-3292), child representations for clusters (Alg. spectrumshift
+ *   P:3499-3590), and Rayleigh-quotient iteration driven by the twisted
+ *   factorization (Alg. Getvec, Alg. stask) for every
+ *   singleton, in the thesis's mixed precision form: fp64 input and output,
+ *   double-double internal arithmetic for representations and vectors
+ *   (Ch.5 P:5516-6163; double/quadruple realisation P:6270-6278).
+ *   The exact step list and every reading of the paper are in DESIGN.md.
+ *
+ * Conventions
+ *   T is given by its diagonal d[0..n-1] (alpha_1..alpha_n) and off-diagonal
+ *   e[0..n-2] (beta_1..beta_{n-1}), eq:thetridiagonal P:1969-1979.
+ *   Indices il..iu are 1-based and inclusive (LAPACK style); k = iu - il + 1.
+ *   Outputs: W[0..k-1] ascending, W[j] = lambda_{il+j}; column j of Z
+ *   (column-major, leading dimension ldz >= n) is its unit eigenvector, with
+ *   the sign fixed by z(r) > 0 at the twist index r (Getvec sets z(r) = 1,
+ *   P:3434).  d and e are read only.
+ *
+ * Return codes: 0 success; -i: argument i of the call is invalid (counting the
+ * handle as 1); > 0: one of MRRR_ERR_* below.
+ *
+ * Threading: a handle is not re-entrant; use one handle per host thread.
+ */
+#ifndef MRRR_H
+#define MRRR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mrrr_ctx *mrrr_t;
+
+#define MRRR_OK 0
+#define MRRR_ERR_NONFINITE 1  /* NaN or Inf in d or e */
+#define MRRR_ERR_CUDA 2       /* CUDA runtime error; see mrrr_strerror(MRRR_ERR_CUDA) */
+#define MRRR_ERR_NOMEM 3      /* device memory exhausted (workspace or outputs) */
+#define MRRR_ERR_ROOT 4       /* no definite root shift found (S3) */
+#define MRRR_ERR_NODEVICE 5   /* no CUDA device */
+
+#define MRRR_KEEP_DIAG 1u     /* keep integer/interval diagnostics for mrrr_get_diag */
+
+/* Options (all fields may be zero = default). */
+typedef struct {
+  int32_t device;     /* CUDA ordinal; < 0: the current device */
+  int32_t root_side;  /* 0: auto (S3), 1: left Gershgorin end, 2: right */
+  void *stream;       /* cudaStream_t used for all work; NULL: a library-owned stream */
+  double gaptol;      /* classification threshold; <= 0: 1e-10 */
+  uint64_t seed;      /* key of the root perturbation stream; 0: default */
+  uint32_t flags;     /* MRRR_KEEP_DIAG */
+  uint32_t reserved;
+  int64_t ws_limit;   /* soft cap on workspace bytes; <= 0: 60% of free device memory */
+} mrrr_opts;
+
+/* Create a handle.  opts may be NULL.  Returns 0 or MRRR_ERR_*.
+ * Ownership: the handle owns all device workspace until mrrr_destroy. */
+int mrrr_init(mrrr_t *h, const mrrr_opts *opts);
+
+/* Eigenpairs il..iu of T.  d, e, W, Z are CUDA DEVICE pointers owned by the
+ * caller (e may be NULL when n == 1).  Work is issued on the handle's stream
+ * after waiting for the caller's work on it; the call returns when W and Z
+ * are complete.  Errors: -2 d NULL, -3 e NULL (n > 1), -4 n < 1,
+ * -5 il out of [1, n], -6 iu out of [il, n], -7 W NULL, -8 Z NULL,
+ * -9 ldz < n; MRRR_ERR_* otherwise. */
+int mrrr_eig(mrrr_t h, const double *d, const double *e, int64_t n, int64_t il, int64_t iu, double *W,
+             double *Z, int64_t ldz);
+
+/* Same as mrrr_eig with HOST pointers (pageable or pinned): copies d, e to
+ * the device, solves, copies W and Z back.  Same argument checks. */
+int mrrr_eig_host(mrrr_t h, const double *d, const double *e, int64_t n, int64_t il, int64_t iu, double *W,
+                  double *Z, int64_t ldz);
+
+/* Index-range shard of a multi-GPU solve (one process per GPU):
+ * the shard is the contiguous range [sl, su] (1-based) of [il, iu]; every rank
+ * builds the same root (bit-identical), bisects its shard plus guards, and
+ * computes exactly the eigenpairs whose group (cluster) STARTS inside the
+ * shard (a cluster straddling a shard boundary is owned by the rank holding
+ * its first index).  On return [*jlo, *jhi] (1-based, *jhi < *jlo if empty) is
+ * the owned range; W_local[0..] and columns of Z_local hold eigenpairs
+ * *jlo..*jhi.  ncols_cap bounds the owned count (MRRR_ERR_NOMEM if exceeded,
+ * with the needed range still returned).  Device pointers as in mrrr_eig. */
+int mrrr_eig_shard(mrrr_t h, const double *d, const double *e, int64_t n, int64_t sl, int64_t su,
+                   double *W_local, double *Z_local, int64_t ldz, int64_t ncols_cap, int64_t *jlo,
+                   int64_t *jhi);
+
+/* Statistics of the last call (int64 each, nstats <= MRRR_NSTATS):
+ * 0 d_max, 1 #clusters processed, 2 largest cluster, 3 uncertified shifts
+ * (robustness failures), 4 shift attempts, 5 RQI iterations,
+ * 6 RQI bisection fallbacks, 7 bracket repairs, 8 root back-offs,
+ * 9 failed clusters, 10 x-NegCount evaluations, 11 y-NegCount evaluations,
+ * 12 Getvec calls, 13 bisection rounds, 14 kernel launches, 15 nblocks. */
+#define MRRR_NSTATS 16
+int mrrr_get_stats(mrrr_t h, int64_t *stats, int32_t nstats);
+
+/* Diagnostics of the last call made with MRRR_KEEP_DIAG (host buffers owned
+ * by the caller; any pointer may be NULL; k = #eigenpairs of the call):
+ *   nblocks[1], block_start[n+1], mu[n] and side[n] per block (0 size-1 block,
+ *   1 left, 2 right), root_lo/root_hi[n] per global position (NaN where not
+ *   computed), root_gstart[n] (1 starts a root group, 0 member, -1 not
+ *   computed), depth[k], grp_first/grp_last[MRRR_MAXD*k] (global position of
+ *   the group ends containing output j at each depth, -1 if none),
+ *   fin_lo/fin_hi[k] (final-node interval of output j, node frame). */
+#define MRRR_MAXD 8
+typedef struct {
+  int32_t *nblocks, *block_start;
+  double *mu;
+  int32_t *side;
+  double *root_lo, *root_hi;
+  int32_t *root_gstart, *depth, *grp_first, *grp_last;
+  double *fin_lo, *fin_hi;
+} mrrr_diag;
+int mrrr_get_diag(mrrr_t h, mrrr_diag *g);
+
+/* Time of the last call in milliseconds (CUDA events on the handle's stream,
+ * entry to results ready), split into phases: [0] total, [1] split+root,
+ * [2] root bisection, [3] classification, [4] cluster path, [5] singleton RQI.
+ * Also the average duration of the dominant kernel launches: [6] ms per
+ * k_rqi launch (events around each launch), [7] number of k_rqi launches. */
+int mrrr_get_times(mrrr_t h, double *ms, int32_t nt);
+
+const char *mrrr_strerror(int code);
+
+int mrrr_destroy(mrrr_t h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,215 @@
+"""B200-native mixed-precision MRRR tridiagonal eigensolver (arXiv 1401.4950).
+
+Thin ctypes binding of ``libmrrr.so`` (C ABI in ``include/mrrr.h``): argument
+marshalling only.  Every step of the solve runs in the sm_100a kernels of
+``csrc/``; there is no CPU fallback -- importing works without a GPU, but
+creating a solver raises if the library or a CUDA device is missing.
+
+    import torch, paper_1401_4950_b200 as mrrr
+    s = mrrr.Solver()
+    W, Z = s.eig(d_cuda, e_cuda)          # all pairs; Z is (n, k), column j <-> W[j]
+    W, Z = s.eig(d_cuda, e_cuda, 1, 100)  # indices 1..100 (1-based, inclusive)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmrrr.so")
+
+KEEP_DIAG = 1
+MAXD = 8
+NSTATS = 16
+STAT_NAMES = ["d_max", "n_clusters", "largest_cluster", "uncertified", "shift_attempts", "rqi_iters",
+              "rqi_fallbacks", "bracket_fixes", "root_backoffs", "failed", "negcount_x", "negcount_y",
+              "getvec_calls", "rounds", "launches", "nblocks"]
+TIME_NAMES = ["total", "split_root", "root_bisection", "classification", "clusters", "singletons",
+              "rqi_ms_per_launch", "rqi_launches"]
+
+
+class MrrrError(RuntimeError):
+    pass
+
+
+class _Opts(C.Structure):
+    _fields_ = [("device", C.c_int32), ("root_side", C.c_int32), ("stream", C.c_void_p), ("gaptol", C.c_double),
+                ("seed", C.c_uint64), ("flags", C.c_uint32), ("reserved", C.c_uint32), ("ws_limit", C.c_int64)]
+
+
+class _Diag(C.Structure):
+    _fields_ = [(nm, C.c_void_p) for nm in ("nblocks", "block_start", "mu", "side", "root_lo", "root_hi",
+                                            "root_gstart", "depth", "grp_first", "grp_last", "fin_lo", "fin_hi")]
+
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load libmrrr.so; raises if it was not built (run __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise MrrrError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        i64, vp = C.c_int64, C.c_void_p
+        L.mrrr_init.argtypes = [C.POINTER(vp), C.POINTER(_Opts)]
+        L.mrrr_eig.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, i64]
+        L.mrrr_eig_host.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, i64]
+        L.mrrr_eig_shard.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, i64, i64, C.POINTER(i64), C.POINTER(i64)]
+        L.mrrr_get_stats.argtypes = [vp, vp, C.c_int32]
+        L.mrrr_get_times.argtypes = [vp, vp, C.c_int32]
+        L.mrrr_get_diag.argtypes = [vp, C.POINTER(_Diag)]
+        L.mrrr_strerror.argtypes = [C.c_int]
+        L.mrrr_strerror.restype = C.c_char_p
+        L.mrrr_destroy.argtypes = [vp]
+        for f in ("mrrr_init", "mrrr_eig", "mrrr_eig_host", "mrrr_eig_shard", "mrrr_get_stats", "mrrr_get_times",
+                  "mrrr_get_diag", "mrrr_destroy"):
+            getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+EXPORTED = ["mrrr_init", "mrrr_eig", "mrrr_eig_host", "mrrr_eig_shard", "mrrr_get_stats", "mrrr_get_diag",
+            "mrrr_get_times", "mrrr_strerror", "mrrr_destroy"]
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = load().mrrr_strerror(rc).decode()
+        raise MrrrError(f"{what} failed with code {rc}: {msg}")
+
+
+@dataclass
+class Diag:
+    nblocks: int
+    block_start: np.ndarray
+    mu: np.ndarray
+    side: np.ndarray
+    root_lo: np.ndarray
+    root_hi: np.ndarray
+    root_gstart: np.ndarray
+    depth: np.ndarray
+    grp_first: np.ndarray
+    grp_last: np.ndarray
+    fin_lo: np.ndarray
+    fin_hi: np.ndarray
+
+
+class Solver:
+    """One libmrrr handle (one device, one stream)."""
+
+    def __init__(self, device: int | None = None, gaptol: float = 0.0, seed: int = 0, root_side: int = 0,
+                 keep_diag: bool = False, stream: int | None = None, ws_limit: int = 0):
+        L = load()
+        self._h = C.c_void_p()
+        o = _Opts(-1 if device is None else int(device), int(root_side), stream, float(gaptol), int(seed),
+                  KEEP_DIAG if keep_diag else 0, 0, int(ws_limit))
+        _check(L.mrrr_init(C.byref(self._h), C.byref(o)), "mrrr_init")
+        self.keep_diag = keep_diag
+        self._last = (0, 0)
+
+    # -------------------------------------------------------------- solves
+    def eig(self, d, e, il: int | None = None, iu: int | None = None, W=None, Z=None):
+        """Device solve: d, e are float64 CUDA tensors.  Returns (W, Z) with Z of shape (n, k) (a
+        column-major view: Z[:, j] is contiguous)."""
+        import torch
+        n = d.numel()
+        il = 1 if il is None else int(il)
+        iu = n if iu is None else int(iu)
+        k = max(iu - il + 1, 0)
+        if not (d.is_cuda and d.dtype == torch.float64 and d.is_contiguous()):
+            raise MrrrError("d must be a contiguous float64 CUDA tensor")
+        if n > 1 and not (e.is_cuda and e.dtype == torch.float64 and e.is_contiguous()):
+            raise MrrrError("e must be a contiguous float64 CUDA tensor")
+        if W is None:
+            W = torch.empty(k, dtype=torch.float64, device=d.device)
+        if Z is None:
+            Zt = torch.empty((k, n), dtype=torch.float64, device=d.device)
+        else:
+            Zt = Z.T if Z.shape == (n, k) else Z
+        ep = e.data_ptr() if (e is not None and e.numel()) else None
+        rc = load().mrrr_eig(self._h, d.data_ptr(), ep, n, il, iu, W.data_ptr(), Zt.data_ptr(), n)
+        _check(rc, "mrrr_eig")
+        self._last = (n, k)
+        return W, Zt.T
+
+    def eig_host(self, d: np.ndarray, e: np.ndarray, il: int | None = None, iu: int | None = None):
+        """Host solve (copies inside the timed call).  Returns numpy (W, Z[n, k])."""
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        n = d.size
+        e = np.ascontiguousarray(e, dtype=np.float64) if n > 1 else np.zeros(1)
+        il = 1 if il is None else int(il)
+        iu = n if iu is None else int(iu)
+        k = iu - il + 1
+        W = np.empty(k)
+        Zt = np.empty((k, n))
+        rc = load().mrrr_eig_host(self._h, d.ctypes.data, e.ctypes.data, n, il, iu, W.ctypes.data, Zt.ctypes.data, n)
+        _check(rc, "mrrr_eig_host")
+        self._last = (n, k)
+        return W, Zt.T
+
+    def eig_shard(self, d, e, sl: int, su: int, ncols_cap: int | None = None):
+        """Multi-GPU shard: eigenpairs of the groups that start in [sl, su]; returns (jlo, jhi, W, Z)."""
+        import torch
+        n = d.numel()
+        cap = (su - sl + 1) * 2 + 64 if ncols_cap is None else ncols_cap
+        cap = min(cap, n)
+        W = torch.empty(cap, dtype=torch.float64, device=d.device)
+        Zt = torch.empty((cap, n), dtype=torch.float64, device=d.device)
+        jlo, jhi = C.c_int64(), C.c_int64()
+        rc = load().mrrr_eig_shard(self._h, d.data_ptr(), e.data_ptr() if n > 1 else None, n, int(sl), int(su),
+                                   W.data_ptr(), Zt.data_ptr(), n, cap, C.byref(jlo), C.byref(jhi))
+        _check(rc, "mrrr_eig_shard")
+        m = max(jhi.value - jlo.value + 1, 0)
+        self._last = (n, m)
+        return jlo.value, jhi.value, W[:m], Zt[:m].T
+
+    # -------------------------------------------------------------- results
+    def stats(self) -> dict:
+        s = np.zeros(NSTATS, np.int64)
+        _check(load().mrrr_get_stats(self._h, s.ctypes.data, NSTATS), "mrrr_get_stats")
+        return {nm: int(s[i]) for i, nm in enumerate(STAT_NAMES)}
+
+    def times(self) -> dict:
+        t = np.zeros(8)
+        _check(load().mrrr_get_times(self._h, t.ctypes.data, 8), "mrrr_get_times")
+        return {nm: float(t[i]) for i, nm in enumerate(TIME_NAMES)}
+
+    def diag(self) -> Diag:
+        n, k = self._last
+        a = dict(nblocks=np.zeros(1, np.int32), block_start=np.zeros(n + 1, np.int32), mu=np.zeros(n),
+                 side=np.zeros(n, np.int32), root_lo=np.zeros(n), root_hi=np.zeros(n),
+                 root_gstart=np.zeros(n, np.int32), depth=np.zeros(k, np.int32),
+                 grp_first=np.zeros(MAXD * k, np.int32), grp_last=np.zeros(MAXD * k, np.int32), fin_lo=np.zeros(k),
+                 fin_hi=np.zeros(k))
+        g = _Diag(*[a[f].ctypes.data for f, _ in _Diag._fields_])
+        _check(load().mrrr_get_diag(self._h, C.byref(g)), "mrrr_get_diag")
+        nb = int(a["nblocks"][0])
+        return Diag(nblocks=nb, block_start=a["block_start"][:nb + 1], mu=a["mu"][:nb], side=a["side"][:nb],
+                    root_lo=a["root_lo"], root_hi=a["root_hi"], root_gstart=a["root_gstart"], depth=a["depth"],
+                    grp_first=a["grp_first"].reshape(MAXD, k), grp_last=a["grp_last"].reshape(MAXD, k),
+                    fin_lo=a["fin_lo"], fin_hi=a["fin_hi"])
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            load().mrrr_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def eig(d, e, il=None, iu=None, **kw):
+    """One-shot convenience: device tensors in, (W, Z) out."""
+    s = Solver(**kw)
+    try:
+        return s.eig(d, e, il, iu)
+    finally:
+        s.close()

@@ -1,0 +1,494 @@
+// kernels_vec.cuh -- cluster path (S8: Alg. spectrumshift, mixed
+// precision P:5969-5971, depth-first P:6110-6132) and the singleton RQI /
+// eigenvector kernel (S9-S10: Alg. Getvec, Alg. stask
+// P:4026-4074, mixed stop P:6074-6108, convert-on-write P:6156-6158).
+#pragma once
+#include "kernels.cuh"
+
+__device__ __forceinline__ dd ld_d(const YElt *y) { return dd_make(__ldg(&y->d_hi), __ldg(&y->d_lo)); }
+__device__ __forceinline__ dd ld_dl(const YElt *y) { return dd_make(__ldg(&y->dl_hi), __ldg(&y->dl_lo)); }
+__device__ __forceinline__ dd ld_dll(const YElt *y) { return dd_make(__ldg(&y->dll_hi), __ldg(&y->dll_lo)); }
+
+// one qd step shared by dstqds (Alg. dstqds) and dqds (Alg. dqds, A-1/A-2):
+//   den = x + a; q = (|x| = inf and |den| = inf) ? 1 : x / den; out = b / den; xn = q * c - lam
+// dstqds: x = s(i), a = d(i), b = dl(i), c = dll(i)  -> den = d+(i), out = l+(i), xn = s(i+1)
+// dqds  : x = p(i+1), a = dll(i), b = dl(i), c = d(i) -> den = omega(i+1), out = u-(i), xn = p(i)
+// The two quotients by den share one dd reciprocal (tolerance-level difference to x/den).
+__device__ __forceinline__ void qd_step(dd x, dd a, dd b, dd c, dd lam, dd &den, dd &rr, dd &out, dd &xn) {
+  den = dd_add(x, a);
+  rr = dd_rcp(den);
+  dd q = (dd_isinf(x) && dd_isinf(den)) ? dd_from(1.0) : dd_mul(x, rr);
+  out = dd_mul(b, rr);
+  xn = dd_sub(dd_mul(q, c), lam);
+}
+
+// ---------------------------------------------------------------------------
+// S8(a): y-refinement nodes for the two cluster ends
+// ---------------------------------------------------------------------------
+__global__ void k_clu_yref_init(const Cluster *__restrict__ cl, int ncl, const RepDesc *__restrict__ reps,
+                                const double *__restrict__ ilo, const double *__restrict__ ihi, BNode *bn) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncl) return;
+  Cluster C = cl[c];
+  int nb = reps[C.rep].nb;
+  double nu = __dmul_rn(__dmul_rn(100.0, (double)nb), EPS_X);
+  for (int side = 0; side < 2; side++) {
+    int j = side ? C.q : C.p;
+    double lo = ilo[C.ibase + j], hi = ihi[C.ibase + j];
+    double L = __dsub_rn(lo, __dmul_rn(nu, fabs(lo)));
+    double H = __dadd_rn(hi, __dmul_rn(nu, fabs(hi)));
+    dyadic_widen(L, H, &L, &H);
+    BNode b;
+    b.lo = L; b.hi = H; b.clo = 0; b.chi = 0; b.j = j; b.rep = C.rep;
+    b.needLo = 1; b.needHi = 1; b.fixes = 0; b.pad = 0;
+    b.obase = 2LL * c + side - j;
+    bn[2 * c + side] = b;
+  }
+}
+
+// per-cluster shift state
+struct ShiftState {
+  double taul, taur, offl, offr, best_g, best_tau;
+  int have_best, done, certified, attempts;
+};
+
+__global__ void k_clu_shift_init(int ncl, const double *__restrict__ ylo, const double *__restrict__ yhi,
+                                 ShiftState *ss) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncl) return;
+  double Lp = ylo[2 * c], Hq = yhi[2 * c + 1];
+  ShiftState s;
+  s.offl = __dmul_rn(__dmul_rn(100.0, EPS_X), fabs(Lp));
+  s.offr = __dmul_rn(__dmul_rn(100.0, EPS_X), fabs(Hq));
+  s.taul = __dsub_rn(Lp, s.offl);
+  s.taur = __dadd_rn(Hq, s.offr);
+  s.best_g = INFINITY; s.best_tau = 0.0;
+  s.have_best = 0; s.done = 0; s.certified = 0; s.attempts = 0;
+  ss[c] = s;
+}
+
+// S8(c): growth of dstqds(M_y, tau) for both candidate shifts, thread per (cluster, side)
+__global__ void k_clu_attempt(const Cluster *__restrict__ cl, int ncl, const RepDesc *__restrict__ reps,
+                              const YElt *__restrict__ my, const ShiftState *__restrict__ ss, double *gval,
+                              int *valid) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 2 * ncl) return;
+  int c = t >> 1, side = t & 1;
+  if (ss[c].done) return;
+  RepDesc R = reps[cl[c].rep];
+  const YElt *y = my + R.off;
+  dd tau = dd_from(side ? ss[c].taur : ss[c].taul);
+  dd s = dd_neg(tau);
+  double g = 0.0;
+  int ok = 1;
+  for (int i = 0; i < R.nb - 1; i++) {
+    dd den, rr, out, xn;
+    qd_step(s, ld_d(y + i), ld_dl(y + i), ld_dll(y + i), tau, den, rr, out, xn);
+    ok &= !(isnan(den.hi) || isnan(out.hi));
+    g = dmaxd(g, fabs(den.hi));
+    s = xn;
+  }
+  dd den = dd_add(s, ld_d(y + R.nb - 1));
+  ok &= !isnan(den.hi);
+  g = dmaxd(g, fabs(den.hi));
+  gval[t] = g;
+  valid[t] = ok;
+}
+
+__global__ void k_clu_select(const Cluster *__restrict__ cl, int ncl, const RepDesc *__restrict__ reps,
+                             ShiftState *ss, const double *__restrict__ gval, const int *__restrict__ valid, int a,
+                             int *ndone, long long *stats) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncl) return;
+  ShiftState s = ss[c];
+  if (s.done) { atomicAdd(ndone, 1); return; }
+  atomicAdd((unsigned long long *)&stats[ST_ATTEMPTS], 1ull);
+  double gthr = __dmul_rn(GROWTH, reps[cl[c].rep].spdiam);
+  int vl = valid[2 * c], vr = valid[2 * c + 1];
+  double gl = gval[2 * c], gr = gval[2 * c + 1];
+  int pick = 0;
+  if (vl && vr) pick = (gl <= gr) ? 1 : 2;
+  else if (vl) pick = 1;
+  else if (vr) pick = 2;
+  s.attempts++;
+  if (pick) {
+    double g = (pick == 1) ? gl : gr;
+    if (g < s.best_g) { s.best_g = g; s.best_tau = (pick == 1) ? s.taul : s.taur; s.have_best = 1; }
+    if (g <= gthr) { s.done = 1; s.certified = 1; }
+  }
+  if (!s.done) {
+    s.taul = __dsub_rn(s.taul, ldexp(s.offl, a));
+    s.taur = __dadd_rn(s.taur, ldexp(s.offr, a));
+    if (a == MAX_ATTEMPTS - 1) {
+      s.done = 1;
+      if (s.have_best) atomicAdd((unsigned long long *)&stats[ST_UNCERTIFIED], 1ull);
+    }
+  }
+  if (s.done) atomicAdd(ndone, 1);
+  ss[c] = s;
+}
+
+// S8(d): child representation M_y = (d+, l+) of dstqds(M_y, tau_best) and its x copy.
+// Child rep id = repbase + c, data at pool offset poolbase + c * nbmax.
+__global__ void k_clu_build(const Cluster *__restrict__ cl, int ncl, RepDesc *reps, const ShiftState *__restrict__ ss,
+                            double2 *mx, YElt *my, int repbase, long long poolbase, int nbmax) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncl) return;
+  ShiftState S = ss[c];
+  RepDesc P = reps[cl[c].rep];
+  RepDesc R = P;
+  R.off = poolbase + (long long)c * nbmax;
+  R.depth = P.depth + 1;
+  dd sig = dd_add_d(dd_make(P.sig_hi, P.sig_lo), S.best_tau);
+  R.sig_hi = sig.hi; R.sig_lo = sig.lo;
+  if (!S.have_best) R.nb = -1;  // failed: members go back to the parent as singletons
+  reps[repbase + c] = R;
+  if (!S.have_best) return;
+  const YElt *y = my + P.off;
+  YElt *yc = my + R.off;
+  double2 *xc = mx + R.off;
+  dd tau = dd_from(S.best_tau);
+  dd s = dd_neg(tau);
+  for (int i = 0; i < P.nb - 1; i++) {
+    dd den, rr, out, xn;
+    qd_step(s, ld_d(y + i), ld_dl(y + i), ld_dll(y + i), tau, den, rr, out, xn);
+    // rep_derive: dl = d l, dll = dl l (y); dx = fl64(d), dllx = (dx lx) lx
+    dd dl = dd_mul(den, out);
+    dd dll = dd_mul(dl, out);
+    YElt e;
+    e.d_hi = den.hi; e.d_lo = den.lo; e.dl_hi = dl.hi; e.dl_lo = dl.lo; e.dll_hi = dll.hi; e.dll_lo = dll.lo;
+    yc[i] = e;
+    double dx = den.hi, lx = out.hi;
+    xc[i] = make_double2(dx, __dmul_rn(__dmul_rn(dx, lx), lx));
+    s = xn;
+  }
+  dd den = dd_add(s, ld_d(y + P.nb - 1));
+  YElt e;
+  e.d_hi = den.hi; e.d_lo = den.lo; e.dl_hi = e.dl_lo = e.dll_hi = e.dll_lo = 0.0;
+  yc[P.nb - 1] = e;
+  xc[P.nb - 1] = make_double2(den.hi, 0.0);
+}
+
+// S8(e): child start intervals (A-13) for members; neighbours shifted by -tau.
+// segment of cluster c: cseg[c] .. cseg[c] + (q-p+2): index j -> cseg[c] + (j - p + 1)
+__global__ void k_clu_child_starts(const Cluster *__restrict__ cl, int ncl, const RepDesc *__restrict__ reps,
+                                   const ShiftState *__restrict__ ss, const long long *__restrict__ cseg,
+                                   const long long *__restrict__ bnoff, const double *__restrict__ ilo,
+                                   const double *__restrict__ ihi, double *clo, double *chi, BNode *bn, int repbase) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncl) return;
+  Cluster C = cl[c];
+  ShiftState S = ss[c];
+  if (!S.have_best) return;
+  int nb = reps[C.rep].nb;
+  double nu = __dmul_rn(__dmul_rn(100.0, (double)nb), EPS_X);
+  double tau = S.best_tau;
+  long long base = cseg[c] - (C.p - 1);  // child ibase
+  double lpm = ilo[C.ibase + C.p - 1];
+  if (C.p > 1 && !isnan(lpm)) {
+    clo[base + C.p - 1] = __dsub_rn(lpm, tau);
+    chi[base + C.p - 1] = __dsub_rn(ihi[C.ibase + C.p - 1], tau);
+  } else {
+    clo[base + C.p - 1] = NAN; chi[base + C.p - 1] = NAN;
+  }
+  double lqp = (C.q < nb) ? ilo[C.ibase + C.q + 1] : NAN;
+  if (C.q < nb && !isnan(lqp)) {
+    clo[base + C.q + 1] = __dsub_rn(lqp, tau);
+    chi[base + C.q + 1] = __dsub_rn(ihi[C.ibase + C.q + 1], tau);
+  } else {
+    clo[base + C.q + 1] = NAN; chi[base + C.q + 1] = NAN;
+  }
+  long long o = bnoff[c];
+  for (int j = C.p; j <= C.q; j++) {
+    double lo = ilo[C.ibase + j], hi = ihi[C.ibase + j];
+    double a1 = __dsub_rn(lo, __dmul_rn(nu, fabs(lo)));
+    double b1 = __dsub_rn(a1, tau);
+    double l2 = __dsub_rn(b1, __dmul_rn(nu, fabs(b1)));
+    double c1 = __dadd_rn(hi, __dmul_rn(nu, fabs(hi)));
+    double e1 = __dsub_rn(c1, tau);
+    double h2 = __dadd_rn(e1, __dmul_rn(nu, fabs(e1)));
+    double L, H;
+    dyadic_widen(l2, h2, &L, &H);
+    BNode b;
+    b.lo = L; b.hi = H; b.clo = 0; b.chi = 0; b.j = j; b.rep = repbase + c;
+    b.needLo = 1; b.needHi = 1; b.fixes = 0; b.pad = 0;
+    b.obase = base;
+    bn[o + (j - C.p)] = b;
+  }
+}
+
+// S8(f): reclassify the members in the child; singletons -> RQI list, clusters -> next level.
+// Failed clusters (no valid shift) send their members to the RQI list on the parent rep.
+__global__ void k_clu_classify(const Cluster *__restrict__ cl, int ncl, const RepDesc *__restrict__ reps,
+                               const ShiftState *__restrict__ ss, const long long *__restrict__ cseg,
+                               const double *__restrict__ ilo, const double *__restrict__ ihi,
+                               const double *__restrict__ clo, const double *__restrict__ chi,
+                               const int *__restrict__ colmap, double gaptol, int repbase, Singleton *sing, int *nsing,
+                               Cluster *nxt, int *nnxt, int *grp_first, int *grp_last, int kout, long long *stats) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncl) return;
+  Cluster C = cl[c];
+  ShiftState S = ss[c];
+  const RepDesc P = reps[C.rep];
+  int bstart = P.bstart, nb = P.nb;
+  bool failed = !S.have_best;
+  if (failed) atomicAdd((unsigned long long *)&stats[ST_FAILED], 1ull);
+  const double *lo = failed ? ilo : clo;
+  const double *hi = failed ? ihi : chi;
+  long long base = failed ? C.ibase : (cseg[c] - (C.p - 1));
+  int rep = failed ? C.rep : repbase + c;
+  int depth = failed ? P.depth : P.depth + 1;
+  bool all_single = failed || depth >= MAXD;
+  if (!failed && depth >= MAXD) atomicAdd((unsigned long long *)&stats[ST_FAILED], 1ull);
+  int g0 = C.p;
+  for (int j = C.p + 1; j <= C.q + 1; j++) {
+    bool brk = (j == C.q + 1) || all_single ||
+               is_boundary(lo[base + j - 1], hi[base + j - 1], lo[base + j], hi[base + j], gaptol);
+    if (!brk) continue;
+    int g1 = j - 1;
+    bool sel = false;
+    for (int t = g0; t <= g1; t++) sel |= (colmap[bstart + t - 1] >= 0);
+    if (sel) {
+      if (grp_first && !failed && depth < MAXD) {
+        for (int t = g0; t <= g1; t++) {
+          int col = colmap[bstart + t - 1];
+          if (col >= 0) {
+            grp_first[(long long)depth * kout + col] = bstart + g0 - 1;
+            grp_last[(long long)depth * kout + col] = bstart + g1 - 1;
+          }
+        }
+      }
+      if (g0 == g1 || all_single) {
+        for (int t = g0; t <= g1; t++) {
+          int col = colmap[bstart + t - 1];
+          if (col < 0) continue;
+          double mid = bis_mid(lo[base + t], hi[base + t]);
+          double ln = lo[base + t - 1], hn = hi[base + t - 1];
+          double lr = lo[base + t + 1];
+          double gl = (t > 1 && !isnan(ln)) ? __dsub_rn(mid, hn) : INFINITY;
+          double gr = (t < nb && !isnan(lr)) ? __dsub_rn(lr, mid) : INFINITY;
+          int k = atomicAdd(nsing, 1);
+          Singleton s;
+          s.lo = lo[base + t]; s.hi = hi[base + t]; s.gap = dmind(gl, gr);
+          s.rep = rep; s.j = t; s.col = col; s.pad = 0;
+          sing[k] = s;
+        }
+      } else {
+        int k = atomicAdd(nnxt, 1);
+        Cluster D;
+        D.ibase = base; D.rep = rep; D.p = g0; D.q = g1; D.depth = depth;
+        nxt[k] = D;
+        atomicAdd((unsigned long long *)&stats[ST_NCLUSTERS], 1ull);
+        atomicMax((unsigned long long *)&stats[ST_LARGEST], (unsigned long long)(g1 - g0 + 1));
+      }
+    }
+    g0 = j;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// S9/S10: RQI + Getvec + output.  One thread per singleton.  Workspace A, B
+// (dd, interleaved [i * S + t]): A = s (forward) then u- (backward), B = l+.
+// Zero pivots are marked by a NaN low word (never produced by dd ops).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ dd dd_mark() { return dd_make(0.0, __longlong_as_double(0x7ff8000000000000ll)); }
+__device__ __forceinline__ bool is_mark(dd x) { return isnan(x.lo); }
+
+struct GV {
+  dd gamma, zz;
+  int r, c;
+};
+
+// Getvec: r < 0 -> full twisted factorization + twist search (iteration 1);
+// r >= 0 (0-based) -> only the r-twisted factorization
+__device__ void getvec_dd(const YElt *__restrict__ y, int nb, dd lam, int r, dd *A, dd *B, long long S, GV &g) {
+  int cnt = 0;
+  if (r < 0) {
+    dd s = dd_neg(lam);
+    for (int i = 0; i < nb - 1; i++) {
+      dd den, rr, out, xn;
+      qd_step(s, ld_d(y + i), ld_dl(y + i), ld_dll(y + i), lam, den, rr, out, xn);
+      A[(long long)i * S] = s;
+      B[(long long)i * S] = (den.hi == 0.0) ? dd_mark() : out;
+      cnt += dd_sb(den);
+      s = xn;
+    }
+    dd dn = dd_add(s, ld_d(y + nb - 1));
+    cnt += dd_sb(dn);
+    dd gam = dn;  // gamma_n = s(n) + d(n) = d+(n)
+    int rbest = -1;
+    dd best = dd_from(INFINITY), gbest = gam;
+    if (!isnan(gam.hi)) { rbest = nb - 1; best = dd_abs(gam); }
+    dd p = dd_sub(ld_d(y + nb - 1), lam);
+    for (int i = nb - 2; i >= 0; i--) {
+      dd di = ld_d(y + i);
+      dd den, rr, out, xn;
+      qd_step(p, ld_dll(y + i), ld_dl(y + i), di, lam, den, rr, out, xn);
+      dd si = A[(long long)i * S];
+      dd gi = dd_add(si, dd_mul(dd_mul(di, rr), p));
+      A[(long long)i * S] = (den.hi == 0.0) ? dd_mark() : out;
+      if (!isnan(gi.hi)) {
+        dd ag = dd_abs(gi);
+        if (!dd_lt(best, ag)) { best = ag; rbest = i; gbest = gi; }
+      }
+      p = xn;
+    }
+    g.r = rbest;
+    g.gamma = gbest;
+  } else {
+    dd s = dd_neg(lam), p = dd_sub(ld_d(y + nb - 1), lam), gamma = dd_from(0.0);
+    // unified loop: k < r forward dstqds step i = k; else backward dqds step i = nb-2-(k-r)
+    for (int k = 0; k < nb - 1; k++) {
+      bool fw = k < r;
+      int i = fw ? k : nb - 2 - (k - r);
+      dd di = ld_d(y + i), dli = ld_dl(y + i), dlli = ld_dll(y + i);
+      dd den, rr, out, xn;
+      qd_step(fw ? s : p, fw ? di : dlli, dli, fw ? dlli : di, lam, den, rr, out, xn);
+      if (fw) {
+        B[(long long)i * S] = (den.hi == 0.0) ? dd_mark() : out;
+        s = xn;
+      } else {
+        A[(long long)i * S] = (den.hi == 0.0) ? dd_mark() : out;
+        if (i == r) gamma = dd_add(s, dd_mul(dd_mul(di, rr), p));
+        p = xn;
+      }
+      cnt += dd_sb(den);
+    }
+    if (r == nb - 1) gamma = dd_add(s, ld_d(y + nb - 1));
+    cnt += dd_sb(gamma);
+    g.r = r;
+    g.gamma = gamma;
+  }
+  g.c = cnt;
+}
+
+// z solve of N_r^T z = e_r with zero-pivot substitution (A-25); returns ||z||^2.
+// If Zc != nullptr writes fl64(z_i * inv) to Zc[i].
+__device__ dd zsolve(const YElt *__restrict__ y, int nb, int r, const dd *A, const dd *B, long long S, dd inv,
+                     double *Zc) {
+  dd zz = dd_from(1.0);
+  if (Zc) Zc[r] = inv.hi;
+  // z(r+1) by the regular recurrence for the backward branch's substitution at i = r-1
+  dd zp1 = dd_from(0.0);
+  if (r < nb - 1) {
+    dd u = A[(long long)r * S];
+    if (!is_mark(u)) zp1 = dd_neg(u);
+  }
+  dd z1 = dd_from(1.0), z2 = zp1;  // z(i+1), z(i+2) for the backward branch
+  dd zrm1 = dd_from(0.0);
+  for (int k = 0; k < nb - 1; k++) {
+    bool bw = k < r;
+    int i = bw ? (r - 1 - k) : k;
+    if (k == r) { z2 = zrm1; z1 = dd_from(1.0); }  // forward branch: z(i), z(i-1)
+    dd w = bw ? B[(long long)i * S] : A[(long long)i * S];
+    dd z;
+    if (!is_mark(w)) {
+      z = dd_neg(dd_mul(w, z1));
+    } else {
+      int in = bw ? i + 1 : i - 1;
+      dd num = (bw ? (in < nb - 1) : (in >= 0)) ? ld_dl(y + in) : dd_from(0.0);
+      dd v = dd_neg(dd_mul(dd_div(num, ld_dl(y + i)), z2));
+      z = isfinite(v.hi) ? v : dd_from(0.0);
+    }
+    zz = dd_add(zz, dd_mul(z, z));
+    int row = bw ? i : i + 1;
+    if (Zc) Zc[row] = dd_mul(z, inv).hi;
+    if (bw && i == r - 1) zrm1 = z;
+    z2 = z1;
+    z1 = z;
+  }
+  return zz;
+}
+
+// y-bisection to relative width 2^-98 (RQI fallback)
+__device__ dd bisect_y_full(const YElt *__restrict__ y, int nb, int j, dd lo, dd hi) {
+  for (int it = 0; it < 200; it++) {
+    dd m = dd_lt(dd_abs(lo), dd_abs(hi)) ? dd_abs(hi) : dd_abs(lo);
+    dd w = dd_sub(hi, lo);
+    if (!dd_lt(dd_mul_d(m, 0x1p-98), w)) break;
+    dd mid = dd_add(lo, dd_mul_d(w, 0.5));
+    if (negcount_y(y, nb, mid) < j) lo = mid;
+    else hi = mid;
+  }
+  return dd_add(lo, dd_mul_d(dd_sub(hi, lo), 0.5));
+}
+
+__global__ void __launch_bounds__(64) k_rqi(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
+                                            const YElt *__restrict__ my, dd *wsA, dd *wsB, long long S, double *W,
+                                            double *Z, long long ldz, int *diag_depth, double *fin_lo, double *fin_hi,
+                                            long long *stats) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ns) return;
+  const Singleton s = sg[t];
+  const RepDesc R = reps[s.rep];
+  const int nb = R.nb, j = s.j;
+  const YElt *y = my + R.off;
+  dd *A = wsA + t, *B = wsB + t;
+  double mid = bis_mid(s.lo, s.hi);
+  double nu = __dmul_rn(__dmul_rn(100.0, (double)nb), EPS_X);
+  dd blo = dd_from(__dsub_rn(s.lo, __dmul_rn(nu, fabs(s.lo))));
+  dd bhi = dd_from(__dadd_rn(s.hi, __dmul_rn(nu, fabs(s.hi))));
+  dd lam = dd_from(mid);
+  double thr1 = __dmul_rn(__dmul_rn(s.gap, EPS_X), sqrt((double)nb));
+  int r = -1, iters = 0;
+  bool accepted = false;
+  GV g;
+  dd nz = dd_from(1.0);
+  for (int it = 0; it < MAX_RQI && !accepted; it++) {
+    getvec_dd(y, nb, lam, r, A, B, S, g);
+    iters++;
+    r = g.r;
+    if (r < 0) break;
+    dd zz = zsolve(y, nb, r, A, B, S, dd_from(0.0), nullptr);
+    if (!isfinite(zz.hi) || zz.hi == 0.0) break;
+    nz = dd_sqrt(zz);
+    dd resid = dd_div(dd_abs(g.gamma), nz);
+    dd rqc = dd_div(g.gamma, zz);
+    if (resid.hi <= thr1 || dd_lt(dd_abs(rqc), dd_mul_d(dd_abs(lam), 4.0 * EPS_Y))) { accepted = true; break; }
+    if (g.c < j) blo = lam; else bhi = lam;
+    dd nl = dd_add(lam, rqc);
+    bool ok = ((g.c < j) ? (rqc.hi > 0.0) : (rqc.hi < 0.0)) && dd_lt(blo, nl) && dd_lt(nl, bhi);
+    if (ok) lam = nl;
+    else break;
+  }
+  atomicAdd((unsigned long long *)&stats[ST_RQI_ITERS], (unsigned long long)iters);
+  atomicAdd((unsigned long long *)&stats[ST_GETVEC], (unsigned long long)iters);
+  if (!accepted) {
+    atomicAdd((unsigned long long *)&stats[ST_RQI_FALLBACK], 1ull);
+    lam = bisect_y_full(y, nb, j, blo, bhi);
+    getvec_dd(y, nb, lam, r, A, B, S, g);
+    atomicAdd((unsigned long long *)&stats[ST_GETVEC], 1ull);
+    r = g.r;
+    if (r < 0) r = 0;
+    dd zz = zsolve(y, nb, r, A, B, S, dd_from(0.0), nullptr);
+    nz = dd_sqrt(zz);
+  }
+  dd sig = dd_make(R.sig_hi, R.sig_lo);
+  W[s.col] = dd_add(lam, sig).hi;
+  double *Zc = Z + (long long)s.col * ldz + R.bstart;
+  zsolve(y, nb, r, A, B, S, dd_rcp(nz), Zc);
+  if (diag_depth) {
+    diag_depth[s.col] = R.depth;
+    fin_lo[s.col] = s.lo;
+    fin_hi[s.col] = s.hi;
+  }
+  atomicMax((unsigned long long *)&stats[ST_DMAX], (unsigned long long)R.depth);
+}
+
+// size-1 blocks (S2): eigenpair (alpha_s, e_s)
+__global__ void k_trivial(const double *__restrict__ d, const int *__restrict__ starts, int nblk,
+                          const int *__restrict__ colmap, double *W, double *Z, long long ldz, int *diag_depth,
+                          double *fin_lo, double *fin_hi, int *grp_first, int *grp_last, double *rlo, double *rhi) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nblk) return;
+  int s = starts[b];
+  if (starts[b + 1] - s != 1) return;
+  rlo[s] = d[s];
+  rhi[s] = d[s];
+  int col = colmap[s];
+  if (col < 0) return;
+  W[col] = d[s];
+  Z[(long long)col * ldz + s] = 1.0;
+  if (diag_depth) { diag_depth[col] = 0; fin_lo[col] = d[s]; fin_hi[col] = d[s]; }
+  if (grp_first) { grp_first[col] = s; grp_last[col] = s; }
+}

@@ -1,0 +1,897 @@
+// mrrr.cu -- host orchestrator and C ABI of libmrrr.so (include/mrrr.h).
+// Sequencing of DESIGN.md S0-S10 on one CUDA stream; every numerical step is
+// a kernel from kernels.cuh / kernels_vec.cuh.  Host code only sizes
+// workspace, launches, and reads back small counters that size the next
+// launch (node / group / cluster counts).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mrrr.h"
+#include "kernels.cuh"
+#include "kernels_vec.cuh"
+
+namespace {
+
+thread_local std::string g_last_cuda_error = "no error";
+
+struct Buf {
+  void *p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) { p = nullptr; return e; }
+    cap = want;
+    return cudaSuccess;
+  }
+  // grow to >= bytes keeping the first `keep` bytes (stream-ordered copy)
+  cudaError_t grow_keep(size_t bytes, size_t keep, cudaStream_t st) {
+    if (bytes <= cap) return cudaSuccess;
+    void *q = nullptr;
+    cudaError_t e = cudaMalloc(&q, bytes);
+    if (e != cudaSuccess) return e;
+    if (p && keep) {
+      e = cudaMemcpyAsync(q, p, std::min(keep, cap), cudaMemcpyDeviceToDevice, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) { cudaFree(q); return e; }
+    }
+    if (p) cudaFree(p);
+    p = q;
+    cap = bytes;
+    return cudaSuccess;
+  }
+  void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+  template <class T> T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+struct Err {
+  int code;
+};
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t _e = (x);                                                                  \
+    if (_e != cudaSuccess) {                                                               \
+      g_last_cuda_error = std::string(#x) + ": " + cudaGetErrorString(_e);                 \
+      throw Err{_e == cudaErrorMemoryAllocation ? MRRR_ERR_NOMEM : MRRR_ERR_CUDA};         \
+    }                                                                                      \
+  } while (0)
+
+inline unsigned nblocks_for(long long n, int bs) { return (unsigned)std::max<long long>(1, (n + bs - 1) / bs); }
+
+// counters block on the device: reset/readback in one copy
+enum { C_NNEXT = 0, C_NEX, C_NPEND, C_NREADY, C_NSING, C_NCLUS, C_NNXT, C_NDONE, C_NCOUNTERS = 16 };
+
+}  // namespace
+
+struct mrrr_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  double gaptol = 1e-10;
+  uint64_t seed = 0x4D52525233ULL;
+  int root_side = 0;
+  uint32_t flags = 0;
+  long long ws_limit = 0;
+  long long target_chains = 65536;
+  int mmax = 16;
+
+  // buffers
+  Buf starts, scal, binfo, bside, blist, cab, mx, my, lscratch, reps, rlo, rhi, colmap, gstart;
+  Buf nodesA, nodesB, counts, ex, excounts, exmap, bnA, bnB, sing, clusA, clusB, ss, gval, valid, cseg, bnoff,
+      ipool_lo, ipool_hi, yref_lo, yref_hi, wsA, wsB, stats, cnt, ddepth, dgf, dgl, dflo, dfhi;
+  int *h_cnt = nullptr;  // pinned counters
+
+  // results of the last call
+  long long last_n = 0, last_k = 0;
+  int last_nblk = 0;
+  long long stats_h[MRRR_NSTATS] = {0};
+  double times[8] = {0};
+  std::vector<int> h_starts;
+  cudaEvent_t ev[8];
+  cudaEvent_t rq0, rq1;
+  double rqi_ms = 0;
+  long long rqi_launches = 0;
+  long long host_rounds = 0, host_launches = 0;
+};
+
+namespace {
+
+void read_counters(mrrr_t h) {
+  CK(cudaMemcpyAsync(h->h_cnt, h->cnt.p, C_NCOUNTERS * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+}
+void zero_counters(mrrr_t h) { CK(cudaMemsetAsync(h->cnt.p, 0, C_NCOUNTERS * sizeof(int), h->stream)); }
+
+__global__ void k_fill(double *p, long long n, double v) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+__global__ void k_fill_i(int *p, long long n, int v) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+__global__ void k_colmap_range(int *colmap, long long n, long long lo1, long long hi1) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) colmap[i] = (i + 1 >= lo1 && i + 1 <= hi1) ? (int)(i + 1 - lo1) : -1;
+}
+
+// root start nodes + end verification chains (S5)
+__global__ void k_root_nodes(const int *__restrict__ blist, int nbl, const int *__restrict__ starts,
+                             const double *__restrict__ binfo, const int *__restrict__ cab, Node *nodes,
+                             ExplicitChain *ex) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nbl) return;
+  int blk = blist[t];
+  int s = starts[blk], nb = starts[blk + 1] - s;
+  const double *bi = binfo + 16 * blk;
+  double P = bi[4];
+  bool left = bi[6] == 1.0;
+  Node nd;
+  nd.lo = left ? 0.0 : -P;
+  nd.hi = left ? P : 0.0;
+  nd.a = 0; nd.b = nb;
+  nd.wlo = cab[2 * blk]; nd.whi = cab[2 * blk + 1];
+  nd.rep = blk; nd.pad = 0;
+  nd.obase = (long long)s - 1;
+  nodes[t] = nd;
+  ex[t] = ExplicitChain{left ? P : -P, blk, 0};
+}
+
+// verification of NegCount at the far root end; doubles P where it fails; flags a restart
+__global__ void k_root_verify(const int *__restrict__ blist, int nbl, const int *__restrict__ starts, double *binfo,
+                              const int *__restrict__ excounts, int *restart) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nbl) return;
+  int blk = blist[t];
+  int nb = starts[blk + 1] - starts[blk];
+  double *bi = binfo + 16 * blk;
+  bool left = bi[6] == 1.0;
+  bool ok = left ? (excounts[t] == nb) : (excounts[t] == 0);
+  if (!ok) { bi[4] = 2.0 * bi[4]; atomicAdd(restart, 1); }
+}
+
+// guard extension test on the root intervals of block 0 (single-block subsets)
+__global__ void k_guard_check(const int *__restrict__ cab, const double *__restrict__ rlo,
+                              const double *__restrict__ rhi, int nb, double gaptol, int *need) {
+  int ca = cab[0], cb = cab[1];
+  // positions: index j at j-1 (single block starts at 0)
+  need[0] = (ca > 1 && !is_boundary(rlo[ca - 1], rhi[ca - 1], rlo[ca], rhi[ca], gaptol)) ? 1 : 0;
+  need[1] = (cb < nb && !is_boundary(rlo[cb - 2], rhi[cb - 2], rlo[cb - 1], rhi[cb - 1], gaptol)) ? 1 : 0;
+}
+
+// multi-block ranking of T-frame midpoints (S4/S6): rank = #{keys before mine}
+__global__ void k_rank(const double *__restrict__ d, const int *__restrict__ starts, int nblk,
+                       const double *__restrict__ binfo, const double *__restrict__ rlo,
+                       const double *__restrict__ rhi, long long n, double *keys) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int lo = 0, hi = nblk - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (starts[mid] <= i) lo = mid; else hi = mid - 1;
+  }
+  int blk = lo;
+  int nbk = starts[blk + 1] - starts[blk];
+  keys[i] = (nbk == 1) ? d[i] : __dadd_rn(bis_mid(rlo[i], rhi[i]), binfo[16 * blk]);
+}
+__global__ void k_rank2(const int *__restrict__ starts, int nblk, const double *__restrict__ keys, long long n,
+                        long long il, long long iu, int *colmap) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double ki = keys[i];
+  long long r = 0;
+  for (long long j = 0; j < n; j++) {
+    double kj = keys[j];
+    // positions are ordered by (block, index): ties go to the earlier position
+    r += (kj < ki) || (kj == ki && j < i);
+  }
+  long long rank = r + 1;
+  colmap[i] = (rank >= il && rank <= iu) ? (int)(rank - il) : -1;
+}
+
+void launch_check(mrrr_t h) {
+  h->host_launches++;
+  CK(cudaGetLastError());
+}
+
+// shared-tree / k-section bisection rounds until every node is finished (S5, S8)
+template <bool Y>
+void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double rtol, int nverify,
+                   const int *blist_dev, int nbl, bool *restart) {
+  Node *cur = h->nodesA.as<Node>(), *nxt = h->nodesB.as<Node>();
+  bool first = true;
+  while (nnode > 0) {
+    int m = 1;
+    while (m < h->mmax && (long long)nnode * ((1LL << (m + 1)) - 1) <= h->target_chains) m++;
+    long long P = (1LL << m) - 1;
+    long long nch = (long long)nnode * P;
+    CK(h->counts.ensure(std::max<long long>(nch, 1) * sizeof(int)));
+    int nex = first ? nverify : 0;
+    zero_counters(h);
+    k_negcount<Y><<<nblocks_for(nch + nex, 128), 128, 0, h->stream>>>(
+        cur, nnode, m, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mx.as<double2>(), h->my.as<YElt>(),
+        h->counts.as<int>(), h->excounts.as<int>());
+    launch_check(h);
+    if (nex > 0) {
+      k_root_verify<<<nblocks_for(nbl, 128), 128, 0, h->stream>>>(blist_dev, nbl, h->starts.as<int>(),
+                                                                  h->binfo.as<double>(), h->excounts.as<int>(),
+                                                                  h->cnt.as<int>() + C_NEX);
+      launch_check(h);
+    }
+    k_bisect_update<<<nblocks_for(nnode, 128), 128, 0, h->stream>>>(cur, nnode, m, h->counts.as<int>(), nxt,
+                                                                    h->cnt.as<int>() + C_NNEXT, out_lo, out_hi, rtol);
+    launch_check(h);
+    read_counters(h);
+    h->host_rounds++;
+    h->stats_h[Y ? ST_NEGY : ST_NEGX] += nch + nex;
+    if (nex > 0 && h->h_cnt[C_NEX] > 0) { *restart = true; return; }
+    nnode = h->h_cnt[C_NNEXT];
+    std::swap(cur, nxt);
+    first = false;
+  }
+}
+
+// bracket verification / repair rounds for per-index start intervals; ready nodes land in nodesA
+template <bool Y>
+int run_brackets(mrrr_t h, int nbn) {
+  BNode *cur = h->bnA.as<BNode>(), *pend = h->bnB.as<BNode>();
+  Node *ready = h->nodesA.as<Node>();
+  int nready = 0;
+  zero_counters(h);
+  while (nbn > 0) {
+    CK(cudaMemsetAsync(h->cnt.as<int>() + C_NEX, 0, sizeof(int), h->stream));
+    CK(cudaMemsetAsync(h->cnt.as<int>() + C_NPEND, 0, sizeof(int), h->stream));
+    k_bracket_chains<<<nblocks_for(nbn, 128), 128, 0, h->stream>>>(cur, nbn, h->ex.as<ExplicitChain>(),
+                                                                  h->exmap.as<int>(), h->cnt.as<int>() + C_NEX);
+    launch_check(h);
+    read_counters(h);
+    int nex = h->h_cnt[C_NEX];
+    if (nex > 0) {
+      k_negcount<Y><<<nblocks_for(nex, 128), 128, 0, h->stream>>>(
+          nullptr, 0, 1, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mx.as<double2>(),
+          h->my.as<YElt>(), h->counts.as<int>(), h->excounts.as<int>());
+      launch_check(h);
+      k_bracket_scatter<<<nblocks_for(nex, 128), 128, 0, h->stream>>>(cur, h->exmap.as<int>(), h->excounts.as<int>(),
+                                                                      nex);
+      launch_check(h);
+      h->stats_h[Y ? ST_NEGY : ST_NEGX] += nex;
+    }
+    k_bracket_update<<<nblocks_for(nbn, 128), 128, 0, h->stream>>>(cur, nbn, pend, h->cnt.as<int>() + C_NPEND, ready,
+                                                                  h->cnt.as<int>() + C_NREADY,
+                                                                  h->stats.as<long long>());
+    launch_check(h);
+    read_counters(h);
+    h->host_rounds++;
+    nbn = h->h_cnt[C_NPEND];
+    nready = h->h_cnt[C_NREADY];
+    std::swap(cur, pend);
+  }
+  return nready;
+}
+
+void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long ldz) {
+  if (ns <= 0) return;
+  long long per = 32LL * std::max<long long>(nbmax, 1);
+  long long budget = std::min<long long>(h->ws_limit / 2, 48LL << 30);
+  long long bmax = std::max<long long>(1, budget / per);
+  long long batch = std::min<long long>(ns, bmax);
+  CK(h->wsA.ensure((size_t)batch * nbmax * sizeof(dd)));
+  CK(h->wsB.ensure((size_t)batch * nbmax * sizeof(dd)));
+  bool diag = (h->flags & MRRR_KEEP_DIAG) != 0;
+  for (long long b0 = 0; b0 < ns; b0 += batch) {
+    long long nb = std::min<long long>(batch, ns - b0);
+    CK(cudaEventRecord(h->rq0, h->stream));
+    k_rqi<<<nblocks_for(nb, 64), 64, 0, h->stream>>>(
+        h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>(),
+        h->wsB.as<dd>(), nb, W, Z, ldz, diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
+        diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>());
+    launch_check(h);
+    CK(cudaEventRecord(h->rq1, h->stream));
+    CK(cudaEventSynchronize(h->rq1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, h->rq0, h->rq1));
+    h->rqi_ms += ms;
+    h->rqi_launches++;
+  }
+}
+
+struct ClusterLevel {
+  int ncl;
+};
+
+// depth-first processing of a cluster list (S8), chunked to bound the child pool
+void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long long pool_top, long long ipool_top,
+                      long long nbmax, bool from_ipool, double *W, double *Z, long long ldz, long long kout,
+                      int level) {
+  if (ncl <= 0) return;
+  bool diag = (h->flags & MRRR_KEEP_DIAG) != 0;
+  // copy the list to host (for chunking / segment offsets)
+  std::vector<Cluster> hl(ncl);
+  CK(cudaMemcpyAsync(hl.data(), list_dev, sizeof(Cluster) * ncl, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  long long per_child = nbmax * (long long)(sizeof(double2) + sizeof(YElt));
+  long long budget = std::max<long long>(per_child, h->ws_limit / 4 - pool_top * (long long)(sizeof(double2) + sizeof(YElt)));
+  int chunk = (int)std::max<long long>(1, std::min<long long>(ncl, budget / per_child));
+  for (int c0 = 0; c0 < ncl; c0 += chunk) {
+    int nc = std::min(chunk, ncl - c0);
+    // own copy of this chunk's cluster list (device list buffers are reused by recursion)
+    Buf L;
+    CK(L.ensure(sizeof(Cluster) * nc));
+    CK(cudaMemcpyAsync(L.p, hl.data() + c0, sizeof(Cluster) * nc, cudaMemcpyHostToDevice, h->stream));
+    Cluster *cl = L.as<Cluster>();
+    // grow the pools (keeping live data): child reps, their data, interval segments
+    int repbase = rep_top;
+    long long poolbase = pool_top;
+    CK(h->reps.grow_keep(sizeof(RepDesc) * (size_t)(repbase + nc), sizeof(RepDesc) * (size_t)repbase, h->stream));
+    CK(h->mx.grow_keep(sizeof(double2) * (size_t)(poolbase + (long long)nc * nbmax),
+                       sizeof(double2) * (size_t)poolbase, h->stream));
+    CK(h->my.grow_keep(sizeof(YElt) * (size_t)(poolbase + (long long)nc * nbmax), sizeof(YElt) * (size_t)poolbase,
+                       h->stream));
+    long long stot = 0, btot = 0;
+    for (int c = 0; c < nc; c++) { stot += hl[c0 + c].q - hl[c0 + c].p + 3; btot += hl[c0 + c].q - hl[c0 + c].p + 1; }
+    CK(h->ipool_lo.grow_keep(sizeof(double) * (size_t)(ipool_top + stot), sizeof(double) * (size_t)ipool_top, h->stream));
+    CK(h->ipool_hi.grow_keep(sizeof(double) * (size_t)(ipool_top + stot), sizeof(double) * (size_t)ipool_top, h->stream));
+    const double *ilo = from_ipool ? h->ipool_lo.as<double>() : h->rlo.as<double>();
+    const double *ihi = from_ipool ? h->ipool_hi.as<double>() : h->rhi.as<double>();
+    // (a) y-refined ends
+    CK(h->bnA.ensure(sizeof(BNode) * std::max<long long>(2LL * nc, 1)));
+    CK(h->bnB.ensure(sizeof(BNode) * std::max<long long>(2LL * nc, 1)));
+    CK(h->ex.ensure(sizeof(ExplicitChain) * 4LL * nc + 64));
+    CK(h->excounts.ensure(sizeof(int) * 4LL * nc + 64));
+    CK(h->exmap.ensure(sizeof(int) * 4LL * nc + 64));
+    CK(h->nodesA.ensure(sizeof(Node) * std::max<long long>(2LL * nc, 1)));
+    CK(h->nodesB.ensure(sizeof(Node) * std::max<long long>(2LL * nc, 1)));
+    CK(h->yref_lo.ensure(sizeof(double) * 2LL * nc));
+    CK(h->yref_hi.ensure(sizeof(double) * 2LL * nc));
+    k_clu_yref_init<<<nblocks_for(nc, 128), 128, 0, h->stream>>>(cl, nc, h->reps.as<RepDesc>(), ilo, ihi,
+                                                                 h->bnA.as<BNode>());
+    launch_check(h);
+    int nr = run_brackets<true>(h, 2 * nc);
+    bool dummy = false;
+    run_bisection<true>(h, nr, h->yref_lo.as<double>(), h->yref_hi.as<double>(), RTOL_Y, 0, nullptr, 0, &dummy);
+    // (b, c) shifts
+    CK(h->ss.ensure(sizeof(ShiftState) * nc));
+    CK(h->gval.ensure(sizeof(double) * 2LL * nc));
+    CK(h->valid.ensure(sizeof(int) * 2LL * nc));
+    k_clu_shift_init<<<nblocks_for(nc, 128), 128, 0, h->stream>>>(nc, h->yref_lo.as<double>(), h->yref_hi.as<double>(),
+                                                                  h->ss.as<ShiftState>());
+    launch_check(h);
+    for (int a = 0; a < MAX_ATTEMPTS; a++) {
+      CK(cudaMemsetAsync(h->cnt.as<int>() + C_NDONE, 0, sizeof(int), h->stream));
+      k_clu_attempt<<<nblocks_for(2LL * nc, 64), 64, 0, h->stream>>>(cl, nc, h->reps.as<RepDesc>(), h->my.as<YElt>(),
+                                                                     h->ss.as<ShiftState>(), h->gval.as<double>(),
+                                                                     h->valid.as<int>());
+      launch_check(h);
+      k_clu_select<<<nblocks_for(nc, 128), 128, 0, h->stream>>>(cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(),
+                                                                h->gval.as<double>(), h->valid.as<int>(), a,
+                                                                h->cnt.as<int>() + C_NDONE, h->stats.as<long long>());
+      launch_check(h);
+      read_counters(h);
+      if (h->h_cnt[C_NDONE] >= nc) break;
+    }
+    // (d) children
+    k_clu_build<<<nblocks_for(nc, 64), 64, 0, h->stream>>>(cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(),
+                                                           h->mx.as<double2>(), h->my.as<YElt>(), repbase, poolbase,
+                                                           (int)nbmax);
+    launch_check(h);
+    // (e) child starts: segments and BNode offsets from the host copy
+    std::vector<long long> seg(nc), bo(nc);
+    {
+      long long s1 = 0, b1 = 0;
+      for (int c = 0; c < nc; c++) {
+        const Cluster &C = hl[c0 + c];
+        seg[c] = ipool_top + s1;
+        s1 += C.q - C.p + 3;
+        bo[c] = b1;
+        b1 += C.q - C.p + 1;
+      }
+    }
+    CK(h->cseg.ensure(sizeof(long long) * nc));
+    CK(h->bnoff.ensure(sizeof(long long) * nc));
+    CK(cudaMemcpyAsync(h->cseg.p, seg.data(), sizeof(long long) * nc, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->bnoff.p, bo.data(), sizeof(long long) * nc, cudaMemcpyHostToDevice, h->stream));
+    CK(h->bnA.ensure(sizeof(BNode) * std::max<long long>(btot, 1)));
+    CK(h->bnB.ensure(sizeof(BNode) * std::max<long long>(btot, 1)));
+    CK(h->ex.ensure(sizeof(ExplicitChain) * 2 * btot + 64));
+    CK(h->excounts.ensure(sizeof(int) * 2 * btot + 64));
+    CK(h->exmap.ensure(sizeof(int) * 2 * btot + 64));
+    CK(h->nodesA.ensure(sizeof(Node) * std::max<long long>(btot, 1)));
+    CK(h->nodesB.ensure(sizeof(Node) * std::max<long long>(btot, 1)));
+    // BNodes of failed clusters are never written: mark them as finished by pre-filling
+    CK(cudaMemsetAsync(h->bnA.p, 0, sizeof(BNode) * btot, h->stream));
+    k_clu_child_starts<<<nblocks_for(nc, 64), 64, 0, h->stream>>>(
+        cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(), h->cseg.as<long long>(), h->bnoff.as<long long>(), ilo,
+        ihi, h->ipool_lo.as<double>(), h->ipool_hi.as<double>(), h->bnA.as<BNode>(), repbase);
+    launch_check(h);
+    int nrd = run_brackets<false>(h, (int)btot);
+    run_bisection<false>(h, nrd, h->ipool_lo.as<double>(), h->ipool_hi.as<double>(), 1e-2 * h->gaptol, 0, nullptr, 0,
+                         &dummy);
+    // (f) reclassify
+    CK(h->sing.ensure(sizeof(Singleton) * std::max<long long>(btot, 1)));
+    Buf NX;
+    CK(NX.ensure(sizeof(Cluster) * std::max<long long>(btot, 1)));
+    zero_counters(h);
+    k_clu_classify<<<nblocks_for(nc, 64), 64, 0, h->stream>>>(
+        cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(), h->cseg.as<long long>(), ilo, ihi,
+        h->ipool_lo.as<double>(), h->ipool_hi.as<double>(), h->colmap.as<int>(), h->gaptol, repbase,
+        h->sing.as<Singleton>(), h->cnt.as<int>() + C_NSING, NX.as<Cluster>(), h->cnt.as<int>() + C_NNXT,
+        diag ? h->dgf.as<int>() : nullptr, diag ? h->dgl.as<int>() : nullptr, (int)kout, h->stats.as<long long>());
+    launch_check(h);
+    read_counters(h);
+    int ns = h->h_cnt[C_NSING], nnx = h->h_cnt[C_NNXT];
+    run_rqi(h, ns, nbmax, W, Z, ldz);
+    process_clusters(h, NX.as<Cluster>(), nnx, repbase + nc, poolbase + (long long)nc * nbmax, ipool_top + stot, nbmax,
+                     true, W, Z, ldz, kout, level + 1);
+    CK(cudaStreamSynchronize(h->stream));
+    NX.release();
+    L.release();
+  }
+}
+
+int solve(mrrr_t h, const double *d, const double *e, long long n, long long il, long long iu, double *W, double *Z,
+          long long ldz, long long shard_lo, long long shard_hi, long long *jlo_out, long long *jhi_out,
+          long long ncols_cap) {
+  cudaStream_t st = h->stream;
+  const bool shard = shard_lo > 0;
+  const long long k = iu - il + 1;
+  h->last_n = n;
+  h->last_k = k;
+  h->host_rounds = h->host_launches = 0;
+  h->rqi_ms = 0;
+  h->rqi_launches = 0;
+  memset(h->stats_h, 0, sizeof(h->stats_h));
+  bool diag = (h->flags & MRRR_KEEP_DIAG) != 0;
+
+  CK(h->starts.ensure(sizeof(int) * (n + 2)));
+  CK(h->scal.ensure(64));
+  CK(h->cnt.ensure(sizeof(int) * C_NCOUNTERS));
+  CK(h->stats.ensure(sizeof(long long) * ST_N));
+  CK(cudaMemsetAsync(h->stats.p, 0, sizeof(long long) * ST_N, st));
+  CK(cudaEventRecord(h->ev[0], st));
+
+  // S1/S2
+  k_split<1024><<<1, 1024, 0, st>>>(d, e, n, h->starts.as<int>(), h->scal.as<int>(), (double *)(h->scal.as<char>() + 8),
+                                    h->scal.as<int>() + 1);
+  launch_check(h);
+  int hs[2];
+  CK(cudaMemcpyAsync(hs, h->scal.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (hs[1]) return MRRR_ERR_NONFINITE;
+  const int nblk = hs[0];
+  h->last_nblk = nblk;
+  h->h_starts.assign(nblk + 1, 0);
+  if (nblk == 1) { h->h_starts[0] = 0; h->h_starts[1] = (int)n; }
+  else CK(cudaMemcpy(h->h_starts.data(), h->starts.p, sizeof(int) * (nblk + 1), cudaMemcpyDeviceToHost));
+  const bool single = (nblk == 1);
+  if (shard && !single) { g_last_cuda_error = "shards of split matrices are not supported"; return MRRR_ERR_CUDA; }
+
+  // per-block side / computed ranges (S3/S4)
+  std::vector<int> bside(nblk, 1), cab(2 * nblk), blist;
+  long long nbmax = 1, ncomp = 0;
+  for (int b = 0; b < nblk; b++) {
+    int nb = h->h_starts[b + 1] - h->h_starts[b];
+    nbmax = std::max<long long>(nbmax, nb);
+    long long jl = 1, ju = nb;
+    if (single) {
+      jl = shard ? shard_lo : il;
+      ju = shard ? shard_hi : iu;
+    }
+    bool left = (h->root_side == 1) ? true : (h->root_side == 2) ? false : ((jl - 1) <= (nb - ju));
+    if (shard && h->root_side == 0) left = (il - 1) <= (n - iu);  // every rank must build the same root
+    bside[b] = left ? 1 : 2;
+    long long ca = jl, cb = ju;
+    if (single && nb > 1) { ca = (jl > 1) ? jl - 1 : jl; cb = (ju < nb) ? ju + 1 : ju; }
+    cab[2 * b] = (int)ca;
+    cab[2 * b + 1] = (int)cb;
+    if (nb > 1) { blist.push_back(b); ncomp += cb - ca + 1; }
+  }
+  const int nbl = (int)blist.size();
+  CK(h->bside.ensure(sizeof(int) * nblk));
+  CK(h->cab.ensure(sizeof(int) * 2 * nblk));
+  CK(h->blist.ensure(sizeof(int) * std::max(nbl, 1)));
+  CK(h->binfo.ensure(sizeof(double) * 16 * nblk));
+  CK(cudaMemcpyAsync(h->bside.p, bside.data(), sizeof(int) * nblk, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(h->cab.p, cab.data(), sizeof(int) * 2 * nblk, cudaMemcpyHostToDevice, st));
+  if (nbl) CK(cudaMemcpyAsync(h->blist.p, blist.data(), sizeof(int) * nbl, cudaMemcpyHostToDevice, st));
+
+  // pools: root reps at [0, n); children appended (sized by the workspace budget)
+  CK(h->mx.ensure(sizeof(double2) * (n + 1)));
+  CK(h->my.ensure(sizeof(YElt) * (n + 1)));
+  CK(h->lscratch.ensure(sizeof(double) * 2 * n));
+  CK(h->reps.ensure(sizeof(RepDesc) * (nblk + 1)));
+  CK(h->rlo.ensure(sizeof(double) * n));
+  CK(h->rhi.ensure(sizeof(double) * n));
+  CK(h->colmap.ensure(sizeof(int) * n));
+  CK(h->gstart.ensure(sizeof(int) * n));
+  if (diag) {
+    CK(h->ddepth.ensure(sizeof(int) * k));
+    CK(h->dgf.ensure(sizeof(int) * MAXD * k));
+    CK(h->dgl.ensure(sizeof(int) * MAXD * k));
+    CK(h->dflo.ensure(sizeof(double) * k));
+    CK(h->dfhi.ensure(sizeof(double) * k));
+    k_fill_i<<<nblocks_for(MAXD * k, 256), 256, 0, st>>>(h->dgf.as<int>(), MAXD * k, -1);
+    k_fill_i<<<nblocks_for(MAXD * k, 256), 256, 0, st>>>(h->dgl.as<int>(), MAXD * k, -1);
+  }
+  k_fill<<<nblocks_for(n, 256), 256, 0, st>>>(h->rlo.as<double>(), n, NAN);
+  k_fill<<<nblocks_for(n, 256), 256, 0, st>>>(h->rhi.as<double>(), n, NAN);
+  launch_check(h);
+
+  // S3 root
+  if (nbl) {
+    k_root<256><<<nbl, 256, 0, st>>>(d, e, n, h->starts.as<int>(), h->blist.as<int>(), h->bside.as<int>(), h->seed,
+                                     h->binfo.as<double>(), h->mx.as<double2>(), h->my.as<YElt>(),
+                                     h->lscratch.as<double>(), h->reps.as<RepDesc>());
+    launch_check(h);
+  }
+  CK(cudaEventRecord(h->ev[1], st));
+
+  // S5 root bisection
+  const double rtol = 1e-2 * h->gaptol;
+  if (nbl) {
+    long long cap = std::max<long long>(ncomp + 2, nbl);
+    CK(h->nodesA.ensure(sizeof(Node) * cap));
+    CK(h->nodesB.ensure(sizeof(Node) * cap));
+    CK(h->ex.ensure(sizeof(ExplicitChain) * (nbl + 64)));
+    CK(h->excounts.ensure(sizeof(int) * (nbl + 64)));
+    for (int attempt = 0; attempt < 64; attempt++) {
+      k_root_nodes<<<nblocks_for(nbl, 128), 128, 0, st>>>(h->blist.as<int>(), nbl, h->starts.as<int>(),
+                                                          h->binfo.as<double>(), h->cab.as<int>(), h->nodesA.as<Node>(),
+                                                          h->ex.as<ExplicitChain>());
+      launch_check(h);
+      bool restart = false;
+      run_bisection<false>(h, nbl, h->rlo.as<double>(), h->rhi.as<double>(), rtol, nbl, h->blist.as<int>(), nbl,
+                           &restart);
+      if (!restart) break;
+    }
+    // root definiteness
+    std::vector<double> hb(16 * nblk);
+    CK(cudaMemcpy(hb.data(), h->binfo.p, sizeof(double) * 16 * nblk, cudaMemcpyDeviceToHost));
+    for (int b : blist) {
+      if (hb[16 * b + 8] == 0.0) return MRRR_ERR_ROOT;
+      h->stats_h[ST_ROOT_BACKOFF] += (long long)hb[16 * b + 7];
+    }
+    // guard extension (single block): bisect one more index until separated
+    if (single && nbl) {
+      int nb = (int)n;
+      CK(h->scal.ensure(64));
+      for (int it = 0; it < nb; it++) {
+        k_guard_check<<<1, 1, 0, st>>>(h->cab.as<int>(), h->rlo.as<double>(), h->rhi.as<double>(), nb, h->gaptol,
+                                       h->cnt.as<int>() + 8);
+        launch_check(h);
+        read_counters(h);
+        bool needL = h->h_cnt[8], needR = h->h_cnt[9];
+        if (!needL && !needR) break;
+        if (needL) cab[0]--;
+        if (needR) cab[1]++;
+        CK(cudaMemcpyAsync(h->cab.p, cab.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, st));
+        // one node per new index, from the root start interval
+        std::vector<int> cab1 = cab;
+        for (int side = 0; side < 2; side++) {
+          bool need = side ? needR : needL;
+          if (!need) continue;
+          int j = side ? cab[1] : cab[0];
+          std::vector<int> cj = {j, j};
+          CK(cudaMemcpyAsync(h->cab.p, cj.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, st));
+          k_root_nodes<<<1, 1, 0, st>>>(h->blist.as<int>(), 1, h->starts.as<int>(), h->binfo.as<double>(),
+                                        h->cab.as<int>(), h->nodesA.as<Node>(), h->ex.as<ExplicitChain>());
+          launch_check(h);
+          bool rs = false;
+          run_bisection<false>(h, 1, h->rlo.as<double>(), h->rhi.as<double>(), rtol, 0, nullptr, 0, &rs);
+        }
+        CK(cudaMemcpyAsync(h->cab.p, cab.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, st));
+      }
+    }
+  }
+  CK(cudaEventRecord(h->ev[2], st));
+
+  // S4/S6 selection and classification
+  if (single) {
+    long long lo1 = il, hi1 = iu;
+    if (shard) { lo1 = 1; hi1 = n; }
+    k_colmap_range<<<nblocks_for(n, 256), 256, 0, st>>>(h->colmap.as<int>(), n, lo1, hi1);
+    launch_check(h);
+  } else {
+    Buf keys;
+    CK(keys.ensure(sizeof(double) * n));
+    k_rank<<<nblocks_for(n, 256), 256, 0, st>>>(d, h->starts.as<int>(), nblk, h->binfo.as<double>(),
+                                                 h->rlo.as<double>(), h->rhi.as<double>(), n, keys.as<double>());
+    launch_check(h);
+    k_rank2<<<nblocks_for(n, 128), 128, 0, st>>>(h->starts.as<int>(), nblk, keys.as<double>(), n, il, iu,
+                                                  h->colmap.as<int>());
+    launch_check(h);
+    CK(cudaStreamSynchronize(st));
+    keys.release();
+  }
+  k_classify_root<<<nblocks_for(n, 256), 256, 0, st>>>(h->starts.as<int>(), h->cab.as<int>(), nblk,
+                                                        h->rlo.as<double>(), h->rhi.as<double>(), h->gaptol,
+                                                        h->gstart.as<int>(), n);
+  launch_check(h);
+  if (shard) {
+    // ownership: groups that START in [shard_lo, shard_hi]; owned range [jlo, jhi]
+    std::vector<int> gs(n);
+    CK(cudaMemcpyAsync(gs.data(), h->gstart.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    long long jlo = -1, jhi = -2;
+    for (long long j = shard_lo; j <= shard_hi; j++)
+      if (gs[j - 1] == 1) { jlo = j; break; }
+    if (jlo > 0) {
+      long long last = jlo;
+      for (long long j = shard_lo; j <= shard_hi; j++)
+        if (gs[j - 1] == 1) last = j;
+      jhi = last;
+      while (jhi < cab[1] && gs[jhi] == 0) jhi++;
+    } else {
+      jlo = shard_hi + 1; jhi = shard_hi;
+    }
+    *jlo_out = jlo;
+    *jhi_out = jhi;
+    long long own = jhi - jlo + 1;
+    if (own > ncols_cap) return MRRR_ERR_NOMEM;
+    il = jlo; iu = jhi;
+    if (own <= 0) { CK(cudaEventRecord(h->ev[3], st)); CK(cudaStreamSynchronize(st)); return 0; }
+    k_colmap_range<<<nblocks_for(n, 256), 256, 0, st>>>(h->colmap.as<int>(), n, jlo, jhi);
+    launch_check(h);
+  }
+  const long long kout = iu - il + 1;
+  if (!single) CK(cudaMemset2DAsync(Z, sizeof(double) * ldz, 0, sizeof(double) * n, kout, st));
+  CK(h->sing.ensure(sizeof(Singleton) * std::max<long long>(ncomp, 1)));
+  CK(h->clusA.ensure(sizeof(Cluster) * std::max<long long>(ncomp, 1)));
+  zero_counters(h);
+  k_groups_root<<<nblocks_for(n, 256), 256, 0, st>>>(
+      h->starts.as<int>(), nblk, h->cab.as<int>(), h->gstart.as<int>(), h->colmap.as<int>(), h->rlo.as<double>(),
+      h->rhi.as<double>(), n, h->sing.as<Singleton>(), h->cnt.as<int>() + C_NSING, h->clusA.as<Cluster>(),
+      h->cnt.as<int>() + C_NCLUS, diag ? h->dgf.as<int>() : nullptr, diag ? h->dgl.as<int>() : nullptr, (int)kout,
+      h->stats.as<long long>());
+  launch_check(h);
+  read_counters(h);
+  int ns = h->h_cnt[C_NSING], ncl = h->h_cnt[C_NCLUS];
+  CK(cudaEventRecord(h->ev[3], st));
+
+  // S9/S10 root singletons
+  run_rqi(h, ns, nbmax, W, Z, ldz);
+  CK(cudaEventRecord(h->ev[4], st));
+  // S8 clusters (depth-first, chunked)
+  if (ncl > 0) {
+    Buf L0;
+    CK(L0.ensure(sizeof(Cluster) * ncl));
+    CK(cudaMemcpyAsync(L0.p, h->clusA.p, sizeof(Cluster) * ncl, cudaMemcpyDeviceToDevice, st));
+    process_clusters(h, L0.as<Cluster>(), ncl, nblk, n, 0, nbmax, false, W, Z, ldz, kout, 0);
+    L0.release();
+  }
+  if (!single || n == 1) {
+    k_trivial<<<nblocks_for(nblk, 128), 128, 0, st>>>(d, h->starts.as<int>(), nblk, h->colmap.as<int>(), W, Z, ldz,
+                                                      diag ? h->ddepth.as<int>() : nullptr,
+                                                      diag ? h->dflo.as<double>() : nullptr,
+                                                      diag ? h->dfhi.as<double>() : nullptr,
+                                                      diag ? h->dgf.as<int>() : nullptr,
+                                                      diag ? h->dgl.as<int>() : nullptr, h->rlo.as<double>(),
+                                                      h->rhi.as<double>());
+    launch_check(h);
+  }
+  CK(cudaEventRecord(h->ev[5], st));
+  CK(cudaStreamSynchronize(st));
+  // stats
+  long long sd[ST_N];
+  CK(cudaMemcpy(sd, h->stats.p, sizeof(sd), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < ST_N; i++) h->stats_h[i] += sd[i];
+  h->stats_h[ST_ROUNDS] = h->host_rounds;
+  h->stats_h[ST_LAUNCHES] = h->host_launches;
+  h->stats_h[ST_NBLK] = nblk;
+  float ms;
+  CK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[5])); h->times[0] = ms;
+  CK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1])); h->times[1] = ms;
+  CK(cudaEventElapsedTime(&ms, h->ev[1], h->ev[2])); h->times[2] = ms;
+  CK(cudaEventElapsedTime(&ms, h->ev[2], h->ev[3])); h->times[3] = ms;
+  CK(cudaEventElapsedTime(&ms, h->ev[4], h->ev[5])); h->times[4] = ms;
+  CK(cudaEventElapsedTime(&ms, h->ev[3], h->ev[4])); h->times[5] = ms;
+  h->times[6] = h->rqi_launches ? h->rqi_ms / h->rqi_launches : 0.0;
+  h->times[7] = (double)h->rqi_launches;
+  return 0;
+}
+
+int check_args(const double *d, const double *e, long long n, long long il, long long iu, const double *W,
+               const double *Z, long long ldz) {
+  if (!d) return -2;
+  if (n > 1 && !e) return -3;
+  if (n < 1) return -4;
+  if (il < 1 || il > n) return -5;
+  if (iu < il || iu > n) return -6;
+  if (!W) return -7;
+  if (!Z) return -8;
+  if (ldz < n) return -9;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
+  if (!out) return -1;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    g_last_cuda_error = "no CUDA device";
+    return MRRR_ERR_NODEVICE;
+  }
+  mrrr_t h = new mrrr_ctx();
+  try {
+    if (o && o->device >= 0) { CK(cudaSetDevice(o->device)); h->device = o->device; }
+    else CK(cudaGetDevice(&h->device));
+    if (o && o->stream) h->stream = (cudaStream_t)o->stream;
+    else { CK(cudaStreamCreate(&h->stream)); h->own_stream = true; }  // blocking: ordered with the legacy stream
+    if (o && o->gaptol > 0) h->gaptol = o->gaptol;
+    if (o && o->seed) h->seed = o->seed;
+    if (o) { h->root_side = o->root_side; h->flags = o->flags; }
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    h->ws_limit = (o && o->ws_limit > 0) ? o->ws_limit : (long long)(0.6 * (double)fr);
+    if (const char *s = getenv("MRRR_TARGET_CHAINS")) h->target_chains = atoll(s);
+    if (const char *s = getenv("MRRR_MMAX")) h->mmax = atoi(s);
+    for (auto &ev : h->ev) CK(cudaEventCreate(&ev));
+    CK(cudaEventCreate(&h->rq0));
+    CK(cudaEventCreate(&h->rq1));
+    CK(cudaMallocHost(&h->h_cnt, sizeof(int) * C_NCOUNTERS));
+  } catch (Err &er) {
+    delete h;
+    return er.code;
+  }
+  *out = h;
+  return 0;
+}
+
+int mrrr_eig(mrrr_t h, const double *d, const double *e, int64_t n, int64_t il, int64_t iu, double *W, double *Z,
+             int64_t ldz) {
+  if (!h) return -1;
+  int a = check_args(d, e, n, il, iu, W, Z, ldz);
+  if (a) return a;
+  try {
+    CK(cudaSetDevice(h->device));
+    return solve(h, d, e, n, il, iu, W, Z, ldz, 0, 0, nullptr, nullptr, 0);
+  } catch (Err &er) {
+    return er.code;
+  }
+}
+
+int mrrr_eig_shard(mrrr_t h, const double *d, const double *e, int64_t n, int64_t sl, int64_t su, double *W,
+                   double *Z, int64_t ldz, int64_t ncols_cap, int64_t *jlo, int64_t *jhi) {
+  if (!h) return -1;
+  int a = check_args(d, e, n, sl, su, W, Z, ldz);
+  if (a) return a;
+  if (!jlo || !jhi) return -11;
+  try {
+    CK(cudaSetDevice(h->device));
+    long long lo = 0, hi = -1;
+    int rc = solve(h, d, e, n, 1, n, W, Z, ldz, sl, su, &lo, &hi, ncols_cap);
+    *jlo = lo;
+    *jhi = hi;
+    return rc;
+  } catch (Err &er) {
+    return er.code;
+  }
+}
+
+int mrrr_eig_host(mrrr_t h, const double *d, const double *e, int64_t n, int64_t il, int64_t iu, double *W,
+                  double *Z, int64_t ldz) {
+  if (!h) return -1;
+  int a = check_args(d, e, n, il, iu, W, Z, ldz);
+  if (a) return a;
+  double *dd_ = nullptr, *de = nullptr, *dW = nullptr, *dZ = nullptr;
+  long long k = iu - il + 1;
+  int rc = 0;
+  try {
+    CK(cudaSetDevice(h->device));
+    CK(cudaMalloc(&dd_, sizeof(double) * n));
+    CK(cudaMalloc(&de, sizeof(double) * std::max<long long>(n - 1, 1)));
+    CK(cudaMalloc(&dW, sizeof(double) * k));
+    CK(cudaMalloc(&dZ, sizeof(double) * n * k));
+    CK(cudaMemcpyAsync(dd_, d, sizeof(double) * n, cudaMemcpyHostToDevice, h->stream));
+    if (n > 1) CK(cudaMemcpyAsync(de, e, sizeof(double) * (n - 1), cudaMemcpyHostToDevice, h->stream));
+    rc = solve(h, dd_, de, n, il, iu, dW, dZ, n, 0, 0, nullptr, nullptr, 0);
+    if (rc == 0) {
+      CK(cudaMemcpyAsync(W, dW, sizeof(double) * k, cudaMemcpyDeviceToHost, h->stream));
+      if (ldz == n) CK(cudaMemcpyAsync(Z, dZ, sizeof(double) * n * k, cudaMemcpyDeviceToHost, h->stream));
+      else CK(cudaMemcpy2DAsync(Z, sizeof(double) * ldz, dZ, sizeof(double) * n, sizeof(double) * n, k,
+                                cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+    }
+  } catch (Err &er) {
+    rc = er.code;
+  }
+  cudaFree(dd_); cudaFree(de); cudaFree(dW); cudaFree(dZ);
+  return rc;
+}
+
+int mrrr_get_stats(mrrr_t h, int64_t *s, int32_t ns) {
+  if (!h || !s) return -1;
+  for (int i = 0; i < ns && i < MRRR_NSTATS; i++) s[i] = h->stats_h[i];
+  return 0;
+}
+
+int mrrr_get_times(mrrr_t h, double *ms, int32_t nt) {
+  if (!h || !ms) return -1;
+  for (int i = 0; i < nt && i < 8; i++) ms[i] = h->times[i];
+  return 0;
+}
+
+int mrrr_get_diag(mrrr_t h, mrrr_diag *g) {
+  if (!h || !g) return -1;
+  if (!(h->flags & MRRR_KEEP_DIAG)) return -1;
+  try {
+    long long n = h->last_n, k = h->last_k;
+    int nblk = h->last_nblk;
+    CK(cudaStreamSynchronize(h->stream));
+    if (g->nblocks) g->nblocks[0] = nblk;
+    if (g->block_start) for (int b = 0; b <= nblk; b++) g->block_start[b] = h->h_starts[b];
+    if (g->mu || g->side) {
+      std::vector<double> hb(16 * nblk);
+      CK(cudaMemcpy(hb.data(), h->binfo.p, sizeof(double) * 16 * nblk, cudaMemcpyDeviceToHost));
+      for (int b = 0; b < nblk; b++) {
+        bool triv = h->h_starts[b + 1] - h->h_starts[b] == 1;
+        if (g->mu) g->mu[b] = triv ? 0.0 : hb[16 * b];
+        if (g->side) g->side[b] = triv ? 0 : (int)hb[16 * b + 6];
+      }
+    }
+    if (g->root_lo) CK(cudaMemcpy(g->root_lo, h->rlo.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    if (g->root_hi) CK(cudaMemcpy(g->root_hi, h->rhi.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    if (g->root_lo && nblk > 1)
+      for (int b = 0; b < nblk; b++)
+        if (h->h_starts[b + 1] - h->h_starts[b] == 1) {
+          // size-1 blocks: [alpha, alpha] (oracle convention); alpha comes from fin_lo via the trivial kernel
+        }
+    if (g->root_gstart) CK(cudaMemcpy(g->root_gstart, h->gstart.p, sizeof(int) * n, cudaMemcpyDeviceToHost));
+    if (g->depth) CK(cudaMemcpy(g->depth, h->ddepth.p, sizeof(int) * k, cudaMemcpyDeviceToHost));
+    if (g->grp_first) CK(cudaMemcpy(g->grp_first, h->dgf.p, sizeof(int) * MAXD * k, cudaMemcpyDeviceToHost));
+    if (g->grp_last) CK(cudaMemcpy(g->grp_last, h->dgl.p, sizeof(int) * MAXD * k, cudaMemcpyDeviceToHost));
+    if (g->fin_lo) CK(cudaMemcpy(g->fin_lo, h->dflo.p, sizeof(double) * k, cudaMemcpyDeviceToHost));
+    if (g->fin_hi) CK(cudaMemcpy(g->fin_hi, h->dfhi.p, sizeof(double) * k, cudaMemcpyDeviceToHost));
+  } catch (Err &er) {
+    return er.code;
+  }
+  return 0;
+}
+
+const char *mrrr_strerror(int code) {
+  switch (code) {
+    case MRRR_OK: return "success";
+    case MRRR_ERR_NONFINITE: return "NaN or Inf in d or e";
+    case MRRR_ERR_CUDA: return g_last_cuda_error.c_str();
+    case MRRR_ERR_NOMEM: return "device memory exhausted";
+    case MRRR_ERR_ROOT: return "no definite root representation found";
+    case MRRR_ERR_NODEVICE: return "no CUDA device";
+    default: return code < 0 ? "invalid argument" : "unknown error";
+  }
+}
+
+int mrrr_destroy(mrrr_t h) {
+  if (!h) return 0;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  Buf *bufs[] = {&h->starts, &h->scal, &h->binfo, &h->bside, &h->blist, &h->cab, &h->mx, &h->my, &h->lscratch,
+                 &h->reps, &h->rlo, &h->rhi, &h->colmap, &h->gstart, &h->nodesA, &h->nodesB, &h->counts, &h->ex,
+                 &h->excounts, &h->exmap, &h->bnA, &h->bnB, &h->sing, &h->clusA, &h->clusB, &h->ss, &h->gval,
+                 &h->valid, &h->cseg, &h->bnoff, &h->ipool_lo, &h->ipool_hi, &h->yref_lo, &h->yref_hi, &h->wsA,
+                 &h->wsB, &h->stats, &h->cnt, &h->ddepth, &h->dgf, &h->dgl, &h->dflo, &h->dfhi};
+  for (Buf *b : bufs) b->release();
+  for (auto &ev : h->ev) cudaEventDestroy(ev);
+  cudaEventDestroy(h->rq0);
+  cudaEventDestroy(h->rq1);
+  if (h->h_cnt) cudaFreeHost(h->h_cnt);
+  if (h->own_stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,301 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 MRRR hot path (BASELINE.json metric: eigenvector entries/s = k*n/s).
+
+One step = one complete solve (every SURVEY §8(a) row: split, root, perturbation, root bisection,
+classification, cluster path, singleton RQI + eigenvectors, W/Z stores) of the workload on device.
+
+    python bench.py                          # N=1, C2 (random n=8192, all pairs)
+    python bench.py --workload C5a --steps 3
+    python bench.py --impl reference         # the CPU oracle timed on this host (reference arm)
+    torchrun --nproc-per-node N bench.py --gpus N   # index-range shards, one rank per GPU
+
+Timing: W warm-up steps, then K steps; each step is bracketed by CUDA events on the solver's stream
+with an L2 flush (256 MiB write) between steps outside the events; barrier + synchronize around the
+timed region; max over ranks.  e2e: the same metric through mrrr_eig_host (host buffers; H2D of d, e
+and D2H of W, Z inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import mrrr_inputs as mi  # noqa: E402
+
+METRIC = "eigenvector entries/s (k·n/s), fp64 mixed-prec MRRR all-pairs, 1/2/4/8 B200"
+UNIT = "entries/s"
+
+
+def peaks():
+    out = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            out.update(json.load(f))
+    except Exception:
+        out["hbm_gbs"] = 6650.0
+        out["hbm_src"] = "fallback"
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak_r01.json")) as f:
+            out["fp64"] = json.load(f)
+    except Exception:
+        out["fp64"] = None
+    return out
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.p = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+                self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            except Exception:
+                pass
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def flush_l2(buf):
+    buf.fill_(1.0)  # 256 MiB > 126 MB L2
+
+
+def reference_arm(args, rank, world):
+    """The CPU oracle (oracle/, test infrastructure) timed on this host: the reference arm."""
+    if rank != 0:
+        return
+    import oracle
+    cfg = mi.CONFIGS[args.workload]
+    d, e = cfg.matrix()
+    ksamp = args.ref_k
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        oracle.mrrr(d, e, 1, min(8, cfg.n), threads=threads)
+    ts = []
+    for s in range(args.steps):
+        a = 1 + (s * 997) % max(cfg.k - ksamp, 1)
+        t0 = time.perf_counter()
+        r = oracle.mrrr(d, e, a, a + ksamp - 1, threads=threads, root_side=1)
+        ts.append(time.perf_counter() - t0)
+        assert r.info == 0
+    t = float(np.mean(ts))
+    v = ksamp * cfg.n / t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64+binary128", "data": "synthetic",
+            "config": {"workload": args.workload, "n": cfg.n, "k_sample": ksamp, "il_iu": "windows of the C2 index range",
+                       "parallelism": "host OpenMP"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": f"{ksamp} eigenpairs per step of {args.workload} (n={cfg.n}), root bisection "
+                                       f"of the sample + guards, binary128 RQI"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, d, e, ksamp):
+    import oracle
+    threads = os.cpu_count() or 1
+    oracle.mrrr(d, e, 1, 4, threads=threads)
+    t0 = time.perf_counter()
+    r = oracle.mrrr(d, e, 1, ksamp, threads=threads, root_side=1)
+    t = time.perf_counter() - t0
+    assert r.info == 0
+    return {"value": ksamp * cfg.n / t, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"eigenpairs 1..{ksamp} of {cfg.name} (n={cfg.n}) incl. root bisection of the sample; "
+                      f"{t:.2f} s wall on {threads} threads"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="C2", choices=sorted(mi.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-k", type=int, default=256)
+    ap.add_argument("--cpu-k", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1401_4950_b200 as mrrr
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = mi.CONFIGS[args.workload]
+    d_np, e_np = cfg.matrix()
+    n, k = cfg.n, cfg.k
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    solver = mrrr.Solver(device=local, stream=stream.cuda_stream)
+    d = torch.from_numpy(d_np).to(dev)
+    e = torch.from_numpy(e_np).to(dev)
+    # shard of the index range: contiguous blocks per rank
+    if world > 1:
+        per = (k + world - 1) // world
+        sl, su = cfg.il + rank * per, min(cfg.il + (rank + 1) * per - 1, cfg.iu)
+        W = None
+    else:
+        W = torch.empty(k, dtype=torch.float64, device=dev)
+        Zt = torch.empty((k, n), dtype=torch.float64, device=dev)
+    flushbuf = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=dev)
+    Wall = torch.empty(k, dtype=torch.float64, device=dev) if world > 1 else None
+
+    def step():
+        with torch.cuda.stream(stream):
+            if world == 1:
+                solver.eig(d, e, cfg.il, cfg.iu, W=W, Z=Zt)
+            else:
+                jlo, jhi, Wl, Zl = solver.eig_shard(d, e, sl, su)
+                # eigenvalue list allgather over NCCL (the only collective)
+                cnt = torch.tensor([jhi - jlo + 1], device=dev)
+                sizes = [torch.zeros_like(cnt) for _ in range(world)]
+                dist.all_gather(sizes, cnt)
+                m = int(max(int(x) for x in sizes))
+                buf = torch.zeros(m, dtype=torch.float64, device=dev)
+                buf[:Wl.numel()] = Wl
+                parts = [torch.empty(m, dtype=torch.float64, device=dev) for _ in range(world)]
+                dist.all_gather(parts, buf)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    st0 = solver.stats()
+    launches_per_step = st0["launches"]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = []
+    rq_ms, rq_n = 0.0, 0
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            flush_l2(flushbuf)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step()
+            b.record(stream)
+            evs.append((a, b))
+            tm = solver.times()
+            rq_ms += tm["rqi_ms_per_launch"] * tm["rqi_launches"]
+            rq_n += int(tm["rqi_launches"])
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    times = [a.elapsed_time(b) for a, b in evs]
+    ms = float(np.sum(times)) / args.steps
+    t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_max = float(t_local.item())
+    value = k * n / (ms_max * 1e-3)
+    stats = solver.stats()
+    tphase = solver.times()
+
+    # roofline of the dominant kernel (k_rqi): counted FP64 flops per launch / event-timed launch duration
+    pk = peaks()
+    fp = pk.get("fp64") or {}
+    roof = None
+    if fp:
+        from paper_1401_4950_b200 import flops as fl
+        launch_ms = rq_ms / max(rq_n, 1)
+        fl_launch = fl.rqi_flops(stats, n, fp.get("w_div", 8.0)) / max(int(tphase["rqi_launches"]), 1)
+        achieved = fl_launch / (launch_ms * 1e-3) / 1e12
+        peak = fp["fp64_tflops"]
+        roof = {"bound": "alu", "kernel": "k_rqi", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None,
+                "peak_src": "profiles/fp64_peak_r01.json (measured DFMA rate x 2, this pool's B200)",
+                "launch_ms": launch_ms, "flops_per_launch": fl_launch}
+
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        import torch as _t
+        hd = _t.from_numpy(d_np).pin_memory().numpy()
+        he = _t.from_numpy(e_np).pin_memory().numpy()
+        hs = mrrr.Solver(device=local)
+        hs.eig_host(hd, he, cfg.il, cfg.iu)
+        t0 = time.perf_counter()
+        reps = max(1, min(args.steps, 3))
+        for _ in range(reps):
+            Wh, Zh = hs.eig_host(hd, he, cfg.il, cfg.iu)
+        te = (time.perf_counter() - t0) / reps
+        hs.close()
+        e2e = {"value": k * n / te, "unit": UNIT, "h2d_bytes_per_step": 8 * (2 * n - 1),
+               "d2h_bytes_per_step": 8 * k + 8 * k * n, "ms_per_step": te * 1e3,
+               "path": "mrrr_eig_host (pageable-or-pinned host in/out, device workspace cached)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, d_np, e_np, min(args.cpu_k, k))
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64+dd", "data": "synthetic",
+                "config": {"workload": cfg.name, "n": n, "k": k, "il": cfg.il, "iu": cfg.iu, "desc": cfg.note,
+                           "parallelism": f"index shards x{world}" if world > 1 else "single GPU",
+                           "l2": "flushed between steps (256 MiB write, outside the events)"},
+                "gpu_launches": int(launches_per_step) * args.steps,
+                "phases_ms": tphase, "stats": stats, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

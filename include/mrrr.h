@@ -98,8 +98,10 @@ int mrrr_eig_shard(mrrr_t h, const double *d, const double *e, int64_t n, int64_
  * (robustness failures), 4 shift attempts, 5 RQI iterations,
  * 6 RQI bisection fallbacks, 7 bracket repairs, 8 root back-offs,
  * 9 failed clusters, 10 x-NegCount evaluations, 11 y-NegCount evaluations,
- * 12 Getvec calls, 13 bisection rounds, 14 kernel launches, 15 nblocks. */
-#define MRRR_NSTATS 16
+ * 12 Getvec calls, 13 bisection rounds, 14 kernel launches, 15 nblocks,
+ * 16 dd qd steps in k_rqi (dstqds/dqds element steps), 17 of them with the twist quantity gamma_k,
+ * 18 z-solve element steps (norm pass), 19 z-solve element steps that write Z. */
+#define MRRR_NSTATS 24
 int mrrr_get_stats(mrrr_t h, int64_t *stats, int32_t nstats);
 
 /* Diagnostics of the last call made with MRRR_KEEP_DIAG (host buffers owned
@@ -127,6 +129,11 @@ int mrrr_get_diag(mrrr_t h, mrrr_diag *g);
  * Also the average duration of the dominant kernel launches: [6] ms per
  * k_rqi launch (events around each launch), [7] number of k_rqi launches. */
 int mrrr_get_times(mrrr_t h, double *ms, int32_t nt);
+
+/* Built-in self tests (run on the current device).  which = 1: the NegCount division fast path
+ * (csrc/kernels.cuh div_ieee) against the IEEE __ddiv_rn on n seeded operand pairs (random bit
+ * patterns incl. subnormals/inf/nan, and the O(1) NegCount regime); *bad = #bitwise mismatches. */
+int mrrr_selftest(int which, int64_t n, uint64_t seed, int64_t *bad);
 
 const char *mrrr_strerror(int code);
 

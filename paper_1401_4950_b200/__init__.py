@@ -23,10 +23,11 @@ LIB_PATH = os.path.join(HERE, "libmrrr.so")
 
 KEEP_DIAG = 1
 MAXD = 8
-NSTATS = 16
+NSTATS = 24
 STAT_NAMES = ["d_max", "n_clusters", "largest_cluster", "uncertified", "shift_attempts", "rqi_iters",
               "rqi_fallbacks", "bracket_fixes", "root_backoffs", "failed", "negcount_x", "negcount_y",
-              "getvec_calls", "rounds", "launches", "nblocks"]
+              "getvec_calls", "rounds", "launches", "nblocks", "qd_steps", "qdg_steps", "z_steps", "zw_steps",
+              "s20", "s21", "s22", "s23"]
 TIME_NAMES = ["total", "split_root", "root_bisection", "classification", "clusters", "singletons",
               "rqi_ms_per_launch", "rqi_launches"]
 
@@ -63,6 +64,8 @@ def load() -> C.CDLL:
         L.mrrr_get_stats.argtypes = [vp, vp, C.c_int32]
         L.mrrr_get_times.argtypes = [vp, vp, C.c_int32]
         L.mrrr_get_diag.argtypes = [vp, C.POINTER(_Diag)]
+        L.mrrr_selftest.argtypes = [C.c_int, i64, C.c_uint64, C.POINTER(i64)]
+        L.mrrr_selftest.restype = C.c_int
         L.mrrr_strerror.argtypes = [C.c_int]
         L.mrrr_strerror.restype = C.c_char_p
         L.mrrr_destroy.argtypes = [vp]
@@ -74,7 +77,14 @@ def load() -> C.CDLL:
 
 
 EXPORTED = ["mrrr_init", "mrrr_eig", "mrrr_eig_host", "mrrr_eig_shard", "mrrr_get_stats", "mrrr_get_diag",
-            "mrrr_get_times", "mrrr_strerror", "mrrr_destroy"]
+            "mrrr_get_times", "mrrr_selftest", "mrrr_strerror", "mrrr_destroy"]
+
+
+def selftest(which: int, n: int, seed: int = 1) -> int:
+    """Run a built-in device self test; returns the number of mismatches (see include/mrrr.h)."""
+    bad = C.c_int64()
+    _check(load().mrrr_selftest(which, n, seed, C.byref(bad)), "mrrr_selftest")
+    return bad.value
 
 
 def _check(rc: int, what: str):

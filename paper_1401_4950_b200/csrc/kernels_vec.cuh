@@ -299,62 +299,105 @@ struct GV {
   int r, c;
 };
 
+// representation element as three 16-byte loads
+struct YV {
+  dd d, dl, dll;
+};
+__device__ __forceinline__ YV ldy(const YElt *__restrict__ y, int i) {
+  const double2 *q = reinterpret_cast<const double2 *>(y + i);
+  double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+  YV v;
+  v.d = dd_make(a.x, a.y);
+  v.dl = dd_make(b.x, b.y);
+  v.dll = dd_make(c.x, c.y);
+  return v;
+}
+__device__ __forceinline__ dd ldw(const dd *w, long long off) {
+  double2 a = *reinterpret_cast<const double2 *>(w + off);
+  return dd_make(a.x, a.y);
+}
+__device__ __forceinline__ void stw(dd *w, long long off, dd v) {
+  *reinterpret_cast<double2 *>(w + off) = make_double2(v.hi, v.lo);
+}
+
 // Getvec: r < 0 -> full twisted factorization + twist search (iteration 1);
-// r >= 0 (0-based) -> only the r-twisted factorization
+// r >= 0 (0-based) -> only the r-twisted factorization.
+// Representation elements and workspace values are prefetched two steps ahead.
 __device__ void getvec_dd(const YElt *__restrict__ y, int nb, dd lam, int r, dd *A, dd *B, long long S, GV &g) {
   int cnt = 0;
+  const int last = nb - 1;
   if (r < 0) {
     dd s = dd_neg(lam);
-    for (int i = 0; i < nb - 1; i++) {
+    YV c0 = ldy(y, 0), c1 = ldy(y, min(1, last));
+    for (int i = 0; i < last; i++) {
+      YV c2 = ldy(y, min(i + 2, last));
       dd den, rr, out, xn;
-      qd_step(s, ld_d(y + i), ld_dl(y + i), ld_dll(y + i), lam, den, rr, out, xn);
-      A[(long long)i * S] = s;
-      B[(long long)i * S] = (den.hi == 0.0) ? dd_mark() : out;
+      qd_step(s, c0.d, c0.dl, c0.dll, lam, den, rr, out, xn);
+      stw(A, (long long)i * S, s);
+      stw(B, (long long)i * S, (den.hi == 0.0) ? dd_mark() : out);
       cnt += dd_sb(den);
       s = xn;
+      c0 = c1;
+      c1 = c2;
     }
-    dd dn = dd_add(s, ld_d(y + nb - 1));
+    dd dlast = c0.d;  // y[nb-1].d
+    dd dn = dd_add(s, dlast);
     cnt += dd_sb(dn);
     dd gam = dn;  // gamma_n = s(n) + d(n) = d+(n)
     int rbest = -1;
     dd best = dd_from(INFINITY), gbest = gam;
-    if (!isnan(gam.hi)) { rbest = nb - 1; best = dd_abs(gam); }
-    dd p = dd_sub(ld_d(y + nb - 1), lam);
-    for (int i = nb - 2; i >= 0; i--) {
-      dd di = ld_d(y + i);
-      dd den, rr, out, xn;
-      qd_step(p, ld_dll(y + i), ld_dl(y + i), di, lam, den, rr, out, xn);
-      dd si = A[(long long)i * S];
-      dd gi = dd_add(si, dd_mul(dd_mul(di, rr), p));
-      A[(long long)i * S] = (den.hi == 0.0) ? dd_mark() : out;
-      if (!isnan(gi.hi)) {
-        dd ag = dd_abs(gi);
-        if (!dd_lt(best, ag)) { best = ag; rbest = i; gbest = gi; }
+    if (!isnan(gam.hi)) { rbest = last; best = dd_abs(gam); }
+    dd p = dd_sub(dlast, lam);
+    if (last >= 1) {
+      YV b0 = ldy(y, last - 1), b1 = ldy(y, max(last - 2, 0));
+      dd a0 = ldw(A, (long long)(last - 1) * S), a1 = ldw(A, (long long)max(last - 2, 0) * S);
+      for (int i = last - 1; i >= 0; i--) {
+        int i2 = max(i - 2, 0);
+        YV b2 = ldy(y, i2);
+        dd a2 = ldw(A, (long long)i2 * S);
+        dd den, rr, out, xn;
+        qd_step(p, b0.dll, b0.dl, b0.d, lam, den, rr, out, xn);
+        dd gi = dd_add(a0, dd_mul(dd_mul(b0.d, rr), p));
+        stw(A, (long long)i * S, (den.hi == 0.0) ? dd_mark() : out);
+        if (!isnan(gi.hi)) {
+          dd ag = dd_abs(gi);
+          if (!dd_lt(best, ag)) { best = ag; rbest = i; gbest = gi; }
+        }
+        p = xn;
+        b0 = b1; b1 = b2;
+        a0 = a1; a1 = a2;
       }
-      p = xn;
     }
     g.r = rbest;
     g.gamma = gbest;
   } else {
-    dd s = dd_neg(lam), p = dd_sub(ld_d(y + nb - 1), lam), gamma = dd_from(0.0);
+    dd s = dd_neg(lam), gamma = dd_from(0.0);
+    dd dlast = ldy(y, last).d;
+    dd p = dd_sub(dlast, lam);
     // unified loop: k < r forward dstqds step i = k; else backward dqds step i = nb-2-(k-r)
-    for (int k = 0; k < nb - 1; k++) {
-      bool fw = k < r;
-      int i = fw ? k : nb - 2 - (k - r);
-      dd di = ld_d(y + i), dli = ld_dl(y + i), dlli = ld_dll(y + i);
+    const int K = last;
+#define IDX(k) ((k) < r ? (k) : last - 1 - ((k) - r))
+    YV c0 = ldy(y, IDX(0)), c1 = ldy(y, IDX(min(1, max(K - 1, 0))));
+    for (int k = 0; k < K; k++) {
+      YV c2 = ldy(y, IDX(min(k + 2, K - 1)));
+      const bool fw = k < r;
+      const int i = IDX(k);
       dd den, rr, out, xn;
-      qd_step(fw ? s : p, fw ? di : dlli, dli, fw ? dlli : di, lam, den, rr, out, xn);
+      qd_step(fw ? s : p, fw ? c0.d : c0.dll, c0.dl, fw ? c0.dll : c0.d, lam, den, rr, out, xn);
       if (fw) {
-        B[(long long)i * S] = (den.hi == 0.0) ? dd_mark() : out;
+        stw(B, (long long)i * S, (den.hi == 0.0) ? dd_mark() : out);
         s = xn;
       } else {
-        A[(long long)i * S] = (den.hi == 0.0) ? dd_mark() : out;
-        if (i == r) gamma = dd_add(s, dd_mul(dd_mul(di, rr), p));
+        stw(A, (long long)i * S, (den.hi == 0.0) ? dd_mark() : out);
+        if (i == r) gamma = dd_add(s, dd_mul(dd_mul(c0.d, rr), p));
         p = xn;
       }
       cnt += dd_sb(den);
+      c0 = c1;
+      c1 = c2;
     }
-    if (r == nb - 1) gamma = dd_add(s, ld_d(y + nb - 1));
+#undef IDX
+    if (r == last) gamma = dd_add(s, dlast);
     cnt += dd_sb(gamma);
     g.r = r;
     g.gamma = gamma;
@@ -363,27 +406,35 @@ __device__ void getvec_dd(const YElt *__restrict__ y, int nb, dd lam, int r, dd 
 }
 
 // z solve of N_r^T z = e_r with zero-pivot substitution (A-25); returns ||z||^2.
-// If Zc != nullptr writes fl64(z_i * inv) to Zc[i].
+// Backward branch (i = r-1 .. 0, uses l+ in B) then forward branch (i = r .. nb-2, uses u- in A),
+// as one loop over k with the workspace prefetched two steps ahead.  If Zc != nullptr writes
+// fl64(z_i * inv) to Zc[i].
 __device__ dd zsolve(const YElt *__restrict__ y, int nb, int r, const dd *A, const dd *B, long long S, dd inv,
                      double *Zc) {
   dd zz = dd_from(1.0);
   if (Zc) Zc[r] = inv.hi;
+  const int K = nb - 1;
+  if (K <= 0) return zz;
   // z(r+1) by the regular recurrence for the backward branch's substitution at i = r-1
   dd zp1 = dd_from(0.0);
   if (r < nb - 1) {
-    dd u = A[(long long)r * S];
+    dd u = ldw(A, (long long)r * S);
     if (!is_mark(u)) zp1 = dd_neg(u);
   }
+#define WOFF(k) ((long long)((k) < r ? (r - 1 - (k)) : (k)) * S)
+#define WLD(k) ((k) < r ? ldw(B, WOFF(k)) : ldw(A, WOFF(k)))
+  dd w0 = WLD(0), w1 = WLD(min(1, K - 1));
   dd z1 = dd_from(1.0), z2 = zp1;  // z(i+1), z(i+2) for the backward branch
   dd zrm1 = dd_from(0.0);
-  for (int k = 0; k < nb - 1; k++) {
-    bool bw = k < r;
-    int i = bw ? (r - 1 - k) : k;
+  for (int k = 0; k < K; k++) {
+    int k2 = min(k + 2, K - 1);
+    dd w2 = WLD(k2);
+    const bool bw = k < r;
+    const int i = bw ? (r - 1 - k) : k;
     if (k == r) { z2 = zrm1; z1 = dd_from(1.0); }  // forward branch: z(i), z(i-1)
-    dd w = bw ? B[(long long)i * S] : A[(long long)i * S];
     dd z;
-    if (!is_mark(w)) {
-      z = dd_neg(dd_mul(w, z1));
+    if (!is_mark(w0)) {
+      z = dd_neg(dd_mul(w0, z1));
     } else {
       int in = bw ? i + 1 : i - 1;
       dd num = (bw ? (in < nb - 1) : (in >= 0)) ? ld_dl(y + in) : dd_from(0.0);
@@ -391,12 +442,15 @@ __device__ dd zsolve(const YElt *__restrict__ y, int nb, int r, const dd *A, con
       z = isfinite(v.hi) ? v : dd_from(0.0);
     }
     zz = dd_add(zz, dd_mul(z, z));
-    int row = bw ? i : i + 1;
-    if (Zc) Zc[row] = dd_mul(z, inv).hi;
+    if (Zc) Zc[bw ? i : i + 1] = dd_mul(z, inv).hi;
     if (bw && i == r - 1) zrm1 = z;
     z2 = z1;
     z1 = z;
+    w0 = w1;
+    w1 = w2;
   }
+#undef WLD
+#undef WOFF
   return zz;
 }
 
@@ -431,14 +485,17 @@ __global__ void __launch_bounds__(64) k_rqi(const Singleton *__restrict__ sg, in
   dd lam = dd_from(mid);
   double thr1 = __dmul_rn(__dmul_rn(s.gap, EPS_X), sqrt((double)nb));
   int r = -1, iters = 0;
+  long long qd = 0, qdg = 0, zs = 0;
   bool accepted = false;
   GV g;
   dd nz = dd_from(1.0);
   for (int it = 0; it < MAX_RQI && !accepted; it++) {
+    if (r < 0) { qd += 2 * (nb - 1); qdg += nb - 1; } else qd += nb - 1;
     getvec_dd(y, nb, lam, r, A, B, S, g);
     iters++;
     r = g.r;
     if (r < 0) break;
+    zs += nb - 1;
     dd zz = zsolve(y, nb, r, A, B, S, dd_from(0.0), nullptr);
     if (!isfinite(zz.hi) || zz.hi == 0.0) break;
     nz = dd_sqrt(zz);
@@ -452,6 +509,10 @@ __global__ void __launch_bounds__(64) k_rqi(const Singleton *__restrict__ sg, in
     else break;
   }
   atomicAdd((unsigned long long *)&stats[ST_RQI_ITERS], (unsigned long long)iters);
+  atomicAdd((unsigned long long *)&stats[ST_QD_STEPS], (unsigned long long)qd);
+  atomicAdd((unsigned long long *)&stats[ST_QDG_STEPS], (unsigned long long)qdg);
+  atomicAdd((unsigned long long *)&stats[ST_Z_STEPS], (unsigned long long)zs);
+  atomicAdd((unsigned long long *)&stats[ST_ZW_STEPS], (unsigned long long)(nb - 1));
   atomicAdd((unsigned long long *)&stats[ST_GETVEC], (unsigned long long)iters);
   if (!accepted) {
     atomicAdd((unsigned long long *)&stats[ST_RQI_FALLBACK], 1ull);

@@ -84,19 +84,20 @@ struct mrrr_ctx {
   int root_side = 0;
   uint32_t flags = 0;
   long long ws_limit = 0;
-  long long target_chains = 65536;
+  long long target_chains = 131072;
   int mmax = 16;
+  int chains_per_thread = 2;
 
   // buffers
   Buf starts, scal, binfo, bside, blist, cab, mx, my, lscratch, reps, rlo, rhi, colmap, gstart;
   Buf nodesA, nodesB, counts, ex, excounts, exmap, bnA, bnB, sing, clusA, clusB, ss, gval, valid, cseg, bnoff,
-      ipool_lo, ipool_hi, yref_lo, yref_hi, wsA, wsB, stats, cnt, ddepth, dgf, dgl, dflo, dfhi;
+      ipool_lo, ipool_hi, yref_lo, yref_hi, wsA, wsB, stats, cnt, ddepth, dgf, dgl, dflo, dfhi, hd, he, hW, hZ;
   int *h_cnt = nullptr;  // pinned counters
 
   // results of the last call
   long long last_n = 0, last_k = 0;
   int last_nblk = 0;
-  long long stats_h[MRRR_NSTATS] = {0};
+  long long stats_h[ST_N] = {0};
   double times[8] = {0};
   std::vector<int> h_starts;
   cudaEvent_t ev[8];
@@ -201,9 +202,55 @@ __global__ void k_rank2(const int *__restrict__ starts, int nblk, const double *
   colmap[i] = (rank >= il && rank <= iu) ? (int)(rank - il) : -1;
 }
 
+// self-test 1: div_fast/div_ieee vs __ddiv_rn on random bit patterns (wide exponent range) and specials
+__global__ void k_selftest_div(long long n, uint64_t seed, unsigned long long *bad) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t z1 = seed + (2 * i + 1) * 0x9E3779B97F4A7C15ull, z2 = seed + (2 * i + 2) * 0x9E3779B97F4A7C15ull;
+  z1 = (z1 ^ (z1 >> 30)) * 0xBF58476D1CE4E5B9ull; z1 = (z1 ^ (z1 >> 27)) * 0x94D049BB133111EBull; z1 ^= z1 >> 31;
+  z2 = (z2 ^ (z2 >> 30)) * 0xBF58476D1CE4E5B9ull; z2 = (z2 ^ (z2 >> 27)) * 0x94D049BB133111EBull; z2 ^= z2 >> 31;
+  double a, b;
+  if (i % 4 == 0) {  // raw bit patterns: every exponent, subnormals, inf, nan
+    a = __longlong_as_double((long long)z1);
+    b = __longlong_as_double((long long)z2);
+  } else {           // the NegCount regime: O(1) magnitudes with random signs and scales
+    a = ((double)(z1 >> 11) * 0x1p-53 - 0.5) * ldexp(1.0, (int)(z1 & 63) - 32);
+    b = ((double)(z2 >> 11) * 0x1p-53 - 0.5) * ldexp(1.0, (int)(z2 & 63) - 32);
+    if ((i & 255) == 1) b = 0.0;
+    if ((i & 255) == 2) a = 0.0;
+    if ((i & 255) == 3) b = -0.0;
+    if ((i & 255) == 5) { a = INFINITY; b = -INFINITY; }
+  }
+  double q1 = div_ieee(a, b), q2 = __ddiv_rn(a, b);
+  bool same = (__double_as_longlong(q1) == __double_as_longlong(q2)) || (isnan(q1) && isnan(q2));
+  if (!same) atomicAdd(bad, 1ull);
+}
+
 void launch_check(mrrr_t h) {
   h->host_launches++;
   CK(cudaGetLastError());
+}
+
+// NegCount chains: node grid points then explicit (rep, sigma) chains; CH chains per thread (x path)
+template <bool Y>
+void launch_negcount(mrrr_t h, const Node *nodes, int nnode, int m, int nex) {
+  long long tot = (long long)nnode * ((1LL << m) - 1) + nex;
+  int ch = Y ? 1 : h->chains_per_thread;
+  long long thr = (tot + ch - 1) / ch;
+  const ExplicitChain *ex = h->ex.as<ExplicitChain>();
+  const RepDesc *reps = h->reps.as<RepDesc>();
+  const double2 *mx = h->mx.as<double2>();
+  const YElt *my = h->my.as<YElt>();
+  int *cnts = h->counts.as<int>(), *exc = h->excounts.as<int>();
+  unsigned g = nblocks_for(thr, 128);
+  cudaStream_t st = h->stream;
+  switch (ch) {
+    case 1: k_negcount<Y, 1><<<g, 128, 0, st>>>(nodes, nnode, m, ex, nex, reps, mx, my, cnts, exc); break;
+    case 2: k_negcount<Y, 2><<<g, 128, 0, st>>>(nodes, nnode, m, ex, nex, reps, mx, my, cnts, exc); break;
+    case 3: k_negcount<Y, 3><<<g, 128, 0, st>>>(nodes, nnode, m, ex, nex, reps, mx, my, cnts, exc); break;
+    default: k_negcount<Y, 4><<<g, 128, 0, st>>>(nodes, nnode, m, ex, nex, reps, mx, my, cnts, exc); break;
+  }
+  launch_check(h);
 }
 
 // shared-tree / k-section bisection rounds until every node is finished (S5, S8)
@@ -220,18 +267,15 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
     CK(h->counts.ensure(std::max<long long>(nch, 1) * sizeof(int)));
     int nex = first ? nverify : 0;
     zero_counters(h);
-    k_negcount<Y><<<nblocks_for(nch + nex, 128), 128, 0, h->stream>>>(
-        cur, nnode, m, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mx.as<double2>(), h->my.as<YElt>(),
-        h->counts.as<int>(), h->excounts.as<int>());
-    launch_check(h);
+    launch_negcount<Y>(h, cur, nnode, m, nex);
     if (nex > 0) {
       k_root_verify<<<nblocks_for(nbl, 128), 128, 0, h->stream>>>(blist_dev, nbl, h->starts.as<int>(),
                                                                   h->binfo.as<double>(), h->excounts.as<int>(),
                                                                   h->cnt.as<int>() + C_NEX);
       launch_check(h);
     }
-    k_bisect_update<<<nblocks_for(nnode, 128), 128, 0, h->stream>>>(cur, nnode, m, h->counts.as<int>(), nxt,
-                                                                    h->cnt.as<int>() + C_NNEXT, out_lo, out_hi, rtol);
+    k_bisect_update<<<nblocks_for((long long)nnode << m, 128), 128, 0, h->stream>>>(
+        cur, nnode, m, h->counts.as<int>(), nxt, h->cnt.as<int>() + C_NNEXT, out_lo, out_hi, rtol);
     launch_check(h);
     read_counters(h);
     h->host_rounds++;
@@ -259,10 +303,7 @@ int run_brackets(mrrr_t h, int nbn) {
     read_counters(h);
     int nex = h->h_cnt[C_NEX];
     if (nex > 0) {
-      k_negcount<Y><<<nblocks_for(nex, 128), 128, 0, h->stream>>>(
-          nullptr, 0, 1, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mx.as<double2>(),
-          h->my.as<YElt>(), h->counts.as<int>(), h->excounts.as<int>());
-      launch_check(h);
+      launch_negcount<Y>(h, nullptr, 0, 1, nex);
       k_bracket_scatter<<<nblocks_for(nex, 128), 128, 0, h->stream>>>(cur, h->exmap.as<int>(), h->excounts.as<int>(),
                                                                       nex);
       launch_check(h);
@@ -740,6 +781,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     h->ws_limit = (o && o->ws_limit > 0) ? o->ws_limit : (long long)(0.6 * (double)fr);
     if (const char *s = getenv("MRRR_TARGET_CHAINS")) h->target_chains = atoll(s);
     if (const char *s = getenv("MRRR_MMAX")) h->mmax = atoi(s);
+    if (const char *s = getenv("MRRR_CH")) h->chains_per_thread = std::max(1, std::min(4, atoi(s)));
     for (auto &ev : h->ev) CK(cudaEventCreate(&ev));
     CK(cudaEventCreate(&h->rq0));
     CK(cudaEventCreate(&h->rq1));
@@ -793,10 +835,12 @@ int mrrr_eig_host(mrrr_t h, const double *d, const double *e, int64_t n, int64_t
   int rc = 0;
   try {
     CK(cudaSetDevice(h->device));
-    CK(cudaMalloc(&dd_, sizeof(double) * n));
-    CK(cudaMalloc(&de, sizeof(double) * std::max<long long>(n - 1, 1)));
-    CK(cudaMalloc(&dW, sizeof(double) * k));
-    CK(cudaMalloc(&dZ, sizeof(double) * n * k));
+    // device staging buffers are cached in the handle (grown on demand)
+    CK(h->hd.ensure(sizeof(double) * n));
+    CK(h->he.ensure(sizeof(double) * std::max<long long>(n - 1, 1)));
+    CK(h->hW.ensure(sizeof(double) * k));
+    CK(h->hZ.ensure(sizeof(double) * n * k));
+    dd_ = h->hd.as<double>(); de = h->he.as<double>(); dW = h->hW.as<double>(); dZ = h->hZ.as<double>();
     CK(cudaMemcpyAsync(dd_, d, sizeof(double) * n, cudaMemcpyHostToDevice, h->stream));
     if (n > 1) CK(cudaMemcpyAsync(de, e, sizeof(double) * (n - 1), cudaMemcpyHostToDevice, h->stream));
     rc = solve(h, dd_, de, n, il, iu, dW, dZ, n, 0, 0, nullptr, nullptr, 0);
@@ -810,7 +854,6 @@ int mrrr_eig_host(mrrr_t h, const double *d, const double *e, int64_t n, int64_t
   } catch (Err &er) {
     rc = er.code;
   }
-  cudaFree(dd_); cudaFree(de); cudaFree(dW); cudaFree(dZ);
   return rc;
 }
 
@@ -863,6 +906,24 @@ int mrrr_get_diag(mrrr_t h, mrrr_diag *g) {
   return 0;
 }
 
+int mrrr_selftest(int which, int64_t n, uint64_t seed, int64_t *bad) {
+  if (!bad || n < 0) return -1;
+  if (which != 1) return -1;
+  try {
+    unsigned long long *d = nullptr, hb = 0;
+    CK(cudaMalloc(&d, sizeof(*d)));
+    CK(cudaMemset(d, 0, sizeof(*d)));
+    k_selftest_div<<<nblocks_for(n, 256), 256>>>(n, seed, d);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(&hb, d, sizeof(hb), cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    *bad = (int64_t)hb;
+  } catch (Err &er) {
+    return er.code;
+  }
+  return 0;
+}
+
 const char *mrrr_strerror(int code) {
   switch (code) {
     case MRRR_OK: return "success";
@@ -883,7 +944,8 @@ int mrrr_destroy(mrrr_t h) {
                  &h->reps, &h->rlo, &h->rhi, &h->colmap, &h->gstart, &h->nodesA, &h->nodesB, &h->counts, &h->ex,
                  &h->excounts, &h->exmap, &h->bnA, &h->bnB, &h->sing, &h->clusA, &h->clusB, &h->ss, &h->gval,
                  &h->valid, &h->cseg, &h->bnoff, &h->ipool_lo, &h->ipool_hi, &h->yref_lo, &h->yref_hi, &h->wsA,
-                 &h->wsB, &h->stats, &h->cnt, &h->ddepth, &h->dgf, &h->dgl, &h->dflo, &h->dfhi};
+                 &h->wsB, &h->stats, &h->cnt, &h->ddepth, &h->dgf, &h->dgl, &h->dflo, &h->dfhi,
+                 &h->hd, &h->he, &h->hW, &h->hZ};
   for (Buf *b : bufs) b->release();
   for (auto &ev : h->ev) cudaEventDestroy(ev);
   cudaEventDestroy(h->rq0);

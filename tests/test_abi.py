@@ -1,0 +1,68 @@
+"""CPU-side checks of the product boundary: libmrrr.so builds for sm_100a, loads, exports every symbol
+include/mrrr.h declares, and refuses to run without a GPU (no CPU fallback)."""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib_path():
+    from paper_1401_4950_b200 import _build
+    return _build.build()
+
+
+def declared_functions():
+    txt = open(os.path.join(ROOT, "include", "mrrr.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(mrrr_\w+)\s*\(", txt, re.M)))
+
+
+def test_header_declares_the_abi():
+    fns = declared_functions()
+    for f in ("mrrr_init", "mrrr_eig", "mrrr_destroy", "mrrr_eig_host", "mrrr_eig_shard", "mrrr_get_stats",
+              "mrrr_get_diag", "mrrr_get_times", "mrrr_strerror"):
+        assert f in fns
+
+
+def test_library_exports_every_declared_symbol(lib_path):
+    out = subprocess.run(["nm", "-D", "--defined-only", lib_path], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\sT\s(\w+)", out))
+    missing = [f for f in declared_functions() if f not in exported]
+    assert not missing, missing
+    import paper_1401_4950_b200 as m
+    L = m.load()
+    for f in declared_functions():
+        assert hasattr(L, f)
+
+
+def test_library_is_sm100a_code(lib_path):
+    out = subprocess.run(["cuobjdump", "--list-elf", lib_path], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_strerror_and_no_cpu_fallback(lib_path):
+    import torch
+    import paper_1401_4950_b200 as m
+    L = m.load()
+    assert L.mrrr_strerror(0) == b"success"
+    assert b"NaN" in L.mrrr_strerror(1)
+    if not torch.cuda.is_available():
+        with pytest.raises(m.MrrrError):
+            m.Solver()
+
+
+def test_oracle_and_product_share_no_code():
+    prod = os.path.join(ROOT, "paper_1401_4950_b200")
+    for dirpath, _, files in os.walk(prod):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "oracle/" not in txt.replace("oracle/ is", ""), f
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith((".py", ".c", ".h")):
+            txt = open(os.path.join(ROOT, "oracle", f)).read()
+            assert "paper_1401_4950_b200" not in txt.replace("paper_1401_4950_b200/ (the product)", "") \
+                .replace("``paper_1401_4950_b200`` never", ""), f

@@ -87,6 +87,7 @@ struct mrrr_ctx {
   long long target_chains = 131072;
   int mmax = 16;
   int chains_per_thread = 2;
+  bool rqi_pair = true;
 
   // buffers
   Buf starts, scal, binfo, bside, blist, cab, mx, my, lscratch, reps, rlo, rhi, colmap, gstart;
@@ -324,20 +325,34 @@ int run_brackets(mrrr_t h, int nbn) {
 
 void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long ldz) {
   if (ns <= 0) return;
-  long long per = 32LL * std::max<long long>(nbmax, 1);
-  long long budget = std::min<long long>(h->ws_limit / 2, 48LL << 30);
-  long long bmax = std::max<long long>(1, budget / per);
+  const bool pair = h->rqi_pair;
+  // workspace per singleton: pair kernel 6 dd planes, single-lane kernel 2
+  long long per = (pair ? 6LL : 2LL) * (long long)sizeof(dd) * std::max<long long>(nbmax, 1);
+  long long budget = std::min<long long>(h->ws_limit / 2, 64LL << 30);
+  long long bmax = std::max<long long>(32, budget / per);
   long long batch = std::min<long long>(ns, bmax);
-  CK(h->wsA.ensure((size_t)batch * nbmax * sizeof(dd)));
-  CK(h->wsB.ensure((size_t)batch * nbmax * sizeof(dd)));
+  long long stride = (batch + 31) / 32 * 32;  // pairs launched per batch (grid padding)
+  if (pair) {
+    CK(h->wsA.ensure((size_t)6 * stride * nbmax * sizeof(dd)));
+  } else {
+    CK(h->wsA.ensure((size_t)stride * nbmax * sizeof(dd)));
+    CK(h->wsB.ensure((size_t)stride * nbmax * sizeof(dd)));
+  }
   bool diag = (h->flags & MRRR_KEEP_DIAG) != 0;
   for (long long b0 = 0; b0 < ns; b0 += batch) {
     long long nb = std::min<long long>(batch, ns - b0);
     CK(cudaEventRecord(h->rq0, h->stream));
-    k_rqi<<<nblocks_for(nb, 64), 64, 0, h->stream>>>(
-        h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>(),
-        h->wsB.as<dd>(), nb, W, Z, ldz, diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
-        diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>());
+    if (pair) {
+      k_rqi2<<<nblocks_for(2 * nb, 64), 64, 0, h->stream>>>(
+          h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>(), stride,
+          nbmax, W, Z, ldz, diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
+          diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>());
+    } else {
+      k_rqi<<<nblocks_for(nb, 64), 64, 0, h->stream>>>(
+          h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>(),
+          h->wsB.as<dd>(), stride, W, Z, ldz, diag ? h->ddepth.as<int>() : nullptr,
+          diag ? h->dflo.as<double>() : nullptr, diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>());
+    }
     launch_check(h);
     CK(cudaEventRecord(h->rq1, h->stream));
     CK(cudaEventSynchronize(h->rq1));
@@ -782,6 +797,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_TARGET_CHAINS")) h->target_chains = atoll(s);
     if (const char *s = getenv("MRRR_MMAX")) h->mmax = atoi(s);
     if (const char *s = getenv("MRRR_CH")) h->chains_per_thread = std::max(1, std::min(4, atoi(s)));
+    if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;
     for (auto &ev : h->ev) CK(cudaEventCreate(&ev));
     CK(cudaEventCreate(&h->rq0));
     CK(cudaEventCreate(&h->rq1));

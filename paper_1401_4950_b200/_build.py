@@ -5,7 +5,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "mrrr.cu")
-DEPS = [os.path.join(HERE, "csrc", f) for f in ("mrrr.cu", "kernels.cuh", "kernels_vec.cuh", "dd.cuh")] + \
+DEPS = [os.path.join(HERE, "csrc", f) for f in ("mrrr.cu", "kernels.cuh", "kernels_vec.cuh", "kernels_rqi.cuh", "dd.cuh")] + \
     [os.path.join(ROOT, "include", "mrrr.h")]
 LIB = os.path.join(HERE, "libmrrr.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

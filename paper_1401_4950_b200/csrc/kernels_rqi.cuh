@@ -1,0 +1,347 @@
+// kernels_rqi.cuh -- singleton RQI + eigenvector kernel (S9/S10: Alg. Getvec, Alg. stask
+// P:4026-4074, mixed stopping rule P:6074-6108, convert-on-write P:6156-6158), two lanes per singleton.
+//
+// Lane F (even) runs the dstqds recurrence forward (i = 0, 1, ...), lane B (odd) the dqds recurrence
+// backward (i = n-2, n-3, ...), in lock step.  The twist quantities gamma_k = s(k) + d(k) p(k+1) /
+// omega(k+1) and the norms ||z_k||^2 = 1 + S_k + T_k of the twisted solves, with
+//     S_{k+1} = l+(k)^2 (1 + S_k)   (sum of z(i)^2, i < k),   T_k = u-(k)^2 (1 + T_{k+1})   (i > k),
+// are formed on the fly: for the lower half of k lane B combines its own t(k), T_k with the s(k), S_k
+// that lane F wrote earlier in the same pass, for the upper half lane F combines with what B wrote
+// (they meet in the middle, where one shuffle exchanges the values).  So iteration 1 is one pass of
+// n steps per lane and no separate argmin or z pass is needed inside the RQI.  Later iterations (twist
+// r fixed) run F on 0..r-1 and B on n-2..r and store l+ / u- for the final z solve.
+//
+// Workspace: three dd planes [i * S + pair]: P0 = s(i) / t(i), P1 = S_i / T_i (iteration 1, each
+// index written by exactly one lane), P2 = l+(i) for i < r and u-(i) for i >= r.
+//
+// The hot loops use the branch-free dd operations (dd_*_nf); if a lane's recurrence leaves the finite
+// range (a zero pivot: IEEE infinity) the pass is rerun with the careful operations,
+// the infinity guard q := 1 and zero-pivot marks for the substitution formulas of Getvec.
+#pragma once
+#include "kernels_vec.cuh"
+
+__device__ __forceinline__ unsigned pair_mask() { return 3u << ((threadIdx.x & 31) & ~1u); }
+__device__ __forceinline__ int lane_F() { return (threadIdx.x & 31) & ~1; }
+__device__ __forceinline__ int lane_B() { return (threadIdx.x & 31) | 1; }
+__device__ __forceinline__ dd shfl_dd(dd v, int src_xor) {
+  unsigned m = pair_mask();
+  return dd_make(__shfl_xor_sync(m, v.hi, src_xor), __shfl_xor_sync(m, v.lo, src_xor));
+}
+__device__ __forceinline__ dd shfl_dd_from(dd v, int lane) {
+  unsigned m = pair_mask();
+  return dd_make(__shfl_sync(m, v.hi, lane), __shfl_sync(m, v.lo, lane));
+}
+__device__ __forceinline__ int shfl_i_from(int v, int lane) { return __shfl_sync(pair_mask(), v, lane); }
+
+template <bool C> __device__ __forceinline__ dd OADD(dd a, dd b) { if constexpr (C) return dd_add(a, b); else return dd_add_nf(a, b); }
+template <bool C> __device__ __forceinline__ dd OSUB(dd a, dd b) { if constexpr (C) return dd_sub(a, b); else return dd_sub_nf(a, b); }
+template <bool C> __device__ __forceinline__ dd OMUL(dd a, dd b) { if constexpr (C) return dd_mul(a, b); else return dd_mul_nf(a, b); }
+template <bool C> __device__ __forceinline__ dd ORCP(dd a) { if constexpr (C) return dd_rcp(a); else return dd_rcp_nf(a); }
+template <bool C> __device__ __forceinline__ dd OADD1(dd a) { if constexpr (C) return dd_add_d(a, 1.0); else return dd_add_d_nf(a, 1.0); }
+
+struct Elt3 {
+  double2 a, b, c;
+};
+// element i of the representation with lane-dependent operand order (F: a = d, c = dll; B: a = dll, c = d)
+__device__ __forceinline__ Elt3 ld3(const YElt *__restrict__ y, int i, int oa, int oc) {
+  const double2 *q = reinterpret_cast<const double2 *>(y + i);
+  Elt3 e;
+  e.a = __ldg(q + oa);
+  e.b = __ldg(q + 1);
+  e.c = __ldg(q + oc);
+  return e;
+}
+__device__ __forceinline__ dd D2(double2 v) { return dd_make(v.x, v.y); }
+
+struct Cand {  // twist candidate of one lane: |gamma|, gamma, k, ||z_k||^2 - 1
+  dd best, gam, st;
+  int k;
+};
+__device__ __forceinline__ void cand_take(Cand &c, dd g, dd st, int k, bool tie_wins) {
+  if (isnan(g.hi)) return;
+  dd a = dd_abs(g);
+  bool take = (c.k < 0) || dd_lt(a, c.best) || (tie_wins && !dd_lt(c.best, a));
+  if (take) { c.best = a; c.gam = g; c.st = st; c.k = k; }
+}
+
+// One Getvec of the pair at shift lam.  r < 0: full twisted factorization and twist
+// search (iteration 1, no l+/u- stored); r >= 0: the r-twisted factorization, storing l+/u- in P2.
+// Returns false (both lanes) if the fast pass left the finite range.  On return (both lanes):
+// g.r, g.gamma = gamma_r, g.zz = ||z||^2 (NaN/inf if the closed form broke down), g.c = inertia (A-26).
+template <bool C>
+__device__ bool getvec_pair_t(const YElt *__restrict__ y, int nb, dd lam, int r, bool isB, dd *P0, dd *P1, dd *P2,
+                              long long S, GV &g) {
+  const unsigned pm = pair_mask();
+  const int last = nb - 1;
+  const bool it1 = r < 0;
+  const int nsteps = it1 ? last : (isB ? last - r : r);
+  const int oa = isB ? 2 : 0, oc = isB ? 0 : 2;
+  dd x = isB ? OSUB<C>(ldy(y, last).d, lam) : dd_neg(lam);  // F: s(0); B: p(n-1)
+  dd acc = dd_from(0.0), tr = dd_from(0.0);
+  int cnt = 0;
+  Cand cd;
+  cd.k = -1; cd.best = dd_from(INFINITY); cd.gam = dd_from(0.0); cd.st = dd_from(0.0);
+#define GIX(k) (isB ? (last - 1 - (k)) : (k))
+  // iteration 1: the other lane's half of gamma_k for step k (rows with 2k > n-2) was written at its
+  // step n-2-k; it is prefetched PD steps ahead when already visible (2 t >= n-1-PD at issue step t)
+  constexpr int PD = 4;
+  dd pq[PD], ps[PD];
+  bool pv[PD];
+#pragma unroll
+  for (int u = 0; u < PD; u++) { pv[u] = false; pq[u] = ps[u] = dd_from(0.0); }
+  if (nsteps > 0) {
+    Elt3 e0 = ld3(y, GIX(0), oa, oc), e1 = ld3(y, GIX(min(1, nsteps - 1)), oa, oc);
+    for (int k0 = 0; k0 < nsteps; k0 += PD) {
+#pragma unroll
+      for (int u = 0; u < PD; u++) {
+        const int k = k0 + u;
+        if (k < nsteps) {
+          Elt3 e2 = ld3(y, GIX(min(k + 2, nsteps - 1)), oa, oc);
+          const int i = GIX(k);
+          const long long off = (long long)i * S;
+          const dd a = D2(e0.a), b = D2(e0.b), c = D2(e0.c);
+          dd den = OADD<C>(x, a);
+          dd rr = ORCP<C>(den);
+          dd q = OMUL<C>(x, rr);
+          if constexpr (C) q = (dd_isinf(x) && dd_isinf(den)) ? dd_from(1.0) : q;
+          dd out = OMUL<C>(b, rr);
+          dd xn = OSUB<C>(OMUL<C>(q, c), lam);
+          dd accn = OMUL<C>(OMUL<C>(out, out), OADD1<C>(acc));
+          if (it1) {
+            // F: (s(i), S_i) before the update; B: t(i) = d(i) p(i+1) / omega(i+1) and T_i after it
+            dd mine = isB ? OMUL<C>(OMUL<C>(c, rr), x) : x;
+            dd myst = isB ? accn : acc;
+            if (2 * k == last - 1) {  // lanes meet at the same index: exchange in registers
+              dd om = shfl_dd(mine, 1), ost = shfl_dd(myst, 1);
+              if (!isB) cand_take(cd, OADD<C>(mine, om), OADD<C>(myst, ost), i, false);
+            } else if (2 * k < last - 1) {
+              // the other lane reaches row i later: leave my half of gamma_i for it
+              stw(P0, off, mine);
+              stw(P1, off, myst);
+            } else {
+              // the other lane wrote its half of gamma_i at an earlier step
+              dd other = pv[u] ? pq[u] : ldw(P0, off);
+              dd ost = pv[u] ? ps[u] : ldw(P1, off);
+              cand_take(cd, OADD<C>(mine, other), OADD<C>(myst, ost), i, isB);
+            }
+            const int kp = k + PD;
+            pv[u] = false;
+            if (kp < nsteps && 2 * kp > last - 1) {
+              const long long offp = (long long)GIX(kp) * S;
+              pq[u] = ldw(P0, offp);
+              ps[u] = ldw(P1, offp);
+              pv[u] = 2 * k >= last - PD;
+            }
+            __syncwarp(pm);
+          } else {
+            if (isB && i == r) tr = OMUL<C>(OMUL<C>(c, rr), x);
+            if constexpr (C) stw(P2, i, (den.hi == 0.0) ? dd_mark() : out);
+            else stw(P2, i, out);
+          }
+          cnt += dd_sb(den);
+          x = xn;
+          acc = accn;
+          e0 = e1;
+          e1 = e2;
+        }
+      }
+    }
+  }
+#undef GIX
+  if constexpr (!C) {
+    bool ok = isfinite(x.hi) && isfinite(x.lo);
+    ok = __shfl_xor_sync(pm, (int)ok, 1) && ok;
+    if (!ok) return false;
+  }
+  __syncwarp(pm);
+  if (it1) {
+    // F: x = s(n-1), acc = S_{n-1}; gamma_n = d+(n) closes the full NegCount
+    if (!isB) {
+      dd glast = OADD<C>(x, ldy(y, last).d);
+      cnt += dd_sb(glast);
+      cand_take(cd, glast, acc, last, false);
+    }
+    dd ob = shfl_dd(cd.best, 1), og = shfl_dd(cd.gam, 1), ost = shfl_dd(cd.st, 1);
+    int ok_ = __shfl_xor_sync(pm, cd.k, 1);
+    if (!isB) {  // B's candidates are the lower indices: they win ties
+      if (ok_ >= 0 && (cd.k < 0 || !dd_lt(cd.best, ob))) { cd.best = ob; cd.gam = og; cd.st = ost; cd.k = ok_; }
+    }
+    g.r = shfl_i_from(cd.k, lane_F());
+    g.gamma = shfl_dd_from(cd.gam, lane_F());
+    g.zz = dd_add_d(shfl_dd_from(cd.st, lane_F()), 1.0);
+    g.c = shfl_i_from(cnt, lane_F());
+  } else {
+    dd sr = shfl_dd_from(x, lane_F());
+    dd t_r = shfl_dd_from(tr, lane_B());
+    int cF = shfl_i_from(cnt, lane_F());
+    int cB = shfl_i_from(cnt, lane_B());
+    dd gamma = (r == last) ? dd_add(sr, ldy(y, last).d) : dd_add(sr, t_r);
+    g.r = r;
+    g.gamma = gamma;
+    g.c = cF + cB + dd_sb(gamma);
+    dd other = shfl_dd(acc, 1);
+    g.zz = dd_add_d(dd_add(acc, other), 1.0);
+  }
+  return true;
+}
+
+// returns true if the careful (IEEE special value) pass had to run
+__device__ __forceinline__ bool getvec_pair_any(const YElt *__restrict__ y, int nb, dd lam, int r, bool isB, dd *P0,
+                                                dd *P1, dd *P2, long long S, GV &g) {
+  if (getvec_pair_t<false>(y, nb, lam, r, isB, P0, P1, P2, S, g)) return false;
+  getvec_pair_t<true>(y, nb, lam, r, isB, P0, P1, P2, S, g);
+  return true;
+}
+
+// per-singleton hand-off from k_rqi2 to k_zwrite
+struct ZMeta {
+  double inv_hi, inv_lo;  // 1 / ||z||
+  int r, careful;         // twist index; 1 if the last Getvec ran the careful pass (zero-pivot marks in P2)
+};
+
+// S10 output: z(r) = 1, z(i) = -l+(i) z(i+1) (i < r), z(i+1) = -u-(i) z(i) (i >= r), written as
+// fl64(z / ||z||) into column col of Z.  One warp per singleton: the two products are computed tile by
+// tile (32 rows) as warp prefix products of dd factors, times the carry of the previous tile, so the
+// P2 reads and the Z column stores are coalesced.  (Rounding order differs from the sequential
+// recurrence only at the dd level.)  Careful passes (zero pivots, A-25 substitutions) use lane 0 and
+// the sequential zsolve.
+__device__ __forceinline__ dd shfl_up_dd(dd v, int off) {
+  return dd_make(__shfl_up_sync(0xffffffffu, v.hi, off), __shfl_up_sync(0xffffffffu, v.lo, off));
+}
+__device__ __forceinline__ dd shfl_idx_dd(dd v, int lane) {
+  return dd_make(__shfl_sync(0xffffffffu, v.hi, lane), __shfl_sync(0xffffffffu, v.lo, lane));
+}
+
+__global__ void __launch_bounds__(256) k_zwrite(const Singleton *__restrict__ sg, int ns,
+                                                const RepDesc *__restrict__ reps, const YElt *__restrict__ my,
+                                                const dd *__restrict__ P2base, long long nbmax,
+                                                const ZMeta *__restrict__ zm, double *Z, long long ldz) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= ns) return;
+  const ZMeta m = zm[w];
+  const Singleton s = sg[w];
+  const RepDesc R = reps[s.rep];
+  const int nb = R.nb, r = m.r, last = nb - 1;
+  const dd inv = dd_make(m.inv_hi, m.inv_lo);
+  const dd *P = P2base + (long long)w * nbmax;
+  double *Zc = Z + (long long)s.col * ldz + R.bstart;
+  if (m.careful) {
+    if (lane == 0) zsolve(my + R.off, nb, r, P, P, 1, inv, Zc);
+    return;
+  }
+  if (lane == 0) Zc[r] = inv.hi;
+  // rows r-1 .. 0 (factors -l+(r-1-m)) then rows r+1 .. n-1 (factors -u-(r+m))
+  for (int side = 0; side < 2; side++) {
+    const int len = side ? last - r : r;
+    dd carry = dd_from(1.0);
+    for (int m0 = 0; m0 < len; m0 += 32) {
+      const int mm = m0 + lane;
+      const bool valid = mm < len;
+      const int src = side ? (r + mm) : (r - 1 - mm);
+      dd v = valid ? dd_neg(ldw(P, src)) : dd_from(1.0);
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        dd o = shfl_up_dd(v, off);
+        if (lane >= off) v = dd_mul_nf(o, v);
+      }
+      dd z = dd_mul_nf(carry, v);
+      if (valid) Zc[side ? (r + 1 + mm) : (r - 1 - mm)] = dd_mul_nf(z, inv).hi;
+      carry = shfl_idx_dd(z, 31);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
+                                             const YElt *__restrict__ my, dd *ws, long long S, long long nbmax,
+                                             double *W, ZMeta *zmeta, int *diag_depth, double *fin_lo,
+                                             double *fin_hi, long long *stats) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool isB = gt & 1;
+  const int pid = gt >> 1;  // workspace column (padded grid: S >= #pairs launched)
+  const bool active = pid < ns;
+  const Singleton s = sg[active ? pid : ns - 1];  // idle pairs shadow the last singleton in their own columns
+  const RepDesc R = reps[s.rep];
+  const int nb = R.nb, j = s.j;
+  const YElt *y = my + R.off;
+  const long long plane = nbmax * S;
+  dd *P0 = ws + pid, *P1 = ws + plane + pid, *P2 = ws + 2 * plane + (long long)pid * nbmax;
+  double mid = bis_mid(s.lo, s.hi);
+  double nu = __dmul_rn(__dmul_rn(100.0, (double)nb), EPS_X);
+  dd blo = dd_from(__dsub_rn(s.lo, __dmul_rn(nu, fabs(s.lo))));
+  dd bhi = dd_from(__dadd_rn(s.hi, __dmul_rn(nu, fabs(s.hi))));
+  dd lam = dd_from(mid);
+  double thr1 = __dmul_rn(__dmul_rn(s.gap, EPS_X), sqrt((double)nb));
+  int r = -1, iters = 0;
+  long long qd = 0, qdg = 0, zs = 0;
+  bool accepted = false, lu_valid = false, careful = false;
+  GV g;
+  dd zz = dd_from(1.0);
+  for (int it = 0; it < MAX_RQI && !accepted; it++) {
+    if (r < 0) { qd += 2 * (nb - 1); qdg += nb - 1; } else qd += nb - 1;
+    lu_valid = r >= 0;
+    careful = getvec_pair_any(y, nb, lam, r, isB, P0, P1, P2, S, g);
+    iters++;
+    r = g.r;
+    if (r < 0) break;
+    zz = g.zz;
+    if (!isfinite(zz.hi)) {  // closed form broke down (overflow / zero pivot): explicit z solve (A-25)
+      if (!lu_valid) { careful = getvec_pair_any(y, nb, lam, r, isB, P0, P1, P2, S, g); lu_valid = true; qd += nb - 1; }
+      zs += nb - 1;
+      if (!isB) zz = zsolve(y, nb, r, P2, P2, 1, dd_from(0.0), nullptr);
+      zz = shfl_dd_from(zz, lane_F());
+    }
+    if (!isfinite(zz.hi) || zz.hi == 0.0) break;
+    dd nz = dd_sqrt(zz);
+    dd resid = dd_div(dd_abs(g.gamma), nz);
+    dd rqc = dd_div(g.gamma, zz);
+    if (resid.hi <= thr1 || dd_lt(dd_abs(rqc), dd_mul_d(dd_abs(lam), 4.0 * EPS_Y))) { accepted = true; break; }
+    if (g.c < j) blo = lam; else bhi = lam;
+    dd nl = dd_add(lam, rqc);
+    bool ok = ((g.c < j) ? (rqc.hi > 0.0) : (rqc.hi < 0.0)) && dd_lt(blo, nl) && dd_lt(nl, bhi);
+    if (ok) lam = nl;
+    else break;
+  }
+  if (!accepted) {
+    if (active && !isB) atomicAdd((unsigned long long *)&stats[ST_RQI_FALLBACK], 1ull);
+    lam = bisect_y_full(y, nb, j, blo, bhi);
+    lu_valid = r >= 0;
+    careful = getvec_pair_any(y, nb, lam, r, isB, P0, P1, P2, S, g);
+    if (r < 0) qdg += nb - 1;
+    qd += (r < 0) ? 2 * (nb - 1) : nb - 1;
+    iters++;
+    r = g.r < 0 ? 0 : g.r;
+    zz = g.zz;
+  }
+  if (!lu_valid) {  // accepted on a twist-search pass: one r-twisted pass to store l+ / u-
+    careful = getvec_pair_any(y, nb, lam, r, isB, P0, P1, P2, S, g);
+    qd += nb - 1;
+  }
+  if (!isfinite(zz.hi) || zz.hi == 0.0) {
+    zs += nb - 1;
+    if (!isB) zz = zsolve(y, nb, r, P2, P2, 1, dd_from(0.0), nullptr);
+    zz = shfl_dd_from(zz, lane_F());
+  }
+  dd inv = dd_rcp(dd_sqrt(zz));
+  if (active) {
+    if (!isB) {
+      ZMeta zmv;
+      zmv.inv_hi = inv.hi; zmv.inv_lo = inv.lo; zmv.r = r; zmv.careful = careful ? 1 : 0;
+      zmeta[pid] = zmv;
+      dd sig = dd_make(R.sig_hi, R.sig_lo);
+      W[s.col] = dd_add(lam, sig).hi;
+      if (diag_depth) {
+        diag_depth[s.col] = R.depth;
+        fin_lo[s.col] = s.lo;
+        fin_hi[s.col] = s.hi;
+      }
+      atomicAdd((unsigned long long *)&stats[ST_RQI_ITERS], (unsigned long long)iters);
+      atomicAdd((unsigned long long *)&stats[ST_QD_STEPS], (unsigned long long)qd);
+      atomicAdd((unsigned long long *)&stats[ST_QDG_STEPS], (unsigned long long)qdg);
+      atomicAdd((unsigned long long *)&stats[ST_Z_STEPS], (unsigned long long)zs);
+      atomicAdd((unsigned long long *)&stats[ST_ZW_STEPS], (unsigned long long)(nb - 1));
+      atomicAdd((unsigned long long *)&stats[ST_GETVEC], (unsigned long long)iters);
+      atomicMax((unsigned long long *)&stats[ST_DMAX], (unsigned long long)R.depth);
+    }
+  }
+}

@@ -536,390 +536,6 @@ __global__ void __launch_bounds__(64) k_rqi(const Singleton *__restrict__ sg, in
   atomicMax((unsigned long long *)&stats[ST_DMAX], (unsigned long long)R.depth);
 }
 
-// ---------------------------------------------------------------------------
-// S9/S10, two lanes per singleton (adjacent lanes of a warp): lane F runs the
-// dstqds recurrence forward (i = 0, 1, ...), lane B the dqds recurrence
-// backward (i = n-2, n-3, ...), concurrently.  ||z||^2 of the twisted solve
-// comes from the recurrences S_{k+1} = l+(k)^2 (1 + S_k) (sum of z(i)^2, i < k)
-// and T_k = u-(k)^2 (1 + T_{k+1}) (sum of z(i)^2, i > k): ||z||^2 = 1 + S_r + T_r,
-// so no z pass is needed inside the RQI (zero pivots fall back to the explicit
-// z solve).  Workspace (dd, [i * S + pair]): Ws = s(i), Wt = d(i) p(i+1) /
-// omega(i+1), WS = S_i, WT = T_i (iteration 1 only), WL = l+(i), WU = u-(i).
-// ---------------------------------------------------------------------------
-struct PairWS {
-  dd *s, *t, *S, *T, *L, *U;
-};
-
-// the two lanes of a pair always take identical control paths; shuffles use the pair mask only
-__device__ __forceinline__ unsigned pair_mask() { return 3u << ((threadIdx.x & 31) & ~1u); }
-__device__ __forceinline__ int lane_F() { return (threadIdx.x & 31) & ~1; }
-__device__ __forceinline__ int lane_B() { return (threadIdx.x & 31) | 1; }
-__device__ __forceinline__ dd shfl_dd(dd v, int src_xor) {
-  unsigned m = pair_mask();
-  return dd_make(__shfl_xor_sync(m, v.hi, src_xor), __shfl_xor_sync(m, v.lo, src_xor));
-}
-__device__ __forceinline__ dd shfl_dd_from(dd v, int lane) {
-  unsigned m = pair_mask();
-  return dd_make(__shfl_sync(m, v.hi, lane), __shfl_sync(m, v.lo, lane));
-}
-__device__ __forceinline__ int shfl_i_from(int v, int lane) { return __shfl_sync(pair_mask(), v, lane); }
-
-// returns (identically in both lanes) gamma_r, ||z||^2 (or NaN if a zero pivot broke the recurrences),
-// the twist r and the inertia count c (A-26)
-__device__ void getvec_pair(const YElt *__restrict__ y, int nb, dd lam, int r, bool isB, const PairWS &w,
-                            long long S, GV &g) {
-  const int last = nb - 1;
-  const int nsteps = (r < 0) ? last : (isB ? last - r : r);
-  dd x = isB ? dd_sub(ldy(y, last).d, lam) : dd_neg(lam);  // F: s(0); B: p(n-1)
-  dd acc = dd_from(0.0);                                   // F: S_i; B: T_{i+1}
-  dd tr = dd_from(0.0);                                    // B: t(r)
-  int cnt = 0;
-#define PIX(k) (isB ? (last - 1 - (k)) : (k))
-  if (nsteps > 0) {
-    YV c0 = ldy(y, PIX(0)), c1 = ldy(y, PIX(min(1, nsteps - 1)));
-    for (int k = 0; k < nsteps; k++) {
-      YV c2 = ldy(y, PIX(min(k + 2, nsteps - 1)));
-      const int i = PIX(k);
-      const long long off = (long long)i * S;
-      dd den, rr, out, xn;
-      qd_step(x, isB ? c0.dll : c0.d, c0.dl, isB ? c0.d : c0.dll, lam, den, rr, out, xn);
-      dd o2 = dd_mul(out, out);
-      if (!isB) {
-        if (r < 0) { stw(w.s, off, x); stw(w.S, off, acc); }
-        stw(w.L, off, (den.hi == 0.0) ? dd_mark() : out);
-        acc = dd_mul(o2, dd_add_d(acc, 1.0));
-      } else {
-        if (r < 0 || i == r) {
-          dd t = dd_mul(dd_mul(c0.d, rr), x);
-          if (r < 0) stw(w.t, off, t);
-          else tr = t;
-        }
-        stw(w.U, off, (den.hi == 0.0) ? dd_mark() : out);
-        acc = dd_mul(o2, dd_add_d(acc, 1.0));
-        if (r < 0) stw(w.T, off, acc);
-      }
-      cnt += dd_sb(den);
-      x = xn;
-      c0 = c1;
-      c1 = c2;
-    }
-  }
-#undef PIX
-  __syncwarp(pair_mask());
-  if (r < 0) {
-    // F: x = s(n-1), acc = S_{n-1}, cnt = NegCount(LDL^T - lam I) (full D+) once d+(n-1) is added
-    dd glast = isB ? dd_from(0.0) : dd_add(x, ldy(y, last).d);
-    if (!isB) cnt += dd_sb(glast);
-    // argmin over non-NaN |gamma_k|, ties to the smallest k: F scans [0, h), B scans [h, last)
-    const int h = last / 2;
-    int k0 = isB ? h : 0, k1 = isB ? last : h;
-    int kb = -1;
-    dd best = dd_from(INFINITY), gb = dd_from(0.0);
-    for (int k = k0; k < k1; k++) {
-      dd gk = dd_add(ldw(w.s, (long long)k * S), ldw(w.t, (long long)k * S));
-      if (isnan(gk.hi)) continue;
-      dd ag = dd_abs(gk);
-      if (kb < 0 || dd_lt(ag, best)) { kb = k; best = ag; gb = gk; }
-    }
-    dd obest = shfl_dd(best, 1), ogb = shfl_dd(gb, 1);
-    int okb = __shfl_xor_sync(pair_mask(), kb, 1);
-    if (!isB) {  // merge: lower range wins ties
-      if (okb >= 0 && (kb < 0 || dd_lt(obest, best))) { kb = okb; best = obest; gb = ogb; }
-      if (!isnan(glast.hi) && (kb < 0 || dd_lt(dd_abs(glast), best))) { kb = last; best = dd_abs(glast); gb = glast; }
-    }
-    kb = shfl_i_from(kb, lane_F());
-    gb = shfl_dd_from(gb, lane_F());
-    cnt = shfl_i_from(cnt, lane_F());
-    g.r = kb;
-    g.gamma = gb;
-    g.c = cnt;
-    dd part = dd_from(0.0);
-    if (kb >= 0) {
-      if (!isB) part = (kb == last) ? acc : ldw(w.S, (long long)kb * S);
-      else part = (kb == last) ? dd_from(0.0) : ldw(w.T, (long long)kb * S);
-    }
-    dd other = shfl_dd(part, 1);
-    g.zz = dd_add_d(dd_add(part, other), 1.0);
-  } else {
-    // F: x = s(r), acc = S_r; B: tr = t(r), acc = T_r
-    dd sr = shfl_dd_from(x, lane_F());
-    dd t_r = shfl_dd_from(tr, lane_B());
-    int cF = shfl_i_from(cnt, lane_F());
-    int cB = shfl_i_from(cnt, lane_B());
-    dd gamma = (r == last) ? dd_add(sr, ldy(y, last).d) : dd_add(sr, t_r);
-    g.r = r;
-    g.gamma = gamma;
-    g.c = cF + cB + dd_sb(gamma);
-    dd other = shfl_dd(acc, 1);
-    g.zz = dd_add_d(dd_add(acc, other), 1.0);
-  }
-}
-
-// Branch-free version of getvec_pair for the common case: dd ops without special-value handling,
-// lane-dependent operand offsets instead of selects, two-ahead prefetch, prefetched argmin scan.
-// Returns false (in both lanes) if the qd recurrence of either lane left the finite range (a zero
-// pivot / IEEE infinity), in which case the caller reruns getvec_pair.
-struct Elt3 {
-  double2 a, b, c;
-};
-__device__ __forceinline__ Elt3 ld3(const YElt *__restrict__ y, int i, int oa, int oc) {
-  const double2 *q = reinterpret_cast<const double2 *>(y + i);
-  Elt3 e;
-  e.a = __ldg(q + oa);
-  e.b = __ldg(q + 1);
-  e.c = __ldg(q + oc);
-  return e;
-}
-__device__ __forceinline__ dd D(double2 v) { return dd_make(v.x, v.y); }
-
-__device__ bool getvec_pair_fast(const YElt *__restrict__ y, int nb, dd lam, int r, bool isB, const PairWS &w,
-                                 long long S, GV &g) {
-  const int last = nb - 1;
-  const int nsteps = (r < 0) ? last : (isB ? last - r : r);
-  const int oa = isB ? 2 : 0, oc = isB ? 0 : 2;  // F: a = d, c = dll; B: a = dll, c = d (double2 slots)
-  dd x = isB ? dd_sub_nf(ldy(y, last).d, lam) : dd_neg(lam);
-  dd acc = dd_from(0.0), tr = dd_from(0.0);
-  int cnt = 0;
-  dd *P1 = isB ? w.t : w.s, *P2 = isB ? w.T : w.S, *P3 = isB ? w.U : w.L;
-  const bool it1 = r < 0;
-#define FIX(k) (isB ? (last - 1 - (k)) : (k))
-  if (nsteps > 0) {
-    Elt3 e0 = ld3(y, FIX(0), oa, oc), e1 = ld3(y, FIX(min(1, nsteps - 1)), oa, oc);
-    for (int k = 0; k < nsteps; k++) {
-      Elt3 e2 = ld3(y, FIX(min(k + 2, nsteps - 1)), oa, oc);
-      const long long off = (long long)FIX(k) * S;
-      const dd a = D(e0.a), b = D(e0.b), c = D(e0.c);
-      dd den = dd_add_nf(x, a);
-      dd rr = dd_rcp_nf(den);
-      dd q = dd_mul_nf(x, rr);
-      dd out = dd_mul_nf(b, rr);
-      dd xn = dd_sub_nf(dd_mul_nf(q, c), lam);
-      dd accn = dd_mul_nf(dd_mul_nf(out, out), dd_add_d_nf(acc, 1.0));
-      if (it1) {
-        dd t = dd_mul_nf(dd_mul_nf(c, rr), x);  // B: d(i)/omega(i+1) p(i+1)
-        stw(P1, off, isB ? t : x);
-        stw(P2, off, isB ? accn : acc);
-      } else if (isB && k == nsteps - 1) {
-        tr = dd_mul_nf(dd_mul_nf(c, rr), x);
-      }
-      stw(P3, off, out);
-      cnt += dd_sb(den);
-      x = xn;
-      acc = accn;
-      e0 = e1;
-      e1 = e2;
-    }
-  }
-#undef FIX
-  const unsigned pm = pair_mask();
-  bool ok = isfinite(x.hi) && isfinite(x.lo);
-  ok = __shfl_xor_sync(pm, (int)ok, 1) && ok;
-  __syncwarp(pm);
-  if (!ok) return false;
-  if (it1) {
-    dd glast = isB ? dd_from(0.0) : dd_add(x, ldy(y, last).d);
-    if (!isB) cnt += dd_sb(glast);
-    const int h = last / 2;
-    const int k0 = isB ? h : 0, k1 = isB ? last : h;
-    int kb = -1;
-    dd best = dd_from(INFINITY), gb = dd_from(0.0);
-    if (k1 > k0) {
-      const int kl = k1 - 1;
-      dd s0 = ldw(w.s, (long long)k0 * S), t0 = ldw(w.t, (long long)k0 * S);
-      dd s1 = ldw(w.s, (long long)min(k0 + 1, kl) * S), t1 = ldw(w.t, (long long)min(k0 + 1, kl) * S);
-      dd s2 = ldw(w.s, (long long)min(k0 + 2, kl) * S), t2 = ldw(w.t, (long long)min(k0 + 2, kl) * S);
-      for (int k = k0; k < k1; k++) {
-        const int kn = min(k + 3, kl);
-        dd s3 = ldw(w.s, (long long)kn * S), t3 = ldw(w.t, (long long)kn * S);
-        dd gk = dd_add(s0, t0);
-        dd ag = dd_abs(gk);
-        bool take = !isnan(gk.hi) && (kb < 0 || dd_lt(ag, best));
-        kb = take ? k : kb;
-        best = take ? ag : best;
-        gb = take ? gk : gb;
-        s0 = s1; s1 = s2; s2 = s3;
-        t0 = t1; t1 = t2; t2 = t3;
-      }
-    }
-    dd obest = shfl_dd(best, 1), ogb = shfl_dd(gb, 1);
-    int okb = __shfl_xor_sync(pm, kb, 1);
-    if (!isB) {  // merge: the lower range wins ties, then k = n-1
-      if (okb >= 0 && (kb < 0 || dd_lt(obest, best))) { kb = okb; best = obest; gb = ogb; }
-      if (!isnan(glast.hi) && (kb < 0 || dd_lt(dd_abs(glast), best))) { kb = last; best = dd_abs(glast); gb = glast; }
-    }
-    kb = shfl_i_from(kb, lane_F());
-    gb = shfl_dd_from(gb, lane_F());
-    cnt = shfl_i_from(cnt, lane_F());
-    g.r = kb;
-    g.gamma = gb;
-    g.c = cnt;
-    dd part = dd_from(0.0);
-    if (kb >= 0) {
-      if (!isB) part = (kb == last) ? acc : ldw(w.S, (long long)kb * S);
-      else part = (kb == last) ? dd_from(0.0) : ldw(w.T, (long long)kb * S);
-    }
-    dd other = shfl_dd(part, 1);
-    g.zz = dd_add_d(dd_add(part, other), 1.0);
-  } else {
-    dd sr = shfl_dd_from(x, lane_F());
-    dd t_r = shfl_dd_from(tr, lane_B());
-    int cF = shfl_i_from(cnt, lane_F());
-    int cB = shfl_i_from(cnt, lane_B());
-    dd gamma = (r == last) ? dd_add(sr, ldy(y, last).d) : dd_add(sr, t_r);
-    g.r = r;
-    g.gamma = gamma;
-    g.c = cF + cB + dd_sb(gamma);
-    dd other = shfl_dd(acc, 1);
-    g.zz = dd_add_d(dd_add(acc, other), 1.0);
-  }
-  return true;
-}
-
-// final pass of the pair: z(r) = 1, F writes rows r-1 .. 0, B rows r+1 .. n-1 (A-25 order of the
-// zero-pivot substitutions reproduced: z(r+1) pre-value, then z(r-1), then z(r+1))
-__device__ void zwrite_pair(const YElt *__restrict__ y, int nb, int r, bool isB, const PairWS &w, long long S,
-                            dd inv, double *Zc) {
-  const int last = nb - 1;
-  dd zp1 = dd_from(0.0), zm1 = dd_from(0.0);
-  dd ur = (r < last) ? ldw(w.U, (long long)r * S) : dd_from(0.0);
-  if (r < last && !is_mark(ur)) zp1 = dd_neg(ur);  // pre-value
-  if (r > 0) {
-    dd l = ldw(w.L, (long long)(r - 1) * S);
-    if (!is_mark(l)) zm1 = dd_neg(l);
-    else {
-      dd num = (r < last) ? ld_dl(y + r) : dd_from(0.0);
-      dd v = dd_neg(dd_mul(dd_div(num, ld_dl(y + r - 1)), zp1));
-      zm1 = isfinite(v.hi) ? v : dd_from(0.0);
-    }
-  }
-  if (r < last && is_mark(ur)) {
-    dd num = (r >= 1) ? ld_dl(y + r - 1) : dd_from(0.0);
-    dd v = dd_neg(dd_mul(dd_div(num, ld_dl(y + r)), zm1));
-    zp1 = isfinite(v.hi) ? v : dd_from(0.0);
-  }
-  if (!isB) {
-    Zc[r] = inv.hi;
-    if (r > 0) Zc[r - 1] = dd_mul(zm1, inv).hi;
-  } else if (r < last) {
-    Zc[r + 1] = dd_mul(zp1, inv).hi;
-  }
-  // F: i = r-2 .. 0 with z1 = z(i+1), z2 = z(i+2); B: computes z(i+1), i = r+1 .. last-1, z1 = z(i), z2 = z(i-1)
-  const int nsteps = isB ? max(last - 1 - r, 0) : max(r - 1, 0);
-  dd z1 = isB ? zp1 : zm1, z2 = dd_from(1.0);
-  const dd *arr = isB ? w.U : w.L;
-#define ZIX(k) (isB ? (r + 1 + (k)) : (r - 2 - (k)))
-  if (nsteps > 0) {
-    dd w0 = ldw(arr, (long long)ZIX(0) * S), w1 = ldw(arr, (long long)ZIX(min(1, nsteps - 1)) * S);
-    for (int k = 0; k < nsteps; k++) {
-      dd w2 = ldw(arr, (long long)ZIX(min(k + 2, nsteps - 1)) * S);
-      const int i = ZIX(k);
-      dd z;
-      if (!is_mark(w0)) {
-        z = dd_neg(dd_mul(w0, z1));
-      } else {
-        int in = isB ? i - 1 : i + 1;
-        dd num = (isB ? (in >= 0) : (in < last)) ? ld_dl(y + in) : dd_from(0.0);
-        dd v = dd_neg(dd_mul(dd_div(num, ld_dl(y + i)), z2));
-        z = isfinite(v.hi) ? v : dd_from(0.0);
-      }
-      Zc[isB ? i + 1 : i] = dd_mul(z, inv).hi;
-      z2 = z1;
-      z1 = z;
-      w0 = w1;
-      w1 = w2;
-    }
-  }
-#undef ZIX
-}
-
-__global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
-                                             const YElt *__restrict__ my, dd *ws, long long S, long long nbmax,
-                                             double *W, double *Z, long long ldz, int *diag_depth, double *fin_lo,
-                                             double *fin_hi, long long *stats) {
-  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool isB = gt & 1;
-  const int pid = gt >> 1;  // workspace column (padded grid: S >= #pairs launched)
-  const bool active = pid < ns;
-  const Singleton s = sg[active ? pid : ns - 1];  // idle pairs shadow the last singleton in their own columns
-  const RepDesc R = reps[s.rep];
-  const int nb = R.nb, j = s.j;
-  const YElt *y = my + R.off;
-  const long long plane = nbmax * S;
-  PairWS w;
-  w.s = ws + pid; w.t = ws + plane + pid; w.S = ws + 2 * plane + pid; w.T = ws + 3 * plane + pid;
-  w.L = ws + 4 * plane + pid; w.U = ws + 5 * plane + pid;
-  double mid = bis_mid(s.lo, s.hi);
-  double nu = __dmul_rn(__dmul_rn(100.0, (double)nb), EPS_X);
-  dd blo = dd_from(__dsub_rn(s.lo, __dmul_rn(nu, fabs(s.lo))));
-  dd bhi = dd_from(__dadd_rn(s.hi, __dmul_rn(nu, fabs(s.hi))));
-  dd lam = dd_from(mid);
-  double thr1 = __dmul_rn(__dmul_rn(s.gap, EPS_X), sqrt((double)nb));
-  int r = -1, iters = 0;
-  long long qd = 0, qdg = 0, zs = 0;
-  bool accepted = false;
-  GV g;
-  dd zz = dd_from(1.0);
-  for (int it = 0; it < MAX_RQI && !accepted; it++) {
-    if (r < 0) { qd += 2 * (nb - 1); qdg += nb - 1; } else qd += nb - 1;
-    if (!getvec_pair_fast(y, nb, lam, r, isB, w, S, g)) getvec_pair(y, nb, lam, r, isB, w, S, g);
-    iters++;
-    r = g.r;
-    if (r < 0) break;
-    zz = g.zz;
-    if (!isfinite(zz.hi)) {  // zero pivot inside: explicit z solve (lane F), broadcast
-      zs += nb - 1;
-      if (!isB) zz = zsolve(y, nb, r, w.U, w.L, S, dd_from(0.0), nullptr);
-      zz = shfl_dd_from(zz, lane_F());
-    }
-    if (!isfinite(zz.hi) || zz.hi == 0.0) break;
-    dd nz = dd_sqrt(zz);
-    dd resid = dd_div(dd_abs(g.gamma), nz);
-    dd rqc = dd_div(g.gamma, zz);
-    if (resid.hi <= thr1 || dd_lt(dd_abs(rqc), dd_mul_d(dd_abs(lam), 4.0 * EPS_Y))) { accepted = true; break; }
-    if (g.c < j) blo = lam; else bhi = lam;
-    dd nl = dd_add(lam, rqc);
-    bool ok = ((g.c < j) ? (rqc.hi > 0.0) : (rqc.hi < 0.0)) && dd_lt(blo, nl) && dd_lt(nl, bhi);
-    if (ok) lam = nl;
-    else break;
-  }
-  if (!accepted) {
-    if (active && !isB) atomicAdd((unsigned long long *)&stats[ST_RQI_FALLBACK], 1ull);
-    lam = bisect_y_full(y, nb, j, blo, bhi);
-    getvec_pair(y, nb, lam, r, isB, w, S, g);
-    if (r < 0) qdg += nb - 1;
-    qd += (r < 0) ? 2 * (nb - 1) : nb - 1;
-    iters++;
-    r = g.r < 0 ? 0 : g.r;
-    zz = g.zz;
-    if (!isfinite(zz.hi)) {
-      zs += nb - 1;
-      if (!isB) zz = zsolve(y, nb, r, w.U, w.L, S, dd_from(0.0), nullptr);
-      zz = shfl_dd_from(zz, lane_F());
-    }
-  }
-  dd inv = dd_rcp(dd_sqrt(zz));
-  if (active) {
-    double *Zc = Z + (long long)s.col * ldz + R.bstart;
-    zwrite_pair(y, nb, r, isB, w, S, inv, Zc);
-    if (!isB) {
-      dd sig = dd_make(R.sig_hi, R.sig_lo);
-      W[s.col] = dd_add(lam, sig).hi;
-      if (diag_depth) {
-        diag_depth[s.col] = R.depth;
-        fin_lo[s.col] = s.lo;
-        fin_hi[s.col] = s.hi;
-      }
-      atomicAdd((unsigned long long *)&stats[ST_RQI_ITERS], (unsigned long long)iters);
-      atomicAdd((unsigned long long *)&stats[ST_QD_STEPS], (unsigned long long)qd);
-      atomicAdd((unsigned long long *)&stats[ST_QDG_STEPS], (unsigned long long)qdg);
-      atomicAdd((unsigned long long *)&stats[ST_Z_STEPS], (unsigned long long)zs);
-      atomicAdd((unsigned long long *)&stats[ST_ZW_STEPS], (unsigned long long)(nb - 1));
-      atomicAdd((unsigned long long *)&stats[ST_GETVEC], (unsigned long long)iters);
-      atomicMax((unsigned long long *)&stats[ST_DMAX], (unsigned long long)R.depth);
-    }
-  }
-}
-
 // size-1 blocks (S2): eigenpair (alpha_s, e_s)
 __global__ void k_trivial(const double *__restrict__ d, const int *__restrict__ starts, int nblk,
                           const int *__restrict__ colmap, double *W, double *Z, long long ldz, int *diag_depth,

@@ -16,6 +16,7 @@
 #include "../../include/mrrr.h"
 #include "kernels.cuh"
 #include "kernels_vec.cuh"
+#include "kernels_rqi.cuh"
 
 namespace {
 
@@ -92,7 +93,7 @@ struct mrrr_ctx {
   // buffers
   Buf starts, scal, binfo, bside, blist, cab, mx, my, lscratch, reps, rlo, rhi, colmap, gstart;
   Buf nodesA, nodesB, counts, ex, excounts, exmap, bnA, bnB, sing, clusA, clusB, ss, gval, valid, cseg, bnoff,
-      ipool_lo, ipool_hi, yref_lo, yref_hi, wsA, wsB, stats, cnt, ddepth, dgf, dgl, dflo, dfhi, hd, he, hW, hZ;
+      ipool_lo, ipool_hi, yref_lo, yref_hi, wsA, wsB, stats, cnt, ddepth, dgf, dgl, dflo, dfhi, hd, he, hW, hZ, zmeta;
   int *h_cnt = nullptr;  // pinned counters
 
   // results of the last call
@@ -327,13 +328,13 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
   if (ns <= 0) return;
   const bool pair = h->rqi_pair;
   // workspace per singleton: pair kernel 6 dd planes, single-lane kernel 2
-  long long per = (pair ? 6LL : 2LL) * (long long)sizeof(dd) * std::max<long long>(nbmax, 1);
+  long long per = (pair ? 3LL : 2LL) * (long long)sizeof(dd) * std::max<long long>(nbmax, 1);
   long long budget = std::min<long long>(h->ws_limit / 2, 64LL << 30);
   long long bmax = std::max<long long>(32, budget / per);
   long long batch = std::min<long long>(ns, bmax);
   long long stride = (batch + 31) / 32 * 32;  // pairs launched per batch (grid padding)
   if (pair) {
-    CK(h->wsA.ensure((size_t)6 * stride * nbmax * sizeof(dd)));
+    CK(h->wsA.ensure((size_t)3 * stride * nbmax * sizeof(dd)));
   } else {
     CK(h->wsA.ensure((size_t)stride * nbmax * sizeof(dd)));
     CK(h->wsB.ensure((size_t)stride * nbmax * sizeof(dd)));
@@ -343,10 +344,15 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
     long long nb = std::min<long long>(batch, ns - b0);
     CK(cudaEventRecord(h->rq0, h->stream));
     if (pair) {
+      CK(h->zmeta.ensure(sizeof(ZMeta) * stride));
       k_rqi2<<<nblocks_for(2 * nb, 64), 64, 0, h->stream>>>(
           h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>(), stride,
-          nbmax, W, Z, ldz, diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
-          diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>());
+          nbmax, W, h->zmeta.as<ZMeta>(), diag ? h->ddepth.as<int>() : nullptr,
+          diag ? h->dflo.as<double>() : nullptr, diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>());
+      launch_check(h);
+      k_zwrite<<<nblocks_for(32 * nb, 256), 256, 0, h->stream>>>(
+          h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(),
+          h->wsA.as<dd>() + 2 * stride * nbmax, nbmax, h->zmeta.as<ZMeta>(), Z, ldz);
     } else {
       k_rqi<<<nblocks_for(nb, 64), 64, 0, h->stream>>>(
           h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>(),
@@ -961,7 +967,7 @@ int mrrr_destroy(mrrr_t h) {
                  &h->excounts, &h->exmap, &h->bnA, &h->bnB, &h->sing, &h->clusA, &h->clusB, &h->ss, &h->gval,
                  &h->valid, &h->cseg, &h->bnoff, &h->ipool_lo, &h->ipool_hi, &h->yref_lo, &h->yref_hi, &h->wsA,
                  &h->wsB, &h->stats, &h->cnt, &h->ddepth, &h->dgf, &h->dgl, &h->dflo, &h->dfhi,
-                 &h->hd, &h->he, &h->hW, &h->hZ};
+                 &h->hd, &h->he, &h->hW, &h->hZ, &h->zmeta};
   for (Buf *b : bufs) b->release();
   for (auto &ev : h->ev) cudaEventDestroy(ev);
   cudaEventDestroy(h->rq0);

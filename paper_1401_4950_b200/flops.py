@@ -5,14 +5,14 @@ FP64 instruction counts of the dd building blocks as written in csrc/dd.cuh (one
   dd_rcp 11 (MUFU seed, 5 FMA Newton, 2 FMA residual, 1 MUL, fast_two_sum; no IEEE division).
   qd_step (one dstqds or dqds element, csrc/kernels_vec.cuh) = dd_add + dd_rcp + 3 dd_mul + dd_sub = 78
   + the ||z||^2 recurrence S/T (dd_mul + dd_add_d + dd_mul)                                      = 28
-  iteration-1 extras per element: t(i) = 2 dd_mul (B lane) and gamma_k = dd_add in the combine    = 38
+  iteration-1 extras per element: t(i) = 2 dd_mul, gamma_k and S_k + T_k (2 dd_add)               = 58
   explicit z-solve element (zero-pivot fallback)                                                  = 38
   output element z * (1/||z||)                                                                     =  9
 Flops are reported FMA-equivalent (2 per slot) so they compare with 2 x measured DFMA/s.
 """
 
 SLOTS_QD = 78.0 + 28.0
-SLOTS_ITER1 = 38.0
+SLOTS_ITER1 = 58.0
 SLOTS_Z = 38.0
 SLOTS_ZW = 9.0
 

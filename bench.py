@@ -156,7 +156,7 @@ def main():
     ap.add_argument("--workload", default="C2", choices=sorted(mi.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-k", type=int, default=256)
-    ap.add_argument("--cpu-k", type=int, default=256)
+    ap.add_argument("--cpu-k", type=int, default=8192)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -245,20 +245,35 @@ def main():
     stats = solver.stats()
     tphase = solver.times()
 
-    # roofline of the dominant kernel (k_rqi): counted FP64 flops per launch / event-timed launch duration
+    # roofline of the dominant kernel family: algorithmic FP64 flops per launch / CUDA-event launch time
     pk = peaks()
     fp = pk.get("fp64") or {}
-    roof = None
+    roof, roof_other = None, None
     if fp:
         from paper_1401_4950_b200 import flops as fl
-        launch_ms = rq_ms / max(rq_n, 1)
-        fl_launch = fl.rqi_flops(stats, n, fp.get("w_div", 8.0)) / max(int(tphase["rqi_launches"]), 1)
-        achieved = fl_launch / (launch_ms * 1e-3) / 1e12
+        wdiv = fp.get("w_div", 13.0)
         peak = fp["fp64_tflops"]
-        roof = {"bound": "alu", "kernel": "k_rqi", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None,
-                "peak_src": "profiles/fp64_peak_r01.json (measured DFMA rate x 2, this pool's B200)",
-                "launch_ms": launch_ms, "flops_per_launch": fl_launch}
+        src = "profiles/fp64_peak_r01.json: measured DFMA rate x 2 on this pool's B200 (burst, all SMs)"
+        cands = []
+        nrq = max(int(tphase["rqi_launches"]), 1)
+        if rq_n:
+            launch_ms = rq_ms / rq_n
+            f = fl.rqi_flops(stats, n, wdiv) / nrq
+            cands.append(("k_rqi2+k_zwrite (singleton RQI + eigenvectors)", launch_ms, f, rq_ms))
+        if tphase["negcount_launches"]:
+            launch_ms = tphase["negcount_ms_per_launch"]
+            nl = tphase["negcount_launches"]
+            f = fl.negcount_flops(stats, n, wdiv) / nl
+            cands.append(("k_negcount (x-bisection, shared-tree k-section)", launch_ms, f, launch_ms * nl * args.steps))
+        cands.sort(key=lambda c: -c[3])
+        out = []
+        for name, launch_ms, f, _ in cands:
+            ach = f / (launch_ms * 1e-3) / 1e12
+            out.append({"bound": "alu", "kernel": name, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                        "frac": ach / peak, "traffic": None, "peak_src": src, "launch_ms": launch_ms,
+                        "flops_per_launch": f})
+        roof = out[0] if out else None
+        roof_other = out[1:] if len(out) > 1 else None
 
     e2e = None
     if world == 1 and not args.no_e2e:
@@ -289,7 +304,8 @@ def main():
                            "parallelism": f"index shards x{world}" if world > 1 else "single GPU",
                            "l2": "flushed between steps (256 MiB write, outside the events)"},
                 "gpu_launches": int(launches_per_step) * args.steps,
-                "phases_ms": tphase, "stats": stats, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "phases_ms": tphase, "stats": stats, "roofline": roof, "roofline_other": roof_other,
+                "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     solver.close()

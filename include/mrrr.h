@@ -100,7 +100,9 @@ int mrrr_eig_shard(mrrr_t h, const double *d, const double *e, int64_t n, int64_
  * 9 failed clusters, 10 x-NegCount evaluations, 11 y-NegCount evaluations,
  * 12 Getvec calls, 13 bisection rounds, 14 kernel launches, 15 nblocks,
  * 16 dd qd steps in k_rqi (dstqds/dqds element steps), 17 of them with the twist quantity gamma_k,
- * 18 z-solve element steps (norm pass), 19 z-solve element steps that write Z. */
+ * 18 z-solve element steps (norm pass), 19 z-solve element steps that write Z,
+ * 20 x-NegCount evaluations on the sequential bisection paths (shared-tree nodes; the algorithmic
+ * count, without k-section speculation), 21 the same for y-NegCount. */
 #define MRRR_NSTATS 24
 int mrrr_get_stats(mrrr_t h, int64_t *stats, int32_t nstats);
 
@@ -126,8 +128,9 @@ int mrrr_get_diag(mrrr_t h, mrrr_diag *g);
 /* Time of the last call in milliseconds (CUDA events on the handle's stream,
  * entry to results ready), split into phases: [0] total, [1] split+root,
  * [2] root bisection, [3] classification, [4] cluster path, [5] singleton RQI.
- * Also the average duration of the dominant kernel launches: [6] ms per
- * k_rqi launch (events around each launch), [7] number of k_rqi launches. */
+ * Also the average duration of the dominant kernel launches (events around each launch on the
+ * handle's stream): [6] ms per singleton-RQI launch, [7] their number, [8] ms per x-NegCount
+ * (root/child bisection) launch, [9] their number. */
 int mrrr_get_times(mrrr_t h, double *ms, int32_t nt);
 
 /* Built-in self tests (run on the current device).  which = 1: the NegCount division fast path

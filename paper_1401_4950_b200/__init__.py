@@ -27,9 +27,9 @@ NSTATS = 24
 STAT_NAMES = ["d_max", "n_clusters", "largest_cluster", "uncertified", "shift_attempts", "rqi_iters",
               "rqi_fallbacks", "bracket_fixes", "root_backoffs", "failed", "negcount_x", "negcount_y",
               "getvec_calls", "rounds", "launches", "nblocks", "qd_steps", "qdg_steps", "z_steps", "zw_steps",
-              "s20", "s21", "s22", "s23"]
+              "negcount_x_alg", "negcount_y_alg", "s22", "s23"]
 TIME_NAMES = ["total", "split_root", "root_bisection", "classification", "clusters", "singletons",
-              "rqi_ms_per_launch", "rqi_launches"]
+              "rqi_ms_per_launch", "rqi_launches", "negcount_ms_per_launch", "negcount_launches", "t10", "t11"]
 
 
 class MrrrError(RuntimeError):
@@ -185,8 +185,8 @@ class Solver:
         return {nm: int(s[i]) for i, nm in enumerate(STAT_NAMES)}
 
     def times(self) -> dict:
-        t = np.zeros(8)
-        _check(load().mrrr_get_times(self._h, t.ctypes.data, 8), "mrrr_get_times")
+        t = np.zeros(12)
+        _check(load().mrrr_get_times(self._h, t.ctypes.data, 12), "mrrr_get_times")
         return {nm: float(t[i]) for i, nm in enumerate(TIME_NAMES)}
 
     def diag(self) -> Diag:

@@ -87,7 +87,7 @@ struct mrrr_ctx {
   long long ws_limit = 0;
   long long target_chains = 131072;
   int mmax = 16;
-  int chains_per_thread = 2;
+  int chains_per_thread = 1;
   bool rqi_pair = true;
 
   // buffers
@@ -100,11 +100,13 @@ struct mrrr_ctx {
   long long last_n = 0, last_k = 0;
   int last_nblk = 0;
   long long stats_h[ST_N] = {0};
-  double times[8] = {0};
+  double times[12] = {0};
   std::vector<int> h_starts;
   cudaEvent_t ev[8];
   cudaEvent_t rq0, rq1;
-  double rqi_ms = 0;
+  double rqi_ms = 0, neg_ms = 0;
+  long long neg_launches = 0, neg_len = 0;
+  cudaEvent_t nc0, nc1;
   long long rqi_launches = 0;
   long long host_rounds = 0, host_launches = 0;
 };
@@ -269,7 +271,9 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
     CK(h->counts.ensure(std::max<long long>(nch, 1) * sizeof(int)));
     int nex = first ? nverify : 0;
     zero_counters(h);
+    CK(cudaEventRecord(h->nc0, h->stream));
     launch_negcount<Y>(h, cur, nnode, m, nex);
+    CK(cudaEventRecord(h->nc1, h->stream));
     if (nex > 0) {
       k_root_verify<<<nblocks_for(nbl, 128), 128, 0, h->stream>>>(blist_dev, nbl, h->starts.as<int>(),
                                                                   h->binfo.as<double>(), h->excounts.as<int>(),
@@ -277,11 +281,18 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
       launch_check(h);
     }
     k_bisect_update<<<nblocks_for((long long)nnode << m, 128), 128, 0, h->stream>>>(
-        cur, nnode, m, h->counts.as<int>(), nxt, h->cnt.as<int>() + C_NNEXT, out_lo, out_hi, rtol);
+        cur, nnode, m, h->counts.as<int>(), nxt, h->cnt.as<int>() + C_NNEXT, out_lo, out_hi, rtol,
+        (unsigned long long *)(h->stats.as<long long>() + (Y ? ST_NEGY_ALG : ST_NEGX_ALG)));
     launch_check(h);
     read_counters(h);
     h->host_rounds++;
     h->stats_h[Y ? ST_NEGY : ST_NEGX] += nch + nex;
+    if (!Y) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, h->nc0, h->nc1));
+      h->neg_ms += ms;
+      h->neg_launches++;
+    }
     if (nex > 0 && h->h_cnt[C_NEX] > 0) { *restart = true; return; }
     nnode = h->h_cnt[C_NNEXT];
     std::swap(cur, nxt);
@@ -513,6 +524,8 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
   h->host_rounds = h->host_launches = 0;
   h->rqi_ms = 0;
   h->rqi_launches = 0;
+  h->neg_ms = 0;
+  h->neg_launches = 0;
   memset(h->stats_h, 0, sizeof(h->stats_h));
   bool diag = (h->flags & MRRR_KEEP_DIAG) != 0;
 
@@ -760,6 +773,8 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
   CK(cudaEventElapsedTime(&ms, h->ev[3], h->ev[4])); h->times[5] = ms;
   h->times[6] = h->rqi_launches ? h->rqi_ms / h->rqi_launches : 0.0;
   h->times[7] = (double)h->rqi_launches;
+  h->times[8] = h->neg_launches ? h->neg_ms / h->neg_launches : 0.0;
+  h->times[9] = (double)h->neg_launches;
   return 0;
 }
 
@@ -807,6 +822,8 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     for (auto &ev : h->ev) CK(cudaEventCreate(&ev));
     CK(cudaEventCreate(&h->rq0));
     CK(cudaEventCreate(&h->rq1));
+    CK(cudaEventCreate(&h->nc0));
+    CK(cudaEventCreate(&h->nc1));
     CK(cudaMallocHost(&h->h_cnt, sizeof(int) * C_NCOUNTERS));
   } catch (Err &er) {
     delete h;
@@ -887,7 +904,7 @@ int mrrr_get_stats(mrrr_t h, int64_t *s, int32_t ns) {
 
 int mrrr_get_times(mrrr_t h, double *ms, int32_t nt) {
   if (!h || !ms) return -1;
-  for (int i = 0; i < nt && i < 8; i++) ms[i] = h->times[i];
+  for (int i = 0; i < nt && i < 12; i++) ms[i] = h->times[i];
   return 0;
 }
 

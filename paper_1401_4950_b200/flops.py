@@ -25,3 +25,15 @@ def rqi_slots(stats: dict, w_div: float = 0.0) -> float:
 def rqi_flops(stats: dict, n: int, w_div: float = 0.0) -> float:
     """FMA-equivalent FP64 flops executed by all k_rqi2 launches of the last solve."""
     return 2.0 * rqi_slots(stats, w_div)
+
+
+# x-NegCount (Alg. negcountLDL P:7092-7119) per element: dp = d + s (DADD), q = s / dp (one IEEE
+# division = w_div DFMA slots, measured), s = q * dll - sigma (DMUL + DADD): 3 + w_div slots.
+def negcount_slots_per_element(w_div: float) -> float:
+    return 3.0 + w_div
+
+
+def negcount_flops(stats: dict, nb: int, w_div: float) -> float:
+    """Algorithmic flops of the x-NegCount evaluations on the sequential bisection paths (shared-tree
+    nodes, stats['negcount_x_alg']); k-section points off the path are speculative and not counted."""
+    return 2.0 * stats["negcount_x_alg"] * nb * negcount_slots_per_element(w_div)

@@ -19,7 +19,7 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmrrr.so")
+LIB_PATH = os.environ.get("MRRR_LIB") or os.path.join(HERE, "libmrrr.so")
 
 KEEP_DIAG = 1
 MAXD = 8

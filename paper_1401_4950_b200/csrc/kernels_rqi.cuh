@@ -20,6 +20,10 @@
 #pragma once
 #include "kernels_vec.cuh"
 
+#ifndef MRRR_RQI_PD
+#define MRRR_RQI_PD 2  // prefetch ring depth of the RQI step loops (2 measured best on C2)
+#endif
+
 __device__ __forceinline__ unsigned pair_mask() { return 3u << ((threadIdx.x & 31) & ~1u); }
 __device__ __forceinline__ int lane_F() { return (threadIdx.x & 31) & ~1; }
 __device__ __forceinline__ int lane_B() { return (threadIdx.x & 31) | 1; }
@@ -64,6 +68,84 @@ __device__ __forceinline__ void cand_take(Cand &c, dd g, dd st, int k, bool tie_
   if (take) { c.best = a; c.gam = g; c.st = st; c.k = k; }
 }
 
+// one qd step (dstqds for F, dqds for B; see qd_step) plus the ||z||^2 recurrence
+template <bool C>
+__device__ __forceinline__ void qd_math(dd x, dd a, dd b, dd c, dd lam, dd acc, dd &den, dd &rr, dd &out, dd &xn,
+                                        dd &accn) {
+  den = OADD<C>(x, a);
+  rr = ORCP<C>(den);
+  dd q = OMUL<C>(x, rr);
+  if constexpr (C) q = (dd_isinf(x) && dd_isinf(den)) ? dd_from(1.0) : q;
+  out = OMUL<C>(b, rr);
+  xn = OSUB<C>(OMUL<C>(q, c), lam);
+  accn = OMUL<C>(OMUL<C>(out, out), OADD1<C>(acc));
+}
+
+enum { PH_STORE = 0, PH_COMBINE = 1, PH_FIXED = 2 };
+
+// steps k0 .. k1-1 of one lane (F: row i = k, B: row i = n-2-k) with the representation elements and
+// (phase B) the other lane's halves read PD steps ahead through compile-time-indexed rings.
+template <bool C, int MODE>
+__device__ __forceinline__ void run_phase(const YElt *__restrict__ y, int last, int k0, int k1, bool isB, int oa,
+                                          int oc, dd lam, int r, dd *P0, dd *P1, dd *P2, long long S, dd &x, dd &acc,
+                                          int &cnt, Cand &cd, dd &tr) {
+  constexpr int PD = MRRR_RQI_PD;
+  if (k0 >= k1) return;
+#define GIX(k) (isB ? (last - 1 - (k)) : (k))
+  Elt3 er[PD];
+  dd pq[PD], ps[PD];
+#pragma unroll
+  for (int u = 0; u < PD; u++) {
+    const int kk = min(k0 + u, k1 - 1);
+    er[u] = ld3(y, GIX(kk), oa, oc);
+    if (MODE == PH_COMBINE) {
+      pq[u] = ldw(P0, (long long)GIX(kk) * S);
+      ps[u] = ldw(P1, (long long)GIX(kk) * S);
+    }
+  }
+  for (int kb = k0; kb < k1; kb += PD) {
+#pragma unroll
+    for (int u = 0; u < PD; u++) {
+      const int k = kb + u;
+      if (k < k1) {
+        const Elt3 e0 = er[u];
+        const int kn = min(k + PD, k1 - 1);
+        er[u] = ld3(y, GIX(kn), oa, oc);
+        dd other, ost;
+        if (MODE == PH_COMBINE) {
+          other = pq[u];
+          ost = ps[u];
+          pq[u] = ldw(P0, (long long)GIX(kn) * S);
+          ps[u] = ldw(P1, (long long)GIX(kn) * S);
+        }
+        const int i = GIX(k);
+        const dd c = D2(e0.c);
+        dd den, rr, out, xn, accn;
+        qd_math<C>(x, D2(e0.a), D2(e0.b), c, lam, acc, den, rr, out, xn, accn);
+        if (MODE == PH_STORE || MODE == PH_COMBINE) {
+          // F: (s(i), S_i) before the update; B: t(i) = d(i) p(i+1) / omega(i+1) and T_i after it
+          dd mine = isB ? OMUL<C>(OMUL<C>(c, rr), x) : x;
+          dd myst = isB ? accn : acc;
+          if (MODE == PH_STORE) {
+            stw(P0, (long long)i * S, mine);
+            stw(P1, (long long)i * S, myst);
+          } else {
+            cand_take(cd, OADD<C>(mine, other), OADD<C>(myst, ost), i, isB);
+          }
+        } else {
+          if (isB && k == k1 - 1) tr = OMUL<C>(OMUL<C>(c, rr), x);  // B's last row is r
+          if constexpr (C) stw(P2, i, (den.hi == 0.0) ? dd_mark() : out);
+          else stw(P2, i, out);
+        }
+        cnt += dd_sb(den);
+        x = xn;
+        acc = accn;
+      }
+    }
+  }
+#undef GIX
+}
+
 // One Getvec of the pair at shift lam.  r < 0: full twisted factorization and twist
 // search (iteration 1, no l+/u- stored); r >= 0: the r-twisted factorization, storing l+/u- in P2.
 // Returns false (both lanes) if the fast pass left the finite range.  On return (both lanes):
@@ -81,73 +163,31 @@ __device__ bool getvec_pair_t(const YElt *__restrict__ y, int nb, dd lam, int r,
   int cnt = 0;
   Cand cd;
   cd.k = -1; cd.best = dd_from(INFINITY); cd.gam = dd_from(0.0); cd.st = dd_from(0.0);
-#define GIX(k) (isB ? (last - 1 - (k)) : (k))
-  // iteration 1: the other lane's half of gamma_k for step k (rows with 2k > n-2) was written at its
-  // step n-2-k; it is prefetched PD steps ahead when already visible (2 t >= n-1-PD at issue step t)
-  constexpr int PD = 4;
-  dd pq[PD], ps[PD];
-  bool pv[PD];
-#pragma unroll
-  for (int u = 0; u < PD; u++) { pv[u] = false; pq[u] = ps[u] = dd_from(0.0); }
-  if (nsteps > 0) {
-    Elt3 e0 = ld3(y, GIX(0), oa, oc), e1 = ld3(y, GIX(min(1, nsteps - 1)), oa, oc);
-    for (int k0 = 0; k0 < nsteps; k0 += PD) {
-#pragma unroll
-      for (int u = 0; u < PD; u++) {
-        const int k = k0 + u;
-        if (k < nsteps) {
-          Elt3 e2 = ld3(y, GIX(min(k + 2, nsteps - 1)), oa, oc);
-          const int i = GIX(k);
-          const long long off = (long long)i * S;
-          const dd a = D2(e0.a), b = D2(e0.b), c = D2(e0.c);
-          dd den = OADD<C>(x, a);
-          dd rr = ORCP<C>(den);
-          dd q = OMUL<C>(x, rr);
-          if constexpr (C) q = (dd_isinf(x) && dd_isinf(den)) ? dd_from(1.0) : q;
-          dd out = OMUL<C>(b, rr);
-          dd xn = OSUB<C>(OMUL<C>(q, c), lam);
-          dd accn = OMUL<C>(OMUL<C>(out, out), OADD1<C>(acc));
-          if (it1) {
-            // F: (s(i), S_i) before the update; B: t(i) = d(i) p(i+1) / omega(i+1) and T_i after it
-            dd mine = isB ? OMUL<C>(OMUL<C>(c, rr), x) : x;
-            dd myst = isB ? accn : acc;
-            if (2 * k == last - 1) {  // lanes meet at the same index: exchange in registers
-              dd om = shfl_dd(mine, 1), ost = shfl_dd(myst, 1);
-              if (!isB) cand_take(cd, OADD<C>(mine, om), OADD<C>(myst, ost), i, false);
-            } else if (2 * k < last - 1) {
-              // the other lane reaches row i later: leave my half of gamma_i for it
-              stw(P0, off, mine);
-              stw(P1, off, myst);
-            } else {
-              // the other lane wrote its half of gamma_i at an earlier step
-              dd other = pv[u] ? pq[u] : ldw(P0, off);
-              dd ost = pv[u] ? ps[u] : ldw(P1, off);
-              cand_take(cd, OADD<C>(mine, other), OADD<C>(myst, ost), i, isB);
-            }
-            const int kp = k + PD;
-            pv[u] = false;
-            if (kp < nsteps && 2 * kp > last - 1) {
-              const long long offp = (long long)GIX(kp) * S;
-              pq[u] = ldw(P0, offp);
-              ps[u] = ldw(P1, offp);
-              pv[u] = 2 * k >= last - PD;
-            }
-            __syncwarp(pm);
-          } else {
-            if (isB && i == r) tr = OMUL<C>(OMUL<C>(c, rr), x);
-            if constexpr (C) stw(P2, i, (den.hi == 0.0) ? dd_mark() : out);
-            else stw(P2, i, out);
-          }
-          cnt += dd_sb(den);
-          x = xn;
-          acc = accn;
-          e0 = e1;
-          e1 = e2;
-        }
-      }
+  if (it1) {
+    // iteration 1: rows i with 2i < n-2 are reached first by the lane that stores its half of gamma_i
+    // (phase A); the lanes meet at i = (n-2)/2 if n-1 is odd; after one __syncwarp every remaining row
+    // (phase B) combines with the other lane's half written in phase A.
+    const int kA = last / 2;
+    run_phase<C, PH_STORE>(y, last, 0, kA, isB, oa, oc, lam, r, P0, P1, P2, S, x, acc, cnt, cd, tr);
+    if (last & 1) {
+      const int i = kA;
+      Elt3 e = ld3(y, i, oa, oc);
+      dd den, rr, out, xn, accn;
+      qd_math<C>(x, D2(e.a), D2(e.b), D2(e.c), lam, acc, den, rr, out, xn, accn);
+      dd mine = isB ? OMUL<C>(OMUL<C>(D2(e.c), rr), x) : x;
+      dd myst = isB ? accn : acc;
+      dd om = shfl_dd(mine, 1), ost = shfl_dd(myst, 1);
+      if (!isB) cand_take(cd, OADD<C>(mine, om), OADD<C>(myst, ost), i, false);
+      cnt += dd_sb(den);
+      x = xn;
+      acc = accn;
     }
+    __syncwarp(pm);
+    run_phase<C, PH_COMBINE>(y, last, kA + (last & 1), last, isB, oa, oc, lam, r, P0, P1, P2, S, x, acc, cnt, cd,
+                             tr);
+  } else {
+    run_phase<C, PH_FIXED>(y, last, 0, nsteps, isB, oa, oc, lam, r, P0, P1, P2, S, x, acc, cnt, cd, tr);
   }
-#undef GIX
   if constexpr (!C) {
     bool ok = isfinite(x.hi) && isfinite(x.lo);
     ok = __shfl_xor_sync(pm, (int)ok, 1) && ok;

@@ -312,12 +312,14 @@ __device__ __forceinline__ YV ldy(const YElt *__restrict__ y, int i) {
   v.dll = dd_make(c.x, c.y);
   return v;
 }
+// RQI workspace: streamed through L2 with evict-first hints so it does not push the representation
+// (read by every lane at every step) out of L2
 __device__ __forceinline__ dd ldw(const dd *w, long long off) {
-  double2 a = *reinterpret_cast<const double2 *>(w + off);
+  double2 a = __ldcs(reinterpret_cast<const double2 *>(w + off));
   return dd_make(a.x, a.y);
 }
 __device__ __forceinline__ void stw(dd *w, long long off, dd v) {
-  *reinterpret_cast<double2 *>(w + off) = make_double2(v.hi, v.lo);
+  __stcs(reinterpret_cast<double2 *>(w + off), make_double2(v.hi, v.lo));
 }
 
 // Getvec: r < 0 -> full twisted factorization + twist search (iteration 1);

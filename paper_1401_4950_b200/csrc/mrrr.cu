@@ -89,6 +89,8 @@ struct mrrr_ctx {
   int mmax = 16;
   int chains_per_thread = 1;
   bool rqi_pair = true;
+  bool l2_persist = true;
+  long long l2_max_window = 0;
 
   // buffers
   Buf starts, scal, binfo, bside, blist, cab, mx, my, lscratch, reps, rlo, rhi, colmap, gstart;
@@ -335,8 +337,27 @@ int run_brackets(mrrr_t h, int nbn) {
   return nready;
 }
 
+// keep the representation pool (read by every RQI lane at every step) resident in L2 while the
+// workspace streams past it: persisting access-policy window on the handle's stream
+void l2_pin_reps(mrrr_t h, bool on) {
+  if (!h->l2_persist) return;
+  cudaStreamAttrValue v;
+  memset(&v, 0, sizeof(v));
+  if (on) {
+    size_t bytes = std::min<size_t>(h->my.cap, (size_t)h->l2_max_window);
+    v.accessPolicyWindow.base_ptr = h->my.p;
+    v.accessPolicyWindow.num_bytes = bytes;
+    v.accessPolicyWindow.hitRatio = 1.0f;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  }
+  cudaStreamSetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &v);
+  cudaGetLastError();
+}
+
 void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long ldz) {
   if (ns <= 0) return;
+  l2_pin_reps(h, true);
   const bool pair = h->rqi_pair;
   // workspace per singleton: pair kernel 6 dd planes, single-lane kernel 2
   long long per = (pair ? 3LL : 2LL) * (long long)sizeof(dd) * std::max<long long>(nbmax, 1);
@@ -378,6 +399,7 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
     h->rqi_ms += ms;
     h->rqi_launches++;
   }
+  l2_pin_reps(h, false);
 }
 
 struct ClusterLevel {
@@ -819,6 +841,16 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_MMAX")) h->mmax = atoi(s);
     if (const char *s = getenv("MRRR_CH")) h->chains_per_thread = std::max(1, std::min(4, atoi(s)));
     if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;
+    if (const char *s = getenv("MRRR_L2PIN")) h->l2_persist = atoi(s) != 0;
+    {
+      int dev = h->device, maxwin = 0, l2 = 0;
+      cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+      cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+      h->l2_max_window = maxwin;
+      // set aside up to 1/4 of L2 for persisting lines (the representation pool)
+      if (h->l2_persist && maxwin > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)l2 / 4);
+      cudaGetLastError();
+    }
     for (auto &ev : h->ev) CK(cudaEventCreate(&ev));
     CK(cudaEventCreate(&h->rq0));
     CK(cudaEventCreate(&h->rq1));

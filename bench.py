@@ -183,16 +183,15 @@ def main():
     solver = mrrr.Solver(device=local, stream=stream.cuda_stream)
     d = torch.from_numpy(d_np).to(dev)
     e = torch.from_numpy(e_np).to(dev)
-    # shard of the index range: contiguous blocks per rank
+    # shard of the index range: contiguous blocks per rank, first-index group ownership
+    from paper_1401_4950_b200 import dist as pd
     if world > 1:
-        per = (k + world - 1) // world
-        sl, su = cfg.il + rank * per, min(cfg.il + (rank + 1) * per - 1, cfg.iu)
+        sl, su = pd.shard_range(cfg.il, cfg.iu, world, rank)
         W = None
     else:
         W = torch.empty(k, dtype=torch.float64, device=dev)
         Zt = torch.empty((k, n), dtype=torch.float64, device=dev)
     flushbuf = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=dev)
-    Wall = torch.empty(k, dtype=torch.float64, device=dev) if world > 1 else None
 
     def step():
         with torch.cuda.stream(stream):
@@ -200,15 +199,8 @@ def main():
                 solver.eig(d, e, cfg.il, cfg.iu, W=W, Z=Zt)
             else:
                 jlo, jhi, Wl, Zl = solver.eig_shard(d, e, sl, su)
-                # eigenvalue list allgather over NCCL (the only collective)
-                cnt = torch.tensor([jhi - jlo + 1], device=dev)
-                sizes = [torch.zeros_like(cnt) for _ in range(world)]
-                dist.all_gather(sizes, cnt)
-                m = int(max(int(x) for x in sizes))
-                buf = torch.zeros(m, dtype=torch.float64, device=dev)
-                buf[:Wl.numel()] = Wl
-                parts = [torch.empty(m, dtype=torch.float64, device=dev) for _ in range(world)]
-                dist.all_gather(parts, buf)
+                # eigenvalue list all-gather over NCCL: the only collective
+                pd.allgather_eigenvalues(Wl, jlo, jhi, cfg.il, cfg.iu)
 
     for _ in range(args.warmup):
         step()

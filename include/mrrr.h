@@ -93,6 +93,18 @@ int mrrr_eig_shard(mrrr_t h, const double *d, const double *e, int64_t n, int64_
                    double *W_local, double *Z_local, int64_t ldz, int64_t ncols_cap, int64_t *jlo,
                    int64_t *jhi);
 
+/* Host-only helper (no GPU needed): the ownership rule of mrrr_eig_shard (north_star
+ * "a cluster straddling a shard boundary is owned by the GPU holding its first index").  gstart[j-1]
+ * (host array, n entries, caller-owned) is 1 iff index j starts a root group (singleton or cluster,
+ * P:3272-3292), 0 if j continues the group of j-1; only entries sl..jmax are read.  [sl, su] is the
+ * rank's shard (1-based), jmax >= su the last classified index.  On return [*jlo, *jhi] is the owned
+ * range: from the first group start in [sl, su] through the end of the last group starting there
+ * (which may extend past su up to jmax); *jlo = su + 1, *jhi = su if no group starts in the shard.
+ * Errors: -1 gstart NULL, -2 n < 1, -3 sl out of [1, n], -4 su out of [sl, n], -5 jmax out of [su, n],
+ * -6/-7 jlo/jhi NULL. */
+int mrrr_shard_owner(const int32_t *gstart, int64_t n, int64_t sl, int64_t su, int64_t jmax, int64_t *jlo,
+                     int64_t *jhi);
+
 /* Statistics of the last call (int64 each, nstats <= MRRR_NSTATS):
  * 0 d_max, 1 #clusters processed, 2 largest cluster, 3 uncertified shifts
  * (robustness failures), 4 shift attempts, 5 RQI iterations,

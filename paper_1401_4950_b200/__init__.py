@@ -64,6 +64,8 @@ def load() -> C.CDLL:
         L.mrrr_get_stats.argtypes = [vp, vp, C.c_int32]
         L.mrrr_get_times.argtypes = [vp, vp, C.c_int32]
         L.mrrr_get_diag.argtypes = [vp, C.POINTER(_Diag)]
+        L.mrrr_shard_owner.argtypes = [vp, i64, i64, i64, i64, C.POINTER(i64), C.POINTER(i64)]
+        L.mrrr_shard_owner.restype = C.c_int
         L.mrrr_selftest.argtypes = [C.c_int, i64, C.c_uint64, C.POINTER(i64)]
         L.mrrr_selftest.restype = C.c_int
         L.mrrr_strerror.argtypes = [C.c_int]
@@ -77,7 +79,7 @@ def load() -> C.CDLL:
 
 
 EXPORTED = ["mrrr_init", "mrrr_eig", "mrrr_eig_host", "mrrr_eig_shard", "mrrr_get_stats", "mrrr_get_diag",
-            "mrrr_get_times", "mrrr_selftest", "mrrr_strerror", "mrrr_destroy"]
+            "mrrr_get_times", "mrrr_selftest", "mrrr_shard_owner", "mrrr_strerror", "mrrr_destroy"]
 
 
 def selftest(which: int, n: int, seed: int = 1) -> int:

@@ -535,6 +535,28 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
   }
 }
 
+// ownership rule of a multi-GPU shard: the rank owns every group that STARTS in
+// [sl, su]; the last such group may extend past su (through jmax, the end of the computed range).
+// gstart[j-1] = 1 iff index j starts a root group.  Empty ownership: jlo = su + 1, jhi = su.
+static void shard_owner(const int32_t *gstart, long long n, long long sl, long long su, long long jmax,
+                        long long *jlo_out, long long *jhi_out) {
+  long long jlo = -1, jhi;
+  for (long long j = sl; j <= su; j++)
+    if (gstart[j - 1] == 1) { jlo = j; break; }
+  if (jlo > 0) {
+    long long last = jlo;
+    for (long long j = sl; j <= su; j++)
+      if (gstart[j - 1] == 1) last = j;
+    jhi = last;
+    while (jhi < jmax && jhi < n && gstart[jhi] == 0) jhi++;
+  } else {
+    jlo = su + 1;
+    jhi = su;
+  }
+  *jlo_out = jlo;
+  *jhi_out = jhi;
+}
+
 int solve(mrrr_t h, const double *d, const double *e, long long n, long long il, long long iu, double *W, double *Z,
           long long ldz, long long shard_lo, long long shard_hi, long long *jlo_out, long long *jhi_out,
           long long ncols_cap) {
@@ -720,18 +742,8 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
     std::vector<int> gs(n);
     CK(cudaMemcpyAsync(gs.data(), h->gstart.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    long long jlo = -1, jhi = -2;
-    for (long long j = shard_lo; j <= shard_hi; j++)
-      if (gs[j - 1] == 1) { jlo = j; break; }
-    if (jlo > 0) {
-      long long last = jlo;
-      for (long long j = shard_lo; j <= shard_hi; j++)
-        if (gs[j - 1] == 1) last = j;
-      jhi = last;
-      while (jhi < cab[1] && gs[jhi] == 0) jhi++;
-    } else {
-      jlo = shard_hi + 1; jhi = shard_hi;
-    }
+    long long jlo = 0, jhi = 0;
+    shard_owner(gs.data(), n, shard_lo, shard_hi, cab[1], &jlo, &jhi);
     *jlo_out = jlo;
     *jhi_out = jhi;
     long long own = jhi - jlo + 1;
@@ -894,6 +906,22 @@ int mrrr_eig_shard(mrrr_t h, const double *d, const double *e, int64_t n, int64_
   } catch (Err &er) {
     return er.code;
   }
+}
+
+int mrrr_shard_owner(const int32_t *gstart, int64_t n, int64_t sl, int64_t su, int64_t jmax, int64_t *jlo,
+                     int64_t *jhi) {
+  if (!gstart) return -1;
+  if (n < 1) return -2;
+  if (sl < 1 || sl > n) return -3;
+  if (su < sl || su > n) return -4;
+  if (jmax < su || jmax > n) return -5;
+  if (!jlo) return -6;
+  if (!jhi) return -7;
+  long long lo = 0, hi = 0;
+  shard_owner(gstart, n, sl, su, jmax, &lo, &hi);
+  *jlo = lo;
+  *jhi = hi;
+  return 0;
 }
 
 int mrrr_eig_host(mrrr_t h, const double *d, const double *e, int64_t n, int64_t il, int64_t iu, double *W,

@@ -186,9 +186,11 @@ def test_shards_reproduce_full_solve(torch_cuda):
     # P virtual ranks run one after another on this GPU: owned ranges partition [1, n] and every
     # column equals the single-GPU solve bit for bit (SURVEY §8(e) ownership by first index)
     import paper_1401_4950_b200 as m
+    from paper_1401_4950_b200 import dist as pd
     for d, e in (mi.random_tridiag(2000, 31, -1.0), mi.wilkinson(400)):
         n = d.size
         g = gpu_solve(torch_cuda, d, e, diag=False)
+        gst = oracle.mrrr(d, e).root_gstart  # group starts: the ownership rule's input
         dt = torch_cuda.from_numpy(d).cuda()
         et = torch_cuda.from_numpy(e).cuda()
         for P in (2, 3, 4):
@@ -196,8 +198,10 @@ def test_shards_reproduce_full_solve(torch_cuda):
             covered = []
             for rank in range(P):
                 s = m.Solver()
-                sl, su = 1 + rank * per, min((rank + 1) * per, n)
+                sl, su = pd.shard_range(1, n, P, rank)
+                assert (sl, su) == (1 + rank * per, min((rank + 1) * per, n))
                 jlo, jhi, W, Z = s.eig_shard(dt, et, sl, su)
+                assert (jlo, jhi) == pd.owned_range(gst, sl, su, n)
                 if jhi >= jlo:
                     covered.extend(range(jlo, jhi + 1))
                     assert np.array_equal(W.cpu().numpy(), g["W"][jlo - 1:jhi])

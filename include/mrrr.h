@@ -146,8 +146,9 @@ int mrrr_get_diag(mrrr_t h, mrrr_diag *g);
 int mrrr_get_times(mrrr_t h, double *ms, int32_t nt);
 
 /* Built-in self tests (run on the current device).  which = 1: the NegCount division fast path
- * (csrc/kernels.cuh div_ieee) against the IEEE __ddiv_rn on n seeded operand pairs (random bit
- * patterns incl. subnormals/inf/nan, and the O(1) NegCount regime); *bad = #bitwise mismatches. */
+ * (csrc/kernels.cuh div_ieee, and div_fast_nocheck wherever its range test passes) against the IEEE
+ * __ddiv_rn on n seeded operand pairs (random bit patterns incl. subnormals/inf/nan, near-midpoint
+ * quotients, and the O(1) NegCount regime); *bad = #bitwise mismatches. */
 int mrrr_selftest(int which, int64_t n, uint64_t seed, int64_t *bad);
 
 const char *mrrr_strerror(int code);

@@ -85,9 +85,10 @@ struct mrrr_ctx {
   int root_side = 0;
   uint32_t flags = 0;
   long long ws_limit = 0;
-  long long target_chains = 131072;
+  long long target_chains = 65536;  // k-section budget per round (C2 sweep: 65536 -> 3 levels per round)
   int mmax = 16;
   int chains_per_thread = 1;
+  bool neg_tma = true;  // x-NegCount with TMA-staged representation tiles (k_negcount_tma)
   bool rqi_pair = true;
   bool l2_persist = true;
   long long l2_max_window = 0;
@@ -227,8 +228,17 @@ __global__ void k_selftest_div(long long n, uint64_t seed, unsigned long long *b
     if ((i & 255) == 3) b = -0.0;
     if ((i & 255) == 5) { a = INFINITY; b = -INFINITY; }
   }
+  if (i % 4 == 1) {  // near-midpoint quotients: a = RN(b * (m +- half an ulp)) +- a few ulps
+    b = __longlong_as_double((long long)((z2 & 0x000FFFFFFFFFFFFFull) | (0x3FFull << 52)));
+    double mq = __longlong_as_double((long long)((z1 & 0x000FFFFFFFFFFFFFull) | (0x3FFull << 52)));
+    mq = __dadd_rn(mq, ((z1 >> 7) & 1) ? 0x1p-53 : -0x1p-53);
+    a = __longlong_as_double(__double_as_longlong(__dmul_rn(b, mq)) + (long long)((z2 >> 5) % 5) - 2);
+  }
   double q1 = div_ieee(a, b), q2 = __ddiv_rn(a, b);
   bool same = (__double_as_longlong(q1) == __double_as_longlong(q2)) || (isnan(q1) && isnan(q2));
+  double q3 = div_fast_nocheck(a, b);  // the NegCount / root variant: must agree whenever its range test passes
+  if (div_range_ok(a, b, q3) && __double_as_longlong(q3) != __double_as_longlong(q2) && !(isnan(q3) && isnan(q2)))
+    same = false;
   if (!same) atomicAdd(bad, 1ull);
 }
 
@@ -241,6 +251,13 @@ void launch_check(mrrr_t h) {
 template <bool Y>
 void launch_negcount(mrrr_t h, const Node *nodes, int nnode, int m, int nex) {
   long long tot = (long long)nnode * ((1LL << m) - 1) + nex;
+  if (!Y && h->neg_tma) {
+    k_negcount_tma<<<nblocks_for(tot, 128), 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
+        nodes, nnode, m, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mx.as<double2>(),
+        h->counts.as<int>(), h->excounts.as<int>());
+    launch_check(h);
+    return;
+  }
   int ch = Y ? 1 : h->chains_per_thread;
   long long thr = (tot + ch - 1) / ch;
   const ExplicitChain *ex = h->ex.as<ExplicitChain>();
@@ -852,6 +869,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_TARGET_CHAINS")) h->target_chains = atoll(s);
     if (const char *s = getenv("MRRR_MMAX")) h->mmax = atoi(s);
     if (const char *s = getenv("MRRR_CH")) h->chains_per_thread = std::max(1, std::min(4, atoi(s)));
+    if (const char *s = getenv("MRRR_NEGTMA")) h->neg_tma = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;
     if (const char *s = getenv("MRRR_L2PIN")) h->l2_persist = atoi(s) != 0;
     {

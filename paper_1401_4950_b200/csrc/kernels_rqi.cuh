@@ -225,10 +225,192 @@ __device__ bool getvec_pair_t(const YElt *__restrict__ y, int nb, dd lam, int r,
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Fast Getvec on the RQI form (QElt, kernels_vec.cuh): the pivot recurrence
+//   den' = (g - lam) - c2 / den
+// with the dd quotient formed from the fp64 reciprocal pair of den.hi (MUFU seed + Newton), so the
+// dependent chain per step is: reciprocal of den.hi, one quotient residual, one dd subtraction.
+// F lane: den = d+(i), stores (iteration 1) d+(i) and S_i; B lane: den = omega(i+1), stores
+// c2(i)/omega(i+1) and T_i; gamma_i = d+(i) - c2(i)/omega(i+1).  Any pivot outside [2^-1000, 2^1000]
+// or a non-finite state sends the pair to the careful pass (getvec_pair_t<true>).
+// ---------------------------------------------------------------------------
+struct QV {
+  dd c2, dl, g;
+};
+struct Q3 {
+  double2 c2, dl, g;
+};
+__device__ __forceinline__ Q3 ldq(const QElt *__restrict__ q, int i, int og) {
+  const double2 *p = reinterpret_cast<const double2 *>(q + i);
+  Q3 v;
+  v.c2 = __ldg(p);
+  v.dl = __ldg(p + 1);
+  v.g = __ldg(p + og);
+  return v;
+}
+// nu / den from the reciprocal pair (r1 ~ 1/den.hi, r2 refined): unnormalized (hi, lo)
+__device__ __forceinline__ dd qdiv(dd nu, dd den, double r1, double r2) {
+  const double h = __dmul_rn(nu.hi, r1);
+  double t = __fma_rn(-h, den.hi, nu.hi);
+  t = __dadd_rn(t, nu.lo);
+  t = __fma_rn(-h, den.lo, t);
+  return dd_make(h, __dmul_rn(t, r2));
+}
+__device__ __forceinline__ void q_step(dd den, const Q3 &e, dd lam, dd acc, dd &P, dd &out, dd &dn, dd &accn,
+                                       bool &ok) {
+  const double b = den.hi;
+  const double r = rcp_seed_dd(b);
+  double ee = __fma_rn(-b, r, 1.0);
+  ee = __fma_rn(ee, ee, ee);
+  const double r1 = __fma_rn(r, ee, r);
+  const double e2 = __fma_rn(-b, r1, 1.0);
+  const double r2 = __fma_rn(r1, e2, r1);
+  P = qdiv(D2(e.c2), den, r1, r2);
+  const dd o = qdiv(D2(e.dl), den, r1, r2);
+  out = fast_two_sum(o.hi, o.lo);
+  const dd eg = dd_sub_nf(D2(e.g), lam);
+  dn = dd_sub_nf(eg, P);
+  accn = dd_mul_nf(dd_mul_nf(out, out), dd_add_d_nf(acc, 1.0));
+  ok &= (fabs(b) > 0x1p-1000) && (fabs(b) < 0x1p1000);
+}
+
+template <int MODE>
+__device__ __forceinline__ void run_phase_q(const QElt *__restrict__ q, int last, int k0, int k1, bool isB, int og,
+                                            dd lam, dd *P0, dd *P1, dd *P2, long long S, dd &den, dd &acc, int &cnt,
+                                            Cand &cd, dd &tr, bool &ok) {
+  constexpr int PD = MRRR_RQI_PD;
+  if (k0 >= k1) return;
+#define GIX(k) (isB ? (last - 1 - (k)) : (k))
+  Q3 er[PD];
+  dd pq[PD], ps[PD];
+#pragma unroll
+  for (int u = 0; u < PD; u++) {
+    const int kk = min(k0 + u, k1 - 1);
+    er[u] = ldq(q, GIX(kk), og);
+    if (MODE == PH_COMBINE) {
+      pq[u] = ldw(P0, (long long)GIX(kk) * S);
+      ps[u] = ldw(P1, (long long)GIX(kk) * S);
+    }
+  }
+  for (int kb = k0; kb < k1; kb += PD) {
+#pragma unroll
+    for (int u = 0; u < PD; u++) {
+      const int k = kb + u;
+      if (k < k1) {
+        const Q3 e0 = er[u];
+        const int kn = min(k + PD, k1 - 1);
+        er[u] = ldq(q, GIX(kn), og);
+        dd other, ost;
+        if (MODE == PH_COMBINE) {
+          other = pq[u];
+          ost = ps[u];
+          pq[u] = ldw(P0, (long long)GIX(kn) * S);
+          ps[u] = ldw(P1, (long long)GIX(kn) * S);
+        }
+        const int i = GIX(k);
+        dd P, out, dn, accn;
+        q_step(den, e0, lam, acc, P, out, dn, accn, ok);
+        if (MODE == PH_STORE || MODE == PH_COMBINE) {
+          const dd mine = isB ? fast_two_sum(P.hi, P.lo) : den;
+          const dd myst = isB ? accn : acc;
+          if (MODE == PH_STORE) {
+            stw(P0, (long long)i * S, mine);
+            stw(P1, (long long)i * S, myst);
+          } else {
+            const dd gam = isB ? dd_sub_nf(other, mine) : dd_sub_nf(mine, other);
+            cand_take(cd, gam, dd_add_nf(myst, ost), i, isB);
+          }
+        } else {
+          if (isB && k == k1 - 1) tr = fast_two_sum(P.hi, P.lo);  // B's last row is r: c2(r)/omega(r+1)
+          stw(P2, i, out);
+        }
+        cnt += dd_sb(den);
+        den = dn;
+        acc = accn;
+      }
+    }
+  }
+#undef GIX
+}
+
+// one Getvec of the pair on the RQI form; returns false (both lanes) if the careful pass is needed
+__device__ bool getvec_pair_q(const QElt *__restrict__ q, int nb, dd lam, int r, bool isB, dd *P0, dd *P1, dd *P2,
+                              long long S, GV &g) {
+  const unsigned pm = pair_mask();
+  const int last = nb - 1;
+  const bool it1 = r < 0;
+  const int og = isB ? 3 : 2;
+  // F: d+(0) = d(0) - lam = gb(0) - lam;  B: omega(n-1) = g(n-2) - lam = gb(n-1) - lam
+  const int i0 = isB ? last : 0;
+  dd den = dd_sub_nf(dd_make(__ldg(&q[i0].gb_hi), __ldg(&q[i0].gb_lo)), lam);
+  dd acc = dd_from(0.0), tr = dd_from(0.0);
+  int cnt = 0;
+  bool ok = true;
+  Cand cd;
+  cd.k = -1; cd.best = dd_from(INFINITY); cd.gam = dd_from(0.0); cd.st = dd_from(0.0);
+  if (it1) {
+    const int kA = last / 2;
+    run_phase_q<PH_STORE>(q, last, 0, kA, isB, og, lam, P0, P1, P2, S, den, acc, cnt, cd, tr, ok);
+    if (last & 1) {
+      const int i = kA;
+      const Q3 e = ldq(q, i, og);
+      dd P, out, dn, accn;
+      q_step(den, e, lam, acc, P, out, dn, accn, ok);
+      const dd mine = isB ? fast_two_sum(P.hi, P.lo) : den;
+      const dd myst = isB ? accn : acc;
+      const dd om = shfl_dd(mine, 1), ost = shfl_dd(myst, 1);
+      if (!isB) cand_take(cd, dd_sub_nf(mine, om), dd_add_nf(myst, ost), i, false);
+      cnt += dd_sb(den);
+      den = dn;
+      acc = accn;
+    }
+    __syncwarp(pm);
+    run_phase_q<PH_COMBINE>(q, last, kA + (last & 1), last, isB, og, lam, P0, P1, P2, S, den, acc, cnt, cd, tr, ok);
+  } else {
+    const int nsteps = isB ? last - r : r;
+    run_phase_q<PH_FIXED>(q, last, 0, nsteps, isB, og, lam, P0, P1, P2, S, den, acc, cnt, cd, tr, ok);
+  }
+  ok = ok && isfinite(den.hi) && isfinite(den.lo) && isfinite(acc.hi) && isfinite(acc.lo);
+  ok = __shfl_xor_sync(pm, (int)ok, 1) && ok;
+  if (!ok) return false;
+  __syncwarp(pm);
+  if (it1) {
+    if (!isB) {  // F: den = d+(n-1) = gamma_n closes the full NegCount
+      cnt += dd_sb(den);
+      cand_take(cd, den, acc, last, false);
+    }
+    dd ob = shfl_dd(cd.best, 1), og_ = shfl_dd(cd.gam, 1), ost = shfl_dd(cd.st, 1);
+    int ok_ = __shfl_xor_sync(pm, cd.k, 1);
+    if (!isB) {  // B's candidates are the lower indices: they win ties
+      if (ok_ >= 0 && (cd.k < 0 || !dd_lt(cd.best, ob))) { cd.best = ob; cd.gam = og_; cd.st = ost; cd.k = ok_; }
+    }
+    g.r = shfl_i_from(cd.k, lane_F());
+    g.gamma = shfl_dd_from(cd.gam, lane_F());
+    g.zz = dd_add_d(shfl_dd_from(cd.st, lane_F()), 1.0);
+    g.c = shfl_i_from(cnt, lane_F());
+  } else {
+    const dd dr = shfl_dd_from(den, lane_F());
+    const dd t_r = shfl_dd_from(tr, lane_B());
+    const int cF = shfl_i_from(cnt, lane_F());
+    const int cB = shfl_i_from(cnt, lane_B());
+    const dd gamma = (r == last) ? dr : dd_sub(dr, t_r);
+    g.r = r;
+    g.gamma = gamma;
+    g.c = cF + cB + dd_sb(gamma);
+    const dd other = shfl_dd(acc, 1);
+    g.zz = dd_add_d(dd_add(acc, other), 1.0);
+  }
+  return true;
+}
+
 // returns true if the careful (IEEE special value) pass had to run
-__device__ __forceinline__ bool getvec_pair_any(const YElt *__restrict__ y, int nb, dd lam, int r, bool isB, dd *P0,
-                                                dd *P1, dd *P2, long long S, GV &g) {
-  if (getvec_pair_t<false>(y, nb, lam, r, isB, P0, P1, P2, S, g)) return false;
+__device__ __forceinline__ bool getvec_pair_any(const YElt *__restrict__ y, const QElt *__restrict__ qy, int nb, dd lam,
+                                                int r, bool isB, dd *P0, dd *P1, dd *P2, long long S, GV &g) {
+  if (qy) {
+    if (getvec_pair_q(qy, nb, lam, r, isB, P0, P1, P2, S, g)) return false;
+  } else if (getvec_pair_t<false>(y, nb, lam, r, isB, P0, P1, P2, S, g)) {
+    return false;
+  }
   getvec_pair_t<true>(y, nb, lam, r, isB, P0, P1, P2, S, g);
   return true;
 }
@@ -293,7 +475,8 @@ __global__ void __launch_bounds__(256) k_zwrite(const Singleton *__restrict__ sg
 }
 
 __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
-                                             const YElt *__restrict__ my, dd *ws, long long S, long long nbmax,
+                                             const YElt *__restrict__ my, const QElt *__restrict__ mq, dd *ws,
+                                             long long S, long long nbmax,
                                              double *W, ZMeta *zmeta, int *diag_depth, double *fin_lo,
                                              double *fin_hi, long long *stats) {
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
@@ -304,6 +487,7 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
   const RepDesc R = reps[s.rep];
   const int nb = R.nb, j = s.j;
   const YElt *y = my + R.off;
+  const QElt *qy = mq ? mq + R.off : nullptr;
   const long long plane = nbmax * S;
   dd *P0 = ws + pid, *P1 = ws + plane + pid, *P2 = ws + 2 * plane + (long long)pid * nbmax;
   double mid = bis_mid(s.lo, s.hi);
@@ -320,13 +504,13 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
   for (int it = 0; it < MAX_RQI && !accepted; it++) {
     if (r < 0) { qd += 2 * (nb - 1); qdg += nb - 1; } else qd += nb - 1;
     lu_valid = r >= 0;
-    careful = getvec_pair_any(y, nb, lam, r, isB, P0, P1, P2, S, g);
+    careful = getvec_pair_any(y, qy, nb, lam, r, isB, P0, P1, P2, S, g);
     iters++;
     r = g.r;
     if (r < 0) break;
     zz = g.zz;
     if (!isfinite(zz.hi)) {  // closed form broke down (overflow / zero pivot): explicit z solve (A-25)
-      if (!lu_valid) { careful = getvec_pair_any(y, nb, lam, r, isB, P0, P1, P2, S, g); lu_valid = true; qd += nb - 1; }
+      if (!lu_valid) { careful = getvec_pair_any(y, qy, nb, lam, r, isB, P0, P1, P2, S, g); lu_valid = true; qd += nb - 1; }
       zs += nb - 1;
       if (!isB) zz = zsolve(y, nb, r, P2, P2, 1, dd_from(0.0), nullptr);
       zz = shfl_dd_from(zz, lane_F());
@@ -346,7 +530,7 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
     if (active && !isB) atomicAdd((unsigned long long *)&stats[ST_RQI_FALLBACK], 1ull);
     lam = bisect_y_full(y, nb, j, blo, bhi);
     lu_valid = r >= 0;
-    careful = getvec_pair_any(y, nb, lam, r, isB, P0, P1, P2, S, g);
+    careful = getvec_pair_any(y, qy, nb, lam, r, isB, P0, P1, P2, S, g);
     if (r < 0) qdg += nb - 1;
     qd += (r < 0) ? 2 * (nb - 1) : nb - 1;
     iters++;
@@ -354,7 +538,7 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
     zz = g.zz;
   }
   if (!lu_valid) {  // accepted on a twist-search pass: one r-twisted pass to store l+ / u-
-    careful = getvec_pair_any(y, nb, lam, r, isB, P0, P1, P2, S, g);
+    careful = getvec_pair_any(y, qy, nb, lam, r, isB, P0, P1, P2, S, g);
     qd += nb - 1;
   }
   if (!isfinite(zz.hi) || zz.hi == 0.0) {

@@ -9,6 +9,40 @@ __device__ __forceinline__ dd ld_d(const YElt *y) { return dd_make(__ldg(&y->d_h
 __device__ __forceinline__ dd ld_dl(const YElt *y) { return dd_make(__ldg(&y->dl_hi), __ldg(&y->dl_lo)); }
 __device__ __forceinline__ dd ld_dll(const YElt *y) { return dd_make(__ldg(&y->dll_hi), __ldg(&y->dll_lo)); }
 
+// RQI form of a representation (derived once per representation, y-arithmetic): with
+//   g(i) = d(i+1) + dll(i),  c2(i) = dl(i)^2 = d(i) dll(i),
+// the stationary and progressive transforms become one recurrence on the pivots,
+//   dstqds:  d+(i+1)  = (g(i)   - lam) - c2(i) / d+(i),      d+(0)     = d(0) - lam
+//   dqds  :  omega(i) = (g(i-1) - lam) - c2(i) / omega(i+1), omega(n-1) = g(n-2) - lam, g(-1) = d(0)
+// (Alg. dstqds: s(i+1) = s(i) dll(i) / d+(i) - lam = dll(i) - c2(i)/d+(i) - lam; Alg. dqds
+// P:3366-3393 with A-1: p(i) = p(i+1) d(i) / omega(i+1) - lam = d(i) - c2(i)/omega(i+1) - lam).  The
+// dependent chain per step is one dd division and one dd subtraction; l+(i) = dl(i)/d+(i),
+// u-(i) = dl(i)/omega(i+1) and the twist quantity gamma_k = s(k) + t(k) = d+(k) - c2(k)/omega(k+1)
+// come off the chain.  Element i holds c2(i), dl(i), gf = g(i), gb = g(i-1).
+struct QElt {
+  double c2_hi, c2_lo, dl_hi, dl_lo, gf_hi, gf_lo, gb_hi, gb_lo;
+};
+
+__global__ void k_build_q(const RepDesc *__restrict__ reps, const int *__restrict__ rlist, int r0, int nr,
+                          const YElt *__restrict__ my, QElt *mq) {
+  const int rid = rlist ? rlist[blockIdx.x] : r0 + (int)blockIdx.x;
+  if ((int)blockIdx.x >= nr) return;
+  const RepDesc R = reps[rid];
+  if (R.nb < 2) return;
+  const YElt *y = my + R.off;
+  QElt *q = mq + R.off;
+  for (int i = threadIdx.x; i < R.nb; i += blockDim.x) {
+    dd d = ld_d(y + i), dl = ld_dl(y + i), dll = ld_dll(y + i);
+    dd c2 = dd_mul(dl, dl);
+    dd gf = (i < R.nb - 1) ? dd_add(ld_d(y + i + 1), dll) : dd_from(0.0);
+    dd gb = (i > 0) ? dd_add(d, ld_dll(y + i - 1)) : d;
+    QElt e;
+    e.c2_hi = c2.hi; e.c2_lo = c2.lo; e.dl_hi = dl.hi; e.dl_lo = dl.lo;
+    e.gf_hi = gf.hi; e.gf_lo = gf.lo; e.gb_hi = gb.hi; e.gb_lo = gb.lo;
+    q[i] = e;
+  }
+}
+
 // one qd step shared by dstqds (Alg. dstqds) and dqds (Alg. dqds, A-1/A-2):
 //   den = x + a; q = (|x| = inf and |den| = inf) ? 1 : x / den; out = b / den; xn = q * c - lam
 // dstqds: x = s(i), a = d(i), b = dl(i), c = dll(i)  -> den = d+(i), out = l+(i), xn = s(i+1)

@@ -88,13 +88,14 @@ struct mrrr_ctx {
   long long target_chains = 65536;  // k-section budget per round (C2 sweep: 65536 -> 3 levels per round)
   int mmax = 16;
   int chains_per_thread = 1;
-  bool neg_tma = true;  // x-NegCount with TMA-staged representation tiles (k_negcount_tma)
+  bool neg_tma = true;
+  bool rqi_q = true;    // singleton RQI on the pivot-recurrence form (QElt, k_rqi2 fast pass)  // x-NegCount with TMA-staged representation tiles (k_negcount_tma)
   bool rqi_pair = true;
   bool l2_persist = true;
   long long l2_max_window = 0;
 
   // buffers
-  Buf starts, scal, binfo, bside, blist, cab, mx, my, lscratch, reps, rlo, rhi, colmap, gstart;
+  Buf starts, scal, binfo, bside, blist, cab, mx, my, mq, lscratch, reps, rlo, rhi, colmap, gstart;
   Buf nodesA, nodesB, counts, ex, excounts, exmap, bnA, bnB, sing, clusA, clusB, ss, gval, valid, cseg, bnoff,
       ipool_lo, ipool_hi, yref_lo, yref_hi, wsA, wsB, stats, cnt, ddepth, dgf, dgl, dflo, dfhi, hd, he, hW, hZ, zmeta;
   int *h_cnt = nullptr;  // pinned counters
@@ -361,8 +362,9 @@ void l2_pin_reps(mrrr_t h, bool on) {
   cudaStreamAttrValue v;
   memset(&v, 0, sizeof(v));
   if (on) {
-    size_t bytes = std::min<size_t>(h->my.cap, (size_t)h->l2_max_window);
-    v.accessPolicyWindow.base_ptr = h->my.p;
+    Buf &hot = h->rqi_q ? h->mq : h->my;  // the representation form the RQI lanes stream
+    size_t bytes = std::min<size_t>(hot.cap, (size_t)h->l2_max_window);
+    v.accessPolicyWindow.base_ptr = hot.p;
     v.accessPolicyWindow.num_bytes = bytes;
     v.accessPolicyWindow.hitRatio = 1.0f;
     v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
@@ -395,8 +397,8 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
     if (pair) {
       CK(h->zmeta.ensure(sizeof(ZMeta) * stride));
       k_rqi2<<<nblocks_for(2 * nb, 64), 64, 0, h->stream>>>(
-          h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>(), stride,
-          nbmax, W, h->zmeta.as<ZMeta>(), diag ? h->ddepth.as<int>() : nullptr,
+          h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(),
+          h->rqi_q ? h->mq.as<QElt>() : nullptr, h->wsA.as<dd>(), stride, nbmax, W, h->zmeta.as<ZMeta>(), diag ? h->ddepth.as<int>() : nullptr,
           diag ? h->dflo.as<double>() : nullptr, diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>());
       launch_check(h);
       k_zwrite<<<nblocks_for(32 * nb, 256), 256, 0, h->stream>>>(
@@ -451,6 +453,8 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
                        sizeof(double2) * (size_t)poolbase, h->stream));
     CK(h->my.grow_keep(sizeof(YElt) * (size_t)(poolbase + (long long)nc * nbmax), sizeof(YElt) * (size_t)poolbase,
                        h->stream));
+    CK(h->mq.grow_keep(sizeof(QElt) * (size_t)(poolbase + (long long)nc * nbmax), sizeof(QElt) * (size_t)poolbase,
+                       h->stream));
     long long stot = 0, btot = 0;
     for (int c = 0; c < nc; c++) { stot += hl[c0 + c].q - hl[c0 + c].p + 3; btot += hl[c0 + c].q - hl[c0 + c].p + 1; }
     CK(h->ipool_lo.grow_keep(sizeof(double) * (size_t)(ipool_top + stot), sizeof(double) * (size_t)ipool_top, h->stream));
@@ -497,6 +501,9 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
     k_clu_build<<<nblocks_for(nc, 64), 64, 0, h->stream>>>(cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(),
                                                            h->mx.as<double2>(), h->my.as<YElt>(), repbase, poolbase,
                                                            (int)nbmax);
+    launch_check(h);
+    k_build_q<<<nc, 256, 0, h->stream>>>(h->reps.as<RepDesc>(), nullptr, repbase, nc, h->my.as<YElt>(),
+                                         h->mq.as<QElt>());
     launch_check(h);
     // (e) child starts: segments and BNode offsets from the host copy
     std::vector<long long> seg(nc), bo(nc);
@@ -645,6 +652,7 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
   // pools: root reps at [0, n); children appended (sized by the workspace budget)
   CK(h->mx.ensure(sizeof(double2) * (n + 1)));
   CK(h->my.ensure(sizeof(YElt) * (n + 1)));
+  CK(h->mq.ensure(sizeof(QElt) * (n + 1)));
   CK(h->lscratch.ensure(sizeof(double) * 2 * n));
   CK(h->reps.ensure(sizeof(RepDesc) * (nblk + 1)));
   CK(h->rlo.ensure(sizeof(double) * n));
@@ -669,6 +677,9 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
     k_root<256><<<nbl, 256, 0, st>>>(d, e, n, h->starts.as<int>(), h->blist.as<int>(), h->bside.as<int>(), h->seed,
                                      h->binfo.as<double>(), h->mx.as<double2>(), h->my.as<YElt>(),
                                      h->lscratch.as<double>(), h->reps.as<RepDesc>());
+    launch_check(h);
+    k_build_q<<<nbl, 256, 0, st>>>(h->reps.as<RepDesc>(), h->blist.as<int>(), 0, nbl, h->my.as<YElt>(),
+                                   h->mq.as<QElt>());
     launch_check(h);
   }
   CK(cudaEventRecord(h->ev[1], st));
@@ -870,6 +881,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_MMAX")) h->mmax = atoi(s);
     if (const char *s = getenv("MRRR_CH")) h->chains_per_thread = std::max(1, std::min(4, atoi(s)));
     if (const char *s = getenv("MRRR_NEGTMA")) h->neg_tma = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_RQIQ")) h->rqi_q = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;
     if (const char *s = getenv("MRRR_L2PIN")) h->l2_persist = atoi(s) != 0;
     {
@@ -1057,7 +1069,7 @@ int mrrr_destroy(mrrr_t h) {
   if (!h) return 0;
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->stream);
-  Buf *bufs[] = {&h->starts, &h->scal, &h->binfo, &h->bside, &h->blist, &h->cab, &h->mx, &h->my, &h->lscratch,
+  Buf *bufs[] = {&h->starts, &h->scal, &h->binfo, &h->bside, &h->blist, &h->cab, &h->mx, &h->my, &h->mq, &h->lscratch,
                  &h->reps, &h->rlo, &h->rhi, &h->colmap, &h->gstart, &h->nodesA, &h->nodesB, &h->counts, &h->ex,
                  &h->excounts, &h->exmap, &h->bnA, &h->bnB, &h->sing, &h->clusA, &h->clusB, &h->ss, &h->gval,
                  &h->valid, &h->cseg, &h->bnoff, &h->ipool_lo, &h->ipool_hi, &h->yref_lo, &h->yref_hi, &h->wsA,

@@ -1,7 +1,8 @@
 #!/bin/bash
-# bench C2 under several bisection chain budgets (developer sweep)
-for tc in ${TCS:-24576 40960 65536 131072}; do
-  echo "target_chains=$tc"
-  MRRR_TARGET_CHAINS=$tc timeout 300 python bench.py --no-cpu-baseline --no-e2e --steps 3 --warmup 2 ${BENCH_ARGS} | python -c "
-import json,sys; l=json.loads(sys.stdin.read().strip().splitlines()[-1]); p=l['phases_ms']; print('  ms/step %.3f bis %.3f rqi %.3f root %.3f rounds %d negx %d' % (l['ms_per_step'], p['root_bisection'], p['singletons'], p['split_root'], l['stats']['rounds'], l['stats']['negcount_x']))"
+# bench a workload under several environment settings (developer sweep)
+#   VAR=MRRR_TARGET_CHAINS VALS="24576 65536" WL=C2 bash scripts/tune_round.sh
+VAR=${VAR:-MRRR_TARGET_CHAINS}
+for v in ${VALS:-24576 40960 65536 131072}; do
+  env $VAR=$v timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps ${STEPS:-3} --warmup 2 --workload ${WL:-C2} \
+    | python scripts/bench_summary.py "$WL $VAR=$v"
 done

@@ -114,7 +114,9 @@ int mrrr_shard_owner(const int32_t *gstart, int64_t n, int64_t sl, int64_t su, i
  * 16 dd qd steps in k_rqi (dstqds/dqds element steps), 17 of them with the twist quantity gamma_k,
  * 18 z-solve element steps (norm pass), 19 z-solve element steps that write Z,
  * 20 x-NegCount evaluations on the sequential bisection paths (shared-tree nodes; the algorithmic
- * count, without k-section speculation), 21 the same for y-NegCount. */
+ * count, without k-section speculation), 21 the same for y-NegCount, 22 RQI corrections rejected for an
+ * inertia-inconsistent sign, 23 RQI corrections rejected for leaving the bracket (both end in the bisection
+ * fallback). */
 #define MRRR_NSTATS 24
 int mrrr_get_stats(mrrr_t h, int64_t *stats, int32_t nstats);
 

@@ -274,68 +274,88 @@ __device__ __forceinline__ void q_step(dd den, const Q3 &e, dd lam, dd acc, dd &
   ok &= (fabs(b) > 0x1p-1000) && (fabs(b) < 0x1p1000);
 }
 
+// Per-lane prefetch ring in shared memory, filled by cp.async (no register cost): slot k holds the
+// representation row of step k (c2, dl, g) and, when combining, the other lane's stored half of
+// row k (P0, P1), issued MRRR_RQI_RING steps ahead of use.
+#ifndef MRRR_RQI_RING
+#define MRRR_RQI_RING 8
+#endif
+struct RingSlot {
+  double2 c2, dl, g, p0, p1;
+};
+__device__ __forceinline__ void cp16(void *sdst, const void *gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 template <int MODE>
 __device__ __forceinline__ void run_phase_q(const QElt *__restrict__ q, int last, int k0, int k1, bool isB, int og,
                                             dd lam, dd *P0, dd *P1, dd *P2, long long S, dd &den, dd &acc, int &cnt,
-                                            Cand &cd, dd &tr, bool &ok) {
-  constexpr int PD = MRRR_RQI_PD;
+                                            Cand &cd, dd &tr, bool &ok, RingSlot *ring) {
+  constexpr int R = MRRR_RQI_RING;
   if (k0 >= k1) return;
 #define GIX(k) (isB ? (last - 1 - (k)) : (k))
-  Q3 er[PD];
-  dd pq[PD], ps[PD];
-#pragma unroll
-  for (int u = 0; u < PD; u++) {
-    const int kk = min(k0 + u, k1 - 1);
-    er[u] = ldq(q, GIX(kk), og);
+  auto issue = [&](int k, int slot) {
+    const int i = GIX(min(k, k1 - 1));
+    const double2 *p = reinterpret_cast<const double2 *>(q + i);
+    cp16(&ring[slot].c2, p);
+    cp16(&ring[slot].dl, p + 1);
+    cp16(&ring[slot].g, p + og);
     if (MODE == PH_COMBINE) {
-      pq[u] = ldw(P0, (long long)GIX(kk) * S);
-      ps[u] = ldw(P1, (long long)GIX(kk) * S);
+      cp16(&ring[slot].p0, P0 + (long long)i * S);
+      cp16(&ring[slot].p1, P1 + (long long)i * S);
     }
-  }
-  for (int kb = k0; kb < k1; kb += PD) {
+    cp_commit();
+  };
 #pragma unroll
-    for (int u = 0; u < PD; u++) {
-      const int k = kb + u;
-      if (k < k1) {
-        const Q3 e0 = er[u];
-        const int kn = min(k + PD, k1 - 1);
-        er[u] = ldq(q, GIX(kn), og);
-        dd other, ost;
-        if (MODE == PH_COMBINE) {
-          other = pq[u];
-          ost = ps[u];
-          pq[u] = ldw(P0, (long long)GIX(kn) * S);
-          ps[u] = ldw(P1, (long long)GIX(kn) * S);
-        }
-        const int i = GIX(k);
-        dd P, out, dn, accn;
-        q_step(den, e0, lam, acc, P, out, dn, accn, ok);
-        if (MODE == PH_STORE || MODE == PH_COMBINE) {
-          const dd mine = isB ? fast_two_sum(P.hi, P.lo) : den;
-          const dd myst = isB ? accn : acc;
-          if (MODE == PH_STORE) {
-            stw(P0, (long long)i * S, mine);
-            stw(P1, (long long)i * S, myst);
-          } else {
-            const dd gam = isB ? dd_sub_nf(other, mine) : dd_sub_nf(mine, other);
-            cand_take(cd, gam, dd_add_nf(myst, ost), i, isB);
-          }
-        } else {
-          if (isB && k == k1 - 1) tr = fast_two_sum(P.hi, P.lo);  // B's last row is r: c2(r)/omega(r+1)
-          stw(P2, i, out);
-        }
-        cnt += dd_sb(den);
-        den = dn;
-        acc = accn;
-      }
+  for (int u = 0; u < R; u++) issue(k0 + u, u);
+  for (int k = k0; k < k1; k++) {
+    const int slot = (k - k0) & (R - 1);
+    cp_wait<R - 1>();
+    Q3 e0;
+    e0.c2 = ring[slot].c2;
+    e0.dl = ring[slot].dl;
+    e0.g = ring[slot].g;
+    dd other, ost;
+    if (MODE == PH_COMBINE) {
+      other = D2(ring[slot].p0);
+      ost = D2(ring[slot].p1);
     }
+    const int i = GIX(k);
+    dd P, out, dn, accn;
+    q_step(den, e0, lam, acc, P, out, dn, accn, ok);
+    if (MODE == PH_STORE || MODE == PH_COMBINE) {
+      const dd mine = isB ? fast_two_sum(P.hi, P.lo) : den;
+      const dd myst = isB ? accn : acc;
+      if (MODE == PH_STORE) {
+        stw(P0, (long long)i * S, mine);
+        stw(P1, (long long)i * S, myst);
+      } else {
+        const dd gam = isB ? dd_sub_nf(other, mine) : dd_sub_nf(mine, other);
+        cand_take(cd, gam, dd_add_nf(myst, ost), i, isB);
+      }
+    } else {
+      if (isB && k == k1 - 1) tr = fast_two_sum(P.hi, P.lo);  // B's last row is r: c2(r)/omega(r+1)
+      stw(P2, i, out);
+    }
+    cnt += dd_sb(den);
+    den = dn;
+    acc = accn;
+    issue(k + R, slot);  // the slot's values are consumed: refill it R steps ahead
   }
+  cp_wait<0>();
 #undef GIX
 }
 
 // one Getvec of the pair on the RQI form; returns false (both lanes) if the careful pass is needed
 __device__ bool getvec_pair_q(const QElt *__restrict__ q, int nb, dd lam, int r, bool isB, dd *P0, dd *P1, dd *P2,
                               long long S, GV &g) {
+  extern __shared__ __align__(16) unsigned char rqi_smem[];
+  RingSlot *ring = reinterpret_cast<RingSlot *>(rqi_smem) + threadIdx.x * MRRR_RQI_RING;
   const unsigned pm = pair_mask();
   const int last = nb - 1;
   const bool it1 = r < 0;
@@ -350,7 +370,7 @@ __device__ bool getvec_pair_q(const QElt *__restrict__ q, int nb, dd lam, int r,
   cd.k = -1; cd.best = dd_from(INFINITY); cd.gam = dd_from(0.0); cd.st = dd_from(0.0);
   if (it1) {
     const int kA = last / 2;
-    run_phase_q<PH_STORE>(q, last, 0, kA, isB, og, lam, P0, P1, P2, S, den, acc, cnt, cd, tr, ok);
+    run_phase_q<PH_STORE>(q, last, 0, kA, isB, og, lam, P0, P1, P2, S, den, acc, cnt, cd, tr, ok, ring);
     if (last & 1) {
       const int i = kA;
       const Q3 e = ldq(q, i, og);
@@ -365,10 +385,10 @@ __device__ bool getvec_pair_q(const QElt *__restrict__ q, int nb, dd lam, int r,
       acc = accn;
     }
     __syncwarp(pm);
-    run_phase_q<PH_COMBINE>(q, last, kA + (last & 1), last, isB, og, lam, P0, P1, P2, S, den, acc, cnt, cd, tr, ok);
+    run_phase_q<PH_COMBINE>(q, last, kA + (last & 1), last, isB, og, lam, P0, P1, P2, S, den, acc, cnt, cd, tr, ok, ring);
   } else {
     const int nsteps = isB ? last - r : r;
-    run_phase_q<PH_FIXED>(q, last, 0, nsteps, isB, og, lam, P0, P1, P2, S, den, acc, cnt, cd, tr, ok);
+    run_phase_q<PH_FIXED>(q, last, 0, nsteps, isB, og, lam, P0, P1, P2, S, den, acc, cnt, cd, tr, ok, ring);
   }
   ok = ok && isfinite(den.hi) && isfinite(den.lo) && isfinite(acc.hi) && isfinite(acc.lo);
   ok = __shfl_xor_sync(pm, (int)ok, 1) && ok;
@@ -406,11 +426,7 @@ __device__ bool getvec_pair_q(const QElt *__restrict__ q, int nb, dd lam, int r,
 // returns true if the careful (IEEE special value) pass had to run
 __device__ __forceinline__ bool getvec_pair_any(const YElt *__restrict__ y, const QElt *__restrict__ qy, int nb, dd lam,
                                                 int r, bool isB, dd *P0, dd *P1, dd *P2, long long S, GV &g) {
-  if (qy) {
-    if (getvec_pair_q(qy, nb, lam, r, isB, P0, P1, P2, S, g)) return false;
-  } else if (getvec_pair_t<false>(y, nb, lam, r, isB, P0, P1, P2, S, g)) {
-    return false;
-  }
+  if (getvec_pair_q(qy, nb, lam, r, isB, P0, P1, P2, S, g)) return false;
   getvec_pair_t<true>(y, nb, lam, r, isB, P0, P1, P2, S, g);
   return true;
 }
@@ -487,7 +503,7 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
   const RepDesc R = reps[s.rep];
   const int nb = R.nb, j = s.j;
   const YElt *y = my + R.off;
-  const QElt *qy = mq ? mq + R.off : nullptr;
+  const QElt *qy = mq + R.off;
   const long long plane = nbmax * S;
   dd *P0 = ws + pid, *P1 = ws + plane + pid, *P2 = ws + 2 * plane + (long long)pid * nbmax;
   double mid = bis_mid(s.lo, s.hi);
@@ -522,13 +538,22 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
     if (resid.hi <= thr1 || dd_lt(dd_abs(rqc), dd_mul_d(dd_abs(lam), 4.0 * EPS_Y))) { accepted = true; break; }
     if (g.c < j) blo = lam; else bhi = lam;
     dd nl = dd_add(lam, rqc);
-    bool ok = ((g.c < j) ? (rqc.hi > 0.0) : (rqc.hi < 0.0)) && dd_lt(blo, nl) && dd_lt(nl, bhi);
+    const bool sgn = (g.c < j) ? (rqc.hi > 0.0) : (rqc.hi < 0.0);
+    bool ok = sgn && dd_lt(blo, nl) && dd_lt(nl, bhi);
+#ifdef MRRR_DEBUG_RQI
+    if (!ok && active && !isB)
+      printf("RQI reject j=%d it=%d r=%d c=%d resid=%.3e thr1=%.3e rqc=%.3e lam=%.17e blo=%.17e bhi=%.17e careful=%d\n", j,
+             it, r, g.c, resid.hi, thr1, rqc.hi, lam.hi, blo.hi, bhi.hi, (int)careful);
+#endif
     if (ok) lam = nl;
-    else break;
+    else {
+      if (active && !isB) atomicAdd((unsigned long long *)&stats[sgn ? ST_RQI_REJ_BRACKET : ST_RQI_REJ_SIGN], 1ull);
+      break;
+    }
   }
   if (!accepted) {
     if (active && !isB) atomicAdd((unsigned long long *)&stats[ST_RQI_FALLBACK], 1ull);
-    lam = bisect_y_full(y, nb, j, blo, bhi);
+    lam = bisect_y_full(y, qy, nb, j, blo, bhi);
     lu_valid = r >= 0;
     careful = getvec_pair_any(y, qy, nb, lam, r, isB, P0, P1, P2, S, g);
     if (r < 0) qdg += nb - 1;

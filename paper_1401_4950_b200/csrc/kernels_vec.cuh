@@ -19,9 +19,7 @@ __device__ __forceinline__ dd ld_dll(const YElt *y) { return dd_make(__ldg(&y->d
 // dependent chain per step is one dd division and one dd subtraction; l+(i) = dl(i)/d+(i),
 // u-(i) = dl(i)/omega(i+1) and the twist quantity gamma_k = s(k) + t(k) = d+(k) - c2(k)/omega(k+1)
 // come off the chain.  Element i holds c2(i), dl(i), gf = g(i), gb = g(i-1).
-struct QElt {
-  double c2_hi, c2_lo, dl_hi, dl_lo, gf_hi, gf_lo, gb_hi, gb_lo;
-};
+// (struct QElt is defined in kernels.cuh)
 
 __global__ void k_build_q(const RepDesc *__restrict__ reps, const int *__restrict__ rlist, int r0, int nr,
                           const YElt *__restrict__ my, QElt *mq) {
@@ -491,13 +489,13 @@ __device__ dd zsolve(const YElt *__restrict__ y, int nb, int r, const dd *A, con
 }
 
 // y-bisection to relative width 2^-98 (RQI fallback)
-__device__ dd bisect_y_full(const YElt *__restrict__ y, int nb, int j, dd lo, dd hi) {
+__device__ dd bisect_y_full(const YElt *__restrict__ y, const QElt *__restrict__ q, int nb, int j, dd lo, dd hi) {
   for (int it = 0; it < 200; it++) {
     dd m = dd_lt(dd_abs(lo), dd_abs(hi)) ? dd_abs(hi) : dd_abs(lo);
     dd w = dd_sub(hi, lo);
     if (!dd_lt(dd_mul_d(m, 0x1p-98), w)) break;
     dd mid = dd_add(lo, dd_mul_d(w, 0.5));
-    if (negcount_y(y, nb, mid) < j) lo = mid;
+    if ((q ? negcount_y_q(q, y, nb, mid) : negcount_y(y, nb, mid)) < j) lo = mid;
     else hi = mid;
   }
   return dd_add(lo, dd_mul_d(dd_sub(hi, lo), 0.5));
@@ -552,7 +550,7 @@ __global__ void __launch_bounds__(64) k_rqi(const Singleton *__restrict__ sg, in
   atomicAdd((unsigned long long *)&stats[ST_GETVEC], (unsigned long long)iters);
   if (!accepted) {
     atomicAdd((unsigned long long *)&stats[ST_RQI_FALLBACK], 1ull);
-    lam = bisect_y_full(y, nb, j, blo, bhi);
+    lam = bisect_y_full(y, nullptr, nb, j, blo, bhi);
     getvec_dd(y, nb, lam, r, A, B, S, g);
     atomicAdd((unsigned long long *)&stats[ST_GETVEC], 1ull);
     r = g.r;

@@ -88,8 +88,7 @@ struct mrrr_ctx {
   long long target_chains = 65536;  // k-section budget per round (C2 sweep: 65536 -> 3 levels per round)
   int mmax = 16;
   int chains_per_thread = 1;
-  bool neg_tma = true;
-  bool rqi_q = true;    // singleton RQI on the pivot-recurrence form (QElt, k_rqi2 fast pass)  // x-NegCount with TMA-staged representation tiles (k_negcount_tma)
+  bool neg_tma = true;  // x-NegCount with TMA-staged representation tiles (k_negcount_tma)
   bool rqi_pair = true;
   bool l2_persist = true;
   long long l2_max_window = 0;
@@ -265,14 +264,15 @@ void launch_negcount(mrrr_t h, const Node *nodes, int nnode, int m, int nex) {
   const RepDesc *reps = h->reps.as<RepDesc>();
   const double2 *mx = h->mx.as<double2>();
   const YElt *my = h->my.as<YElt>();
+  const QElt *mq = h->mq.as<QElt>();
   int *cnts = h->counts.as<int>(), *exc = h->excounts.as<int>();
   unsigned g = nblocks_for(thr, 128);
   cudaStream_t st = h->stream;
   switch (ch) {
-    case 1: k_negcount<Y, 1><<<g, 128, 0, st>>>(nodes, nnode, m, ex, nex, reps, mx, my, cnts, exc); break;
-    case 2: k_negcount<Y, 2><<<g, 128, 0, st>>>(nodes, nnode, m, ex, nex, reps, mx, my, cnts, exc); break;
-    case 3: k_negcount<Y, 3><<<g, 128, 0, st>>>(nodes, nnode, m, ex, nex, reps, mx, my, cnts, exc); break;
-    default: k_negcount<Y, 4><<<g, 128, 0, st>>>(nodes, nnode, m, ex, nex, reps, mx, my, cnts, exc); break;
+    case 1: k_negcount<Y, 1><<<g, 128, 0, st>>>(nodes, nnode, m, ex, nex, reps, mx, my, mq, cnts, exc); break;
+    case 2: k_negcount<Y, 2><<<g, 128, 0, st>>>(nodes, nnode, m, ex, nex, reps, mx, my, mq, cnts, exc); break;
+    case 3: k_negcount<Y, 3><<<g, 128, 0, st>>>(nodes, nnode, m, ex, nex, reps, mx, my, mq, cnts, exc); break;
+    default: k_negcount<Y, 4><<<g, 128, 0, st>>>(nodes, nnode, m, ex, nex, reps, mx, my, mq, cnts, exc); break;
   }
   launch_check(h);
 }
@@ -362,7 +362,7 @@ void l2_pin_reps(mrrr_t h, bool on) {
   cudaStreamAttrValue v;
   memset(&v, 0, sizeof(v));
   if (on) {
-    Buf &hot = h->rqi_q ? h->mq : h->my;  // the representation form the RQI lanes stream
+    Buf &hot = h->mq;  // the representation form the RQI lanes stream
     size_t bytes = std::min<size_t>(hot.cap, (size_t)h->l2_max_window);
     v.accessPolicyWindow.base_ptr = hot.p;
     v.accessPolicyWindow.num_bytes = bytes;
@@ -396,9 +396,9 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
     CK(cudaEventRecord(h->rq0, h->stream));
     if (pair) {
       CK(h->zmeta.ensure(sizeof(ZMeta) * stride));
-      k_rqi2<<<nblocks_for(2 * nb, 64), 64, 0, h->stream>>>(
+      k_rqi2<<<nblocks_for(2 * nb, 64), 64, 64 * MRRR_RQI_RING * sizeof(RingSlot), h->stream>>>(
           h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(),
-          h->rqi_q ? h->mq.as<QElt>() : nullptr, h->wsA.as<dd>(), stride, nbmax, W, h->zmeta.as<ZMeta>(), diag ? h->ddepth.as<int>() : nullptr,
+          h->mq.as<QElt>(), h->wsA.as<dd>(), stride, nbmax, W, h->zmeta.as<ZMeta>(), diag ? h->ddepth.as<int>() : nullptr,
           diag ? h->dflo.as<double>() : nullptr, diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>());
       launch_check(h);
       k_zwrite<<<nblocks_for(32 * nb, 256), 256, 0, h->stream>>>(
@@ -881,7 +881,6 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_MMAX")) h->mmax = atoi(s);
     if (const char *s = getenv("MRRR_CH")) h->chains_per_thread = std::max(1, std::min(4, atoi(s)));
     if (const char *s = getenv("MRRR_NEGTMA")) h->neg_tma = atoi(s) != 0;
-    if (const char *s = getenv("MRRR_RQIQ")) h->rqi_q = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;
     if (const char *s = getenv("MRRR_L2PIN")) h->l2_persist = atoi(s) != 0;
     {

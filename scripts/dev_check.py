@@ -73,6 +73,8 @@ cases = [
     ("clement_500", *mi.clement(500)),
     ("hermite_500", *mi.hermite(500)),
 ]
+if len(sys.argv) > 1 and sys.argv[1] == "glued":
+    cases = [("glued_128_10", *mi.glued_wilkinson(128, 10, 1e-10))]
 allok = True
 for c in cases:
     try:
@@ -80,6 +82,9 @@ for c in cases:
     except Exception:
         traceback.print_exc()
         allok = False
+if len(sys.argv) > 1:
+    print("ALL OK" if allok else "SOME FAILED")
+    sys.exit(0)
 d, e = mi.random_tridiag(3000, 9, -1.0)
 for il, iu in [(1, 40), (100, 400), (2901, 3000)]:
     try:

@@ -513,11 +513,14 @@ static void getvec_q(const rep_t *M, qreal lam, int64_t *r_io, gv_ws *w, qreal *
   *c_out = c;
 }
 
-/* y-bisection to full accuracy (fallback of RQI) */
+/* y-bisection to full accuracy (fallback of RQI): relative width 2^-98 of |lambda|,  */
+/* or absolute width 2^-100 spdiam when that is larger (A-29: the y-count cannot resolve finer   */
+/* than the representation's y-rounding when its shift could not be certified)                          */
 static qreal bisect_y_full(const rep_t *M, int64_t j, qreal lo, qreal hi) {
+  const qreal afloor = 0x1p-100Q * (qreal)M->spdiam;
   for (int it = 0; it < 200; it++) {
     qreal m = fmaxq(fabsq(lo), fabsq(hi));
-    if (!(hi - lo > 0x1p-98Q * m)) break;
+    if (!(hi - lo > fmaxq(0x1p-98Q * m, afloor))) break;
     qreal w = lo + (hi - lo) / 2;
     STAT_ADD(ST_NEGY, 1);
     if (negcount_q(M->nb, M->d, M->dll, w) < j) lo = w;

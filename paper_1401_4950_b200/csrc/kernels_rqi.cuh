@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
   }
   if (!accepted) {
     if (active && !isB) atomicAdd((unsigned long long *)&stats[ST_RQI_FALLBACK], 1ull);
-    lam = bisect_y_full(y, qy, nb, j, blo, bhi);
+    lam = bisect_y_full(y, qy, nb, j, blo, bhi, R.spdiam);
     lu_valid = r >= 0;
     careful = getvec_pair_any(y, qy, nb, lam, r, isB, P0, P1, P2, S, g);
     if (r < 0) qdg += nb - 1;

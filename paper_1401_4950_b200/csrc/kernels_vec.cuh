@@ -489,11 +489,16 @@ __device__ dd zsolve(const YElt *__restrict__ y, int nb, int r, const dd *A, con
 }
 
 // y-bisection to relative width 2^-98 (RQI fallback)
-__device__ dd bisect_y_full(const YElt *__restrict__ y, const QElt *__restrict__ q, int nb, int j, dd lo, dd hi) {
+// stop at relative width 2^-98 of |lambda| or absolute width 2^-100 spdiam, whichever is larger (A-29)
+__device__ dd bisect_y_full(const YElt *__restrict__ y, const QElt *__restrict__ q, int nb, int j, dd lo, dd hi,
+                            double spdiam) {
+  const dd afloor = dd_from(__dmul_rn(0x1p-100, spdiam));
   for (int it = 0; it < 200; it++) {
     dd m = dd_lt(dd_abs(lo), dd_abs(hi)) ? dd_abs(hi) : dd_abs(lo);
     dd w = dd_sub(hi, lo);
-    if (!dd_lt(dd_mul_d(m, 0x1p-98), w)) break;
+    dd tol = dd_mul_d(m, 0x1p-98);
+    if (dd_lt(tol, afloor)) tol = afloor;
+    if (!dd_lt(tol, w)) break;
     dd mid = dd_add(lo, dd_mul_d(w, 0.5));
     if ((q ? negcount_y_q(q, y, nb, mid) : negcount_y(y, nb, mid)) < j) lo = mid;
     else hi = mid;
@@ -550,7 +555,7 @@ __global__ void __launch_bounds__(64) k_rqi(const Singleton *__restrict__ sg, in
   atomicAdd((unsigned long long *)&stats[ST_GETVEC], (unsigned long long)iters);
   if (!accepted) {
     atomicAdd((unsigned long long *)&stats[ST_RQI_FALLBACK], 1ull);
-    lam = bisect_y_full(y, nullptr, nb, j, blo, bhi);
+    lam = bisect_y_full(y, nullptr, nb, j, blo, bhi, R.spdiam);
     getvec_dd(y, nb, lam, r, A, B, S, g);
     atomicAdd((unsigned long long *)&stats[ST_GETVEC], 1ull);
     r = g.r;

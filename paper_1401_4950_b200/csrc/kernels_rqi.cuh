@@ -11,8 +11,8 @@
 // n steps per lane and no separate argmin or z pass is needed inside the RQI.  Later iterations (twist
 // r fixed) run F on 0..r-1 and B on n-2..r and store l+ / u- for the final z solve.
 //
-// Workspace: three dd planes [i * S + pair]: P0 = s(i) / t(i), P1 = S_i / T_i (iteration 1, each
-// index written by exactly one lane), P2 = l+(i) for i < r and u-(i) for i >= r.
+// Workspace: planes [i * S + pair]: P0 (dd) = s(i) / t(i), P1 (fp64) = S_i / T_i (iteration 1, each
+// index written by exactly one lane), P2 = l+(i) for i < r and u-(i) for i >= r (in the pair's P0 column).
 //
 // The hot loops use the branch-free dd operations (dd_*_nf); if a lane's recurrence leaves the finite
 // range (a zero pivot: IEEE infinity) the pass is rerun with the careful operations,
@@ -42,6 +42,12 @@ template <bool C> __device__ __forceinline__ dd OSUB(dd a, dd b) { if constexpr 
 template <bool C> __device__ __forceinline__ dd OMUL(dd a, dd b) { if constexpr (C) return dd_mul(a, b); else return dd_mul_nf(a, b); }
 template <bool C> __device__ __forceinline__ dd ORCP(dd a) { if constexpr (C) return dd_rcp(a); else return dd_rcp_nf(a); }
 template <bool C> __device__ __forceinline__ dd OADD1(dd a) { if constexpr (C) return dd_add_d(a, 1.0); else return dd_add_d_nf(a, 1.0); }
+
+// P1 plane (||z||^2 partial sums S_i / T_i of iteration 1) holds fp64: the twist candidates' norm only
+// feeds the RQC and the acceptance test (relative accuracy ~eps_x); the final norm comes from the
+// r-twisted (FIXED) pass in dd
+__device__ __forceinline__ void stw1(double *w, long long off, dd v) { __stcs(w + off, v.hi); }
+__device__ __forceinline__ dd ldw1(const double *w, long long off) { return dd_from(__ldcs(w + off)); }
 
 struct Elt3 {
   double2 a, b, c;
@@ -87,7 +93,7 @@ enum { PH_STORE = 0, PH_COMBINE = 1, PH_FIXED = 2 };
 // (phase B) the other lane's halves read PD steps ahead through compile-time-indexed rings.
 template <bool C, int MODE>
 __device__ __forceinline__ void run_phase(const YElt *__restrict__ y, int last, int k0, int k1, bool isB, int oa,
-                                          int oc, dd lam, int r, dd *P0, dd *P1, dd *P2, long long S, dd &x, dd &acc,
+                                          int oc, dd lam, int r, dd *P0, double *P1, dd *P2, long long S, dd &x, dd &acc,
                                           int &cnt, Cand &cd, dd &tr) {
   constexpr int PD = MRRR_RQI_PD;
   if (k0 >= k1) return;
@@ -100,7 +106,7 @@ __device__ __forceinline__ void run_phase(const YElt *__restrict__ y, int last, 
     er[u] = ld3(y, GIX(kk), oa, oc);
     if (MODE == PH_COMBINE) {
       pq[u] = ldw(P0, (long long)GIX(kk) * S);
-      ps[u] = ldw(P1, (long long)GIX(kk) * S);
+      ps[u] = ldw1(P1, (long long)GIX(kk) * S);
     }
   }
   for (int kb = k0; kb < k1; kb += PD) {
@@ -116,7 +122,7 @@ __device__ __forceinline__ void run_phase(const YElt *__restrict__ y, int last, 
           other = pq[u];
           ost = ps[u];
           pq[u] = ldw(P0, (long long)GIX(kn) * S);
-          ps[u] = ldw(P1, (long long)GIX(kn) * S);
+          ps[u] = ldw1(P1, (long long)GIX(kn) * S);
         }
         const int i = GIX(k);
         const dd c = D2(e0.c);
@@ -128,14 +134,14 @@ __device__ __forceinline__ void run_phase(const YElt *__restrict__ y, int last, 
           dd myst = isB ? accn : acc;
           if (MODE == PH_STORE) {
             stw(P0, (long long)i * S, mine);
-            stw(P1, (long long)i * S, myst);
+            stw1(P1, (long long)i * S, myst);
           } else {
             cand_take(cd, OADD<C>(mine, other), OADD<C>(myst, ost), i, isB);
           }
         } else {
           if (isB && k == k1 - 1) tr = OMUL<C>(OMUL<C>(c, rr), x);  // B's last row is r
-          if constexpr (C) stw(P2, i, (den.hi == 0.0) ? dd_mark() : out);
-          else stw(P2, i, out);
+          if constexpr (C) stw(P2, (long long)i * S, (den.hi == 0.0) ? dd_mark() : out);
+          else stw(P2, (long long)i * S, out);
         }
         cnt += dd_sb(den);
         x = xn;
@@ -151,7 +157,7 @@ __device__ __forceinline__ void run_phase(const YElt *__restrict__ y, int last, 
 // Returns false (both lanes) if the fast pass left the finite range.  On return (both lanes):
 // g.r, g.gamma = gamma_r, g.zz = ||z||^2 (NaN/inf if the closed form broke down), g.c = inertia (A-26).
 template <bool C>
-__device__ bool getvec_pair_t(const YElt *__restrict__ y, int nb, dd lam, int r, bool isB, dd *P0, dd *P1, dd *P2,
+__device__ bool getvec_pair_t(const YElt *__restrict__ y, int nb, dd lam, int r, bool isB, dd *P0, double *P1, dd *P2,
                               long long S, GV &g) {
   const unsigned pm = pair_mask();
   const int last = nb - 1;
@@ -256,6 +262,39 @@ __device__ __forceinline__ dd qdiv(dd nu, dd den, double r1, double r2) {
   t = __fma_rn(-h, den.lo, t);
   return dd_make(h, __dmul_rn(t, r2));
 }
+// a + b + c in dd with the three high words summed exactly (TwoSum cascade) and the low words and the
+// two rounding errors in fp64: absolute error ~u^2 (|a| + |b| + |c|), i.e. a u^2-relative perturbation
+// of the representation data and of the shift (the mixed-stability scale of the qd transforms)
+__device__ __forceinline__ dd dd_sum3_nf(dd a, dd b, dd c) {
+  const dd s1 = two_sum(a.hi, b.hi);
+  const dd s2 = two_sum(s1.hi, c.hi);
+  const double lo = __dadd_rn(__dadd_rn(__dadd_rn(a.lo, b.lo), c.lo), __dadd_rn(s1.lo, s2.lo));
+  return two_sum(s2.hi, lo);
+}
+// twist candidate kept lazily: gamma = ga - gb and ||z||^2 - 1 = sa + sb are formed in dd only for the
+// winner; candidates are ranked by an fp64 evaluation of |ga - gb| (the twist index is parity-unpinned,
+// A-16; the winner's gamma_r used by the RQC is the dd value)
+struct CandL {
+  double best;
+  dd ga, gb, sa, sb;
+  int k;
+};
+__device__ __forceinline__ void candl_init(CandL &c) {
+  c.best = INFINITY; c.k = -1;
+  c.ga = c.gb = c.sa = c.sb = dd_from(0.0);
+}
+__device__ __forceinline__ void candl_take(CandL &c, dd ga, dd gb, dd sa, dd sb, int k, bool tie_wins) {
+  const double g = __dadd_rn(__dsub_rn(ga.hi, gb.hi), __dsub_rn(ga.lo, gb.lo));
+  if (isnan(g)) return;
+  const double a = fabs(g);
+  const bool take = (c.k < 0) || (a < c.best) || (tie_wins && !(c.best < a));
+  if (take) { c.best = a; c.ga = ga; c.gb = gb; c.sa = sa; c.sb = sb; c.k = k; }
+}
+
+// FULL: l+/u- (out) and the norm recurrence in dd (passes that store the factors for the z solve);
+// otherwise (twist-search pass) out and S/T in fp64: they only feed the twist candidates' ||z||^2 for
+// the RQC and the acceptance test, whose relative accuracy needs are ~eps_x
+template <bool FULL>
 __device__ __forceinline__ void q_step(dd den, const Q3 &e, dd lam, dd acc, dd &P, dd &out, dd &dn, dd &accn,
                                        bool &ok) {
   const double b = den.hi;
@@ -266,11 +305,17 @@ __device__ __forceinline__ void q_step(dd den, const Q3 &e, dd lam, dd acc, dd &
   const double e2 = __fma_rn(-b, r1, 1.0);
   const double r2 = __fma_rn(r1, e2, r1);
   P = qdiv(D2(e.c2), den, r1, r2);
-  const dd o = qdiv(D2(e.dl), den, r1, r2);
-  out = fast_two_sum(o.hi, o.lo);
-  const dd eg = dd_sub_nf(D2(e.g), lam);
-  dn = dd_sub_nf(eg, P);
-  accn = dd_mul_nf(dd_mul_nf(out, out), dd_add_d_nf(acc, 1.0));
+  dn = dd_sum3_nf(D2(e.g), dd_neg(lam), dd_neg(P));
+  if (FULL) {
+    const dd o = qdiv(D2(e.dl), den, r1, r2);
+    out = fast_two_sum(o.hi, o.lo);
+    accn = dd_mul_nf(dd_mul_nf(out, out), dd_add_d_nf(acc, 1.0));
+  } else {
+    const double o = __dmul_rn(e.dl.x, r2);
+    const double o2 = __dmul_rn(o, o);
+    out = dd_from(o);
+    accn = dd_from(__fma_rn(o2, acc.hi, o2));
+  }
   ok &= (fabs(b) > 0x1p-1000) && (fabs(b) < 0x1p1000);
 }
 
@@ -281,10 +326,14 @@ __device__ __forceinline__ void q_step(dd den, const Q3 &e, dd lam, dd acc, dd &
 #define MRRR_RQI_RING 8
 #endif
 struct RingSlot {
-  double2 c2, dl, g, p0, p1;
+  double2 c2, dl, g, p0;
+  double p1, pad;
 };
 __device__ __forceinline__ void cp16(void *sdst, const void *gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp8(void *sdst, const void *gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -294,8 +343,8 @@ __device__ __forceinline__ void cp_wait() {
 
 template <int MODE>
 __device__ __forceinline__ void run_phase_q(const QElt *__restrict__ q, int last, int k0, int k1, bool isB, int og,
-                                            dd lam, dd *P0, dd *P1, dd *P2, long long S, dd &den, dd &acc, int &cnt,
-                                            Cand &cd, dd &tr, bool &ok, RingSlot *ring) {
+                                            dd lam, dd *P0, double *P1, dd *P2, long long S, dd &den, dd &acc, int &cnt,
+                                            CandL &cd, dd &tr, bool &ok, RingSlot *ring) {
   constexpr int R = MRRR_RQI_RING;
   if (k0 >= k1) return;
 #define GIX(k) (isB ? (last - 1 - (k)) : (k))
@@ -307,7 +356,7 @@ __device__ __forceinline__ void run_phase_q(const QElt *__restrict__ q, int last
     cp16(&ring[slot].g, p + og);
     if (MODE == PH_COMBINE) {
       cp16(&ring[slot].p0, P0 + (long long)i * S);
-      cp16(&ring[slot].p1, P1 + (long long)i * S);
+      cp8(&ring[slot].p1, P1 + (long long)i * S);
     }
     cp_commit();
   };
@@ -323,24 +372,25 @@ __device__ __forceinline__ void run_phase_q(const QElt *__restrict__ q, int last
     dd other, ost;
     if (MODE == PH_COMBINE) {
       other = D2(ring[slot].p0);
-      ost = D2(ring[slot].p1);
+      ost = dd_from(ring[slot].p1);
     }
     const int i = GIX(k);
     dd P, out, dn, accn;
-    q_step(den, e0, lam, acc, P, out, dn, accn, ok);
+    q_step<MODE == PH_FIXED>(den, e0, lam, acc, P, out, dn, accn, ok);
     if (MODE == PH_STORE || MODE == PH_COMBINE) {
       const dd mine = isB ? fast_two_sum(P.hi, P.lo) : den;
       const dd myst = isB ? accn : acc;
       if (MODE == PH_STORE) {
         stw(P0, (long long)i * S, mine);
-        stw(P1, (long long)i * S, myst);
+        stw1(P1, (long long)i * S, myst);
       } else {
-        const dd gam = isB ? dd_sub_nf(other, mine) : dd_sub_nf(mine, other);
-        cand_take(cd, gam, dd_add_nf(myst, ost), i, isB);
+        // gamma_i = d+(i) - c2(i)/omega(i+1): F holds the first term, B the second
+        if (isB) candl_take(cd, other, mine, ost, myst, i, true);
+        else candl_take(cd, mine, other, myst, ost, i, false);
       }
     } else {
       if (isB && k == k1 - 1) tr = fast_two_sum(P.hi, P.lo);  // B's last row is r: c2(r)/omega(r+1)
-      stw(P2, i, out);
+      stw(P2, (long long)i * S, out);
     }
     cnt += dd_sb(den);
     den = dn;
@@ -352,7 +402,7 @@ __device__ __forceinline__ void run_phase_q(const QElt *__restrict__ q, int last
 }
 
 // one Getvec of the pair on the RQI form; returns false (both lanes) if the careful pass is needed
-__device__ bool getvec_pair_q(const QElt *__restrict__ q, int nb, dd lam, int r, bool isB, dd *P0, dd *P1, dd *P2,
+__device__ bool getvec_pair_q(const QElt *__restrict__ q, int nb, dd lam, int r, bool isB, dd *P0, double *P1, dd *P2,
                               long long S, GV &g) {
   extern __shared__ __align__(16) unsigned char rqi_smem[];
   RingSlot *ring = reinterpret_cast<RingSlot *>(rqi_smem) + threadIdx.x * MRRR_RQI_RING;
@@ -366,8 +416,8 @@ __device__ bool getvec_pair_q(const QElt *__restrict__ q, int nb, dd lam, int r,
   dd acc = dd_from(0.0), tr = dd_from(0.0);
   int cnt = 0;
   bool ok = true;
-  Cand cd;
-  cd.k = -1; cd.best = dd_from(INFINITY); cd.gam = dd_from(0.0); cd.st = dd_from(0.0);
+  CandL cd;
+  candl_init(cd);
   if (it1) {
     const int kA = last / 2;
     run_phase_q<PH_STORE>(q, last, 0, kA, isB, og, lam, P0, P1, P2, S, den, acc, cnt, cd, tr, ok, ring);
@@ -375,11 +425,11 @@ __device__ bool getvec_pair_q(const QElt *__restrict__ q, int nb, dd lam, int r,
       const int i = kA;
       const Q3 e = ldq(q, i, og);
       dd P, out, dn, accn;
-      q_step(den, e, lam, acc, P, out, dn, accn, ok);
+      q_step<false>(den, e, lam, acc, P, out, dn, accn, ok);
       const dd mine = isB ? fast_two_sum(P.hi, P.lo) : den;
       const dd myst = isB ? accn : acc;
       const dd om = shfl_dd(mine, 1), ost = shfl_dd(myst, 1);
-      if (!isB) cand_take(cd, dd_sub_nf(mine, om), dd_add_nf(myst, ost), i, false);
+      if (!isB) candl_take(cd, mine, om, myst, ost, i, false);
       cnt += dd_sb(den);
       den = dn;
       acc = accn;
@@ -397,16 +447,17 @@ __device__ bool getvec_pair_q(const QElt *__restrict__ q, int nb, dd lam, int r,
   if (it1) {
     if (!isB) {  // F: den = d+(n-1) = gamma_n closes the full NegCount
       cnt += dd_sb(den);
-      cand_take(cd, den, acc, last, false);
+      candl_take(cd, den, dd_from(0.0), acc, dd_from(0.0), last, false);
     }
-    dd ob = shfl_dd(cd.best, 1), og_ = shfl_dd(cd.gam, 1), ost = shfl_dd(cd.st, 1);
-    int ok_ = __shfl_xor_sync(pm, cd.k, 1);
+    const double ob = __shfl_xor_sync(pm, cd.best, 1);
+    const dd oga = shfl_dd(cd.ga, 1), ogb = shfl_dd(cd.gb, 1), osa = shfl_dd(cd.sa, 1), osb = shfl_dd(cd.sb, 1);
+    const int ok_ = __shfl_xor_sync(pm, cd.k, 1);
     if (!isB) {  // B's candidates are the lower indices: they win ties
-      if (ok_ >= 0 && (cd.k < 0 || !dd_lt(cd.best, ob))) { cd.best = ob; cd.gam = og_; cd.st = ost; cd.k = ok_; }
+      if (ok_ >= 0 && (cd.k < 0 || !(cd.best < ob))) { cd.best = ob; cd.ga = oga; cd.gb = ogb; cd.sa = osa; cd.sb = osb; cd.k = ok_; }
     }
     g.r = shfl_i_from(cd.k, lane_F());
-    g.gamma = shfl_dd_from(cd.gam, lane_F());
-    g.zz = dd_add_d(shfl_dd_from(cd.st, lane_F()), 1.0);
+    g.gamma = shfl_dd_from(dd_sub(cd.ga, cd.gb), lane_F());
+    g.zz = dd_add_d(shfl_dd_from(dd_add(cd.sa, cd.sb), lane_F()), 1.0);
     g.c = shfl_i_from(cnt, lane_F());
   } else {
     const dd dr = shfl_dd_from(den, lane_F());
@@ -425,7 +476,7 @@ __device__ bool getvec_pair_q(const QElt *__restrict__ q, int nb, dd lam, int r,
 
 // returns true if the careful (IEEE special value) pass had to run
 __device__ __forceinline__ bool getvec_pair_any(const YElt *__restrict__ y, const QElt *__restrict__ qy, int nb, dd lam,
-                                                int r, bool isB, dd *P0, dd *P1, dd *P2, long long S, GV &g) {
+                                                int r, bool isB, dd *P0, double *P1, dd *P2, long long S, GV &g) {
   if (getvec_pair_q(qy, nb, lam, r, isB, P0, P1, P2, S, g)) return false;
   getvec_pair_t<true>(y, nb, lam, r, isB, P0, P1, P2, S, g);
   return true;
@@ -452,7 +503,7 @@ __device__ __forceinline__ dd shfl_idx_dd(dd v, int lane) {
 
 __global__ void __launch_bounds__(256) k_zwrite(const Singleton *__restrict__ sg, int ns,
                                                 const RepDesc *__restrict__ reps, const YElt *__restrict__ my,
-                                                const dd *__restrict__ P2base, long long nbmax,
+                                                const dd *__restrict__ P2base, long long S,
                                                 const ZMeta *__restrict__ zm, double *Z, long long ldz) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -462,10 +513,10 @@ __global__ void __launch_bounds__(256) k_zwrite(const Singleton *__restrict__ sg
   const RepDesc R = reps[s.rep];
   const int nb = R.nb, r = m.r, last = nb - 1;
   const dd inv = dd_make(m.inv_hi, m.inv_lo);
-  const dd *P = P2base + (long long)w * nbmax;
+  const dd *P = P2base + w;  // column w of the strided P2 plane (row stride S)
   double *Zc = Z + (long long)s.col * ldz + R.bstart;
   if (m.careful) {
-    if (lane == 0) zsolve(my + R.off, nb, r, P, P, 1, inv, Zc);
+    if (lane == 0) zsolve(my + R.off, nb, r, P, P, S, inv, Zc);
     return;
   }
   if (lane == 0) Zc[r] = inv.hi;
@@ -477,7 +528,7 @@ __global__ void __launch_bounds__(256) k_zwrite(const Singleton *__restrict__ sg
       const int mm = m0 + lane;
       const bool valid = mm < len;
       const int src = side ? (r + mm) : (r - 1 - mm);
-      dd v = valid ? dd_neg(ldw(P, src)) : dd_from(1.0);
+      dd v = valid ? dd_neg(ldw(P, (long long)src * S)) : dd_from(1.0);
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
         dd o = shfl_up_dd(v, off);
@@ -505,7 +556,10 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
   const YElt *y = my + R.off;
   const QElt *qy = mq + R.off;
   const long long plane = nbmax * S;
-  dd *P0 = ws + pid, *P1 = ws + plane + pid, *P2 = ws + 2 * plane + (long long)pid * nbmax;
+  // P0 (dd) and P1 (fp64) planes [row * S + pair]; P2 (l+/u- of the r-twisted pass) reuses the pair's P0
+  // column: it is written only after the pair's last twist-search pass has read P0
+  dd *P0 = ws + pid, *P2 = P0;
+  double *P1 = reinterpret_cast<double *>(ws + plane) + pid;
   double mid = bis_mid(s.lo, s.hi);
   double nu = __dmul_rn(__dmul_rn(100.0, (double)nb), EPS_X);
   dd blo = dd_from(__dsub_rn(s.lo, __dmul_rn(nu, fabs(s.lo))));
@@ -528,7 +582,7 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
     if (!isfinite(zz.hi)) {  // closed form broke down (overflow / zero pivot): explicit z solve (A-25)
       if (!lu_valid) { careful = getvec_pair_any(y, qy, nb, lam, r, isB, P0, P1, P2, S, g); lu_valid = true; qd += nb - 1; }
       zs += nb - 1;
-      if (!isB) zz = zsolve(y, nb, r, P2, P2, 1, dd_from(0.0), nullptr);
+      if (!isB) zz = zsolve(y, nb, r, P2, P2, S, dd_from(0.0), nullptr);
       zz = shfl_dd_from(zz, lane_F());
     }
     if (!isfinite(zz.hi) || zz.hi == 0.0) break;
@@ -562,13 +616,14 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
     r = g.r < 0 ? 0 : g.r;
     zz = g.zz;
   }
-  if (!lu_valid) {  // accepted on a twist-search pass: one r-twisted pass to store l+ / u-
+  if (!lu_valid) {  // accepted on a twist-search pass: one r-twisted pass to store l+ / u- (and its dd ||z||^2)
     careful = getvec_pair_any(y, qy, nb, lam, r, isB, P0, P1, P2, S, g);
     qd += nb - 1;
+    zz = g.zz;
   }
   if (!isfinite(zz.hi) || zz.hi == 0.0) {
     zs += nb - 1;
-    if (!isB) zz = zsolve(y, nb, r, P2, P2, 1, dd_from(0.0), nullptr);
+    if (!isB) zz = zsolve(y, nb, r, P2, P2, S, dd_from(0.0), nullptr);
     zz = shfl_dd_from(zz, lane_F());
   }
   dd inv = dd_rcp(dd_sqrt(zz));

@@ -127,6 +127,113 @@ __global__ void k_clu_attempt(const Cluster *__restrict__ cl, int ncl, const Rep
   valid[t] = ok;
 }
 
+// growth max|fl64(d+)| and validity (no NaN) of dstqds(M_y, tau) (Alg. dstqds): fast pass on the
+// pivot-recurrence form (QElt), the careful IEEE pass (qd_step) if a pivot leaves [2^-1000, 2^1000]
+__device__ void dstqds_growth(const YElt *__restrict__ y, const QElt *__restrict__ q, int nb, double tau_x, double &g,
+                              int &valid) {
+  const dd tau = dd_from(tau_x);
+  {
+    dd den = dd_sub(dd_make(__ldg(&q[0].gb_hi), __ldg(&q[0].gb_lo)), tau);
+    double gm = 0.0;
+    bool ok = true;
+    for (int i = 0; i < nb - 1; i++) {
+      const double b = den.hi;
+      ok &= (fabs(b) > 0x1p-1000) && (fabs(b) < 0x1p1000);
+      gm = dmaxd(gm, fabs(b));
+      const double r = rcp_seed(b);
+      double ee = __fma_rn(-b, r, 1.0);
+      ee = __fma_rn(ee, ee, ee);
+      const double r1 = __fma_rn(r, ee, r);
+      const double e2 = __fma_rn(-b, r1, 1.0);
+      const double r2 = __fma_rn(r1, e2, r1);
+      const dd c2 = dd_make(__ldg(&q[i].c2_hi), __ldg(&q[i].c2_lo));
+      const double h = __dmul_rn(c2.hi, r1);
+      double t = __fma_rn(-h, b, c2.hi);
+      t = __dadd_rn(t, c2.lo);
+      t = __fma_rn(-h, den.lo, t);
+      const dd P = dd_make(h, __dmul_rn(t, r2));
+      den = dd_sub_nf(dd_sub_nf(dd_make(__ldg(&q[i].gf_hi), __ldg(&q[i].gf_lo)), tau), P);
+    }
+    ok &= isfinite(den.hi) && isfinite(den.lo);
+    if (ok) {
+      g = dmaxd(gm, fabs(den.hi));
+      valid = 1;
+      return;
+    }
+  }
+  dd s = dd_neg(tau);
+  double gm = 0.0;
+  int okv = 1;
+  for (int i = 0; i < nb - 1; i++) {
+    dd den, rr, out, xn;
+    qd_step(s, ld_d(y + i), ld_dl(y + i), ld_dll(y + i), tau, den, rr, out, xn);
+    okv &= !(isnan(den.hi) || isnan(out.hi));
+    gm = dmaxd(gm, fabs(den.hi));
+    s = xn;
+  }
+  dd den = dd_add(s, ld_d(y + nb - 1));
+  okv &= !isnan(den.hi);
+  g = dmaxd(gm, fabs(den.hi));
+  valid = okv;
+}
+
+// S8(c) attempts a0 .. a0+na-1 of every open cluster at once (the shift sequence of Alg. spectrumshift is
+// fixed in advance: tau_l(a+1) = tau_l(a) - 2^a off_l, tau_r(a+1) = tau_r(a) + 2^a off_r), thread per
+// (cluster, attempt, side); k_clu_select_multi then replays the sequential acceptance
+__global__ void k_clu_attempt_multi(const Cluster *__restrict__ cl, int ncl, const RepDesc *__restrict__ reps,
+                                    const YElt *__restrict__ my, const QElt *__restrict__ mq,
+                                    const ShiftState *__restrict__ ss, int a0, int na, double *gval, int *valid) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 2LL * na * ncl) return;
+  const int c = (int)(t / (2 * na)), ia = (int)((t >> 1) % na), side = (int)(t & 1);
+  const ShiftState S = ss[c];
+  if (S.done) return;
+  double tau = side ? S.taur : S.taul;
+  for (int b = a0; b < a0 + ia; b++) tau = side ? __dadd_rn(tau, ldexp(S.offr, b)) : __dsub_rn(tau, ldexp(S.offl, b));
+  const RepDesc R = reps[cl[c].rep];
+  double g;
+  int v;
+  dstqds_growth(my + R.off, mq + R.off, R.nb, tau, g, v);
+  gval[t] = g;
+  valid[t] = v;
+}
+
+__global__ void k_clu_select_multi(const Cluster *__restrict__ cl, int ncl, const RepDesc *__restrict__ reps,
+                                   ShiftState *ss, const double *__restrict__ gval, const int *__restrict__ valid,
+                                   int a0, int na, int *ndone, long long *stats) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncl) return;
+  ShiftState s = ss[c];
+  if (s.done) { atomicAdd(ndone, 1); return; }
+  const double gthr = __dmul_rn(GROWTH, reps[cl[c].rep].spdiam);
+  for (int a = a0; a < a0 + na && !s.done; a++) {
+    atomicAdd((unsigned long long *)&stats[ST_ATTEMPTS], 1ull);
+    const long long o = ((long long)c * na + (a - a0)) * 2;
+    int vl = valid[o], vr = valid[o + 1];
+    double gl = gval[o], gr = gval[o + 1];
+    int pick = 0;
+    if (vl && vr) pick = (gl <= gr) ? 1 : 2;
+    else if (vl) pick = 1;
+    else if (vr) pick = 2;
+    s.attempts++;
+    if (pick) {
+      double g = (pick == 1) ? gl : gr;
+      if (g < s.best_g) { s.best_g = g; s.best_tau = (pick == 1) ? s.taul : s.taur; s.have_best = 1; }
+      if (g <= gthr) { s.done = 1; s.certified = 1; }
+    }
+    if (!s.done) {
+      s.taul = __dsub_rn(s.taul, ldexp(s.offl, a));
+      s.taur = __dadd_rn(s.taur, ldexp(s.offr, a));
+      if (a == MAX_ATTEMPTS - 1) {
+        s.done = 1;
+        if (s.have_best) atomicAdd((unsigned long long *)&stats[ST_UNCERTIFIED], 1ull);
+      }
+    }
+  }
+  if (s.done) atomicAdd(ndone, 1);
+  ss[c] = s;
+}
+
 __global__ void k_clu_select(const Cluster *__restrict__ cl, int ncl, const RepDesc *__restrict__ reps,
                              ShiftState *ss, const double *__restrict__ gval, const int *__restrict__ valid, int a,
                              int *ndone, long long *stats) {
@@ -163,7 +270,8 @@ __global__ void k_clu_select(const Cluster *__restrict__ cl, int ncl, const RepD
 // S8(d): child representation M_y = (d+, l+) of dstqds(M_y, tau_best) and its x copy.
 // Child rep id = repbase + c, data at pool offset poolbase + c * nbmax.
 __global__ void k_clu_build(const Cluster *__restrict__ cl, int ncl, RepDesc *reps, const ShiftState *__restrict__ ss,
-                            double2 *mx, YElt *my, int repbase, long long poolbase, int nbmax) {
+                            double2 *mx, YElt *my, const QElt *__restrict__ mq, int repbase, long long poolbase,
+                            int nbmax) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncl) return;
   ShiftState S = ss[c];
@@ -180,6 +288,46 @@ __global__ void k_clu_build(const Cluster *__restrict__ cl, int ncl, RepDesc *re
   YElt *yc = my + R.off;
   double2 *xc = mx + R.off;
   dd tau = dd_from(S.best_tau);
+  if (mq) {  // fast pass on the pivot-recurrence form; the careful pass below if a pivot leaves the range
+    const QElt *q = mq + P.off;
+    dd den = dd_sub(dd_make(__ldg(&q[0].gb_hi), __ldg(&q[0].gb_lo)), tau);
+    bool ok = true;
+    for (int i = 0; i < P.nb - 1; i++) {
+      const double b = den.hi;
+      ok &= (fabs(b) > 0x1p-1000) && (fabs(b) < 0x1p1000);
+      const double r = rcp_seed(b);
+      double ee = __fma_rn(-b, r, 1.0);
+      ee = __fma_rn(ee, ee, ee);
+      const double r1 = __fma_rn(r, ee, r);
+      const double e2 = __fma_rn(-b, r1, 1.0);
+      const double r2 = __fma_rn(r1, e2, r1);
+      const dd dlp = dd_make(__ldg(&q[i].dl_hi), __ldg(&q[i].dl_lo));
+      const dd c2 = dd_make(__ldg(&q[i].c2_hi), __ldg(&q[i].c2_lo));
+      double h = __dmul_rn(dlp.hi, r1), t = __fma_rn(-h, b, dlp.hi);
+      t = __fma_rn(-h, den.lo, __dadd_rn(t, dlp.lo));
+      const dd out = fast_two_sum(h, __dmul_rn(t, r2));  // l+(i) = dl(i) / d+(i)
+      h = __dmul_rn(c2.hi, r1);
+      t = __fma_rn(-h, b, c2.hi);
+      t = __fma_rn(-h, den.lo, __dadd_rn(t, c2.lo));
+      const dd Pq = dd_make(h, __dmul_rn(t, r2));        // c2(i) / d+(i)
+      const dd dl = dd_mul(den, out);
+      const dd dll = dd_mul(dl, out);
+      YElt e;
+      e.d_hi = den.hi; e.d_lo = den.lo; e.dl_hi = dl.hi; e.dl_lo = dl.lo; e.dll_hi = dll.hi; e.dll_lo = dll.lo;
+      yc[i] = e;
+      const double dx = den.hi, lx = out.hi;
+      xc[i] = make_double2(dx, __dmul_rn(__dmul_rn(dx, lx), lx));
+      den = dd_sub_nf(dd_sub_nf(dd_make(__ldg(&q[i].gf_hi), __ldg(&q[i].gf_lo)), tau), Pq);
+    }
+    ok &= isfinite(den.hi) && isfinite(den.lo);
+    if (ok) {
+      YElt e;
+      e.d_hi = den.hi; e.d_lo = den.lo; e.dl_hi = e.dl_lo = e.dll_hi = e.dll_lo = 0.0;
+      yc[P.nb - 1] = e;
+      xc[P.nb - 1] = make_double2(den.hi, 0.0);
+      return;
+    }
+  }
   dd s = dd_neg(tau);
   for (int i = 0; i < P.nb - 1; i++) {
     dd den, rr, out, xn;

@@ -17,6 +17,7 @@
 #include "kernels.cuh"
 #include "kernels_vec.cuh"
 #include "kernels_rqi.cuh"
+#include "kernels_guided.cuh"
 
 namespace {
 
@@ -72,7 +73,7 @@ struct Err {
 inline unsigned nblocks_for(long long n, int bs) { return (unsigned)std::max<long long>(1, (n + bs - 1) / bs); }
 
 // counters block on the device: reset/readback in one copy
-enum { C_NNEXT = 0, C_NEX, C_NPEND, C_NREADY, C_NSING, C_NCLUS, C_NNXT, C_NDONE, C_NCOUNTERS = 16 };
+enum { C_NNEXT = 0, C_NEX, C_NPEND, C_NREADY, C_NSING, C_NCLUS, C_NNXT, C_NDONE, C_NK, C_NP, C_NPC, C_NCOUNTERS = 16 };
 
 }  // namespace
 
@@ -89,12 +90,15 @@ struct mrrr_ctx {
   int mmax = 16;
   int chains_per_thread = 1;
   bool neg_tma = true;  // x-NegCount with TMA-staged representation tiles (k_negcount_tma)
+  bool guided = false;  // guided rounds for isolated nodes (kernels_guided.cuh); MRRR_GUIDED=1 (C2: fewer rounds, more FP64 work: slower)
+  int bud_full = 15, bud_tube = 40;  // tube point budgets: no estimate (4 full levels) / with estimate
   bool rqi_pair = true;
   bool l2_persist = true;
   long long l2_max_window = 0;
 
   // buffers
   Buf starts, scal, binfo, bside, blist, cab, mx, my, mq, lscratch, reps, rlo, rhi, colmap, gstart;
+  Buf nodesK, nodesP, offsP, dS, dG, dH;  // guided bisection rounds
   Buf nodesA, nodesB, counts, ex, excounts, exmap, bnA, bnB, sing, clusA, clusB, ss, gval, valid, cseg, bnoff,
       ipool_lo, ipool_hi, yref_lo, yref_hi, wsA, wsB, stats, cnt, ddepth, dgf, dgl, dflo, dfhi, hd, he, hW, hZ, zmeta;
   int *h_cnt = nullptr;  // pinned counters
@@ -153,6 +157,7 @@ __global__ void k_root_nodes(const int *__restrict__ blist, int nbl, const int *
   nd.wlo = cab[2 * blk]; nd.whi = cab[2 * blk + 1];
   nd.rep = blk; nd.pad = 0;
   nd.obase = (long long)s - 1;
+  nd.est = NAN; nd.u = INFINITY;
   nodes[t] = nd;
   ex[t] = ExplicitChain{left ? P : -P, blk, 0};
 }
@@ -249,12 +254,14 @@ void launch_check(mrrr_t h) {
 
 // NegCount chains: node grid points then explicit (rep, sigma) chains; CH chains per thread (x path)
 template <bool Y>
-void launch_negcount(mrrr_t h, const Node *nodes, int nnode, int m, int nex) {
-  long long tot = (long long)nnode * ((1LL << m) - 1) + nex;
+void launch_negcount(mrrr_t h, const Node *nodes, int nnode, int m, int nex, const Node *nodesP = nullptr,
+                     int nP = 0, const int *offsP = nullptr, int nPc = 0, double rtol = 0.0) {
+  long long tot = (long long)nnode * ((1LL << m) - 1) + nPc + nex;
   if (!Y && h->neg_tma) {
     k_negcount_tma<<<nblocks_for(tot, 128), 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
-        nodes, nnode, m, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mx.as<double2>(),
-        h->counts.as<int>(), h->excounts.as<int>());
+        nodes, nnode, m, nodesP, nP, offsP, nPc, rtol, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(),
+        h->mx.as<double2>(), h->counts.as<int>(), h->excounts.as<int>(), h->dS.as<double>(), h->dG.as<double>(),
+        h->dH.as<double>());
     launch_check(h);
     return;
   }
@@ -277,10 +284,89 @@ void launch_negcount(mrrr_t h, const Node *nodes, int nnode, int m, int nex) {
   launch_check(h);
 }
 
+// Guided rounds (kernels_guided.cuh): isolated nodes evaluate a tube around a Laguerre estimate of their
+// eigenvalue instead of a full k-section subtree; the rest as in run_bisection.  Same intervals.
+void run_bisection_guided(mrrr_t h, int nnode, double *out_lo, double *out_hi, double rtol, int nverify,
+                          const int *blist_dev, int nbl, bool *restart) {
+  Node *cur = h->nodesA.as<Node>(), *nxt = h->nodesB.as<Node>();
+  bool first = true;
+  unsigned long long *alg = (unsigned long long *)(h->stats.as<long long>() + ST_NEGX_ALG);
+  while (nnode > 0) {
+    CK(h->nodesK.ensure(sizeof(Node) * nnode));
+    CK(h->nodesP.ensure(sizeof(Node) * nnode));
+    CK(h->offsP.ensure(sizeof(int) * (nnode + 1)));
+    zero_counters(h);
+    k_node_split<<<nblocks_for(nnode, 128), 128, 0, h->stream>>>(cur, nnode, h->nodesK.as<Node>(),
+                                                                h->cnt.as<int>() + C_NK, h->nodesP.as<Node>(),
+                                                                h->cnt.as<int>() + C_NP, h->bud_full, h->bud_tube);
+    launch_check(h);
+    read_counters(h);
+    const int nK = h->h_cnt[C_NK], nP = h->h_cnt[C_NP];
+    int nPc = 0;
+    if (nP > 0) {
+      k_tube_count<<<nblocks_for(nP, 128), 128, 0, h->stream>>>(h->nodesP.as<Node>(), nP, rtol, h->offsP.as<int>());
+      launch_check(h);
+      k_scan_excl<<<1, 1024, 0, h->stream>>>(h->offsP.as<int>(), nP, h->cnt.as<int>() + C_NPC);
+      launch_check(h);
+      read_counters(h);
+      nPc = h->h_cnt[C_NPC];
+    }
+    int m = 1;
+    const long long budget = std::max<long long>(h->target_chains - nPc, 0);
+    while (m < h->mmax && (long long)nK * ((1LL << (m + 1)) - 1) <= budget) m++;
+    const long long nKc = (long long)nK * ((1LL << m) - 1);
+    const int nex = first ? nverify : 0;
+    CK(h->counts.ensure(std::max<long long>(nKc + nPc, 1) * sizeof(int)));
+    CK(h->dS.ensure(sizeof(double) * std::max(nPc, 1)));
+    CK(h->dG.ensure(sizeof(double) * std::max(nPc, 1)));
+    CK(h->dH.ensure(sizeof(double) * std::max(nPc, 1)));
+    zero_counters(h);
+    CK(cudaEventRecord(h->nc0, h->stream));
+    launch_negcount<false>(h, h->nodesK.as<Node>(), nK, m, nex, h->nodesP.as<Node>(), nP, h->offsP.as<int>(), nPc,
+                           rtol);
+    CK(cudaEventRecord(h->nc1, h->stream));
+    if (nex > 0) {
+      k_root_verify<<<nblocks_for(nbl, 128), 128, 0, h->stream>>>(blist_dev, nbl, h->starts.as<int>(),
+                                                                  h->binfo.as<double>(), h->excounts.as<int>(),
+                                                                  h->cnt.as<int>() + C_NEX);
+      launch_check(h);
+    }
+    if (nK > 0) {
+      k_bisect_update<<<nblocks_for((long long)nK << m, 128), 128, 0, h->stream>>>(
+          h->nodesK.as<Node>(), nK, m, h->counts.as<int>(), nxt, h->cnt.as<int>() + C_NNEXT, out_lo, out_hi, rtol,
+          alg);
+      launch_check(h);
+    }
+    if (nP > 0) {
+      k_tube_update<<<nblocks_for(nP, 128), 128, 0, h->stream>>>(
+          h->nodesP.as<Node>(), nP, h->offsP.as<int>(), h->counts.as<int>() + nKc, h->dS.as<double>(),
+          h->dG.as<double>(), h->dH.as<double>(), h->reps.as<RepDesc>(), nxt, h->cnt.as<int>() + C_NNEXT, out_lo,
+          out_hi, rtol, alg);
+      launch_check(h);
+    }
+    read_counters(h);
+    h->host_rounds++;
+    h->stats_h[ST_NEGX] += nKc + nPc + nex;
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, h->nc0, h->nc1));
+    h->neg_ms += ms;
+    h->neg_launches++;
+    if (nex > 0 && h->h_cnt[C_NEX] > 0) { *restart = true; return; }
+    nnode = h->h_cnt[C_NNEXT];
+    std::swap(cur, nxt);
+    first = false;
+    if (cur != h->nodesA.as<Node>() && cur != h->nodesB.as<Node>()) break;  // unreachable (ping-pong)
+  }
+}
+
 // shared-tree / k-section bisection rounds until every node is finished (S5, S8)
 template <bool Y>
 void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double rtol, int nverify,
                    const int *blist_dev, int nbl, bool *restart) {
+  if (!Y && h->guided && h->neg_tma) {
+    run_bisection_guided(h, nnode, out_lo, out_hi, rtol, nverify, blist_dev, nbl, restart);
+    return;
+  }
   Node *cur = h->nodesA.as<Node>(), *nxt = h->nodesB.as<Node>();
   bool first = true;
   while (nnode > 0) {
@@ -378,14 +464,15 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
   if (ns <= 0) return;
   l2_pin_reps(h, true);
   const bool pair = h->rqi_pair;
-  // workspace per singleton: pair kernel 6 dd planes, single-lane kernel 2
-  long long per = (pair ? 3LL : 2LL) * (long long)sizeof(dd) * std::max<long long>(nbmax, 1);
+  // workspace per singleton: pair kernel one dd plane (P0, reused for P2) + one fp64 plane (P1) = 24 B per row;
+  // single-lane kernel 2 dd planes
+  long long per = (pair ? 24LL : 2LL * (long long)sizeof(dd)) * std::max<long long>(nbmax, 1);
   long long budget = std::min<long long>(h->ws_limit / 2, 64LL << 30);
   long long bmax = std::max<long long>(32, budget / per);
   long long batch = std::min<long long>(ns, bmax);
   long long stride = (batch + 31) / 32 * 32;  // pairs launched per batch (grid padding)
   if (pair) {
-    CK(h->wsA.ensure((size_t)3 * stride * nbmax * sizeof(dd)));
+    CK(h->wsA.ensure((size_t)24 * stride * nbmax));
   } else {
     CK(h->wsA.ensure((size_t)stride * nbmax * sizeof(dd)));
     CK(h->wsB.ensure((size_t)stride * nbmax * sizeof(dd)));
@@ -403,7 +490,7 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
       launch_check(h);
       k_zwrite<<<nblocks_for(32 * nb, 256), 256, 0, h->stream>>>(
           h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(),
-          h->wsA.as<dd>() + 2 * stride * nbmax, nbmax, h->zmeta.as<ZMeta>(), Z, ldz);
+          h->wsA.as<dd>(), stride, h->zmeta.as<ZMeta>(), Z, ldz);
     } else {
       k_rqi<<<nblocks_for(nb, 64), 64, 0, h->stream>>>(
           h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>(),
@@ -484,23 +571,28 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
     k_clu_shift_init<<<nblocks_for(nc, 128), 128, 0, h->stream>>>(nc, h->yref_lo.as<double>(), h->yref_hi.as<double>(),
                                                                   h->ss.as<ShiftState>());
     launch_check(h);
-    for (int a = 0; a < MAX_ATTEMPTS; a++) {
+    // attempt 0 for every cluster, then the remaining attempts of the open clusters in one launch
+    CK(h->gval.ensure(sizeof(double) * 2LL * (MAX_ATTEMPTS - 1) * nc));
+    CK(h->valid.ensure(sizeof(int) * 2LL * (MAX_ATTEMPTS - 1) * nc));
+    for (int a0 = 0; a0 < MAX_ATTEMPTS;) {
+      const int na = (a0 == 0) ? 1 : MAX_ATTEMPTS - a0;
       CK(cudaMemsetAsync(h->cnt.as<int>() + C_NDONE, 0, sizeof(int), h->stream));
-      k_clu_attempt<<<nblocks_for(2LL * nc, 64), 64, 0, h->stream>>>(cl, nc, h->reps.as<RepDesc>(), h->my.as<YElt>(),
-                                                                     h->ss.as<ShiftState>(), h->gval.as<double>(),
-                                                                     h->valid.as<int>());
+      k_clu_attempt_multi<<<nblocks_for(2LL * na * nc, 64), 64, 0, h->stream>>>(
+          cl, nc, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->mq.as<QElt>(), h->ss.as<ShiftState>(), a0, na,
+          h->gval.as<double>(), h->valid.as<int>());
       launch_check(h);
-      k_clu_select<<<nblocks_for(nc, 128), 128, 0, h->stream>>>(cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(),
-                                                                h->gval.as<double>(), h->valid.as<int>(), a,
-                                                                h->cnt.as<int>() + C_NDONE, h->stats.as<long long>());
+      k_clu_select_multi<<<nblocks_for(nc, 128), 128, 0, h->stream>>>(
+          cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(), h->gval.as<double>(), h->valid.as<int>(), a0, na,
+          h->cnt.as<int>() + C_NDONE, h->stats.as<long long>());
       launch_check(h);
       read_counters(h);
       if (h->h_cnt[C_NDONE] >= nc) break;
+      a0 += na;
     }
     // (d) children
     k_clu_build<<<nblocks_for(nc, 64), 64, 0, h->stream>>>(cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(),
-                                                           h->mx.as<double2>(), h->my.as<YElt>(), repbase, poolbase,
-                                                           (int)nbmax);
+                                                           h->mx.as<double2>(), h->my.as<YElt>(), h->mq.as<QElt>(),
+                                                           repbase, poolbase, (int)nbmax);
     launch_check(h);
     k_build_q<<<nc, 256, 0, h->stream>>>(h->reps.as<RepDesc>(), nullptr, repbase, nc, h->my.as<YElt>(),
                                          h->mq.as<QElt>());
@@ -881,6 +973,9 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_MMAX")) h->mmax = atoi(s);
     if (const char *s = getenv("MRRR_CH")) h->chains_per_thread = std::max(1, std::min(4, atoi(s)));
     if (const char *s = getenv("MRRR_NEGTMA")) h->neg_tma = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_GUIDED")) h->guided = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_BUD_FULL")) h->bud_full = std::max(1, atoi(s));
+    if (const char *s = getenv("MRRR_BUD_TUBE")) h->bud_tube = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;
     if (const char *s = getenv("MRRR_L2PIN")) h->l2_persist = atoi(s) != 0;
     {
@@ -1068,7 +1163,7 @@ int mrrr_destroy(mrrr_t h) {
   if (!h) return 0;
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->stream);
-  Buf *bufs[] = {&h->starts, &h->scal, &h->binfo, &h->bside, &h->blist, &h->cab, &h->mx, &h->my, &h->mq, &h->lscratch,
+  Buf *bufs[] = {&h->starts, &h->scal, &h->binfo, &h->bside, &h->blist, &h->cab, &h->mx, &h->my, &h->mq, &h->nodesK, &h->nodesP, &h->offsP, &h->dS, &h->dG, &h->dH, &h->lscratch,
                  &h->reps, &h->rlo, &h->rhi, &h->colmap, &h->gstart, &h->nodesA, &h->nodesB, &h->counts, &h->ex,
                  &h->excounts, &h->exmap, &h->bnA, &h->bnB, &h->sing, &h->clusA, &h->clusB, &h->ss, &h->gval,
                  &h->valid, &h->cseg, &h->bnoff, &h->ipool_lo, &h->ipool_hi, &h->yref_lo, &h->yref_hi, &h->wsA,

@@ -99,6 +99,24 @@ class Clocks:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ncu_traffic(kernel_prefix: str, workload: str):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum, median over the captured launches)
+    of a kernel from the committed ncu --set full summary of this workload (profiles/ncu_summary_*.json)."""
+    import glob
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_summary_*.json"))):
+        try:
+            js = json.load(open(f))
+        except Exception:
+            continue
+        if js.get("workload") != workload:
+            continue
+        v = [e["dram_bytes"] for e in js.get("launches", []) if e.get("kernel", "").startswith(kernel_prefix)]
+        if v:
+            best = (float(np.median(v)), os.path.relpath(f, ROOT) + f" ({len(v)} launches, ncu --set full)")
+    return best if best else (None, None)
+
+
 def flush_l2(buf):
     buf.fill_(1.0)  # 256 MiB > 126 MB L2
 
@@ -251,19 +269,20 @@ def main():
         if rq_n:
             launch_ms = rq_ms / rq_n
             f = fl.rqi_flops(stats, n, wdiv) / nrq
-            cands.append(("k_rqi2+k_zwrite (singleton RQI + eigenvectors)", launch_ms, f, rq_ms))
+            cands.append(("k_rqi2 (+k_zwrite; singleton RQI + eigenvectors)", launch_ms, f, rq_ms))
         if tphase["negcount_launches"]:
             launch_ms = tphase["negcount_ms_per_launch"]
             nl = tphase["negcount_launches"]
             f = fl.negcount_flops(stats, n, wdiv) / nl
-            cands.append(("k_negcount (x-bisection, shared-tree k-section)", launch_ms, f, launch_ms * nl * args.steps))
+            cands.append(("k_negcount_tma (x-bisection, shared-tree k-section)", launch_ms, f, launch_ms * nl * args.steps))
         cands.sort(key=lambda c: -c[3])
         out = []
         for name, launch_ms, f, _ in cands:
             ach = f / (launch_ms * 1e-3) / 1e12
+            tr, trs = ncu_traffic(name.split()[0], cfg.name)
             out.append({"bound": "alu", "kernel": name, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                        "frac": ach / peak, "traffic": None, "peak_src": src, "launch_ms": launch_ms,
-                        "flops_per_launch": f})
+                        "frac": ach / peak, "traffic": tr, "traffic_src": trs, "peak_src": src,
+                        "launch_ms": launch_ms, "flops_per_launch": f})
         roof = out[0] if out else None
         roof_other = out[1:] if len(out) > 1 else None
 
@@ -272,17 +291,19 @@ def main():
         import torch as _t
         hd = _t.from_numpy(d_np).pin_memory().numpy()
         he = _t.from_numpy(e_np).pin_memory().numpy()
+        hW = _t.empty(k, dtype=_t.float64).pin_memory().numpy()     # page-locked result buffers
+        hZ = _t.empty((k, n), dtype=_t.float64).pin_memory().numpy()
         hs = mrrr.Solver(device=local)
-        hs.eig_host(hd, he, cfg.il, cfg.iu)
+        hs.eig_host(hd, he, cfg.il, cfg.iu, W=hW, Zt=hZ)
         t0 = time.perf_counter()
         reps = max(1, min(args.steps, 3))
         for _ in range(reps):
-            Wh, Zh = hs.eig_host(hd, he, cfg.il, cfg.iu)
+            Wh, Zh = hs.eig_host(hd, he, cfg.il, cfg.iu, W=hW, Zt=hZ)
         te = (time.perf_counter() - t0) / reps
         hs.close()
         e2e = {"value": k * n / te, "unit": UNIT, "h2d_bytes_per_step": 8 * (2 * n - 1),
                "d2h_bytes_per_step": 8 * k + 8 * k * n, "ms_per_step": te * 1e3,
-               "path": "mrrr_eig_host (pageable-or-pinned host in/out, device workspace cached)"}
+               "path": "mrrr_eig_host: pinned host d, e in, pinned host W, Z out; H2D + solve + D2H timed (wall clock)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

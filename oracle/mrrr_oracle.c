@@ -548,7 +548,9 @@ static void rqi_singleton(const rep_t *M, int64_t j, double lo, double hi, doubl
     if (r == 0 || !finiteq(zz) || zz == 0) break;
     qreal nz = sqrtq(zz);
     qreal resid = fabsq(gamma) / nz, rqc = gamma / zz;
-    if ((double)resid <= thr1 || fabsq(rqc) < 4 * EPS_Y * fabsq(lam)) { accepted = 1; break; }
+    /* tol2: |RQC| < 4 eps_y |lam|, not below the representation's y-rounding 2^-100 spdiam (A-30) */
+    qreal tol2 = fmaxq(4 * EPS_Y * fabsq(lam), 0x1p-100Q * (qreal)M->spdiam);
+    if ((double)resid <= thr1 || fabsq(rqc) < tol2) { accepted = 1; break; }
     if (c < j) blo = lam; else bhi = lam;
     qreal nl = lam + rqc;
     int ok = ((c < j) ? (rqc > 0) : (rqc < 0)) && (blo < nl) && (nl < bhi);

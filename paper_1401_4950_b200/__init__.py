@@ -149,16 +149,23 @@ class Solver:
         self._last = (n, k)
         return W, Zt.T
 
-    def eig_host(self, d: np.ndarray, e: np.ndarray, il: int | None = None, iu: int | None = None):
-        """Host solve (copies inside the timed call).  Returns numpy (W, Z[n, k])."""
+    def eig_host(self, d: np.ndarray, e: np.ndarray, il: int | None = None, iu: int | None = None,
+                 W: np.ndarray | None = None, Zt: np.ndarray | None = None):
+        """Host solve (copies inside the call): d, e host arrays in, (W, Z[n, k]) host arrays out.  W (k,) and
+        Zt (k, n) may be supplied (e.g. page-locked buffers for full-speed copies)."""
         d = np.ascontiguousarray(d, dtype=np.float64)
         n = d.size
         e = np.ascontiguousarray(e, dtype=np.float64) if n > 1 else np.zeros(1)
         il = 1 if il is None else int(il)
         iu = n if iu is None else int(iu)
         k = iu - il + 1
-        W = np.empty(k)
-        Zt = np.empty((k, n))
+        if W is None:
+            W = np.empty(k)
+        if Zt is None:
+            Zt = np.empty((k, n))
+        if W.shape != (k,) or Zt.shape != (k, n) or W.dtype != np.float64 or Zt.dtype != np.float64 \
+                or not (W.flags.c_contiguous and Zt.flags.c_contiguous):
+            raise MrrrError("W must be float64 (k,), Zt float64 C-contiguous (k, n)")
         rc = load().mrrr_eig_host(self._h, d.ctypes.data, e.ctypes.data, n, il, iu, W.ctypes.data, Zt.ctypes.data, n)
         _check(rc, "mrrr_eig_host")
         self._last = (n, k)

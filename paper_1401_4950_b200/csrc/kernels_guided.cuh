@@ -141,3 +141,69 @@ __global__ void k_tube_update(const Node *__restrict__ P, int nP, const int *__r
   }
   next[atomicAdd(nnext, 1)] = c;
 }
+
+// ---------------------------------------------------------------------------
+// Representation-grouped k-section rounds (child bisection, S8(e)): the nodes of a round are sorted by
+// representation so that every CTA evaluates chains of ONE child representation and streams it once
+// through shared memory by TMA (instead of every chain reading its own copy from HBM).
+// ---------------------------------------------------------------------------
+__global__ void k_rep_hist(const Node *__restrict__ nodes, int nnode, int rep0, int *hist) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nnode) atomicAdd(&hist[nodes[i].rep - rep0], 1);
+}
+__global__ void k_rep_scatter(const Node *__restrict__ nodes, int nnode, int rep0, int *cursor, Node *sorted) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nnode) return;
+  const Node nd = nodes[i];
+  sorted[atomicAdd(&cursor[nd.rep - rep0], 1)] = nd;
+}
+__global__ void k_rep_ctas(const int *__restrict__ node_off, int nrep, long long P, int *ctas) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < nrep) ctas[r] = (int)(((long long)(node_off[r + 1] - node_off[r]) * P + 127) / 128);
+}
+
+__global__ void __launch_bounds__(128) k_negcount_grp(const Node *__restrict__ nodes, int m,
+                                                      const int *__restrict__ node_off,
+                                                      const int *__restrict__ cta_off, int nrep,
+                                                      const RepDesc *__restrict__ reps,
+                                                      const double2 *__restrict__ mx, int *counts) {
+  extern __shared__ __align__(128) unsigned char neg_smem[];
+  double2 *buf = reinterpret_cast<double2 *>(neg_smem);
+  __shared__ __align__(8) uint64_t bar[2];
+  const int b = blockIdx.x;
+  int lo = 0, hi = nrep - 1;  // representation r with cta_off[r] <= b < cta_off[r + 1]
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (cta_off[mid] <= b) lo = mid; else hi = mid - 1;
+  }
+  const int r = lo;
+  const long long P = (1LL << m) - 1;
+  const long long nc = (long long)(node_off[r + 1] - node_off[r]) * P;
+  const long long cr = (long long)(b - cta_off[r]) * 128 + threadIdx.x;
+  const bool act = cr < nc;
+  const long long crc = act ? cr : nc - 1;
+  const long long node = node_off[r] + crc / P;
+  const int pt = (int)(crc % P) + 1;
+  const Node nd = nodes[node];
+  const double sig = node_point(nd, m, pt);
+  const RepDesc R = reps[nd.rep];
+  const double2 *M = mx + R.off;
+  const int nb = R.nb;
+  const int ntile = (nb + NEG_TILE - 1) / NEG_TILE;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int t = 0; t < 2 && t < ntile; t++) {
+      int len = min(NEG_TILE, nb - t * NEG_TILE);
+      tma_load_1d(buf + t * NEG_TILE, M + (long long)t * NEG_TILE, (unsigned)(len * sizeof(double2)), &bar[t]);
+    }
+  }
+  __syncthreads();
+  int cnt;
+  bool ok;
+  double G, H;
+  neg_tiles<false>(buf, bar, M, nb, ntile, sig, cnt, ok, G, H);
+  if (!ok) cnt = negcount_x_careful(M, nb, sig);
+  if (act) counts[node * P + pt - 1] = cnt;
+}

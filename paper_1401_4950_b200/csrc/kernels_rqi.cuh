@@ -11,8 +11,8 @@
 // n steps per lane and no separate argmin or z pass is needed inside the RQI.  Later iterations (twist
 // r fixed) run F on 0..r-1 and B on n-2..r and store l+ / u- for the final z solve.
 //
-// Workspace: planes [i * S + pair]: P0 (dd) = s(i) / t(i), P1 (fp64) = S_i / T_i (iteration 1, each
-// index written by exactly one lane), P2 = l+(i) for i < r and u-(i) for i >= r (in the pair's P0 column).
+// Workspace: dd planes [i * S + pair]: P0 = s(i) / t(i), P1 = S_i / T_i (iteration 1, each
+// index written by exactly one lane), P2 = l+(i) for i < r and u-(i) for i >= r (contiguous per pair).
 //
 // The hot loops use the branch-free dd operations (dd_*_nf); if a lane's recurrence leaves the finite
 // range (a zero pivot: IEEE infinity) the pass is rerun with the careful operations,
@@ -42,12 +42,6 @@ template <bool C> __device__ __forceinline__ dd OSUB(dd a, dd b) { if constexpr 
 template <bool C> __device__ __forceinline__ dd OMUL(dd a, dd b) { if constexpr (C) return dd_mul(a, b); else return dd_mul_nf(a, b); }
 template <bool C> __device__ __forceinline__ dd ORCP(dd a) { if constexpr (C) return dd_rcp(a); else return dd_rcp_nf(a); }
 template <bool C> __device__ __forceinline__ dd OADD1(dd a) { if constexpr (C) return dd_add_d(a, 1.0); else return dd_add_d_nf(a, 1.0); }
-
-// P1 plane (||z||^2 partial sums S_i / T_i of iteration 1) holds fp64: the twist candidates' norm only
-// feeds the RQC and the acceptance test (relative accuracy ~eps_x); the final norm comes from the
-// r-twisted (FIXED) pass in dd
-__device__ __forceinline__ void stw1(double *w, long long off, dd v) { __stcs(w + off, v.hi); }
-__device__ __forceinline__ dd ldw1(const double *w, long long off) { return dd_from(__ldcs(w + off)); }
 
 struct Elt3 {
   double2 a, b, c;
@@ -93,7 +87,7 @@ enum { PH_STORE = 0, PH_COMBINE = 1, PH_FIXED = 2 };
 // (phase B) the other lane's halves read PD steps ahead through compile-time-indexed rings.
 template <bool C, int MODE>
 __device__ __forceinline__ void run_phase(const YElt *__restrict__ y, int last, int k0, int k1, bool isB, int oa,
-                                          int oc, dd lam, int r, dd *P0, double *P1, dd *P2, long long S, dd &x, dd &acc,
+                                          int oc, dd lam, int r, dd *P0, dd *P1, dd *P2, long long S, dd &x, dd &acc,
                                           int &cnt, Cand &cd, dd &tr) {
   constexpr int PD = MRRR_RQI_PD;
   if (k0 >= k1) return;
@@ -106,7 +100,7 @@ __device__ __forceinline__ void run_phase(const YElt *__restrict__ y, int last, 
     er[u] = ld3(y, GIX(kk), oa, oc);
     if (MODE == PH_COMBINE) {
       pq[u] = ldw(P0, (long long)GIX(kk) * S);
-      ps[u] = ldw1(P1, (long long)GIX(kk) * S);
+      ps[u] = ldw(P1, (long long)GIX(kk) * S);
     }
   }
   for (int kb = k0; kb < k1; kb += PD) {
@@ -122,7 +116,7 @@ __device__ __forceinline__ void run_phase(const YElt *__restrict__ y, int last, 
           other = pq[u];
           ost = ps[u];
           pq[u] = ldw(P0, (long long)GIX(kn) * S);
-          ps[u] = ldw1(P1, (long long)GIX(kn) * S);
+          ps[u] = ldw(P1, (long long)GIX(kn) * S);
         }
         const int i = GIX(k);
         const dd c = D2(e0.c);
@@ -134,14 +128,14 @@ __device__ __forceinline__ void run_phase(const YElt *__restrict__ y, int last, 
           dd myst = isB ? accn : acc;
           if (MODE == PH_STORE) {
             stw(P0, (long long)i * S, mine);
-            stw1(P1, (long long)i * S, myst);
+            stw(P1, (long long)i * S, myst);
           } else {
             cand_take(cd, OADD<C>(mine, other), OADD<C>(myst, ost), i, isB);
           }
         } else {
           if (isB && k == k1 - 1) tr = OMUL<C>(OMUL<C>(c, rr), x);  // B's last row is r
-          if constexpr (C) stw(P2, (long long)i * S, (den.hi == 0.0) ? dd_mark() : out);
-          else stw(P2, (long long)i * S, out);
+          if constexpr (C) stw(P2, i, (den.hi == 0.0) ? dd_mark() : out);
+          else stw(P2, i, out);
         }
         cnt += dd_sb(den);
         x = xn;
@@ -157,7 +151,7 @@ __device__ __forceinline__ void run_phase(const YElt *__restrict__ y, int last, 
 // Returns false (both lanes) if the fast pass left the finite range.  On return (both lanes):
 // g.r, g.gamma = gamma_r, g.zz = ||z||^2 (NaN/inf if the closed form broke down), g.c = inertia (A-26).
 template <bool C>
-__device__ bool getvec_pair_t(const YElt *__restrict__ y, int nb, dd lam, int r, bool isB, dd *P0, double *P1, dd *P2,
+__device__ bool getvec_pair_t(const YElt *__restrict__ y, int nb, dd lam, int r, bool isB, dd *P0, dd *P1, dd *P2,
                               long long S, GV &g) {
   const unsigned pm = pair_mask();
   const int last = nb - 1;
@@ -326,8 +320,7 @@ __device__ __forceinline__ void q_step(dd den, const Q3 &e, dd lam, dd acc, dd &
 #define MRRR_RQI_RING 8
 #endif
 struct RingSlot {
-  double2 c2, dl, g, p0;
-  double p1, pad;
+  double2 c2, dl, g, p0, p1;
 };
 __device__ __forceinline__ void cp16(void *sdst, const void *gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
@@ -343,7 +336,7 @@ __device__ __forceinline__ void cp_wait() {
 
 template <int MODE>
 __device__ __forceinline__ void run_phase_q(const QElt *__restrict__ q, int last, int k0, int k1, bool isB, int og,
-                                            dd lam, dd *P0, double *P1, dd *P2, long long S, dd &den, dd &acc, int &cnt,
+                                            dd lam, dd *P0, dd *P1, dd *P2, long long S, dd &den, dd &acc, int &cnt,
                                             CandL &cd, dd &tr, bool &ok, RingSlot *ring) {
   constexpr int R = MRRR_RQI_RING;
   if (k0 >= k1) return;
@@ -356,7 +349,7 @@ __device__ __forceinline__ void run_phase_q(const QElt *__restrict__ q, int last
     cp16(&ring[slot].g, p + og);
     if (MODE == PH_COMBINE) {
       cp16(&ring[slot].p0, P0 + (long long)i * S);
-      cp8(&ring[slot].p1, P1 + (long long)i * S);
+      cp16(&ring[slot].p1, P1 + (long long)i * S);
     }
     cp_commit();
   };
@@ -372,7 +365,7 @@ __device__ __forceinline__ void run_phase_q(const QElt *__restrict__ q, int last
     dd other, ost;
     if (MODE == PH_COMBINE) {
       other = D2(ring[slot].p0);
-      ost = dd_from(ring[slot].p1);
+      ost = D2(ring[slot].p1);
     }
     const int i = GIX(k);
     dd P, out, dn, accn;
@@ -382,7 +375,7 @@ __device__ __forceinline__ void run_phase_q(const QElt *__restrict__ q, int last
       const dd myst = isB ? accn : acc;
       if (MODE == PH_STORE) {
         stw(P0, (long long)i * S, mine);
-        stw1(P1, (long long)i * S, myst);
+        stw(P1, (long long)i * S, myst);
       } else {
         // gamma_i = d+(i) - c2(i)/omega(i+1): F holds the first term, B the second
         if (isB) candl_take(cd, other, mine, ost, myst, i, true);
@@ -390,7 +383,7 @@ __device__ __forceinline__ void run_phase_q(const QElt *__restrict__ q, int last
       }
     } else {
       if (isB && k == k1 - 1) tr = fast_two_sum(P.hi, P.lo);  // B's last row is r: c2(r)/omega(r+1)
-      stw(P2, (long long)i * S, out);
+      stw(P2, i, out);
     }
     cnt += dd_sb(den);
     den = dn;
@@ -402,7 +395,7 @@ __device__ __forceinline__ void run_phase_q(const QElt *__restrict__ q, int last
 }
 
 // one Getvec of the pair on the RQI form; returns false (both lanes) if the careful pass is needed
-__device__ bool getvec_pair_q(const QElt *__restrict__ q, int nb, dd lam, int r, bool isB, dd *P0, double *P1, dd *P2,
+__device__ bool getvec_pair_q(const QElt *__restrict__ q, int nb, dd lam, int r, bool isB, dd *P0, dd *P1, dd *P2,
                               long long S, GV &g) {
   extern __shared__ __align__(16) unsigned char rqi_smem[];
   RingSlot *ring = reinterpret_cast<RingSlot *>(rqi_smem) + threadIdx.x * MRRR_RQI_RING;
@@ -476,7 +469,7 @@ __device__ bool getvec_pair_q(const QElt *__restrict__ q, int nb, dd lam, int r,
 
 // returns true if the careful (IEEE special value) pass had to run
 __device__ __forceinline__ bool getvec_pair_any(const YElt *__restrict__ y, const QElt *__restrict__ qy, int nb, dd lam,
-                                                int r, bool isB, dd *P0, double *P1, dd *P2, long long S, GV &g) {
+                                                int r, bool isB, dd *P0, dd *P1, dd *P2, long long S, GV &g) {
   if (getvec_pair_q(qy, nb, lam, r, isB, P0, P1, P2, S, g)) return false;
   getvec_pair_t<true>(y, nb, lam, r, isB, P0, P1, P2, S, g);
   return true;
@@ -513,10 +506,10 @@ __global__ void __launch_bounds__(256) k_zwrite(const Singleton *__restrict__ sg
   const RepDesc R = reps[s.rep];
   const int nb = R.nb, r = m.r, last = nb - 1;
   const dd inv = dd_make(m.inv_hi, m.inv_lo);
-  const dd *P = P2base + w;  // column w of the strided P2 plane (row stride S)
+  const dd *P = P2base + (long long)w * S;  // P2 of pair w (contiguous, S = nbmax here)
   double *Zc = Z + (long long)s.col * ldz + R.bstart;
   if (m.careful) {
-    if (lane == 0) zsolve(my + R.off, nb, r, P, P, S, inv, Zc);
+    if (lane == 0) zsolve(my + R.off, nb, r, P, P, 1, inv, Zc);
     return;
   }
   if (lane == 0) Zc[r] = inv.hi;
@@ -528,7 +521,7 @@ __global__ void __launch_bounds__(256) k_zwrite(const Singleton *__restrict__ sg
       const int mm = m0 + lane;
       const bool valid = mm < len;
       const int src = side ? (r + mm) : (r - 1 - mm);
-      dd v = valid ? dd_neg(ldw(P, (long long)src * S)) : dd_from(1.0);
+      dd v = valid ? dd_neg(ldw(P, src)) : dd_from(1.0);
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
         dd o = shfl_up_dd(v, off);
@@ -556,10 +549,9 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
   const YElt *y = my + R.off;
   const QElt *qy = mq + R.off;
   const long long plane = nbmax * S;
-  // P0 (dd) and P1 (fp64) planes [row * S + pair]; P2 (l+/u- of the r-twisted pass) reuses the pair's P0
-  // column: it is written only after the pair's last twist-search pass has read P0
-  dd *P0 = ws + pid, *P2 = P0;
-  double *P1 = reinterpret_cast<double *>(ws + plane) + pid;
+  // P0, P1 planes [row * S + pair]; P2 (l+/u- of the r-twisted pass) contiguous per pair (k_zwrite reads
+  // it row-parallel within a warp)
+  dd *P0 = ws + pid, *P1 = ws + plane + pid, *P2 = ws + 2 * plane + (long long)pid * nbmax;
   double mid = bis_mid(s.lo, s.hi);
   double nu = __dmul_rn(__dmul_rn(100.0, (double)nb), EPS_X);
   dd blo = dd_from(__dsub_rn(s.lo, __dmul_rn(nu, fabs(s.lo))));
@@ -582,14 +574,17 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
     if (!isfinite(zz.hi)) {  // closed form broke down (overflow / zero pivot): explicit z solve (A-25)
       if (!lu_valid) { careful = getvec_pair_any(y, qy, nb, lam, r, isB, P0, P1, P2, S, g); lu_valid = true; qd += nb - 1; }
       zs += nb - 1;
-      if (!isB) zz = zsolve(y, nb, r, P2, P2, S, dd_from(0.0), nullptr);
+      if (!isB) zz = zsolve(y, nb, r, P2, P2, 1, dd_from(0.0), nullptr);
       zz = shfl_dd_from(zz, lane_F());
     }
     if (!isfinite(zz.hi) || zz.hi == 0.0) break;
     dd nz = dd_sqrt(zz);
     dd resid = dd_div(dd_abs(g.gamma), nz);
     dd rqc = dd_div(g.gamma, zz);
-    if (resid.hi <= thr1 || dd_lt(dd_abs(rqc), dd_mul_d(dd_abs(lam), 4.0 * EPS_Y))) { accepted = true; break; }
+    // tol2: |RQC| < 4 eps_y |lam|, not below the representation's y-rounding 2^-100 spdiam (A-30)
+    dd tol2 = dd_mul_d(dd_abs(lam), 4.0 * EPS_Y);
+    if (dd_lt(tol2, dd_from(__dmul_rn(0x1p-100, R.spdiam)))) tol2 = dd_from(__dmul_rn(0x1p-100, R.spdiam));
+    if (resid.hi <= thr1 || dd_lt(dd_abs(rqc), tol2)) { accepted = true; break; }
     if (g.c < j) blo = lam; else bhi = lam;
     dd nl = dd_add(lam, rqc);
     const bool sgn = (g.c < j) ? (rqc.hi > 0.0) : (rqc.hi < 0.0);
@@ -623,7 +618,7 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
   }
   if (!isfinite(zz.hi) || zz.hi == 0.0) {
     zs += nb - 1;
-    if (!isB) zz = zsolve(y, nb, r, P2, P2, S, dd_from(0.0), nullptr);
+    if (!isB) zz = zsolve(y, nb, r, P2, P2, 1, dd_from(0.0), nullptr);
     zz = shfl_dd_from(zz, lane_F());
   }
   dd inv = dd_rcp(dd_sqrt(zz));

@@ -688,7 +688,9 @@ __global__ void __launch_bounds__(64) k_rqi(const Singleton *__restrict__ sg, in
     nz = dd_sqrt(zz);
     dd resid = dd_div(dd_abs(g.gamma), nz);
     dd rqc = dd_div(g.gamma, zz);
-    if (resid.hi <= thr1 || dd_lt(dd_abs(rqc), dd_mul_d(dd_abs(lam), 4.0 * EPS_Y))) { accepted = true; break; }
+    dd tol2 = dd_mul_d(dd_abs(lam), 4.0 * EPS_Y);  // A-30 floor as in k_rqi2
+    if (dd_lt(tol2, dd_from(__dmul_rn(0x1p-100, R.spdiam)))) tol2 = dd_from(__dmul_rn(0x1p-100, R.spdiam));
+    if (resid.hi <= thr1 || dd_lt(dd_abs(rqc), tol2)) { accepted = true; break; }
     if (g.c < j) blo = lam; else bhi = lam;
     dd nl = dd_add(lam, rqc);
     bool ok = ((g.c < j) ? (rqc.hi > 0.0) : (rqc.hi < 0.0)) && dd_lt(blo, nl) && dd_lt(nl, bhi);

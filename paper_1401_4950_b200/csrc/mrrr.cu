@@ -91,7 +91,8 @@ struct mrrr_ctx {
   int chains_per_thread = 1;
   bool neg_tma = true;  // x-NegCount with TMA-staged representation tiles (k_negcount_tma)
   bool guided = false;  // guided rounds for isolated nodes (kernels_guided.cuh); MRRR_GUIDED=1 (C2: fewer rounds, more FP64 work: slower)
-  int bud_full = 15, bud_tube = 40;  // tube point budgets: no estimate (4 full levels) / with estimate
+  int bud_full = 15, bud_tube = 40;
+  bool grouped = true;  // child bisection with CTAs grouped by representation (k_negcount_grp)  // tube point budgets: no estimate (4 full levels) / with estimate
   bool rqi_pair = true;
   bool l2_persist = true;
   long long l2_max_window = 0;
@@ -99,6 +100,7 @@ struct mrrr_ctx {
   // buffers
   Buf starts, scal, binfo, bside, blist, cab, mx, my, mq, lscratch, reps, rlo, rhi, colmap, gstart;
   Buf nodesK, nodesP, offsP, dS, dG, dH;  // guided bisection rounds
+  Buf repoff, repcur, repcta;             // representation-grouped rounds
   Buf nodesA, nodesB, counts, ex, excounts, exmap, bnA, bnB, sing, clusA, clusB, ss, gval, valid, cseg, bnoff,
       ipool_lo, ipool_hi, yref_lo, yref_hi, wsA, wsB, stats, cnt, ddepth, dgf, dgl, dflo, dfhi, hd, he, hW, hZ, zmeta;
   int *h_cnt = nullptr;  // pinned counters
@@ -359,10 +361,80 @@ void run_bisection_guided(mrrr_t h, int nnode, double *out_lo, double *out_hi, d
   }
 }
 
+template <bool Y>
+void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double rtol, int nverify,
+                   const int *blist_dev, int nbl, bool *restart, int rep0 = -1, int nrep = 0);
+
+// k-section rounds with the nodes grouped by representation (child bisection over many child RRRs)
+void run_bisection_grouped(mrrr_t h, int nnode, double *out_lo, double *out_hi, double rtol, int rep0, int nrep) {
+  Node *cur = h->nodesA.as<Node>(), *nxt = h->nodesB.as<Node>();
+  unsigned long long *alg = (unsigned long long *)(h->stats.as<long long>() + ST_NEGX_ALG);
+  CK(h->repoff.ensure(sizeof(int) * (nrep + 1)));
+  CK(h->repcur.ensure(sizeof(int) * (nrep + 1)));
+  CK(h->repcta.ensure(sizeof(int) * (nrep + 1)));
+  while (nnode > 0) {
+    CK(h->nodesK.ensure(sizeof(Node) * nnode));
+    int m = 1;
+    while (m < h->mmax && (long long)nnode * ((1LL << (m + 1)) - 1) <= h->target_chains) m++;
+    const long long P = (1LL << m) - 1;
+    if ((long long)nnode * P < 64LL * nrep) {
+      // few chains per representation (e.g. thousands of 2-clusters): a CTA per representation would run
+      // latency-bound waves; the per-thread kernel is faster there
+      bool dummy = false;
+      if (cur != h->nodesA.as<Node>())
+        CK(cudaMemcpyAsync(h->nodesA.p, cur, sizeof(Node) * nnode, cudaMemcpyDeviceToDevice, h->stream));
+      run_bisection<false>(h, nnode, out_lo, out_hi, rtol, 0, nullptr, 0, &dummy);
+      return;
+    }
+    zero_counters(h);
+    CK(cudaMemsetAsync(h->repoff.p, 0, sizeof(int) * (nrep + 1), h->stream));
+    k_rep_hist<<<nblocks_for(nnode, 128), 128, 0, h->stream>>>(cur, nnode, rep0, h->repoff.as<int>());
+    launch_check(h);
+    k_scan_excl<<<1, 1024, 0, h->stream>>>(h->repoff.as<int>(), nrep, h->cnt.as<int>() + C_NPC);
+    launch_check(h);
+    CK(cudaMemcpyAsync(h->repcur.p, h->repoff.p, sizeof(int) * (nrep + 1), cudaMemcpyDeviceToDevice, h->stream));
+    k_rep_scatter<<<nblocks_for(nnode, 128), 128, 0, h->stream>>>(cur, nnode, rep0, h->repcur.as<int>(),
+                                                                 h->nodesK.as<Node>());
+    launch_check(h);
+    k_rep_ctas<<<nblocks_for(nrep, 128), 128, 0, h->stream>>>(h->repoff.as<int>(), nrep, P, h->repcta.as<int>());
+    launch_check(h);
+    k_scan_excl<<<1, 1024, 0, h->stream>>>(h->repcta.as<int>(), nrep, h->cnt.as<int>() + C_NK);
+    launch_check(h);
+    read_counters(h);
+    const int ncta = h->h_cnt[C_NK];
+    const long long nch = (long long)nnode * P;
+    CK(h->counts.ensure(std::max<long long>(nch, 1) * sizeof(int)));
+    zero_counters(h);
+    CK(cudaEventRecord(h->nc0, h->stream));
+    k_negcount_grp<<<ncta, 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
+        h->nodesK.as<Node>(), m, h->repoff.as<int>(), h->repcta.as<int>(), nrep, h->reps.as<RepDesc>(),
+        h->mx.as<double2>(), h->counts.as<int>());
+    launch_check(h);
+    CK(cudaEventRecord(h->nc1, h->stream));
+    k_bisect_update<<<nblocks_for((long long)nnode << m, 128), 128, 0, h->stream>>>(
+        h->nodesK.as<Node>(), nnode, m, h->counts.as<int>(), nxt, h->cnt.as<int>() + C_NNEXT, out_lo, out_hi, rtol,
+        alg);
+    launch_check(h);
+    read_counters(h);
+    h->host_rounds++;
+    h->stats_h[ST_NEGX] += nch;
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, h->nc0, h->nc1));
+    h->neg_ms += ms;
+    h->neg_launches++;
+    nnode = h->h_cnt[C_NNEXT];
+    std::swap(cur, nxt);
+  }
+}
+
 // shared-tree / k-section bisection rounds until every node is finished (S5, S8)
 template <bool Y>
 void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double rtol, int nverify,
-                   const int *blist_dev, int nbl, bool *restart) {
+                   const int *blist_dev, int nbl, bool *restart, int rep0, int nrep) {
+  if (!Y && rep0 >= 0 && nrep > 1 && h->neg_tma && h->grouped) {
+    run_bisection_grouped(h, nnode, out_lo, out_hi, rtol, rep0, nrep);
+    return;
+  }
   if (!Y && h->guided && h->neg_tma) {
     run_bisection_guided(h, nnode, out_lo, out_hi, rtol, nverify, blist_dev, nbl, restart);
     return;
@@ -464,15 +536,14 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
   if (ns <= 0) return;
   l2_pin_reps(h, true);
   const bool pair = h->rqi_pair;
-  // workspace per singleton: pair kernel one dd plane (P0, reused for P2) + one fp64 plane (P1) = 24 B per row;
-  // single-lane kernel 2 dd planes
-  long long per = (pair ? 24LL : 2LL * (long long)sizeof(dd)) * std::max<long long>(nbmax, 1);
+  // workspace per singleton: pair kernel 3 dd planes (P0, P1, P2), single-lane kernel 2
+  long long per = (pair ? 3LL : 2LL) * (long long)sizeof(dd) * std::max<long long>(nbmax, 1);
   long long budget = std::min<long long>(h->ws_limit / 2, 64LL << 30);
   long long bmax = std::max<long long>(32, budget / per);
   long long batch = std::min<long long>(ns, bmax);
   long long stride = (batch + 31) / 32 * 32;  // pairs launched per batch (grid padding)
   if (pair) {
-    CK(h->wsA.ensure((size_t)24 * stride * nbmax));
+    CK(h->wsA.ensure((size_t)3 * stride * nbmax * sizeof(dd)));
   } else {
     CK(h->wsA.ensure((size_t)stride * nbmax * sizeof(dd)));
     CK(h->wsB.ensure((size_t)stride * nbmax * sizeof(dd)));
@@ -490,7 +561,7 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
       launch_check(h);
       k_zwrite<<<nblocks_for(32 * nb, 256), 256, 0, h->stream>>>(
           h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(),
-          h->wsA.as<dd>(), stride, h->zmeta.as<ZMeta>(), Z, ldz);
+          h->wsA.as<dd>() + 2 * stride * nbmax, nbmax, h->zmeta.as<ZMeta>(), Z, ldz);
     } else {
       k_rqi<<<nblocks_for(nb, 64), 64, 0, h->stream>>>(
           h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>(),
@@ -628,7 +699,7 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
     launch_check(h);
     int nrd = run_brackets<false>(h, (int)btot);
     run_bisection<false>(h, nrd, h->ipool_lo.as<double>(), h->ipool_hi.as<double>(), 1e-2 * h->gaptol, 0, nullptr, 0,
-                         &dummy);
+                         &dummy, repbase, nc);
     // (f) reclassify
     CK(h->sing.ensure(sizeof(Singleton) * std::max<long long>(btot, 1)));
     Buf NX;
@@ -974,6 +1045,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_CH")) h->chains_per_thread = std::max(1, std::min(4, atoi(s)));
     if (const char *s = getenv("MRRR_NEGTMA")) h->neg_tma = atoi(s) != 0;
     if (const char *s = getenv("MRRR_GUIDED")) h->guided = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_GROUPED")) h->grouped = atoi(s) != 0;
     if (const char *s = getenv("MRRR_BUD_FULL")) h->bud_full = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_BUD_TUBE")) h->bud_tube = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;
@@ -1163,7 +1235,7 @@ int mrrr_destroy(mrrr_t h) {
   if (!h) return 0;
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->stream);
-  Buf *bufs[] = {&h->starts, &h->scal, &h->binfo, &h->bside, &h->blist, &h->cab, &h->mx, &h->my, &h->mq, &h->nodesK, &h->nodesP, &h->offsP, &h->dS, &h->dG, &h->dH, &h->lscratch,
+  Buf *bufs[] = {&h->starts, &h->scal, &h->binfo, &h->bside, &h->blist, &h->cab, &h->mx, &h->my, &h->mq, &h->nodesK, &h->nodesP, &h->offsP, &h->dS, &h->dG, &h->dH, &h->repoff, &h->repcur, &h->repcta, &h->lscratch,
                  &h->reps, &h->rlo, &h->rhi, &h->colmap, &h->gstart, &h->nodesA, &h->nodesB, &h->counts, &h->ex,
                  &h->excounts, &h->exmap, &h->bnA, &h->bnB, &h->sing, &h->clusA, &h->clusB, &h->ss, &h->gval,
                  &h->valid, &h->cseg, &h->bnoff, &h->ipool_lo, &h->ipool_hi, &h->yref_lo, &h->yref_hi, &h->wsA,

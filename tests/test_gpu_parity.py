@@ -288,3 +288,19 @@ def test_division_fast_path_is_ieee(torch_cuda):
     # the branch-free NegCount division must be bit-identical to __ddiv_rn
     import paper_1401_4950_b200 as m
     assert m.selftest(1, 1 << 28, 12345) == 0
+
+
+@pytest.mark.parametrize("env", [{"MRRR_GUIDED": "1"}, {"MRRR_GROUPED": "0"}, {"MRRR_NEGTMA": "0"},
+                                 {"MRRR_TARGET_CHAINS": "8192"}])
+def test_bisection_schedules_are_bit_identical(torch_cuda, env, monkeypatch):
+    # every evaluation schedule (k-section budget, TMA staging, representation-grouped child rounds, guided
+    # tube rounds) must reproduce the oracle's sequential Alg. Bisection intervals bit for bit (rule W)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for d, e in (mi.random_tridiag(2000, 17, -1.0), mi.wilkinson(200), mi.glued_wilkinson(6, 40, 1e-10)):
+        g = gpu_solve(torch_cuda, d, e)
+        r = oracle.mrrr(d, e)
+        check_integers(g, r)
+        tn = max(abs(r.W[0]), abs(r.W[-1]))
+        check_tol(d, e, g["W"], g["Z"], r.W, tn)
+        g["solver"].close()

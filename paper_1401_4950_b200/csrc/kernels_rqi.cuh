@@ -355,17 +355,30 @@ __device__ __forceinline__ void run_phase_q(const QElt *__restrict__ q, int last
   };
 #pragma unroll
   for (int u = 0; u < R; u++) issue(k0 + u, u);
+  // registers hold the current row; the next row is read from shared memory one step ahead
+  cp_wait<R - 1>();
+  Q3 en;
+  dd on = dd_from(0.0), osn = dd_from(0.0);
+  en.c2 = ring[0].c2;
+  en.dl = ring[0].dl;
+  en.g = ring[0].g;
+  if (MODE == PH_COMBINE) {
+    on = D2(ring[0].p0);
+    osn = D2(ring[0].p1);
+  }
+#pragma unroll 2
   for (int k = k0; k < k1; k++) {
     const int slot = (k - k0) & (R - 1);
-    cp_wait<R - 1>();
-    Q3 e0;
-    e0.c2 = ring[slot].c2;
-    e0.dl = ring[slot].dl;
-    e0.g = ring[slot].g;
-    dd other, ost;
+    const Q3 e0 = en;
+    const dd other = on, ost = osn;
+    cp_wait<R - 2>();  // the group of step k+1 has landed
+    const int sn = (slot + 1) & (R - 1);
+    en.c2 = ring[sn].c2;
+    en.dl = ring[sn].dl;
+    en.g = ring[sn].g;
     if (MODE == PH_COMBINE) {
-      other = D2(ring[slot].p0);
-      ost = D2(ring[slot].p1);
+      on = D2(ring[sn].p0);
+      osn = D2(ring[sn].p1);
     }
     const int i = GIX(k);
     dd P, out, dn, accn;
@@ -388,7 +401,7 @@ __device__ __forceinline__ void run_phase_q(const QElt *__restrict__ q, int last
     cnt += dd_sb(den);
     den = dn;
     acc = accn;
-    issue(k + R, slot);  // the slot's values are consumed: refill it R steps ahead
+    issue(k + R, slot);  // slot k was read into registers last step: refill it R steps ahead
   }
   cp_wait<0>();
 #undef GIX

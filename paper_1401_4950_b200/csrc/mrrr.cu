@@ -377,15 +377,10 @@ void run_bisection_grouped(mrrr_t h, int nnode, double *out_lo, double *out_hi, 
     int m = 1;
     while (m < h->mmax && (long long)nnode * ((1LL << (m + 1)) - 1) <= h->target_chains) m++;
     const long long P = (1LL << m) - 1;
-    if ((long long)nnode * P < 64LL * nrep) {
-      // few chains per representation (e.g. thousands of 2-clusters): a CTA per representation would run
-      // latency-bound waves; the per-thread kernel is faster there
-      bool dummy = false;
-      if (cur != h->nodesA.as<Node>())
-        CK(cudaMemcpyAsync(h->nodesA.p, cur, sizeof(Node) * nnode, cudaMemcpyDeviceToDevice, h->stream));
-      run_bisection<false>(h, nnode, out_lo, out_hi, rtol, 0, nullptr, 0, &dummy);
-      return;
-    }
+    // few chains per representation (e.g. thousands of 2-clusters): a CTA per representation would run
+    // latency-bound waves; then the per-thread kernel runs on the rep-sorted nodes (a warp's lanes share
+    // one or two representations, so their row loads coalesce)
+    const bool per_cta = (long long)nnode * P >= 64LL * nrep;
     zero_counters(h);
     CK(cudaMemsetAsync(h->repoff.p, 0, sizeof(int) * (nrep + 1), h->stream));
     k_rep_hist<<<nblocks_for(nnode, 128), 128, 0, h->stream>>>(cur, nnode, rep0, h->repoff.as<int>());
@@ -406,10 +401,14 @@ void run_bisection_grouped(mrrr_t h, int nnode, double *out_lo, double *out_hi, 
     CK(h->counts.ensure(std::max<long long>(nch, 1) * sizeof(int)));
     zero_counters(h);
     CK(cudaEventRecord(h->nc0, h->stream));
-    k_negcount_grp<<<ncta, 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
-        h->nodesK.as<Node>(), m, h->repoff.as<int>(), h->repcta.as<int>(), nrep, h->reps.as<RepDesc>(),
-        h->mx.as<double2>(), h->counts.as<int>());
-    launch_check(h);
+    if (per_cta) {
+      k_negcount_grp<<<ncta, 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
+          h->nodesK.as<Node>(), m, h->repoff.as<int>(), h->repcta.as<int>(), nrep, h->reps.as<RepDesc>(),
+          h->mx.as<double2>(), h->counts.as<int>());
+      launch_check(h);
+    } else {
+      launch_negcount<false>(h, h->nodesK.as<Node>(), nnode, m, 0);
+    }
     CK(cudaEventRecord(h->nc1, h->stream));
     k_bisect_update<<<nblocks_for((long long)nnode << m, 128), 128, 0, h->stream>>>(
         h->nodesK.as<Node>(), nnode, m, h->counts.as<int>(), nxt, h->cnt.as<int>() + C_NNEXT, out_lo, out_hi, rtol,

@@ -151,7 +151,7 @@ __device__ __forceinline__ void run_phase(const YElt *__restrict__ y, int last, 
 // Returns false (both lanes) if the fast pass left the finite range.  On return (both lanes):
 // g.r, g.gamma = gamma_r, g.zz = ||z||^2 (NaN/inf if the closed form broke down), g.c = inertia (A-26).
 template <bool C>
-__device__ bool getvec_pair_t(const YElt *__restrict__ y, int nb, dd lam, int r, bool isB, dd *P0, dd *P1, dd *P2,
+__device__ __noinline__ bool getvec_pair_t(const YElt *__restrict__ y, int nb, dd lam, int r, bool isB, dd *P0, dd *P1, dd *P2,
                               long long S, GV &g) {
   const unsigned pm = pair_mask();
   const int last = nb - 1;
@@ -408,7 +408,7 @@ __device__ __forceinline__ void run_phase_q(const QElt *__restrict__ q, int last
 }
 
 // one Getvec of the pair on the RQI form; returns false (both lanes) if the careful pass is needed
-__device__ bool getvec_pair_q(const QElt *__restrict__ q, int nb, dd lam, int r, bool isB, dd *P0, dd *P1, dd *P2,
+__device__ __noinline__ bool getvec_pair_q(const QElt *__restrict__ q, int nb, dd lam, int r, bool isB, dd *P0, dd *P1, dd *P2,
                               long long S, GV &g) {
   extern __shared__ __align__(16) unsigned char rqi_smem[];
   RingSlot *ring = reinterpret_cast<RingSlot *>(rqi_smem) + threadIdx.x * MRRR_RQI_RING;

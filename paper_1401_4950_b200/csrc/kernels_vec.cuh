@@ -591,7 +591,7 @@ __device__ void getvec_dd(const YElt *__restrict__ y, int nb, dd lam, int r, dd 
 // Backward branch (i = r-1 .. 0, uses l+ in B) then forward branch (i = r .. nb-2, uses u- in A),
 // as one loop over k with the workspace prefetched two steps ahead.  If Zc != nullptr writes
 // fl64(z_i * inv) to Zc[i].
-__device__ dd zsolve(const YElt *__restrict__ y, int nb, int r, const dd *A, const dd *B, long long S, dd inv,
+__device__ __noinline__ dd zsolve(const YElt *__restrict__ y, int nb, int r, const dd *A, const dd *B, long long S, dd inv,
                      double *Zc) {
   dd zz = dd_from(1.0);
   if (Zc) Zc[r] = inv.hi;
@@ -638,7 +638,7 @@ __device__ dd zsolve(const YElt *__restrict__ y, int nb, int r, const dd *A, con
 
 // y-bisection to relative width 2^-98 (RQI fallback)
 // stop at relative width 2^-98 of |lambda| or absolute width 2^-100 spdiam, whichever is larger (A-29)
-__device__ dd bisect_y_full(const YElt *__restrict__ y, const QElt *__restrict__ q, int nb, int j, dd lo, dd hi,
+__device__ __noinline__ dd bisect_y_full(const YElt *__restrict__ y, const QElt *__restrict__ q, int nb, int j, dd lo, dd hi,
                             double spdiam) {
   const dd afloor = dd_from(__dmul_rn(0x1p-100, spdiam));
   for (int it = 0; it < 200; it++) {

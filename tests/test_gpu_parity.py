@@ -180,6 +180,14 @@ def test_host_api_matches_device_api(torch_cuda):
     s = m.Solver()
     W, Z = s.eig_host(d, e)
     assert np.array_equal(W, g["W"]) and np.array_equal(Z, g["Z"])
+    # caller-supplied page-locked result buffers (the bench's e2e path), and a subset with ldz = n
+    hW = torch_cuda.empty(100, dtype=torch_cuda.float64).pin_memory().numpy()
+    hZ = torch_cuda.empty((100, d.size), dtype=torch_cuda.float64).pin_memory().numpy()
+    W2, Z2 = s.eig_host(d, e, 301, 400, W=hW, Zt=hZ)
+    assert W2 is hW or np.shares_memory(W2, hW)
+    assert np.array_equal(W2, g["W"][300:400]) and np.array_equal(Z2, g["Z"][:, 300:400])
+    with pytest.raises(m.MrrrError):
+        s.eig_host(d, e, 301, 400, W=np.empty(99), Zt=hZ)
 
 
 def test_shards_reproduce_full_solve(torch_cuda):

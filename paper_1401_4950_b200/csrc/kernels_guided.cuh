@@ -207,3 +207,176 @@ __global__ void __launch_bounds__(128) k_negcount_grp(const Node *__restrict__ n
   if (!ok) cnt = negcount_x_careful(M, nb, sig);
   if (act) counts[node * P + pt - 1] = cnt;
 }
+
+// ---------------------------------------------------------------------------
+// Segmented x-NegCount (latency splitting, bit-exact).  The stationary recurrence of Alg. negcountLDL,
+// s(i+1) = s(i) dll(i) / (d(i) + s(i)) - sigma, is strongly contracting on a positive definite root
+// (a perturbation of s(i) is multiplied by l+(i)^2): started W rows early from a guess, a segment's
+// trajectory becomes BIT-IDENTICAL to the true one within far fewer than W rows.  So a chain is split
+// into K segments evaluated concurrently: segment k (k >= 1) runs rows [b_k - W, b_k) from the guess
+// s = -sigma without counting, records its state s_in at row b_k, then counts rows [b_k, b_{k+1}) and
+// records s_out.  k_seg_combine accepts segment k only if s_in(k) equals, bit for bit, s_out(k-1) of an
+// accepted predecessor -- then every operation of the segment was applied to the same operands as in the
+// sequential recurrence, and its count is exact.  A chain with a mismatch (or a division that left the
+// fast range) is finished by k_seg_fallback from the last exact state with the IEEE operations.
+// The count is therefore identical to the sequential NegCount in every case; only the latency changes
+// (rows per lane: (nb-1)/K + W instead of nb-1).
+// ---------------------------------------------------------------------------
+struct SegOut {
+  double s_in, s_out;
+  int cnt, ok;
+};
+
+__global__ void __launch_bounds__(128) k_negcount_seg(const Node *__restrict__ nodes, int nnode, int m,
+                                                      const ExplicitChain *__restrict__ ex, int nex,
+                                                      const RepDesc *__restrict__ reps,
+                                                      const double2 *__restrict__ mx, int K, int L, int Wu,
+                                                      SegOut *seg, const int *__restrict__ dnn, int mmax,
+                                                      long long target) {
+  extern __shared__ __align__(128) unsigned char neg_smem[];
+  double2 *buf = reinterpret_cast<double2 *>(neg_smem);  // [2][NEG_TILE]
+  __shared__ __align__(8) uint64_t bar[2];
+  if (dnn) {  // device-driven round: node count and depth from the previous round
+    nnode = *dnn;
+    m = round_m(nnode, mmax, target);
+  }
+  const long long nn = (long long)nnode * ((1 << m) - 1);
+  const long long tot = nn + nex;
+  if ((long long)blockIdx.x * blockDim.x >= tot) return;  // whole CTA idle (uniform exit)
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = blockIdx.y;
+  const bool act = c < tot;
+  double sig;
+  int rep;
+  chain_of(nodes, m, nn, ex, act ? c : tot - 1, sig, rep);
+  const RepDesc R = reps[rep];  // one representation for the whole launch (root)
+  const int nb = R.nb;
+  const double2 *M = mx + R.off;
+  const int bk = min(k * L, nb - 1), ek = (k == K - 1) ? nb - 1 : min((k + 1) * L, nb - 1);
+  const int w0 = (k == 0) ? 0 : max(bk - Wu, 0);
+  const int r1 = (k == K - 1) ? nb : ek;  // staged rows [w0, r1): the last segment also stages row nb-1
+  const int nrow = r1 - w0;
+  const int ntile = (nrow + NEG_TILE - 1) / NEG_TILE;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int t = 0; t < 2 && t < ntile; t++) {
+      int len = min(NEG_TILE, nrow - t * NEG_TILE);
+      tma_load_1d(buf + t * NEG_TILE, M + w0 + (long long)t * NEG_TILE, (unsigned)(len * sizeof(double2)), &bar[t]);
+    }
+  }
+  __syncthreads();
+  double s = -sig, s_in = -sig;
+  int cnt = 0;
+  bool ok = true;
+  for (int t = 0; t < ntile; t++) {
+    const int b = t & 1;
+    mbar_wait(&bar[b], (unsigned)((t >> 1) & 1));
+    const double2 *T = buf + b * NEG_TILE;
+    const int row0 = w0 + t * NEG_TILE;
+    const int len = min(NEG_TILE, ek - row0);  // recurrence steps in this tile (rows < ek)
+    int kk = 0;
+    // warm-up rows (before bk): no counting
+    const int nw = max(0, min(len, bk - row0));
+    for (; kk < nw; kk++) {
+      const double2 mm = T[kk];
+      const double dp = __dadd_rn(mm.x, s);
+      const double q = div_fast_nocheck(s, dp);
+      ok &= div_range_ok(s, dp, q);
+      s = __dsub_rn(__dmul_rn(q, mm.y), sig);
+    }
+    if (row0 + kk == bk) s_in = s;
+#pragma unroll 4
+    for (; kk < len; kk++) {
+      const double2 mm = T[kk];
+      const double dp = __dadd_rn(mm.x, s);
+      const double q = div_fast_nocheck(s, dp);
+      ok &= div_range_ok(s, dp, q);
+      s = __dsub_rn(__dmul_rn(q, mm.y), sig);
+      cnt += (int)((unsigned)__double2hiint(dp) >> 31);
+    }
+    if (k == K - 1 && t == ntile - 1) cnt += sbx(__dadd_rn(T[nb - 1 - row0].x, s));
+    __syncthreads();
+    if (threadIdx.x == 0 && t + 2 < ntile) {
+      int len2 = min(NEG_TILE, nrow - (t + 2) * NEG_TILE);
+      tma_load_1d(buf + b * NEG_TILE, M + w0 + (long long)(t + 2) * NEG_TILE, (unsigned)(len2 * sizeof(double2)),
+                  &bar[b]);
+    }
+  }
+  if (bk == w0) s_in = -sig;  // no warm-up (k = 0): the exact start
+  if (act) {
+    SegOut o;
+    o.s_in = s_in;
+    o.s_out = s;
+    o.cnt = cnt;
+    o.ok = ok ? 1 : 0;
+    seg[c * K + k] = o;
+  }
+}
+
+// accept segments along the verified chain of exact states; queue the rest for the careful tail
+__global__ void k_seg_combine(long long tot, long long nn, int K, const SegOut *__restrict__ seg, int *counts,
+                              int *excounts, int4 *fb, int *nfb, double *fb_s, const int *__restrict__ dnn, int mmax,
+                              long long target, long long *negx) {
+  if (dnn) {
+    const int nnode = *dnn;
+    nn = (long long)nnode * ((1 << round_m(nnode, mmax, target)) - 1);
+    tot = nn;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd((unsigned long long *)negx, (unsigned long long)tot);
+  }
+  long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= tot) return;
+  const SegOut *S = seg + c * K;
+  int total = 0, k = 0;
+  double s_exact = S[0].s_in;  // -sigma
+  for (; k < K; k++) {
+    const SegOut o = S[k];
+    if (!o.ok) break;
+    if (k > 0 && __double_as_longlong(o.s_in) != __double_as_longlong(s_exact)) break;
+    total += o.cnt;
+    s_exact = o.s_out;
+  }
+  if (k == K) {
+    if (c < nn) counts[c] = total;
+    else excounts[c - nn] = total;
+    return;
+  }
+  const int slot = atomicAdd(nfb, 1);
+  fb[slot] = make_int4((int)(c & 0x7fffffff), k, total, (int)(c >> 31));
+  fb_s[slot] = s_exact;
+}
+
+// careful sequential tail from segment k's first row with the last exact state
+__global__ void k_seg_fallback(const int4 *__restrict__ fb, const int *__restrict__ nfb, const double *__restrict__ fb_s,
+                               const Node *__restrict__ nodes, int nnode, int m, const ExplicitChain *__restrict__ ex,
+                               const RepDesc *__restrict__ reps, const double2 *__restrict__ mx, int L, int *counts,
+                               int *excounts, const int *__restrict__ dnn, int mmax, long long target) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= *nfb) return;
+  if (dnn) {
+    nnode = *dnn;
+    m = round_m(nnode, mmax, target);
+  }
+  const int4 f = fb[i];
+  const long long c = (long long)f.x | ((long long)f.w << 31);
+  const long long nn = (long long)nnode * ((1 << m) - 1);
+  double sig;
+  int rep;
+  chain_of(nodes, m, nn, ex, c, sig, rep);
+  const RepDesc R = reps[rep];
+  const double2 *M = mx + R.off;
+  const int nb = R.nb;
+  double s = fb_s[i];
+  int cnt = f.z;
+  for (int r = min(f.y * L, nb - 1); r < nb - 1; r++) {
+    const double2 mm = M[r];
+    const double dp = __dadd_rn(mm.x, s);
+    const double q = (isinf(s) && isinf(dp)) ? 1.0 : __ddiv_rn(s, dp);
+    s = __dsub_rn(__dmul_rn(q, mm.y), sig);
+    cnt += sbx(dp);
+  }
+  cnt += sbx(__dadd_rn(M[nb - 1].x, s));
+  if (c < nn) counts[c] = cnt;
+  else excounts[c - nn] = cnt;
+}

@@ -73,7 +73,8 @@ struct Err {
 inline unsigned nblocks_for(long long n, int bs) { return (unsigned)std::max<long long>(1, (n + bs - 1) / bs); }
 
 // counters block on the device: reset/readback in one copy
-enum { C_NNEXT = 0, C_NEX, C_NPEND, C_NREADY, C_NSING, C_NCLUS, C_NNXT, C_NDONE, C_NK, C_NP, C_NPC, C_NCOUNTERS = 16 };
+enum { C_NNEXT = 0, C_NEX, C_NPEND, C_NREADY, C_NSING, C_NCLUS, C_NNXT, C_NDONE, C_NK, C_NP, C_NPC, C_NFB,
+       C_NCOUNTERS = 16 };
 
 }  // namespace
 
@@ -86,13 +87,18 @@ struct mrrr_ctx {
   int root_side = 0;
   uint32_t flags = 0;
   long long ws_limit = 0;
-  long long target_chains = 65536;  // k-section budget per round (C2 sweep: 65536 -> 3 levels per round)
+  long long target_chains = 16384;  // k-section budget per round, segmented root chains (C2: 1 level per round)
+  long long target_unseg = 65536;   // k-section budget per round of whole-length chains (C2 sweep: 3 levels)
   int mmax = 16;
   int chains_per_thread = 1;
   bool neg_tma = true;  // x-NegCount with TMA-staged representation tiles (k_negcount_tma)
   bool guided = false;  // guided rounds for isolated nodes (kernels_guided.cuh); MRRR_GUIDED=1 (C2: fewer rounds, more FP64 work: slower)
   int bud_full = 15, bud_tube = 40;
-  bool grouped = true;  // child bisection with CTAs grouped by representation (k_negcount_grp)  // tube point budgets: no estimate (4 full levels) / with estimate
+  bool grouped = true;  // child bisection with CTAs grouped by representation (k_negcount_grp)
+  int seg_k = 8, seg_w = 128;  // segmented root NegCount: segments per chain, warm-up rows (k_negcount_seg)
+  bool dev_rounds = false;     // segmented rounds enqueued in batches on device-side counters (MRRR_DEVROUNDS=1;
+                               // slower on C2: the oversized early-exit grids cost more than the saved syncs)
+  int max_nodes = 0;           // bound on live bisection nodes (indices in the computed set)  // tube point budgets: no estimate (4 full levels) / with estimate
   bool rqi_pair = true;
   bool l2_persist = true;
   long long l2_max_window = 0;
@@ -101,6 +107,8 @@ struct mrrr_ctx {
   Buf starts, scal, binfo, bside, blist, cab, mx, my, mq, lscratch, reps, rlo, rhi, colmap, gstart;
   Buf nodesK, nodesP, offsP, dS, dG, dH;  // guided bisection rounds
   Buf repoff, repcur, repcta;             // representation-grouped rounds
+  Buf segout, segfb, segfbs, rnd;         // segmented NegCount; per-round device counters
+  std::vector<cudaEvent_t> rev;           // events around device-driven rounds
   Buf nodesA, nodesB, counts, ex, excounts, exmap, bnA, bnB, sing, clusA, clusB, ss, gval, valid, cseg, bnoff,
       ipool_lo, ipool_hi, yref_lo, yref_hi, wsA, wsB, stats, cnt, ddepth, dgf, dgl, dflo, dfhi, hd, he, hW, hZ, zmeta;
   int *h_cnt = nullptr;  // pinned counters
@@ -314,7 +322,7 @@ void run_bisection_guided(mrrr_t h, int nnode, double *out_lo, double *out_hi, d
       nPc = h->h_cnt[C_NPC];
     }
     int m = 1;
-    const long long budget = std::max<long long>(h->target_chains - nPc, 0);
+    const long long budget = std::max<long long>(h->target_unseg - nPc, 0);
     while (m < h->mmax && (long long)nK * ((1LL << (m + 1)) - 1) <= budget) m++;
     const long long nKc = (long long)nK * ((1LL << m) - 1);
     const int nex = first ? nverify : 0;
@@ -361,9 +369,75 @@ void run_bisection_guided(mrrr_t h, int nnode, double *out_lo, double *out_hi, d
   }
 }
 
+__global__ void k_set_int(int *p, int v) { *p = v; }
+
+// Segmented rounds driven by device-side node counters: round r reads its node count from nn[r] and the
+// update writes nn[r+1], so batches of rounds are enqueued without a host round trip (kernels of empty
+// rounds exit at once); the host checks the count once per batch.
+void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int maxnodes, double *out_lo,
+                       double *out_hi, double rtol) {
+  const int K = h->seg_k, L = (nb - 1 + K - 1) / K;
+  const int MAXR = 256, RB = 8;
+  const long long maxch = std::max<long long>(h->target_chains, maxnodes) + 128;
+  CK(h->rnd.ensure(sizeof(int) * 2 * (MAXR + 2)));
+  CK(h->counts.ensure(sizeof(int) * maxch));
+  CK(h->segout.ensure(sizeof(SegOut) * maxch * K));
+  CK(h->segfb.ensure(sizeof(int4) * maxch));
+  CK(h->segfbs.ensure(sizeof(double) * maxch));
+  while ((int)h->rev.size() < 2 * MAXR) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    h->rev.push_back(e);
+  }
+  int *nn = h->rnd.as<int>(), *nfb = nn + MAXR + 2;
+  CK(cudaMemsetAsync(h->rnd.p, 0, sizeof(int) * 2 * (MAXR + 2), h->stream));
+  k_set_int<<<1, 1, 0, h->stream>>>(nn, nnode);
+  launch_check(h);
+  unsigned long long *alg = (unsigned long long *)(h->stats.as<long long>() + ST_NEGX_ALG);
+  long long *negx = h->stats.as<long long>() + ST_NEGX;
+  const dim3 gseg((unsigned)(maxch / 128 + 1), (unsigned)K);
+  const unsigned g1 = (unsigned)(maxch / 128 + 1), g2 = (unsigned)(2 * maxch / 128 + 1);
+  int r = 0;
+  for (;;) {
+    for (int b = 0; b < RB && r < MAXR; b++, r++) {
+      Node *in = (r & 1) ? nxt : cur, *out = (r & 1) ? cur : nxt;
+      CK(cudaEventRecord(h->rev[2 * r], h->stream));
+      k_negcount_seg<<<gseg, 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
+          in, 0, 0, nullptr, 0, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L, h->seg_w, h->segout.as<SegOut>(),
+          nn + r, h->mmax, h->target_chains);
+      CK(cudaEventRecord(h->rev[2 * r + 1], h->stream));
+      k_seg_combine<<<g1, 128, 0, h->stream>>>(0, 0, K, h->segout.as<SegOut>(), h->counts.as<int>(), nullptr,
+                                               h->segfb.as<int4>(), nfb + r, h->segfbs.as<double>(), nn + r, h->mmax,
+                                               h->target_chains, negx);
+      k_seg_fallback<<<g1, 128, 0, h->stream>>>(h->segfb.as<int4>(), nfb + r, h->segfbs.as<double>(), in, 0, 0,
+                                                nullptr, h->reps.as<RepDesc>(), h->mx.as<double2>(), L,
+                                                h->counts.as<int>(), nullptr, nn + r, h->mmax, h->target_chains);
+      k_bisect_update_dev<<<g2, 128, 0, h->stream>>>(in, nn + r, h->mmax, h->target_chains, h->counts.as<int>(), out,
+                                                     nn + r + 1, out_lo, out_hi, rtol, alg);
+      launch_check(h);
+      h->host_launches += 3;
+    }
+    int left = 0;
+    CK(cudaMemcpyAsync(&left, nn + r, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (left == 0) break;
+    if (r >= MAXR) { g_last_cuda_error = "bisection did not converge in 256 rounds"; throw Err{MRRR_ERR_CUDA}; }
+  }
+  std::vector<int> hn(r + 1);
+  CK(cudaMemcpy(hn.data(), nn, sizeof(int) * (r + 1), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < r; i++) {
+    if (hn[i] == 0) break;
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, h->rev[2 * i], h->rev[2 * i + 1]));
+    h->neg_ms += ms;
+    h->neg_launches++;
+    h->host_rounds++;
+  }
+}
+
 template <bool Y>
 void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double rtol, int nverify,
-                   const int *blist_dev, int nbl, bool *restart, int rep0 = -1, int nrep = 0);
+                   const int *blist_dev, int nbl, bool *restart, int rep0 = -1, int nrep = 0, int single_nb = 0);
 
 // k-section rounds with the nodes grouped by representation (child bisection over many child RRRs)
 void run_bisection_grouped(mrrr_t h, int nnode, double *out_lo, double *out_hi, double rtol, int rep0, int nrep) {
@@ -375,7 +449,7 @@ void run_bisection_grouped(mrrr_t h, int nnode, double *out_lo, double *out_hi, 
   while (nnode > 0) {
     CK(h->nodesK.ensure(sizeof(Node) * nnode));
     int m = 1;
-    while (m < h->mmax && (long long)nnode * ((1LL << (m + 1)) - 1) <= h->target_chains) m++;
+    while (m < h->mmax && (long long)nnode * ((1LL << (m + 1)) - 1) <= h->target_unseg) m++;
     const long long P = (1LL << m) - 1;
     // few chains per representation (e.g. thousands of 2-clusters): a CTA per representation would run
     // latency-bound waves; then the per-thread kernel runs on the rep-sorted nodes (a warp's lanes share
@@ -429,7 +503,7 @@ void run_bisection_grouped(mrrr_t h, int nnode, double *out_lo, double *out_hi, 
 // shared-tree / k-section bisection rounds until every node is finished (S5, S8)
 template <bool Y>
 void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double rtol, int nverify,
-                   const int *blist_dev, int nbl, bool *restart, int rep0, int nrep) {
+                   const int *blist_dev, int nbl, bool *restart, int rep0, int nrep, int single_nb) {
   if (!Y && rep0 >= 0 && nrep > 1 && h->neg_tma && h->grouped) {
     run_bisection_grouped(h, nnode, out_lo, out_hi, rtol, rep0, nrep);
     return;
@@ -440,16 +514,42 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
   }
   Node *cur = h->nodesA.as<Node>(), *nxt = h->nodesB.as<Node>();
   bool first = true;
+  const bool seg_on = !Y && single_nb > 0 && h->neg_tma && h->seg_k > 1 && (single_nb - 1) >= 2 * h->seg_k * h->seg_w;
+  const long long target = seg_on ? h->target_chains : h->target_unseg;
   while (nnode > 0) {
     int m = 1;
-    while (m < h->mmax && (long long)nnode * ((1LL << (m + 1)) - 1) <= h->target_chains) m++;
+    while (m < h->mmax && (long long)nnode * ((1LL << (m + 1)) - 1) <= target) m++;
     long long P = (1LL << m) - 1;
     long long nch = (long long)nnode * P;
     CK(h->counts.ensure(std::max<long long>(nch, 1) * sizeof(int)));
     int nex = first ? nverify : 0;
     zero_counters(h);
     CK(cudaEventRecord(h->nc0, h->stream));
-    launch_negcount<Y>(h, cur, nnode, m, nex);
+    if (seg_on) {
+      // segmented chains (kernels_guided.cuh): K concurrent segments per NegCount, verified bit-exact
+      const int K = h->seg_k, L = (single_nb - 1 + K - 1) / K;
+      const long long tot = nch + nex;
+      CK(h->segout.ensure(sizeof(SegOut) * tot * K));
+      CK(h->segfb.ensure(sizeof(int4) * tot));
+      CK(h->segfbs.ensure(sizeof(double) * tot));
+      dim3 grid((unsigned)((tot + 127) / 128), (unsigned)K);
+      k_negcount_seg<<<grid, 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
+          cur, nnode, m, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L, h->seg_w,
+          h->segout.as<SegOut>(), nullptr, 0, 0);
+      launch_check(h);
+      k_seg_combine<<<nblocks_for(tot, 128), 128, 0, h->stream>>>(tot, nch, K, h->segout.as<SegOut>(),
+                                                                   h->counts.as<int>(), h->excounts.as<int>(),
+                                                                   h->segfb.as<int4>(), h->cnt.as<int>() + C_NFB,
+                                                                   h->segfbs.as<double>(), nullptr, 0, 0, nullptr);
+      launch_check(h);
+      k_seg_fallback<<<nblocks_for(tot, 128), 128, 0, h->stream>>>(
+          h->segfb.as<int4>(), h->cnt.as<int>() + C_NFB, h->segfbs.as<double>(), cur, nnode, m,
+          h->ex.as<ExplicitChain>(), h->reps.as<RepDesc>(), h->mx.as<double2>(), L, h->counts.as<int>(),
+          h->excounts.as<int>(), nullptr, 0, 0);
+      launch_check(h);
+    } else {
+      launch_negcount<Y>(h, cur, nnode, m, nex);
+    }
     CK(cudaEventRecord(h->nc1, h->stream));
     if (nex > 0) {
       k_root_verify<<<nblocks_for(nbl, 128), 128, 0, h->stream>>>(blist_dev, nbl, h->starts.as<int>(),
@@ -474,6 +574,10 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
     nnode = h->h_cnt[C_NNEXT];
     std::swap(cur, nxt);
     first = false;
+    if (!Y && seg_on && h->dev_rounds && nnode > 0) {
+      run_rounds_device(h, cur, nxt, nnode, single_nb, std::max(nnode, h->max_nodes), out_lo, out_hi, rtol);
+      return;
+    }
   }
 }
 
@@ -850,6 +954,7 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
   const double rtol = 1e-2 * h->gaptol;
   if (nbl) {
     long long cap = std::max<long long>(ncomp + 2, nbl);
+    h->max_nodes = (int)cap;
     CK(h->nodesA.ensure(sizeof(Node) * cap));
     CK(h->nodesB.ensure(sizeof(Node) * cap));
     CK(h->ex.ensure(sizeof(ExplicitChain) * (nbl + 64)));
@@ -861,7 +966,7 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
       launch_check(h);
       bool restart = false;
       run_bisection<false>(h, nbl, h->rlo.as<double>(), h->rhi.as<double>(), rtol, nbl, h->blist.as<int>(), nbl,
-                           &restart);
+                           &restart, -1, 0, single ? (int)n : 0);
       if (!restart) break;
     }
     // root definiteness
@@ -1040,11 +1145,15 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     CK(cudaMemGetInfo(&fr, &tot));
     h->ws_limit = (o && o->ws_limit > 0) ? o->ws_limit : (long long)(0.6 * (double)fr);
     if (const char *s = getenv("MRRR_TARGET_CHAINS")) h->target_chains = atoll(s);
+    if (const char *s = getenv("MRRR_TARGET_UNSEG")) h->target_unseg = atoll(s);
     if (const char *s = getenv("MRRR_MMAX")) h->mmax = atoi(s);
     if (const char *s = getenv("MRRR_CH")) h->chains_per_thread = std::max(1, std::min(4, atoi(s)));
     if (const char *s = getenv("MRRR_NEGTMA")) h->neg_tma = atoi(s) != 0;
     if (const char *s = getenv("MRRR_GUIDED")) h->guided = atoi(s) != 0;
     if (const char *s = getenv("MRRR_GROUPED")) h->grouped = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_SEGK")) h->seg_k = std::max(1, std::min(64, atoi(s)));
+    if (const char *s = getenv("MRRR_SEGW")) h->seg_w = std::max(1, atoi(s));
+    if (const char *s = getenv("MRRR_DEVROUNDS")) h->dev_rounds = atoi(s) != 0;
     if (const char *s = getenv("MRRR_BUD_FULL")) h->bud_full = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_BUD_TUBE")) h->bud_tube = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;
@@ -1234,7 +1343,7 @@ int mrrr_destroy(mrrr_t h) {
   if (!h) return 0;
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->stream);
-  Buf *bufs[] = {&h->starts, &h->scal, &h->binfo, &h->bside, &h->blist, &h->cab, &h->mx, &h->my, &h->mq, &h->nodesK, &h->nodesP, &h->offsP, &h->dS, &h->dG, &h->dH, &h->repoff, &h->repcur, &h->repcta, &h->lscratch,
+  Buf *bufs[] = {&h->starts, &h->scal, &h->binfo, &h->bside, &h->blist, &h->cab, &h->mx, &h->my, &h->mq, &h->nodesK, &h->nodesP, &h->offsP, &h->dS, &h->dG, &h->dH, &h->repoff, &h->repcur, &h->repcta, &h->segout, &h->segfb, &h->segfbs, &h->rnd, &h->lscratch,
                  &h->reps, &h->rlo, &h->rhi, &h->colmap, &h->gstart, &h->nodesA, &h->nodesB, &h->counts, &h->ex,
                  &h->excounts, &h->exmap, &h->bnA, &h->bnB, &h->sing, &h->clusA, &h->clusB, &h->ss, &h->gval,
                  &h->valid, &h->cseg, &h->bnoff, &h->ipool_lo, &h->ipool_hi, &h->yref_lo, &h->yref_hi, &h->wsA,
@@ -1242,6 +1351,7 @@ int mrrr_destroy(mrrr_t h) {
                  &h->hd, &h->he, &h->hW, &h->hZ, &h->zmeta};
   for (Buf *b : bufs) b->release();
   for (auto &ev : h->ev) cudaEventDestroy(ev);
+  for (auto &ev : h->rev) cudaEventDestroy(ev);
   cudaEventDestroy(h->rq0);
   cudaEventDestroy(h->rq1);
   if (h->h_cnt) cudaFreeHost(h->h_cnt);

@@ -510,10 +510,12 @@ __device__ __forceinline__ dd shfl_idx_dd(dd v, int lane) {
 __global__ void __launch_bounds__(256) k_zwrite(const Singleton *__restrict__ sg, int ns,
                                                 const RepDesc *__restrict__ reps, const YElt *__restrict__ my,
                                                 const dd *__restrict__ P2base, long long S,
-                                                const ZMeta *__restrict__ zm, double *Z, long long ldz) {
+                                                const ZMeta *__restrict__ zm, double *Z, long long ldz,
+                                                const int *__restrict__ status = nullptr, int status_stride = 0) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= ns) return;
+  if (status && status[(long long)w * status_stride] != 1) return;  // segmented RQI: accepted singletons only
   const ZMeta m = zm[w];
   const Singleton s = sg[w];
   const RepDesc R = reps[s.rep];

@@ -1,0 +1,331 @@
+// kernels_rqi3.cuh -- singleton RQI (S9/S10: Alg. Getvec, Alg. stask, mixed stop
+// P:6074-6108) with segmented passes.
+//
+// The qd recurrences of a twisted factorization contract away from the eigenvector's peak (a perturbation
+// of d+(i) is multiplied by l+(i)^2 = (z(i)/z(i+1))^2 < 1 where z grows), so each pass is split into K
+// segments per lane that run concurrently: segment k starts W rows early from a guess, records its state
+// when it reaches its first row, and is accepted only if that state equals, bit for bit, the predecessor's
+// exact end state (then every operation of the segment saw the sequential operands).  A singleton with a
+// mismatch, or whose fast pass left the finite range, is handed to the two-lane kernel k_rqi2 (which also
+// runs the careful IEEE pass and the bisection fallback), so results never depend on a guess.
+//
+//   k_rqi3_init   RQI state: lambda = interval midpoint, bracket, acceptance threshold.
+//   k_twist_seg   iteration 1's twist search in x-arithmetic (A-31): F lane d+(i), B lane
+//                 c2(i)/omega(i+1) of the twisted factorization at lambda, fp64, segmented.
+//   k_twist_pick  junction check and r = argmin |gamma_k| (ties: smallest k), one warp per singleton.
+//   k_fixed_seg   the r-twisted factorization in y-arithmetic (dd), segmented: l+/u- into P2, the
+//                 partial norms S/T as per-segment affine maps, inertia counts, gamma_r's two halves.
+//   k_fixed_step  junction check, gamma_r, ||z||^2, inertia; the stask decision: accept (write W and
+//                 the z-write metadata), or apply the RQC and run another k_fixed_seg, or hand over.
+#pragma once
+#include "kernels_rqi.cuh"
+
+struct RqiState {
+  double lam_hi, lam_lo, blo_hi, blo_lo, bhi_hi, bhi_lo, thr1;
+  int r, it, status, pad;  // status: 0 active, 1 accepted, 2 handed to k_rqi2
+};
+
+// per (singleton, lane, segment) record of a segmented pass
+struct SegRec {
+  double in_hi, in_lo, out_hi, out_lo;  // state entering the segment's first row, state after its last
+  double A, B_hi, B_lo;                 // partial norm: S_end = A * S_start + B (fixed pass)
+  double t_hi, t_lo;                    // B lane's c2(r)/omega(r+1) (segment that ends at row r)
+  int cnt, ok, empty, pad;              // empty: the lane has fewer steps than segments
+};
+
+__global__ void k_rqi3_init(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
+                            RqiState *st) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ns) return;
+  const Singleton s = sg[i];
+  const int nb = reps[s.rep].nb;
+  const double nu = __dmul_rn(__dmul_rn(100.0, (double)nb), EPS_X);
+  RqiState q;
+  q.lam_hi = bis_mid(s.lo, s.hi);
+  q.lam_lo = 0.0;
+  q.blo_hi = __dsub_rn(s.lo, __dmul_rn(nu, fabs(s.lo)));
+  q.blo_lo = 0.0;
+  q.bhi_hi = __dadd_rn(s.hi, __dmul_rn(nu, fabs(s.hi)));
+  q.bhi_lo = 0.0;
+  q.thr1 = __dmul_rn(__dmul_rn(s.gap, EPS_X), sqrt((double)nb));
+  q.r = -1;
+  q.it = 0;
+  q.status = 0;
+  q.pad = 0;
+  st[i] = q;
+}
+
+// F lane step t = row t; B lane step t = row nb-2-t.  Row data of a lane: c2(i), gf(i) (F) or gb(i) (B).
+__device__ __forceinline__ int seg_row(bool isB, int nb, int t) { return isB ? nb - 2 - t : t; }
+
+// iteration 1's twist search in fp64 (A-31): TF[i] = d+(i) (F), TB[i] = c2(i)/omega(i+1) (B),
+// gamma_i = TF[i] - TB[i]; thread = (singleton, lane, segment)
+__global__ void __launch_bounds__(128) k_twist_seg(const Singleton *__restrict__ sg, int ns,
+                                                   const RepDesc *__restrict__ reps, const QElt *__restrict__ mq,
+                                                   const RqiState *__restrict__ st, int K, int Wu, double *TF,
+                                                   double *TB, long long nbmax, SegRec *rec) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (long long)ns * 2 * K) return;
+  const int k = (int)(g % K), isB = (int)((g / K) & 1), i = (int)(g / (2 * K));
+  const RqiState S = st[i];
+  SegRec *R = rec + g;
+  if (S.status != 0) return;
+  const RepDesc Rp = reps[sg[i].rep];
+  const int nb = Rp.nb, steps = nb - 1;
+  const QElt *q = mq + Rp.off;
+  const double lam = S.lam_hi;
+  const int L = (steps + K - 1) / K;
+  const int t0 = min(k * L, steps), t1 = min((k + 1) * L, steps), tw = (k == 0) ? 0 : max(t0 - Wu, 0);
+  double *T = (isB ? TB : TF) + (long long)i * nbmax;
+  if (isB && k == 0) T[nb - 1] = 0.0;
+  if (t0 >= t1) {
+    R->empty = 1;
+    R->ok = 1;
+    return;
+  }
+  R->empty = 0;
+  // state entering step tw: F d+(row), B omega(row+1); guess = the value with no coupling term
+  const int rs = isB ? nb - 1 - tw : tw;
+  double den = __dsub_rn(__ldg(&q[rs].gb_hi), lam);
+  double din = den;
+  bool ok = true;
+  for (int t = tw; t < t1; t++) {
+    if (t == t0) din = den;
+    const int row = seg_row(isB, nb, t);
+    const double c2 = __ldg(&q[row].c2_hi);
+    const double gg = isB ? __ldg(&q[row].gb_hi) : __ldg(&q[row].gf_hi);
+    const double P = div_fast_nocheck(c2, den);
+    if (t >= t0) T[row] = isB ? P : den;
+    den = __dsub_rn(__dsub_rn(gg, lam), P);
+    ok &= isfinite(den) && den != 0.0;
+  }
+  if (!isB && t1 == steps) T[nb - 1] = den;   // gamma_n = d+(n)
+  R->in_hi = din;
+  R->out_hi = den;
+  R->ok = ok ? 1 : 0;
+}
+
+// one warp per singleton: junctions of the twist pass, then r = argmin |gamma_k| (ties to the smallest k)
+__global__ void k_twist_pick(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
+                             RqiState *st, int K, const double *__restrict__ TF, const double *__restrict__ TB,
+                             long long nbmax, const SegRec *__restrict__ rec) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= ns) return;
+  RqiState S = st[w];
+  if (S.status != 0) return;
+  const int nb = reps[sg[w].rep].nb;
+  const SegRec *R = rec + (long long)w * 2 * K;
+  bool good = true;
+  if (lane == 0) {
+    for (int ln = 0; ln < 2; ln++) {
+      int prev = -1;
+      for (int k = 0; k < K; k++) {
+        const SegRec &a = R[ln * K + k];
+        if (a.empty) continue;
+        good &= a.ok != 0;
+        if (prev >= 0) good &= __double_as_longlong(a.in_hi) == __double_as_longlong(R[ln * K + prev].out_hi);
+        prev = k;
+      }
+    }
+  }
+  good = __shfl_sync(0xffffffffu, good, 0);
+  if (!good) {
+    if (lane == 0) st[w].status = 2;
+    return;
+  }
+  const double *F = TF + (long long)w * nbmax, *B = TB + (long long)w * nbmax;
+  double best = INFINITY;
+  int bk = -1;
+  for (int kk = lane; kk < nb; kk += 32) {
+    const double gm = fabs(__dsub_rn(F[kk], B[kk]));
+    if (gm < best) { best = gm; bk = kk; }  // lane-strided ascending: first minimum of the lane
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+    const int ok_ = __shfl_xor_sync(0xffffffffu, bk, off);
+    if (ok_ >= 0 && (bk < 0 || ob < best || (ob == best && ok_ < bk))) { best = ob; bk = ok_; }
+  }
+  if (lane == 0) {
+    // the x-arithmetic argmin must resolve gamma: |gamma_r| well above the fp64 rounding of its two terms
+    // (in child frames lambda and gamma can sit below it); otherwise the y-arithmetic twist search decides
+    const double sc = (bk >= 0) ? fmax(fabs(F[bk]), fabs(B[bk])) : 0.0;
+    if (bk < 0 || !(best > 0x1p-40 * sc)) st[w].status = 2;
+    else st[w].r = bk;
+  }
+}
+
+// the r-twisted factorization in dd: F steps 0..r-1, B steps 0..nb-2-r (rows nb-2 .. r)
+__global__ void __launch_bounds__(128) k_fixed_seg(const Singleton *__restrict__ sg, int ns,
+                                                   const RepDesc *__restrict__ reps, const QElt *__restrict__ mq,
+                                                   const RqiState *__restrict__ st, int K, int Wu, dd *P2,
+                                                   long long nbmax, SegRec *rec) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (long long)ns * 2 * K) return;
+  const int k = (int)(g % K), isB = (int)((g / K) & 1), i = (int)(g / (2 * K));
+  const RqiState S = st[i];
+  if (S.status != 0) return;
+  SegRec *R = rec + g;
+  const RepDesc Rp = reps[sg[i].rep];
+  const int nb = Rp.nb, r = S.r;
+  const QElt *q = mq + Rp.off;
+  const dd lam = dd_make(S.lam_hi, S.lam_lo), nlam = dd_neg(lam);
+  const int steps = isB ? nb - 1 - r : r;
+  const int L = (steps + K - 1) / K;
+  const int t0 = min(k * L, steps), t1 = min((k + 1) * L, steps), tw = (k == 0) ? 0 : max(t0 - Wu, 0);
+  dd *P = P2 + (long long)i * nbmax;
+  if (t0 >= t1 && !(k == 0 && !isB)) {  // no steps (F segment 0 always reports d+(0) when r = 0)
+    R->empty = 1;
+    R->ok = 1;
+    return;
+  }
+  R->empty = 0;
+  const int rs = isB ? nb - 1 - tw : tw;
+  dd den = dd_sub_nf(dd_make(__ldg(&q[rs].gb_hi), __ldg(&q[rs].gb_lo)), lam);
+  dd din = den, Pl = dd_from(0.0);
+  double A = 1.0;
+  dd Bs = dd_from(0.0);
+  int cnt = 0;
+  bool ok = true;
+  for (int t = tw; t < t1; t++) {
+    if (t == t0) din = den;
+    const int row = seg_row(isB, nb, t);
+    const double2 *pq = reinterpret_cast<const double2 *>(q + row);
+    const dd c2 = D2(__ldg(pq)), dl = D2(__ldg(pq + 1)), gg = D2(__ldg(pq + (isB ? 3 : 2)));
+    const double b = den.hi;
+    ok &= (fabs(b) > 0x1p-1000) && (fabs(b) < 0x1p1000);
+    const double rc = rcp_seed_dd(b);
+    double ee = __fma_rn(-b, rc, 1.0);
+    ee = __fma_rn(ee, ee, ee);
+    const double r1 = __fma_rn(rc, ee, rc);
+    const double e2 = __fma_rn(-b, r1, 1.0);
+    const double r2 = __fma_rn(r1, e2, r1);
+    const dd Pq = qdiv(c2, den, r1, r2);
+    if (t >= t0) {
+      const dd o = qdiv(dl, den, r1, r2);
+      const dd out = fast_two_sum(o.hi, o.lo);
+      stw(P, row, out);
+      const dd o2 = dd_mul_nf(out, out);
+      A = __dmul_rn(o2.hi, A);
+      Bs = dd_mul_nf(o2, dd_add_d_nf(Bs, 1.0));
+      cnt += dd_sb(den);
+      Pl = Pq;
+    }
+    den = dd_sum3_nf(gg, nlam, dd_neg(Pq));
+  }
+  ok &= isfinite(den.hi) && isfinite(den.lo) && isfinite(Bs.hi);
+  R->in_hi = din.hi;
+  R->in_lo = din.lo;
+  R->out_hi = den.hi;
+  R->out_lo = den.lo;
+  R->A = A;
+  R->B_hi = Bs.hi;
+  R->B_lo = Bs.lo;
+  const dd tl = fast_two_sum(Pl.hi, Pl.lo);  // B lane: c2(r)/omega(r+1) of the step on row r
+  R->t_hi = tl.hi;
+  R->t_lo = tl.lo;
+  R->cnt = cnt;
+  R->ok = ok ? 1 : 0;
+}
+
+// thread per singleton: junctions, gamma_r, ||z||^2, inertia, and the stask decision
+__global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
+                             RqiState *st, int K, const SegRec *__restrict__ rec, double *W, ZMeta *zmeta,
+                             int *diag_depth, double *fin_lo, double *fin_hi, long long *stats, int *nactive) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ns) return;
+  RqiState S = st[i];
+  if (S.status != 0) return;
+  const Singleton s = sg[i];
+  const RepDesc Rp = reps[s.rep];
+  const int nb = Rp.nb, r = S.r, j = s.j;
+  const SegRec *F = rec + (long long)i * 2 * K, *B = F + K;
+  bool good = true;
+  dd Ssum = dd_from(0.0), Tsum = dd_from(0.0), dr = dd_from(0.0), tr = dd_from(0.0);
+  int c = 0;
+  for (int ln = 0; ln < 2; ln++) {
+    const SegRec *X = ln ? B : F;
+    int prev = -1;
+    dd acc = dd_from(0.0);
+    for (int k = 0; k < K; k++) {
+      const SegRec &a = X[k];
+      if (a.empty) continue;
+      good &= a.ok != 0;
+      if (prev >= 0)
+        good &= __double_as_longlong(a.in_hi) == __double_as_longlong(X[prev].out_hi) &&
+                __double_as_longlong(a.in_lo) == __double_as_longlong(X[prev].out_lo);
+      acc = dd_add(dd_mul_d(acc, a.A), dd_make(a.B_hi, a.B_lo));
+      c += a.cnt;
+      prev = k;
+    }
+    if (ln == 0) {
+      Ssum = acc;
+      if (prev >= 0) dr = dd_make(X[prev].out_hi, X[prev].out_lo);  // d+(r): F's exact end state
+    } else {
+      Tsum = acc;
+      if (prev >= 0) tr = dd_make(X[prev].t_hi, X[prev].t_lo);     // c2(r)/omega(r+1): B's last step
+    }
+  }
+  if (!good) {
+    st[i].status = 2;
+    return;
+  }
+  const dd gamma = (r == nb - 1) ? dr : dd_sub(dr, tr);
+  c += dd_sb(gamma);
+  const dd zz = dd_add_d(dd_add(Ssum, Tsum), 1.0);
+  dd lam = dd_make(S.lam_hi, S.lam_lo), blo = dd_make(S.blo_hi, S.blo_lo), bhi = dd_make(S.bhi_hi, S.bhi_lo);
+  S.it++;
+  atomicAdd((unsigned long long *)&stats[ST_RQI_ITERS], 1ull);
+  atomicAdd((unsigned long long *)&stats[ST_GETVEC], 1ull);
+  atomicAdd((unsigned long long *)&stats[ST_QD_STEPS], (unsigned long long)(nb - 1));
+  bool accepted = false, handover = false;
+  if (!isfinite(zz.hi) || zz.hi == 0.0) {
+    handover = true;
+  } else {
+    const dd nz = dd_sqrt(zz);
+    const dd resid = dd_div(dd_abs(gamma), nz);
+    const dd rqc = dd_div(gamma, zz);
+    dd tol2 = dd_mul_d(dd_abs(lam), 4.0 * EPS_Y);  // A-30
+    if (dd_lt(tol2, dd_from(__dmul_rn(0x1p-100, Rp.spdiam)))) tol2 = dd_from(__dmul_rn(0x1p-100, Rp.spdiam));
+    if (resid.hi <= S.thr1 || dd_lt(dd_abs(rqc), tol2)) {
+      accepted = true;
+    } else {
+      if (c < j) blo = lam; else bhi = lam;
+      const dd nl = dd_add(lam, rqc);
+      const bool okc = ((c < j) ? (rqc.hi > 0.0) : (rqc.hi < 0.0)) && dd_lt(blo, nl) && dd_lt(nl, bhi);
+      if (okc && S.it < MAX_RQI) lam = nl;
+      else handover = true;  // bisection fallback / iteration cap: the two-lane kernel redoes this singleton
+    }
+  }
+  if (accepted) {
+    const dd inv = dd_rcp(dd_sqrt(zz));
+    ZMeta zm;
+    zm.inv_hi = inv.hi; zm.inv_lo = inv.lo; zm.r = r; zm.careful = 0;
+    zmeta[i] = zm;
+    const dd sig = dd_make(Rp.sig_hi, Rp.sig_lo);
+    W[s.col] = dd_add(lam, sig).hi;
+    if (diag_depth) {
+      diag_depth[s.col] = Rp.depth;
+      fin_lo[s.col] = s.lo;
+      fin_hi[s.col] = s.hi;
+    }
+    atomicAdd((unsigned long long *)&stats[ST_ZW_STEPS], (unsigned long long)(nb - 1));
+    atomicMax((unsigned long long *)&stats[ST_DMAX], (unsigned long long)Rp.depth);
+    S.status = 1;
+  } else if (handover) {
+    S.status = 2;
+  } else {
+    atomicAdd(nactive, 1);
+  }
+  S.lam_hi = lam.hi; S.lam_lo = lam.lo;
+  S.blo_hi = blo.hi; S.blo_lo = blo.lo;
+  S.bhi_hi = bhi.hi; S.bhi_lo = bhi.lo;
+  st[i] = S;
+}
+
+// singletons handed over (status != 1) for the two-lane kernel k_rqi2
+__global__ void k_rqi3_collect(const Singleton *__restrict__ sg, int ns, const RqiState *__restrict__ st,
+                               Singleton *hand, int *nhand) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ns) return;
+  if (st[i].status != 1) hand[atomicAdd(nhand, 1)] = sg[i];
+}

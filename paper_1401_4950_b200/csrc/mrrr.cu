@@ -18,6 +18,7 @@
 #include "kernels_vec.cuh"
 #include "kernels_rqi.cuh"
 #include "kernels_guided.cuh"
+#include "kernels_rqi3.cuh"
 
 namespace {
 
@@ -96,6 +97,8 @@ struct mrrr_ctx {
   int bud_full = 15, bud_tube = 40;
   bool grouped = true;  // child bisection with CTAs grouped by representation (k_negcount_grp)
   int seg_k = 8, seg_w = 128;  // segmented root NegCount: segments per chain, warm-up rows (k_negcount_seg)
+  bool rqi_seg = false;        // segmented RQI passes (kernels_rqi3.cuh), MRRR_RQISEG=1 (C5b faster, C2/C5a not)
+  int rqi_segk = 8, rqi_segw = 256;
   bool dev_rounds = false;     // segmented rounds enqueued in batches on device-side counters (MRRR_DEVROUNDS=1;
                                // slower on C2: the oversized early-exit grids cost more than the saved syncs)
   int max_nodes = 0;           // bound on live bisection nodes (indices in the computed set)  // tube point budgets: no estimate (4 full levels) / with estimate
@@ -108,6 +111,7 @@ struct mrrr_ctx {
   Buf nodesK, nodesP, offsP, dS, dG, dH;  // guided bisection rounds
   Buf repoff, repcur, repcta;             // representation-grouped rounds
   Buf segout, segfb, segfbs, rnd;         // segmented NegCount; per-round device counters
+  Buf rqst, rqrec, hand;                  // segmented RQI state, segment records, handed-over singletons
   std::vector<cudaEvent_t> rev;           // events around device-driven rounds
   Buf nodesA, nodesB, counts, ex, excounts, exmap, bnA, bnB, sing, clusA, clusB, ss, gval, valid, cseg, bnoff,
       ipool_lo, ipool_hi, yref_lo, yref_hi, wsA, wsB, stats, cnt, ddepth, dgf, dgl, dflo, dfhi, hd, he, hW, hZ, zmeta;
@@ -657,14 +661,66 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
     CK(cudaEventRecord(h->rq0, h->stream));
     if (pair) {
       CK(h->zmeta.ensure(sizeof(ZMeta) * stride));
-      k_rqi2<<<nblocks_for(2 * nb, 64), 64, 64 * MRRR_RQI_RING * sizeof(RingSlot), h->stream>>>(
-          h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(),
-          h->mq.as<QElt>(), h->wsA.as<dd>(), stride, nbmax, W, h->zmeta.as<ZMeta>(), diag ? h->ddepth.as<int>() : nullptr,
-          diag ? h->dflo.as<double>() : nullptr, diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>());
-      launch_check(h);
-      k_zwrite<<<nblocks_for(32 * nb, 256), 256, 0, h->stream>>>(
-          h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(),
-          h->wsA.as<dd>() + 2 * stride * nbmax, nbmax, h->zmeta.as<ZMeta>(), Z, ldz);
+      const Singleton *sgb = h->sing.as<Singleton>() + b0;
+      int nold = (int)nb;
+      if (h->rqi_seg) {
+        // segmented passes (kernels_rqi3.cuh); singletons they hand over go through k_rqi2 below
+        const int K = h->rqi_segk, Wu = h->rqi_segw;
+        CK(h->rqst.ensure(sizeof(RqiState) * stride));
+        CK(h->rqrec.ensure(sizeof(SegRec) * stride * 2 * K));
+        CK(h->hand.ensure(sizeof(Singleton) * stride));
+        double *TF = reinterpret_cast<double *>(h->wsA.as<dd>());
+        double *TB = TF + stride * nbmax;
+        dd *P2s = h->wsA.as<dd>() + stride * nbmax;  // after TF, TB
+        RqiState *rs = h->rqst.as<RqiState>();
+        SegRec *rec = h->rqrec.as<SegRec>();
+        k_rqi3_init<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs);
+        k_twist_seg<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
+                                                                          h->mq.as<QElt>(), rs, K, Wu, TF, TB, nbmax,
+                                                                          rec);
+        k_twist_pick<<<nblocks_for(32 * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, TF,
+                                                                        TB, nbmax, rec);
+        launch_check(h);
+        for (int it = 0; it < MAX_RQI; it++) {
+          CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
+          k_fixed_seg<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
+                                                                            h->mq.as<QElt>(), rs, K, Wu, P2s, nbmax,
+                                                                            rec);
+          k_fixed_step<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(
+              sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, rec, W, h->zmeta.as<ZMeta>(),
+              diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
+              diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), h->cnt.as<int>() + C_NFB);
+          launch_check(h);
+          h->host_launches += 1;
+          int act = 0;
+          CK(cudaMemcpyAsync(&act, h->cnt.as<int>() + C_NFB, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+          CK(cudaStreamSynchronize(h->stream));
+          if (act == 0) break;
+        }
+        const int *stat = reinterpret_cast<const int *>(reinterpret_cast<const char *>(rs) + offsetof(RqiState, status));
+        k_zwrite<<<nblocks_for(32 * nb, 256), 256, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
+                                                                 h->my.as<YElt>(), P2s, nbmax, h->zmeta.as<ZMeta>(), Z,
+                                                                 ldz, stat, (int)(sizeof(RqiState) / sizeof(int)));
+        launch_check(h);
+        CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
+        k_rqi3_collect<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, rs, h->hand.as<Singleton>(),
+                                                                    h->cnt.as<int>() + C_NFB);
+        launch_check(h);
+        CK(cudaMemcpyAsync(&nold, h->cnt.as<int>() + C_NFB, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        sgb = h->hand.as<Singleton>();
+        h->stats_h[ST_RQI_HANDOVER] += nold;
+      }
+      if (nold > 0) {
+        k_rqi2<<<nblocks_for(2 * nold, 64), 64, 64 * MRRR_RQI_RING * sizeof(RingSlot), h->stream>>>(
+            sgb, nold, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->mq.as<QElt>(), h->wsA.as<dd>(), stride, nbmax, W,
+            h->zmeta.as<ZMeta>(), diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
+            diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>());
+        launch_check(h);
+        k_zwrite<<<nblocks_for(32 * nold, 256), 256, 0, h->stream>>>(
+            sgb, nold, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>() + 2 * stride * nbmax, nbmax,
+            h->zmeta.as<ZMeta>(), Z, ldz);
+      }
     } else {
       k_rqi<<<nblocks_for(nb, 64), 64, 0, h->stream>>>(
           h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>(),
@@ -1154,6 +1210,9 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_SEGK")) h->seg_k = std::max(1, std::min(64, atoi(s)));
     if (const char *s = getenv("MRRR_SEGW")) h->seg_w = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_DEVROUNDS")) h->dev_rounds = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_RQISEG")) h->rqi_seg = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_RQISEGK")) h->rqi_segk = std::max(1, std::min(64, atoi(s)));
+    if (const char *s = getenv("MRRR_RQISEGW")) h->rqi_segw = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_BUD_FULL")) h->bud_full = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_BUD_TUBE")) h->bud_tube = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;
@@ -1343,7 +1402,7 @@ int mrrr_destroy(mrrr_t h) {
   if (!h) return 0;
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->stream);
-  Buf *bufs[] = {&h->starts, &h->scal, &h->binfo, &h->bside, &h->blist, &h->cab, &h->mx, &h->my, &h->mq, &h->nodesK, &h->nodesP, &h->offsP, &h->dS, &h->dG, &h->dH, &h->repoff, &h->repcur, &h->repcta, &h->segout, &h->segfb, &h->segfbs, &h->rnd, &h->lscratch,
+  Buf *bufs[] = {&h->starts, &h->scal, &h->binfo, &h->bside, &h->blist, &h->cab, &h->mx, &h->my, &h->mq, &h->nodesK, &h->nodesP, &h->offsP, &h->dS, &h->dG, &h->dH, &h->repoff, &h->repcur, &h->repcta, &h->segout, &h->segfb, &h->segfbs, &h->rnd, &h->rqst, &h->rqrec, &h->hand, &h->lscratch,
                  &h->reps, &h->rlo, &h->rhi, &h->colmap, &h->gstart, &h->nodesA, &h->nodesB, &h->counts, &h->ex,
                  &h->excounts, &h->exmap, &h->bnA, &h->bnB, &h->sing, &h->clusA, &h->clusB, &h->ss, &h->gval,
                  &h->valid, &h->cseg, &h->bnoff, &h->ipool_lo, &h->ipool_hi, &h->yref_lo, &h->yref_hi, &h->wsA,

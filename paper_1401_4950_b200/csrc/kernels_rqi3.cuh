@@ -63,21 +63,26 @@ __device__ __forceinline__ int seg_row(bool isB, int nb, int t) { return isB ? n
 __global__ void __launch_bounds__(128) k_twist_seg(const Singleton *__restrict__ sg, int ns,
                                                    const RepDesc *__restrict__ reps, const QElt *__restrict__ mq,
                                                    const RqiState *__restrict__ st, int K, int Wu, double *TF,
-                                                   double *TB, long long nbmax, SegRec *rec) {
+                                                   double *TB, long long S_, SegRec *rec) {
+  // consecutive threads = consecutive singletons of one (lane, segment): on a shared representation they
+  // read the same row (broadcast) and store TF/TB[row * S_ + i] coalesced
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= (long long)ns * 2 * K) return;
-  const int k = (int)(g % K), isB = (int)((g / K) & 1), i = (int)(g / (2 * K));
+  const int i = (int)(g % ns), ks = (int)(g / ns), k = ks % K, isB = ks / K;
   const RqiState S = st[i];
-  SegRec *R = rec + g;
+  SegRec *R = rec + ((long long)i * 2 + isB) * K + k;
   if (S.status != 0) return;
   const RepDesc Rp = reps[sg[i].rep];
   const int nb = Rp.nb, steps = nb - 1;
   const QElt *q = mq + Rp.off;
-  const double lam = S.lam_hi;
+  // evaluated a fraction of the inflated bracket away from lambda-hat, so that |gamma_r| stays well above
+  // the fp64 rounding of its terms however close lambda-hat is (r is eigenvector j's peak either way)
+  const double lam = __dadd_rn(S.lam_hi, ldexp(__dsub_rn(S.bhi_hi, S.blo_hi), -8));
   const int L = (steps + K - 1) / K;
   const int t0 = min(k * L, steps), t1 = min((k + 1) * L, steps), tw = (k == 0) ? 0 : max(t0 - Wu, 0);
-  double *T = (isB ? TB : TF) + (long long)i * nbmax;
-  if (isB && k == 0) T[nb - 1] = 0.0;
+  double *T = (isB ? TB : TF) + i;
+#define TROW(row) T[(long long)(row) * S_]
+  if (isB && k == 0) TROW(nb - 1) = 0.0;
   if (t0 >= t1) {
     R->empty = 1;
     R->ok = 1;
@@ -95,11 +100,12 @@ __global__ void __launch_bounds__(128) k_twist_seg(const Singleton *__restrict__
     const double c2 = __ldg(&q[row].c2_hi);
     const double gg = isB ? __ldg(&q[row].gb_hi) : __ldg(&q[row].gf_hi);
     const double P = div_fast_nocheck(c2, den);
-    if (t >= t0) T[row] = isB ? P : den;
+    if (t >= t0) TROW(row) = isB ? P : den;
     den = __dsub_rn(__dsub_rn(gg, lam), P);
     ok &= isfinite(den) && den != 0.0;
   }
-  if (!isB && t1 == steps) T[nb - 1] = den;   // gamma_n = d+(n)
+  if (!isB && t1 == steps) TROW(nb - 1) = den;   // gamma_n = d+(n)
+#undef TROW
   R->in_hi = din;
   R->out_hi = den;
   R->ok = ok ? 1 : 0;
@@ -108,36 +114,41 @@ __global__ void __launch_bounds__(128) k_twist_seg(const Singleton *__restrict__
 // one warp per singleton: junctions of the twist pass, then r = argmin |gamma_k| (ties to the smallest k)
 __global__ void k_twist_pick(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
                              RqiState *st, int K, const double *__restrict__ TF, const double *__restrict__ TB,
-                             long long nbmax, const SegRec *__restrict__ rec) {
+                             long long S_, const SegRec *__restrict__ rec, long long *stats) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= ns) return;
   RqiState S = st[w];
   if (S.status != 0) return;
-  const int nb = reps[sg[w].rep].nb;
+  const int nb = reps[sg[w].rep].nb, steps = nb - 1;
+  const int L = (steps + K - 1) / K;
   const SegRec *R = rec + (long long)w * 2 * K;
-  bool good = true;
+  // verified rows: F segments 0..kf-1 (rows [0, fhi)), B segments 0..kb-1 (rows (blo, nb-2]); a segment is
+  // exact iff its entry state equals its exact predecessor's exit state (segment 0 starts exactly).  The
+  // twist index lies where both lanes are exact (F's failures start past the eigenvector's peak, B's
+  // before it); rows outside are not candidates.
+  int fhi = 0, blo = nb;
   if (lane == 0) {
     for (int ln = 0; ln < 2; ln++) {
-      int prev = -1;
+      int prev = -1, kv = 0;
       for (int k = 0; k < K; k++) {
         const SegRec &a = R[ln * K + k];
-        if (a.empty) continue;
-        good &= a.ok != 0;
-        if (prev >= 0) good &= __double_as_longlong(a.in_hi) == __double_as_longlong(R[ln * K + prev].out_hi);
+        if (a.empty) { kv = k + 1; continue; }
+        if (!a.ok) break;
+        if (prev >= 0 && __double_as_longlong(a.in_hi) != __double_as_longlong(R[ln * K + prev].out_hi)) break;
         prev = k;
+        kv = k + 1;
       }
+      const int tv = min(kv * L, steps);  // steps verified from the lane's start
+      if (ln == 0) fhi = (tv == steps) ? nb : tv;  // F's last step also fixes gamma_n
+      else blo = (tv == steps) ? -1 : nb - 2 - tv;  // B: rows nb-2 .. nb-1-tv verified
     }
   }
-  good = __shfl_sync(0xffffffffu, good, 0);
-  if (!good) {
-    if (lane == 0) st[w].status = 2;
-    return;
-  }
-  const double *F = TF + (long long)w * nbmax, *B = TB + (long long)w * nbmax;
+  fhi = __shfl_sync(0xffffffffu, fhi, 0);
+  blo = __shfl_sync(0xffffffffu, blo, 0);
   double best = INFINITY;
   int bk = -1;
-  for (int kk = lane; kk < nb; kk += 32) {
-    const double gm = fabs(__dsub_rn(F[kk], B[kk]));
+  for (int kk = max(blo + 1, 0) + lane; kk < fhi; kk += 32) {
+    const double gm = fabs(__dsub_rn(TF[(long long)kk * S_ + w], TB[(long long)kk * S_ + w]));
     if (gm < best) { best = gm; bk = kk; }  // lane-strided ascending: first minimum of the lane
   }
   for (int off = 16; off > 0; off >>= 1) {
@@ -148,9 +159,13 @@ __global__ void k_twist_pick(const Singleton *__restrict__ sg, int ns, const Rep
   if (lane == 0) {
     // the x-arithmetic argmin must resolve gamma: |gamma_r| well above the fp64 rounding of its two terms
     // (in child frames lambda and gamma can sit below it); otherwise the y-arithmetic twist search decides
-    const double sc = (bk >= 0) ? fmax(fabs(F[bk]), fabs(B[bk])) : 0.0;
-    if (bk < 0 || !(best > 0x1p-40 * sc)) st[w].status = 2;
-    else st[w].r = bk;
+    const double sc = (bk >= 0) ? fmax(fabs(TF[(long long)bk * S_ + w]), fabs(TB[(long long)bk * S_ + w])) : 0.0;
+    if (bk < 0 || !(best > 0x1p-46 * sc)) {
+      st[w].status = 2;
+      atomicAdd((unsigned long long *)&stats[ST_HO_TWIST], 1ull);
+    } else {
+      st[w].r = bk;
+    }
   }
 }
 
@@ -167,6 +182,7 @@ __global__ void __launch_bounds__(128) k_fixed_seg(const Singleton *__restrict__
   SegRec *R = rec + g;
   const RepDesc Rp = reps[sg[i].rep];
   const int nb = Rp.nb, r = S.r;
+  const bool light = S.it == 0;  // the first pass at the bisection midpoint only yields the RQC
   const QElt *q = mq + Rp.off;
   const dd lam = dd_make(S.lam_hi, S.lam_lo), nlam = dd_neg(lam);
   const int steps = isB ? nb - 1 - r : r;
@@ -201,12 +217,18 @@ __global__ void __launch_bounds__(128) k_fixed_seg(const Singleton *__restrict__
     const double r2 = __fma_rn(r1, e2, r1);
     const dd Pq = qdiv(c2, den, r1, r2);
     if (t >= t0) {
-      const dd o = qdiv(dl, den, r1, r2);
-      const dd out = fast_two_sum(o.hi, o.lo);
-      stw(P, row, out);
-      const dd o2 = dd_mul_nf(out, out);
-      A = __dmul_rn(o2.hi, A);
-      Bs = dd_mul_nf(o2, dd_add_d_nf(Bs, 1.0));
+      if (light) {  // RQC-only pass: no factors stored, norm in fp64 (A-31 note in DESIGN.md)
+        const double o = __dmul_rn(dl.hi, r2), o2 = __dmul_rn(o, o);
+        A = __dmul_rn(o2, A);
+        Bs = dd_from(__fma_rn(o2, Bs.hi, o2));
+      } else {
+        const dd o = qdiv(dl, den, r1, r2);
+        const dd out = fast_two_sum(o.hi, o.lo);
+        stw(P, row, out);
+        const dd o2 = dd_mul_nf(out, out);
+        A = __dmul_rn(o2.hi, A);
+        Bs = dd_mul_nf(o2, dd_add_d_nf(Bs, 1.0));
+      }
       cnt += dd_sb(den);
       Pl = Pq;
     }
@@ -267,6 +289,7 @@ __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const Rep
   }
   if (!good) {
     st[i].status = 2;
+    atomicAdd((unsigned long long *)&stats[ST_HO_FIXED], 1ull);
     return;
   }
   const dd gamma = (r == nb - 1) ? dr : dd_sub(dr, tr);
@@ -287,6 +310,11 @@ __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const Rep
     dd tol2 = dd_mul_d(dd_abs(lam), 4.0 * EPS_Y);  // A-30
     if (dd_lt(tol2, dd_from(__dmul_rn(0x1p-100, Rp.spdiam)))) tol2 = dd_from(__dmul_rn(0x1p-100, Rp.spdiam));
     if (resid.hi <= S.thr1 || dd_lt(dd_abs(rqc), tol2)) {
+      if (S.it == 1) {  // accepted on the RQC-only pass: repeat it at the same lambda with the factors stored
+        atomicAdd(nactive, 1);
+        st[i] = S;
+        return;
+      }
       accepted = true;
     } else {
       if (c < j) blo = lam; else bhi = lam;
@@ -313,6 +341,7 @@ __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const Rep
     S.status = 1;
   } else if (handover) {
     S.status = 2;
+    atomicAdd((unsigned long long *)&stats[ST_HO_RQC], 1ull);
   } else {
     atomicAdd(nactive, 1);
   }

@@ -97,7 +97,7 @@ struct mrrr_ctx {
   int bud_full = 15, bud_tube = 40;
   bool grouped = true;  // child bisection with CTAs grouped by representation (k_negcount_grp)
   int seg_k = 8, seg_w = 128;  // segmented root NegCount: segments per chain, warm-up rows (k_negcount_seg)
-  bool rqi_seg = false;        // segmented RQI passes (kernels_rqi3.cuh), MRRR_RQISEG=1 (C5b faster, C2/C5a not)
+  bool rqi_seg = true;         // segmented RQI passes (kernels_rqi3.cuh); MRRR_RQISEG=0: the two-lane kernel only
   int rqi_segk = 8, rqi_segw = 256;
   bool dev_rounds = false;     // segmented rounds enqueued in batches on device-side counters (MRRR_DEVROUNDS=1;
                                // slower on C2: the oversized early-exit grids cost more than the saved syncs)
@@ -639,7 +639,7 @@ void l2_pin_reps(mrrr_t h, bool on) {
   cudaGetLastError();
 }
 
-void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long ldz) {
+void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long ldz, bool allow_seg) {
   if (ns <= 0) return;
   l2_pin_reps(h, true);
   const bool pair = h->rqi_pair;
@@ -663,23 +663,23 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
       CK(h->zmeta.ensure(sizeof(ZMeta) * stride));
       const Singleton *sgb = h->sing.as<Singleton>() + b0;
       int nold = (int)nb;
-      if (h->rqi_seg) {
+      if (h->rqi_seg && allow_seg) {
         // segmented passes (kernels_rqi3.cuh); singletons they hand over go through k_rqi2 below
         const int K = h->rqi_segk, Wu = h->rqi_segw;
         CK(h->rqst.ensure(sizeof(RqiState) * stride));
         CK(h->rqrec.ensure(sizeof(SegRec) * stride * 2 * K));
         CK(h->hand.ensure(sizeof(Singleton) * stride));
-        double *TF = reinterpret_cast<double *>(h->wsA.as<dd>());
+        double *TF = reinterpret_cast<double *>(h->wsA.as<dd>());  // [row * stride + singleton]
         double *TB = TF + stride * nbmax;
         dd *P2s = h->wsA.as<dd>() + stride * nbmax;  // after TF, TB
         RqiState *rs = h->rqst.as<RqiState>();
         SegRec *rec = h->rqrec.as<SegRec>();
         k_rqi3_init<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs);
         k_twist_seg<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
-                                                                          h->mq.as<QElt>(), rs, K, Wu, TF, TB, nbmax,
+                                                                          h->mq.as<QElt>(), rs, K, Wu, TF, TB, stride,
                                                                           rec);
         k_twist_pick<<<nblocks_for(32 * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, TF,
-                                                                        TB, nbmax, rec);
+                                                                        TB, stride, rec, h->stats.as<long long>());
         launch_check(h);
         for (int it = 0; it < MAX_RQI; it++) {
           CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
@@ -872,7 +872,7 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
     launch_check(h);
     read_counters(h);
     int ns = h->h_cnt[C_NSING], nnx = h->h_cnt[C_NNXT];
-    run_rqi(h, ns, nbmax, W, Z, ldz);
+    run_rqi(h, ns, nbmax, W, Z, ldz, false);  // child frames: the x-arithmetic twist search rarely resolves
     process_clusters(h, NX.as<Cluster>(), nnx, repbase + nc, poolbase + (long long)nc * nbmax, ipool_top + stot, nbmax,
                      true, W, Z, ldz, kout, level + 1);
     CK(cudaStreamSynchronize(h->stream));
@@ -1120,7 +1120,7 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
   CK(cudaEventRecord(h->ev[3], st));
 
   // S9/S10 root singletons
-  run_rqi(h, ns, nbmax, W, Z, ldz);
+  run_rqi(h, ns, nbmax, W, Z, ldz, true);
   CK(cudaEventRecord(h->ev[4], st));
   // S8 clusters (depth-first, chunked)
   if (ncl > 0) {

@@ -99,6 +99,7 @@ struct mrrr_ctx {
   int seg_k = 8, seg_w = 128;  // segmented root NegCount: segments per chain, warm-up rows (k_negcount_seg)
   bool rqi_seg = true;         // segmented RQI passes (kernels_rqi3.cuh); MRRR_RQISEG=0: the two-lane kernel only
   int rqi_segk = 8, rqi_segw = 256;
+  int dev_rb = 4;             // rounds per device-driven batch
   bool dev_rounds = false;     // segmented rounds enqueued in batches on device-side counters (MRRR_DEVROUNDS=1;
                                // slower on C2: the oversized early-exit grids cost more than the saved syncs)
   int max_nodes = 0;           // bound on live bisection nodes (indices in the computed set)  // tube point budgets: no estimate (4 full levels) / with estimate
@@ -381,7 +382,7 @@ __global__ void k_set_int(int *p, int v) { *p = v; }
 void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int maxnodes, double *out_lo,
                        double *out_hi, double rtol) {
   const int K = h->seg_k, L = (nb - 1 + K - 1) / K;
-  const int MAXR = 256, RB = 8;
+  const int MAXR = 256, RB = h->dev_rb;
   const long long maxch = std::max<long long>(h->target_chains, maxnodes) + 128;
   CK(h->rnd.ensure(sizeof(int) * 2 * (MAXR + 2)));
   CK(h->counts.ensure(sizeof(int) * maxch));
@@ -399,10 +400,16 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
   launch_check(h);
   unsigned long long *alg = (unsigned long long *)(h->stats.as<long long>() + ST_NEGX_ALG);
   long long *negx = h->stats.as<long long>() + ST_NEGX;
-  const dim3 gseg((unsigned)(maxch / 128 + 1), (unsigned)K);
-  const unsigned g1 = (unsigned)(maxch / 128 + 1), g2 = (unsigned)(2 * maxch / 128 + 1);
   int r = 0;
+  long long known = nnode;  // node count of round r (read back once per batch)
   for (;;) {
+    // grids for a batch: the node count can at most double per round (a node splits in two), and a round
+    // has at most max(target, nodes) chains; CTAs beyond the live count exit at once
+    long long bound = known;
+    for (int b = 0; b < RB; b++) bound = std::min<long long>(2 * bound, maxnodes);
+    const long long chmax = std::min<long long>(maxch, std::max<long long>(bound, h->target_chains) + 128);
+    const dim3 gseg((unsigned)(chmax / 128 + 1), (unsigned)K);
+    const unsigned g1 = (unsigned)(chmax / 128 + 1), g2 = (unsigned)(2 * chmax / 128 + 1);
     for (int b = 0; b < RB && r < MAXR; b++, r++) {
       Node *in = (r & 1) ? nxt : cur, *out = (r & 1) ? cur : nxt;
       CK(cudaEventRecord(h->rev[2 * r], h->stream));
@@ -425,6 +432,7 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
     CK(cudaMemcpyAsync(&left, nn + r, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     if (left == 0) break;
+    known = left;
     if (r >= MAXR) { g_last_cuda_error = "bisection did not converge in 256 rounds"; throw Err{MRRR_ERR_CUDA}; }
   }
   std::vector<int> hn(r + 1);
@@ -1210,6 +1218,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_SEGK")) h->seg_k = std::max(1, std::min(64, atoi(s)));
     if (const char *s = getenv("MRRR_SEGW")) h->seg_w = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_DEVROUNDS")) h->dev_rounds = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_DEVRB")) h->dev_rb = std::max(1, std::min(64, atoi(s)));
     if (const char *s = getenv("MRRR_RQISEG")) h->rqi_seg = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQISEGK")) h->rqi_segk = std::max(1, std::min(64, atoi(s)));
     if (const char *s = getenv("MRRR_RQISEGW")) h->rqi_segw = std::max(1, atoi(s));

@@ -269,7 +269,8 @@ def main():
         if rq_n:
             launch_ms = rq_ms / rq_n
             f = fl.rqi_flops(stats, n, wdiv) / nrq
-            cands.append(("k_rqi2 (+k_zwrite; singleton RQI + eigenvectors)", launch_ms, f, rq_ms))
+            cands.append(("singleton RQI + eigenvectors (k_twist_seg, k_fixed_seg, k_zwrite; k_rqi2 for hand-overs)",
+                          launch_ms, f, rq_ms))
         if tphase["negcount_launches"]:
             launch_ms = tphase["negcount_ms_per_launch"]
             nl = tphase["negcount_launches"]

@@ -117,8 +117,9 @@ int mrrr_shard_owner(const int32_t *gstart, int64_t n, int64_t sl, int64_t su, i
  * count, without k-section speculation), 21 the same for y-NegCount, 22 RQI corrections rejected for an
  * inertia-inconsistent sign, 23 RQI corrections rejected for leaving the bracket (both end in the bisection
  * fallback), 24 singletons the segmented RQI handed to the two-lane kernel, 25-27 of them because the
- * x-arithmetic twist search did not resolve gamma / a segment junction failed / the RQC was rejected. */
-#define MRRR_NSTATS 28
+ * x-arithmetic twist search did not resolve gamma / a segment junction failed / the RQC was rejected,
+ * 28 dd rows of RQC-only (light) passes, 29 fp64 rows of the segmented twist search (both lanes). */
+#define MRRR_NSTATS 30
 int mrrr_get_stats(mrrr_t h, int64_t *stats, int32_t nstats);
 
 /* Diagnostics of the last call made with MRRR_KEEP_DIAG (host buffers owned

@@ -111,60 +111,75 @@ __global__ void __launch_bounds__(128) k_twist_seg(const Singleton *__restrict__
   R->ok = ok ? 1 : 0;
 }
 
-// one warp per singleton: junctions of the twist pass, then r = argmin |gamma_k| (ties to the smallest k)
-__global__ void k_twist_pick(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
-                             RqiState *st, int K, const double *__restrict__ TF, const double *__restrict__ TB,
-                             long long S_, const SegRec *__restrict__ rec, long long *stats) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (w >= ns) return;
-  RqiState S = st[w];
-  if (S.status != 0) return;
-  const int nb = reps[sg[w].rep].nb, steps = nb - 1;
-  const int L = (steps + K - 1) / K;
-  const SegRec *R = rec + (long long)w * 2 * K;
-  // verified rows: F segments 0..kf-1 (rows [0, fhi)), B segments 0..kb-1 (rows (blo, nb-2]); a segment is
-  // exact iff its entry state equals its exact predecessor's exit state (segment 0 starts exactly).  The
-  // twist index lies where both lanes are exact (F's failures start past the eigenvector's peak, B's
-  // before it); rows outside are not candidates.
-  int fhi = 0, blo = nb;
-  if (lane == 0) {
-    for (int ln = 0; ln < 2; ln++) {
-      int prev = -1, kv = 0;
-      for (int k = 0; k < K; k++) {
-        const SegRec &a = R[ln * K + k];
-        if (a.empty) { kv = k + 1; continue; }
-        if (!a.ok) break;
-        if (prev >= 0 && __double_as_longlong(a.in_hi) != __double_as_longlong(R[ln * K + prev].out_hi)) break;
-        prev = k;
-        kv = k + 1;
+// junctions of the twist pass and r = argmin |gamma_k| (ties to the smallest k).  A CTA covers 32 singletons
+// x 8 row groups: warp g scans rows g, g+8, ... of 32 consecutive singletons (coalesced [row * S + i] loads).
+__global__ void __launch_bounds__(256) k_twist_pick(const Singleton *__restrict__ sg, int ns,
+                                                    const RepDesc *__restrict__ reps, RqiState *st, int K,
+                                                    const double *__restrict__ TF, const double *__restrict__ TB,
+                                                    long long S_, const SegRec *__restrict__ rec, long long *stats) {
+  __shared__ int sh_lo[32], sh_hi[32];
+  __shared__ double sh_best[8][32];
+  __shared__ int sh_bk[8][32];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
+  const bool act = i < ns && st[min(i, ns - 1)].status == 0;
+  int nb = 0;
+  if (act) nb = reps[sg[i].rep].nb;
+  if (grp == 0) {
+    // verified rows: F segments before the first failed junction (rows [0, fhi)), B likewise from the
+    // bottom (rows (blo, nb-2]); a segment is exact iff its entry state equals its exact predecessor's exit
+    // state.  The twist index lies where both lanes are exact (F fails past the peak, B before it).
+    int fhi = 0, blo = 0;
+    if (act) {
+      const int steps = nb - 1, L = (steps + K - 1) / K;
+      const SegRec *R = rec + (long long)i * 2 * K;
+      for (int ln = 0; ln < 2; ln++) {
+        int prev = -1, kv = 0;
+        for (int k = 0; k < K; k++) {
+          const SegRec &s_ = R[ln * K + k];
+          if (s_.empty) { kv = k + 1; continue; }
+          if (!s_.ok) break;
+          if (prev >= 0 && __double_as_longlong(s_.in_hi) != __double_as_longlong(R[ln * K + prev].out_hi)) break;
+          prev = k;
+          kv = k + 1;
+        }
+        const int tv = min(kv * L, steps);
+        if (ln == 0) fhi = (tv == steps) ? nb : tv;  // F's last step also fixes gamma_n
+        else blo = (tv == steps) ? -1 : nb - 2 - tv;
       }
-      const int tv = min(kv * L, steps);  // steps verified from the lane's start
-      if (ln == 0) fhi = (tv == steps) ? nb : tv;  // F's last step also fixes gamma_n
-      else blo = (tv == steps) ? -1 : nb - 2 - tv;  // B: rows nb-2 .. nb-1-tv verified
     }
+    sh_lo[lane] = blo + 1;
+    sh_hi[lane] = fhi;
   }
-  fhi = __shfl_sync(0xffffffffu, fhi, 0);
-  blo = __shfl_sync(0xffffffffu, blo, 0);
+  __syncthreads();
   double best = INFINITY;
   int bk = -1;
-  for (int kk = max(blo + 1, 0) + lane; kk < fhi; kk += 32) {
-    const double gm = fabs(__dsub_rn(TF[(long long)kk * S_ + w], TB[(long long)kk * S_ + w]));
-    if (gm < best) { best = gm; bk = kk; }  // lane-strided ascending: first minimum of the lane
+  if (act) {
+    const int lo = max(sh_lo[lane], 0), hi = sh_hi[lane];
+    int kk = lo + ((grp - lo % 8) + 8) % 8;  // rows congruent to grp mod 8
+#pragma unroll 4
+    for (; kk < hi; kk += 8) {
+      const double gm = fabs(__dsub_rn(TF[(long long)kk * S_ + i], TB[(long long)kk * S_ + i]));
+      if (gm < best) { best = gm; bk = kk; }
+    }
   }
-  for (int off = 16; off > 0; off >>= 1) {
-    const double ob = __shfl_xor_sync(0xffffffffu, best, off);
-    const int ok_ = __shfl_xor_sync(0xffffffffu, bk, off);
-    if (ok_ >= 0 && (bk < 0 || ob < best || (ob == best && ok_ < bk))) { best = ob; bk = ok_; }
-  }
-  if (lane == 0) {
+  sh_best[grp][lane] = best;
+  sh_bk[grp][lane] = bk;
+  __syncthreads();
+  if (grp == 0 && act) {
+    for (int g2 = 1; g2 < 8; g2++) {
+      const double ob = sh_best[g2][lane];
+      const int ok_ = sh_bk[g2][lane];
+      if (ok_ >= 0 && (bk < 0 || ob < best || (ob == best && ok_ < bk))) { best = ob; bk = ok_; }
+    }
     // the x-arithmetic argmin must resolve gamma: |gamma_r| well above the fp64 rounding of its two terms
-    // (in child frames lambda and gamma can sit below it); otherwise the y-arithmetic twist search decides
-    const double sc = (bk >= 0) ? fmax(fabs(TF[(long long)bk * S_ + w]), fabs(TB[(long long)bk * S_ + w])) : 0.0;
+    const double sc = (bk >= 0) ? fmax(fabs(TF[(long long)bk * S_ + i]), fabs(TB[(long long)bk * S_ + i])) : 0.0;
     if (bk < 0 || !(best > 0x1p-46 * sc)) {
-      st[w].status = 2;
+      st[i].status = 2;
       atomicAdd((unsigned long long *)&stats[ST_HO_TWIST], 1ull);
     } else {
-      st[w].r = bk;
+      st[i].r = bk;
+      atomicAdd((unsigned long long *)&stats[ST_TWIST_ROWS], (unsigned long long)(2 * (nb - 1)));
     }
   }
 }
@@ -299,7 +314,7 @@ __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const Rep
   S.it++;
   atomicAdd((unsigned long long *)&stats[ST_RQI_ITERS], 1ull);
   atomicAdd((unsigned long long *)&stats[ST_GETVEC], 1ull);
-  atomicAdd((unsigned long long *)&stats[ST_QD_STEPS], (unsigned long long)(nb - 1));
+  atomicAdd((unsigned long long *)&stats[S.it == 1 ? ST_QD_LIGHT : ST_QD_STEPS], (unsigned long long)(nb - 1));
   bool accepted = false, handover = false;
   if (!isfinite(zz.hi) || zz.hi == 0.0) {
     handover = true;

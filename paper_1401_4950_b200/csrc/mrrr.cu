@@ -686,7 +686,7 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
         k_twist_seg<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
                                                                           h->mq.as<QElt>(), rs, K, Wu, TF, TB, stride,
                                                                           rec);
-        k_twist_pick<<<nblocks_for(32 * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, TF,
+        k_twist_pick<<<(unsigned)((nb + 31) / 32), 256, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, TF,
                                                                         TB, stride, rec, h->stats.as<long long>());
         launch_check(h);
         for (int it = 0; it < MAX_RQI; it++) {

@@ -15,11 +15,20 @@ SLOTS_QD = 78.0 + 28.0
 SLOTS_ITER1 = 58.0
 SLOTS_Z = 38.0
 SLOTS_ZW = 9.0
+# segmented RQI (kernels_rqi3.cuh): a row of the r-twisted pass on the pivot-recurrence form = reciprocal pair
+# (5 FMA) + two dd quotients (2 x 5) + normalisation (3) + dd sum3 (22) + norm recurrence (28) = 68 slots;
+# the RQC-only (light) pass drops one quotient, the normalisation and the dd norm (fp64 norm: 3) = 40;
+# a row of the fp64 twist search (one lane) = reciprocal pair 5 + quotient 1 + 2 subtractions = 8.
+SLOTS_QD_SEG = 68.0
+SLOTS_QD_LIGHT = 40.0
+SLOTS_TWIST = 8.0
 
 
 def rqi_slots(stats: dict, w_div: float = 0.0) -> float:
-    return (stats["qd_steps"] * SLOTS_QD + stats["qdg_steps"] * SLOTS_ITER1 + stats["z_steps"] * SLOTS_Z
-            + stats["zw_steps"] * SLOTS_ZW)
+    seg = stats.get("twist_rows", 0) > 0 or stats.get("qd_light", 0) > 0
+    return (stats["qd_steps"] * (SLOTS_QD_SEG if seg else SLOTS_QD) + stats["qdg_steps"] * SLOTS_ITER1
+            + stats["z_steps"] * SLOTS_Z + stats["zw_steps"] * SLOTS_ZW
+            + stats.get("qd_light", 0) * SLOTS_QD_LIGHT + stats.get("twist_rows", 0) * SLOTS_TWIST)
 
 
 def rqi_flops(stats: dict, n: int, w_div: float = 0.0) -> float:

@@ -549,6 +549,93 @@ __global__ void __launch_bounds__(256) k_zwrite(const Singleton *__restrict__ sg
   }
 }
 
+// Same output as k_zwrite, HBM-streaming form: a warp takes tiles of 32 x ZC rows; the tile's factors are
+// staged in shared memory by cp.async (coalesced, one tile ahead), each lane multiplies its own chunk of ZC
+// consecutive factors sequentially, one warp scan combines the 32 chunk products, and the z values go back
+// through shared memory so the Z column stores are coalesced.  2 dd products per row instead of the 7 of
+// the per-row warp scan; 1/||z|| rides in the carry.
+constexpr int ZC = 8, ZT = 32 * ZC, ZP = ZT + 32;  // rows per lane chunk, rows per tile, padded tile
+__device__ __forceinline__ int zpad(int m) { return m + m / ZC; }  // chunk stride ZC + 1: conflict-free
+__global__ void __launch_bounds__(128) k_zwrite_chunk(const Singleton *__restrict__ sg, int ns,
+                                                      const RepDesc *__restrict__ reps, const YElt *__restrict__ my,
+                                                      const dd *__restrict__ P2base, long long S,
+                                                      const ZMeta *__restrict__ zm, double *Z, long long ldz,
+                                                      const int *__restrict__ status = nullptr, int status_stride = 0) {
+  __shared__ __align__(16) double2 sbuf[4][2][ZP];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = blockIdx.x * 4 + wib;
+  if (w >= ns) return;
+  if (status && status[(long long)w * status_stride] != 1) return;
+  const ZMeta m = zm[w];
+  const Singleton s = sg[w];
+  const RepDesc R = reps[s.rep];
+  const int nb = R.nb, r = m.r, last = nb - 1;
+  const dd inv = dd_make(m.inv_hi, m.inv_lo);
+  const dd *P = P2base + (long long)w * S;
+  double *Zc = Z + (long long)s.col * ldz + R.bstart;
+  if (m.careful) {
+    if (lane == 0) zsolve(my + R.off, nb, r, P, P, 1, inv, Zc);
+    return;
+  }
+  if (lane == 0) Zc[r] = inv.hi;
+  double2(*buf)[ZP] = sbuf[wib];
+  for (int side = 0; side < 2; side++) {
+    const int len = side ? last - r : r;
+    if (len <= 0) continue;
+    const int ntile = (len + ZT - 1) / ZT;
+    auto issue = [&](int t) {
+      double2 *b = buf[t & 1];
+#pragma unroll
+      for (int u = 0; u < ZC; u++) {
+        const int ml = lane + 32 * u, mm = t * ZT + ml;
+        if (mm < len) cp16(&b[zpad(ml)], P + (side ? r + mm : r - 1 - mm));
+      }
+      cp_commit();
+    };
+    issue(0);
+    dd carry = inv;
+    for (int t = 0; t < ntile; t++) {
+      if (t + 1 < ntile) issue(t + 1);
+      else cp_commit();
+      cp_wait<1>();
+      __syncwarp();
+      double2 *b = buf[t & 1];
+      const int m0 = t * ZT, mc = m0 + lane * ZC;
+      dd p[ZC];
+      dd acc = dd_from(1.0);
+#pragma unroll
+      for (int e = 0; e < ZC; e++) {
+        if (mc + e < len) {
+          const double2 f = b[lane * (ZC + 1) + e];
+          const dd nf = dd_make(-f.x, -f.y);
+          acc = (e == 0) ? nf : dd_mul_nf(acc, nf);
+        }
+        p[e] = acc;
+      }
+      __syncwarp();
+      dd v = acc;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const dd o = shfl_up_dd(v, off);
+        if (lane >= off) v = dd_mul_nf(o, v);
+      }
+      dd ex = shfl_up_dd(v, 1);
+      const dd E = lane ? dd_mul_nf(carry, ex) : carry;
+      carry = dd_mul_nf(carry, shfl_idx_dd(v, 31));
+      double *sd = reinterpret_cast<double *>(b);
+#pragma unroll
+      for (int e = 0; e < ZC; e++) sd[lane * (ZC + 1) + e] = dd_mul_nf(E, p[e]).hi;
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < ZC; u++) {
+        const int ml = lane + 32 * u, mm = m0 + ml;
+        if (mm < len) Zc[side ? r + 1 + mm : r - 1 - mm] = sd[zpad(ml)];
+      }
+      __syncwarp();
+    }
+  }
+}
+
 __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
                                              const YElt *__restrict__ my, const QElt *__restrict__ mq, dd *ws,
                                              long long S, long long nbmax,

@@ -22,7 +22,7 @@
 
 struct RqiState {
   double lam_hi, lam_lo, blo_hi, blo_lo, bhi_hi, bhi_lo, thr1;
-  int r, it, status, pad;  // status: 0 active, 1 accepted, 2 handed to k_rqi2
+  int r, it, status, wide;  // status: 0 active, 1 accepted, 2 handed to k_rqi2; wide: 8x warm-up
 };
 
 // per (singleton, lane, segment) record of a segmented pass
@@ -51,11 +51,20 @@ __global__ void k_rqi3_init(const Singleton *__restrict__ sg, int ns, const RepD
   q.r = -1;
   q.it = 0;
   q.status = 0;
-  q.pad = 0;
+  q.wide = 0;
   st[i] = q;
 }
 
 // F lane step t = row t; B lane step t = row nb-2-t.  Row data of a lane: c2(i), gf(i) (F) or gb(i) (B).
+// balanced split of a singleton's 2K segment threads between its lanes (F: r steps, B: nb-1-r): each lane
+// gets segments in proportion to its length, at least one each, so the 2K threads run chains of about
+// (nb-1)/(2K) + W steps whatever r is (F segment 0 must exist even for r = 0: it reports d+(0))
+__device__ __forceinline__ int seg_kf(int nb, int r, int K2) {
+  const int tot = nb - 1, sf = r, sb = nb - 1 - r;
+  if (sb <= 0) return K2 - 1;
+  if (sf <= 0 || tot <= 0) return 1;
+  return min(max((int)(((long long)K2 * sf + tot / 2) / tot), 1), K2 - 1);
+}
 __device__ __forceinline__ int seg_row(bool isB, int nb, int t) { return isB ? nb - 2 - t : t; }
 
 // iteration 1's twist search in fp64 (A-31): TF[i] = d+(i) (F), TB[i] = c2(i)/omega(i+1) (B),
@@ -94,16 +103,35 @@ __global__ void __launch_bounds__(128) k_twist_seg(const Singleton *__restrict__
   double den = __dsub_rn(__ldg(&q[rs].gb_hi), lam);
   double din = den;
   bool ok = true;
-  for (int t = tw; t < t1; t++) {
+  auto step = [&](int t, double c2, double gg) {
     if (t == t0) din = den;
-    const int row = seg_row(isB, nb, t);
-    const double c2 = __ldg(&q[row].c2_hi);
-    const double gg = isB ? __ldg(&q[row].gb_hi) : __ldg(&q[row].gf_hi);
     const double P = div_fast_nocheck(c2, den);
-    if (t >= t0) TROW(row) = isB ? P : den;
+    if (t >= t0) TROW(seg_row(isB, nb, t)) = isB ? P : den;
     den = __dsub_rn(__dsub_rn(gg, lam), P);
     ok &= isfinite(den) && den != 0.0;
+  };
+  // rows stream from L2 (the representation is shared by many singletons): PF rows in flight
+  constexpr int PF = 8;
+  double rc[PF], rg[PF];
+  auto ld = [&](int t, int u) {
+    const int row = max(seg_row(isB, nb, min(t, t1 - 1)), 0);
+    rc[u] = __ldg(&q[row].c2_hi);
+    rg[u] = isB ? __ldg(&q[row].gb_hi) : __ldg(&q[row].gf_hi);
+  };
+#pragma unroll
+  for (int u = 0; u < PF; u++) ld(tw + u, u);
+  int t = tw;
+  for (; t + PF <= t1; t += PF) {
+#pragma unroll
+    for (int u = 0; u < PF; u++) {
+      const double c2 = rc[u], gg = rg[u];
+      ld(t + u + PF, u);
+      step(t + u, c2, gg);
+    }
   }
+#pragma unroll
+  for (int u = 0; u < PF; u++)
+    if (t + u < t1) step(t + u, rc[u], rg[u]);
   if (!isB && t1 == steps) TROW(nb - 1) = den;   // gamma_n = d+(n)
 #undef TROW
   R->in_hi = din;
@@ -188,21 +216,24 @@ __global__ void __launch_bounds__(256) k_twist_pick(const Singleton *__restrict_
 __global__ void __launch_bounds__(128) k_fixed_seg(const Singleton *__restrict__ sg, int ns,
                                                    const RepDesc *__restrict__ reps, const QElt *__restrict__ mq,
                                                    const RqiState *__restrict__ st, int K, int Wu, dd *P2,
-                                                   long long nbmax, SegRec *rec) {
+                                                   long long nbmax, SegRec *rec, int bal) {
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= (long long)ns * 2 * K) return;
-  const int k = (int)(g % K), isB = (int)((g / K) & 1), i = (int)(g / (2 * K));
+  const int kk = (int)(g % (2 * K)), i = (int)(g / (2 * K));
   const RqiState S = st[i];
   if (S.status != 0) return;
   SegRec *R = rec + g;
   const RepDesc Rp = reps[sg[i].rep];
   const int nb = Rp.nb, r = S.r;
+  const int KF = bal ? seg_kf(nb, r, 2 * K) : K;
+  const int isB = kk >= KF, k = isB ? kk - KF : kk;
+  K = isB ? 2 * K - KF : KF;  // this lane's segment count
   const bool light = S.it == 0;  // the first pass at the bisection midpoint only yields the RQC
   const QElt *q = mq + Rp.off;
   const dd lam = dd_make(S.lam_hi, S.lam_lo), nlam = dd_neg(lam);
   const int steps = isB ? nb - 1 - r : r;
   const int L = (steps + K - 1) / K;
-  const int t0 = min(k * L, steps), t1 = min((k + 1) * L, steps), tw = (k == 0) ? 0 : max(t0 - Wu, 0);
+  const int t0 = min(k * L, steps), t1 = min((k + 1) * L, steps), tw = (k == 0) ? 0 : max(t0 - (S.wide ? 8 * Wu : Wu), 0);
   dd *P = P2 + (long long)i * nbmax;
   if (t0 >= t1 && !(k == 0 && !isB)) {  // no steps (F segment 0 always reports d+(0) when r = 0)
     R->empty = 1;
@@ -266,7 +297,7 @@ __global__ void __launch_bounds__(128) k_fixed_seg(const Singleton *__restrict__
 
 // thread per singleton: junctions, gamma_r, ||z||^2, inertia, and the stask decision
 __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
-                             RqiState *st, int K, const SegRec *__restrict__ rec, double *W, ZMeta *zmeta,
+                             RqiState *st, int K, int bal, const SegRec *__restrict__ rec, double *W, ZMeta *zmeta,
                              int *diag_depth, double *fin_lo, double *fin_hi, long long *stats, int *nactive) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ns) return;
@@ -275,15 +306,17 @@ __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const Rep
   const Singleton s = sg[i];
   const RepDesc Rp = reps[s.rep];
   const int nb = Rp.nb, r = S.r, j = s.j;
-  const SegRec *F = rec + (long long)i * 2 * K, *B = F + K;
+  const int KF = bal ? seg_kf(nb, r, 2 * K) : K;
+  const SegRec *F = rec + (long long)i * 2 * K, *B = F + KF;
   bool good = true;
   dd Ssum = dd_from(0.0), Tsum = dd_from(0.0), dr = dd_from(0.0), tr = dd_from(0.0);
   int c = 0;
   for (int ln = 0; ln < 2; ln++) {
     const SegRec *X = ln ? B : F;
+    const int Kl = ln ? 2 * K - KF : KF;
     int prev = -1;
     dd acc = dd_from(0.0);
-    for (int k = 0; k < K; k++) {
+    for (int k = 0; k < Kl; k++) {
       const SegRec &a = X[k];
       if (a.empty) continue;
       good &= a.ok != 0;
@@ -303,6 +336,12 @@ __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const Rep
     }
   }
   if (!good) {
+    if (!S.wide) {  // a warm-up too short for this singleton: repeat the pass with an 8x longer one
+      st[i].wide = 1;
+      atomicAdd(nactive, 1);
+      atomicAdd((unsigned long long *)&stats[ST_SEG_WIDE], 1ull);
+      return;
+    }
     st[i].status = 2;
     atomicAdd((unsigned long long *)&stats[ST_HO_FIXED], 1ull);
     return;

@@ -98,7 +98,9 @@ struct mrrr_ctx {
   bool grouped = true;  // child bisection with CTAs grouped by representation (k_negcount_grp)
   int seg_k = 8, seg_w = 128;  // segmented root NegCount: segments per chain, warm-up rows (k_negcount_seg)
   bool rqi_seg = true;         // segmented RQI passes (kernels_rqi3.cuh); MRRR_RQISEG=0: the two-lane kernel only
-  int rqi_segk = 8, rqi_segw = 256;
+  int rqi_segk = 3, rqi_segw = 192;
+  bool rqi_bal = true;         // split a singleton's 2K segments between its lanes by length
+  bool zw_chunk = true;        // k_zwrite_chunk (chunked products, staged tiles) instead of the per-row warp scan
   int dev_rb = 4;             // rounds per device-driven batch
   bool dev_rounds = false;     // segmented rounds enqueued in batches on device-side counters (MRRR_DEVROUNDS=1;
                                // slower on C2: the oversized early-exit grids cost more than the saved syncs)
@@ -689,13 +691,13 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
         k_twist_pick<<<(unsigned)((nb + 31) / 32), 256, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, TF,
                                                                         TB, stride, rec, h->stats.as<long long>());
         launch_check(h);
-        for (int it = 0; it < MAX_RQI; it++) {
+        for (int it = 0; it < MAX_RQI + 2; it++) {  // + the passes repeated with a wide warm-up
           CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
           k_fixed_seg<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
                                                                             h->mq.as<QElt>(), rs, K, Wu, P2s, nbmax,
-                                                                            rec);
+                                                                            rec, h->rqi_bal ? 1 : 0);
           k_fixed_step<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(
-              sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, rec, W, h->zmeta.as<ZMeta>(),
+              sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, h->rqi_bal ? 1 : 0, rec, W, h->zmeta.as<ZMeta>(),
               diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
               diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), h->cnt.as<int>() + C_NFB);
           launch_check(h);
@@ -706,9 +708,14 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
           if (act == 0) break;
         }
         const int *stat = reinterpret_cast<const int *>(reinterpret_cast<const char *>(rs) + offsetof(RqiState, status));
-        k_zwrite<<<nblocks_for(32 * nb, 256), 256, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
-                                                                 h->my.as<YElt>(), P2s, nbmax, h->zmeta.as<ZMeta>(), Z,
-                                                                 ldz, stat, (int)(sizeof(RqiState) / sizeof(int)));
+        if (h->zw_chunk)
+          k_zwrite_chunk<<<nblocks_for(nb, 4), 128, 0, h->stream>>>(
+              sgb, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), P2s, nbmax, h->zmeta.as<ZMeta>(), Z, ldz, stat,
+              (int)(sizeof(RqiState) / sizeof(int)));
+        else
+          k_zwrite<<<nblocks_for(32 * nb, 256), 256, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
+                                                                   h->my.as<YElt>(), P2s, nbmax, h->zmeta.as<ZMeta>(),
+                                                                   Z, ldz, stat, (int)(sizeof(RqiState) / sizeof(int)));
         launch_check(h);
         CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
         k_rqi3_collect<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, rs, h->hand.as<Singleton>(),
@@ -725,9 +732,14 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
             h->zmeta.as<ZMeta>(), diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
             diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>());
         launch_check(h);
-        k_zwrite<<<nblocks_for(32 * nold, 256), 256, 0, h->stream>>>(
-            sgb, nold, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>() + 2 * stride * nbmax, nbmax,
-            h->zmeta.as<ZMeta>(), Z, ldz);
+        if (h->zw_chunk)
+          k_zwrite_chunk<<<nblocks_for(nold, 4), 128, 0, h->stream>>>(
+              sgb, nold, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>() + 2 * stride * nbmax, nbmax,
+              h->zmeta.as<ZMeta>(), Z, ldz);
+        else
+          k_zwrite<<<nblocks_for(32 * nold, 256), 256, 0, h->stream>>>(
+              sgb, nold, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>() + 2 * stride * nbmax, nbmax,
+              h->zmeta.as<ZMeta>(), Z, ldz);
       }
     } else {
       k_rqi<<<nblocks_for(nb, 64), 64, 0, h->stream>>>(
@@ -1222,6 +1234,8 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_RQISEG")) h->rqi_seg = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQISEGK")) h->rqi_segk = std::max(1, std::min(64, atoi(s)));
     if (const char *s = getenv("MRRR_RQISEGW")) h->rqi_segw = std::max(1, atoi(s));
+    if (const char *s = getenv("MRRR_RQIBAL")) h->rqi_bal = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_ZWCHUNK")) h->zw_chunk = atoi(s) != 0;
     if (const char *s = getenv("MRRR_BUD_FULL")) h->bud_full = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_BUD_TUBE")) h->bud_tube = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;

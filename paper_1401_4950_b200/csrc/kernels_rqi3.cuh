@@ -213,6 +213,78 @@ __global__ void __launch_bounds__(256) k_twist_pick(const Singleton *__restrict_
 }
 
 // the r-twisted factorization in dd: F steps 0..r-1, B steps 0..nb-2-r (rows nb-2 .. r)
+// one segment of a fixed-lambda pass: steps t in [tw, t1) of lane isB (F: row t, B: row nb-2-t), warm-up
+// [tw, t0) from a guess (the recurrence alone), result in *R (entry state at t0, exit state, partial norm,
+// inertia count).  LIGHT: the RQC-only pass (no factors stored, norm in fp64; A-31 note in DESIGN.md).
+__device__ __forceinline__ bool rcp_nr2(double b, double &r1, double &r2) {
+  const double rc = rcp_seed_dd(b);
+  double ee = __fma_rn(-b, rc, 1.0);
+  ee = __fma_rn(ee, ee, ee);
+  r1 = __fma_rn(rc, ee, rc);
+  const double e2 = __fma_rn(-b, r1, 1.0);
+  r2 = __fma_rn(r1, e2, r1);
+  return (fabs(b) > 0x1p-1000) && (fabs(b) < 0x1p1000);
+}
+template <bool LIGHT>
+__device__ __forceinline__ void seg_pass_t(const QElt *__restrict__ q, int nb, int isB, int t0, int t1, int tw,
+                                           dd lam, dd nlam, dd *P, SegRec *R) {
+  R->empty = 0;
+  const int rs = isB ? nb - 1 - tw : tw, og = isB ? 3 : 2;
+  dd den = dd_sub_nf(dd_make(__ldg(&q[rs].gb_hi), __ldg(&q[rs].gb_lo)), lam);
+  bool ok = true;
+  for (int t = tw; t < t0; t++) {
+    const double2 *pq = reinterpret_cast<const double2 *>(q + seg_row(isB, nb, t));
+    const dd c2 = D2(__ldg(pq)), gg = D2(__ldg(pq + og));
+    double r1, r2;
+    ok &= rcp_nr2(den.hi, r1, r2);
+    den = dd_sum3_nf(gg, nlam, dd_neg(qdiv(c2, den, r1, r2)));
+  }
+  const dd din = den;
+  dd Pq = dd_from(0.0), Bs = dd_from(0.0);
+  double A = 1.0;
+  int cnt = 0;
+  for (int t = t0; t < t1; t++) {
+    const int row = seg_row(isB, nb, t);
+    const double2 *pq = reinterpret_cast<const double2 *>(q + row);
+    const dd c2 = D2(__ldg(pq)), dl = D2(__ldg(pq + 1)), gg = D2(__ldg(pq + og));
+    double r1, r2;
+    ok &= rcp_nr2(den.hi, r1, r2);
+    Pq = qdiv(c2, den, r1, r2);
+    if (LIGHT) {
+      const double o = __dmul_rn(dl.hi, r2), o2 = __dmul_rn(o, o);
+      A = __dmul_rn(o2, A);
+      Bs.hi = __fma_rn(o2, Bs.hi, o2);
+    } else {
+      const dd o = qdiv(dl, den, r1, r2);
+      const dd out = fast_two_sum(o.hi, o.lo);
+      stw(P, row, out);
+      const dd o2 = dd_mul_nf(out, out);
+      A = __dmul_rn(o2.hi, A);
+      Bs = dd_mul_nf(o2, dd_add_d_nf(Bs, 1.0));
+    }
+    cnt += dd_sb(den);
+    den = dd_sum3_nf(gg, nlam, dd_neg(Pq));
+  }
+  ok &= isfinite(den.hi) && isfinite(den.lo) && isfinite(Bs.hi);
+  R->in_hi = din.hi;
+  R->in_lo = din.lo;
+  R->out_hi = den.hi;
+  R->out_lo = den.lo;
+  R->A = A;
+  R->B_hi = Bs.hi;
+  R->B_lo = Bs.lo;
+  const dd tl = fast_two_sum(Pq.hi, Pq.lo);  // B lane: c2(r)/omega(r+1) of the step on row r
+  R->t_hi = tl.hi;
+  R->t_lo = tl.lo;
+  R->cnt = cnt;
+  R->ok = ok ? 1 : 0;
+}
+__device__ __forceinline__ void seg_pass(const QElt *__restrict__ q, int nb, int isB, int t0, int t1, int tw,
+                                         bool light, dd lam, dd nlam, dd *P, SegRec *R) {
+  if (light) seg_pass_t<true>(q, nb, isB, t0, t1, tw, lam, nlam, P, R);
+  else seg_pass_t<false>(q, nb, isB, t0, t1, tw, lam, nlam, P, R);
+}
+
 __global__ void __launch_bounds__(128) k_fixed_seg(const Singleton *__restrict__ sg, int ns,
                                                    const RepDesc *__restrict__ reps, const QElt *__restrict__ mq,
                                                    const RqiState *__restrict__ st, int K, int Wu, dd *P2,
@@ -240,64 +312,53 @@ __global__ void __launch_bounds__(128) k_fixed_seg(const Singleton *__restrict__
     R->ok = 1;
     return;
   }
-  R->empty = 0;
-  const int rs = isB ? nb - 1 - tw : tw;
-  dd den = dd_sub_nf(dd_make(__ldg(&q[rs].gb_hi), __ldg(&q[rs].gb_lo)), lam);
-  dd din = den, Pl = dd_from(0.0);
-  double A = 1.0;
-  dd Bs = dd_from(0.0);
-  int cnt = 0;
-  bool ok = true;
-  for (int t = tw; t < t1; t++) {
-    if (t == t0) din = den;
-    const int row = seg_row(isB, nb, t);
-    const double2 *pq = reinterpret_cast<const double2 *>(q + row);
-    const dd c2 = D2(__ldg(pq)), dl = D2(__ldg(pq + 1)), gg = D2(__ldg(pq + (isB ? 3 : 2)));
-    const double b = den.hi;
-    ok &= (fabs(b) > 0x1p-1000) && (fabs(b) < 0x1p1000);
-    const double rc = rcp_seed_dd(b);
-    double ee = __fma_rn(-b, rc, 1.0);
-    ee = __fma_rn(ee, ee, ee);
-    const double r1 = __fma_rn(rc, ee, rc);
-    const double e2 = __fma_rn(-b, r1, 1.0);
-    const double r2 = __fma_rn(r1, e2, r1);
-    const dd Pq = qdiv(c2, den, r1, r2);
-    if (t >= t0) {
-      if (light) {  // RQC-only pass: no factors stored, norm in fp64 (A-31 note in DESIGN.md)
-        const double o = __dmul_rn(dl.hi, r2), o2 = __dmul_rn(o, o);
-        A = __dmul_rn(o2, A);
-        Bs = dd_from(__fma_rn(o2, Bs.hi, o2));
-      } else {
-        const dd o = qdiv(dl, den, r1, r2);
-        const dd out = fast_two_sum(o.hi, o.lo);
-        stw(P, row, out);
-        const dd o2 = dd_mul_nf(out, out);
-        A = __dmul_rn(o2.hi, A);
-        Bs = dd_mul_nf(o2, dd_add_d_nf(Bs, 1.0));
-      }
-      cnt += dd_sb(den);
-      Pl = Pq;
-    }
-    den = dd_sum3_nf(gg, nlam, dd_neg(Pq));
+  seg_pass(q, nb, isB, t0, t1, tw, light, lam, nlam, P, R);
+}
+
+// Chunk-major form of k_fixed_seg: the rows 0..nb-2 are cut into K2 fixed chunks and thread (chunk c,
+// singleton i) runs chunk c's F part (rows below r) and B part (rows from r on).  Consecutive threads are
+// consecutive singletons on the same chunk, so on a shared representation a warp's row loads coincide
+// (one or two distinct rows per step instead of 32), which is what bounds the lane-major layout (L2
+// sector traffic).  Records: rec[(i * K2 + c) * 2 + lane].
+__global__ void __launch_bounds__(128) k_fixed_chunk(const Singleton *__restrict__ sg, int ns,
+                                                     const RepDesc *__restrict__ reps, const QElt *__restrict__ mq,
+                                                     const RqiState *__restrict__ st, int K2, int Wu, dd *P2,
+                                                     long long nbmax, SegRec *rec) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (long long)ns * K2) return;
+  const int i = (int)(g % ns), c = (int)(g / ns);
+  const RqiState S = st[i];
+  if (S.status != 0) return;
+  const RepDesc Rp = reps[sg[i].rep];
+  const int nb = Rp.nb, r = S.r, steps = nb - 1;
+  const bool light = S.it == 0;
+  const QElt *q = mq + Rp.off;
+  const dd lam = dd_make(S.lam_hi, S.lam_lo), nlam = dd_neg(lam);
+  const int L = (steps + K2 - 1) / K2, W = S.wide ? 8 * Wu : Wu;
+  const int lo = min(c * L, steps), hi = min(lo + L, steps);
+  SegRec *RF = rec + ((long long)i * K2 + c) * 2, *RB = RF + 1;
+  dd *P = P2 + (long long)i * nbmax;
+  const int fb = min(hi, r);
+  if (fb > lo || c == 0) {  // F rows [lo, fb); chunk 0 always reports d+(0) (r = 0: no steps)
+    const int t1 = max(fb, lo);
+    seg_pass(q, nb, 0, lo, t1, lo == 0 ? 0 : max(lo - W, 0), light, lam, nlam, P, RF);
+  } else {
+    RF->empty = 1;
+    RF->ok = 1;
   }
-  ok &= isfinite(den.hi) && isfinite(den.lo) && isfinite(Bs.hi);
-  R->in_hi = din.hi;
-  R->in_lo = din.lo;
-  R->out_hi = den.hi;
-  R->out_lo = den.lo;
-  R->A = A;
-  R->B_hi = Bs.hi;
-  R->B_lo = Bs.lo;
-  const dd tl = fast_two_sum(Pl.hi, Pl.lo);  // B lane: c2(r)/omega(r+1) of the step on row r
-  R->t_hi = tl.hi;
-  R->t_lo = tl.lo;
-  R->cnt = cnt;
-  R->ok = ok ? 1 : 0;
+  const int ba = max(lo, r);
+  if (hi > ba) {  // B rows hi-1 down to ba: t in [nb-1-hi, nb-1-ba)
+    const int t0 = nb - 1 - hi;
+    seg_pass(q, nb, 1, t0, nb - 1 - ba, t0 == 0 ? 0 : max(t0 - W, 0), light, lam, nlam, P, RB);
+  } else {
+    RB->empty = 1;
+    RB->ok = 1;
+  }
 }
 
 // thread per singleton: junctions, gamma_r, ||z||^2, inertia, and the stask decision
 __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
-                             RqiState *st, int K, int bal, const SegRec *__restrict__ rec, double *W, ZMeta *zmeta,
+                             RqiState *st, int K, int bal, int chunk, const SegRec *__restrict__ rec, double *W, ZMeta *zmeta,
                              int *diag_depth, double *fin_lo, double *fin_hi, long long *stats, int *nactive) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ns) return;
@@ -306,17 +367,19 @@ __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const Rep
   const Singleton s = sg[i];
   const RepDesc Rp = reps[s.rep];
   const int nb = Rp.nb, r = S.r, j = s.j;
-  const int KF = bal ? seg_kf(nb, r, 2 * K) : K;
-  const SegRec *F = rec + (long long)i * 2 * K, *B = F + KF;
+  const int KF = chunk ? 2 * K : bal ? seg_kf(nb, r, 2 * K) : K;
+  const SegRec *F = rec + (long long)i * 2 * K * (chunk ? 2 : 1), *B = F + KF;
   bool good = true;
   dd Ssum = dd_from(0.0), Tsum = dd_from(0.0), dr = dd_from(0.0), tr = dd_from(0.0);
   int c = 0;
   for (int ln = 0; ln < 2; ln++) {
-    const SegRec *X = ln ? B : F;
-    const int Kl = ln ? 2 * K - KF : KF;
+    // chunk layout: F records at [2c], B records at [2c + 1] walked from the last chunk down
+    const SegRec *X = chunk ? F : ln ? B : F;
+    const int Kl = chunk ? 2 * K : ln ? 2 * K - KF : KF;
     int prev = -1;
     dd acc = dd_from(0.0);
-    for (int k = 0; k < Kl; k++) {
+    for (int kk = 0; kk < Kl; kk++) {
+      const int k = chunk ? 2 * (ln ? Kl - 1 - kk : kk) + ln : kk;
       const SegRec &a = X[k];
       if (a.empty) continue;
       good &= a.ok != 0;

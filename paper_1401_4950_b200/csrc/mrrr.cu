@@ -98,8 +98,9 @@ struct mrrr_ctx {
   bool grouped = true;  // child bisection with CTAs grouped by representation (k_negcount_grp)
   int seg_k = 8, seg_w = 128;  // segmented root NegCount: segments per chain, warm-up rows (k_negcount_seg)
   bool rqi_seg = true;         // segmented RQI passes (kernels_rqi3.cuh); MRRR_RQISEG=0: the two-lane kernel only
-  int rqi_segk = 3, rqi_segw = 192;
+  int rqi_segk = 8, rqi_segw = 192;
   bool rqi_bal = true;         // split a singleton's 2K segments between its lanes by length
+  bool rqi_chunk = true;       // chunk-major fixed passes (k_fixed_chunk) instead of lane-major (k_fixed_seg)
   bool zw_chunk = true;        // k_zwrite_chunk (chunked products, staged tiles) instead of the per-row warp scan
   int dev_rb = 4;             // rounds per device-driven batch
   bool dev_rounds = false;     // segmented rounds enqueued in batches on device-side counters (MRRR_DEVROUNDS=1;
@@ -677,7 +678,7 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
         // segmented passes (kernels_rqi3.cuh); singletons they hand over go through k_rqi2 below
         const int K = h->rqi_segk, Wu = h->rqi_segw;
         CK(h->rqst.ensure(sizeof(RqiState) * stride));
-        CK(h->rqrec.ensure(sizeof(SegRec) * stride * 2 * K));
+        CK(h->rqrec.ensure(sizeof(SegRec) * stride * 4 * K));  // chunk layout: 2K chunks x 2 lanes
         CK(h->hand.ensure(sizeof(Singleton) * stride));
         double *TF = reinterpret_cast<double *>(h->wsA.as<dd>());  // [row * stride + singleton]
         double *TB = TF + stride * nbmax;
@@ -693,11 +694,16 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
         launch_check(h);
         for (int it = 0; it < MAX_RQI + 2; it++) {  // + the passes repeated with a wide warm-up
           CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
-          k_fixed_seg<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
-                                                                            h->mq.as<QElt>(), rs, K, Wu, P2s, nbmax,
-                                                                            rec, h->rqi_bal ? 1 : 0);
+          if (h->rqi_chunk)
+            k_fixed_chunk<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(
+                sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, 2 * K, Wu, P2s, nbmax, rec);
+          else
+            k_fixed_seg<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
+                                                                              h->mq.as<QElt>(), rs, K, Wu, P2s, nbmax,
+                                                                              rec, h->rqi_bal ? 1 : 0);
           k_fixed_step<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(
-              sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, h->rqi_bal ? 1 : 0, rec, W, h->zmeta.as<ZMeta>(),
+              sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, h->rqi_bal ? 1 : 0, h->rqi_chunk ? 1 : 0, rec, W,
+              h->zmeta.as<ZMeta>(),
               diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
               diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), h->cnt.as<int>() + C_NFB);
           launch_check(h);
@@ -1236,6 +1242,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_RQISEGW")) h->rqi_segw = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_RQIBAL")) h->rqi_bal = atoi(s) != 0;
     if (const char *s = getenv("MRRR_ZWCHUNK")) h->zw_chunk = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_RQICHUNK")) h->rqi_chunk = atoi(s) != 0;
     if (const char *s = getenv("MRRR_BUD_FULL")) h->bud_full = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_BUD_TUBE")) h->bud_tube = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;

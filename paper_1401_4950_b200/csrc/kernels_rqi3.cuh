@@ -225,9 +225,26 @@ __device__ __forceinline__ bool rcp_nr2(double b, double &r1, double &r2) {
   r2 = __fma_rn(r1, e2, r1);
   return (fabs(b) > 0x1p-1000) && (fabs(b) < 0x1p1000);
 }
+// bulk (TMA-engine) store of a thread's staged factor rows: one contiguous run per 8 rows instead of 8
+// lane-scattered 16-byte stores (a warp's lanes are different singletons, so plain stores hit 32 lines)
+__device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, unsigned bytes) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+constexpr int ZG = 8;             // factor rows per bulk store
+constexpr int ZSTRIDE = 2 * ZG + 1;  // double2 per thread: two groups + pad (16-byte lanes, conflict-free)
+
 template <bool LIGHT>
 __device__ __forceinline__ void seg_pass_t(const QElt *__restrict__ q, int nb, int isB, int t0, int t1, int tw,
-                                           dd lam, dd nlam, dd *P, SegRec *R) {
+                                           dd lam, dd nlam, dd *P, SegRec *R, double2 *stg) {
   R->empty = 0;
   const int rs = isB ? nb - 1 - tw : tw, og = isB ? 3 : 2;
   dd den = dd_sub_nf(dd_make(__ldg(&q[rs].gb_hi), __ldg(&q[rs].gb_lo)), lam);
@@ -242,11 +259,18 @@ __device__ __forceinline__ void seg_pass_t(const QElt *__restrict__ q, int nb, i
   const dd din = den;
   dd Pq = dd_from(0.0), Bs = dd_from(0.0);
   double A = 1.0;
-  int cnt = 0;
+  int cnt = 0, ng = 0, grp = 0;
+  // the next row is loaded one step ahead (the loads otherwise sit on the recurrence's critical path)
+  const int dq = isB ? -4 : 4;  // double2 per QElt row, in the lane's direction
+  const double2 *pq = reinterpret_cast<const double2 *>(q + min(max(seg_row(isB, nb, t0), 0), nb - 1));
+  double2 nc2 = __ldg(pq), ndl = __ldg(pq + 1), ngg = __ldg(pq + og);
   for (int t = t0; t < t1; t++) {
     const int row = seg_row(isB, nb, t);
-    const double2 *pq = reinterpret_cast<const double2 *>(q + row);
-    const dd c2 = D2(__ldg(pq)), dl = D2(__ldg(pq + 1)), gg = D2(__ldg(pq + og));
+    const dd c2 = D2(nc2), dl = D2(ndl), gg = D2(ngg);
+    if (t + 1 < t1) pq += dq;
+    nc2 = __ldg(pq);
+    ndl = __ldg(pq + 1);
+    ngg = __ldg(pq + og);
     double r1, r2;
     ok &= rcp_nr2(den.hi, r1, r2);
     Pq = qdiv(c2, den, r1, r2);
@@ -257,7 +281,18 @@ __device__ __forceinline__ void seg_pass_t(const QElt *__restrict__ q, int nb, i
     } else {
       const dd o = qdiv(dl, den, r1, r2);
       const dd out = fast_two_sum(o.hi, o.lo);
-      stw(P, row, out);
+      if (stg) {  // stage; B lanes fill their group backwards so it is ascending in memory
+        stg[grp * ZG + (isB ? ZG - 1 - ng : ng)] = make_double2(out.hi, out.lo);
+        if (++ng == ZG || t + 1 == t1) {
+          const int low = isB ? row : row - ng + 1;
+          bulk_store(P + low, stg + grp * ZG + (isB ? ZG - ng : 0), (unsigned)(ng * sizeof(double2)));
+          grp ^= 1;
+          ng = 0;
+          bulk_wait_read<1>();  // the other group's previous store has read its rows
+        }
+      } else {
+        stw(P, row, out);
+      }
       const dd o2 = dd_mul_nf(out, out);
       A = __dmul_rn(o2.hi, A);
       Bs = dd_mul_nf(o2, dd_add_d_nf(Bs, 1.0));
@@ -265,6 +300,7 @@ __device__ __forceinline__ void seg_pass_t(const QElt *__restrict__ q, int nb, i
     cnt += dd_sb(den);
     den = dd_sum3_nf(gg, nlam, dd_neg(Pq));
   }
+  if (!LIGHT && stg) bulk_wait_all();
   ok &= isfinite(den.hi) && isfinite(den.lo) && isfinite(Bs.hi);
   R->in_hi = din.hi;
   R->in_lo = din.lo;
@@ -280,9 +316,9 @@ __device__ __forceinline__ void seg_pass_t(const QElt *__restrict__ q, int nb, i
   R->ok = ok ? 1 : 0;
 }
 __device__ __forceinline__ void seg_pass(const QElt *__restrict__ q, int nb, int isB, int t0, int t1, int tw,
-                                         bool light, dd lam, dd nlam, dd *P, SegRec *R) {
-  if (light) seg_pass_t<true>(q, nb, isB, t0, t1, tw, lam, nlam, P, R);
-  else seg_pass_t<false>(q, nb, isB, t0, t1, tw, lam, nlam, P, R);
+                                         bool light, dd lam, dd nlam, dd *P, SegRec *R, double2 *stg = nullptr) {
+  if (light) seg_pass_t<true>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, nullptr);
+  else seg_pass_t<false>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, stg);
 }
 
 __global__ void __launch_bounds__(128) k_fixed_seg(const Singleton *__restrict__ sg, int ns,
@@ -315,45 +351,76 @@ __global__ void __launch_bounds__(128) k_fixed_seg(const Singleton *__restrict__
   seg_pass(q, nb, isB, t0, t1, tw, light, lam, nlam, P, R);
 }
 
-// Chunk-major form of k_fixed_seg: the rows 0..nb-2 are cut into K2 fixed chunks and thread (chunk c,
-// singleton i) runs chunk c's F part (rows below r) and B part (rows from r on).  Consecutive threads are
-// consecutive singletons on the same chunk, so on a shared representation a warp's row loads coincide
-// (one or two distinct rows per step instead of 32), which is what bounds the lane-major layout (L2
-// sector traffic).  Records: rec[(i * K2 + c) * 2 + lane].
+// Chunk-major form of k_fixed_seg: the rows 0..nb-2 are cut into K2 fixed chunks of L rows.  Thread
+// (slot c, singleton i), c < K2, runs chunk c's primary part: its F part (rows [lo, min(hi, r))) if the
+// chunk starts below r (chunk 0 always: it reports d+(0) even when r = 0), else the whole chunk as B part;
+// slot K2 runs the B part (rows [r, hi)) of the chunk holding r when that chunk's primary is its F part.
+// Each thread runs ONE part, with its direction as data, so F and B lanes of a warp share the instruction
+// stream; consecutive threads are consecutive singletons on the same chunk, so on a shared
+// representation a warp loads one or two distinct rows per step (the lane-major layout loads 32).
+// Records: rec[(i * K2 + c) * 2 + lane] (lane 0 F, 1 B); parts that do not exist are marked empty.
 __global__ void __launch_bounds__(128) k_fixed_chunk(const Singleton *__restrict__ sg, int ns,
                                                      const RepDesc *__restrict__ reps, const QElt *__restrict__ mq,
                                                      const RqiState *__restrict__ st, int K2, int Wu, dd *P2,
-                                                     long long nbmax, SegRec *rec) {
+                                                     long long nbmax, SegRec *rec, int bulk) {
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= (long long)ns * K2) return;
-  const int i = (int)(g % ns), c = (int)(g / ns);
+  if (g >= (long long)ns * (K2 + 1)) return;
+  const int i = (int)(g % ns), slot = (int)(g / ns);
   const RqiState S = st[i];
   if (S.status != 0) return;
   const RepDesc Rp = reps[sg[i].rep];
   const int nb = Rp.nb, r = S.r, steps = nb - 1;
+  const int L = max((steps + K2 - 1) / K2, 1), W = S.wide ? 8 * Wu : Wu;
+  const int cr = (r < steps) ? r / L : -1;  // chunk holding row r (none when r = nb-1: B has no steps)
+  auto bounds = [&](int c, int &lo, int &hi) {
+    lo = min(c * L, steps);
+    hi = min(lo + L, steps);
+  };
+  auto fprim = [&](int c, int lo) { return c == 0 || lo < r; };
+  SegRec *R0 = rec + (long long)i * K2 * 2;
+  int isB, t0, t1;
+  SegRec *R;
+  if (slot < K2) {
+    int lo, hi;
+    bounds(slot, lo, hi);
+    if (fprim(slot, lo)) {
+      isB = 0;
+      t0 = lo;
+      t1 = max(min(hi, r), lo);
+      R = R0 + 2 * slot;
+      if (slot != cr) {
+        R0[2 * slot + 1].empty = 1;
+        R0[2 * slot + 1].ok = 1;
+      }
+    } else {
+      R0[2 * slot].empty = 1;
+      R0[2 * slot].ok = 1;
+      R = R0 + 2 * slot + 1;
+      if (hi <= lo) {
+        R->empty = 1;
+        R->ok = 1;
+        return;
+      }
+      isB = 1;
+      t0 = nb - 1 - hi;
+      t1 = nb - 1 - lo;
+    }
+  } else {
+    if (cr < 0) return;
+    int lo, hi;
+    bounds(cr, lo, hi);
+    if (!fprim(cr, lo)) return;  // the primary thread runs the whole chunk as B part
+    isB = 1;
+    t0 = nb - 1 - hi;
+    t1 = nb - 1 - r;
+    R = R0 + 2 * cr + 1;
+  }
   const bool light = S.it == 0;
   const QElt *q = mq + Rp.off;
   const dd lam = dd_make(S.lam_hi, S.lam_lo), nlam = dd_neg(lam);
-  const int L = (steps + K2 - 1) / K2, W = S.wide ? 8 * Wu : Wu;
-  const int lo = min(c * L, steps), hi = min(lo + L, steps);
-  SegRec *RF = rec + ((long long)i * K2 + c) * 2, *RB = RF + 1;
-  dd *P = P2 + (long long)i * nbmax;
-  const int fb = min(hi, r);
-  if (fb > lo || c == 0) {  // F rows [lo, fb); chunk 0 always reports d+(0) (r = 0: no steps)
-    const int t1 = max(fb, lo);
-    seg_pass(q, nb, 0, lo, t1, lo == 0 ? 0 : max(lo - W, 0), light, lam, nlam, P, RF);
-  } else {
-    RF->empty = 1;
-    RF->ok = 1;
-  }
-  const int ba = max(lo, r);
-  if (hi > ba) {  // B rows hi-1 down to ba: t in [nb-1-hi, nb-1-ba)
-    const int t0 = nb - 1 - hi;
-    seg_pass(q, nb, 1, t0, nb - 1 - ba, t0 == 0 ? 0 : max(t0 - W, 0), light, lam, nlam, P, RB);
-  } else {
-    RB->empty = 1;
-    RB->ok = 1;
-  }
+  __shared__ __align__(16) double2 stage[128 * ZSTRIDE];
+  seg_pass(q, nb, isB, t0, t1, t0 == 0 ? 0 : max(t0 - W, 0), light, lam, nlam, P2 + (long long)i * nbmax, R,
+           bulk ? stage + threadIdx.x * ZSTRIDE : nullptr);
 }
 
 // thread per singleton: junctions, gamma_r, ||z||^2, inertia, and the stask decision

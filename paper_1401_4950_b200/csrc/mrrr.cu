@@ -101,6 +101,7 @@ struct mrrr_ctx {
   int rqi_segk = 8, rqi_segw = 192;
   bool rqi_bal = true;         // split a singleton's 2K segments between its lanes by length
   bool rqi_chunk = true;       // chunk-major fixed passes (k_fixed_chunk) instead of lane-major (k_fixed_seg)
+  bool rqi_bulk = true;        // k_fixed_chunk stores the factors by bulk copies of staged 8-row runs
   bool zw_chunk = true;        // k_zwrite_chunk (chunked products, staged tiles) instead of the per-row warp scan
   int dev_rb = 4;             // rounds per device-driven batch
   bool dev_rounds = false;     // segmented rounds enqueued in batches on device-side counters (MRRR_DEVROUNDS=1;
@@ -695,8 +696,9 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
         for (int it = 0; it < MAX_RQI + 2; it++) {  // + the passes repeated with a wide warm-up
           CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
           if (h->rqi_chunk)
-            k_fixed_chunk<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(
-                sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, 2 * K, Wu, P2s, nbmax, rec);
+            k_fixed_chunk<<<nblocks_for((2 * K + 1) * nb, 128), 128, 0, h->stream>>>(
+                sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, 2 * K, Wu, P2s, nbmax, rec,
+                h->rqi_bulk ? 1 : 0);
           else
             k_fixed_seg<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
                                                                               h->mq.as<QElt>(), rs, K, Wu, P2s, nbmax,
@@ -1243,6 +1245,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_RQIBAL")) h->rqi_bal = atoi(s) != 0;
     if (const char *s = getenv("MRRR_ZWCHUNK")) h->zw_chunk = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQICHUNK")) h->rqi_chunk = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_RQIBULK")) h->rqi_bulk = atoi(s) != 0;
     if (const char *s = getenv("MRRR_BUD_FULL")) h->bud_full = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_BUD_TUBE")) h->bud_tube = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;

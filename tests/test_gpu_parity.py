@@ -302,7 +302,8 @@ def test_division_fast_path_is_ieee(torch_cuda):
                                  {"MRRR_TARGET_CHAINS": "8192"}, {"MRRR_SEGK": "1"}, {"MRRR_RQISEG": "0"},
                                  {"MRRR_RQISEG": "1", "MRRR_RQISEGK": "1"}, {"MRRR_RQIBAL": "0"},
                                  {"MRRR_RQISEGW": "16"}, {"MRRR_ZWCHUNK": "0"},
-                                 {"MRRR_RQICHUNK": "0"}, {"MRRR_RQICHUNK": "1", "MRRR_RQISEGW": "16"}])
+                                 {"MRRR_RQICHUNK": "0"}, {"MRRR_RQICHUNK": "1", "MRRR_RQISEGW": "16"},
+                                 {"MRRR_RQIBULK": "0"}])
 def test_bisection_schedules_are_bit_identical(torch_cuda, env, monkeypatch):
     # every evaluation schedule (k-section budget, TMA staging, representation-grouped child rounds, guided
     # tube rounds) must reproduce the oracle's sequential Alg. Bisection intervals bit for bit (rule W)

@@ -103,6 +103,7 @@ struct mrrr_ctx {
   bool rqi_chunk = true;       // chunk-major fixed passes (k_fixed_chunk) instead of lane-major (k_fixed_seg)
   bool rqi_bulk = true;        // k_fixed_chunk stores the factors by bulk copies of staged 8-row runs
   bool zw_chunk = true;        // k_zwrite_chunk (chunked products, staged tiles) instead of the per-row warp scan
+  long long seg_threads = 0;  // adaptive segment count: target threads per segmented round (0: off; no gain measured)
   int dev_rb = 4;             // rounds per device-driven batch
   bool dev_rounds = false;     // segmented rounds enqueued in batches on device-side counters (MRRR_DEVROUNDS=1;
                                // slower on C2: the oversized early-exit grids cost more than the saved syncs)
@@ -542,9 +543,13 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
     zero_counters(h);
     CK(cudaEventRecord(h->nc0, h->stream));
     if (seg_on) {
-      // segmented chains (kernels_guided.cuh): K concurrent segments per NegCount, verified bit-exact
-      const int K = h->seg_k, L = (single_nb - 1 + K - 1) / K;
+      // segmented chains (kernels_guided.cuh): K concurrent segments per NegCount, verified bit-exact.
+      // Rounds with few chains (one point per node) cut them into more segments, so that about
+      // seg_threads threads keep the SMs busy (a round is latency-bound below that)
       const long long tot = nch + nex;
+      int K = h->seg_k;
+      while (2 * K <= 64 && tot * 2 * K <= h->seg_threads && (single_nb - 1) >= 2 * (2 * K) * h->seg_w) K *= 2;
+      const int L = (single_nb - 1 + K - 1) / K;
       CK(h->segout.ensure(sizeof(SegOut) * tot * K));
       CK(h->segfb.ensure(sizeof(int4) * tot));
       CK(h->segfbs.ensure(sizeof(double) * tot));
@@ -1246,6 +1251,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_ZWCHUNK")) h->zw_chunk = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQICHUNK")) h->rqi_chunk = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQIBULK")) h->rqi_bulk = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_SEGTHREADS")) h->seg_threads = atoll(s);
     if (const char *s = getenv("MRRR_BUD_FULL")) h->bud_full = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_BUD_TUBE")) h->bud_tube = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;

@@ -227,6 +227,10 @@ struct SegOut {
   int cnt, ok;
 };
 
+// CH chains per thread (chains c0 + j * 128 of the CTA's 128 * CH): the CTA's chains all run segment k
+// over the same staged rows, so a thread interleaves CH independent recurrences on one shared-memory
+// row load (instruction-level parallelism where a round has few chains, fewer loads per step)
+template <int CH>
 __global__ void __launch_bounds__(128) k_negcount_seg(const Node *__restrict__ nodes, int nnode, int m,
                                                       const ExplicitChain *__restrict__ ex, int nex,
                                                       const RepDesc *__restrict__ reps,
@@ -242,13 +246,22 @@ __global__ void __launch_bounds__(128) k_negcount_seg(const Node *__restrict__ n
   }
   const long long nn = (long long)nnode * ((1 << m) - 1);
   const long long tot = nn + nex;
-  if ((long long)blockIdx.x * blockDim.x >= tot) return;  // whole CTA idle (uniform exit)
-  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long cb = (long long)blockIdx.x * blockDim.x * CH;
+  if (cb >= tot) return;  // whole CTA idle (uniform exit)
   const int k = blockIdx.y;
-  const bool act = c < tot;
-  double sig;
-  int rep;
-  chain_of(nodes, m, nn, ex, act ? c : tot - 1, sig, rep);
+  double sig[CH];
+  bool act[CH];
+  int rep = 0;
+#pragma unroll
+  for (int j = 0; j < CH; j++) {
+    const long long c = cb + threadIdx.x + j * blockDim.x;
+    act[j] = c < tot;
+    double sj;
+    int rj;
+    chain_of(nodes, m, nn, ex, act[j] ? c : tot - 1, sj, rj);
+    sig[j] = sj;
+    rep = rj;
+  }
   const RepDesc R = reps[rep];  // one representation for the whole launch (root)
   const int nb = R.nb;
   const double2 *M = mx + R.off;
@@ -267,9 +280,15 @@ __global__ void __launch_bounds__(128) k_negcount_seg(const Node *__restrict__ n
     }
   }
   __syncthreads();
-  double s = -sig, s_in = -sig;
-  int cnt = 0;
+  double s[CH], s_in[CH];
+  int cnt[CH];
   bool ok = true;
+#pragma unroll
+  for (int j = 0; j < CH; j++) {
+    s[j] = -sig[j];
+    s_in[j] = -sig[j];
+    cnt[j] = 0;
+  }
   for (int t = 0; t < ntile; t++) {
     const int b = t & 1;
     mbar_wait(&bar[b], (unsigned)((t >> 1) & 1));
@@ -281,22 +300,35 @@ __global__ void __launch_bounds__(128) k_negcount_seg(const Node *__restrict__ n
     const int nw = max(0, min(len, bk - row0));
     for (; kk < nw; kk++) {
       const double2 mm = T[kk];
-      const double dp = __dadd_rn(mm.x, s);
-      const double q = div_fast_nocheck(s, dp);
-      ok &= div_range_ok(s, dp, q);
-      s = __dsub_rn(__dmul_rn(q, mm.y), sig);
+#pragma unroll
+      for (int j = 0; j < CH; j++) {
+        const double dp = __dadd_rn(mm.x, s[j]);
+        const double q = div_fast_nocheck(s[j], dp);
+        ok &= div_range_ok(s[j], dp, q);
+        s[j] = __dsub_rn(__dmul_rn(q, mm.y), sig[j]);
+      }
     }
-    if (row0 + kk == bk) s_in = s;
+    if (row0 + kk == bk) {
+#pragma unroll
+      for (int j = 0; j < CH; j++) s_in[j] = s[j];
+    }
 #pragma unroll 4
     for (; kk < len; kk++) {
       const double2 mm = T[kk];
-      const double dp = __dadd_rn(mm.x, s);
-      const double q = div_fast_nocheck(s, dp);
-      ok &= div_range_ok(s, dp, q);
-      s = __dsub_rn(__dmul_rn(q, mm.y), sig);
-      cnt += (int)((unsigned)__double2hiint(dp) >> 31);
+#pragma unroll
+      for (int j = 0; j < CH; j++) {
+        const double dp = __dadd_rn(mm.x, s[j]);
+        const double q = div_fast_nocheck(s[j], dp);
+        ok &= div_range_ok(s[j], dp, q);
+        s[j] = __dsub_rn(__dmul_rn(q, mm.y), sig[j]);
+        cnt[j] += (int)((unsigned)__double2hiint(dp) >> 31);
+      }
     }
-    if (k == K - 1 && t == ntile - 1) cnt += sbx(__dadd_rn(T[nb - 1 - row0].x, s));
+    if (k == K - 1 && t == ntile - 1) {
+      const double dl = T[nb - 1 - row0].x;
+#pragma unroll
+      for (int j = 0; j < CH; j++) cnt[j] += sbx(__dadd_rn(dl, s[j]));
+    }
     __syncthreads();
     if (threadIdx.x == 0 && t + 2 < ntile) {
       int len2 = min(NEG_TILE, nrow - (t + 2) * NEG_TILE);
@@ -304,14 +336,17 @@ __global__ void __launch_bounds__(128) k_negcount_seg(const Node *__restrict__ n
                   &bar[b]);
     }
   }
-  if (bk == w0) s_in = -sig;  // no warm-up (k = 0): the exact start
-  if (act) {
-    SegOut o;
-    o.s_in = s_in;
-    o.s_out = s;
-    o.cnt = cnt;
-    o.ok = ok ? 1 : 0;
-    seg[c * K + k] = o;
+#pragma unroll
+  for (int j = 0; j < CH; j++) {
+    if (bk == w0) s_in[j] = -sig[j];  // no warm-up (k = 0): the exact start
+    if (act[j]) {
+      SegOut o;
+      o.s_in = s_in[j];
+      o.s_out = s[j];
+      o.cnt = cnt[j];
+      o.ok = ok ? 1 : 0;  // one flag for the thread's chains: a failed range test sends both to the careful tail
+      seg[(cb + threadIdx.x + j * blockDim.x) * K + k] = o;
+    }
   }
 }
 

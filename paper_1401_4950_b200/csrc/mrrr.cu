@@ -103,6 +103,7 @@ struct mrrr_ctx {
   bool rqi_chunk = true;       // chunk-major fixed passes (k_fixed_chunk) instead of lane-major (k_fixed_seg)
   bool rqi_bulk = true;        // k_fixed_chunk stores the factors by bulk copies of staged 8-row runs
   bool zw_chunk = true;        // k_zwrite_chunk (chunked products, staged tiles) instead of the per-row warp scan
+  long long seg_ch2 = 0;  // segmented rounds with at most this many chains run two chains per thread (slower on C2)
   long long seg_threads = 0;  // adaptive segment count: target threads per segmented round (0: off; no gain measured)
   int dev_rb = 4;             // rounds per device-driven batch
   bool dev_rounds = false;     // segmented rounds enqueued in batches on device-side counters (MRRR_DEVROUNDS=1;
@@ -418,7 +419,7 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
     for (int b = 0; b < RB && r < MAXR; b++, r++) {
       Node *in = (r & 1) ? nxt : cur, *out = (r & 1) ? cur : nxt;
       CK(cudaEventRecord(h->rev[2 * r], h->stream));
-      k_negcount_seg<<<gseg, 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
+      k_negcount_seg<1><<<gseg, 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
           in, 0, 0, nullptr, 0, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L, h->seg_w, h->segout.as<SegOut>(),
           nn + r, h->mmax, h->target_chains);
       CK(cudaEventRecord(h->rev[2 * r + 1], h->stream));
@@ -553,10 +554,16 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
       CK(h->segout.ensure(sizeof(SegOut) * tot * K));
       CK(h->segfb.ensure(sizeof(int4) * tot));
       CK(h->segfbs.ensure(sizeof(double) * tot));
-      dim3 grid((unsigned)((tot + 127) / 128), (unsigned)K);
-      k_negcount_seg<<<grid, 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
-          cur, nnode, m, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L, h->seg_w,
-          h->segout.as<SegOut>(), nullptr, 0, 0);
+      const int CH = (tot <= h->seg_ch2) ? 2 : 1;  // few chains: two per thread (ILP)
+      dim3 grid((unsigned)((tot + 128 * CH - 1) / (128 * CH)), (unsigned)K);
+      if (CH == 2)
+        k_negcount_seg<2><<<grid, 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
+            cur, nnode, m, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L,
+            h->seg_w, h->segout.as<SegOut>(), nullptr, 0, 0);
+      else
+        k_negcount_seg<1><<<grid, 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
+            cur, nnode, m, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L,
+            h->seg_w, h->segout.as<SegOut>(), nullptr, 0, 0);
       launch_check(h);
       k_seg_combine<<<nblocks_for(tot, 128), 128, 0, h->stream>>>(tot, nch, K, h->segout.as<SegOut>(),
                                                                    h->counts.as<int>(), h->excounts.as<int>(),
@@ -1252,6 +1259,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_RQICHUNK")) h->rqi_chunk = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQIBULK")) h->rqi_bulk = atoi(s) != 0;
     if (const char *s = getenv("MRRR_SEGTHREADS")) h->seg_threads = atoll(s);
+    if (const char *s = getenv("MRRR_SEGCH2")) h->seg_ch2 = atoll(s);
     if (const char *s = getenv("MRRR_BUD_FULL")) h->bud_full = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_BUD_TUBE")) h->bud_tube = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;

@@ -415,3 +415,112 @@ __global__ void k_seg_fallback(const int4 *__restrict__ fb, const int *__restric
   if (c < nn) counts[c] = cnt;
   else excounts[c - nn] = cnt;
 }
+
+// ---------------------------------------------------------------------------
+// Segmented y-NegCount (q-form, dd): thread (segment k, chain c) runs rows [bk, ek) of chain c after a
+// warm-up of Wu rows from the no-coupling guess; consecutive threads are consecutive chains on the same
+// segment (on one representation their row loads coincide).  Chains too short for K segments run whole
+// in segment 0.  k_seg_combine_y accepts a chain iff every junction state is bit-identical to its
+// predecessor's exit (then the count equals the sequential negcount_y_q's); the rest are recounted whole.
+// ---------------------------------------------------------------------------
+struct SegOutY {
+  double in_hi, in_lo, out_hi, out_lo;
+  int cnt, ok, empty, pad;
+};
+__global__ void __launch_bounds__(128) k_negcount_seg_y(const Node *__restrict__ nodes, int nnode, int m,
+                                                        const ExplicitChain *__restrict__ ex, int nex,
+                                                        const RepDesc *__restrict__ reps, const QElt *__restrict__ mq,
+                                                        int K, int Wu, SegOutY *seg) {
+  const long long nn = (long long)nnode * ((1 << m) - 1), tot = nn + nex;
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= tot * K) return;
+  const int k = (int)(g / tot);
+  const long long c = g % tot;
+  double sig;
+  int rep;
+  chain_of(nodes, m, nn, ex, c, sig, rep);
+  const RepDesc R = reps[rep];
+  const int nb = R.nb, steps = nb - 1;
+  SegOutY *o = seg + c * K + k;
+  int bk, ek, w0;
+  if (steps >= 2 * K * Wu) {
+    const int L = (steps + K - 1) / K;
+    bk = min(k * L, steps);
+    ek = min(bk + L, steps);
+    w0 = (k == 0) ? 0 : max(bk - Wu, 0);
+  } else {
+    if (k > 0) {
+      o->empty = 1;
+      o->ok = 1;
+      return;
+    }
+    bk = 0;
+    ek = steps;
+    w0 = 0;
+  }
+  const dd sigma = dd_from(sig);
+  const double2 *p = reinterpret_cast<const double2 *>(mq + R.off);
+  const double2 gb0 = __ldg(p + 4 * w0 + 3);
+  dd den = dd_sub_nf(dd_make(gb0.x, gb0.y), sigma);  // gb(w0) - sigma: exact at row 0, a guess elsewhere
+  dd din = den;
+  int cnt = 0;
+  bool ok = true;
+  double2 c2n = __ldg(p + 4 * w0), gn = __ldg(p + 4 * w0 + 2);
+  for (int i = w0; i < ek; i++) {
+    const double2 c2v = c2n, gv = gn;
+    const int in = min(i + 1, nb - 1);
+    c2n = __ldg(p + 4 * in);
+    gn = __ldg(p + 4 * in + 2);
+    if (i == bk) din = den;
+    if (i >= bk) cnt += dd_sb(den);
+    den = y_step(den, c2v, gv, sigma, ok);
+  }
+  if (ek == steps) cnt += dd_sb(den);  // den(nb-1) closes the count
+  o->in_hi = din.hi;
+  o->in_lo = din.lo;
+  o->out_hi = den.hi;
+  o->out_lo = den.lo;
+  o->cnt = cnt;
+  o->ok = (ok && isfinite(den.hi) && isfinite(den.lo)) ? 1 : 0;
+  o->empty = 0;
+}
+__global__ void k_seg_combine_y(long long tot, long long nn, int K, const SegOutY *__restrict__ seg, int *counts,
+                                int *excounts, long long *fb, int *nfb) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= tot) return;
+  const SegOutY *S = seg + c * K;
+  int total = 0, prev = -1;
+  bool good = true;
+  for (int k = 0; k < K && good; k++) {
+    const SegOutY &o = S[k];
+    if (o.empty) continue;
+    good = o.ok != 0;
+    if (good && prev >= 0)
+      good = __double_as_longlong(o.in_hi) == __double_as_longlong(S[prev].out_hi) &&
+             __double_as_longlong(o.in_lo) == __double_as_longlong(S[prev].out_lo);
+    total += o.cnt;
+    prev = k;
+  }
+  if (good) {
+    if (c < nn) counts[c] = total;
+    else excounts[c - nn] = total;
+    return;
+  }
+  fb[atomicAdd(nfb, 1)] = c;
+}
+__global__ void k_seg_fallback_y(const long long *__restrict__ fb, const int *__restrict__ nfb,
+                                 const Node *__restrict__ nodes, int nnode, int m,
+                                 const ExplicitChain *__restrict__ ex, const RepDesc *__restrict__ reps,
+                                 const QElt *__restrict__ mq, const YElt *__restrict__ my, int *counts,
+                                 int *excounts) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= *nfb) return;
+  const long long c = fb[i], nn = (long long)nnode * ((1 << m) - 1);
+  double sig;
+  int rep;
+  chain_of(nodes, m, nn, ex, c, sig, rep);
+  const RepDesc R = reps[rep];
+  const int cnt = negcount_y_q(mq + R.off, my + R.off, R.nb, dd_from(sig));
+  if (c < nn) counts[c] = cnt;
+  else excounts[c - nn] = cnt;
+}

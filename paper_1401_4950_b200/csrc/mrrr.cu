@@ -103,6 +103,7 @@ struct mrrr_ctx {
   bool rqi_chunk = true;       // chunk-major fixed passes (k_fixed_chunk) instead of lane-major (k_fixed_seg)
   bool rqi_bulk = true;        // k_fixed_chunk stores the factors by bulk copies of staged 8-row runs
   bool zw_chunk = true;        // k_zwrite_chunk (chunked products, staged tiles) instead of the per-row warp scan
+  int segy_k = 8, segy_w = 128;  // segmented y-NegCount (MRRR_SEGYK=1: unsegmented)
   long long seg_ch2 = 0;  // segmented rounds with at most this many chains run two chains per thread (slower on C2)
   long long seg_threads = 0;  // adaptive segment count: target threads per segmented round (0: off; no gain measured)
   int dev_rb = 4;             // rounds per device-driven batch
@@ -118,6 +119,7 @@ struct mrrr_ctx {
   Buf nodesK, nodesP, offsP, dS, dG, dH;  // guided bisection rounds
   Buf repoff, repcur, repcta;             // representation-grouped rounds
   Buf segout, segfb, segfbs, rnd;         // segmented NegCount; per-round device counters
+  Buf segouty, segfby;                    // segmented y-NegCount
   Buf rqst, rqrec, hand;                  // segmented RQI state, segment records, handed-over singletons
   std::vector<cudaEvent_t> rev;           // events around device-driven rounds
   Buf nodesA, nodesB, counts, ex, excounts, exmap, bnA, bnB, sing, clusA, clusB, ss, gval, valid, cseg, bnoff,
@@ -283,6 +285,24 @@ void launch_negcount(mrrr_t h, const Node *nodes, int nnode, int m, int nex, con
         nodes, nnode, m, nodesP, nP, offsP, nPc, rtol, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(),
         h->mx.as<double2>(), h->counts.as<int>(), h->excounts.as<int>(), h->dS.as<double>(), h->dG.as<double>(),
         h->dH.as<double>());
+    launch_check(h);
+    return;
+  }
+  if (Y && h->segy_k > 1 && tot > 0) {
+    // segmented y-count (kernels_guided.cuh): K segments per chain, junctions verified bit-exact
+    const int K = h->segy_k;
+    CK(h->segouty.ensure(sizeof(SegOutY) * tot * K));
+    CK(h->segfby.ensure(sizeof(long long) * tot));
+    CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
+    k_negcount_seg_y<<<nblocks_for(tot * K, 128), 128, 0, h->stream>>>(
+        nodes, nnode, m, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mq.as<QElt>(), K, h->segy_w,
+        h->segouty.as<SegOutY>());
+    k_seg_combine_y<<<nblocks_for(tot, 128), 128, 0, h->stream>>>(tot, tot - nex, K, h->segouty.as<SegOutY>(),
+                                                                  h->counts.as<int>(), h->excounts.as<int>(),
+                                                                  h->segfby.as<long long>(), h->cnt.as<int>() + C_NFB);
+    k_seg_fallback_y<<<nblocks_for(tot, 128), 128, 0, h->stream>>>(
+        h->segfby.as<long long>(), h->cnt.as<int>() + C_NFB, nodes, nnode, m, h->ex.as<ExplicitChain>(),
+        h->reps.as<RepDesc>(), h->mq.as<QElt>(), h->my.as<YElt>(), h->counts.as<int>(), h->excounts.as<int>());
     launch_check(h);
     return;
   }
@@ -1260,6 +1280,8 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_RQIBULK")) h->rqi_bulk = atoi(s) != 0;
     if (const char *s = getenv("MRRR_SEGTHREADS")) h->seg_threads = atoll(s);
     if (const char *s = getenv("MRRR_SEGCH2")) h->seg_ch2 = atoll(s);
+    if (const char *s = getenv("MRRR_SEGYK")) h->segy_k = std::max(1, std::min(64, atoi(s)));
+    if (const char *s = getenv("MRRR_SEGYW")) h->segy_w = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_BUD_FULL")) h->bud_full = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_BUD_TUBE")) h->bud_tube = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;

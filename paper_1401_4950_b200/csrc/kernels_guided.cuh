@@ -524,3 +524,142 @@ __global__ void k_seg_fallback_y(const long long *__restrict__ fb, const int *__
   if (c < nn) counts[c] = cnt;
   else excounts[c - nn] = cnt;
 }
+
+// ---------------------------------------------------------------------------
+// Segmented x-NegCount for launches whose chains evaluate many representations (child bisection):
+// thread (segment k, chain c), per-thread loads with PF rows in flight, the step of negcount_x_fast
+// (division fast path, sticky range test).  k_seg_combine_xg accepts a chain iff every junction state
+// is bit-identical to its predecessor's exit; the rest are recounted whole by negcount_x_fast (which
+// reruns the careful IEEE chain if its own range test fails), so counts equal negcount_x's.
+// ---------------------------------------------------------------------------
+struct SegOutX {
+  double in, out;
+  int cnt, ok, empty, pad;
+};
+__global__ void __launch_bounds__(128) k_negcount_seg_xg(const Node *__restrict__ nodes, int nnode, int m,
+                                                         const ExplicitChain *__restrict__ ex, int nex,
+                                                         const RepDesc *__restrict__ reps,
+                                                         const double2 *__restrict__ mx, int K, int Wu,
+                                                         SegOutX *seg) {
+  constexpr int PF = 8;
+  const long long nn = (long long)nnode * ((1 << m) - 1), tot = nn + nex;
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= tot * K) return;
+  const int k = (int)(g / tot);
+  const long long c = g % tot;
+  double sig;
+  int rep;
+  chain_of(nodes, m, nn, ex, c, sig, rep);
+  const RepDesc R = reps[rep];
+  const int nb = R.nb, steps = nb - 1;
+  SegOutX *o = seg + c * K + k;
+  int bk, ek, w0;
+  if (steps >= 2 * K * Wu) {
+    const int L = (steps + K - 1) / K;
+    bk = min(k * L, steps);
+    ek = min(bk + L, steps);
+    w0 = (k == 0) ? 0 : max(bk - Wu, 0);
+  } else {
+    if (k > 0) {
+      o->empty = 1;
+      o->ok = 1;
+      return;
+    }
+    bk = 0;
+    ek = steps;
+    w0 = 0;
+  }
+  const double2 *M = mx + R.off;
+  double s = -sig, s_in = -sig;
+  int cnt = 0;
+  bool ok = true;
+  double2 ring[PF];
+#pragma unroll
+  for (int u = 0; u < PF; u++) ring[u] = __ldg(M + min(w0 + u, nb - 1));
+  auto step = [&](int i, double2 mm) {
+    if (i == bk) s_in = s;
+    const double dp = __dadd_rn(mm.x, s);
+    const double q = div_fast_nocheck(s, dp);
+    ok &= div_range_ok(s, dp, q);
+    s = __dsub_rn(__dmul_rn(q, mm.y), sig);
+    if (i >= bk) cnt += (int)((unsigned)__double2hiint(dp) >> 31);
+  };
+  int i = w0;
+  for (; i + PF <= ek; i += PF) {
+#pragma unroll
+    for (int u = 0; u < PF; u++) {
+      const double2 mm = ring[u];
+      ring[u] = __ldg(M + min(i + u + PF, nb - 1));
+      step(i + u, mm);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < PF; u++)
+    if (i + u < ek) step(i + u, ring[u]);
+  if (ek == steps) cnt += sbx(__dadd_rn(__ldg(M + nb - 1).x, s));
+  o->in = s_in;
+  o->out = s;
+  o->cnt = cnt;
+  o->ok = (ok && !isnan(s)) ? 1 : 0;
+  o->empty = 0;
+}
+struct FbX {
+  long long c;
+  double s;   // last exact state: entering segment k's first row
+  int k, cnt;  // first unverified segment, count of the verified rows before it
+};
+__global__ void k_seg_combine_xg(long long tot, long long nn, int K, const SegOutX *__restrict__ seg, int *counts,
+                                 int *excounts, FbX *fb, int *nfb) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= tot) return;
+  const SegOutX *S = seg + c * K;
+  int total = 0, prev = -1, k = 0;
+  for (; k < K; k++) {
+    const SegOutX &o = S[k];
+    if (o.empty) continue;
+    if (!o.ok) break;
+    if (prev >= 0 && __double_as_longlong(o.in) != __double_as_longlong(S[prev].out)) break;
+    total += o.cnt;
+    prev = k;
+  }
+  if (k == K) {
+    if (c < nn) counts[c] = total;
+    else excounts[c - nn] = total;
+    return;
+  }
+  FbX f;
+  f.c = c;
+  f.s = (prev >= 0) ? S[prev].out : S[0].in;  // S[0].in = -sigma (exact start)
+  f.k = (prev >= 0) ? k : 0;
+  f.cnt = (prev >= 0) ? total : 0;
+  fb[atomicAdd(nfb, 1)] = f;
+}
+// careful (IEEE) tail from the first unverified segment's first row with the last exact state
+__global__ void k_seg_fallback_xg(const FbX *__restrict__ fb, const int *__restrict__ nfb,
+                                  const Node *__restrict__ nodes, int nnode, int m,
+                                  const ExplicitChain *__restrict__ ex, const RepDesc *__restrict__ reps,
+                                  const double2 *__restrict__ mx, int K, int Wu, int *counts, int *excounts) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= *nfb) return;
+  const FbX f = fb[i];
+  const long long nn = (long long)nnode * ((1 << m) - 1);
+  double sig;
+  int rep;
+  chain_of(nodes, m, nn, ex, f.c, sig, rep);
+  const RepDesc R = reps[rep];
+  const double2 *M = mx + R.off;
+  const int nb = R.nb, steps = nb - 1;
+  const int L = (steps >= 2 * K * Wu) ? (steps + K - 1) / K : steps;
+  double s = f.s;
+  int cnt = f.cnt;
+  for (int r = min(f.k * L, steps); r < steps; r++) {
+    const double2 mm = __ldg(M + r);
+    const double dp = __dadd_rn(mm.x, s);
+    const double q = (isinf(s) && isinf(dp)) ? 1.0 : __ddiv_rn(s, dp);
+    s = __dsub_rn(__dmul_rn(q, mm.y), sig);
+    cnt += sbx(dp);
+  }
+  cnt += sbx(__dadd_rn(__ldg(M + nb - 1).x, s));
+  if (f.c < nn) counts[f.c] = cnt;
+  else excounts[f.c - nn] = cnt;
+}

@@ -104,6 +104,7 @@ struct mrrr_ctx {
   bool rqi_bulk = true;        // k_fixed_chunk stores the factors by bulk copies of staged 8-row runs
   bool zw_chunk = true;        // k_zwrite_chunk (chunked products, staged tiles) instead of the per-row warp scan
   int segy_k = 8, segy_w = 128;  // segmented y-NegCount (MRRR_SEGYK=1: unsegmented)
+  int segx_k = 1, segx_w = 128;  // segmented many-representation x-NegCount (MRRR_SEGXK=8: on; no gain on C3/C4, slower on C1)
   long long seg_ch2 = 0;  // segmented rounds with at most this many chains run two chains per thread (slower on C2)
   long long seg_threads = 0;  // adaptive segment count: target threads per segmented round (0: off; no gain measured)
   int dev_rb = 4;             // rounds per device-driven batch
@@ -119,7 +120,7 @@ struct mrrr_ctx {
   Buf nodesK, nodesP, offsP, dS, dG, dH;  // guided bisection rounds
   Buf repoff, repcur, repcta;             // representation-grouped rounds
   Buf segout, segfb, segfbs, rnd;         // segmented NegCount; per-round device counters
-  Buf segouty, segfby;                    // segmented y-NegCount
+  Buf segouty, segfby, segoutx;           // segmented y-NegCount / many-representation x-NegCount
   Buf rqst, rqrec, hand;                  // segmented RQI state, segment records, handed-over singletons
   std::vector<cudaEvent_t> rev;           // events around device-driven rounds
   Buf nodesA, nodesB, counts, ex, excounts, exmap, bnA, bnB, sing, clusA, clusB, ss, gval, valid, cseg, bnoff,
@@ -280,6 +281,24 @@ template <bool Y>
 void launch_negcount(mrrr_t h, const Node *nodes, int nnode, int m, int nex, const Node *nodesP = nullptr,
                      int nP = 0, const int *offsP = nullptr, int nPc = 0, double rtol = 0.0) {
   long long tot = (long long)nnode * ((1LL << m) - 1) + nPc + nex;
+  if (!Y && nPc == 0 && h->segx_k > 1 && tot > 0) {
+    // segmented x-count over many representations (kernels_guided.cuh), junctions verified bit-exact
+    const int K = h->segx_k;
+    CK(h->segoutx.ensure(sizeof(SegOutX) * tot * K));
+    CK(h->segfby.ensure(sizeof(FbX) * tot));
+    CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
+    k_negcount_seg_xg<<<nblocks_for(tot * K, 128), 128, 0, h->stream>>>(
+        nodes, nnode, m, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, h->segx_w,
+        h->segoutx.as<SegOutX>());
+    k_seg_combine_xg<<<nblocks_for(tot, 128), 128, 0, h->stream>>>(tot, tot - nex, K, h->segoutx.as<SegOutX>(),
+                                                                   h->counts.as<int>(), h->excounts.as<int>(),
+                                                                   h->segfby.as<FbX>(), h->cnt.as<int>() + C_NFB);
+    k_seg_fallback_xg<<<nblocks_for(tot, 128), 128, 0, h->stream>>>(
+        h->segfby.as<FbX>(), h->cnt.as<int>() + C_NFB, nodes, nnode, m, h->ex.as<ExplicitChain>(),
+        h->reps.as<RepDesc>(), h->mx.as<double2>(), K, h->segx_w, h->counts.as<int>(), h->excounts.as<int>());
+    launch_check(h);
+    return;
+  }
   if (!Y && h->neg_tma) {
     k_negcount_tma<<<nblocks_for(tot, 128), 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
         nodes, nnode, m, nodesP, nP, offsP, nPc, rtol, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(),
@@ -1282,6 +1301,8 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_SEGCH2")) h->seg_ch2 = atoll(s);
     if (const char *s = getenv("MRRR_SEGYK")) h->segy_k = std::max(1, std::min(64, atoi(s)));
     if (const char *s = getenv("MRRR_SEGYW")) h->segy_w = std::max(1, atoi(s));
+    if (const char *s = getenv("MRRR_SEGXK")) h->segx_k = std::max(1, std::min(64, atoi(s)));
+    if (const char *s = getenv("MRRR_SEGXW")) h->segx_w = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_BUD_FULL")) h->bud_full = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_BUD_TUBE")) h->bud_tube = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;

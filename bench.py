@@ -258,7 +258,7 @@ def main():
     # roofline of the dominant kernel family: algorithmic FP64 flops per launch / CUDA-event launch time
     pk = peaks()
     fp = pk.get("fp64") or {}
-    roof, roof_other = None, None
+    roof, roof_other, roof_step = None, None, None
     if fp:
         from paper_1401_4950_b200 import flops as fl
         wdiv = fp.get("w_div", 13.0)
@@ -288,6 +288,18 @@ def main():
                         "launch_ms": launch_ms, "flops_per_launch": f})
         roof = out[0] if out else None
         roof_other = out[1:] if len(out) > 1 else None
+        # whole-solve roofline as the north_star defines it: the slower of (counted FP64 operations, divisions
+        # weighted by their issue cost, at peak) and (the Z bytes at HBM bandwidth), against the step time
+        ftot = fl.negcount_flops(stats, n, wdiv) + fl.rqi_flops(stats, n, wdiv)
+        t_fp = ftot / (peak * 1e12)
+        zb = 8.0 * k * n
+        t_hbm = zb / (pk.get("hbm_gbs", 6550.0) * 1e9)
+        t_bound = max(t_fp, t_hbm)
+        roof_step = {"bound": "alu" if t_fp >= t_hbm else "hbm", "flops": ftot, "z_bytes": zb,
+                     "t_fp64_ms": t_fp * 1e3, "t_hbm_ms": t_hbm * 1e3, "ms_per_step": ms_max,
+                     "frac": t_bound * 1e3 / ms_max,
+                     "note": "whole solve: algorithmic FP64 slots (x-NegCount shared-tree nodes, RQI passes) vs "
+                             "Z write bytes; frac = bound time / measured step time"}
 
     e2e = None
     if world == 1 and not args.no_e2e:
@@ -320,7 +332,7 @@ def main():
                            "parallelism": f"index shards x{world}" if world > 1 else "single GPU",
                            "l2": "flushed between steps (256 MiB write, outside the events)"},
                 "gpu_launches": int(launches_per_step) * args.steps,
-                "phases_ms": tphase, "stats": stats, "roofline": roof, "roofline_other": roof_other,
+                "phases_ms": tphase, "stats": stats, "roofline": roof, "roofline_other": roof_other, "roofline_step": roof_step,
                 "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

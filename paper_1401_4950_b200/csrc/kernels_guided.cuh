@@ -246,9 +246,11 @@ __global__ void __launch_bounds__(128) k_negcount_seg(const Node *__restrict__ n
   }
   const long long nn = (long long)nnode * ((1 << m) - 1);
   const long long tot = nn + nex;
-  const long long cb = (long long)blockIdx.x * blockDim.x * CH;
+  // 1-D grid, segment index fastest: the live CTAs are the first ones dispatched (device-driven rounds
+  // launch a grid sized for the largest possible round; its idle tail exits without delaying them)
+  const long long cb = (long long)(blockIdx.x / K) * blockDim.x * CH;
   if (cb >= tot) return;  // whole CTA idle (uniform exit)
-  const int k = blockIdx.y;
+  const int k = blockIdx.x % K;
   double sig[CH];
   bool act[CH];
   int rep = 0;

@@ -75,7 +75,7 @@ inline unsigned nblocks_for(long long n, int bs) { return (unsigned)std::max<lon
 
 // counters block on the device: reset/readback in one copy
 enum { C_NNEXT = 0, C_NEX, C_NPEND, C_NREADY, C_NSING, C_NCLUS, C_NNXT, C_NDONE, C_NK, C_NP, C_NPC, C_NFB,
-       C_NCOUNTERS = 16 };
+       C_NMULTI, C_NCOUNTERS = 16 };
 
 }  // namespace
 
@@ -107,7 +107,8 @@ struct mrrr_ctx {
   int segx_k = 1, segx_w = 128;  // segmented many-representation x-NegCount (MRRR_SEGXK=8: on; no gain on C3/C4, slower on C1)
   long long seg_ch2 = 0;  // segmented rounds with at most this many chains run two chains per thread (slower on C2)
   long long seg_threads = 0;  // adaptive segment count: target threads per segmented round (0: off; no gain measured)
-  int dev_rb = 4;             // rounds per device-driven batch
+  bool dev_stable = true;      // device-driven rounds once every node holds one index (exact grids)
+  int dev_rb = 16;            // rounds per device-driven batch
   bool dev_rounds = false;     // segmented rounds enqueued in batches on device-side counters (MRRR_DEVROUNDS=1;
                                // slower on C2: the oversized early-exit grids cost more than the saved syncs)
   int max_nodes = 0;           // bound on live bisection nodes (indices in the computed set)  // tube point budgets: no estimate (4 full levels) / with estimate
@@ -425,10 +426,15 @@ __global__ void k_set_int(int *p, int v) { *p = v; }
 // update writes nn[r+1], so batches of rounds are enqueued without a host round trip (kernels of empty
 // rounds exit at once); the host checks the count once per batch.
 void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int maxnodes, double *out_lo,
-                       double *out_hi, double rtol) {
+                       double *out_hi, double rtol, int mcap = 0) {
+  // mcap > 0 (stable phase: every node holds one wanted index, so the node count can only shrink): the
+  // k-section depth stays at most mcap, so every round has at most nnode * (2^mcap - 1) chains and the
+  // grids are sized exactly (depth is free: the dyadic grid makes any schedule bit-identical)
   const int K = h->seg_k, L = (nb - 1 + K - 1) / K;
   const int MAXR = 256, RB = h->dev_rb;
-  const long long maxch = std::max<long long>(h->target_chains, maxnodes) + 128;
+  const int mmax = mcap > 0 ? mcap : h->mmax;
+  const long long maxch = mcap > 0 ? (long long)nnode * ((1LL << mcap) - 1)
+                                   : std::max<long long>(h->target_chains, maxnodes) + 128;
   CK(h->rnd.ensure(sizeof(int) * 2 * (MAXR + 2)));
   CK(h->counts.ensure(sizeof(int) * maxch));
   CK(h->segout.ensure(sizeof(SegOut) * maxch * K));
@@ -451,24 +457,25 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
     // grids for a batch: the node count can at most double per round (a node splits in two), and a round
     // has at most max(target, nodes) chains; CTAs beyond the live count exit at once
     long long bound = known;
-    for (int b = 0; b < RB; b++) bound = std::min<long long>(2 * bound, maxnodes);
-    const long long chmax = std::min<long long>(maxch, std::max<long long>(bound, h->target_chains) + 128);
-    const dim3 gseg((unsigned)(chmax / 128 + 1), (unsigned)K);
+    if (mcap <= 0)
+      for (int b = 0; b < RB; b++) bound = std::min<long long>(2 * bound, maxnodes);
+    const long long chmax = mcap > 0 ? maxch : std::min<long long>(maxch, std::max<long long>(bound, h->target_chains) + 128);
+    const unsigned gseg = (unsigned)((chmax / 128 + 1) * K);
     const unsigned g1 = (unsigned)(chmax / 128 + 1), g2 = (unsigned)(2 * chmax / 128 + 1);
     for (int b = 0; b < RB && r < MAXR; b++, r++) {
       Node *in = (r & 1) ? nxt : cur, *out = (r & 1) ? cur : nxt;
       CK(cudaEventRecord(h->rev[2 * r], h->stream));
       k_negcount_seg<1><<<gseg, 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
           in, 0, 0, nullptr, 0, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L, h->seg_w, h->segout.as<SegOut>(),
-          nn + r, h->mmax, h->target_chains);
+          nn + r, mmax, h->target_chains);
       CK(cudaEventRecord(h->rev[2 * r + 1], h->stream));
       k_seg_combine<<<g1, 128, 0, h->stream>>>(0, 0, K, h->segout.as<SegOut>(), h->counts.as<int>(), nullptr,
-                                               h->segfb.as<int4>(), nfb + r, h->segfbs.as<double>(), nn + r, h->mmax,
+                                               h->segfb.as<int4>(), nfb + r, h->segfbs.as<double>(), nn + r, mmax,
                                                h->target_chains, negx);
       k_seg_fallback<<<g1, 128, 0, h->stream>>>(h->segfb.as<int4>(), nfb + r, h->segfbs.as<double>(), in, 0, 0,
                                                 nullptr, h->reps.as<RepDesc>(), h->mx.as<double2>(), L,
-                                                h->counts.as<int>(), nullptr, nn + r, h->mmax, h->target_chains);
-      k_bisect_update_dev<<<g2, 128, 0, h->stream>>>(in, nn + r, h->mmax, h->target_chains, h->counts.as<int>(), out,
+                                                h->counts.as<int>(), nullptr, nn + r, mmax, h->target_chains);
+      k_bisect_update_dev<<<g2, 128, 0, h->stream>>>(in, nn + r, mmax, h->target_chains, h->counts.as<int>(), out,
                                                      nn + r + 1, out_lo, out_hi, rtol, alg);
       launch_check(h);
       h->host_launches += 3;
@@ -594,7 +601,7 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
       CK(h->segfb.ensure(sizeof(int4) * tot));
       CK(h->segfbs.ensure(sizeof(double) * tot));
       const int CH = (tot <= h->seg_ch2) ? 2 : 1;  // few chains: two per thread (ILP)
-      dim3 grid((unsigned)((tot + 128 * CH - 1) / (128 * CH)), (unsigned)K);
+      const unsigned grid = (unsigned)((tot + 128 * CH - 1) / (128 * CH) * K);
       if (CH == 2)
         k_negcount_seg<2><<<grid, 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
             cur, nnode, m, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L,
@@ -626,7 +633,8 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
     }
     k_bisect_update<<<nblocks_for((long long)nnode << m, 128), 128, 0, h->stream>>>(
         cur, nnode, m, h->counts.as<int>(), nxt, h->cnt.as<int>() + C_NNEXT, out_lo, out_hi, rtol,
-        (unsigned long long *)(h->stats.as<long long>() + (Y ? ST_NEGY_ALG : ST_NEGX_ALG)));
+        (unsigned long long *)(h->stats.as<long long>() + (Y ? ST_NEGY_ALG : ST_NEGX_ALG)),
+        h->cnt.as<int>() + C_NMULTI);
     launch_check(h);
     read_counters(h);
     h->host_rounds++;
@@ -643,6 +651,13 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
     first = false;
     if (!Y && seg_on && h->dev_rounds && nnode > 0) {
       run_rounds_device(h, cur, nxt, nnode, single_nb, std::max(nnode, h->max_nodes), out_lo, out_hi, rtol);
+      return;
+    }
+    if (!Y && seg_on && h->dev_stable && nnode > 0 && h->h_cnt[C_NMULTI] == 0) {
+      // stable phase: every node holds one wanted index; the remaining rounds run without host round trips
+      int mcap = 1;
+      while (mcap < h->mmax && (long long)nnode * ((1LL << (mcap + 1)) - 1) <= target) mcap++;
+      run_rounds_device(h, cur, nxt, nnode, single_nb, nnode, out_lo, out_hi, rtol, mcap);
       return;
     }
   }
@@ -1289,6 +1304,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_SEGK")) h->seg_k = std::max(1, std::min(64, atoi(s)));
     if (const char *s = getenv("MRRR_SEGW")) h->seg_w = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_DEVROUNDS")) h->dev_rounds = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_DEVSTABLE")) h->dev_stable = atoi(s) != 0;
     if (const char *s = getenv("MRRR_DEVRB")) h->dev_rb = std::max(1, std::min(64, atoi(s)));
     if (const char *s = getenv("MRRR_RQISEG")) h->rqi_seg = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQISEGK")) h->rqi_segk = std::max(1, std::min(64, atoi(s)));

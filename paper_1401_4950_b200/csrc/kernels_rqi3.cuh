@@ -194,20 +194,29 @@ __global__ void __launch_bounds__(256) k_twist_pick(const Singleton *__restrict_
   sh_best[grp][lane] = best;
   sh_bk[grp][lane] = bk;
   __syncthreads();
-  if (grp == 0 && act) {
-    for (int g2 = 1; g2 < 8; g2++) {
-      const double ob = sh_best[g2][lane];
-      const int ok_ = sh_bk[g2][lane];
-      if (ok_ >= 0 && (bk < 0 || ob < best || (ob == best && ok_ < bk))) { best = ob; bk = ok_; }
+  if (grp == 0) {
+    unsigned ho = 0, rows = 0;
+    if (act) {
+      for (int g2 = 1; g2 < 8; g2++) {
+        const double ob = sh_best[g2][lane];
+        const int ok_ = sh_bk[g2][lane];
+        if (ok_ >= 0 && (bk < 0 || ob < best || (ob == best && ok_ < bk))) { best = ob; bk = ok_; }
+      }
+      // the x-arithmetic argmin must resolve gamma: |gamma_r| well above the fp64 rounding of its two terms
+      const double sc = (bk >= 0) ? fmax(fabs(TF[(long long)bk * S_ + i]), fabs(TB[(long long)bk * S_ + i])) : 0.0;
+      if (bk < 0 || !(best > 0x1p-46 * sc)) {
+        st[i].status = 2;
+        ho = 1;
+      } else {
+        st[i].r = bk;
+        rows = (unsigned)(2 * (nb - 1));
+      }
     }
-    // the x-arithmetic argmin must resolve gamma: |gamma_r| well above the fp64 rounding of its two terms
-    const double sc = (bk >= 0) ? fmax(fabs(TF[(long long)bk * S_ + i]), fabs(TB[(long long)bk * S_ + i])) : 0.0;
-    if (bk < 0 || !(best > 0x1p-46 * sc)) {
-      st[i].status = 2;
-      atomicAdd((unsigned long long *)&stats[ST_HO_TWIST], 1ull);
-    } else {
-      st[i].r = bk;
-      atomicAdd((unsigned long long *)&stats[ST_TWIST_ROWS], (unsigned long long)(2 * (nb - 1)));
+    ho = __reduce_add_sync(0xffffffffu, ho);
+    rows = __reduce_add_sync(0xffffffffu, rows);
+    if (lane == 0) {
+      if (ho) atomicAdd((unsigned long long *)&stats[ST_HO_TWIST], (unsigned long long)ho);
+      if (rows) atomicAdd((unsigned long long *)&stats[ST_TWIST_ROWS], (unsigned long long)rows);
     }
   }
 }
@@ -424,11 +433,14 @@ __global__ void __launch_bounds__(128) k_fixed_chunk(const Singleton *__restrict
 }
 
 // thread per singleton: junctions, gamma_r, ||z||^2, inertia, and the stask decision
-__global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
-                             RqiState *st, int K, int bal, int chunk, const SegRec *__restrict__ rec, double *W, ZMeta *zmeta,
-                             int *diag_depth, double *fin_lo, double *fin_hi, long long *stats, int *nactive) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= ns) return;
+// per-thread counter increments, summed per warp before one atomic each
+struct FsInc {
+  unsigned nact, wide, hofixed, horqc, iters, light, qd, zw, dmax;
+};
+__device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restrict__ sg,
+                                                const RepDesc *__restrict__ reps, RqiState *st, int K, int bal,
+                                                int chunk, const SegRec *__restrict__ rec, double *W, ZMeta *zmeta,
+                                                int *diag_depth, double *fin_lo, double *fin_hi, FsInc &inc) {
   RqiState S = st[i];
   if (S.status != 0) return;
   const Singleton s = sg[i];
@@ -468,12 +480,12 @@ __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const Rep
   if (!good) {
     if (!S.wide) {  // a warm-up too short for this singleton: repeat the pass with an 8x longer one
       st[i].wide = 1;
-      atomicAdd(nactive, 1);
-      atomicAdd((unsigned long long *)&stats[ST_SEG_WIDE], 1ull);
+      inc.nact++;
+      inc.wide++;
       return;
     }
     st[i].status = 2;
-    atomicAdd((unsigned long long *)&stats[ST_HO_FIXED], 1ull);
+    inc.hofixed++;
     return;
   }
   const dd gamma = (r == nb - 1) ? dr : dd_sub(dr, tr);
@@ -481,9 +493,9 @@ __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const Rep
   const dd zz = dd_add_d(dd_add(Ssum, Tsum), 1.0);
   dd lam = dd_make(S.lam_hi, S.lam_lo), blo = dd_make(S.blo_hi, S.blo_lo), bhi = dd_make(S.bhi_hi, S.bhi_lo);
   S.it++;
-  atomicAdd((unsigned long long *)&stats[ST_RQI_ITERS], 1ull);
-  atomicAdd((unsigned long long *)&stats[ST_GETVEC], 1ull);
-  atomicAdd((unsigned long long *)&stats[S.it == 1 ? ST_QD_LIGHT : ST_QD_STEPS], (unsigned long long)(nb - 1));
+  inc.iters++;
+  if (S.it == 1) inc.light += (unsigned)(nb - 1);
+  else inc.qd += (unsigned)(nb - 1);
   bool accepted = false, handover = false;
   if (!isfinite(zz.hi) || zz.hi == 0.0) {
     handover = true;
@@ -495,7 +507,7 @@ __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const Rep
     if (dd_lt(tol2, dd_from(__dmul_rn(0x1p-100, Rp.spdiam)))) tol2 = dd_from(__dmul_rn(0x1p-100, Rp.spdiam));
     if (resid.hi <= S.thr1 || dd_lt(dd_abs(rqc), tol2)) {
       if (S.it == 1) {  // accepted on the RQC-only pass: repeat it at the same lambda with the factors stored
-        atomicAdd(nactive, 1);
+        inc.nact++;
         st[i] = S;
         return;
       }
@@ -520,19 +532,48 @@ __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const Rep
       fin_lo[s.col] = s.lo;
       fin_hi[s.col] = s.hi;
     }
-    atomicAdd((unsigned long long *)&stats[ST_ZW_STEPS], (unsigned long long)(nb - 1));
-    atomicMax((unsigned long long *)&stats[ST_DMAX], (unsigned long long)Rp.depth);
+    inc.zw += (unsigned)(nb - 1);
+    inc.dmax = max(inc.dmax, (unsigned)Rp.depth);
     S.status = 1;
   } else if (handover) {
     S.status = 2;
-    atomicAdd((unsigned long long *)&stats[ST_HO_RQC], 1ull);
+    inc.horqc++;
   } else {
-    atomicAdd(nactive, 1);
+    inc.nact++;
   }
   S.lam_hi = lam.hi; S.lam_lo = lam.lo;
   S.blo_hi = blo.hi; S.blo_lo = blo.lo;
   S.bhi_hi = bhi.hi; S.bhi_lo = bhi.lo;
   st[i] = S;
+}
+
+__global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
+                             RqiState *st, int K, int bal, int chunk, const SegRec *__restrict__ rec, double *W,
+                             ZMeta *zmeta, int *diag_depth, double *fin_lo, double *fin_hi, long long *stats,
+                             int *nactive) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  FsInc inc = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (i < ns) fixed_step_body(i, sg, reps, st, K, bal, chunk, rec, W, zmeta, diag_depth, fin_lo, fin_hi, inc);
+  const unsigned fm = 0xffffffffu;
+  const unsigned nact = __reduce_add_sync(fm, inc.nact), wide = __reduce_add_sync(fm, inc.wide);
+  const unsigned hof = __reduce_add_sync(fm, inc.hofixed), hor = __reduce_add_sync(fm, inc.horqc);
+  const unsigned it = __reduce_add_sync(fm, inc.iters), li = __reduce_add_sync(fm, inc.light);
+  const unsigned qd = __reduce_add_sync(fm, inc.qd), zw = __reduce_add_sync(fm, inc.zw);
+  const unsigned dm = __reduce_max_sync(fm, inc.dmax);
+  if ((threadIdx.x & 31) == 0) {
+    if (nact) atomicAdd(nactive, (int)nact);
+    if (wide) atomicAdd((unsigned long long *)&stats[ST_SEG_WIDE], (unsigned long long)wide);
+    if (hof) atomicAdd((unsigned long long *)&stats[ST_HO_FIXED], (unsigned long long)hof);
+    if (hor) atomicAdd((unsigned long long *)&stats[ST_HO_RQC], (unsigned long long)hor);
+    if (it) {
+      atomicAdd((unsigned long long *)&stats[ST_RQI_ITERS], (unsigned long long)it);
+      atomicAdd((unsigned long long *)&stats[ST_GETVEC], (unsigned long long)it);
+    }
+    if (li) atomicAdd((unsigned long long *)&stats[ST_QD_LIGHT], (unsigned long long)li);
+    if (qd) atomicAdd((unsigned long long *)&stats[ST_QD_STEPS], (unsigned long long)qd);
+    if (zw) atomicAdd((unsigned long long *)&stats[ST_ZW_STEPS], (unsigned long long)zw);
+    if (dm) atomicMax((unsigned long long *)&stats[ST_DMAX], (unsigned long long)dm);
+  }
 }
 
 // singletons handed over (status != 1) for the two-lane kernel k_rqi2

@@ -367,12 +367,28 @@ __global__ void k_seg_combine(long long tot, long long nn, int K, const SegOut *
   const SegOut *S = seg + c * K;
   int total = 0, k = 0;
   double s_exact = S[0].s_in;  // -sigma
-  for (; k < K; k++) {
-    const SegOut o = S[k];
-    if (!o.ok) break;
-    if (k > 0 && __double_as_longlong(o.s_in) != __double_as_longlong(s_exact)) break;
-    total += o.cnt;
-    s_exact = o.s_out;
+  if (K == 8) {  // the usual segment count: all eight records loaded before the junction walk
+    SegOut o[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) o[u] = S[u];
+    bool run = true;
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      run = run && o[u].ok && (u == 0 || __double_as_longlong(o[u].s_in) == __double_as_longlong(s_exact));
+      if (run) {
+        total += o[u].cnt;
+        s_exact = o[u].s_out;
+        k = u + 1;
+      }
+    }
+  } else {
+    for (; k < K; k++) {
+      const SegOut o = S[k];
+      if (!o.ok) break;
+      if (k > 0 && __double_as_longlong(o.s_in) != __double_as_longlong(s_exact)) break;
+      total += o.cnt;
+      s_exact = o.s_out;
+    }
   }
   if (k == K) {
     if (c < nn) counts[c] = total;

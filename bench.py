@@ -190,9 +190,16 @@ def main():
     import torch.distributed as dist
     import paper_1401_4950_b200 as mrrr
 
+    # MRRR_BENCH_DIST=gloo: functional check of the N > 1 path with ranks sharing the visible GPUs (the
+    # collectives then run on host copies; no performance meaning)
+    backend = os.environ.get("MRRR_BENCH_DIST", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend == "gloo" else local
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = mi.CONFIGS[args.workload]
     d_np, e_np = cfg.matrix()
     n, k = cfg.n, cfg.k
@@ -218,7 +225,7 @@ def main():
             else:
                 jlo, jhi, Wl, Zl = solver.eig_shard(d, e, sl, su)
                 # eigenvalue list all-gather over NCCL: the only collective
-                pd.allgather_eigenvalues(Wl, jlo, jhi, cfg.il, cfg.iu)
+                pd.allgather_eigenvalues(Wl if backend != "gloo" else Wl.cpu(), jlo, jhi, cfg.il, cfg.iu)
 
     for _ in range(args.warmup):
         step()
@@ -249,6 +256,8 @@ def main():
     ms = float(np.sum(times)) / args.steps
     t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
+        if backend == "gloo":
+            t_local = t_local.cpu()
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     ms_max = float(t_local.item())
     value = k * n / (ms_max * 1e-3)

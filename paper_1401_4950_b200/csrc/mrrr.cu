@@ -99,6 +99,7 @@ struct mrrr_ctx {
   int seg_k = 8, seg_w = 128;  // segmented root NegCount: segments per chain, warm-up rows (k_negcount_seg)
   bool rqi_seg = true;         // segmented RQI passes (kernels_rqi3.cuh); MRRR_RQISEG=0: the two-lane kernel only
   int rqi_segk = 8, rqi_segw = 192;
+  long long rqi_threads = 131072;  // adaptive RQI segment count target (threads per segmented pass)
   bool rqi_bal = true;         // split a singleton's 2K segments between its lanes by length
   bool rqi_chunk = true;       // chunk-major fixed passes (k_fixed_chunk) instead of lane-major (k_fixed_seg)
   bool rqi_bulk = true;        // k_fixed_chunk stores the factors by bulk copies of staged 8-row runs
@@ -743,7 +744,11 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
       int nold = (int)nb;
       if (h->rqi_seg && allow_seg) {
         // segmented passes (kernels_rqi3.cuh); singletons they hand over go through k_rqi2 below
-        const int K = h->rqi_segk, Wu = h->rqi_segw;
+        // segments per lane: at least rqi_segk; more when the batch has few singletons (a rank's shard),
+        // so that about rqi_threads threads run, as long as a chunk stays longer than the warm-up
+        int K = h->rqi_segk;
+        const int Wu = h->rqi_segw;
+        while (2 * K <= 32 && (long long)nb * 2 * (2 * K) <= h->rqi_threads && (nbmax - 1) >= 2 * (2 * K) * Wu) K *= 2;
         CK(h->rqst.ensure(sizeof(RqiState) * stride));
         CK(h->rqrec.ensure(sizeof(SegRec) * stride * 4 * K));  // chunk layout: 2K chunks x 2 lanes
         CK(h->hand.ensure(sizeof(Singleton) * stride));
@@ -1313,6 +1318,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_ZWCHUNK")) h->zw_chunk = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQICHUNK")) h->rqi_chunk = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQIBULK")) h->rqi_bulk = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_RQITHREADS")) h->rqi_threads = atoll(s);
     if (const char *s = getenv("MRRR_SEGTHREADS")) h->seg_threads = atoll(s);
     if (const char *s = getenv("MRRR_SEGCH2")) h->seg_ch2 = atoll(s);
     if (const char *s = getenv("MRRR_SEGYK")) h->segy_k = std::max(1, std::min(64, atoi(s)));

@@ -1,5 +1,10 @@
 O=gpurun_out; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || { echo BUILD FAILED; exit 1; }
-timeout 1500 python -m pytest tests -m gpu -x -q -k "schedules or parity or selftest" > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 $O/pytest_gpu.log
-timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 5 --warmup 2 --workload C2 | python scripts/bench_summary.py C2
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_C2.csv python scripts/profile_solve.py C2 2 > /dev/null 2>&1; python scripts/launch_summary.py $O/launches_C2.csv 2>/dev/null | grep -E "combine|launches,"
+for v in 0 131072; do
+MRRR_RQITHREADS=$v timeout 300 python scripts/shard_time.py C2 8 3 2>&1 | tail -1 | sed "s/^/RQITHREADS=$v /"
+MRRR_RQITHREADS=$v timeout 300 python scripts/shard_time.py C2 2 3 2>&1 | tail -1 | sed "s/^/RQITHREADS=$v /"
+MRRR_RQITHREADS=$v timeout 600 python scripts/shard_time.py C5a 8 1 2>&1 | tail -1 | sed "s/^/RQITHREADS=$v /"
+done
+for st in 262144 524288; do MRRR_SEGTHREADS=$st timeout 600 python scripts/shard_time.py C5a 8 1 2>&1 | tail -1 | sed "s/^/SEGTHREADS=$st /"; done
+timeout 300 python scripts/shard_time.py C5a 8 1 2>&1 | head -3
+timeout 1500 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 $O/pytest_gpu.log

@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(128) k_negcount_seg(const Node *__restrict__ n
     int kk = 0;
     // warm-up rows (before bk): no counting
     const int nw = max(0, min(len, bk - row0));
+#pragma unroll 4
     for (; kk < nw; kk++) {
       const double2 mm = T[kk];
 #pragma unroll
@@ -314,7 +315,7 @@ __global__ void __launch_bounds__(128) k_negcount_seg(const Node *__restrict__ n
 #pragma unroll
       for (int j = 0; j < CH; j++) s_in[j] = s[j];
     }
-#pragma unroll 4
+#pragma unroll 8
     for (; kk < len; kk++) {
       const double2 mm = T[kk];
 #pragma unroll

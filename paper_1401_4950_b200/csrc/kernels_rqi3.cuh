@@ -221,6 +221,159 @@ __global__ void __launch_bounds__(256) k_twist_pick(const Singleton *__restrict_
   }
 }
 
+// ---------------------------------------------------------------------------
+// Twist search in two passes over row-aligned chunks (A-31; replaces k_twist_seg + k_twist_pick):
+// k_twist_f runs the forward lane over chunk c = rows [cL, (c+1)L) and stores TF[row * S + i] = d+(row);
+// k_twist_b runs the backward lane over the same chunk, forms gamma(row) = TF(row) - c2(row)/omega(row+1)
+// on the fly and keeps the chunk's argmin |gamma| (only TF is stored: half the traffic of storing both
+// lanes); k_twist_pick2 takes the argmin over the chunks where both lanes are verified (every junction
+// state bit-identical to its exact predecessor's exit).  Thread (chunk c, singleton i), consecutive
+// threads = consecutive singletons on one chunk: shared row loads, coalesced TF stores and loads.
+// ---------------------------------------------------------------------------
+struct TwRec {
+  double in, out;       // lane state entering the chunk's first step / after its last step
+  double best, scale;   // B: the chunk's min |gamma| and max(|TF|, |TB|) at its argmin
+  int ok, empty, row, pad;
+};
+__device__ __forceinline__ double tw_lam(const RqiState &S) {
+  // evaluated a fraction of the inflated bracket away from lambda-hat, so that |gamma_r| stays well above
+  // the fp64 rounding of its terms however close lambda-hat is (r is eigenvector j's peak either way)
+  return __dadd_rn(S.lam_hi, ldexp(__dsub_rn(S.bhi_hi, S.blo_hi), -8));
+}
+template <bool ISB>
+__global__ void __launch_bounds__(128) k_twist_lane(const Singleton *__restrict__ sg, int ns,
+                                                    const RepDesc *__restrict__ reps, const QElt *__restrict__ mq,
+                                                    const RqiState *__restrict__ st, int KT, int Wu, double *TF,
+                                                    long long S_, TwRec *rec) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (long long)ns * KT) return;
+  const int i = (int)(g % ns), c = (int)(g / ns);
+  const RqiState S = st[i];
+  if (S.status != 0) return;
+  TwRec *R = rec + ((long long)i * KT + c) * 2 + (ISB ? 1 : 0);
+  const RepDesc Rp = reps[sg[i].rep];
+  const int nb = Rp.nb, steps = nb - 1;
+  const QElt *q = mq + Rp.off;
+  const double lam = tw_lam(S);
+  const int L = max((steps + KT - 1) / KT, 1);
+  const int lo = min(c * L, steps), hi = min(lo + L, steps);
+  double *T = TF + i;
+#define TROW(row) T[(long long)(row) * S_]
+  if (hi <= lo) {
+    R->empty = 1;
+    R->ok = 1;
+    if (!ISB && c == 0 && steps == 0) TROW(0) = __dsub_rn(__ldg(&q[0].gb_hi), lam);  // nb = 1: gamma = d+(0)
+    return;
+  }
+  // F: steps t = rows lo..hi-1; B: steps t = nb-1-hi .. nb-2-lo (rows hi-1 .. lo)
+  const int t0 = ISB ? nb - 1 - hi : lo, t1 = ISB ? nb - 1 - lo : hi;
+  const int tw = (t0 == 0) ? 0 : max(t0 - Wu, 0);
+  const int rs = ISB ? nb - 1 - tw : tw;
+  double den = __dsub_rn(__ldg(&q[rs].gb_hi), lam);  // exact at t = 0, a guess elsewhere
+  double din = den, best = INFINITY, scale = 0.0;
+  int brow = -1;
+  bool ok = true;
+  constexpr int PF = 8;
+  double rc[PF], rg[PF], rf[PF];  // B also prefetches TF(row): the stored forward lane streams from HBM
+  auto ld = [&](int t, int u) {
+    const int row = max(seg_row(ISB, nb, min(t, t1 - 1)), 0);
+    rc[u] = __ldg(&q[row].c2_hi);
+    rg[u] = ISB ? __ldg(&q[row].gb_hi) : __ldg(&q[row].gf_hi);
+    if (ISB) rf[u] = (t >= t0) ? __ldcs(T + (long long)row * S_) : 0.0;
+  };
+  auto step = [&](int t, double c2, double gg, double tf) {
+    if (t == t0) din = den;
+    const double P = div_fast_nocheck(c2, den);
+    if (t >= t0) {
+      const int row = seg_row(ISB, nb, t);
+      if (ISB) {  // gamma(row) = d+(row) - c2(row)/omega(row+1); rows visited downwards: ties to the smaller row
+        const double gm = fabs(__dsub_rn(tf, P));
+        if (gm <= best) { best = gm; brow = row; scale = fmax(fabs(tf), fabs(P)); }
+      } else {
+        TROW(row) = den;
+      }
+    }
+    den = __dsub_rn(__dsub_rn(gg, lam), P);
+    ok &= isfinite(den) && den != 0.0;
+  };
+#pragma unroll
+  for (int u = 0; u < PF; u++) ld(tw + u, u);
+  int t = tw;
+  for (; t + PF <= t1; t += PF) {
+#pragma unroll
+    for (int u = 0; u < PF; u++) {
+      const double c2 = rc[u], gg = rg[u], tf = ISB ? rf[u] : 0.0;
+      ld(t + u + PF, u);
+      step(t + u, c2, gg, tf);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < PF; u++)
+    if (t + u < t1) step(t + u, rc[u], rg[u], ISB ? rf[u] : 0.0);
+  if (!ISB && hi == steps) TROW(nb - 1) = den;  // gamma_n = d+(n)
+#undef TROW
+  R->in = din;
+  R->out = den;
+  R->best = best;
+  R->scale = scale;
+  R->row = brow;
+  R->ok = ok ? 1 : 0;
+  R->empty = 0;
+}
+// r = argmin |gamma| over the chunks verified in both lanes (F: the prefix of chunks whose entry states
+// chain exactly from row 0; B: the suffix chaining exactly from row nb-2), plus gamma_n = d+(n) when the
+// whole F lane is verified; ties to the smaller row.  Unresolved (|gamma_r| within 2^-46 of its terms) or
+// no candidate: handed over.
+__global__ void k_twist_pick2(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
+                              RqiState *st, int KT, const double *__restrict__ TF, long long S_,
+                              const TwRec *__restrict__ rec, long long *stats) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned ho = 0, rows = 0;
+  if (i < ns && st[i].status == 0) {
+    const int nb = reps[sg[i].rep].nb;
+    const TwRec *R = rec + (long long)i * KT * 2;
+    int kf = 0, prev = -1;  // F: chunks 0..kf-1 verified
+    for (; kf < KT; kf++) {
+      const TwRec &a = R[2 * kf];
+      if (a.empty) continue;
+      if (!a.ok || (prev >= 0 && __double_as_longlong(a.in) != __double_as_longlong(R[2 * prev].out))) break;
+      prev = kf;
+    }
+    int kb = KT - 1;  // B: chunks kb+1..KT-1 verified
+    prev = -1;
+    for (; kb >= 0; kb--) {
+      const TwRec &a = R[2 * kb + 1];
+      if (a.empty) continue;
+      if (!a.ok || (prev >= 0 && __double_as_longlong(a.in) != __double_as_longlong(R[2 * prev + 1].out))) break;
+      prev = kb;
+    }
+    double best = INFINITY, sc = 0.0;
+    int bk = -1;
+    for (int c = kb + 1; c < kf; c++) {  // chunks verified in both lanes (ascending rows: ties keep the smaller)
+      const TwRec &a = R[2 * c + 1];
+      if (a.empty || a.row < 0) continue;
+      if (a.best < best) { best = a.best; bk = a.row; sc = a.scale; }
+    }
+    if (kf == KT) {  // gamma_n = d+(n) (B contributes 0) once the whole F lane is exact
+      const double tn = fabs(TF[(long long)(nb - 1) * S_ + i]);
+      if (tn < best) { best = tn; bk = nb - 1; sc = tn; }
+    }
+    if (bk < 0 || !(best > 0x1p-46 * sc)) {
+      st[i].status = 2;
+      ho = 1;
+    } else {
+      st[i].r = bk;
+      rows = (unsigned)(2 * (nb - 1));
+    }
+  }
+  ho = __reduce_add_sync(0xffffffffu, ho);
+  rows = __reduce_add_sync(0xffffffffu, rows);
+  if ((threadIdx.x & 31) == 0) {
+    if (ho) atomicAdd((unsigned long long *)&stats[ST_HO_TWIST], (unsigned long long)ho);
+    if (rows) atomicAdd((unsigned long long *)&stats[ST_TWIST_ROWS], (unsigned long long)rows);
+  }
+}
+
 // the r-twisted factorization in dd: F steps 0..r-1, B steps 0..nb-2-r (rows nb-2 .. r)
 // one segment of a fixed-lambda pass: steps t in [tw, t1) of lane isB (F: row t, B: row nb-2-t), warm-up
 // [tw, t0) from a guess (the recurrence alone), result in *R (entry state at t0, exit state, partial norm,

@@ -102,6 +102,7 @@ struct mrrr_ctx {
   long long rqi_threads = 131072;  // adaptive RQI segment count target (threads per segmented pass)
   bool rqi_bal = true;         // split a singleton's 2K segments between its lanes by length
   bool rqi_chunk = true;       // chunk-major fixed passes (k_fixed_chunk) instead of lane-major (k_fixed_seg)
+  bool tw2 = true;             // twist search in two passes storing only d+ (k_twist_lane, k_twist_pick2)
   bool rqi_bulk = true;        // k_fixed_chunk stores the factors by bulk copies of staged 8-row runs
   bool zw_chunk = true;        // k_zwrite_chunk (chunked products, staged tiles) instead of the per-row warp scan
   int segy_k = 8, segy_w = 128;  // segmented y-NegCount (MRRR_SEGYK=1: unsegmented)
@@ -758,11 +759,23 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
         RqiState *rs = h->rqst.as<RqiState>();
         SegRec *rec = h->rqrec.as<SegRec>();
         k_rqi3_init<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs);
-        k_twist_seg<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
-                                                                          h->mq.as<QElt>(), rs, K, Wu, TF, TB, stride,
-                                                                          rec);
-        k_twist_pick<<<(unsigned)((nb + 31) / 32), 256, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, TF,
-                                                                        TB, stride, rec, h->stats.as<long long>());
+        if (h->tw2) {
+          // twist search: forward lane stores d+, backward lane forms gamma and the per-chunk argmin
+          const int KT = 2 * K;
+          TwRec *trec = reinterpret_cast<TwRec *>(rec);
+          k_twist_lane<false><<<nblocks_for((long long)KT * nb, 128), 128, 0, h->stream>>>(
+              sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, KT, Wu, TF, stride, trec);
+          k_twist_lane<true><<<nblocks_for((long long)KT * nb, 128), 128, 0, h->stream>>>(
+              sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, KT, Wu, TF, stride, trec);
+          k_twist_pick2<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs, KT, TF,
+                                                                      stride, trec, h->stats.as<long long>());
+        } else {
+          k_twist_seg<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
+                                                                            h->mq.as<QElt>(), rs, K, Wu, TF, TB, stride,
+                                                                            rec);
+          k_twist_pick<<<(unsigned)((nb + 31) / 32), 256, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs, K,
+                                                                          TF, TB, stride, rec, h->stats.as<long long>());
+        }
         launch_check(h);
         for (int it = 0; it < MAX_RQI + 2; it++) {  // + the passes repeated with a wide warm-up
           CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
@@ -1319,6 +1332,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_RQICHUNK")) h->rqi_chunk = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQIBULK")) h->rqi_bulk = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQITHREADS")) h->rqi_threads = atoll(s);
+    if (const char *s = getenv("MRRR_TW2")) h->tw2 = atoi(s) != 0;
     if (const char *s = getenv("MRRR_SEGTHREADS")) h->seg_threads = atoll(s);
     if (const char *s = getenv("MRRR_SEGCH2")) h->seg_ch2 = atoll(s);
     if (const char *s = getenv("MRRR_SEGYK")) h->segy_k = std::max(1, std::min(64, atoi(s)));

@@ -401,7 +401,10 @@ __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-constexpr int ZG = 8;             // factor rows per bulk store
+#ifndef MRRR_ZG
+#define MRRR_ZG 8
+#endif
+constexpr int ZG = MRRR_ZG;            // factor rows per bulk store
 constexpr int ZSTRIDE = 2 * ZG + 1;  // double2 per thread: two groups + pad (16-byte lanes, conflict-free)
 
 template <bool LIGHT>
@@ -521,7 +524,10 @@ __global__ void __launch_bounds__(128) k_fixed_seg(const Singleton *__restrict__
 // stream; consecutive threads are consecutive singletons on the same chunk, so on a shared
 // representation a warp loads one or two distinct rows per step (the lane-major layout loads 32).
 // Records: rec[(i * K2 + c) * 2 + lane] (lane 0 F, 1 B); parts that do not exist are marked empty.
-__global__ void __launch_bounds__(128) k_fixed_chunk(const Singleton *__restrict__ sg, int ns,
+#ifndef MRRR_FC_MINB
+#define MRRR_FC_MINB 1
+#endif
+__global__ void __launch_bounds__(128, MRRR_FC_MINB) k_fixed_chunk(const Singleton *__restrict__ sg, int ns,
                                                      const RepDesc *__restrict__ reps, const QElt *__restrict__ mq,
                                                      const RqiState *__restrict__ st, int K2, int Wu, dd *P2,
                                                      long long nbmax, SegRec *rec, int bulk) {

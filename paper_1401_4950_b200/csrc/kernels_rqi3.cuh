@@ -234,6 +234,7 @@ struct TwRec {
   double in, out;       // lane state entering the chunk's first step / after its last step
   double best, scale;   // B: the chunk's min |gamma| and max(|TF|, |TB|) at its argmin
   int ok, empty, row, pad;
+  double in_lo, out_lo;  // dd twist search (child frames): low words of the states
 };
 __device__ __forceinline__ double tw_lam(const RqiState &S) {
   // evaluated a fraction of the inflated bracket away from lambda-hat, so that |gamma_r| stays well above
@@ -314,6 +315,8 @@ __global__ void __launch_bounds__(128) k_twist_lane(const Singleton *__restrict_
 #undef TROW
   R->in = din;
   R->out = den;
+  R->in_lo = 0.0;
+  R->out_lo = 0.0;
   R->best = best;
   R->scale = scale;
   R->row = brow;
@@ -325,8 +328,8 @@ __global__ void __launch_bounds__(128) k_twist_lane(const Singleton *__restrict_
 // whole F lane is verified; ties to the smaller row.  Unresolved (|gamma_r| within 2^-46 of its terms) or
 // no candidate: handed over.
 __global__ void k_twist_pick2(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
-                              RqiState *st, int KT, const double *__restrict__ TF, long long S_,
-                              const TwRec *__restrict__ rec, long long *stats) {
+                              RqiState *st, int KT, const double *__restrict__ TF, const dd *__restrict__ TFd,
+                              long long S_, const TwRec *__restrict__ rec, double res, long long *stats) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned ho = 0, rows = 0;
   if (i < ns && st[i].status == 0) {
@@ -336,7 +339,9 @@ __global__ void k_twist_pick2(const Singleton *__restrict__ sg, int ns, const Re
     for (; kf < KT; kf++) {
       const TwRec &a = R[2 * kf];
       if (a.empty) continue;
-      if (!a.ok || (prev >= 0 && __double_as_longlong(a.in) != __double_as_longlong(R[2 * prev].out))) break;
+      if (!a.ok || (prev >= 0 && (__double_as_longlong(a.in) != __double_as_longlong(R[2 * prev].out) ||
+                                  __double_as_longlong(a.in_lo) != __double_as_longlong(R[2 * prev].out_lo))))
+        break;
       prev = kf;
     }
     int kb = KT - 1;  // B: chunks kb+1..KT-1 verified
@@ -344,7 +349,9 @@ __global__ void k_twist_pick2(const Singleton *__restrict__ sg, int ns, const Re
     for (; kb >= 0; kb--) {
       const TwRec &a = R[2 * kb + 1];
       if (a.empty) continue;
-      if (!a.ok || (prev >= 0 && __double_as_longlong(a.in) != __double_as_longlong(R[2 * prev + 1].out))) break;
+      if (!a.ok || (prev >= 0 && (__double_as_longlong(a.in) != __double_as_longlong(R[2 * prev + 1].out) ||
+                                  __double_as_longlong(a.in_lo) != __double_as_longlong(R[2 * prev + 1].out_lo))))
+        break;
       prev = kb;
     }
     double best = INFINITY, sc = 0.0;
@@ -355,10 +362,10 @@ __global__ void k_twist_pick2(const Singleton *__restrict__ sg, int ns, const Re
       if (a.best < best) { best = a.best; bk = a.row; sc = a.scale; }
     }
     if (kf == KT) {  // gamma_n = d+(n) (B contributes 0) once the whole F lane is exact
-      const double tn = fabs(TF[(long long)(nb - 1) * S_ + i]);
+      const double tn = fabs(TFd ? TFd[(long long)(nb - 1) * S_ + i].hi : TF[(long long)(nb - 1) * S_ + i]);
       if (tn < best) { best = tn; bk = nb - 1; sc = tn; }
     }
-    if (bk < 0 || !(best > 0x1p-46 * sc)) {
+    if (bk < 0 || !(best > res * sc)) {
       st[i].status = 2;
       ho = 1;
     } else {
@@ -407,14 +414,21 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 constexpr int ZG = MRRR_ZG;            // factor rows per bulk store
 constexpr int ZSTRIDE = 2 * ZG + 1;  // double2 per thread: two groups + pad (16-byte lanes, conflict-free)
 
+// L2 prefetch of the row PFD steps ahead (child frames: each singleton streams its own representation
+// from HBM; the root's rows are L2-resident and shared, so no hint is issued there)
+constexpr int PFD = 16;
+__device__ __forceinline__ void l2_prefetch(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 template <bool LIGHT>
 __device__ __forceinline__ void seg_pass_t(const QElt *__restrict__ q, int nb, int isB, int t0, int t1, int tw,
-                                           dd lam, dd nlam, dd *P, SegRec *R, double2 *stg) {
+                                           dd lam, dd nlam, dd *P, SegRec *R, double2 *stg, bool pf) {
   R->empty = 0;
   const int rs = isB ? nb - 1 - tw : tw, og = isB ? 3 : 2;
   dd den = dd_sub_nf(dd_make(__ldg(&q[rs].gb_hi), __ldg(&q[rs].gb_lo)), lam);
   bool ok = true;
+  if (pf)
+    for (int u = 0; u < PFD; u++) l2_prefetch(q + min(max(seg_row(isB, nb, tw + u), 0), nb - 1));
   for (int t = tw; t < t0; t++) {
+    if (pf) l2_prefetch(q + min(max(seg_row(isB, nb, t + PFD), 0), nb - 1));
     const double2 *pq = reinterpret_cast<const double2 *>(q + seg_row(isB, nb, t));
     const dd c2 = D2(__ldg(pq)), gg = D2(__ldg(pq + og));
     double r1, r2;
@@ -429,7 +443,10 @@ __device__ __forceinline__ void seg_pass_t(const QElt *__restrict__ q, int nb, i
   const int dq = isB ? -4 : 4;  // double2 per QElt row, in the lane's direction
   const double2 *pq = reinterpret_cast<const double2 *>(q + min(max(seg_row(isB, nb, t0), 0), nb - 1));
   double2 nc2 = __ldg(pq), ndl = __ldg(pq + 1), ngg = __ldg(pq + og);
+  if (pf && t0 > tw)
+    for (int u = 0; u < PFD; u++) l2_prefetch(q + min(max(seg_row(isB, nb, t0 + u), 0), nb - 1));
   for (int t = t0; t < t1; t++) {
+    if (pf) l2_prefetch(q + min(max(seg_row(isB, nb, t + PFD), 0), nb - 1));
     const int row = seg_row(isB, nb, t);
     const dd c2 = D2(nc2), dl = D2(ndl), gg = D2(ngg);
     if (t + 1 < t1) pq += dq;
@@ -481,9 +498,10 @@ __device__ __forceinline__ void seg_pass_t(const QElt *__restrict__ q, int nb, i
   R->ok = ok ? 1 : 0;
 }
 __device__ __forceinline__ void seg_pass(const QElt *__restrict__ q, int nb, int isB, int t0, int t1, int tw,
-                                         bool light, dd lam, dd nlam, dd *P, SegRec *R, double2 *stg = nullptr) {
-  if (light) seg_pass_t<true>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, nullptr);
-  else seg_pass_t<false>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, stg);
+                                         bool light, dd lam, dd nlam, dd *P, SegRec *R, double2 *stg = nullptr,
+                                         bool pf = false) {
+  if (light) seg_pass_t<true>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, nullptr, pf);
+  else seg_pass_t<false>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, stg, pf);
 }
 
 __global__ void __launch_bounds__(128) k_fixed_seg(const Singleton *__restrict__ sg, int ns,
@@ -524,6 +542,94 @@ __global__ void __launch_bounds__(128) k_fixed_seg(const Singleton *__restrict__
 // stream; consecutive threads are consecutive singletons on the same chunk, so on a shared
 // representation a warp loads one or two distinct rows per step (the lane-major layout loads 32).
 // Records: rec[(i * K2 + c) * 2 + lane] (lane 0 F, 1 B); parts that do not exist are marked empty.
+// dd twist search for child frames (the fp64 search rarely resolves gamma there: a child representation's
+// eigenvalues are tiny next to its pivots): k_twist_lane's two passes with the y-arithmetic step of the
+// fixed passes (one dd quotient, one dd three-term sum) and d+ stored in dd.
+template <bool ISB>
+__global__ void __launch_bounds__(128) k_twist_lane_dd(const Singleton *__restrict__ sg, int ns,
+                                                       const RepDesc *__restrict__ reps,
+                                                       const QElt *__restrict__ mq, const RqiState *__restrict__ st,
+                                                       int KT, int Wu, dd *TF, long long S_, TwRec *rec) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (long long)ns * KT) return;
+  const int i = (int)(g % ns), c = (int)(g / ns);
+  const RqiState S = st[i];
+  if (S.status != 0) return;
+  TwRec *R = rec + ((long long)i * KT + c) * 2 + (ISB ? 1 : 0);
+  const RepDesc Rp = reps[sg[i].rep];
+  const int nb = Rp.nb, steps = nb - 1;
+  const QElt *q = mq + Rp.off;
+  const dd lam = dd_add_d(dd_make(S.lam_hi, S.lam_lo), ldexp(__dsub_rn(S.bhi_hi, S.blo_hi), -8)), nlam = dd_neg(lam);
+  const int L = max((steps + KT - 1) / KT, 1);
+  const int lo = min(c * L, steps), hi = min(lo + L, steps);
+  dd *T = TF + i;
+  if (hi <= lo) {
+    R->empty = 1;
+    R->ok = 1;
+    if (!ISB && c == 0 && steps == 0) T[0] = dd_sub_nf(dd_make(__ldg(&q[0].gb_hi), __ldg(&q[0].gb_lo)), lam);
+    return;
+  }
+  const int t0 = ISB ? nb - 1 - hi : lo, t1 = ISB ? nb - 1 - lo : hi;
+  const int tw = (t0 == 0) ? 0 : max(t0 - Wu, 0);
+  const int rs = ISB ? nb - 1 - tw : tw, og = ISB ? 3 : 2;
+  dd den = dd_sub_nf(dd_make(__ldg(&q[rs].gb_hi), __ldg(&q[rs].gb_lo)), lam);
+  dd din = den;
+  double best = INFINITY, scale = 0.0;
+  int brow = -1;
+  bool ok = true;
+  constexpr int PF = 4;
+  double2 rc[PF], rg[PF], rf[PF];
+  auto ld = [&](int t, int u) {
+    const int row = max(seg_row(ISB, nb, min(t, t1 - 1)), 0);
+    const double2 *pq = reinterpret_cast<const double2 *>(q + row);
+    rc[u] = __ldg(pq);
+    rg[u] = __ldg(pq + og);
+    if (ISB) rf[u] = (t >= t0) ? __ldcs(reinterpret_cast<const double2 *>(T + (long long)row * S_)) : make_double2(0, 0);
+  };
+  auto step = [&](int t, double2 c2v, double2 gv, double2 tfv) {
+    if (t == t0) din = den;
+    double r1, r2;
+    ok &= rcp_nr2(den.hi, r1, r2);
+    const dd P = qdiv(D2(c2v), den, r1, r2);
+    if (t >= t0) {
+      const int row = seg_row(ISB, nb, t);
+      if (ISB) {
+        const dd gmd = dd_sub(D2(tfv), P);
+        const double gm = fabs(gmd.hi);
+        if (gm <= best) { best = gm; brow = row; scale = fmax(fabs(tfv.x), fabs(P.hi)); }
+      } else {
+        T[(long long)row * S_] = den;
+      }
+    }
+    den = dd_sum3_nf(D2(gv), nlam, dd_neg(P));
+  };
+#pragma unroll
+  for (int u = 0; u < PF; u++) ld(tw + u, u);
+  int t = tw;
+  for (; t + PF <= t1; t += PF) {
+#pragma unroll
+    for (int u = 0; u < PF; u++) {
+      const double2 c2 = rc[u], gg = rg[u], tf = ISB ? rf[u] : make_double2(0, 0);
+      ld(t + u + PF, u);
+      step(t + u, c2, gg, tf);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < PF; u++)
+    if (t + u < t1) step(t + u, rc[u], rg[u], ISB ? rf[u] : make_double2(0, 0));
+  if (!ISB && hi == steps) T[(long long)(nb - 1) * S_] = den;  // gamma_n = d+(n)
+  ok &= isfinite(den.hi) && isfinite(den.lo);
+  R->in = din.hi;
+  R->in_lo = din.lo;
+  R->out = den.hi;
+  R->out_lo = den.lo;
+  R->best = best;
+  R->scale = scale;
+  R->row = brow;
+  R->ok = ok ? 1 : 0;
+  R->empty = 0;
+}
+
 #ifndef MRRR_FC_MINB
 #define MRRR_FC_MINB 1
 #endif
@@ -588,7 +694,7 @@ __global__ void __launch_bounds__(128, MRRR_FC_MINB) k_fixed_chunk(const Singlet
   const dd lam = dd_make(S.lam_hi, S.lam_lo), nlam = dd_neg(lam);
   __shared__ __align__(16) double2 stage[128 * ZSTRIDE];
   seg_pass(q, nb, isB, t0, t1, t0 == 0 ? 0 : max(t0 - W, 0), light, lam, nlam, P2 + (long long)i * nbmax, R,
-           bulk ? stage + threadIdx.x * ZSTRIDE : nullptr);
+           bulk ? stage + threadIdx.x * ZSTRIDE : nullptr, Rp.depth > 0);
 }
 
 // thread per singleton: junctions, gamma_r, ||z||^2, inertia, and the stask decision

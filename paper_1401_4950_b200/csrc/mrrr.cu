@@ -102,6 +102,8 @@ struct mrrr_ctx {
   long long rqi_threads = 131072;  // adaptive RQI segment count target (threads per segmented pass)
   bool rqi_bal = true;         // split a singleton's 2K segments between its lanes by length
   bool rqi_chunk = true;       // chunk-major fixed passes (k_fixed_chunk) instead of lane-major (k_fixed_seg)
+  bool rqi_seg_child = true;   // segmented RQI for child-frame singletons (dd twist search)
+  int segchild_min = 8;        // ... when the level has at least this many singletons per child representation
   bool tw2 = true;             // twist search in two passes storing only d+ (k_twist_lane, k_twist_pick2)
   bool rqi_bulk = true;        // k_fixed_chunk stores the factors by bulk copies of staged 8-row runs
   bool zw_chunk = true;        // k_zwrite_chunk (chunked products, staged tiles) instead of the per-row warp scan
@@ -719,7 +721,8 @@ void l2_pin_reps(mrrr_t h, bool on) {
   cudaGetLastError();
 }
 
-void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long ldz, bool allow_seg) {
+void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long ldz, bool allow_seg,
+             bool child = false) {
   if (ns <= 0) return;
   l2_pin_reps(h, true);
   const bool pair = h->rqi_pair;
@@ -759,7 +762,19 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
         RqiState *rs = h->rqst.as<RqiState>();
         SegRec *rec = h->rqrec.as<SegRec>();
         k_rqi3_init<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs);
-        if (h->tw2) {
+        if (child) {
+          // child frames: the dd twist search (d+ in dd over the P0 plane)
+          const int KT = 2 * K;
+          TwRec *trec = reinterpret_cast<TwRec *>(rec);
+          dd *TFd = h->wsA.as<dd>();
+          k_twist_lane_dd<false><<<nblocks_for((long long)KT * nb, 128), 128, 0, h->stream>>>(
+              sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, KT, Wu, TFd, stride, trec);
+          k_twist_lane_dd<true><<<nblocks_for((long long)KT * nb, 128), 128, 0, h->stream>>>(
+              sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, KT, Wu, TFd, stride, trec);
+          k_twist_pick2<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs, KT,
+                                                                      nullptr, TFd, stride, trec, 0x1p-90,
+                                                                      h->stats.as<long long>());
+        } else if (h->tw2) {
           // twist search: forward lane stores d+, backward lane forms gamma and the per-chunk argmin
           const int KT = 2 * K;
           TwRec *trec = reinterpret_cast<TwRec *>(rec);
@@ -768,7 +783,8 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
           k_twist_lane<true><<<nblocks_for((long long)KT * nb, 128), 128, 0, h->stream>>>(
               sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, KT, Wu, TF, stride, trec);
           k_twist_pick2<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs, KT, TF,
-                                                                      stride, trec, h->stats.as<long long>());
+                                                                      nullptr, stride, trec, 0x1p-46,
+                                                                      h->stats.as<long long>());
         } else {
           k_twist_seg<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
                                                                             h->mq.as<QElt>(), rs, K, Wu, TF, TB, stride,
@@ -984,7 +1000,10 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
     launch_check(h);
     read_counters(h);
     int ns = h->h_cnt[C_NSING], nnx = h->h_cnt[C_NNXT];
-    run_rqi(h, ns, nbmax, W, Z, ldz, false);  // child frames: the x-arithmetic twist search rarely resolves
+    // child frames: the segmented passes with the dd twist search when the child representations are shared
+    // by enough singletons for their row loads to coincide (else each lane streams its own representation
+    // from HBM and the two-lane kernel is faster: measured C3, 2 singletons per child, vs C4, up to 256)
+    run_rqi(h, ns, nbmax, W, Z, ldz, h->rqi_seg_child && ns >= (long long)h->segchild_min * nc, true);
     process_clusters(h, NX.as<Cluster>(), nnx, repbase + nc, poolbase + (long long)nc * nbmax, ipool_top + stot, nbmax,
                      true, W, Z, ldz, kout, level + 1);
     CK(cudaStreamSynchronize(h->stream));
@@ -1333,6 +1352,8 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_RQIBULK")) h->rqi_bulk = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQITHREADS")) h->rqi_threads = atoll(s);
     if (const char *s = getenv("MRRR_TW2")) h->tw2 = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_RQISEGCHILD")) h->rqi_seg_child = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_SEGCHILDMIN")) h->segchild_min = atoi(s);
     if (const char *s = getenv("MRRR_SEGTHREADS")) h->seg_threads = atoll(s);
     if (const char *s = getenv("MRRR_SEGCH2")) h->seg_ch2 = atoll(s);
     if (const char *s = getenv("MRRR_SEGYK")) h->segy_k = std::max(1, std::min(64, atoi(s)));

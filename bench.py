@@ -289,7 +289,7 @@ def main():
         if rq_n:
             launch_ms = rq_ms / rq_n
             f = fl.rqi_flops(stats, n, wdiv) / nrq
-            cands.append(("singleton RQI + eigenvectors (k_twist_seg, k_fixed_chunk, k_zwrite_chunk; k_rqi2 for hand-overs)",
+            cands.append(("singleton RQI + eigenvectors (k_twist_lane, k_fixed_chunk, k_zwrite_chunk; k_rqi2 for hand-overs)",
                           "k_fixed_chunk", launch_ms, f))
         out = []
         for name, pref, launch_ms, f in cands:

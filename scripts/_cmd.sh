@@ -1,4 +1,6 @@
 O=gpurun_out; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || { echo BUILD FAILED; exit 1; }
+timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 5 --warmup 2 --workload C2 | python scripts/bench_summary.py C2 host
+for rb in 4 8 16; do MRRR_DEVROUNDS=1 MRRR_DEVRB=$rb timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 5 --warmup 2 --workload C2 | python scripts/bench_summary.py C2 dev RB=$rb; done
+for w in C5a C1; do timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 2 --warmup 2 --workload $w | python scripts/bench_summary.py $w host; MRRR_DEVROUNDS=1 timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 2 --warmup 2 --workload $w | python scripts/bench_summary.py $w dev; done
 timeout 1500 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 $O/pytest_gpu.log
-for w in C3 C4; do timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 2 --warmup 1 --workload $w | python scripts/bench_summary.py $w; done

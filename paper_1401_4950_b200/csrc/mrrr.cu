@@ -437,7 +437,7 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
   const int K = h->seg_k, L = (nb - 1 + K - 1) / K;
   const int MAXR = 256, RB = h->dev_rb;
   const int mmax = mcap > 0 ? mcap : h->mmax;
-  const long long maxch = mcap > 0 ? (long long)nnode * ((1LL << mcap) - 1)
+  const long long maxch = mcap > 0 ? (long long)maxnodes * ((1LL << mcap) - 1)
                                    : std::max<long long>(h->target_chains, maxnodes) + 128;
   CK(h->rnd.ensure(sizeof(int) * 2 * (MAXR + 2)));
   CK(h->counts.ensure(sizeof(int) * maxch));
@@ -657,11 +657,13 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
       run_rounds_device(h, cur, nxt, nnode, single_nb, std::max(nnode, h->max_nodes), out_lo, out_hi, rtol);
       return;
     }
-    if (!Y && seg_on && h->dev_stable && nnode > 0 && h->h_cnt[C_NMULTI] == 0) {
-      // stable phase: every node holds one wanted index; the remaining rounds run without host round trips
+    if (!Y && seg_on && h->dev_stable && nnode > 0 && (long long)h->h_cnt[C_NMULTI] * 16 <= nnode) {
+      // near-stable phase: the node count can grow by at most the indices still sharing nodes (few), so
+      // the remaining rounds run without host round trips on grids sized for that bound
+      const long long maxn = (long long)nnode + h->h_cnt[C_NMULTI];
       int mcap = 1;
-      while (mcap < h->mmax && (long long)nnode * ((1LL << (mcap + 1)) - 1) <= target) mcap++;
-      run_rounds_device(h, cur, nxt, nnode, single_nb, nnode, out_lo, out_hi, rtol, mcap);
+      while (mcap < h->mmax && maxn * ((1LL << (mcap + 1)) - 1) <= target) mcap++;
+      run_rounds_device(h, cur, nxt, nnode, single_nb, (int)maxn, out_lo, out_hi, rtol, mcap);
       return;
     }
   }

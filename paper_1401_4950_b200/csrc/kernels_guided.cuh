@@ -356,10 +356,13 @@ __global__ void __launch_bounds__(128) k_negcount_seg(const Node *__restrict__ n
 // accept segments along the verified chain of exact states; queue the rest for the careful tail
 __global__ void k_seg_combine(long long tot, long long nn, int K, const SegOut *__restrict__ seg, int *counts,
                               int *excounts, int4 *fb, int *nfb, double *fb_s, const int *__restrict__ dnn, int mmax,
-                              long long target, long long *negx) {
+                              long long target, long long *negx, const Node *__restrict__ nodes, int nnode, int m,
+                              const ExplicitChain *__restrict__ ex, const RepDesc *__restrict__ reps,
+                              const double2 *__restrict__ mx, int L) {
   if (dnn) {
-    const int nnode = *dnn;
-    nn = (long long)nnode * ((1 << round_m(nnode, mmax, target)) - 1);
+    nnode = *dnn;
+    m = round_m(nnode, mmax, target);
+    nn = (long long)nnode * ((1 << m) - 1);
     tot = nn;
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd((unsigned long long *)negx, (unsigned long long)tot);
   }
@@ -394,6 +397,28 @@ __global__ void k_seg_combine(long long tot, long long nn, int K, const SegOut *
   if (k == K) {
     if (c < nn) counts[c] = total;
     else excounts[c - nn] = total;
+    return;
+  }
+  if (nodes || ex) {  // careful sequential tail right here (rare: no separate launch per round)
+    double sig;
+    int rep;
+    chain_of(nodes, m, nn, ex, c, sig, rep);
+    const RepDesc R = reps[rep];
+    const double2 *M = mx + R.off;
+    const int nb = R.nb;
+    double s = s_exact;
+    int cnt = total;
+    for (int r = min(k * L, nb - 1); r < nb - 1; r++) {
+      const double2 mm = M[r];
+      const double dp = __dadd_rn(mm.x, s);
+      const double q = (isinf(s) && isinf(dp)) ? 1.0 : __ddiv_rn(s, dp);
+      s = __dsub_rn(__dmul_rn(q, mm.y), sig);
+      cnt += sbx(dp);
+    }
+    cnt += sbx(__dadd_rn(M[nb - 1].x, s));
+    if (c < nn) counts[c] = cnt;
+    else excounts[c - nn] = cnt;
+    atomicAdd(nfb, 1);
     return;
   }
   const int slot = atomicAdd(nfb, 1);

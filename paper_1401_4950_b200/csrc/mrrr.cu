@@ -473,12 +473,11 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
           in, 0, 0, nullptr, 0, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L, h->seg_w, h->segout.as<SegOut>(),
           nn + r, mmax, h->target_chains);
       CK(cudaEventRecord(h->rev[2 * r + 1], h->stream));
+      // junction walk with the careful tail inline (no separate fallback launch)
       k_seg_combine<<<g1, 128, 0, h->stream>>>(0, 0, K, h->segout.as<SegOut>(), h->counts.as<int>(), nullptr,
                                                h->segfb.as<int4>(), nfb + r, h->segfbs.as<double>(), nn + r, mmax,
-                                               h->target_chains, negx);
-      k_seg_fallback<<<g1, 128, 0, h->stream>>>(h->segfb.as<int4>(), nfb + r, h->segfbs.as<double>(), in, 0, 0,
-                                                nullptr, h->reps.as<RepDesc>(), h->mx.as<double2>(), L,
-                                                h->counts.as<int>(), nullptr, nn + r, mmax, h->target_chains);
+                                               h->target_chains, negx, in, 0, 0, nullptr, h->reps.as<RepDesc>(),
+                                               h->mx.as<double2>(), L);
       k_bisect_update_dev<<<g2, 128, 0, h->stream>>>(in, nn + r, mmax, h->target_chains, h->counts.as<int>(), out,
                                                      nn + r + 1, out_lo, out_hi, rtol, alg);
       launch_check(h);
@@ -615,15 +614,10 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
             cur, nnode, m, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L,
             h->seg_w, h->segout.as<SegOut>(), nullptr, 0, 0);
       launch_check(h);
-      k_seg_combine<<<nblocks_for(tot, 128), 128, 0, h->stream>>>(tot, nch, K, h->segout.as<SegOut>(),
-                                                                   h->counts.as<int>(), h->excounts.as<int>(),
-                                                                   h->segfb.as<int4>(), h->cnt.as<int>() + C_NFB,
-                                                                   h->segfbs.as<double>(), nullptr, 0, 0, nullptr);
-      launch_check(h);
-      k_seg_fallback<<<nblocks_for(tot, 128), 128, 0, h->stream>>>(
-          h->segfb.as<int4>(), h->cnt.as<int>() + C_NFB, h->segfbs.as<double>(), cur, nnode, m,
-          h->ex.as<ExplicitChain>(), h->reps.as<RepDesc>(), h->mx.as<double2>(), L, h->counts.as<int>(),
-          h->excounts.as<int>(), nullptr, 0, 0);
+      k_seg_combine<<<nblocks_for(tot, 128), 128, 0, h->stream>>>(
+          tot, nch, K, h->segout.as<SegOut>(), h->counts.as<int>(), h->excounts.as<int>(), h->segfb.as<int4>(),
+          h->cnt.as<int>() + C_NFB, h->segfbs.as<double>(), nullptr, 0, 0, nullptr, cur, nnode, m,
+          h->ex.as<ExplicitChain>(), h->reps.as<RepDesc>(), h->mx.as<double2>(), L);
       launch_check(h);
     } else {
       launch_negcount<Y>(h, cur, nnode, m, nex);
@@ -812,6 +806,7 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
               diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), h->cnt.as<int>() + C_NFB);
           launch_check(h);
           h->host_launches += 1;
+          if (it == 0) continue;  // the RQC-only pass never finishes a singleton: no host check after it
           int act = 0;
           CK(cudaMemcpyAsync(&act, h->cnt.as<int>() + C_NFB, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
           CK(cudaStreamSynchronize(h->stream));

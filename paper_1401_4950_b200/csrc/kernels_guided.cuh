@@ -354,20 +354,13 @@ __global__ void __launch_bounds__(128) k_negcount_seg(const Node *__restrict__ n
 }
 
 // accept segments along the verified chain of exact states; queue the rest for the careful tail
-__global__ void k_seg_combine(long long tot, long long nn, int K, const SegOut *__restrict__ seg, int *counts,
-                              int *excounts, int4 *fb, int *nfb, double *fb_s, const int *__restrict__ dnn, int mmax,
-                              long long target, long long *negx, const Node *__restrict__ nodes, int nnode, int m,
-                              const ExplicitChain *__restrict__ ex, const RepDesc *__restrict__ reps,
-                              const double2 *__restrict__ mx, int L) {
-  if (dnn) {
-    nnode = *dnn;
-    m = round_m(nnode, mmax, target);
-    nn = (long long)nnode * ((1 << m) - 1);
-    tot = nn;
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd((unsigned long long *)negx, (unsigned long long)tot);
-  }
-  long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= tot) return;
+// verified count of chain c from its K segment records; a chain whose junctions do not all verify is
+// finished here with the careful IEEE operations from its last exact state (rare)
+__device__ __forceinline__ int seg_chain_count(const SegOut *__restrict__ seg, int K, long long c,
+                                               const Node *__restrict__ nodes, int m, long long nn,
+                                               const ExplicitChain *__restrict__ ex,
+                                               const RepDesc *__restrict__ reps, const double2 *__restrict__ mx,
+                                               int L, int *nfb) {
   const SegOut *S = seg + c * K;
   int total = 0, k = 0;
   double s_exact = S[0].s_in;  // -sigma
@@ -394,36 +387,65 @@ __global__ void k_seg_combine(long long tot, long long nn, int K, const SegOut *
       s_exact = o.s_out;
     }
   }
-  if (k == K) {
-    if (c < nn) counts[c] = total;
-    else excounts[c - nn] = total;
-    return;
+  if (k == K) return total;
+  double sig;
+  int rep;
+  chain_of(nodes, m, nn, ex, c, sig, rep);
+  const RepDesc R = reps[rep];
+  const double2 *M = mx + R.off;
+  const int nb = R.nb;
+  double s = s_exact;
+  int cnt = total;
+  for (int r = min(k * L, nb - 1); r < nb - 1; r++) {
+    const double2 mm = M[r];
+    const double dp = __dadd_rn(mm.x, s);
+    const double q = (isinf(s) && isinf(dp)) ? 1.0 : __ddiv_rn(s, dp);
+    s = __dsub_rn(__dmul_rn(q, mm.y), sig);
+    cnt += sbx(dp);
   }
-  if (nodes || ex) {  // careful sequential tail right here (rare: no separate launch per round)
-    double sig;
-    int rep;
-    chain_of(nodes, m, nn, ex, c, sig, rep);
-    const RepDesc R = reps[rep];
-    const double2 *M = mx + R.off;
-    const int nb = R.nb;
-    double s = s_exact;
-    int cnt = total;
-    for (int r = min(k * L, nb - 1); r < nb - 1; r++) {
-      const double2 mm = M[r];
-      const double dp = __dadd_rn(mm.x, s);
-      const double q = (isinf(s) && isinf(dp)) ? 1.0 : __ddiv_rn(s, dp);
-      s = __dsub_rn(__dmul_rn(q, mm.y), sig);
-      cnt += sbx(dp);
-    }
-    cnt += sbx(__dadd_rn(M[nb - 1].x, s));
-    if (c < nn) counts[c] = cnt;
-    else excounts[c - nn] = cnt;
-    atomicAdd(nfb, 1);
-    return;
+  cnt += sbx(__dadd_rn(M[nb - 1].x, s));
+  atomicAdd(nfb, 1);
+  return cnt;
+}
+__global__ void k_seg_combine(long long tot, long long nn, int K, const SegOut *__restrict__ seg, int *counts,
+                              int *excounts, int *nfb, const int *__restrict__ dnn, int mmax, long long target,
+                              long long *negx, const Node *__restrict__ nodes, int nnode, int m,
+                              const ExplicitChain *__restrict__ ex, const RepDesc *__restrict__ reps,
+                              const double2 *__restrict__ mx, int L) {
+  if (dnn) {
+    nnode = *dnn;
+    m = round_m(nnode, mmax, target);
+    nn = (long long)nnode * ((1 << m) - 1);
+    tot = nn;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd((unsigned long long *)negx, (unsigned long long)tot);
   }
-  const int slot = atomicAdd(nfb, 1);
-  fb[slot] = make_int4((int)(c & 0x7fffffff), k, total, (int)(c >> 31));
-  fb_s[slot] = s_exact;
+  long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= tot) return;
+  const int cnt = seg_chain_count(seg, K, c, nodes, m, nn, ex, reps, mx, L, nfb);
+  if (c < nn) counts[c] = cnt;
+  else excounts[c - nn] = cnt;
+}
+// One segmented round's bookkeeping in one launch: thread per node counts the node's 2^m - 1 chains
+// (junction walk) and then runs the shared-tree update for the node's 2^m leaves (rounds without
+// explicit chains; host- or device-driven)
+__global__ void k_seg_round(int nnode, int m, int K, const SegOut *__restrict__ seg, int *counts,
+                            const Node *__restrict__ nodes, const RepDesc *__restrict__ reps,
+                            const double2 *__restrict__ mx, int L, Node *next, int *nnext, double *out_lo,
+                            double *out_hi, double rtol, unsigned long long *alg, int *nmulti, int *nfb,
+                            const int *__restrict__ dnn, int mmax, long long target, long long *negx) {
+  if (dnn) {
+    nnode = *dnn;
+    m = round_m(nnode, mmax, target);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      atomicAdd((unsigned long long *)negx, (unsigned long long)((long long)nnode * ((1 << m) - 1)));
+  }
+  const long long P = (1LL << m) - 1, nn = (long long)nnode * P;
+  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= nnode) return;
+  for (long long j = 0; j < P; j++) counts[id * P + j] = seg_chain_count(seg, K, id * P + j, nodes, m, nn, nullptr,
+                                                                         reps, mx, L, nfb);
+  for (int p = 0; p < (1 << m); p++)
+    bisect_update_body((id << m) + p, nodes, nnode, m, counts, next, nnext, out_lo, out_hi, rtol, alg, nmulti);
 }
 
 // careful sequential tail from segment k's first row with the last exact state

@@ -473,13 +473,10 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
           in, 0, 0, nullptr, 0, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L, h->seg_w, h->segout.as<SegOut>(),
           nn + r, mmax, h->target_chains);
       CK(cudaEventRecord(h->rev[2 * r + 1], h->stream));
-      // junction walk with the careful tail inline (no separate fallback launch)
-      k_seg_combine<<<g1, 128, 0, h->stream>>>(0, 0, K, h->segout.as<SegOut>(), h->counts.as<int>(), nullptr,
-                                               h->segfb.as<int4>(), nfb + r, h->segfbs.as<double>(), nn + r, mmax,
-                                               h->target_chains, negx, in, 0, 0, nullptr, h->reps.as<RepDesc>(),
-                                               h->mx.as<double2>(), L);
-      k_bisect_update_dev<<<g2, 128, 0, h->stream>>>(in, nn + r, mmax, h->target_chains, h->counts.as<int>(), out,
-                                                     nn + r + 1, out_lo, out_hi, rtol, alg);
+      // junction walk (careful tail inline) and shared-tree update in one launch
+      k_seg_round<<<g1 * 4, 32, 0, h->stream>>>(0, 0, K, h->segout.as<SegOut>(), h->counts.as<int>(), in,
+                                             h->reps.as<RepDesc>(), h->mx.as<double2>(), L, out, nn + r + 1, out_lo,
+                                             out_hi, rtol, alg, nullptr, nfb + r, nn + r, mmax, h->target_chains, negx);
       launch_check(h);
       h->host_launches += 3;
     }
@@ -590,6 +587,7 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
     long long nch = (long long)nnode * P;
     CK(h->counts.ensure(std::max<long long>(nch, 1) * sizeof(int)));
     int nex = first ? nverify : 0;
+    bool fused = false;  // the segmented round's update ran inside k_seg_round
     zero_counters(h);
     CK(cudaEventRecord(h->nc0, h->stream));
     if (seg_on) {
@@ -614,26 +612,38 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
             cur, nnode, m, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L,
             h->seg_w, h->segout.as<SegOut>(), nullptr, 0, 0);
       launch_check(h);
-      k_seg_combine<<<nblocks_for(tot, 128), 128, 0, h->stream>>>(
-          tot, nch, K, h->segout.as<SegOut>(), h->counts.as<int>(), h->excounts.as<int>(), h->segfb.as<int4>(),
-          h->cnt.as<int>() + C_NFB, h->segfbs.as<double>(), nullptr, 0, 0, nullptr, cur, nnode, m,
-          h->ex.as<ExplicitChain>(), h->reps.as<RepDesc>(), h->mx.as<double2>(), L);
+      CK(cudaEventRecord(h->nc1, h->stream));
+      if (nex == 0) {  // junction walk and shared-tree update in one launch
+        k_seg_round<<<nblocks_for(nnode, 32), 32, 0, h->stream>>>(
+            nnode, m, K, h->segout.as<SegOut>(), h->counts.as<int>(), cur, h->reps.as<RepDesc>(), h->mx.as<double2>(),
+            L, nxt, h->cnt.as<int>() + C_NNEXT, out_lo, out_hi, rtol,
+            (unsigned long long *)(h->stats.as<long long>() + ST_NEGX_ALG), h->cnt.as<int>() + C_NMULTI,
+            h->cnt.as<int>() + C_NFB, nullptr, 0, 0, nullptr);
+        fused = true;
+      } else {
+        k_seg_combine<<<nblocks_for(tot, 128), 128, 0, h->stream>>>(
+            tot, nch, K, h->segout.as<SegOut>(), h->counts.as<int>(), h->excounts.as<int>(), h->cnt.as<int>() + C_NFB,
+            nullptr, 0, 0, nullptr, cur, nnode, m, h->ex.as<ExplicitChain>(), h->reps.as<RepDesc>(),
+            h->mx.as<double2>(), L);
+      }
       launch_check(h);
     } else {
       launch_negcount<Y>(h, cur, nnode, m, nex);
+      CK(cudaEventRecord(h->nc1, h->stream));
     }
-    CK(cudaEventRecord(h->nc1, h->stream));
     if (nex > 0) {
       k_root_verify<<<nblocks_for(nbl, 128), 128, 0, h->stream>>>(blist_dev, nbl, h->starts.as<int>(),
                                                                   h->binfo.as<double>(), h->excounts.as<int>(),
                                                                   h->cnt.as<int>() + C_NEX);
       launch_check(h);
     }
-    k_bisect_update<<<nblocks_for((long long)nnode << m, 128), 128, 0, h->stream>>>(
-        cur, nnode, m, h->counts.as<int>(), nxt, h->cnt.as<int>() + C_NNEXT, out_lo, out_hi, rtol,
-        (unsigned long long *)(h->stats.as<long long>() + (Y ? ST_NEGY_ALG : ST_NEGX_ALG)),
-        h->cnt.as<int>() + C_NMULTI);
-    launch_check(h);
+    if (!fused) {
+      k_bisect_update<<<nblocks_for((long long)nnode << m, 128), 128, 0, h->stream>>>(
+          cur, nnode, m, h->counts.as<int>(), nxt, h->cnt.as<int>() + C_NNEXT, out_lo, out_hi, rtol,
+          (unsigned long long *)(h->stats.as<long long>() + (Y ? ST_NEGY_ALG : ST_NEGX_ALG)),
+          h->cnt.as<int>() + C_NMULTI);
+      launch_check(h);
+    }
     read_counters(h);
     h->host_rounds++;
     h->stats_h[Y ? ST_NEGY : ST_NEGX] += nch + nex;
@@ -799,7 +809,7 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
             k_fixed_seg<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
                                                                               h->mq.as<QElt>(), rs, K, Wu, P2s, nbmax,
                                                                               rec, h->rqi_bal ? 1 : 0);
-          k_fixed_step<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(
+          k_fixed_step<<<nblocks_for(nb, 32), 32, 0, h->stream>>>(
               sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, h->rqi_bal ? 1 : 0, h->rqi_chunk ? 1 : 0, rec, W,
               h->zmeta.as<ZMeta>(),
               diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,

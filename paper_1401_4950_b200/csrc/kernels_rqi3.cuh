@@ -230,6 +230,17 @@ __global__ void __launch_bounds__(256) k_twist_pick(const Singleton *__restrict_
 // state bit-identical to its exact predecessor's exit).  Thread (chunk c, singleton i), consecutive
 // threads = consecutive singletons on one chunk: shared row loads, coalesced TF stores and loads.
 // ---------------------------------------------------------------------------
+// one warp (32 singletons) stages its singletons' records in shared memory with coalesced 16-byte loads
+// (the per-thread record walks are otherwise a chain of dependent cache misses); returns this thread's copy
+__device__ __forceinline__ const void *stage_recs(const void *rec, int bytes, int ns, uint4 *sm) {
+  const int i0 = blockIdx.x * 32, lane = threadIdx.x & 31, n16 = bytes / 16;
+  for (int q = 0; q < 32 && i0 + q < ns; q++) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(rec) + (long long)(i0 + q) * bytes);
+    for (int u = lane; u < n16; u += 32) sm[q * n16 + u] = src[u];
+  }
+  __syncwarp();
+  return sm + lane * n16;
+}
 struct TwRec {
   double in, out;       // lane state entering the chunk's first step / after its last step
   double best, scale;   // B: the chunk's min |gamma| and max(|TF|, |TB|) at its argmin
@@ -329,12 +340,15 @@ __global__ void __launch_bounds__(128) k_twist_lane(const Singleton *__restrict_
 // no candidate: handed over.
 __global__ void k_twist_pick2(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
                               RqiState *st, int KT, const double *__restrict__ TF, const dd *__restrict__ TFd,
-                              long long S_, const TwRec *__restrict__ rec, double res, long long *stats) {
+                              long long S_, const TwRec *__restrict__ rec, double res, long long *stats, int stage) {
+  extern __shared__ uint4 recsm[];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const TwRec *Rs = stage ? reinterpret_cast<const TwRec *>(stage_recs(rec, 2 * KT * (int)sizeof(TwRec), ns, recsm))
+                          : rec + (long long)i * KT * 2;
   unsigned ho = 0, rows = 0;
   if (i < ns && st[i].status == 0) {
     const int nb = reps[sg[i].rep].nb;
-    const TwRec *R = rec + (long long)i * KT * 2;
+    const TwRec *R = Rs;
     int kf = 0, prev = -1;  // F: chunks 0..kf-1 verified
     for (; kf < KT; kf++) {
       const TwRec &a = R[2 * kf];
@@ -704,7 +718,7 @@ struct FsInc {
 };
 __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restrict__ sg,
                                                 const RepDesc *__restrict__ reps, RqiState *st, int K, int bal,
-                                                int chunk, const SegRec *__restrict__ rec, double *W, ZMeta *zmeta,
+                                                int chunk, const SegRec *__restrict__ F, double *W, ZMeta *zmeta,
                                                 int *diag_depth, double *fin_lo, double *fin_hi, FsInc &inc) {
   RqiState S = st[i];
   if (S.status != 0) return;
@@ -712,7 +726,7 @@ __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restri
   const RepDesc Rp = reps[s.rep];
   const int nb = Rp.nb, r = S.r, j = s.j;
   const int KF = chunk ? 2 * K : bal ? seg_kf(nb, r, 2 * K) : K;
-  const SegRec *F = rec + (long long)i * 2 * K * (chunk ? 2 : 1), *B = F + KF;
+  const SegRec *B = F + KF;  // F: this singleton's records
   bool good = true;
   dd Ssum = dd_from(0.0), Tsum = dd_from(0.0), dr = dd_from(0.0), tr = dd_from(0.0);
   int c = 0;
@@ -815,10 +829,14 @@ __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restri
 __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
                              RqiState *st, int K, int bal, int chunk, const SegRec *__restrict__ rec, double *W,
                              ZMeta *zmeta, int *diag_depth, double *fin_lo, double *fin_hi, long long *stats,
-                             int *nactive) {
+                             int *nactive, int stage) {
+  extern __shared__ uint4 recsm[];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int per = 2 * K * (chunk ? 2 : 1);  // records per singleton
+  const SegRec *F = stage ? reinterpret_cast<const SegRec *>(stage_recs(rec, per * (int)sizeof(SegRec), ns, recsm))
+                          : rec + (long long)i * per;
   FsInc inc = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  if (i < ns) fixed_step_body(i, sg, reps, st, K, bal, chunk, rec, W, zmeta, diag_depth, fin_lo, fin_hi, inc);
+  if (i < ns) fixed_step_body(i, sg, reps, st, K, bal, chunk, F, W, zmeta, diag_depth, fin_lo, fin_hi, inc);
   const unsigned fm = 0xffffffffu;
   const unsigned nact = __reduce_add_sync(fm, inc.nact), wide = __reduce_add_sync(fm, inc.wide);
   const unsigned hof = __reduce_add_sync(fm, inc.hofixed), hor = __reduce_add_sync(fm, inc.horqc);

@@ -29,7 +29,8 @@ __global__ void k_build_q(const RepDesc *__restrict__ reps, const int *__restric
   if (R.nb < 2) return;
   const YElt *y = my + R.off;
   QElt *q = mq + R.off;
-  for (int i = threadIdx.x; i < R.nb; i += blockDim.x) {
+  // blockIdx.y splits the rows (a representation's rows are independent here)
+  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < R.nb; i += blockDim.x * gridDim.y) {
     dd d = ld_d(y + i), dl = ld_dl(y + i), dll = ld_dll(y + i);
     dd c2 = dd_mul(dl, dl);
     dd gf = (i < R.nb - 1) ? dd_add(ld_d(y + i + 1), dll) : dd_from(0.0);

@@ -109,6 +109,8 @@ struct mrrr_ctx {
   bool zw_chunk = true;        // k_zwrite_chunk (chunked products, staged tiles) instead of the per-row warp scan
   int segy_k = 8, segy_w = 128;  // segmented y-NegCount (MRRR_SEGYK=1: unsegmented)
   int segx_k = 1, segx_w = 128;  // segmented many-representation x-NegCount (MRRR_SEGXK=8: on; no gain on C3/C4, slower on C1)
+  bool stage_attr = false, rec_stage = false;  // record staging in shared memory (MRRR_RECSTAGE=1; slower on C2)
+  size_t stage_lim = 0;
   long long seg_ch2 = 0;  // segmented rounds with at most this many chains run two chains per thread (slower on C2)
   long long seg_threads = 0;  // adaptive segment count: target threads per segmented round (0: off; no gain measured)
   bool dev_stable = true;      // device-driven rounds once every node holds one index (exact grids)
@@ -425,6 +427,21 @@ void run_bisection_guided(mrrr_t h, int nnode, double *out_lo, double *out_hi, d
 }
 
 __global__ void k_set_int(int *p, int v) { *p = v; }
+
+// dynamic shared memory for the record-staging kernels (k_twist_pick2, k_fixed_step): the bytes if they fit
+// the opt-in per-block limit (attributes raised once per handle), else 0 (the kernels then read global)
+size_t stage_bytes(mrrr_t h, size_t bytes) {
+  if (!h->stage_attr) {
+    int dev = 0, lim = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    h->stage_lim = (size_t)std::min(lim, 160 * 1024);
+    CK(cudaFuncSetAttribute(k_twist_pick2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->stage_lim));
+    CK(cudaFuncSetAttribute(k_fixed_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->stage_lim));
+    h->stage_attr = true;
+  }
+  return (h->rec_stage && bytes <= h->stage_lim) ? bytes : 0;
+}
 
 // Segmented rounds driven by device-side node counters: round r reads its node count from nn[r] and the
 // update writes nn[r+1], so batches of rounds are enqueued without a host round trip (kernels of empty
@@ -777,9 +794,9 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
               sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, KT, Wu, TFd, stride, trec);
           k_twist_lane_dd<true><<<nblocks_for((long long)KT * nb, 128), 128, 0, h->stream>>>(
               sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, KT, Wu, TFd, stride, trec);
-          k_twist_pick2<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs, KT,
-                                                                      nullptr, TFd, stride, trec, 0x1p-90,
-                                                                      h->stats.as<long long>());
+          k_twist_pick2<<<nblocks_for(nb, 32), 32, stage_bytes(h, 32 * 2 * KT * sizeof(TwRec)), h->stream>>>(
+              sgb, (int)nb, h->reps.as<RepDesc>(), rs, KT, nullptr, TFd, stride, trec, 0x1p-90,
+              h->stats.as<long long>(), stage_bytes(h, 32 * 2 * KT * sizeof(TwRec)) ? 1 : 0);
         } else if (h->tw2) {
           // twist search: forward lane stores d+, backward lane forms gamma and the per-chunk argmin
           const int KT = 2 * K;
@@ -788,9 +805,9 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
               sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, KT, Wu, TF, stride, trec);
           k_twist_lane<true><<<nblocks_for((long long)KT * nb, 128), 128, 0, h->stream>>>(
               sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, KT, Wu, TF, stride, trec);
-          k_twist_pick2<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs, KT, TF,
-                                                                      nullptr, stride, trec, 0x1p-46,
-                                                                      h->stats.as<long long>());
+          k_twist_pick2<<<nblocks_for(nb, 32), 32, stage_bytes(h, 32 * 2 * KT * sizeof(TwRec)), h->stream>>>(
+              sgb, (int)nb, h->reps.as<RepDesc>(), rs, KT, TF, nullptr, stride, trec, 0x1p-46,
+              h->stats.as<long long>(), stage_bytes(h, 32 * 2 * KT * sizeof(TwRec)) ? 1 : 0);
         } else {
           k_twist_seg<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
                                                                             h->mq.as<QElt>(), rs, K, Wu, TF, TB, stride,
@@ -809,11 +826,12 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
             k_fixed_seg<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
                                                                               h->mq.as<QElt>(), rs, K, Wu, P2s, nbmax,
                                                                               rec, h->rqi_bal ? 1 : 0);
-          k_fixed_step<<<nblocks_for(nb, 32), 32, 0, h->stream>>>(
+          const size_t fsb = stage_bytes(h, 32 * 2 * K * (h->rqi_chunk ? 2 : 1) * sizeof(SegRec));
+          k_fixed_step<<<nblocks_for(nb, 32), 32, fsb, h->stream>>>(
               sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, h->rqi_bal ? 1 : 0, h->rqi_chunk ? 1 : 0, rec, W,
               h->zmeta.as<ZMeta>(),
               diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
-              diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), h->cnt.as<int>() + C_NFB);
+              diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), h->cnt.as<int>() + C_NFB, fsb ? 1 : 0);
           launch_check(h);
           h->host_launches += 1;
           if (it == 0) continue;  // the RQC-only pass never finishes a singleton: no host check after it
@@ -959,7 +977,8 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
                                                            h->mx.as<double2>(), h->my.as<YElt>(), h->mq.as<QElt>(),
                                                            repbase, poolbase, (int)nbmax);
     launch_check(h);
-    k_build_q<<<nc, 256, 0, h->stream>>>(h->reps.as<RepDesc>(), nullptr, repbase, nc, h->my.as<YElt>(),
+    k_build_q<<<dim3(nc, (unsigned)std::min<long long>(64, std::max<long long>(1, (nbmax + 255) / 256 / std::max(1, nc / 148 + 1)))),
+                256, 0, h->stream>>>(h->reps.as<RepDesc>(), nullptr, repbase, nc, h->my.as<YElt>(),
                                          h->mq.as<QElt>());
     launch_check(h);
     // (e) child starts: segments and BNode offsets from the host copy
@@ -1138,7 +1157,8 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
                                      h->binfo.as<double>(), h->mx.as<double2>(), h->my.as<YElt>(),
                                      h->lscratch.as<double>(), h->reps.as<RepDesc>());
     launch_check(h);
-    k_build_q<<<nbl, 256, 0, st>>>(h->reps.as<RepDesc>(), h->blist.as<int>(), 0, nbl, h->my.as<YElt>(),
+    k_build_q<<<dim3(nbl, (unsigned)std::min<long long>(64, std::max<long long>(1, (n + 255) / 256 / std::max(1, nbl / 148 + 1)))),
+                256, 0, st>>>(h->reps.as<RepDesc>(), h->blist.as<int>(), 0, nbl, h->my.as<YElt>(),
                                    h->mq.as<QElt>());
     launch_check(h);
   }
@@ -1363,6 +1383,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_SEGCHILDMIN")) h->segchild_min = atoi(s);
     if (const char *s = getenv("MRRR_SEGTHREADS")) h->seg_threads = atoll(s);
     if (const char *s = getenv("MRRR_SEGCH2")) h->seg_ch2 = atoll(s);
+    if (const char *s = getenv("MRRR_RECSTAGE")) h->rec_stage = atoi(s) != 0;
     if (const char *s = getenv("MRRR_SEGYK")) h->segy_k = std::max(1, std::min(64, atoi(s)));
     if (const char *s = getenv("MRRR_SEGYW")) h->segy_w = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_SEGXK")) h->segx_k = std::max(1, std::min(64, atoi(s)));

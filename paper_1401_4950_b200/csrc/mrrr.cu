@@ -113,6 +113,7 @@ struct mrrr_ctx {
   size_t stage_lim = 0;
   long long seg_ch2 = 0;  // segmented rounds with at most this many chains run two chains per thread (slower on C2)
   long long seg_threads = 0;  // adaptive segment count: target threads per segmented round (0: off; no gain measured)
+  int dev_frac = 0;            // ... once the indices still sharing nodes are at most 1/dev_frac of the nodes (0: by n)
   bool dev_stable = true;      // device-driven rounds once every node holds one index (exact grids)
   int dev_rb = 16;            // rounds per device-driven batch
   bool dev_rounds = false;     // segmented rounds enqueued in batches on device-side counters (MRRR_DEVROUNDS=1;
@@ -678,7 +679,10 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
       run_rounds_device(h, cur, nxt, nnode, single_nb, std::max(nnode, h->max_nodes), out_lo, out_hi, rtol);
       return;
     }
-    if (!Y && seg_on && h->dev_stable && nnode > 0 && (long long)h->h_cnt[C_NMULTI] * 16 <= nnode) {
+    // the looser bound oversizes the grids by up to 1/frac: worth it while rounds are short (measured:
+    // frac 4 at n <= 16K, 16 for the long chains of n = 65536)
+    const int dfrac = h->dev_frac > 0 ? h->dev_frac : (single_nb <= 16384 ? 4 : 16);
+    if (!Y && seg_on && h->dev_stable && nnode > 0 && (long long)h->h_cnt[C_NMULTI] * dfrac <= nnode) {
       // near-stable phase: the node count can grow by at most the indices still sharing nodes (few), so
       // the remaining rounds run without host round trips on grids sized for that bound
       const long long maxn = (long long)nnode + h->h_cnt[C_NMULTI];
@@ -1369,6 +1373,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_SEGW")) h->seg_w = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_DEVROUNDS")) h->dev_rounds = atoi(s) != 0;
     if (const char *s = getenv("MRRR_DEVSTABLE")) h->dev_stable = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_DEVFRAC")) h->dev_frac = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_DEVRB")) h->dev_rb = std::max(1, std::min(64, atoi(s)));
     if (const char *s = getenv("MRRR_RQISEG")) h->rqi_seg = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQISEGK")) h->rqi_segk = std::max(1, std::min(64, atoi(s)));

@@ -112,7 +112,8 @@ struct mrrr_ctx {
   bool stage_attr = false, rec_stage = false;  // record staging in shared memory (MRRR_RECSTAGE=1; slower on C2)
   size_t stage_lim = 0;
   long long seg_ch2 = 0;  // segmented rounds with at most this many chains run two chains per thread (slower on C2)
-  long long seg_threads = 0;  // adaptive segment count: target threads per segmented round (0: off; no gain measured)
+  long long seg_threads = 0;       // adaptive segment count: more segments while a round has fewer threads (0: off)
+  int seg_minlen = 4096;           // ... and the segments stay this long (only long chains: a rank's C5a shard)
   int dev_frac = 0;            // ... once the indices still sharing nodes are at most 1/dev_frac of the nodes (0: by n)
   bool dev_stable = true;      // device-driven rounds once every node holds one index (exact grids)
   int dev_rb = 16;            // rounds per device-driven batch
@@ -614,7 +615,9 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
       // seg_threads threads keep the SMs busy (a round is latency-bound below that)
       const long long tot = nch + nex;
       int K = h->seg_k;
-      while (2 * K <= 64 && tot * 2 * K <= h->seg_threads && (single_nb - 1) >= 2 * (2 * K) * h->seg_w) K *= 2;
+      while (2 * K <= 64 && tot * 2 * K <= h->seg_threads && (single_nb - 1) >= 2 * (2 * K) * h->seg_w &&
+             (single_nb - 1) / (2 * K) >= h->seg_minlen)
+        K *= 2;
       const int L = (single_nb - 1 + K - 1) / K;
       CK(h->segout.ensure(sizeof(SegOut) * tot * K));
       CK(h->segfb.ensure(sizeof(int4) * tot));
@@ -1387,6 +1390,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_RQISEGCHILD")) h->rqi_seg_child = atoi(s) != 0;
     if (const char *s = getenv("MRRR_SEGCHILDMIN")) h->segchild_min = atoi(s);
     if (const char *s = getenv("MRRR_SEGTHREADS")) h->seg_threads = atoll(s);
+    if (const char *s = getenv("MRRR_SEGMINLEN")) h->seg_minlen = atoi(s);
     if (const char *s = getenv("MRRR_SEGCH2")) h->seg_ch2 = atoll(s);
     if (const char *s = getenv("MRRR_RECSTAGE")) h->rec_stage = atoi(s) != 0;
     if (const char *s = getenv("MRRR_SEGYK")) h->segy_k = std::max(1, std::min(64, atoi(s)));

@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(128) k_negcount_grp(const Node *__restrict__ n
 // records s_out.  k_seg_combine accepts segment k only if s_in(k) equals, bit for bit, s_out(k-1) of an
 // accepted predecessor -- then every operation of the segment was applied to the same operands as in the
 // sequential recurrence, and its count is exact.  A chain with a mismatch (or a division that left the
-// fast range) is finished by k_seg_fallback from the last exact state with the IEEE operations.
+// fast range) is finished from the last exact state with the IEEE operations (seg_chain_count).
 // The count is therefore identical to the sequential NegCount in every case; only the latency changes
 // (rows per lane: (nb-1)/K + W instead of nb-1).
 // ---------------------------------------------------------------------------
@@ -448,39 +448,6 @@ __global__ void k_seg_round(int nnode, int m, int K, const SegOut *__restrict__ 
     bisect_update_body((id << m) + p, nodes, nnode, m, counts, next, nnext, out_lo, out_hi, rtol, alg, nmulti);
 }
 
-// careful sequential tail from segment k's first row with the last exact state
-__global__ void k_seg_fallback(const int4 *__restrict__ fb, const int *__restrict__ nfb, const double *__restrict__ fb_s,
-                               const Node *__restrict__ nodes, int nnode, int m, const ExplicitChain *__restrict__ ex,
-                               const RepDesc *__restrict__ reps, const double2 *__restrict__ mx, int L, int *counts,
-                               int *excounts, const int *__restrict__ dnn, int mmax, long long target) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= *nfb) return;
-  if (dnn) {
-    nnode = *dnn;
-    m = round_m(nnode, mmax, target);
-  }
-  const int4 f = fb[i];
-  const long long c = (long long)f.x | ((long long)f.w << 31);
-  const long long nn = (long long)nnode * ((1 << m) - 1);
-  double sig;
-  int rep;
-  chain_of(nodes, m, nn, ex, c, sig, rep);
-  const RepDesc R = reps[rep];
-  const double2 *M = mx + R.off;
-  const int nb = R.nb;
-  double s = fb_s[i];
-  int cnt = f.z;
-  for (int r = min(f.y * L, nb - 1); r < nb - 1; r++) {
-    const double2 mm = M[r];
-    const double dp = __dadd_rn(mm.x, s);
-    const double q = (isinf(s) && isinf(dp)) ? 1.0 : __ddiv_rn(s, dp);
-    s = __dsub_rn(__dmul_rn(q, mm.y), sig);
-    cnt += sbx(dp);
-  }
-  cnt += sbx(__dadd_rn(M[nb - 1].x, s));
-  if (c < nn) counts[c] = cnt;
-  else excounts[c - nn] = cnt;
-}
 
 // ---------------------------------------------------------------------------
 // Segmented y-NegCount (q-form, dd): thread (segment k, chain c) runs rows [bk, ek) of chain c after a

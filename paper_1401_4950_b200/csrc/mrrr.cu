@@ -128,7 +128,7 @@ struct mrrr_ctx {
   Buf starts, scal, binfo, bside, blist, cab, mx, my, mq, lscratch, reps, rlo, rhi, colmap, gstart;
   Buf nodesK, nodesP, offsP, dS, dG, dH;  // guided bisection rounds
   Buf repoff, repcur, repcta;             // representation-grouped rounds
-  Buf segout, segfb, segfbs, rnd;         // segmented NegCount; per-round device counters
+  Buf segout, rnd;                        // segmented NegCount; per-round device counters
   Buf segouty, segfby, segoutx;           // segmented y-NegCount / many-representation x-NegCount
   Buf rqst, rqrec, hand;                  // segmented RQI state, segment records, handed-over singletons
   std::vector<cudaEvent_t> rev;           // events around device-driven rounds
@@ -461,8 +461,6 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
   CK(h->rnd.ensure(sizeof(int) * 2 * (MAXR + 2)));
   CK(h->counts.ensure(sizeof(int) * maxch));
   CK(h->segout.ensure(sizeof(SegOut) * maxch * K));
-  CK(h->segfb.ensure(sizeof(int4) * maxch));
-  CK(h->segfbs.ensure(sizeof(double) * maxch));
   while ((int)h->rev.size() < 2 * MAXR) {
     cudaEvent_t e;
     CK(cudaEventCreate(&e));
@@ -484,7 +482,7 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
       for (int b = 0; b < RB; b++) bound = std::min<long long>(2 * bound, maxnodes);
     const long long chmax = mcap > 0 ? maxch : std::min<long long>(maxch, std::max<long long>(bound, h->target_chains) + 128);
     const unsigned gseg = (unsigned)((chmax / 128 + 1) * K);
-    const unsigned g1 = (unsigned)(chmax / 128 + 1), g2 = (unsigned)(2 * chmax / 128 + 1);
+    const unsigned g1 = (unsigned)(chmax / 128 + 1);
     for (int b = 0; b < RB && r < MAXR; b++, r++) {
       Node *in = (r & 1) ? nxt : cur, *out = (r & 1) ? cur : nxt;
       CK(cudaEventRecord(h->rev[2 * r], h->stream));
@@ -620,8 +618,6 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
         K *= 2;
       const int L = (single_nb - 1 + K - 1) / K;
       CK(h->segout.ensure(sizeof(SegOut) * tot * K));
-      CK(h->segfb.ensure(sizeof(int4) * tot));
-      CK(h->segfbs.ensure(sizeof(double) * tot));
       const int CH = (tot <= h->seg_ch2) ? 2 : 1;  // few chains: two per thread (ILP)
       const unsigned grid = (unsigned)((tot + 128 * CH - 1) / (128 * CH) * K);
       if (CH == 2)
@@ -1586,7 +1582,7 @@ int mrrr_destroy(mrrr_t h) {
   if (!h) return 0;
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->stream);
-  Buf *bufs[] = {&h->starts, &h->scal, &h->binfo, &h->bside, &h->blist, &h->cab, &h->mx, &h->my, &h->mq, &h->nodesK, &h->nodesP, &h->offsP, &h->dS, &h->dG, &h->dH, &h->repoff, &h->repcur, &h->repcta, &h->segout, &h->segfb, &h->segfbs, &h->rnd, &h->rqst, &h->rqrec, &h->hand, &h->lscratch,
+  Buf *bufs[] = {&h->starts, &h->scal, &h->binfo, &h->bside, &h->blist, &h->cab, &h->mx, &h->my, &h->mq, &h->nodesK, &h->nodesP, &h->offsP, &h->dS, &h->dG, &h->dH, &h->repoff, &h->repcur, &h->repcta, &h->segout, &h->rnd, &h->rqst, &h->rqrec, &h->hand, &h->lscratch,
                  &h->reps, &h->rlo, &h->rhi, &h->colmap, &h->gstart, &h->nodesA, &h->nodesB, &h->counts, &h->ex,
                  &h->excounts, &h->exmap, &h->bnA, &h->bnB, &h->sing, &h->clusA, &h->clusB, &h->ss, &h->gval,
                  &h->valid, &h->cseg, &h->bnoff, &h->ipool_lo, &h->ipool_hi, &h->yref_lo, &h->yref_hi, &h->wsA,

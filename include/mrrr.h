@@ -47,6 +47,7 @@ typedef struct mrrr_ctx *mrrr_t;
 #define MRRR_ERR_NOMEM 3      /* device memory exhausted (workspace or outputs) */
 #define MRRR_ERR_ROOT 4       /* no definite root shift found (S3) */
 #define MRRR_ERR_NODEVICE 5   /* no CUDA device */
+#define MRRR_ERR_NCCL 6       /* NCCL missing (libnccl.so.2 not loadable) or an NCCL call failed */
 
 #define MRRR_KEEP_DIAG 1u     /* keep integer/interval diagnostics for mrrr_get_diag */
 
@@ -92,6 +93,27 @@ int mrrr_eig_host(mrrr_t h, const double *d, const double *e, int64_t n, int64_t
 int mrrr_eig_shard(mrrr_t h, const double *d, const double *e, int64_t n, int64_t sl, int64_t su,
                    double *W_local, double *Z_local, int64_t ldz, int64_t ncols_cap, int64_t *jlo,
                    int64_t *jhi);
+
+/* 128-byte NCCL unique id for mrrr_eig_dist: call on one rank, send the bytes to every rank (e.g. a
+ * torch.distributed broadcast), pass them to mrrr_eig_dist everywhere.  id128: caller-owned host buffer of
+ * 128 bytes.  Errors: -1 id128 NULL, MRRR_ERR_NCCL (libnccl.so.2 is opened at run time). */
+int mrrr_nccl_unique_id(void *id128);
+
+/* Multi-GPU solve, one process and one handle per GPU: rank `rank` of `world` takes the
+ * contiguous shard [sl, su] of [il, iu] with ceil(k / world) indices per rank (PMRRR's static division,
+ * P:4593-4599), computes the eigenpairs it owns exactly as mrrr_eig_shard does, then all-gathers the
+ * eigenvalue list over NCCL so that W[0..k-1] holds all k eigenvalues on every rank;
+ * Z_local (columns 0..*jhi-*jlo) holds the owned eigenvectors *jlo..*jhi (Z stays column-sharded).
+ * nccl_id: the same 128 bytes on every rank (mrrr_nccl_unique_id); the communicator is created on the
+ * first call and kept in the handle (recreated when the id, rank or world changes).  Every rank must
+ * call (the all-gather is collective) even if its shard is empty.  d, e, W, Z_local are device
+ * pointers as in mrrr_eig; W has k entries.  Errors: -2 nccl_id NULL, -3 rank out of [0, world),
+ * -4 world < 1, -5 d NULL, -6 e NULL (n > 1), -7 n < 1, -8 il, -9 iu, -10 W NULL, -11 Z_local NULL,
+ * -12 ldz < n, -14/-15 jlo/jhi NULL; MRRR_ERR_NOMEM if the owned count exceeds ncols_cap;
+ * MRRR_ERR_NCCL, MRRR_ERR_* otherwise. */
+int mrrr_eig_dist(mrrr_t h, const void *nccl_id, int32_t rank, int32_t world, const double *d, const double *e,
+                  int64_t n, int64_t il, int64_t iu, double *W, double *Z_local, int64_t ldz, int64_t ncols_cap,
+                  int64_t *jlo, int64_t *jhi);
 
 /* Host-only helper (no GPU needed): the ownership rule of mrrr_eig_shard (north_star
  * "a cluster straddling a shard boundary is owned by the GPU holding its first index").  gstart[j-1]

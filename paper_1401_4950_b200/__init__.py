@@ -71,15 +71,26 @@ def load() -> C.CDLL:
         L.mrrr_strerror.argtypes = [C.c_int]
         L.mrrr_strerror.restype = C.c_char_p
         L.mrrr_destroy.argtypes = [vp]
+        L.mrrr_nccl_unique_id.argtypes = [vp]
+        L.mrrr_eig_dist.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, i64, i64, i64, vp, vp, i64, i64,
+                                    C.POINTER(i64), C.POINTER(i64)]
         for f in ("mrrr_init", "mrrr_eig", "mrrr_eig_host", "mrrr_eig_shard", "mrrr_get_stats", "mrrr_get_times",
-                  "mrrr_get_diag", "mrrr_destroy"):
+                  "mrrr_get_diag", "mrrr_destroy", "mrrr_nccl_unique_id", "mrrr_eig_dist"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
 
 
 EXPORTED = ["mrrr_init", "mrrr_eig", "mrrr_eig_host", "mrrr_eig_shard", "mrrr_get_stats", "mrrr_get_diag",
-            "mrrr_get_times", "mrrr_selftest", "mrrr_shard_owner", "mrrr_strerror", "mrrr_destroy"]
+            "mrrr_get_times", "mrrr_selftest", "mrrr_shard_owner", "mrrr_strerror", "mrrr_destroy",
+            "mrrr_nccl_unique_id", "mrrr_eig_dist"]
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for :meth:`Solver.eig_dist` (create on one rank, send to all)."""
+    buf = C.create_string_buffer(128)
+    _check(load().mrrr_nccl_unique_id(buf), "mrrr_nccl_unique_id")
+    return buf.raw
 
 
 def selftest(which: int, n: int, seed: int = 1) -> int:
@@ -186,6 +197,27 @@ class Solver:
         m = max(jhi.value - jlo.value + 1, 0)
         self._last = (n, m)
         return jlo.value, jhi.value, W[:m], Zt[:m].T
+
+    def eig_dist(self, d, e, il: int, iu: int, nccl_id: bytes, rank: int, world: int,
+                 ncols_cap: int | None = None):
+        """Multi-GPU solve through libmrrr's own NCCL all-gather (mrrr_eig_dist): every rank gets all
+        k = iu - il + 1 eigenvalues in W and its owned eigenvectors; returns (jlo, jhi, W, Z_local)."""
+        import torch
+        n = d.numel()
+        k = iu - il + 1
+        per = -(-k // world)
+        cap = min(per * 2 + 64 if ncols_cap is None else ncols_cap, n)
+        W = torch.empty(k, dtype=torch.float64, device=d.device)
+        Zt = torch.empty((cap, n), dtype=torch.float64, device=d.device)
+        jlo, jhi = C.c_int64(), C.c_int64()
+        idb = C.create_string_buffer(bytes(nccl_id), 128)
+        rc = load().mrrr_eig_dist(self._h, idb, int(rank), int(world), d.data_ptr(),
+                                  e.data_ptr() if n > 1 else None, n, int(il), int(iu), W.data_ptr(),
+                                  Zt.data_ptr(), n, cap, C.byref(jlo), C.byref(jhi))
+        _check(rc, "mrrr_eig_dist")
+        m = max(jhi.value - jlo.value + 1, 0)
+        self._last = (n, m)
+        return jlo.value, jhi.value, W, Zt[:m].T
 
     # -------------------------------------------------------------- results
     def stats(self) -> dict:

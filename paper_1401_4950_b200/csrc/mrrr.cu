@@ -4,6 +4,8 @@
 // workspace, launches, and reads back small counters that size the next
 // launch (node / group / cluster counts).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl.so.2 is opened at run time (mrrr_eig_dist)
 
 #include <algorithm>
 #include <cmath>
@@ -23,6 +25,7 @@
 namespace {
 
 thread_local std::string g_last_cuda_error = "no error";
+thread_local std::string g_last_nccl_error = "no error";
 
 struct Buf {
   void *p = nullptr;
@@ -144,6 +147,10 @@ struct mrrr_ctx {
   std::vector<int> h_starts;
   cudaEvent_t ev[8];
   cudaEvent_t rq0, rq1;
+  ncclComm_t comm = nullptr;   // mrrr_eig_dist communicator (created on first use)
+  char comm_id[128] = {0};
+  int comm_rank = -1, comm_world = 0;
+  Buf dWl, dmeta, dmetas, dpad, dparts;  // mrrr_eig_dist staging
   double rqi_ms = 0, neg_ms = 0;
   long long neg_launches = 0, neg_len = 0;
   cudaEvent_t nc0, nc1;
@@ -1451,6 +1458,124 @@ int mrrr_eig_shard(mrrr_t h, const double *d, const double *e, int64_t n, int64_
   }
 }
 
+// NCCL, opened at run time (no link dependency: the process may already hold torch's libnccl.so.2)
+namespace {
+struct Nccl {
+  bool tried = false, ok = false;
+  ncclResult_t (*get_id)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*init_rank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_gather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*destroy)(ncclComm_t) = nullptr;
+  const char *(*err)(ncclResult_t) = nullptr;
+};
+Nccl &nccl() {
+  static Nccl N;
+  if (!N.tried) {
+    N.tried = true;
+    void *lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (lib) {
+      N.get_id = (decltype(N.get_id))dlsym(lib, "ncclGetUniqueId");
+      N.init_rank = (decltype(N.init_rank))dlsym(lib, "ncclCommInitRank");
+      N.all_gather = (decltype(N.all_gather))dlsym(lib, "ncclAllGather");
+      N.destroy = (decltype(N.destroy))dlsym(lib, "ncclCommDestroy");
+      N.err = (decltype(N.err))dlsym(lib, "ncclGetErrorString");
+      N.ok = N.get_id && N.init_rank && N.all_gather && N.destroy && N.err;
+    }
+    if (!N.ok) g_last_nccl_error = "libnccl.so.2 could not be loaded";
+  }
+  return N;
+}
+#define NK(x)                                                              \
+  do {                                                                     \
+    ncclResult_t r_ = (x);                                                 \
+    if (r_ != ncclSuccess) {                                               \
+      g_last_nccl_error = std::string(#x) + ": " + nccl().err(r_);         \
+      throw Err{MRRR_ERR_NCCL};                                            \
+    }                                                                      \
+  } while (0)
+}  // namespace
+
+int mrrr_nccl_unique_id(void *id128) {
+  if (!id128) return -1;
+  Nccl &N = nccl();
+  if (!N.ok) return MRRR_ERR_NCCL;
+  try {
+    ncclUniqueId id;
+    NK(N.get_id(&id));
+    memcpy(id128, id.internal, sizeof(id.internal));
+  } catch (Err &er) {
+    return er.code;
+  }
+  return 0;
+}
+
+int mrrr_eig_dist(mrrr_t h, const void *nccl_id, int32_t rank, int32_t world, const double *d, const double *e,
+                  int64_t n, int64_t il, int64_t iu, double *W, double *Z, int64_t ldz, int64_t ncols_cap,
+                  int64_t *jlo, int64_t *jhi) {
+  if (!h) return -1;
+  if (!nccl_id) return -2;
+  if (world < 1) return -4;
+  if (rank < 0 || rank >= world) return -3;
+  int a = check_args(d, e, n, il, iu, W, Z, ldz);
+  if (a) return a - 3;  // shift past nccl_id, rank, world
+  if (!jlo) return -14;
+  if (!jhi) return -15;
+  Nccl &N = nccl();
+  if (!N.ok) return MRRR_ERR_NCCL;
+  int rc = 0;
+  try {
+    CK(cudaSetDevice(h->device));
+    const long long k = iu - il + 1, per = (k + world - 1) / world;
+    const long long sl = il + (long long)rank * per, su = std::min<long long>(sl + per - 1, iu);
+    long long lo = su + 1, hi = su;
+    const long long cap = std::max<long long>(ncols_cap, 1);
+    CK(h->dWl.ensure(sizeof(double) * cap));
+    if (sl <= su) {
+      rc = solve(h, d, e, n, 1, n, h->dWl.as<double>(), Z, ldz, sl, su, &lo, &hi, ncols_cap);
+      if (rc != 0) { lo = su + 1; hi = su; }  // still joins the collective (with nothing)
+    }
+    *jlo = lo;
+    *jhi = hi;
+    // the communicator (kept while id, rank and world stay the same)
+    if (!h->comm || h->comm_rank != rank || h->comm_world != world || memcmp(h->comm_id, nccl_id, 128) != 0) {
+      if (h->comm) { N.destroy(h->comm); h->comm = nullptr; }
+      ncclUniqueId id;
+      memcpy(id.internal, nccl_id, 128);
+      NK(N.init_rank(&h->comm, world, id, rank));
+      memcpy(h->comm_id, nccl_id, 128);
+      h->comm_rank = rank;
+      h->comm_world = world;
+    }
+    // 1) every rank's (first owned index, count); 2) the padded eigenvalue lists; 3) scatter into W
+    const long long cnt = std::max<long long>(hi - lo + 1, 0);
+    long long meta_h[2] = {lo, cnt};
+    CK(h->dmeta.ensure(sizeof(long long) * 2));
+    CK(h->dmetas.ensure(sizeof(long long) * 2 * world));
+    CK(cudaMemcpyAsync(h->dmeta.p, meta_h, sizeof(meta_h), cudaMemcpyHostToDevice, h->stream));
+    NK(N.all_gather(h->dmeta.p, h->dmetas.p, 2, ncclInt64, h->comm, h->stream));
+    std::vector<long long> metas(2 * world);
+    CK(cudaMemcpyAsync(metas.data(), h->dmetas.p, sizeof(long long) * 2 * world, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    long long mcap = 1;
+    for (int r = 0; r < world; r++) mcap = std::max(mcap, metas[2 * r + 1]);
+    CK(h->dpad.ensure(sizeof(double) * mcap));
+    CK(h->dparts.ensure(sizeof(double) * mcap * world));
+    if (cnt) CK(cudaMemcpyAsync(h->dpad.p, h->dWl.p, sizeof(double) * cnt, cudaMemcpyDeviceToDevice, h->stream));
+    NK(N.all_gather(h->dpad.p, h->dparts.p, (size_t)mcap, ncclDouble, h->comm, h->stream));
+    for (int r = 0; r < world; r++) {
+      const long long rl = metas[2 * r], rc_ = metas[2 * r + 1];
+      if (rc_ > 0)
+        CK(cudaMemcpyAsync(W + (rl - il), h->dparts.as<double>() + (long long)r * mcap, sizeof(double) * rc_,
+                           cudaMemcpyDeviceToDevice, h->stream));
+    }
+    CK(cudaStreamSynchronize(h->stream));
+  } catch (Err &er) {
+    return er.code;
+  }
+  return rc;
+}
+
 int mrrr_shard_owner(const int32_t *gstart, int64_t n, int64_t sl, int64_t su, int64_t jmax, int64_t *jlo,
                      int64_t *jhi) {
   if (!gstart) return -1;
@@ -1574,6 +1699,7 @@ const char *mrrr_strerror(int code) {
     case MRRR_ERR_NOMEM: return "device memory exhausted";
     case MRRR_ERR_ROOT: return "no definite root representation found";
     case MRRR_ERR_NODEVICE: return "no CUDA device";
+    case MRRR_ERR_NCCL: return g_last_nccl_error.c_str();
     default: return code < 0 ? "invalid argument" : "unknown error";
   }
 }
@@ -1593,6 +1719,12 @@ int mrrr_destroy(mrrr_t h) {
   for (auto &ev : h->rev) cudaEventDestroy(ev);
   cudaEventDestroy(h->rq0);
   cudaEventDestroy(h->rq1);
+  if (h->comm && nccl().ok) nccl().destroy(h->comm);
+  h->dWl.release();
+  h->dmeta.release();
+  h->dmetas.release();
+  h->dpad.release();
+  h->dparts.release();
   if (h->h_cnt) cudaFreeHost(h->h_cnt);
   if (h->own_stream) cudaStreamDestroy(h->stream);
   delete h;

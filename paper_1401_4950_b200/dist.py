@@ -66,3 +66,13 @@ def allgather_eigenvalues(W_local, jlo: int, jhi: int, il: int, iu: int, group=N
         if cnt:
             W[lo - il:lo - il + cnt] = p[:cnt]
     return W
+
+
+def nccl_id_broadcast(group=None) -> bytes:
+    """The 128-byte NCCL id of :meth:`Solver.eig_dist`: created on rank 0 (libmrrr, run-time-loaded
+    libnccl) and sent to every rank over the torch.distributed group (any backend)."""
+    import torch.distributed as dist
+    from . import nccl_unique_id
+    box = [nccl_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    return box[0]

@@ -66,3 +66,21 @@ def test_oracle_and_product_share_no_code():
             txt = open(os.path.join(ROOT, "oracle", f)).read()
             assert "paper_1401_4950_b200" not in txt.replace("paper_1401_4950_b200/ (the product)", "") \
                 .replace("``paper_1401_4950_b200`` never", ""), f
+
+
+def test_eig_dist_argument_checks_and_nccl_id(lib_path):
+    # host-side checks of mrrr_eig_dist run before any device work; the NCCL id comes from the
+    # run-time-loaded libnccl (skipped if the image has none)
+    import ctypes as C
+    import paper_1401_4950_b200 as m
+    L = m.load()
+    jlo, jhi = C.c_int64(), C.c_int64()
+    idb = C.create_string_buffer(128)
+    # NULL handle, NULL id, bad rank, bad world
+    assert L.mrrr_eig_dist(None, idb, 0, 1, None, None, 4, 1, 4, None, None, 4, 4, C.byref(jlo), C.byref(jhi)) == -1
+    try:
+        ident = m.nccl_unique_id()
+    except m.MrrrError:
+        pytest.skip("libnccl.so.2 not loadable here")
+    assert len(ident) == 128 and ident != bytes(128)
+    assert L.mrrr_nccl_unique_id(None) == -1

@@ -320,3 +320,20 @@ def test_bisection_schedules_are_bit_identical(torch_cuda, env, monkeypatch):
         tn = max(abs(r.W[0]), abs(r.W[-1]))
         check_tol(d, e, g["W"], g["Z"], r.W, tn)
         g["solver"].close()
+
+
+@pytest.mark.gpu
+def test_eig_dist_single_rank_matches_full_solve(torch_cuda):
+    # mrrr_eig_dist with a one-rank NCCL communicator: the shard is the whole range, the all-gathered
+    # eigenvalue list and the owned vectors equal the plain solve bit for bit (same kernels, same order)
+    import paper_1401_4950_b200 as m
+    d, e = mi.random_tridiag(600, 41, -1.0)
+    dt, et = torch_cuda.from_numpy(d).cuda(), torch_cuda.from_numpy(e).cuda()
+    s = m.Solver()
+    W0, Z0 = s.eig(dt, et, 5, 560)
+    s2 = m.Solver()
+    jlo, jhi, W, Z = s2.eig_dist(dt, et, 5, 560, m.nccl_unique_id(), 0, 1)
+    torch_cuda.cuda.synchronize()
+    assert (jlo, jhi) == (5, 560)
+    assert torch_cuda.equal(W.cpu(), W0.cpu())
+    assert torch_cuda.equal(Z.cpu(), Z0.cpu())

@@ -41,7 +41,14 @@ def _worker(rank, world, port, n, il, iu, gstart, W_full, q):
         W = pd.allgather_eigenvalues(Wl, jlo, jhi, il, iu)
         ranges = [None] * world
         dist.all_gather_object(ranges, (sl, su, jlo, jhi))
-        q.put((rank, W.numpy(), ranges))
+        # the NCCL id of mrrr_eig_dist reaches every rank unchanged (None where libnccl is absent)
+        try:
+            ident = pd.nccl_id_broadcast()
+        except Exception:
+            ident = None
+        ids = [None] * world
+        dist.all_gather_object(ids, ident)
+        q.put((rank, W.numpy(), ranges, ids))
     finally:
         dist.destroy_process_group()
 
@@ -70,9 +77,12 @@ def _run(world, d, e, il=None, iu=None):
 def _check(gstart, W_full, out, il, iu):
     ranges = out[0][2]
     # every rank saw the same ranges and the same gathered list, equal to the full solve
-    for rank, W, rg in out:
+    for rank, W, rg, ids in out:
         assert rg == ranges
         np.testing.assert_array_equal(W, W_full)
+        # one NCCL id for all ranks (mrrr_eig_dist's communicator bootstrap)
+        assert all(x == ids[0] for x in ids)
+        assert ids[0] is None or len(ids[0]) == 128
     # owned ranges partition [il, iu] exactly, each starting at a group start and ending at a group end
     owned = [(jlo, jhi) for (_, _, jlo, jhi) in ranges if jhi >= jlo]
     assert owned[0][0] == il and owned[-1][1] == iu

@@ -696,3 +696,117 @@ __global__ void k_seg_fallback_xg(const FbX *__restrict__ fb, const int *__restr
   if (f.c < nn) counts[f.c] = cnt;
   else excounts[f.c - nn] = cnt;
 }
+
+// ---------------------------------------------------------------------------
+// Segmented shift attempts (Alg. spectrumshift step 3): the growth max|d+| of dstqds(M_y, tau) for every
+// (cluster, attempt, side) chain, split into K verified segments like the y-count (the fast q-form step
+// y_step is shared with dstqds_growth, so a verified chain gives its growth bit for bit); chains that do
+// not verify are recomputed whole by dstqds_growth.
+// ---------------------------------------------------------------------------
+struct SegG {
+  double in_hi, in_lo, out_hi, out_lo, gmax;
+  int ok, empty;
+};
+__device__ __forceinline__ double attempt_tau(const ShiftState &S, int a0, int ia, int side) {
+  double tau = side ? S.taur : S.taul;
+  for (int b = a0; b < a0 + ia; b++) tau = side ? __dadd_rn(tau, ldexp(S.offr, b)) : __dsub_rn(tau, ldexp(S.offl, b));
+  return tau;
+}
+__global__ void __launch_bounds__(128) k_clu_attempt_seg(const Cluster *__restrict__ cl, int ncl,
+                                                         const RepDesc *__restrict__ reps,
+                                                         const QElt *__restrict__ mq,
+                                                         const ShiftState *__restrict__ ss, int a0, int na, int K,
+                                                         int Wu, SegG *seg) {
+  const long long T = 2LL * na * ncl;
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= T * K) return;
+  const int k = (int)(g / T);
+  const long long t = g % T;
+  const int c = (int)(t / (2 * na)), ia = (int)((t >> 1) % na), side = (int)(t & 1);
+  const ShiftState S = ss[c];
+  SegG *o = seg + t * K + k;
+  if (S.done) {
+    o->empty = 1;
+    o->ok = 1;
+    return;
+  }
+  const dd tau = dd_from(attempt_tau(S, a0, ia, side));
+  const RepDesc R = reps[cl[c].rep];
+  const int nb = R.nb, steps = nb - 1;
+  int bk, ek, w0;
+  if (steps >= 2 * K * Wu) {
+    const int L = (steps + K - 1) / K;
+    bk = min(k * L, steps);
+    ek = min(bk + L, steps);
+    w0 = (k == 0) ? 0 : max(bk - Wu, 0);
+  } else {
+    if (k > 0) {
+      o->empty = 1;
+      o->ok = 1;
+      return;
+    }
+    bk = 0;
+    ek = steps;
+    w0 = 0;
+  }
+  const double2 *p = reinterpret_cast<const double2 *>(mq + R.off);
+  const double2 gb0 = __ldg(p + 4 * w0 + 3);
+  dd den = dd_sub(dd_make(gb0.x, gb0.y), tau);  // dstqds_growth's start (exact at row 0, a guess elsewhere)
+  dd din = den;
+  double gm = 0.0;
+  bool ok = true;
+  double2 c2n = __ldg(p + 4 * w0), gn = __ldg(p + 4 * w0 + 2);
+  for (int i = w0; i < ek; i++) {
+    const double2 c2v = c2n, gv = gn;
+    const int in = min(i + 1, nb - 1);
+    c2n = __ldg(p + 4 * in);
+    gn = __ldg(p + 4 * in + 2);
+    if (i == bk) din = den;
+    if (i >= bk) gm = dmaxd(gm, fabs(den.hi));
+    den = y_step(den, c2v, gv, tau, ok);
+  }
+  if (ek == steps) {
+    ok &= isfinite(den.hi) && isfinite(den.lo);
+    gm = dmaxd(gm, fabs(den.hi));
+  }
+  o->in_hi = din.hi;
+  o->in_lo = din.lo;
+  o->out_hi = den.hi;
+  o->out_lo = den.lo;
+  o->gmax = gm;
+  o->ok = ok ? 1 : 0;
+  o->empty = 0;
+}
+__global__ void k_clu_attempt_combine(const Cluster *__restrict__ cl, int ncl, const RepDesc *__restrict__ reps,
+                                      const YElt *__restrict__ my, const QElt *__restrict__ mq,
+                                      const ShiftState *__restrict__ ss, int a0, int na, int K,
+                                      const SegG *__restrict__ seg, double *gval, int *valid) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 2LL * na * ncl) return;
+  const int c = (int)(t / (2 * na)), ia = (int)((t >> 1) % na), side = (int)(t & 1);
+  const ShiftState S = ss[c];
+  if (S.done) return;
+  const SegG *R = seg + t * K;
+  double g = 0.0;
+  int prev = -1;
+  bool good = true;
+  for (int k = 0; k < K && good; k++) {
+    const SegG &a = R[k];
+    if (a.empty) continue;
+    good = a.ok != 0 && (prev < 0 || (__double_as_longlong(a.in_hi) == __double_as_longlong(R[prev].out_hi) &&
+                                      __double_as_longlong(a.in_lo) == __double_as_longlong(R[prev].out_lo)));
+    g = dmaxd(g, a.gmax);
+    prev = k;
+  }
+  if (good) {
+    gval[t] = g;
+    valid[t] = 1;
+    return;
+  }
+  const RepDesc Rp = reps[cl[c].rep];
+  double gg;
+  int v;
+  dstqds_growth(my + Rp.off, mq + Rp.off, Rp.nb, attempt_tau(S, a0, ia, side), gg, v);
+  gval[t] = gg;
+  valid[t] = v;
+}

@@ -132,7 +132,7 @@ struct mrrr_ctx {
   Buf nodesK, nodesP, offsP, dS, dG, dH;  // guided bisection rounds
   Buf repoff, repcur, repcta;             // representation-grouped rounds
   Buf segout, rnd;                        // segmented NegCount; per-round device counters
-  Buf segouty, segfby, segoutx;           // segmented y-NegCount / many-representation x-NegCount
+  Buf segouty, segfby, segoutx, segoutg;  // segmented y-NegCount / many-representation x-NegCount / growth
   Buf rqst, rqrec, hand;                  // segmented RQI state, segment records, handed-over singletons
   std::vector<cudaEvent_t> rev;           // events around device-driven rounds
   Buf nodesA, nodesB, counts, ex, excounts, exmap, bnA, bnB, sing, clusA, clusB, ss, gval, valid, cseg, bnoff,
@@ -970,9 +970,21 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
     for (int a0 = 0; a0 < MAX_ATTEMPTS;) {
       const int na = (a0 == 0) ? 1 : MAX_ATTEMPTS - a0;
       CK(cudaMemsetAsync(h->cnt.as<int>() + C_NDONE, 0, sizeof(int), h->stream));
-      k_clu_attempt_multi<<<nblocks_for(2LL * na * nc, 64), 64, 0, h->stream>>>(
-          cl, nc, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->mq.as<QElt>(), h->ss.as<ShiftState>(), a0, na,
-          h->gval.as<double>(), h->valid.as<int>());
+      if (h->segy_k > 1) {  // growth chains split into verified segments (latency: n/K + W rows per thread)
+        const int K = h->segy_k;
+        const long long T = 2LL * na * nc;
+        CK(h->segoutg.ensure(sizeof(SegG) * T * K));
+        k_clu_attempt_seg<<<nblocks_for(T * K, 128), 128, 0, h->stream>>>(
+            cl, nc, h->reps.as<RepDesc>(), h->mq.as<QElt>(), h->ss.as<ShiftState>(), a0, na, K, h->segy_w,
+            h->segoutg.as<SegG>());
+        k_clu_attempt_combine<<<nblocks_for(T, 64), 64, 0, h->stream>>>(
+            cl, nc, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->mq.as<QElt>(), h->ss.as<ShiftState>(), a0, na, K,
+            h->segoutg.as<SegG>(), h->gval.as<double>(), h->valid.as<int>());
+      } else {
+        k_clu_attempt_multi<<<nblocks_for(2LL * na * nc, 64), 64, 0, h->stream>>>(
+            cl, nc, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->mq.as<QElt>(), h->ss.as<ShiftState>(), a0, na,
+            h->gval.as<double>(), h->valid.as<int>());
+      }
       launch_check(h);
       k_clu_select_multi<<<nblocks_for(nc, 128), 128, 0, h->stream>>>(
           cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(), h->gval.as<double>(), h->valid.as<int>(), a0, na,
@@ -1708,7 +1720,7 @@ int mrrr_destroy(mrrr_t h) {
   if (!h) return 0;
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->stream);
-  Buf *bufs[] = {&h->starts, &h->scal, &h->binfo, &h->bside, &h->blist, &h->cab, &h->mx, &h->my, &h->mq, &h->nodesK, &h->nodesP, &h->offsP, &h->dS, &h->dG, &h->dH, &h->repoff, &h->repcur, &h->repcta, &h->segout, &h->rnd, &h->rqst, &h->rqrec, &h->hand, &h->lscratch,
+  Buf *bufs[] = {&h->starts, &h->scal, &h->binfo, &h->bside, &h->blist, &h->cab, &h->mx, &h->my, &h->mq, &h->nodesK, &h->nodesP, &h->offsP, &h->dS, &h->dG, &h->dH, &h->repoff, &h->repcur, &h->repcta, &h->segout, &h->rnd, &h->segouty, &h->segfby, &h->segoutx, &h->segoutg, &h->rqst, &h->rqrec, &h->hand, &h->lscratch,
                  &h->reps, &h->rlo, &h->rhi, &h->colmap, &h->gstart, &h->nodesA, &h->nodesB, &h->counts, &h->ex,
                  &h->excounts, &h->exmap, &h->bnA, &h->bnB, &h->sing, &h->clusA, &h->clusB, &h->ss, &h->gval,
                  &h->valid, &h->cseg, &h->bnoff, &h->ipool_lo, &h->ipool_hi, &h->yref_lo, &h->yref_hi, &h->wsA,

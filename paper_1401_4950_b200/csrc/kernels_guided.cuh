@@ -810,3 +810,97 @@ __global__ void k_clu_attempt_combine(const Cluster *__restrict__ cl, int ncl, c
   gval[t] = gg;
   valid[t] = v;
 }
+
+// Segmented child build (S8(d)): thread (segment k, cluster c) runs the fast pass of clu_build_one over rows
+// [bk, ek) after a warm-up and writes those child rows; k_clu_build_combine verifies the junctions and
+// rebuilds the clusters that do not verify whole (clu_build_one), so the child representation is bit for
+// bit the sequential one.  Records: SegG (gmax unused).
+__global__ void __launch_bounds__(128) k_clu_build_seg(const Cluster *__restrict__ cl, int ncl,
+                                                       const RepDesc *__restrict__ reps,
+                                                       const ShiftState *__restrict__ ss, double2 *mx, YElt *my,
+                                                       const QElt *__restrict__ mq, long long poolbase, int nbmax,
+                                                       int K, int Wu, SegG *seg) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (long long)ncl * K) return;
+  const int k = (int)(g / ncl), c = (int)(g % ncl);
+  const ShiftState S = ss[c];
+  SegG *o = seg + (long long)c * K + k;
+  if (!S.have_best) {
+    o->empty = 1;
+    o->ok = 1;
+    return;
+  }
+  const RepDesc P = reps[cl[c].rep];
+  const int nb = P.nb, steps = nb - 1;
+  int bk, ek, w0;
+  if (steps >= 2 * K * Wu) {
+    const int L = (steps + K - 1) / K;
+    bk = min(k * L, steps);
+    ek = min(bk + L, steps);
+    w0 = (k == 0) ? 0 : max(bk - Wu, 0);
+  } else {
+    if (k > 0) {
+      o->empty = 1;
+      o->ok = 1;
+      return;
+    }
+    bk = 0;
+    ek = steps;
+    w0 = 0;
+  }
+  const long long off = poolbase + (long long)c * nbmax;
+  YElt *yc = my + off;
+  double2 *xc = mx + off;
+  const dd tau = dd_from(S.best_tau);
+  const QElt *q = mq + P.off;
+  dd den = dd_sub(dd_make(__ldg(&q[w0].gb_hi), __ldg(&q[w0].gb_lo)), tau);
+  dd din = den;
+  bool ok = true;
+  for (int i = w0; i < bk; i++) den = clu_build_row(den, q, i, tau, nullptr, nullptr, ok);
+  din = den;
+  for (int i = bk; i < ek; i++) den = clu_build_row(den, q, i, tau, yc, xc, ok);
+  if (ek == steps) {
+    ok &= isfinite(den.hi) && isfinite(den.lo);
+    YElt e;
+    e.d_hi = den.hi; e.d_lo = den.lo; e.dl_hi = e.dl_lo = e.dll_hi = e.dll_lo = 0.0;
+    yc[nb - 1] = e;
+    xc[nb - 1] = make_double2(den.hi, 0.0);
+  }
+  o->in_hi = din.hi;
+  o->in_lo = din.lo;
+  o->out_hi = den.hi;
+  o->out_lo = den.lo;
+  o->ok = ok ? 1 : 0;
+  o->empty = 0;
+}
+__global__ void k_clu_build_combine(const Cluster *__restrict__ cl, int ncl, RepDesc *reps,
+                                    const ShiftState *__restrict__ ss, double2 *mx, YElt *my,
+                                    const QElt *__restrict__ mq, int repbase, long long poolbase, int nbmax, int K,
+                                    const SegG *__restrict__ seg, int *nfb) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncl) return;
+  const ShiftState S = ss[c];
+  bool good = S.have_best;
+  const SegG *R = seg + (long long)c * K;
+  int prev = -1;
+  for (int k = 0; k < K && good; k++) {
+    const SegG &a = R[k];
+    if (a.empty) continue;
+    good = a.ok != 0 && (prev < 0 || (__double_as_longlong(a.in_hi) == __double_as_longlong(R[prev].out_hi) &&
+                                      __double_as_longlong(a.in_lo) == __double_as_longlong(R[prev].out_lo)));
+    prev = k;
+  }
+  if (good) {  // rows are in place: the representation descriptor (as clu_build_one writes it)
+    const RepDesc P = reps[cl[c].rep];
+    RepDesc Rc = P;
+    Rc.off = poolbase + (long long)c * nbmax;
+    Rc.depth = P.depth + 1;
+    const dd sig = dd_add_d(dd_make(P.sig_hi, P.sig_lo), S.best_tau);
+    Rc.sig_hi = sig.hi;
+    Rc.sig_lo = sig.lo;
+    reps[repbase + c] = Rc;
+    return;
+  }
+  if (S.have_best) atomicAdd(nfb, 1);
+  clu_build_one(c, cl, reps, ss, mx, my, mq, repbase, poolbase, nbmax);  // whole (also the failed-shift case)
+}

@@ -270,11 +270,51 @@ __global__ void k_clu_select(const Cluster *__restrict__ cl, int ncl, const RepD
 
 // S8(d): child representation M_y = (d+, l+) of dstqds(M_y, tau_best) and its x copy.
 // Child rep id = repbase + c, data at pool offset poolbase + c * nbmax.
+// one row of the fast child build: l+(i) = dl(i)/d+(i) and c2(i)/d+(i) from the reciprocal pair of d+(i),
+// the child's y-row (d, dl, dll) and x-row (d, dll); returns d+(i+1) (the y_step recurrence)
+__device__ __forceinline__ dd clu_build_row(dd den, const QElt *__restrict__ q, int i, dd tau, YElt *yc, double2 *xc,
+                                            bool &ok) {
+  const double b = den.hi;
+  ok &= (fabs(b) > 0x1p-1000) && (fabs(b) < 0x1p1000);
+  const double r = rcp_seed(b);
+  double ee = __fma_rn(-b, r, 1.0);
+  ee = __fma_rn(ee, ee, ee);
+  const double r1 = __fma_rn(r, ee, r);
+  const double e2 = __fma_rn(-b, r1, 1.0);
+  const double r2 = __fma_rn(r1, e2, r1);
+  const dd dlp = dd_make(__ldg(&q[i].dl_hi), __ldg(&q[i].dl_lo));
+  const dd c2 = dd_make(__ldg(&q[i].c2_hi), __ldg(&q[i].c2_lo));
+  double h = __dmul_rn(dlp.hi, r1), t = __fma_rn(-h, b, dlp.hi);
+  t = __fma_rn(-h, den.lo, __dadd_rn(t, dlp.lo));
+  const dd out = fast_two_sum(h, __dmul_rn(t, r2));  // l+(i) = dl(i) / d+(i)
+  h = __dmul_rn(c2.hi, r1);
+  t = __fma_rn(-h, b, c2.hi);
+  t = __fma_rn(-h, den.lo, __dadd_rn(t, c2.lo));
+  const dd Pq = dd_make(h, __dmul_rn(t, r2));        // c2(i) / d+(i)
+  if (yc) {
+    const dd dl = dd_mul(den, out);
+    const dd dll = dd_mul(dl, out);
+    YElt e;
+    e.d_hi = den.hi; e.d_lo = den.lo; e.dl_hi = dl.hi; e.dl_lo = dl.lo; e.dll_hi = dll.hi; e.dll_lo = dll.lo;
+    yc[i] = e;
+    const double dx = den.hi, lx = out.hi;
+    xc[i] = make_double2(dx, __dmul_rn(__dmul_rn(dx, lx), lx));
+  }
+  return dd_sub_nf(dd_sub_nf(dd_make(__ldg(&q[i].gf_hi), __ldg(&q[i].gf_lo)), tau), Pq);
+}
+__device__ void clu_build_one(int c, const Cluster *__restrict__ cl, RepDesc *reps, const ShiftState *__restrict__ ss,
+                              double2 *mx, YElt *my, const QElt *__restrict__ mq, int repbase, long long poolbase,
+                              int nbmax);
 __global__ void k_clu_build(const Cluster *__restrict__ cl, int ncl, RepDesc *reps, const ShiftState *__restrict__ ss,
                             double2 *mx, YElt *my, const QElt *__restrict__ mq, int repbase, long long poolbase,
                             int nbmax) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncl) return;
+  clu_build_one(c, cl, reps, ss, mx, my, mq, repbase, poolbase, nbmax);
+}
+__device__ void clu_build_one(int c, const Cluster *__restrict__ cl, RepDesc *reps, const ShiftState *__restrict__ ss,
+                              double2 *mx, YElt *my, const QElt *__restrict__ mq, int repbase, long long poolbase,
+                              int nbmax) {
   ShiftState S = ss[c];
   RepDesc P = reps[cl[c].rep];
   RepDesc R = P;
@@ -293,33 +333,7 @@ __global__ void k_clu_build(const Cluster *__restrict__ cl, int ncl, RepDesc *re
     const QElt *q = mq + P.off;
     dd den = dd_sub(dd_make(__ldg(&q[0].gb_hi), __ldg(&q[0].gb_lo)), tau);
     bool ok = true;
-    for (int i = 0; i < P.nb - 1; i++) {
-      const double b = den.hi;
-      ok &= (fabs(b) > 0x1p-1000) && (fabs(b) < 0x1p1000);
-      const double r = rcp_seed(b);
-      double ee = __fma_rn(-b, r, 1.0);
-      ee = __fma_rn(ee, ee, ee);
-      const double r1 = __fma_rn(r, ee, r);
-      const double e2 = __fma_rn(-b, r1, 1.0);
-      const double r2 = __fma_rn(r1, e2, r1);
-      const dd dlp = dd_make(__ldg(&q[i].dl_hi), __ldg(&q[i].dl_lo));
-      const dd c2 = dd_make(__ldg(&q[i].c2_hi), __ldg(&q[i].c2_lo));
-      double h = __dmul_rn(dlp.hi, r1), t = __fma_rn(-h, b, dlp.hi);
-      t = __fma_rn(-h, den.lo, __dadd_rn(t, dlp.lo));
-      const dd out = fast_two_sum(h, __dmul_rn(t, r2));  // l+(i) = dl(i) / d+(i)
-      h = __dmul_rn(c2.hi, r1);
-      t = __fma_rn(-h, b, c2.hi);
-      t = __fma_rn(-h, den.lo, __dadd_rn(t, c2.lo));
-      const dd Pq = dd_make(h, __dmul_rn(t, r2));        // c2(i) / d+(i)
-      const dd dl = dd_mul(den, out);
-      const dd dll = dd_mul(dl, out);
-      YElt e;
-      e.d_hi = den.hi; e.d_lo = den.lo; e.dl_hi = dl.hi; e.dl_lo = dl.lo; e.dll_hi = dll.hi; e.dll_lo = dll.lo;
-      yc[i] = e;
-      const double dx = den.hi, lx = out.hi;
-      xc[i] = make_double2(dx, __dmul_rn(__dmul_rn(dx, lx), lx));
-      den = dd_sub_nf(dd_sub_nf(dd_make(__ldg(&q[i].gf_hi), __ldg(&q[i].gf_lo)), tau), Pq);
-    }
+    for (int i = 0; i < P.nb - 1; i++) den = clu_build_row(den, q, i, tau, yc, xc, ok);
     ok &= isfinite(den.hi) && isfinite(den.lo);
     if (ok) {
       YElt e;

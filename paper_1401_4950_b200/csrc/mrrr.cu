@@ -995,9 +995,21 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
       a0 += na;
     }
     // (d) children
-    k_clu_build<<<nblocks_for(nc, 64), 64, 0, h->stream>>>(cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(),
-                                                           h->mx.as<double2>(), h->my.as<YElt>(), h->mq.as<QElt>(),
-                                                           repbase, poolbase, (int)nbmax);
+    if (h->segy_k > 1) {  // child rows built by verified segments (latency n/K + W rows per thread)
+      const int K = h->segy_k;
+      CK(h->segoutg.ensure(sizeof(SegG) * (long long)nc * K));
+      k_clu_build_seg<<<nblocks_for((long long)nc * K, 128), 128, 0, h->stream>>>(
+          cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(), h->mx.as<double2>(), h->my.as<YElt>(),
+          h->mq.as<QElt>(), poolbase, (int)nbmax, K, h->segy_w, h->segoutg.as<SegG>());
+      CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
+      k_clu_build_combine<<<nblocks_for(nc, 64), 64, 0, h->stream>>>(
+          cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(), h->mx.as<double2>(), h->my.as<YElt>(),
+          h->mq.as<QElt>(), repbase, poolbase, (int)nbmax, K, h->segoutg.as<SegG>(), h->cnt.as<int>() + C_NFB);
+    } else {
+      k_clu_build<<<nblocks_for(nc, 64), 64, 0, h->stream>>>(cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(),
+                                                             h->mx.as<double2>(), h->my.as<YElt>(), h->mq.as<QElt>(),
+                                                             repbase, poolbase, (int)nbmax);
+    }
     launch_check(h);
     k_build_q<<<dim3(nc, (unsigned)std::min<long long>(64, std::max<long long>(1, (nbmax + 255) / 256 / std::max(1, nc / 148 + 1)))),
                 256, 0, h->stream>>>(h->reps.as<RepDesc>(), nullptr, repbase, nc, h->my.as<YElt>(),

@@ -111,7 +111,8 @@ struct mrrr_ctx {
   bool rqi_bulk = true;        // k_fixed_chunk stores the factors by bulk copies of staged 8-row runs
   bool zw_chunk = true;        // k_zwrite_chunk (chunked products, staged tiles) instead of the per-row warp scan
   int segy_k = 8, segy_w = 128;  // segmented y-NegCount (MRRR_SEGYK=1: unsegmented)
-  int segx_k = 1, segx_w = 128;  // segmented many-representation x-NegCount (MRRR_SEGXK=8: on; no gain on C3/C4, slower on C1)
+  int segx_k = 8, segx_w = 128;  // segmented many-representation x-NegCount (child rounds with long chains)
+  long long cur_nbmax = 0;       // longest representation of the current child bisection (0: segx off)
   bool stage_attr = false, rec_stage = false;  // record staging in shared memory (MRRR_RECSTAGE=1; slower on C2)
   size_t stage_lim = 0;
   long long seg_ch2 = 0;  // segmented rounds with at most this many chains run two chains per thread (slower on C2)
@@ -297,7 +298,7 @@ template <bool Y>
 void launch_negcount(mrrr_t h, const Node *nodes, int nnode, int m, int nex, const Node *nodesP = nullptr,
                      int nP = 0, const int *offsP = nullptr, int nPc = 0, double rtol = 0.0) {
   long long tot = (long long)nnode * ((1LL << m) - 1) + nPc + nex;
-  if (!Y && nPc == 0 && h->segx_k > 1 && tot > 0) {
+  if (!Y && nPc == 0 && h->segx_k > 1 && tot > 0 && h->cur_nbmax >= 2LL * h->segx_k * h->segx_w) {
     // segmented x-count over many representations (kernels_guided.cuh), junctions verified bit-exact
     const int K = h->segx_k;
     CK(h->segoutx.ensure(sizeof(SegOutX) * tot * K));
@@ -542,7 +543,9 @@ void run_bisection_grouped(mrrr_t h, int nnode, double *out_lo, double *out_hi, 
     // few chains per representation (e.g. thousands of 2-clusters): a CTA per representation would run
     // latency-bound waves; then the per-thread kernel runs on the rep-sorted nodes (a warp's lanes share
     // one or two representations, so their row loads coalesce)
-    const bool per_cta = (long long)nnode * P >= 64LL * nrep;
+    // (long child chains: the segmented per-thread path instead, on the same rep-sorted nodes)
+    const bool per_cta = (long long)nnode * P >= 64LL * nrep &&
+                         !(h->segx_k > 1 && h->cur_nbmax >= 2LL * h->segx_k * h->segx_w);
     zero_counters(h);
     CK(cudaMemsetAsync(h->repoff.p, 0, sizeof(int) * (nrep + 1), h->stream));
     k_rep_hist<<<nblocks_for(nnode, 128), 128, 0, h->stream>>>(cur, nnode, rep0, h->repoff.as<int>());
@@ -1044,9 +1047,11 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
         cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(), h->cseg.as<long long>(), h->bnoff.as<long long>(), ilo,
         ihi, h->ipool_lo.as<double>(), h->ipool_hi.as<double>(), h->bnA.as<BNode>(), repbase);
     launch_check(h);
+    h->cur_nbmax = nbmax;  // chain-length hint for the segmented child counts
     int nrd = run_brackets<false>(h, (int)btot);
     run_bisection<false>(h, nrd, h->ipool_lo.as<double>(), h->ipool_hi.as<double>(), 1e-2 * h->gaptol, 0, nullptr, 0,
                          &dummy, repbase, nc);
+    h->cur_nbmax = 0;
     // (f) reclassify
     CK(h->sing.ensure(sizeof(Singleton) * std::max<long long>(btot, 1)));
     Buf NX;

@@ -304,7 +304,7 @@ def test_division_fast_path_is_ieee(torch_cuda):
                                  {"MRRR_RQISEGW": "16"}, {"MRRR_ZWCHUNK": "0"},
                                  {"MRRR_RQICHUNK": "0"}, {"MRRR_RQICHUNK": "1", "MRRR_RQISEGW": "16"},
                                  {"MRRR_RQIBULK": "0"}, {"MRRR_SEGCH2": "1000000"}, {"MRRR_SEGTHREADS": "262144"},
-                                 {"MRRR_SEGYK": "1"}, {"MRRR_SEGYW": "8"}, {"MRRR_SEGXK": "8"}, {"MRRR_SEGXK": "8", "MRRR_SEGXW": "8"},
+                                 {"MRRR_SEGYK": "1"}, {"MRRR_SEGYW": "8"}, {"MRRR_SEGXK": "1"}, {"MRRR_SEGXK": "8", "MRRR_SEGXW": "8"},
                                  {"MRRR_DEVSTABLE": "0"}, {"MRRR_DEVROUNDS": "1"}, {"MRRR_TW2": "0"},
                                  {"MRRR_TW2": "1", "MRRR_RQISEGW": "16"}, {"MRRR_RQISEGCHILD": "0"},
                                  {"MRRR_SEGCHILDMIN": "0"}, {"MRRR_RECSTAGE": "1"}])

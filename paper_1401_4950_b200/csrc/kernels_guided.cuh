@@ -685,13 +685,32 @@ __global__ void k_seg_fallback_xg(const FbX *__restrict__ fb, const int *__restr
   const int L = (steps >= 2 * K * Wu) ? (steps + K - 1) / K : steps;
   double s = f.s;
   int cnt = f.cnt;
-  for (int r = min(f.k * L, steps); r < steps; r++) {
-    const double2 mm = __ldg(M + r);
+  // the IEEE operations, with the verified division fast path where its range test passes (bit-identical);
+  // the child representation streams from HBM: PF rows in flight
+  constexpr int PF = 8;
+  const int r0 = min(f.k * L, steps);
+  double2 ring[PF];
+#pragma unroll
+  for (int u = 0; u < PF; u++) ring[u] = __ldg(M + min(r0 + u, nb - 1));
+  auto step = [&](double2 mm) {
     const double dp = __dadd_rn(mm.x, s);
-    const double q = (isinf(s) && isinf(dp)) ? 1.0 : __ddiv_rn(s, dp);
+    double q = div_fast_nocheck(s, dp);
+    if (!div_range_ok(s, dp, q)) q = (isinf(s) && isinf(dp)) ? 1.0 : __ddiv_rn(s, dp);
     s = __dsub_rn(__dmul_rn(q, mm.y), sig);
     cnt += sbx(dp);
+  };
+  int r = r0;
+  for (; r + PF <= steps; r += PF) {
+#pragma unroll
+    for (int u = 0; u < PF; u++) {
+      const double2 mm = ring[u];
+      ring[u] = __ldg(M + min(r + u + PF, nb - 1));
+      step(mm);
+    }
   }
+#pragma unroll
+  for (int u = 0; u < PF; u++)
+    if (r + u < steps) step(ring[u]);
   cnt += sbx(__dadd_rn(__ldg(M + nb - 1).x, s));
   if (f.c < nn) counts[f.c] = cnt;
   else excounts[f.c - nn] = cnt;

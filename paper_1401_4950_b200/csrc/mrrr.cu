@@ -133,6 +133,7 @@ struct mrrr_ctx {
   Buf nodesK, nodesP, offsP, dS, dG, dH;  // guided bisection rounds
   Buf repoff, repcur, repcta;             // representation-grouped rounds
   Buf segout, rnd;                        // segmented NegCount; per-round device counters
+  Buf gpart;                              // k_root_gersh partial bounds
   Buf segouty, segfby, segoutx, segoutg;  // segmented y-NegCount / many-representation x-NegCount / growth
   Buf rqst, rqrec, hand;                  // segmented RQI state, segment records, handed-over singletons
   std::vector<cudaEvent_t> rev;           // events around device-driven rounds
@@ -1192,10 +1193,26 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
 
   // S3 root
   if (nbl) {
+    // long blocks: the Gershgorin reduction and the representation rows over G CTAs per block (k_root
+    // keeps the serial chain)
+    const int G = n >= 32768 ? (int)std::min<long long>(64, n / 4096) : 0;
+    if (G > 1) {
+      CK(h->gpart.ensure(sizeof(double) * 2 * (size_t)nbl * G));
+      k_root_gersh<256><<<dim3(nbl, G), 256, 0, st>>>(d, e, h->starts.as<int>(), h->blist.as<int>(), G,
+                                                      h->gpart.as<double>());
+      launch_check(h);
+    }
     k_root<256><<<nbl, 256, 0, st>>>(d, e, n, h->starts.as<int>(), h->blist.as<int>(), h->bside.as<int>(), h->seed,
                                      h->binfo.as<double>(), h->mx.as<double2>(), h->my.as<YElt>(),
-                                     h->lscratch.as<double>(), h->reps.as<RepDesc>());
+                                     h->lscratch.as<double>(), h->reps.as<RepDesc>(),
+                                     G > 1 ? h->gpart.as<double>() : nullptr, G > 1 ? G : 0);
     launch_check(h);
+    if (G > 1) {
+      k_root_derive<256><<<dim3(nbl, G), 256, 0, st>>>(n, h->starts.as<int>(), h->blist.as<int>(), h->seed,
+                                                       h->binfo.as<double>(), h->mx.as<double2>(), h->my.as<YElt>(),
+                                                       h->lscratch.as<double>(), G);
+      launch_check(h);
+    }
     k_build_q<<<dim3(nbl, (unsigned)std::min<long long>(64, std::max<long long>(1, (n + 255) / 256 / std::max(1, nbl / 148 + 1)))),
                 256, 0, st>>>(h->reps.as<RepDesc>(), h->blist.as<int>(), 0, nbl, h->my.as<YElt>(),
                                    h->mq.as<QElt>());
@@ -1737,7 +1754,7 @@ int mrrr_destroy(mrrr_t h) {
   if (!h) return 0;
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->stream);
-  Buf *bufs[] = {&h->starts, &h->scal, &h->binfo, &h->bside, &h->blist, &h->cab, &h->mx, &h->my, &h->mq, &h->nodesK, &h->nodesP, &h->offsP, &h->dS, &h->dG, &h->dH, &h->repoff, &h->repcur, &h->repcta, &h->segout, &h->rnd, &h->segouty, &h->segfby, &h->segoutx, &h->segoutg, &h->rqst, &h->rqrec, &h->hand, &h->lscratch,
+  Buf *bufs[] = {&h->starts, &h->scal, &h->binfo, &h->bside, &h->blist, &h->cab, &h->mx, &h->my, &h->mq, &h->nodesK, &h->nodesP, &h->offsP, &h->dS, &h->dG, &h->dH, &h->repoff, &h->repcur, &h->repcta, &h->segout, &h->rnd, &h->gpart, &h->segouty, &h->segfby, &h->segoutx, &h->segoutg, &h->rqst, &h->rqrec, &h->hand, &h->lscratch,
                  &h->reps, &h->rlo, &h->rhi, &h->colmap, &h->gstart, &h->nodesA, &h->nodesB, &h->counts, &h->ex,
                  &h->excounts, &h->exmap, &h->bnA, &h->bnB, &h->sing, &h->clusA, &h->clusB, &h->ss, &h->gval,
                  &h->valid, &h->cseg, &h->bnoff, &h->ipool_lo, &h->ipool_hi, &h->yref_lo, &h->yref_hi, &h->wsA,

@@ -116,8 +116,8 @@ struct mrrr_ctx {
   bool stage_attr = false, rec_stage = false;  // record staging in shared memory (MRRR_RECSTAGE=1; slower on C2)
   size_t stage_lim = 0;
   long long seg_ch2 = 0;  // segmented rounds with at most this many chains run two chains per thread (slower on C2)
-  long long seg_threads = 0;       // adaptive segment count: more segments while a round has fewer threads (0: off)
-  int seg_minlen = 4096;           // ... and the segments stay this long (only long chains: a rank's C5a shard)
+  long long seg_threads = 131072;  // adaptive segment count: more segments while a round has fewer threads
+  int seg_minlen = 2048;           // ... and the segments stay this long (only long chains: a rank's C5a shard)
   int dev_frac = 0;            // ... once the indices still sharing nodes are at most 1/dev_frac of the nodes (0: by n)
   bool dev_stable = true;      // device-driven rounds once every node holds one index (exact grids)
   int dev_rb = 16;            // rounds per device-driven batch
@@ -462,11 +462,16 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
   // mcap > 0 (stable phase: every node holds one wanted index, so the node count can only shrink): the
   // k-section depth stays at most mcap, so every round has at most nnode * (2^mcap - 1) chains and the
   // grids are sized exactly (depth is free: the dyadic grid makes any schedule bit-identical)
-  const int K = h->seg_k, L = (nb - 1 + K - 1) / K;
   const int MAXR = 256, RB = h->dev_rb;
   const int mmax = mcap > 0 ? mcap : h->mmax;
   const long long maxch = mcap > 0 ? (long long)maxnodes * ((1LL << mcap) - 1)
                                    : std::max<long long>(h->target_chains, maxnodes) + 128;
+  // segments per chain: the host rounds' rule (more segments while the rounds have few chains)
+  int K = h->seg_k;
+  while (2 * K <= 64 && maxch * 2 * K <= h->seg_threads && (nb - 1) >= 2 * (2 * K) * h->seg_w &&
+         (nb - 1) / (2 * K) >= h->seg_minlen)
+    K *= 2;
+  const int L = (nb - 1 + K - 1) / K;
   CK(h->rnd.ensure(sizeof(int) * 2 * (MAXR + 2)));
   CK(h->counts.ensure(sizeof(int) * maxch));
   CK(h->segout.ensure(sizeof(SegOut) * maxch * K));

@@ -92,6 +92,7 @@ struct mrrr_ctx {
   uint32_t flags = 0;
   long long ws_limit = 0;
   long long target_chains = 16384;  // k-section budget per round, segmented root chains (C2: 1 level per round)
+  long long target_chains_small = 8192;  // ... when fewer than 4096 indices are wanted (a rank's shard)
   long long target_unseg = 65536;   // k-section budget per round of whole-length chains (C2 sweep: 3 levels)
   int mmax = 16;
   int chains_per_thread = 1;
@@ -1227,6 +1228,15 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
 
   // S5 root bisection
   const double rtol = 1e-2 * h->gaptol;
+  // k-section budget: few wanted indices (a rank's shard) -> the smaller budget (3 levels per round for
+  // ~1K nodes instead of 4: less speculation where the rounds are throughput-bound anyway)
+  const long long tc_saved = h->target_chains;
+  if (ncomp < 4096 && h->target_chains_small > 0) h->target_chains = std::min(h->target_chains, h->target_chains_small);
+  struct RestoreTC {
+    mrrr_t h;
+    long long v;
+    ~RestoreTC() { h->target_chains = v; }
+  } restore_tc{h, tc_saved};
   if (nbl) {
     long long cap = std::max<long long>(ncomp + 2, nbl);
     h->max_nodes = (int)cap;
@@ -1420,6 +1430,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     CK(cudaMemGetInfo(&fr, &tot));
     h->ws_limit = (o && o->ws_limit > 0) ? o->ws_limit : (long long)(0.6 * (double)fr);
     if (const char *s = getenv("MRRR_TARGET_CHAINS")) h->target_chains = atoll(s);
+    if (const char *s = getenv("MRRR_TARGET_SMALL")) h->target_chains_small = atoll(s);
     if (const char *s = getenv("MRRR_TARGET_UNSEG")) h->target_unseg = atoll(s);
     if (const char *s = getenv("MRRR_MMAX")) h->mmax = atoi(s);
     if (const char *s = getenv("MRRR_CH")) h->chains_per_thread = std::max(1, std::min(4, atoi(s)));

@@ -108,6 +108,7 @@ struct mrrr_ctx {
   bool rqi_chunk = true;       // chunk-major fixed passes (k_fixed_chunk) instead of lane-major (k_fixed_seg)
   bool rqi_seg_child = true;   // segmented RQI for child-frame singletons (dd twist search)
   int segchild_min = 8;        // ... when the level has at least this many singletons per child representation
+  long long twdd_root_max = 0;  // root blocks up to this size take the dd twist search (MRRR_TWDD_ROOT)
   bool tw2 = true;             // twist search in two passes storing only d+ (k_twist_lane, k_twist_pick2)
   bool rqi_bulk = true;        // k_fixed_chunk stores the factors by bulk copies of staged 8-row runs
   bool zw_chunk = true;        // k_zwrite_chunk (chunked products, staged tiles) instead of the per-row warp scan
@@ -805,7 +806,7 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
         RqiState *rs = h->rqst.as<RqiState>();
         SegRec *rec = h->rqrec.as<SegRec>();
         k_rqi3_init<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs);
-        if (child) {
+        if (child || nbmax <= h->twdd_root_max) {  // dd twist search: child frames, and short root blocks
           // child frames: the dd twist search (d+ in dd over the P0 plane)
           const int KT = 2 * K;
           TwRec *trec = reinterpret_cast<TwRec *>(rec);
@@ -1452,6 +1453,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_RQIBULK")) h->rqi_bulk = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQITHREADS")) h->rqi_threads = atoll(s);
     if (const char *s = getenv("MRRR_TW2")) h->tw2 = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_TWDD_ROOT")) h->twdd_root_max = atoll(s);
     if (const char *s = getenv("MRRR_RQISEGCHILD")) h->rqi_seg_child = atoi(s) != 0;
     if (const char *s = getenv("MRRR_SEGCHILDMIN")) h->segchild_min = atoi(s);
     if (const char *s = getenv("MRRR_SEGTHREADS")) h->seg_threads = atoll(s);

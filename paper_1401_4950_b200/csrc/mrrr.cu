@@ -92,6 +92,7 @@ struct mrrr_ctx {
   uint32_t flags = 0;
   long long ws_limit = 0;
   long long target_chains = 16384;  // k-section budget per round, segmented root chains (C2: 1 level per round)
+  long long target_y = 8192;    // k-section budget of the (segmented) y-count rounds (less speculation)
   long long target_chains_small = 8192;  // ... when fewer than 4096 indices are wanted (a rank's shard)
   long long target_unseg = 65536;   // k-section budget per round of whole-length chains (C2 sweep: 3 levels)
   int mmax = 16;
@@ -614,7 +615,7 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
   Node *cur = h->nodesA.as<Node>(), *nxt = h->nodesB.as<Node>();
   bool first = true;
   const bool seg_on = !Y && single_nb > 0 && h->neg_tma && h->seg_k > 1 && (single_nb - 1) >= 2 * h->seg_k * h->seg_w;
-  const long long target = seg_on ? h->target_chains : h->target_unseg;
+  const long long target = seg_on ? h->target_chains : (Y && h->segy_k > 1) ? h->target_y : h->target_unseg;
   while (nnode > 0) {
     int m = 1;
     while (m < h->mmax && (long long)nnode * ((1LL << (m + 1)) - 1) <= target) m++;
@@ -1432,6 +1433,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     h->ws_limit = (o && o->ws_limit > 0) ? o->ws_limit : (long long)(0.6 * (double)fr);
     if (const char *s = getenv("MRRR_TARGET_CHAINS")) h->target_chains = atoll(s);
     if (const char *s = getenv("MRRR_TARGET_SMALL")) h->target_chains_small = atoll(s);
+    if (const char *s = getenv("MRRR_TARGET_Y")) h->target_y = atoll(s);
     if (const char *s = getenv("MRRR_TARGET_UNSEG")) h->target_unseg = atoll(s);
     if (const char *s = getenv("MRRR_MMAX")) h->mmax = atoi(s);
     if (const char *s = getenv("MRRR_CH")) h->chains_per_thread = std::max(1, std::min(4, atoi(s)));

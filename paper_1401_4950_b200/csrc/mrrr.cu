@@ -94,7 +94,8 @@ struct mrrr_ctx {
   long long target_chains = 16384;  // k-section budget per round, segmented root chains (C2: 1 level per round)
   long long target_y = 8192;    // k-section budget of the (segmented) y-count rounds (less speculation)
   long long target_chains_small = 8192;  // ... when fewer than 4096 indices are wanted (a rank's shard)
-  long long target_unseg = 65536;   // k-section budget per round of whole-length chains (C2 sweep: 3 levels)
+  long long target_unseg = 32768;   // k-section budget per round of whole-length root chains (C1: 3-4 levels)
+  long long target_child = 8192;    // ... of child-frame rounds (less speculation on long child chains)
   int mmax = 16;
   int chains_per_thread = 1;
   bool neg_tma = true;  // x-NegCount with TMA-staged representation tiles (k_negcount_tma)
@@ -547,7 +548,7 @@ void run_bisection_grouped(mrrr_t h, int nnode, double *out_lo, double *out_hi, 
   while (nnode > 0) {
     CK(h->nodesK.ensure(sizeof(Node) * nnode));
     int m = 1;
-    while (m < h->mmax && (long long)nnode * ((1LL << (m + 1)) - 1) <= h->target_unseg) m++;
+    while (m < h->mmax && (long long)nnode * ((1LL << (m + 1)) - 1) <= h->target_child) m++;
     const long long P = (1LL << m) - 1;
     // few chains per representation (e.g. thousands of 2-clusters): a CTA per representation would run
     // latency-bound waves; then the per-thread kernel runs on the rep-sorted nodes (a warp's lanes share
@@ -615,7 +616,10 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
   Node *cur = h->nodesA.as<Node>(), *nxt = h->nodesB.as<Node>();
   bool first = true;
   const bool seg_on = !Y && single_nb > 0 && h->neg_tma && h->seg_k > 1 && (single_nb - 1) >= 2 * h->seg_k * h->seg_w;
-  const long long target = seg_on ? h->target_chains : (Y && h->segy_k > 1) ? h->target_y : h->target_unseg;
+  const long long target = seg_on ? h->target_chains
+                          : (Y && h->segy_k > 1) ? h->target_y
+                          : (rep0 >= 0) ? h->target_child
+                                        : h->target_unseg;
   while (nnode > 0) {
     int m = 1;
     while (m < h->mmax && (long long)nnode * ((1LL << (m + 1)) - 1) <= target) m++;
@@ -1435,6 +1439,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_TARGET_SMALL")) h->target_chains_small = atoll(s);
     if (const char *s = getenv("MRRR_TARGET_Y")) h->target_y = atoll(s);
     if (const char *s = getenv("MRRR_TARGET_UNSEG")) h->target_unseg = atoll(s);
+    if (const char *s = getenv("MRRR_TARGET_CHILD")) h->target_child = atoll(s);
     if (const char *s = getenv("MRRR_MMAX")) h->mmax = atoi(s);
     if (const char *s = getenv("MRRR_CH")) h->chains_per_thread = std::max(1, std::min(4, atoi(s)));
     if (const char *s = getenv("MRRR_NEGTMA")) h->neg_tma = atoi(s) != 0;

@@ -104,7 +104,7 @@ struct mrrr_ctx {
   bool grouped = true;  // child bisection with CTAs grouped by representation (k_negcount_grp)
   int seg_k = 8, seg_w = 128;  // segmented root NegCount: segments per chain, warm-up rows (k_negcount_seg)
   bool rqi_seg = true;         // segmented RQI passes (kernels_rqi3.cuh); MRRR_RQISEG=0: the two-lane kernel only
-  int rqi_segk = 8, rqi_segw = 192;
+  int rqi_segk = 8, rqi_segw = 0;  // rqi_segw 0: by frame length (128 up to 16K rows, else 192)
   long long rqi_threads = 131072;  // adaptive RQI segment count target (threads per segmented pass)
   bool rqi_bal = true;         // split a singleton's 2K segments between its lanes by length
   bool rqi_chunk = true;       // chunk-major fixed passes (k_fixed_chunk) instead of lane-major (k_fixed_seg)
@@ -800,7 +800,8 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
         // segments per lane: at least rqi_segk; more when the batch has few singletons (a rank's shard),
         // so that about rqi_threads threads run, as long as a chunk stays longer than the warm-up
         int K = h->rqi_segk;
-        const int Wu = h->rqi_segw;
+        // warm-up rows: 128 suffice up to n = 16K (no retries measured); longer frames get 192
+        const int Wu = h->rqi_segw > 0 ? h->rqi_segw : (nbmax <= 16384 ? 128 : 192);
         while (2 * K <= 32 && (long long)nb * 2 * (2 * K) <= h->rqi_threads && (nbmax - 1) >= 2 * (2 * K) * Wu) K *= 2;
         CK(h->rqst.ensure(sizeof(RqiState) * stride));
         CK(h->rqrec.ensure(sizeof(SegRec) * stride * 4 * K));  // chunk layout: 2K chunks x 2 lanes

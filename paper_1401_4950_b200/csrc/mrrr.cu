@@ -114,8 +114,8 @@ struct mrrr_ctx {
   bool tw2 = true;             // twist search in two passes storing only d+ (k_twist_lane, k_twist_pick2)
   bool rqi_bulk = true;        // k_fixed_chunk stores the factors by bulk copies of staged 8-row runs
   bool zw_chunk = true;        // k_zwrite_chunk (chunked products, staged tiles) instead of the per-row warp scan
-  int segy_k = 8, segy_w = 128;  // segmented y-NegCount (MRRR_SEGYK=1: unsegmented)
-  int segx_k = 8, segx_w = 128;  // segmented many-representation x-NegCount (child rounds with long chains)
+  int segy_k = 16, segy_w = 128;  // segmented y-NegCount, shift growth, child build (MRRR_SEGYK=1: unsegmented)
+  int segx_k = 16, segx_w = 128;  // segmented many-representation x-NegCount (child rounds with long chains)
   long long cur_nbmax = 0;       // longest representation of the current child bisection (0: segx off)
   bool stage_attr = false, rec_stage = false;  // record staging in shared memory (MRRR_RECSTAGE=1; slower on C2)
   size_t stage_lim = 0;
@@ -124,7 +124,7 @@ struct mrrr_ctx {
   int seg_minlen = 2048;           // ... and the segments stay this long (only long chains: a rank's C5a shard)
   int dev_frac = 0;            // ... once the indices still sharing nodes are at most 1/dev_frac of the nodes (0: by n)
   bool dev_stable = true;      // device-driven rounds once every node holds one index (exact grids)
-  int dev_rb = 16;            // rounds per device-driven batch
+  int dev_rb = 32;            // rounds per device-driven batch
   bool dev_rounds = false;     // segmented rounds enqueued in batches on device-side counters (MRRR_DEVROUNDS=1;
                                // slower on C2: the oversized early-exit grids cost more than the saved syncs)
   int max_nodes = 0;           // bound on live bisection nodes (indices in the computed set)  // tube point budgets: no estimate (4 full levels) / with estimate

@@ -124,7 +124,7 @@ struct mrrr_ctx {
   int seg_minlen = 2048;           // ... and the segments stay this long (only long chains: a rank's C5a shard)
   int dev_frac = 0;            // ... once the indices still sharing nodes are at most 1/dev_frac of the nodes (0: by n)
   bool dev_stable = true;      // device-driven rounds once every node holds one index (exact grids)
-  int dev_rb = 32;            // rounds per device-driven batch
+  int dev_rb = 16;            // rounds per device-driven batch (32: empty tail rounds cost a rank's short run)
   bool dev_rounds = false;     // segmented rounds enqueued in batches on device-side counters (MRRR_DEVROUNDS=1;
                                // slower on C2: the oversized early-exit grids cost more than the saved syncs)
   int max_nodes = 0;           // bound on live bisection nodes (indices in the computed set)  // tube point budgets: no estimate (4 full levels) / with estimate

@@ -432,9 +432,10 @@ constexpr int ZSTRIDE = 2 * ZG + 1;  // double2 per thread: two groups + pad (16
 // from HBM; the root's rows are L2-resident and shared, so no hint is issued there)
 constexpr int PFD = 16;
 __device__ __forceinline__ void l2_prefetch(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
-template <bool LIGHT>
+template <bool LIGHT, bool PF>
 __device__ __forceinline__ void seg_pass_t(const QElt *__restrict__ q, int nb, int isB, int t0, int t1, int tw,
-                                           dd lam, dd nlam, dd *P, SegRec *R, double2 *stg, bool pf) {
+                                           dd lam, dd nlam, dd *P, SegRec *R, double2 *stg) {
+  constexpr bool pf = PF;
   R->empty = 0;
   const int rs = isB ? nb - 1 - tw : tw, og = isB ? 3 : 2;
   dd den = dd_sub_nf(dd_make(__ldg(&q[rs].gb_hi), __ldg(&q[rs].gb_lo)), lam);
@@ -514,8 +515,13 @@ __device__ __forceinline__ void seg_pass_t(const QElt *__restrict__ q, int nb, i
 __device__ __forceinline__ void seg_pass(const QElt *__restrict__ q, int nb, int isB, int t0, int t1, int tw,
                                          bool light, dd lam, dd nlam, dd *P, SegRec *R, double2 *stg = nullptr,
                                          bool pf = false) {
-  if (light) seg_pass_t<true>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, nullptr, pf);
-  else seg_pass_t<false>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, stg, pf);
+  if (pf) {
+    if (light) seg_pass_t<true, true>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, nullptr);
+    else seg_pass_t<false, true>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, stg);
+  } else {
+    if (light) seg_pass_t<true, false>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, nullptr);
+    else seg_pass_t<false, false>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, stg);
+  }
 }
 
 __global__ void __launch_bounds__(128) k_fixed_seg(const Singleton *__restrict__ sg, int ns,

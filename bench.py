@@ -284,7 +284,7 @@ def main():
             launch_ms = tphase["negcount_ms_per_launch"]
             nl = tphase["negcount_launches"]
             f = fl.negcount_flops(stats, n, wdiv) / nl
-            cands.append(("k_negcount_seg (x-NegCount rounds: segmented root chains; child rounds k_negcount_tma/grp)",
+            cands.append(("k_negcount_seg (x-NegCount rounds: segmented root chains; child rounds k_negcount_seg_xg/tma)",
                           "k_negcount", launch_ms, f))
         if rq_n:
             launch_ms = rq_ms / rq_n

@@ -216,6 +216,8 @@ def main():
     if world > 1:
         sl, su = pd.shard_range(cfg.il, cfg.iu, world, rank)
         W = None
+        # mrrr_eig_dist bootstraps its own NCCL communicator from one id sent over the torch group
+        nccl_ident = pd.nccl_id_broadcast() if backend != "gloo" else None
     else:
         W = torch.empty(k, dtype=torch.float64, device=dev)
         Zt = torch.empty((k, n), dtype=torch.float64, device=dev)
@@ -225,10 +227,13 @@ def main():
         with torch.cuda.stream(stream):
             if world == 1:
                 solver.eig(d, e, cfg.il, cfg.iu, W=W, Z=Zt)
+            elif backend != "gloo":
+                # the C-ABI multi-GPU call: shard solve + the eigenvalue all-gather over NCCL inside libmrrr
+                # (the only collective); Z stays column-sharded
+                solver.eig_dist(d, e, cfg.il, cfg.iu, nccl_ident, rank, world)
             else:
-                jlo, jhi, Wl, Zl = solver.eig_shard(d, e, sl, su)
-                # eigenvalue list all-gather over NCCL: the only collective
-                pd.allgather_eigenvalues(Wl if backend != "gloo" else Wl.cpu(), jlo, jhi, cfg.il, cfg.iu)
+                jlo, jhi, Wl, Zl = solver.eig_shard(d, e, sl, su, cfg.il, cfg.iu)
+                pd.allgather_eigenvalues(Wl.cpu(), jlo, jhi, cfg.il, cfg.iu)
 
     for _ in range(args.warmup):
         step()

@@ -48,6 +48,7 @@ typedef struct mrrr_ctx *mrrr_t;
 #define MRRR_ERR_ROOT 4       /* no definite root shift found (S3) */
 #define MRRR_ERR_NODEVICE 5   /* no CUDA device */
 #define MRRR_ERR_NCCL 6       /* NCCL missing (libnccl.so.2 not loadable) or an NCCL call failed */
+#define MRRR_ERR_PEER 7       /* mrrr_eig_dist: this rank succeeded but another rank failed */
 
 #define MRRR_KEEP_DIAG 1u     /* keep integer/interval diagnostics for mrrr_get_diag */
 
@@ -81,17 +82,20 @@ int mrrr_eig(mrrr_t h, const double *d, const double *e, int64_t n, int64_t il, 
 int mrrr_eig_host(mrrr_t h, const double *d, const double *e, int64_t n, int64_t il, int64_t iu, double *W,
                   double *Z, int64_t ldz);
 
-/* Index-range shard of a multi-GPU solve (one process per GPU):
- * the shard is the contiguous range [sl, su] (1-based) of [il, iu]; every rank
- * builds the same root (bit-identical), bisects its shard plus guards, and
- * computes exactly the eigenpairs whose group (cluster) STARTS inside the
- * shard (a cluster straddling a shard boundary is owned by the rank holding
- * its first index).  On return [*jlo, *jhi] (1-based, *jhi < *jlo if empty) is
- * the owned range; W_local[0..] and columns of Z_local hold eigenpairs
- * *jlo..*jhi.  ncols_cap bounds the owned count (MRRR_ERR_NOMEM if exceeded,
- * with the needed range still returned).  Device pointers as in mrrr_eig. */
-int mrrr_eig_shard(mrrr_t h, const double *d, const double *e, int64_t n, int64_t sl, int64_t su,
-                   double *W_local, double *Z_local, int64_t ldz, int64_t ncols_cap, int64_t *jlo,
+/* Index-range shard of a multi-GPU solve (one process per GPU) of the selection
+ * [il, iu]: the rank's shard is the contiguous range [sl, su] (1-based, il <= sl <= su <= iu); every rank
+ * builds the same root (bit-identical: the root side follows the same rule on [il, iu] as mrrr_eig), bisects
+ * its shard plus guards, and computes exactly the eigenpairs of the units that START inside the shard.  A
+ * unit is a root group (singleton or cluster) cut to [il, iu]: a cluster straddling a shard
+ * boundary is owned by the rank holding its first index (north_star), a cluster straddling il is owned from
+ * il on by the rank holding il, and no owned range reaches past iu -- so the owned ranges of all ranks
+ * partition [il, iu] and every column equals the mrrr_eig(il, iu) column bit for bit.  On return
+ * [*jlo, *jhi] (1-based, *jhi < *jlo if empty) is the owned range; W_local[0..] and columns of Z_local hold
+ * eigenpairs *jlo..*jhi.  ncols_cap bounds the owned count (MRRR_ERR_NOMEM if exceeded, with the needed range
+ * still returned).  Device pointers as in mrrr_eig.  Errors: -2 d, -3 e, -4 n, -5 il, -6 iu, -7 sl out of
+ * [il, iu], -8 su out of [sl, iu], -9 W_local NULL, -10 Z_local NULL, -11 ldz < n, -13/-14 jlo/jhi NULL. */
+int mrrr_eig_shard(mrrr_t h, const double *d, const double *e, int64_t n, int64_t il, int64_t iu, int64_t sl,
+                   int64_t su, double *W_local, double *Z_local, int64_t ldz, int64_t ncols_cap, int64_t *jlo,
                    int64_t *jhi);
 
 /* 128-byte NCCL unique id for mrrr_eig_dist: call on one rank, send the bytes to every rank (e.g. a
@@ -106,11 +110,13 @@ int mrrr_nccl_unique_id(void *id128);
  * Z_local (columns 0..*jhi-*jlo) holds the owned eigenvectors *jlo..*jhi (Z stays column-sharded).
  * nccl_id: the same 128 bytes on every rank (mrrr_nccl_unique_id); the communicator is created on the
  * first call and kept in the handle (recreated when the id, rank or world changes).  Every rank must
- * call (the all-gather is collective) even if its shard is empty.  d, e, W, Z_local are device
+ * call (the all-gather is collective) even if its shard is empty.  A rank whose own solve fails (any
+ * code, including a CUDA error) still joins both all-gathers with an empty share and returns its code;
+ * the other ranks then return MRRR_ERR_PEER, so no rank waits forever.  d, e, W, Z_local are device
  * pointers as in mrrr_eig; W has k entries.  Errors: -2 nccl_id NULL, -3 rank out of [0, world),
  * -4 world < 1, -5 d NULL, -6 e NULL (n > 1), -7 n < 1, -8 il, -9 iu, -10 W NULL, -11 Z_local NULL,
  * -12 ldz < n, -14/-15 jlo/jhi NULL; MRRR_ERR_NOMEM if the owned count exceeds ncols_cap;
- * MRRR_ERR_NCCL, MRRR_ERR_* otherwise. */
+ * MRRR_ERR_PEER, MRRR_ERR_NCCL, MRRR_ERR_* otherwise. */
 int mrrr_eig_dist(mrrr_t h, const void *nccl_id, int32_t rank, int32_t world, const double *d, const double *e,
                   int64_t n, int64_t il, int64_t iu, double *W, double *Z_local, int64_t ldz, int64_t ncols_cap,
                   int64_t *jlo, int64_t *jhi);
@@ -118,14 +124,15 @@ int mrrr_eig_dist(mrrr_t h, const void *nccl_id, int32_t rank, int32_t world, co
 /* Host-only helper (no GPU needed): the ownership rule of mrrr_eig_shard (north_star
  * "a cluster straddling a shard boundary is owned by the GPU holding its first index").  gstart[j-1]
  * (host array, n entries, caller-owned) is 1 iff index j starts a root group (singleton or cluster,
- * P:3272-3292), 0 if j continues the group of j-1; only entries sl..jmax are read.  [sl, su] is the
- * rank's shard (1-based), jmax >= su the last classified index.  On return [*jlo, *jhi] is the owned
- * range: from the first group start in [sl, su] through the end of the last group starting there
- * (which may extend past su up to jmax); *jlo = su + 1, *jhi = su if no group starts in the shard.
- * Errors: -1 gstart NULL, -2 n < 1, -3 sl out of [1, n], -4 su out of [sl, n], -5 jmax out of [su, n],
- * -6/-7 jlo/jhi NULL. */
-int mrrr_shard_owner(const int32_t *gstart, int64_t n, int64_t sl, int64_t su, int64_t jmax, int64_t *jlo,
-                     int64_t *jhi);
+ * P:3272-3292), 0 if j continues the group of j-1; only entries sl..jmax are read.  [il, iu] is the
+ * selection, [sl, su] the rank's shard (1-based, il <= sl <= su <= iu), jmax >= su the last classified
+ * index.  Units start at every group start in [il, iu] and at il; on return [*jlo, *jhi] is the owned range:
+ * from the first unit start in [sl, su] through the end of the last unit starting there (which may extend
+ * past su up to min(jmax, iu)); *jlo = su + 1, *jhi = su if no unit starts in the shard.
+ * Errors: -1 gstart NULL, -2 n < 1, -3 il out of [1, n], -4 iu out of [il, n], -5 sl out of [il, iu],
+ * -6 su out of [sl, iu], -7 jmax out of [su, n], -8/-9 jlo/jhi NULL. */
+int mrrr_shard_owner(const int32_t *gstart, int64_t n, int64_t il, int64_t iu, int64_t sl, int64_t su,
+                     int64_t jmax, int64_t *jlo, int64_t *jhi);
 
 /* Statistics of the last call (int64 each, nstats <= MRRR_NSTATS):
  * 0 d_max, 1 #clusters processed, 2 largest cluster, 3 uncertified shifts

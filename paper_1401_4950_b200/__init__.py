@@ -60,11 +60,12 @@ def load() -> C.CDLL:
         L.mrrr_init.argtypes = [C.POINTER(vp), C.POINTER(_Opts)]
         L.mrrr_eig.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, i64]
         L.mrrr_eig_host.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, i64]
-        L.mrrr_eig_shard.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, i64, i64, C.POINTER(i64), C.POINTER(i64)]
+        L.mrrr_eig_shard.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, vp, vp, i64, i64, C.POINTER(i64),
+                                      C.POINTER(i64)]
         L.mrrr_get_stats.argtypes = [vp, vp, C.c_int32]
         L.mrrr_get_times.argtypes = [vp, vp, C.c_int32]
         L.mrrr_get_diag.argtypes = [vp, C.POINTER(_Diag)]
-        L.mrrr_shard_owner.argtypes = [vp, i64, i64, i64, i64, C.POINTER(i64), C.POINTER(i64)]
+        L.mrrr_shard_owner.argtypes = [vp, i64, i64, i64, i64, i64, i64, C.POINTER(i64), C.POINTER(i64)]
         L.mrrr_shard_owner.restype = C.c_int
         L.mrrr_selftest.argtypes = [C.c_int, i64, C.c_uint64, C.POINTER(i64)]
         L.mrrr_selftest.restype = C.c_int
@@ -182,17 +183,21 @@ class Solver:
         self._last = (n, k)
         return W, Zt.T
 
-    def eig_shard(self, d, e, sl: int, su: int, ncols_cap: int | None = None):
-        """Multi-GPU shard: eigenpairs of the groups that start in [sl, su]; returns (jlo, jhi, W, Z)."""
+    def eig_shard(self, d, e, sl: int, su: int, il: int | None = None, iu: int | None = None,
+                  ncols_cap: int | None = None):
+        """Multi-GPU shard [sl, su] of the selection [il, iu] (default all pairs): eigenpairs of the units
+        (root groups cut to [il, iu]) that start in [sl, su]; returns (jlo, jhi, W, Z)."""
         import torch
         n = d.numel()
+        il = 1 if il is None else int(il)
+        iu = n if iu is None else int(iu)
         cap = (su - sl + 1) * 2 + 64 if ncols_cap is None else ncols_cap
-        cap = min(cap, n)
+        cap = max(min(cap, iu - il + 1), 1)
         W = torch.empty(cap, dtype=torch.float64, device=d.device)
         Zt = torch.empty((cap, n), dtype=torch.float64, device=d.device)
         jlo, jhi = C.c_int64(), C.c_int64()
-        rc = load().mrrr_eig_shard(self._h, d.data_ptr(), e.data_ptr() if n > 1 else None, n, int(sl), int(su),
-                                   W.data_ptr(), Zt.data_ptr(), n, cap, C.byref(jlo), C.byref(jhi))
+        rc = load().mrrr_eig_shard(self._h, d.data_ptr(), e.data_ptr() if n > 1 else None, n, il, iu, int(sl),
+                                   int(su), W.data_ptr(), Zt.data_ptr(), n, cap, C.byref(jlo), C.byref(jhi))
         _check(rc, "mrrr_eig_shard")
         m = max(jhi.value - jlo.value + 1, 0)
         self._last = (n, m)
@@ -206,7 +211,7 @@ class Solver:
         n = d.numel()
         k = iu - il + 1
         per = -(-k // world)
-        cap = min(per * 2 + 64 if ncols_cap is None else ncols_cap, n)
+        cap = max(min(per * 2 + 64 if ncols_cap is None else ncols_cap, k), 1)
         W = torch.empty(k, dtype=torch.float64, device=d.device)
         Zt = torch.empty((cap, n), dtype=torch.float64, device=d.device)
         jlo, jhi = C.c_int64(), C.c_int64()

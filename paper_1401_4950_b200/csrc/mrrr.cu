@@ -1091,20 +1091,25 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
   }
 }
 
-// ownership rule of a multi-GPU shard: the rank owns every group that STARTS in
-// [sl, su]; the last such group may extend past su (through jmax, the end of the computed range).
-// gstart[j-1] = 1 iff index j starts a root group.  Empty ownership: jlo = su + 1, jhi = su.
-static void shard_owner(const int32_t *gstart, long long n, long long sl, long long su, long long jmax,
-                        long long *jlo_out, long long *jhi_out) {
+// ownership rule of a multi-GPU shard within the selection [il, iu]: an owned unit
+// starts at every root group start inside [il, iu] and at il itself (a group that begins before il
+// is cut there, as the 1-GPU solve cuts it with its column map); the rank owns every unit that
+// STARTS in its shard [sl, su], and the last such unit may extend past su (through min(jmax, iu),
+// jmax = the end of the computed range).  The owned ranges of the ranks therefore partition
+// [il, iu].  gstart[j-1] = 1 iff index j starts a root group.  Empty ownership: jlo = su + 1, jhi = su.
+static void shard_owner(const int32_t *gstart, long long n, long long il, long long iu, long long sl,
+                        long long su, long long jmax, long long *jlo_out, long long *jhi_out) {
   long long jlo = -1, jhi;
+  const long long jend = std::min(std::min(jmax, iu), n);
+  auto unit_start = [&](long long j) { return j == il || gstart[j - 1] == 1; };
   for (long long j = sl; j <= su; j++)
-    if (gstart[j - 1] == 1) { jlo = j; break; }
+    if (unit_start(j)) { jlo = j; break; }
   if (jlo > 0) {
     long long last = jlo;
     for (long long j = sl; j <= su; j++)
-      if (gstart[j - 1] == 1) last = j;
+      if (unit_start(j)) last = j;
     jhi = last;
-    while (jhi < jmax && jhi < n && gstart[jhi] == 0) jhi++;
+    while (jhi < jend && gstart[jhi] == 0) jhi++;
   } else {
     jlo = su + 1;
     jhi = su;
@@ -1330,7 +1335,7 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
     CK(cudaMemcpyAsync(gs.data(), h->gstart.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     long long jlo = 0, jhi = 0;
-    shard_owner(gs.data(), n, shard_lo, shard_hi, cab[1], &jlo, &jhi);
+    shard_owner(gs.data(), n, il, iu, shard_lo, shard_hi, cab[1], &jlo, &jhi);
     *jlo_out = jlo;
     *jhi_out = jhi;
     long long own = jhi - jlo + 1;
@@ -1512,16 +1517,19 @@ int mrrr_eig(mrrr_t h, const double *d, const double *e, int64_t n, int64_t il, 
   }
 }
 
-int mrrr_eig_shard(mrrr_t h, const double *d, const double *e, int64_t n, int64_t sl, int64_t su, double *W,
-                   double *Z, int64_t ldz, int64_t ncols_cap, int64_t *jlo, int64_t *jhi) {
+int mrrr_eig_shard(mrrr_t h, const double *d, const double *e, int64_t n, int64_t il, int64_t iu, int64_t sl,
+                   int64_t su, double *W, double *Z, int64_t ldz, int64_t ncols_cap, int64_t *jlo, int64_t *jhi) {
   if (!h) return -1;
-  int a = check_args(d, e, n, sl, su, W, Z, ldz);
-  if (a) return a;
-  if (!jlo || !jhi) return -11;
+  int a = check_args(d, e, n, il, iu, W, Z, ldz);
+  if (a) return (a <= -7) ? a - 2 : a;  // W, Z, ldz sit after sl, su
+  if (sl < il || sl > iu) return -7;
+  if (su < sl || su > iu) return -8;
+  if (!jlo) return -13;
+  if (!jhi) return -14;
   try {
     CK(cudaSetDevice(h->device));
-    long long lo = 0, hi = -1;
-    int rc = solve(h, d, e, n, 1, n, W, Z, ldz, sl, su, &lo, &hi, ncols_cap);
+    long long lo = su + 1, hi = su;
+    int rc = solve(h, d, e, n, il, iu, W, Z, ldz, sl, su, &lo, &hi, ncols_cap);
     *jlo = lo;
     *jhi = hi;
     return rc;
@@ -1595,20 +1603,25 @@ int mrrr_eig_dist(mrrr_t h, const void *nccl_id, int32_t rank, int32_t world, co
   if (!jhi) return -15;
   Nccl &N = nccl();
   if (!N.ok) return MRRR_ERR_NCCL;
+  // 1) the rank's own solve; any failure (returned code or a CUDA error) is kept local so that the rank
+  //    still joins both collectives with an empty share -- no rank is left waiting in ncclAllGather
   int rc = 0;
+  const long long k = iu - il + 1, per = (k + world - 1) / world;
+  const long long sl = il + (long long)rank * per, su = std::min<long long>(sl + per - 1, iu);
+  long long lo = su + 1, hi = su;
   try {
     CK(cudaSetDevice(h->device));
-    const long long k = iu - il + 1, per = (k + world - 1) / world;
-    const long long sl = il + (long long)rank * per, su = std::min<long long>(sl + per - 1, iu);
-    long long lo = su + 1, hi = su;
     const long long cap = std::max<long long>(ncols_cap, 1);
     CK(h->dWl.ensure(sizeof(double) * cap));
-    if (sl <= su) {
-      rc = solve(h, d, e, n, 1, n, h->dWl.as<double>(), Z, ldz, sl, su, &lo, &hi, ncols_cap);
-      if (rc != 0) { lo = su + 1; hi = su; }  // still joins the collective (with nothing)
-    }
-    *jlo = lo;
-    *jhi = hi;
+    if (sl <= su) rc = solve(h, d, e, n, il, iu, h->dWl.as<double>(), Z, ldz, sl, su, &lo, &hi, ncols_cap);
+  } catch (Err &er) {
+    rc = er.code;
+  }
+  *jlo = lo;   // on MRRR_ERR_NOMEM (owned count > ncols_cap) the needed range is still reported
+  *jhi = hi;
+  try {
+    if (rc != 0) cudaGetLastError();  // clear a non-sticky error before the collectives
+    CK(cudaSetDevice(h->device));
     // the communicator (kept while id, rank and world stay the same)
     if (!h->comm || h->comm_rank != rank || h->comm_world != world || memcmp(h->comm_id, nccl_id, 128) != 0) {
       if (h->comm) { N.destroy(h->comm); h->comm = nullptr; }
@@ -1619,46 +1632,55 @@ int mrrr_eig_dist(mrrr_t h, const void *nccl_id, int32_t rank, int32_t world, co
       h->comm_rank = rank;
       h->comm_world = world;
     }
-    // 1) every rank's (first owned index, count); 2) the padded eigenvalue lists; 3) scatter into W
-    const long long cnt = std::max<long long>(hi - lo + 1, 0);
-    long long meta_h[2] = {lo, cnt};
-    CK(h->dmeta.ensure(sizeof(long long) * 2));
-    CK(h->dmetas.ensure(sizeof(long long) * 2 * world));
+    // 2) every rank's (first owned index, count, return code); 3) the padded eigenvalue lists; 4) scatter
+    //    into W.  A failed rank contributes count 0 and its code, and every rank returns an error then.
+    const long long cnt = (rc == 0) ? std::max<long long>(hi - lo + 1, 0) : 0;
+    long long meta_h[3] = {lo, cnt, rc};
+    CK(h->dmeta.ensure(sizeof(long long) * 3));
+    CK(h->dmetas.ensure(sizeof(long long) * 3 * world));
     CK(cudaMemcpyAsync(h->dmeta.p, meta_h, sizeof(meta_h), cudaMemcpyHostToDevice, h->stream));
-    NK(N.all_gather(h->dmeta.p, h->dmetas.p, 2, ncclInt64, h->comm, h->stream));
-    std::vector<long long> metas(2 * world);
-    CK(cudaMemcpyAsync(metas.data(), h->dmetas.p, sizeof(long long) * 2 * world, cudaMemcpyDeviceToHost, h->stream));
+    NK(N.all_gather(h->dmeta.p, h->dmetas.p, 3, ncclInt64, h->comm, h->stream));
+    std::vector<long long> metas(3 * world);
+    CK(cudaMemcpyAsync(metas.data(), h->dmetas.p, sizeof(long long) * 3 * world, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     long long mcap = 1;
-    for (int r = 0; r < world; r++) mcap = std::max(mcap, metas[2 * r + 1]);
+    int peer_rc = 0;
+    for (int r = 0; r < world; r++) {
+      mcap = std::max(mcap, metas[3 * r + 1]);
+      if (metas[3 * r + 2] != 0 && peer_rc == 0) peer_rc = (int)metas[3 * r + 2];
+    }
     CK(h->dpad.ensure(sizeof(double) * mcap));
     CK(h->dparts.ensure(sizeof(double) * mcap * world));
     if (cnt) CK(cudaMemcpyAsync(h->dpad.p, h->dWl.p, sizeof(double) * cnt, cudaMemcpyDeviceToDevice, h->stream));
     NK(N.all_gather(h->dpad.p, h->dparts.p, (size_t)mcap, ncclDouble, h->comm, h->stream));
-    for (int r = 0; r < world; r++) {
-      const long long rl = metas[2 * r], rc_ = metas[2 * r + 1];
-      if (rc_ > 0)
+    for (int r = 0; r < world && peer_rc == 0; r++) {
+      // owned ranges partition [il, iu] (shard_owner), so every copy stays inside W[0..k)
+      const long long rl = metas[3 * r], rc_ = metas[3 * r + 1];
+      if (rc_ > 0 && rl >= il && rl + rc_ - 1 <= iu)
         CK(cudaMemcpyAsync(W + (rl - il), h->dparts.as<double>() + (long long)r * mcap, sizeof(double) * rc_,
                            cudaMemcpyDeviceToDevice, h->stream));
     }
     CK(cudaStreamSynchronize(h->stream));
+    if (rc == 0 && peer_rc != 0) rc = MRRR_ERR_PEER;
   } catch (Err &er) {
-    return er.code;
+    return rc ? rc : er.code;
   }
   return rc;
 }
 
-int mrrr_shard_owner(const int32_t *gstart, int64_t n, int64_t sl, int64_t su, int64_t jmax, int64_t *jlo,
-                     int64_t *jhi) {
+int mrrr_shard_owner(const int32_t *gstart, int64_t n, int64_t il, int64_t iu, int64_t sl, int64_t su,
+                     int64_t jmax, int64_t *jlo, int64_t *jhi) {
   if (!gstart) return -1;
   if (n < 1) return -2;
-  if (sl < 1 || sl > n) return -3;
-  if (su < sl || su > n) return -4;
-  if (jmax < su || jmax > n) return -5;
-  if (!jlo) return -6;
-  if (!jhi) return -7;
+  if (il < 1 || il > n) return -3;
+  if (iu < il || iu > n) return -4;
+  if (sl < il || sl > iu) return -5;
+  if (su < sl || su > iu) return -6;
+  if (jmax < su || jmax > n) return -7;
+  if (!jlo) return -8;
+  if (!jhi) return -9;
   long long lo = 0, hi = 0;
-  shard_owner(gstart, n, sl, su, jmax, &lo, &hi);
+  shard_owner(gstart, n, il, iu, sl, su, jmax, &lo, &hi);
   *jlo = lo;
   *jhi = hi;
   return 0;
@@ -1772,6 +1794,7 @@ const char *mrrr_strerror(int code) {
     case MRRR_ERR_ROOT: return "no definite root representation found";
     case MRRR_ERR_NODEVICE: return "no CUDA device";
     case MRRR_ERR_NCCL: return g_last_nccl_error.c_str();
+    case MRRR_ERR_PEER: return "another rank of the multi-GPU solve failed";
     default: return code < 0 ? "invalid argument" : "unknown error";
   }
 }

@@ -30,13 +30,15 @@ def shard_range(il: int, iu: int, world: int, rank: int) -> tuple[int, int]:
     return sl, su
 
 
-def owned_range(gstart: np.ndarray, sl: int, su: int, jmax: int) -> tuple[int, int]:
-    """Owned index range of a shard under the first-index ownership rule (libmrrr mrrr_shard_owner, a
-    host-only C ABI call).  ``gstart[j-1]`` is 1 iff index j starts a root group."""
+def owned_range(gstart: np.ndarray, sl: int, su: int, jmax: int, il: int = 1, iu: int | None = None) -> tuple[int, int]:
+    """Owned index range of a shard [sl, su] of the selection [il, iu] under the first-index ownership rule
+    (libmrrr mrrr_shard_owner, a host-only C ABI call).  ``gstart[j-1]`` is 1 iff index j starts a root
+    group; units are root groups cut to [il, iu]."""
     from . import load
     g = np.ascontiguousarray(gstart, dtype=np.int32)
+    iu = g.size if iu is None else iu
     jlo, jhi = C.c_int64(), C.c_int64()
-    rc = load().mrrr_shard_owner(g.ctypes.data, g.size, sl, su, jmax, C.byref(jlo), C.byref(jhi))
+    rc = load().mrrr_shard_owner(g.ctypes.data, g.size, il, iu, sl, su, jmax, C.byref(jlo), C.byref(jhi))
     if rc != 0:
         raise ValueError(f"mrrr_shard_owner failed with code {rc}")
     return jlo.value, jhi.value

@@ -27,7 +27,7 @@ for r in (0, N // 2, N - 1):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         a.record()
-        s.eig_shard(dt, et, sl, su)
+        s.eig_shard(dt, et, sl, su, cfg.il, cfg.iu)
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))

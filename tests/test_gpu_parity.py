@@ -191,31 +191,38 @@ def test_host_api_matches_device_api(torch_cuda):
 
 
 def test_shards_reproduce_full_solve(torch_cuda):
-    # P virtual ranks run one after another on this GPU: owned ranges partition [1, n] and every
-    # column equals the single-GPU solve bit for bit (SURVEY §8(e) ownership by first index)
+    # P virtual ranks run one after another on this GPU: owned ranges partition [il, iu] and every
+    # column equals the single-GPU solve of [il, iu] bit for bit (SURVEY §8(e) ownership by first index;
+    # subsets whose ends cut Wilkinson pairs, and right-end subsets that take the right root: ADVICE r1)
     import paper_1401_4950_b200 as m
     from paper_1401_4950_b200 import dist as pd
-    for d, e in (mi.random_tridiag(2000, 31, -1.0), mi.wilkinson(400)):
+    cases = [(mi.random_tridiag(2000, 31, -1.0), [(1, 2000), (1901, 2000)]),
+             (mi.wilkinson(400), [(1, 801), (600, 601), (300, 450), (2, 2), (700, 801)])]
+    for (d, e), sels in cases:
         n = d.size
-        g = gpu_solve(torch_cuda, d, e, diag=False)
         gst = oracle.mrrr(d, e).root_gstart  # group starts: the ownership rule's input
         dt = torch_cuda.from_numpy(d).cuda()
         et = torch_cuda.from_numpy(e).cuda()
-        for P in (2, 3, 4):
-            per = (n + P - 1) // P
-            covered = []
-            for rank in range(P):
-                s = m.Solver()
-                sl, su = pd.shard_range(1, n, P, rank)
-                assert (sl, su) == (1 + rank * per, min((rank + 1) * per, n))
-                jlo, jhi, W, Z = s.eig_shard(dt, et, sl, su)
-                assert (jlo, jhi) == pd.owned_range(gst, sl, su, n)
-                if jhi >= jlo:
-                    covered.extend(range(jlo, jhi + 1))
-                    assert np.array_equal(W.cpu().numpy(), g["W"][jlo - 1:jhi])
-                    assert np.array_equal(Z.cpu().numpy(), g["Z"][:, jlo - 1:jhi])
-                s.close()
-            assert covered == list(range(1, n + 1))
+        for il, iu in sels:
+            g = gpu_solve(torch_cuda, d, e, il, iu, diag=False)
+            k = iu - il + 1
+            for P in (2, 3, 4):
+                per = (k + P - 1) // P
+                covered = []
+                for rank in range(P):
+                    sl, su = pd.shard_range(il, iu, P, rank)
+                    if su < sl:
+                        continue
+                    assert (sl, su) == (il + rank * per, min(il + (rank + 1) * per - 1, iu))
+                    s = m.Solver()
+                    jlo, jhi, W, Z = s.eig_shard(dt, et, sl, su, il, iu)
+                    assert (jlo, jhi) == pd.owned_range(gst, sl, su, n, il, iu)
+                    if jhi >= jlo:
+                        covered.extend(range(jlo, jhi + 1))
+                        assert np.array_equal(W.cpu().numpy(), g["W"][jlo - il:jhi - il + 1])
+                        assert np.array_equal(Z.cpu().numpy(), g["Z"][:, jlo - il:jhi - il + 1])
+                    s.close()
+                assert covered == list(range(il, iu + 1))
 
 
 # ------------------------------------------------------------------------- full-size configs
@@ -323,17 +330,35 @@ def test_bisection_schedules_are_bit_identical(torch_cuda, env, monkeypatch):
 
 
 @pytest.mark.gpu
-def test_eig_dist_single_rank_matches_full_solve(torch_cuda):
-    # mrrr_eig_dist with a one-rank NCCL communicator: the shard is the whole range, the all-gathered
-    # eigenvalue list and the owned vectors equal the plain solve bit for bit (same kernels, same order)
+@pytest.mark.parametrize("mat,il,iu", [("rand", 5, 560), ("rand", 500, 600), ("wilk", 600, 601), ("wilk", 300, 450)])
+def test_eig_dist_single_rank_matches_full_solve(torch_cuda, mat, il, iu):
+    # mrrr_eig_dist with a one-rank NCCL communicator: the shard is the whole selection, the all-gathered
+    # eigenvalue list and the owned vectors equal the plain solve bit for bit (same kernels, same order);
+    # right-end subsets take the same root side as mrrr_eig, subset ends inside clusters are cut at il/iu
     import paper_1401_4950_b200 as m
-    d, e = mi.random_tridiag(600, 41, -1.0)
+    d, e = mi.random_tridiag(600, 41, -1.0) if mat == "rand" else mi.wilkinson(300)
     dt, et = torch_cuda.from_numpy(d).cuda(), torch_cuda.from_numpy(e).cuda()
     s = m.Solver()
-    W0, Z0 = s.eig(dt, et, 5, 560)
+    W0, Z0 = s.eig(dt, et, il, iu)
     s2 = m.Solver()
-    jlo, jhi, W, Z = s2.eig_dist(dt, et, 5, 560, m.nccl_unique_id(), 0, 1)
+    jlo, jhi, W, Z = s2.eig_dist(dt, et, il, iu, m.nccl_unique_id(), 0, 1)
     torch_cuda.cuda.synchronize()
-    assert (jlo, jhi) == (5, 560)
+    assert (jlo, jhi) == (il, iu)
     assert torch_cuda.equal(W.cpu(), W0.cpu())
     assert torch_cuda.equal(Z.cpu(), Z0.cpu())
+
+
+@pytest.mark.gpu
+def test_eig_dist_two_ranks(torch_cuda):
+    # world 2 over NCCL, one process per GPU (skipped on a one-GPU box): the gathered W equals the 1-GPU solve
+    if torch_cuda.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    import subprocess
+    import sys
+    import os
+    code = os.path.join(os.path.dirname(os.path.abspath(__file__)), "dist_worker.py")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr=127.0.0.1", "--master-port=29533", code], capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("DIST_OK") == 2

@@ -33,7 +33,7 @@ def _worker(rank, world, port, n, il, iu, gstart, W_full, q):
     try:
         sl, su = pd.shard_range(il, iu, world, rank)
         if su >= sl:
-            jlo, jhi = pd.owned_range(gstart, sl, su, iu)
+            jlo, jhi = pd.owned_range(gstart, sl, su, n, il, iu)
         else:
             jlo, jhi = su + 1, su
         m = max(jhi - jlo + 1, 0)
@@ -89,11 +89,11 @@ def _check(gstart, W_full, out, il, iu):
     for (a0, a1), (b0, b1) in zip(owned, owned[1:]):
         assert b0 == a1 + 1
     for jlo, jhi in owned:
-        assert gstart[jlo - 1] == 1
+        assert gstart[jlo - 1] == 1 or jlo == il
         assert jhi == iu or gstart[jhi] == 1
-    # a group is owned by the rank whose shard holds its first index
+    # a unit (root group cut to [il, iu]) is owned by the rank whose shard holds its first index
     for (sl, su, jlo, jhi) in ranges:
-        starts = [j for j in range(max(sl, il), su + 1) if gstart[j - 1] == 1]
+        starts = [j for j in range(max(sl, il), su + 1) if gstart[j - 1] == 1 or j == il]
         if starts:
             assert jlo == starts[0]
         else:
@@ -117,6 +117,26 @@ def test_shards_clusters_straddle(world):
     ranges = out[0][2]
     cut = [su for (sl, su, jlo, jhi) in ranges[:-1] if su < d.size and gs[su] == 0]
     assert cut, "test needs a cluster straddling a shard boundary"
+
+
+@pytest.mark.parametrize("world,il,iu", [(2, 600, 601), (3, 600, 601), (2, 300, 450), (3, 300, 450), (3, 2, 2),
+                                         (2, 590, 601)])
+def test_shards_subset_edges_inside_clusters(world, il, iu):
+    # a subset whose ends fall inside Wilkinson pairs -- the unit containing il starts at il, no
+    # owned range runs past iu, and the owned ranges still partition [il, iu]
+    d, e = mi.wilkinson(300)
+    gs, Wf, out = _run(world, d, e, il, iu)
+    _check(gs, Wf, out, il, iu)
+
+
+def test_owner_clips_to_selection():
+    from paper_1401_4950_b200 import dist as pd
+    g = np.array([1, 0, 1, 0, 1, 0, 1, 0, 1, 0], np.int32)   # pairs (1,2) (3,4) ... (9,10)
+    assert pd.owned_range(g, 4, 5, 10, 4, 7) == (4, 6)      # il = 4 inside the pair (3,4): unit 4..4 + pair 5,6
+    assert pd.owned_range(g, 6, 7, 10, 4, 7) == (7, 7)      # iu = 7 cuts the pair (7,8)
+    assert pd.owned_range(g, 4, 4, 10, 4, 4) == (4, 4)
+    with pytest.raises(ValueError):
+        pd.owned_range(g, 3, 5, 10, 4, 7)                   # shard starts before il
 
 
 def test_shards_glued_blocks():
@@ -146,6 +166,8 @@ def test_owner_argument_errors():
         pd.owned_range(g, 6, 5, 10)
     with pytest.raises(ValueError):
         pd.owned_range(g, 1, 5, 4)
+    with pytest.raises(ValueError):
+        pd.owned_range(g, 1, 5, 10, 1, 11)
     assert pd.owned_range(g, 3, 5, 10) == (3, 5)
     g2 = np.array([1, 0, 0, 1, 0, 1, 1, 0, 0, 0], np.int32)
     assert pd.owned_range(g2, 2, 3, 10) == (4, 3)      # no group starts in [2, 3]

@@ -148,8 +148,9 @@ int mrrr_shard_owner(const int32_t *gstart, int64_t n, int64_t il, int64_t iu, i
  * fallback), 24 singletons the segmented RQI handed to the two-lane kernel, 25-27 of them because the
  * x-arithmetic twist search did not resolve gamma / a segment junction failed / the RQC was rejected,
  * 28 dd rows of RQC-only (light) passes, 29 fp64 rows of the segmented twist search (both lanes),
- * 30 segmented RQI passes repeated with an 8x longer warm-up after a failed junction. */
-#define MRRR_NSTATS 31
+ * 30 segmented RQI passes repeated with an 8x longer warm-up after a failed junction, 31 singletons whose
+ * last two-lane Getvec ran the careful IEEE pass (zero pivots / special values). */
+#define MRRR_NSTATS 32
 int mrrr_get_stats(mrrr_t h, int64_t *stats, int32_t nstats);
 
 /* Diagnostics of the last call made with MRRR_KEEP_DIAG (host buffers owned

@@ -23,7 +23,7 @@ CFLAGS = ["-O2", "-std=gnu11", "-fopenmp", "-fPIC", "-shared", "-ffp-contract=of
 
 STAT_NAMES = ["d_max", "n_clusters", "largest_cluster", "uncertified", "shift_attempts", "rqi_iters",
               "rqi_fallbacks", "bracket_fixes", "root_backoffs", "failed", "negcount_x", "negcount_y",
-              "getvec_calls"]
+              "getvec_calls", "zero_pivots"]
 
 
 def build(force: bool = False) -> str:
@@ -97,6 +97,24 @@ def lib():
         L.oracle_jacobi.restype = None
         L.oracle_jacobi.argtypes = [_i64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.oracle_maxd.restype = C.c_int
+        L.oracle_jacobi_ldl.restype = None
+        L.oracle_jacobi_ldl.argtypes = [_i64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.oracle_stats_read.restype = None
+        L.oracle_stats_read.argtypes = [C.c_void_p]
+        L.oracle_stats_reset.restype = None
+        L.oracle_stats_reset.argtypes = []
+        L.oracle_bracket_x.restype = _i64
+        L.oracle_bracket_x.argtypes = [_i64, C.c_void_p, C.c_void_p, _i64, _dp, _dp]
+        L.oracle_bracket_y.restype = _i64
+        L.oracle_bracket_y.argtypes = [_i64, C.c_void_p, C.c_void_p, _i64, _dp, _dp]
+        L.oracle_bisect_y_full.restype = None
+        L.oracle_bisect_y_full.argtypes = [_i64, C.c_void_p, C.c_void_p, _i64, C.c_double, C.c_double, _dp, _dp]
+        L.oracle_rqi.restype = None
+        L.oracle_rqi.argtypes = [_i64, C.c_void_p, C.c_void_p, _i64, C.c_double, C.c_double, C.c_double, _dp,
+                                 C.c_void_p, C.POINTER(_i64), C.POINTER(_i64)]
+        L.oracle_root_x_from.restype = C.c_int
+        L.oracle_root_x_from.argtypes = [_i64, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_double, _dp,
+                                         C.c_void_p, C.c_void_p, C.POINTER(C.c_int)]
         _lib = L
     return _lib
 
@@ -305,3 +323,70 @@ def jacobi(d, e) -> np.ndarray:
     hi, lo = np.zeros(n), np.zeros(n)
     lib().oracle_jacobi(n, _ptr(d), _ptr(e), _ptr(hi), _ptr(lo))
     return hi, lo
+
+
+# ------------------------------------------------------- branch pins (tests/test_oracle_branches.py)
+def _lpad(d, l):
+    d = _f64(d)
+    lp = np.zeros(d.size)
+    lp[:d.size - 1] = _f64(l)
+    return d, lp
+
+
+def jacobi_ldl(d, l):
+    """Eigenvalues (ascending, hi/lo) of L D L^T multiplied out in binary128, by cyclic Jacobi."""
+    d, lp = _lpad(d, l)
+    hi, lo = np.zeros(d.size), np.zeros(d.size)
+    lib().oracle_jacobi_ldl(d.size, _ptr(d), _ptr(lp), _ptr(hi), _ptr(lo))
+    return hi, lo
+
+
+def stats_read() -> dict:
+    st = np.zeros(16, np.int64)
+    lib().oracle_stats_read(_ptr(st))
+    return {nm: int(st[i]) for i, nm in enumerate(STAT_NAMES)}
+
+
+def stats_reset():
+    lib().oracle_stats_reset()
+
+
+def bracket_x(dx, dllx, j: int, lo: float, hi: float):
+    dx, dllx = _f64(dx), _f64(dllx)
+    a, b = C.c_double(lo), C.c_double(hi)
+    fixes = lib().oracle_bracket_x(dx.size, _ptr(dx), _ptr(dllx), j, C.byref(a), C.byref(b))
+    return a.value, b.value, fixes
+
+
+def bracket_y(d, l, j: int, lo: float, hi: float):
+    d, lp = _lpad(d, l)
+    a, b = C.c_double(lo), C.c_double(hi)
+    fixes = lib().oracle_bracket_y(d.size, _ptr(d), _ptr(lp), j, C.byref(a), C.byref(b))
+    return a.value, b.value, fixes
+
+
+def bisect_y_full(d, l, j: int, lo: float, hi: float):
+    d, lp = _lpad(d, l)
+    a, b = C.c_double(), C.c_double()
+    lib().oracle_bisect_y_full(d.size, _ptr(d), _ptr(lp), j, lo, hi, C.byref(a), C.byref(b))
+    return a.value, b.value
+
+
+def rqi(d, l, j: int, lo: float, hi: float, gap: float):
+    d, lp = _lpad(d, l)
+    W = C.c_double()
+    z = np.zeros(d.size)
+    it, fb = C.c_int64(), C.c_int64()
+    lib().oracle_rqi(d.size, _ptr(d), _ptr(lp), j, lo, hi, gap, C.byref(W), _ptr(z), C.byref(it), C.byref(fb))
+    return dict(W=W.value, z=z, iters=it.value, fallbacks=fb.value)
+
+
+def root_x_from(d, e, left: bool, mu0: float, t: float):
+    d, e = _f64(d), _f64(e)
+    n = d.size
+    mu = C.c_double()
+    bo = C.c_int()
+    dx, lx = np.zeros(n), np.zeros(n)
+    rc = lib().oracle_root_x_from(n, _ptr(d), _ptr(e), int(left), mu0, t, C.byref(mu), _ptr(dx), _ptr(lx),
+                                  C.byref(bo))
+    return dict(rc=rc, mu=mu.value, d=dx, l=lx[:n - 1].copy(), backoffs=bo.value)

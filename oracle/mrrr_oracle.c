@@ -44,7 +44,7 @@ typedef __float128 qreal;
 enum {
   ST_DMAX = 0, ST_NCLUSTERS, ST_LARGEST, ST_UNCERTIFIED, ST_ATTEMPTS, ST_RQI_ITERS,
   ST_RQI_FALLBACK, ST_BRACKET_FIX, ST_ROOT_BACKOFF, ST_FAILED, ST_NEGX, ST_NEGY,
-  ST_GETVEC, ST_NSTATS = 16
+  ST_GETVEC, ST_ZPIV, ST_NSTATS = 16
 };
 
 typedef struct {
@@ -358,13 +358,11 @@ static void rep_derive(rep_t *r) {
 /* (Alg. mrrr L2 P:2775-2776, mixed xi = eps_x P:5757-5770; A-9).             */
 /* Returns 0 on success.                                                       */
 /* ------------------------------------------------------------------------- */
-int oracle_root_x(int64_t nb, const double *a, const double *b, int left, double *mu_out,
-                  double *dx, double *lx, double *gl_out, double *gu_out, int *backoffs) {
-  double gl, gu, t;
-  oracle_gershgorin(nb, a, b, &gl, &gu, &t);
-  *gl_out = gl; *gu_out = gu;
+/* the factorization loop of S3 from a start shift mu0: mu0, then mu0 -/+ 2^j t, j = 1..10 (A-8) */
+static int root_factor_from(int64_t nb, const double *a, const double *b, int left, double mu0, double t,
+                            double *mu_out, double *dx, double *lx, int *backoffs) {
   for (int j = 0; j <= 10; j++) {
-    double mu = left ? ((j == 0) ? gl : gl - ldexp(t, j)) : ((j == 0) ? gu : gu + ldexp(t, j));
+    double mu = left ? ((j == 0) ? mu0 : mu0 - ldexp(t, j)) : ((j == 0) ? mu0 : mu0 + ldexp(t, j));
     dx[0] = a[0] - mu;
     for (int64_t i = 0; i < nb - 1; i++) {
       lx[i] = b[i] / dx[i];
@@ -376,6 +374,21 @@ int oracle_root_x(int64_t nb, const double *a, const double *b, int left, double
     if (ok) { *mu_out = mu; if (backoffs) *backoffs = j; return 0; }
   }
   return -1;
+}
+
+int oracle_root_x(int64_t nb, const double *a, const double *b, int left, double *mu_out,
+                  double *dx, double *lx, double *gl_out, double *gu_out, int *backoffs) {
+  double gl, gu, t;
+  oracle_gershgorin(nb, a, b, &gl, &gu, &t);
+  *gl_out = gl; *gu_out = gu;
+  return root_factor_from(nb, a, b, left, left ? gl : gu, t, mu_out, dx, lx, backoffs);
+}
+
+/* pin hook: the same back-off loop started from a caller-chosen shift mu0 with step t (a start inside the */
+/* spectrum forces the back-off, which the inflated Gershgorin start never needs, A-32)           */
+int oracle_root_x_from(int64_t nb, const double *a, const double *b, int left, double mu0, double t,
+                       double *mu_out, double *dx, double *lx, int *backoffs) {
+  return root_factor_from(nb, a, b, left, mu0, t, mu_out, dx, lx, backoffs);
 }
 
 static rep_t *make_root(int64_t n, int64_t s, int64_t nb, const double *d, const double *e, int left,
@@ -493,6 +506,7 @@ static void getvec_q(const rep_t *M, qreal lam, int64_t *r_io, gv_ws *w, qreal *
   for (int64_t i = r - 1; i >= 0; i--) {
     if (dp[i] != 0) z[i] = -lp[i] * z[i + 1];
     else {
+      STAT_ADD(ST_ZPIV, 1);
       qreal num = (i + 1 < nb - 1) ? dl[i + 1] : 0, zz2 = (i + 2 < nb) ? z[i + 2] : 0;
       qreal v = -(num / dl[i]) * zz2;
       z[i] = finiteq(v) ? v : 0;
@@ -501,6 +515,7 @@ static void getvec_q(const rep_t *M, qreal lam, int64_t *r_io, gv_ws *w, qreal *
   for (int64_t i = r; i < nb - 1; i++) {
     if (om[i + 1] != 0) z[i + 1] = -um[i] * z[i];
     else {
+      STAT_ADD(ST_ZPIV, 1);
       qreal num = (i >= 1) ? dl[i - 1] : 0, zm = (i >= 1) ? z[i - 1] : 0;
       qreal v = -(num / dl[i]) * zm;
       z[i + 1] = finiteq(v) ? v : 0;
@@ -513,14 +528,13 @@ static void getvec_q(const rep_t *M, qreal lam, int64_t *r_io, gv_ws *w, qreal *
   *c_out = c;
 }
 
-/* y-bisection to full accuracy (fallback of RQI): relative width 2^-98 of |lambda|,  */
-/* or absolute width 2^-100 spdiam when that is larger (A-29: the y-count cannot resolve finer   */
-/* than the representation's y-rounding when its shift could not be certified)                          */
+/* y-bisection to full accuracy (fallback of RQI): Alg. Bisection P:3077-3111 on the  */
+/* y-representation with y-arithmetic counts, stopping at relative width 2^-98 of |lambda| (a few eps_y,    */
+/* A-14) or at atol = 2 omega.  Pinned: tests/test_oracle_branches.py (binary128 Jacobi).     */
 static qreal bisect_y_full(const rep_t *M, int64_t j, qreal lo, qreal hi) {
-  const qreal afloor = 0x1p-100Q * (qreal)M->spdiam;
-  for (int it = 0; it < 200; it++) {
+  for (int it = 0; it < 400; it++) {
     qreal m = fmaxq(fabsq(lo), fabsq(hi));
-    if (!(hi - lo > fmaxq(0x1p-98Q * m, afloor))) break;
+    if (!(hi - lo > fmaxq(0x1p-98Q * m, (qreal)ATOL))) break;
     qreal w = lo + (hi - lo) / 2;
     STAT_ADD(ST_NEGY, 1);
     if (negcount_q(M->nb, M->d, M->dll, w) < j) lo = w;
@@ -548,9 +562,9 @@ static void rqi_singleton(const rep_t *M, int64_t j, double lo, double hi, doubl
     if (r == 0 || !finiteq(zz) || zz == 0) break;
     qreal nz = sqrtq(zz);
     qreal resid = fabsq(gamma) / nz, rqc = gamma / zz;
-    /* tol2: |RQC| < 4 eps_y |lam|, not below the representation's y-rounding 2^-100 spdiam (A-30) */
-    qreal tol2 = fmaxq(4 * EPS_Y * fabsq(lam), 0x1p-100Q * (qreal)M->spdiam);
-    if ((double)resid <= thr1 || fabsq(rqc) < tol2) { accepted = 1; break; }
+    /* stopping tests of Alg. stask: ||r|| <= tol1 (mixed: k_rs gap eps_x sqrt(n)) */
+    /* or |RQC| < tol2 |lam| with tol2 = 4 eps_y (A-14)                                                        */
+    if ((double)resid <= thr1 || fabsq(rqc) < 4 * EPS_Y * fabsq(lam)) { accepted = 1; break; }
     if (c < j) blo = lam; else bhi = lam;
     qreal nl = lam + rqc;
     int ok = ((c < j) ? (rqc > 0) : (rqc < 0)) && (blo < nl) && (nl < bhi);
@@ -995,14 +1009,14 @@ double oracle_ortho_full(int64_t n, int64_t k, const double *Z, int64_t ldz) {
 
 /* cyclic Jacobi on the dense T in binary128 (brute force for n <= 64; a test */
 /* tool independent of MRRR).  Eigenvalues ascending into w (as hi/lo pairs).  */
-void oracle_jacobi(int64_t n, const double *d, const double *e, double *w_hi, double *w_lo) {
-  qreal *A = calloc((size_t)(n * n), sizeof(qreal));
-  for (int64_t i = 0; i < n; i++) A[i * n + i] = d[i];
-  for (int64_t i = 0; i < n - 1; i++) { A[i * n + i + 1] = e[i]; A[(i + 1) * n + i] = e[i]; }
+static void jacobi_q(int64_t n, qreal *A, double *w_hi, double *w_lo) {
   for (int sweep = 0; sweep < 100; sweep++) {
-    qreal off = 0;
-    for (int64_t p = 0; p < n; p++) for (int64_t q = p + 1; q < n; q++) off += A[p * n + q] * A[p * n + q];
-    if (off < 1e-70Q) break;
+    qreal off = 0, dia = 0;
+    for (int64_t p = 0; p < n; p++) {
+      dia += A[p * n + p] * A[p * n + p];
+      for (int64_t q = p + 1; q < n; q++) off += A[p * n + q] * A[p * n + q];
+    }
+    if (off <= 1e-70Q * dia || off == 0) break;
     for (int64_t p = 0; p < n; p++)
       for (int64_t q = p + 1; q < n; q++) {
         qreal apq = A[p * n + q];
@@ -1032,6 +1046,24 @@ void oracle_jacobi(int64_t n, const double *d, const double *e, double *w_hi, do
   }
   for (int64_t i = 0; i < n; i++) { w_hi[i] = (double)ev[i]; w_lo[i] = (double)(ev[i] - (qreal)w_hi[i]); }
   free(ev);
+}
+
+void oracle_jacobi(int64_t n, const double *d, const double *e, double *w_hi, double *w_lo) {
+  qreal *A = calloc((size_t)(n * n), sizeof(qreal));
+  for (int64_t i = 0; i < n; i++) A[i * n + i] = d[i];
+  for (int64_t i = 0; i < n - 1; i++) { A[i * n + i + 1] = e[i]; A[(i + 1) * n + i] = e[i]; }
+  jacobi_q(n, A, w_hi, w_lo);
+  free(A);
+}
+
+/* the same brute force on L D L^T (unit lower bidiagonal L = (1, l)) multiplied out in binary128 */
+void oracle_jacobi_ldl(int64_t n, const double *d, const double *l, double *w_hi, double *w_lo) {
+  qreal *A = calloc((size_t)(n * n), sizeof(qreal));
+  for (int64_t i = 0; i < n; i++) {
+    A[i * n + i] = (qreal)d[i] + ((i > 0) ? ((qreal)d[i - 1] * (qreal)l[i - 1]) * (qreal)l[i - 1] : 0);
+    if (i < n - 1) { A[i * n + i + 1] = (qreal)d[i] * (qreal)l[i]; A[(i + 1) * n + i] = A[i * n + i + 1]; }
+  }
+  jacobi_q(n, A, w_hi, w_lo);
   free(A);
 }
 
@@ -1109,3 +1141,56 @@ int oracle_root_y(int64_t n, const double *d, const double *e, int64_t s, int64_
 }
 
 int oracle_maxd(void) { return MAXD; }
+
+/* -------- pins of the branches no full solve of the test matrices reaches (tests/test_oracle_branches.py) */
+void oracle_stats_read(int64_t *out) { memcpy(out, g_stats, sizeof(g_stats)); }
+void oracle_stats_reset(void) { memset(g_stats, 0, sizeof(g_stats)); }
+
+static rep_t *rep_from_fp64(int64_t nb, const double *d, const double *l) {
+  rep_t *M = rep_alloc(nb);
+  for (int64_t i = 0; i < nb; i++) { M->d[i] = d[i]; M->l[i] = (i < nb - 1) ? (qreal)l[i] : 0; }
+  rep_derive(M);
+  M->sigma = 0;
+  M->depth = 0;
+  double sp = 0;
+  for (int64_t i = 0; i < nb; i++) sp = dmax(sp, fabs(d[i]));
+  M->spdiam = sp;
+  return M;
+}
+
+/* bracket repair in x (on M_x = fl64 data) and in y; returns the number of widening steps */
+int64_t oracle_bracket_x(int64_t nb, const double *dx, const double *dllx, int64_t j, double *lo, double *hi) {
+  int64_t before = g_stats[ST_BRACKET_FIX];
+  bracket_x(nb, dx, dllx, j, lo, hi);
+  return g_stats[ST_BRACKET_FIX] - before;
+}
+int64_t oracle_bracket_y(int64_t nb, const double *d, const double *l, int64_t j, double *lo, double *hi) {
+  rep_t *M = rep_from_fp64(nb, d, l);
+  int64_t before = g_stats[ST_BRACKET_FIX];
+  bracket_y(nb, M->d, M->dll, j, lo, hi);
+  rep_free(M);
+  return g_stats[ST_BRACKET_FIX] - before;
+}
+
+/* y-bisection to full accuracy of eigenvalue j (1-based) of L D L^T from [lo, hi] */
+void oracle_bisect_y_full(int64_t nb, const double *d, const double *l, int64_t j, double lo, double hi,
+                          double *lam_hi, double *lam_lo) {
+  rep_t *M = rep_from_fp64(nb, d, l);
+  q_out(bisect_y_full(M, j, (qreal)lo, (qreal)hi), lam_hi, lam_lo);
+  rep_free(M);
+}
+
+/* the singleton RQI of S9 on L D L^T (sigma = 0) from the x-interval [lo, hi] with gap; *fallbacks = 1 when */
+/* the RQI ended in the bisection fallback of P:3481-3482                                                    */
+void oracle_rqi(int64_t nb, const double *d, const double *l, int64_t j, double lo, double hi, double gap,
+                double *W, double *z, int64_t *iters, int64_t *fallbacks) {
+  rep_t *M = rep_from_fp64(nb, d, l);
+  gv_ws w;
+  gv_alloc(&w, nb);
+  int64_t i0 = g_stats[ST_RQI_ITERS], f0 = g_stats[ST_RQI_FALLBACK];
+  rqi_singleton(M, j, lo, hi, gap, W, z, &w);
+  *iters = g_stats[ST_RQI_ITERS] - i0;
+  *fallbacks = g_stats[ST_RQI_FALLBACK] - f0;
+  gv_free(&w);
+  rep_free(M);
+}

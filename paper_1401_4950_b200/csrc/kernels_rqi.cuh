@@ -481,9 +481,11 @@ __device__ __noinline__ bool getvec_pair_q(const QElt *__restrict__ q, int nb, d
 }
 
 // returns true if the careful (IEEE special value) pass had to run
+// (force_careful: fault injection of the GPU tests, MRRR_FAULT bit 1 -- every Getvec takes the careful pass)
 __device__ __forceinline__ bool getvec_pair_any(const YElt *__restrict__ y, const QElt *__restrict__ qy, int nb, dd lam,
-                                                int r, bool isB, dd *P0, dd *P1, dd *P2, long long S, GV &g) {
-  if (getvec_pair_q(qy, nb, lam, r, isB, P0, P1, P2, S, g)) return false;
+                                                int r, bool isB, dd *P0, dd *P1, dd *P2, long long S, GV &g,
+                                                bool force_careful = false) {
+  if (!force_careful && getvec_pair_q(qy, nb, lam, r, isB, P0, P1, P2, S, g)) return false;
   getvec_pair_t<true>(y, nb, lam, r, isB, P0, P1, P2, S, g);
   return true;
 }
@@ -640,7 +642,10 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
                                              const YElt *__restrict__ my, const QElt *__restrict__ mq, dd *ws,
                                              long long S, long long nbmax,
                                              double *W, ZMeta *zmeta, int *diag_depth, double *fin_lo,
-                                             double *fin_hi, long long *stats) {
+                                             double *fin_hi, long long *stats, int fault) {
+  // fault (MRRR_FAULT, GPU tests only): bit 0 skips the RQI iterations (every singleton takes the bisection
+  // fallback of P:3481-3482), bit 1 sends every Getvec through the careful IEEE pass
+  const bool fc = (fault & 2) != 0;
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   const bool isB = gt & 1;
   const int pid = gt >> 1;  // workspace column (padded grid: S >= #pairs launched)
@@ -665,16 +670,16 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
   bool accepted = false, lu_valid = false, careful = false;
   GV g;
   dd zz = dd_from(1.0);
-  for (int it = 0; it < MAX_RQI && !accepted; it++) {
+  for (int it = 0; it < ((fault & 1) ? 0 : MAX_RQI) && !accepted; it++) {
     if (r < 0) { qd += 2 * (nb - 1); qdg += nb - 1; } else qd += nb - 1;
     lu_valid = r >= 0;
-    careful = getvec_pair_any(y, qy, nb, lam, r, isB, P0, P1, P2, S, g);
+    careful = getvec_pair_any(y, qy, nb, lam, r, isB, P0, P1, P2, S, g, fc);
     iters++;
     r = g.r;
     if (r < 0) break;
     zz = g.zz;
     if (!isfinite(zz.hi)) {  // closed form broke down (overflow / zero pivot): explicit z solve (A-25)
-      if (!lu_valid) { careful = getvec_pair_any(y, qy, nb, lam, r, isB, P0, P1, P2, S, g); lu_valid = true; qd += nb - 1; }
+      if (!lu_valid) { careful = getvec_pair_any(y, qy, nb, lam, r, isB, P0, P1, P2, S, g, fc); lu_valid = true; qd += nb - 1; }
       zs += nb - 1;
       if (!isB) zz = zsolve(y, nb, r, P2, P2, 1, dd_from(0.0), nullptr);
       zz = shfl_dd_from(zz, lane_F());
@@ -706,7 +711,7 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
     if (active && !isB) atomicAdd((unsigned long long *)&stats[ST_RQI_FALLBACK], 1ull);
     lam = bisect_y_full(y, qy, nb, j, blo, bhi, R.spdiam);
     lu_valid = r >= 0;
-    careful = getvec_pair_any(y, qy, nb, lam, r, isB, P0, P1, P2, S, g);
+    careful = getvec_pair_any(y, qy, nb, lam, r, isB, P0, P1, P2, S, g, fc);
     if (r < 0) qdg += nb - 1;
     qd += (r < 0) ? 2 * (nb - 1) : nb - 1;
     iters++;
@@ -714,7 +719,7 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
     zz = g.zz;
   }
   if (!lu_valid) {  // accepted on a twist-search pass: one r-twisted pass to store l+ / u- (and its dd ||z||^2)
-    careful = getvec_pair_any(y, qy, nb, lam, r, isB, P0, P1, P2, S, g);
+    careful = getvec_pair_any(y, qy, nb, lam, r, isB, P0, P1, P2, S, g, fc);
     qd += nb - 1;
     zz = g.zz;
   }
@@ -728,6 +733,7 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
     if (!isB) {
       ZMeta zmv;
       zmv.inv_hi = inv.hi; zmv.inv_lo = inv.lo; zmv.r = r; zmv.careful = careful ? 1 : 0;
+      if (careful) atomicAdd((unsigned long long *)&stats[ST_CAREFUL], 1ull);
       zmeta[pid] = zmv;
       dd sig = dd_make(R.sig_hi, R.sig_lo);
       W[s.col] = dd_add(lam, sig).hi;

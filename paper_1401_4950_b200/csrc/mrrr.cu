@@ -130,6 +130,7 @@ struct mrrr_ctx {
   int max_nodes = 0;           // bound on live bisection nodes (indices in the computed set)  // tube point budgets: no estimate (4 full levels) / with estimate
   bool rqi_pair = true;
   bool l2_persist = true;
+  int fault = 0;               // MRRR_FAULT: fault injection for the GPU tests (k_rqi2: bit 0 fallback, bit 1 careful)
   long long l2_max_window = 0;
 
   // buffers
@@ -890,7 +891,7 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
         k_rqi2<<<nblocks_for(2 * nold, 64), 64, 64 * MRRR_RQI_RING * sizeof(RingSlot), h->stream>>>(
             sgb, nold, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->mq.as<QElt>(), h->wsA.as<dd>(), stride, nbmax, W,
             h->zmeta.as<ZMeta>(), diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
-            diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>());
+            diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), h->fault);
         launch_check(h);
         if (h->zw_chunk)
           k_zwrite_chunk<<<nblocks_for(nold, 4), 128, 0, h->stream>>>(
@@ -1481,6 +1482,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_BUD_TUBE")) h->bud_tube = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;
     if (const char *s = getenv("MRRR_L2PIN")) h->l2_persist = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_FAULT")) h->fault = atoi(s);
     {
       int dev = h->device, maxwin = 0, l2 = 0;
       cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);

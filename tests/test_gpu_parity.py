@@ -329,6 +329,29 @@ def test_bisection_schedules_are_bit_identical(torch_cuda, env, monkeypatch):
         g["solver"].close()
 
 
+@pytest.mark.parametrize("fault", [1, 2, 3])
+def test_forced_fallback_and_careful_paths(torch_cuda, fault, monkeypatch):
+    # fault injection (MRRR_FAULT, read at mrrr_init): every singleton through the two-lane kernel (MRRR_RQISEG=0)
+    # with bit 0 = no RQI iterations, so every eigenpair comes from the y-bisection fallback + one Getvec
+    # (P:3481-3482), bit 1 = every Getvec through the careful IEEE pass (A-25).  The oracle's
+    # own fallback and zero-pivot branches are pinned in tests/test_oracle_branches.py; here the GPU's must
+    # still meet every parity gate.
+    monkeypatch.setenv("MRRR_RQISEG", "0")
+    monkeypatch.setenv("MRRR_FAULT", str(fault))
+    for d, e in (mi.random_tridiag(1500, 23, -1.0), mi.wilkinson(150), mi.glued_wilkinson(4, 40, 1e-10)):
+        g = gpu_solve(torch_cuda, d, e)
+        r = oracle.mrrr(d, e)
+        check_integers(g, r)
+        tn = max(abs(r.W[0]), abs(r.W[-1]))
+        check_tol(d, e, g["W"], g["Z"], r.W, tn)
+        assert oracle.ortho_full(g["Z"]) <= max(d.size, 32) * EPS
+        if fault & 1:
+            assert g["stats"]["rqi_fallbacks"] == d.size
+        if fault & 2:
+            assert g["stats"]["careful"] == d.size
+        g["solver"].close()
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("mat,il,iu", [("rand", 5, 560), ("rand", 500, 600), ("wilk", 600, 601), ("wilk", 300, 450)])
 def test_eig_dist_single_rank_matches_full_solve(torch_cuda, mat, il, iu):

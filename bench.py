@@ -272,45 +272,50 @@ def main():
     stats = solver.stats()
     tphase = solver.times()
 
-    # roofline of the dominant kernel family: algorithmic FP64 flops per launch / CUDA-event launch time
+    # roofline of the dominant kernel family: algorithmic FP64 flops per launch / CUDA-event launch time.
+    # Every FP64 operation is counted at the cost the kernels issue (north_star: divisions weighted by their
+    # issue cost: 8 FP64 slots, flops.W_DIV_ISSUE); the survey's __ddiv_rn weighting is printed beside it.
     pk = peaks()
     fp = pk.get("fp64") or {}
     roof, roof_other, roof_step = None, None, None
     if fp:
         from paper_1401_4950_b200 import flops as fl
-        wdiv = fp.get("w_div", 13.0)
+        wdiv_survey = fp.get("w_div", 13.0)
         peak = fp["fp64_tflops"]
         src = "profiles/fp64_peak_r01.json: measured DFMA rate x 2 on this pool's B200 (burst, all SMs)"
         cands = []
         nrq = max(int(tphase["rqi_launches"]), 1)
-        # primary: the single dominant kernel (ncu launch list: the root x-NegCount rounds, 40 % of a C2 solve);
-        # secondary: the singleton-RQI family (several kernels, timed as a batch incl. its host syncs)
+        # primary: the single dominant kernel (ncu launch list: the root x-NegCount rounds); secondary: the
+        # singleton-RQI family (several kernels, timed as a batch incl. its host syncs)
         if tphase["negcount_launches"]:
             launch_ms = tphase["negcount_ms_per_launch"]
             nl = tphase["negcount_launches"]
-            f = fl.negcount_flops(stats, n, wdiv) / nl
+            f = fl.negcount_flops(stats, n) / nl
+            f_sv = fl.negcount_flops(stats, n, wdiv_survey) / nl
             cands.append(("k_negcount_seg (x-NegCount rounds: segmented root chains; child rounds k_negcount_seg_xg/tma)",
-                          "k_negcount", launch_ms, f))
+                          "k_negcount", launch_ms, f, f_sv))
         if rq_n:
             launch_ms = rq_ms / rq_n
-            f = fl.rqi_flops(stats, n, wdiv) / nrq
+            f = fl.rqi_flops(stats, n) / nrq
             cands.append(("singleton RQI + eigenvectors (k_twist_lane, k_fixed_chunk, k_zwrite_chunk; k_rqi2 for hand-overs)",
-                          "k_fixed_chunk", launch_ms, f))
+                          "k_fixed_chunk", launch_ms, f, f))
         out = []
-        for name, pref, launch_ms, f in cands:
+        for name, pref, launch_ms, f, f_sv in cands:
             ach = f / (launch_ms * 1e-3) / 1e12
             tr, trs, pipe = ncu_traffic(pref, cfg.name)
             out.append({"bound": "alu", "kernel": name, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                         "frac": ach / peak, "traffic": tr, "traffic_src": trs, "peak_src": src,
                         "launch_ms": launch_ms, "flops_per_launch": f, "ncu_fp64_pipe_pct": pipe,
-                        "note": "achieved = algorithmic FP64 slots (IEEE divisions weighted w_div = measured "
-                                "__ddiv_rn cost) x 2 / launch time; the kernels divide with a verified fast "
-                                "path of 8 FP64 slots, so frac can exceed the FP64-pipe busy fraction (ncu)"})
+                        "frac_survey_wdiv": f_sv / (launch_ms * 1e-3) / 1e12 / peak,
+                        "note": "achieved = algorithmic FP64 slots at their issued cost (IEEE division = 8 slots) x 2 "
+                                "/ launch time; frac_survey_wdiv weights each division by the measured __ddiv_rn "
+                                f"cost (w_div = {wdiv_survey}) instead"})
         roof = out[0] if out else None
         roof_other = out[1:] if len(out) > 1 else None
         # whole-solve roofline as the north_star defines it: the slower of (counted FP64 operations, divisions
         # weighted by their issue cost, at peak) and (the Z bytes at HBM bandwidth), against the step time
-        ftot = fl.negcount_flops(stats, n, wdiv) + fl.rqi_flops(stats, n, wdiv)
+        ftot = fl.negcount_flops(stats, n) + fl.rqi_flops(stats, n)
+        ftot_sv = fl.negcount_flops(stats, n, wdiv_survey) + fl.rqi_flops(stats, n)
         t_fp = ftot / (peak * 1e12)
         zb = 8.0 * k * n
         t_hbm = zb / (pk.get("hbm_gbs", 6550.0) * 1e9)
@@ -318,8 +323,12 @@ def main():
         roof_step = {"bound": "alu" if t_fp >= t_hbm else "hbm", "flops": ftot, "z_bytes": zb,
                      "t_fp64_ms": t_fp * 1e3, "t_hbm_ms": t_hbm * 1e3, "ms_per_step": ms_max,
                      "frac": t_bound * 1e3 / ms_max,
-                     "note": "whole solve: algorithmic FP64 slots (x-NegCount shared-tree nodes, RQI passes) vs "
-                             "Z write bytes; frac = bound time / measured step time"}
+                     "frac_survey_wdiv": max(ftot_sv / (peak * 1e12), t_hbm) * 1e3 / ms_max,
+                     "note": "whole solve: algorithmic FP64 slots at issue cost (x-NegCount shared-tree nodes, RQI "
+                             "passes) vs Z write bytes; frac = bound time / measured step time"}
+        for r_ in out + [roof_step]:
+            if r_["frac"] > 1.0:
+                raise SystemExit(f"roofline accounting error: frac {r_['frac']:.3f} > 1 for {r_.get('kernel', 'step')}")
 
     e2e = None
     if world == 1 and not args.no_e2e:

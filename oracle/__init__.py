@@ -34,7 +34,8 @@ def build(force: bool = False) -> str:
 
 
 class _Opts(C.Structure):
-    _fields_ = [("gaptol", C.c_double), ("seed", C.c_uint64), ("root_side", C.c_int32), ("threads", C.c_int32)]
+    _fields_ = [("gaptol", C.c_double), ("seed", C.c_uint64), ("root_side", C.c_int32), ("threads", C.c_int32),
+                ("roots_only", C.c_int32)]
 
 
 class _Diag(C.Structure):
@@ -97,6 +98,8 @@ def lib():
         L.oracle_jacobi.restype = None
         L.oracle_jacobi.argtypes = [_i64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.oracle_maxd.restype = C.c_int
+        L.oracle_negcount_x_many.restype = None
+        L.oracle_negcount_x_many.argtypes = [_i64, C.c_void_p, C.c_void_p, _i64, C.c_void_p, C.c_void_p]
         L.oracle_jacobi_ldl.restype = None
         L.oracle_jacobi_ldl.argtypes = [_i64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.oracle_stats_read.restype = None
@@ -148,8 +151,9 @@ class OracleResult:
 
 
 def mrrr(d, e, il: int | None = None, iu: int | None = None, *, gaptol: float = 1e-10, seed: int = 0,
-         root_side: int = 0, threads: int = 0) -> OracleResult:
-    """Eigenpairs il..iu (1-based, inclusive) of the tridiagonal (d, e) by the oracle."""
+         root_side: int = 0, threads: int = 0, roots_only: bool = False) -> OracleResult:
+    """Eigenpairs il..iu (1-based, inclusive) of the tridiagonal (d, e) by the oracle.  roots_only: stop after
+    the root bisection (S1-S5): only nblocks/block_start/mu/side/root_lo/root_hi/root_gstart are filled."""
     d = _f64(d)
     n = d.size
     e = _f64(e) if n > 1 else np.zeros(1)
@@ -174,7 +178,7 @@ def mrrr(d, e, il: int | None = None, iu: int | None = None, *, gaptol: float = 
     fhi = np.zeros(k)
     st = np.zeros(16, np.int64)
     dg = _Diag(*[_ptr(a) for a in (nblocks, bstart, mu, side, rlo, rhi, rgs, depth, gf, gl, flo, fhi, st)])
-    op = _Opts(gaptol, seed, root_side, threads)
+    op = _Opts(gaptol, seed, root_side, threads, int(roots_only))
     info = L.oracle_mrrr(n, _ptr(d), _ptr(e), il, iu, C.byref(op), _ptr(W), _ptr(Z), n, C.byref(dg))
     nbk = int(nblocks[0])
     return OracleResult(W=W, Z=Z.T, info=info, nblocks=nbk, block_start=bstart[:nbk + 1].copy(),
@@ -210,6 +214,13 @@ def gershgorin(d, e):
 def negcount_x(dx, dllx, sigma: float) -> int:
     dx, dllx = _f64(dx), _f64(dllx)
     return lib().oracle_negcount_x(dx.size, _ptr(dx), _ptr(dllx), sigma)
+
+
+def negcount_x_many(dx, dllx, sigmas) -> np.ndarray:
+    dx, dllx, sg = _f64(dx), _f64(dllx), _f64(sigmas)
+    out = np.zeros(sg.size, np.int64)
+    lib().oracle_negcount_x_many(dx.size, _ptr(dx), _ptr(dllx), sg.size, _ptr(sg), _ptr(out))
+    return out
 
 
 def negcount_t(d, e, sigma: float, mu: float = 0.0) -> int:

@@ -52,6 +52,7 @@ typedef struct {
   uint64_t seed;      /* perturbation key, 0 -> DEFAULT_SEED */
   int32_t root_side;  /* 0 auto (S3 rule), 1 left, 2 right */
   int32_t threads;    /* 0 -> OpenMP default */
+  int32_t roots_only; /* 1: stop after S5 (split, roots, root bisection of the computed set; diagnostics only) */
 } oracle_opts;
 
 typedef struct {      /* every pointer optional */
@@ -173,6 +174,13 @@ static int64_t negcount_q(int64_t nb, const qreal *d, const qreal *dll, qreal si
   dp = d[nb - 1] + s;
   count += sbq(dp);
   return count;
+}
+
+/* test helper: oracle_negcount_x at many shifts (OpenMP over the shifts) */
+void oracle_negcount_x_many(int64_t nb, const double *d, const double *dll, int64_t ns, const double *sig,
+                            int64_t *counts) {
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t t = 0; t < ns; t++) counts[t] = oracle_negcount_x(nb, d, dll, sig[t]);
 }
 
 /* Alg. negcountT P:7055-7077 in binary128 on T - (mu + sigma) I (pin helper) */
@@ -787,6 +795,14 @@ static void root_bisect_one(blk_t *B, int64_t j, double rtol) {
   B->hi[j] = hi;
 }
 
+static int mrrr_scaled(int64_t n, const double *d, const double *e, int64_t il, int64_t iu, const oracle_opts *op,
+                       double *W, double *Z, int64_t ldz, oracle_diag *dg);
+
+/* S0 scaling (P:3026-3027 defers it; A-21): when the largest |entry| a = max(|alpha_i|, |beta_i|)  */
+/* lies outside [2^-500, 2^500] the solve runs on 2^s T with 2^s a in [1/2, 1) (so 2^s ||T||_1 < 3) -- a     */
+/* power of two, so every step of the scaled solve is the exact image of the unscaled one away from         */
+/* over/underflow -- and W is scaled back by 2^-s (Z is scale invariant).  Diagnostics (mu, intervals) stay  */
+/* in the scaled frame.                                                                                      */
 int oracle_mrrr(int64_t n, const double *d, const double *e, int64_t il, int64_t iu, const oracle_opts *op,
                 double *W, double *Z, int64_t ldz, oracle_diag *dg) {
   if (n < 1) return -4;
@@ -795,6 +811,27 @@ int oracle_mrrr(int64_t n, const double *d, const double *e, int64_t il, int64_t
   if (!d || (n > 1 && !e)) return -2;
   if (ldz < n) return -9;
   for (int64_t i = 0; i < n; i++) if (!isfinite(d[i]) || (i < n - 1 && !isfinite(e[i]))) return 1;
+  double amax = 0;
+  for (int64_t i = 0; i < n; i++) amax = dmax(amax, fabs(d[i]));
+  for (int64_t i = 0; i < n - 1; i++) amax = dmax(amax, fabs(e[i]));
+  if (amax == 0 || (amax >= 0x1p-500 && amax <= 0x1p500))
+    return mrrr_scaled(n, d, e, il, iu, op, W, Z, ldz, dg);
+  int ex;
+  frexp(amax, &ex);   /* amax = f 2^ex, f in [1/2, 1) */
+  double *ds = malloc(sizeof(double) * n), *es = malloc(sizeof(double) * (n > 1 ? n - 1 : 1));
+  for (int64_t i = 0; i < n; i++) ds[i] = ldexp(d[i], -ex);
+  for (int64_t i = 0; i < n - 1; i++) es[i] = ldexp(e[i], -ex);
+  int rc = mrrr_scaled(n, ds, es, il, iu, op, W, Z, ldz, dg);
+  if (rc == 0)
+    for (int64_t j = 0; j < iu - il + 1; j++) W[j] = ldexp(W[j], ex);
+  free(ds);
+  free(es);
+  return rc;
+}
+
+/* the solve proper (S1-S10) on an input with ||T||_1 in range (or 0) */
+static int mrrr_scaled(int64_t n, const double *d, const double *e, int64_t il, int64_t iu, const oracle_opts *op,
+                       double *W, double *Z, int64_t ldz, oracle_diag *dg) {
   double gaptol = (op && op->gaptol > 0) ? op->gaptol : DEFAULT_GAPTOL;
   uint64_t seed = (op && op->seed) ? op->seed : DEFAULT_SEED;
   int force = op ? op->root_side : 0;
@@ -878,6 +915,18 @@ int oracle_mrrr(int64_t n, const double *d, const double *e, int64_t il, int64_t
       root_bisect_one(X, X->cb, rtol);
     }
     X->hi[0] = NAN;
+  }
+
+  if (op && op->roots_only) {
+    for (int64_t b = 0; b < nblk; b++) {
+      blk_t *X = &B[b];
+      if (dg && dg->root_lo)
+        for (int64_t j = X->ca; j <= X->cb; j++) { dg->root_lo[X->s + j - 1] = X->lo[j]; dg->root_hi[X->s + j - 1] = X->hi[j]; }
+      if (dg && dg->root_gstart)
+        for (int64_t j = X->ca; j <= X->cb; j++)
+          dg->root_gstart[X->s + j - 1] = (j == X->ca) ? 1 : oracle_is_boundary(X->lo[j - 1], X->hi[j - 1], X->lo[j], X->hi[j], gaptol);
+    }
+    goto done;
   }
 
   /* S4: selection -> output columns */

@@ -227,6 +227,12 @@ struct SegOut {
   int cnt, ok;
 };
 
+// Staged rows per tile: 2 x 512 rows x 16 B = 16 KB per CTA, so that the register limit (64 per thread: 8 CTAs of
+// 128 threads per SM) and not shared memory bounds residency -- a round's grid then fits in one wave of
+// 148 x 8 CTAs (with 1024-row tiles, 33 KB per CTA, only 6 fit and a 1024-CTA round ran 1.15 waves)
+#ifndef SEG_TILE
+#define SEG_TILE 512
+#endif
 // CH chains per thread (chains c0 + j * 128 of the CTA's 128 * CH): the CTA's chains all run segment k
 // over the same staged rows, so a thread interleaves CH independent recurrences on one shared-memory
 // row load (instruction-level parallelism where a round has few chains, fewer loads per step)
@@ -238,7 +244,7 @@ __global__ void __launch_bounds__(128) k_negcount_seg(const Node *__restrict__ n
                                                       SegOut *seg, const int *__restrict__ dnn, int mmax,
                                                       long long target) {
   extern __shared__ __align__(128) unsigned char neg_smem[];
-  double2 *buf = reinterpret_cast<double2 *>(neg_smem);  // [2][NEG_TILE]
+  double2 *buf = reinterpret_cast<double2 *>(neg_smem);  // [2][SEG_TILE]
   __shared__ __align__(8) uint64_t bar[2];
   if (dnn) {  // device-driven round: node count and depth from the previous round
     nnode = *dnn;
@@ -271,14 +277,14 @@ __global__ void __launch_bounds__(128) k_negcount_seg(const Node *__restrict__ n
   const int w0 = (k == 0) ? 0 : max(bk - Wu, 0);
   const int r1 = (k == K - 1) ? nb : ek;  // staged rows [w0, r1): the last segment also stages row nb-1
   const int nrow = r1 - w0;
-  const int ntile = (nrow + NEG_TILE - 1) / NEG_TILE;
+  const int ntile = (nrow + SEG_TILE - 1) / SEG_TILE;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     for (int t = 0; t < 2 && t < ntile; t++) {
-      int len = min(NEG_TILE, nrow - t * NEG_TILE);
-      tma_load_1d(buf + t * NEG_TILE, M + w0 + (long long)t * NEG_TILE, (unsigned)(len * sizeof(double2)), &bar[t]);
+      int len = min(SEG_TILE, nrow - t * SEG_TILE);
+      tma_load_1d(buf + t * SEG_TILE, M + w0 + (long long)t * SEG_TILE, (unsigned)(len * sizeof(double2)), &bar[t]);
     }
   }
   __syncthreads();
@@ -294,9 +300,9 @@ __global__ void __launch_bounds__(128) k_negcount_seg(const Node *__restrict__ n
   for (int t = 0; t < ntile; t++) {
     const int b = t & 1;
     mbar_wait(&bar[b], (unsigned)((t >> 1) & 1));
-    const double2 *T = buf + b * NEG_TILE;
-    const int row0 = w0 + t * NEG_TILE;
-    const int len = min(NEG_TILE, ek - row0);  // recurrence steps in this tile (rows < ek)
+    const double2 *T = buf + b * SEG_TILE;
+    const int row0 = w0 + t * SEG_TILE;
+    const int len = min(SEG_TILE, ek - row0);  // recurrence steps in this tile (rows < ek)
     int kk = 0;
     // warm-up rows (before bk): no counting
     const int nw = max(0, min(len, bk - row0));
@@ -334,8 +340,8 @@ __global__ void __launch_bounds__(128) k_negcount_seg(const Node *__restrict__ n
     }
     __syncthreads();
     if (threadIdx.x == 0 && t + 2 < ntile) {
-      int len2 = min(NEG_TILE, nrow - (t + 2) * NEG_TILE);
-      tma_load_1d(buf + b * NEG_TILE, M + w0 + (long long)(t + 2) * NEG_TILE, (unsigned)(len2 * sizeof(double2)),
+      int len2 = min(SEG_TILE, nrow - (t + 2) * SEG_TILE);
+      tma_load_1d(buf + b * SEG_TILE, M + w0 + (long long)(t + 2) * SEG_TILE, (unsigned)(len2 * sizeof(double2)),
                   &bar[b]);
     }
   }

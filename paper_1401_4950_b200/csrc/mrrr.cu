@@ -130,6 +130,7 @@ struct mrrr_ctx {
   int max_nodes = 0;           // bound on live bisection nodes (indices in the computed set)  // tube point budgets: no estimate (4 full levels) / with estimate
   bool rqi_pair = true;
   bool l2_persist = true;
+  long long rqi_seg_min = 2048; // root blocks up to this size skip the segmented RQI (MRRR_RQISEGMIN)
   int fault = 0;               // MRRR_FAULT: fault injection for the GPU tests (k_rqi2: bit 0 fallback, bit 1 careful)
   long long l2_max_window = 0;
 
@@ -143,7 +144,8 @@ struct mrrr_ctx {
   Buf rqst, rqrec, hand;                  // segmented RQI state, segment records, handed-over singletons
   std::vector<cudaEvent_t> rev;           // events around device-driven rounds
   Buf nodesA, nodesB, counts, ex, excounts, exmap, bnA, bnB, sing, clusA, clusB, ss, gval, valid, cseg, bnoff,
-      ipool_lo, ipool_hi, yref_lo, yref_hi, wsA, wsB, stats, cnt, ddepth, dgf, dgl, dflo, dfhi, hd, he, hW, hZ, zmeta;
+      ipool_lo, ipool_hi, yref_lo, yref_hi, wsA, wsB, stats, cnt, ddepth, dgf, dgl, dflo, dfhi, hd, he, hW, hZ, zmeta,
+      hd2;
   int *h_cnt = nullptr;  // pinned counters
 
   // results of the last call
@@ -292,6 +294,13 @@ __global__ void k_selftest_div(long long n, uint64_t seed, unsigned long long *b
   if (div_range_ok(a, b, q3) && __double_as_longlong(q3) != __double_as_longlong(q2) && !(isnan(q3) && isnan(q2)))
     same = false;
   if (!same) atomicAdd(bad, 1ull);
+}
+
+// base segment count of the segmented root rounds for a chain of nb rows: seg_k when a segment spans at least
+// 2 warm-ups, else 1 (whole chains).  Short chains are not cut further: C1's 1-2-1 recurrence does not contract
+// (no localisation), so its segments never verify (measured: 3 segments at n = 1000 fell back, 6x slower).
+int seg_base_k(mrrr_t h, long long nb) {
+  return (nb - 1) >= 2LL * h->seg_k * h->seg_w ? h->seg_k : 1;
 }
 
 void launch_check(mrrr_t h) {
@@ -472,7 +481,7 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
   const long long maxch = mcap > 0 ? (long long)maxnodes * ((1LL << mcap) - 1)
                                    : std::max<long long>(h->target_chains, maxnodes) + 128;
   // segments per chain: the host rounds' rule (more segments while the rounds have few chains)
-  int K = h->seg_k;
+  int K = seg_base_k(h, nb);
   while (2 * K <= 64 && maxch * 2 * K <= h->seg_threads && (nb - 1) >= 2 * (2 * K) * h->seg_w &&
          (nb - 1) / (2 * K) >= h->seg_minlen)
     K *= 2;
@@ -505,7 +514,7 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
     for (int b = 0; b < RB && r < MAXR; b++, r++) {
       Node *in = (r & 1) ? nxt : cur, *out = (r & 1) ? cur : nxt;
       CK(cudaEventRecord(h->rev[2 * r], h->stream));
-      k_negcount_seg<1><<<gseg, 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
+      k_negcount_seg<1><<<gseg, 128, 2 * SEG_TILE * sizeof(double2), h->stream>>>(
           in, 0, 0, nullptr, 0, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L, h->seg_w, h->segout.as<SegOut>(),
           nn + r, mmax, h->target_chains);
       CK(cudaEventRecord(h->rev[2 * r + 1], h->stream));
@@ -616,7 +625,7 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
   }
   Node *cur = h->nodesA.as<Node>(), *nxt = h->nodesB.as<Node>();
   bool first = true;
-  const bool seg_on = !Y && single_nb > 0 && h->neg_tma && h->seg_k > 1 && (single_nb - 1) >= 2 * h->seg_k * h->seg_w;
+  const bool seg_on = !Y && single_nb > 0 && h->neg_tma && seg_base_k(h, single_nb) > 1;
   const long long target = seg_on ? h->target_chains
                           : (Y && h->segy_k > 1) ? h->target_y
                           : (rep0 >= 0) ? h->target_child
@@ -636,7 +645,7 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
       // Rounds with few chains (one point per node) cut them into more segments, so that about
       // seg_threads threads keep the SMs busy (a round is latency-bound below that)
       const long long tot = nch + nex;
-      int K = h->seg_k;
+      int K = seg_base_k(h, single_nb);
       while (2 * K <= 64 && tot * 2 * K <= h->seg_threads && (single_nb - 1) >= 2 * (2 * K) * h->seg_w &&
              (single_nb - 1) / (2 * K) >= h->seg_minlen)
         K *= 2;
@@ -645,11 +654,11 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
       const int CH = (tot <= h->seg_ch2) ? 2 : 1;  // few chains: two per thread (ILP)
       const unsigned grid = (unsigned)((tot + 128 * CH - 1) / (128 * CH) * K);
       if (CH == 2)
-        k_negcount_seg<2><<<grid, 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
+        k_negcount_seg<2><<<grid, 128, 2 * SEG_TILE * sizeof(double2), h->stream>>>(
             cur, nnode, m, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L,
             h->seg_w, h->segout.as<SegOut>(), nullptr, 0, 0);
       else
-        k_negcount_seg<1><<<grid, 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
+        k_negcount_seg<1><<<grid, 128, 2 * SEG_TILE * sizeof(double2), h->stream>>>(
             cur, nnode, m, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L,
             h->seg_w, h->segout.as<SegOut>(), nullptr, 0, 0);
       launch_check(h);
@@ -1142,15 +1151,38 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
   CK(cudaMemsetAsync(h->stats.p, 0, sizeof(long long) * ST_N, st));
   CK(cudaEventRecord(h->ev[0], st));
 
-  // S1/S2
+  // S1/S2 (and the S0 scale test: the largest |entry| comes out of the same pass)
+  struct ScalRec { int nblk, err; double tnorm, amax; };
   k_split<1024><<<1, 1024, 0, st>>>(d, e, n, h->starts.as<int>(), h->scal.as<int>(), (double *)(h->scal.as<char>() + 8),
-                                    h->scal.as<int>() + 1);
+                                    h->scal.as<int>() + 1, (double *)(h->scal.as<char>() + 16));
   launch_check(h);
-  int hs[2];
-  CK(cudaMemcpyAsync(hs, h->scal.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  ScalRec hs;
+  CK(cudaMemcpyAsync(&hs, h->scal.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  if (hs[1]) return MRRR_ERR_NONFINITE;
-  const int nblk = hs[0];
+  if (hs.err) return MRRR_ERR_NONFINITE;
+  // S0 scaling (A-21): max |entry| outside [2^-500, 2^500] -> solve 2^-ex T (exact power of two,
+  // max |entry| in [1/2, 1)) and scale W back at the end; Z is scale invariant
+  int scale_ex = 0;
+  if (hs.amax != 0.0 && (hs.amax < 0x1p-500 || hs.amax > 0x1p500)) {
+    std::frexp(hs.amax, &scale_ex);
+    CK(h->hd2.ensure(sizeof(double) * 2 * n));
+    double *ds = h->hd2.as<double>(), *es = ds + n;
+    k_scale2<<<nblocks_for(n, 256), 256, 0, st>>>(d, ds, n, -scale_ex);
+    if (n > 1) k_scale2<<<nblocks_for(n - 1, 256), 256, 0, st>>>(e, es, n - 1, -scale_ex);
+    d = ds;
+    e = es;
+    k_split<1024><<<1, 1024, 0, st>>>(d, e, n, h->starts.as<int>(), h->scal.as<int>(),
+                                      (double *)(h->scal.as<char>() + 8), h->scal.as<int>() + 1,
+                                      (double *)(h->scal.as<char>() + 16));
+    launch_check(h);
+    CK(cudaMemcpyAsync(&hs, h->scal.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  struct ScaleBack {  // W of the computed columns back to the input's scale on every successful return path
+    mrrr_t h; double *W; long long cnt; int ex;
+    void run() { if (ex && cnt > 0) k_scale2<<<nblocks_for(cnt, 256), 256, 0, h->stream>>>(W, W, cnt, ex); }
+  } scale_back{h, W, 0, scale_ex};
+  const int nblk = hs.nblk;
   h->last_nblk = nblk;
   h->h_starts.assign(nblk + 1, 0);
   if (nblk == 1) { h->h_starts[0] = 0; h->h_starts[1] = (int)n; }
@@ -1362,7 +1394,9 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
   CK(cudaEventRecord(h->ev[3], st));
 
   // S9/S10 root singletons
-  run_rqi(h, ns, nbmax, W, Z, ldz, true);
+  // short root blocks: the two-lane kernel directly (chains are short; oscillatory vectors such as C1's defeat the
+  // segmented twist search, which would hand every singleton over after a wasted pass)
+  run_rqi(h, ns, nbmax, W, Z, ldz, nbmax > h->rqi_seg_min);
   CK(cudaEventRecord(h->ev[4], st));
   // S8 clusters (depth-first, chunked)
   if (ncl > 0) {
@@ -1382,6 +1416,9 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
                                                       h->rhi.as<double>());
     launch_check(h);
   }
+  scale_back.cnt = kout;
+  scale_back.run();
+  launch_check(h);
   CK(cudaEventRecord(h->ev[5], st));
   CK(cudaStreamSynchronize(st));
   // stats
@@ -1483,6 +1520,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;
     if (const char *s = getenv("MRRR_L2PIN")) h->l2_persist = atoi(s) != 0;
     if (const char *s = getenv("MRRR_FAULT")) h->fault = atoi(s);
+    if (const char *s = getenv("MRRR_RQISEGMIN")) h->rqi_seg_min = atoll(s);
     {
       int dev = h->device, maxwin = 0, l2 = 0;
       cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
@@ -1810,7 +1848,7 @@ int mrrr_destroy(mrrr_t h) {
                  &h->excounts, &h->exmap, &h->bnA, &h->bnB, &h->sing, &h->clusA, &h->clusB, &h->ss, &h->gval,
                  &h->valid, &h->cseg, &h->bnoff, &h->ipool_lo, &h->ipool_hi, &h->yref_lo, &h->yref_hi, &h->wsA,
                  &h->wsB, &h->stats, &h->cnt, &h->ddepth, &h->dgf, &h->dgl, &h->dflo, &h->dfhi,
-                 &h->hd, &h->he, &h->hW, &h->hZ, &h->zmeta};
+                 &h->hd, &h->he, &h->hW, &h->hZ, &h->zmeta, &h->hd2};
   for (Buf *b : bufs) b->release();
   for (auto &ev : h->ev) cudaEventDestroy(ev);
   for (auto &ev : h->rev) cudaEventDestroy(ev);

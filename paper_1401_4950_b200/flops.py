@@ -36,13 +36,21 @@ def rqi_flops(stats: dict, n: int, w_div: float = 0.0) -> float:
     return 2.0 * rqi_slots(stats, w_div)
 
 
-# x-NegCount (Alg. negcountLDL) per element: dp = d + s (DADD), q = s / dp (one IEEE
-# division = w_div DFMA slots, measured), s = q * dll - sigma (DMUL + DADD): 3 + w_div slots.
-def negcount_slots_per_element(w_div: float) -> float:
+# x-NegCount (Alg. negcountLDL) per element: dp = d + s (DADD), q = s / dp (one IEEE division),
+# s = q * dll - sigma (DMUL + DADD).  The division is counted at the cost the kernels ISSUE for it (north_star:
+# "divisions weighted by their issue cost"): div_fast_nocheck (csrc/kernels.cuh) = 7 DFMA + 1 DMUL on the FP64
+# pipe (+ one MUFU.RCP64H seed on the XU pipe, not an FP64 slot) -> 3 + 8 = 11 FP64 slots per element.  The
+# survey's weighting by the measured cost of a compiler __ddiv_rn (w_div = 13.07 slots, profiles/fp64_peak_r01.json)
+# is reported beside it but is not the roofline (it credits work the kernel does not issue).
+W_DIV_ISSUE = 8.0
+
+
+def negcount_slots_per_element(w_div: float = W_DIV_ISSUE) -> float:
     return 3.0 + w_div
 
 
-def negcount_flops(stats: dict, nb: int, w_div: float) -> float:
-    """Algorithmic flops of the x-NegCount evaluations on the sequential bisection paths (shared-tree
-    nodes, stats['negcount_x_alg']); k-section points off the path are speculative and not counted."""
+def negcount_flops(stats: dict, nb: int, w_div: float = W_DIV_ISSUE) -> float:
+    """Algorithmic flops (2 per FP64 slot) of the x-NegCount evaluations on the sequential bisection paths
+    (shared-tree nodes, stats['negcount_x_alg']); k-section points off the path are speculative and not
+    counted."""
     return 2.0 * stats["negcount_x_alg"] * nb * negcount_slots_per_element(w_div)

@@ -21,6 +21,12 @@ KEYS = {
     "block": "launch__block_size",
     "l2_hit_pct": "lts__t_sector_hit_rate.pct",
     "sm_mhz": "sm__cycles_elapsed.avg.per_second",
+    # executed FP64 instruction mix (thread-level, predicated on) and the XU pipe (MUFU.RCP64H seeds)
+    "dfma_thread_inst": "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
+    "dadd_thread_inst": "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
+    "dmul_thread_inst": "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
+    "xu_warp_inst": "sm__inst_executed_pipe_xu.sum",
+    "fp64_warp_inst": "sm__inst_executed_pipe_fp64.sum",
 }
 SCALE = {"dram_read": 1, "dram_write": 1}
 
@@ -51,6 +57,8 @@ def main():
                 x *= {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "msecond": 1, "ms": 1, "nsecond": 1e-6}.get(un, 1)
             e[k] = x
         e["dram_bytes"] = e.get("dram_read", 0.0) + e.get("dram_write", 0.0)
+        if "dfma_thread_inst" in e:
+            e["fp64_thread_inst"] = e["dfma_thread_inst"] + e.get("dadd_thread_inst", 0.0) + e.get("dmul_thread_inst", 0.0)
         res["launches"].append(e)
     json.dump(res, open(out, "w"), indent=1)
     for e in res["launches"]:

@@ -3,8 +3,8 @@
 Bit-exact: block starts, mu and side per block, root intervals (fp64 bits), root group
 starts, group extents per depth, final-node intervals.  Toleranced (north_star): |W - W_oracle| <=
 8 n eps ||T||, max ||T z - lambda z|| <= n eps ||T||, max |Z^T Z - I| <= n eps (n -> max(n, 32), A-27).
-Full-size configs are compared on the oracle's windows of the same all-pairs solve (root side forced to
-the GPU run's side), plus properties that hold at any size.
+C1 and C2 are compared in full against a live oracle run here; C3, C4, C5a and C5b in full against stored
+oracle results in tests/test_gpu_fullsize.py.
 """
 import numpy as np
 import pytest
@@ -61,12 +61,12 @@ def check_integers(g, r, cols=None, positions=None):
     assert same(dg.grp_last[:, cols], r.grp_last)
     assert same(dg.depth[cols], r.depth)
     mism = ~((dg.fin_lo[cols] == r.fin_lo) & (dg.fin_hi[cols] == r.fin_hi))
-    # child intervals depend on fl64 of y-computed data (dd vs binary128): report, allow a 2^-40 fraction
+    # child intervals depend on fl64 of y-computed data (dd vs binary128): equal unless a datum lies within
+    # ~2^-100 of a rounding boundary (~2^-47 per datum); zero mismatches allowed, any is printed
     if np.any(mism):
         idx = np.nonzero(mism)[0]
-        print("final-interval mismatches at", idx[:10], "depths", dg.depth[cols][idx[:10]])
-    assert np.all(dg.depth[cols][mism] > 0)
-    assert mism.sum() <= max(1, mism.size // 1000)
+        print("final-interval mismatches at", idx[:20], "depths", dg.depth[cols][idx[:20]])
+    assert mism.sum() == 0
 
 
 def check_tol(d, e, W, Z, Wref, tn):
@@ -155,6 +155,23 @@ def test_parity_split_threshold_exact(torch_cuda):
         r = oracle.mrrr(d, e)
         assert g["diag"].nblocks == r.nblocks == nblk
         check_integers(g, r)
+
+
+@pytest.mark.parametrize("s", [600, -600, 1022, -1040])
+def test_scaled_inputs(torch_cuda, s):
+    # max |entry| outside [2^-500, 2^500] (A-21): solved on 2^-e T, W scaled back -- the same as the oracle's
+    # exact power-of-two image, and Z equal to the unscaled solve's
+    d, e = mi.random_tridiag(700, 19, -1.0)
+    ds, es = np.ldexp(d, s), np.ldexp(e, s)
+    g = gpu_solve(torch_cuda, ds, es)
+    r = oracle.mrrr(ds, es)
+    assert r.info == 0
+    check_integers(g, r)
+    d1, e1 = np.ldexp(ds, -s), np.ldexp(es, -s)
+    g1 = gpu_solve(torch_cuda, d1, e1, diag=False)
+    assert np.array_equal(g["Z"], g1["Z"])
+    assert np.array_equal(g["W"], np.ldexp(g1["W"], s))
+    assert np.array_equal(r.W, g["W"]) or np.max(np.abs(np.ldexp(g["W"] - r.W, -s))) <= 8 * 700 * EPS * 3
 
 
 def test_error_codes(torch_cuda):
@@ -247,56 +264,14 @@ def test_config_full_parity(torch_cuda, cfg):
     big = torch_cuda.nonzero(G.abs() > 0.25 * c.n * EPS).cpu().numpy()
     assert oracle.ortho_pairs(g["Z"], big[:, 0], big[:, 1]) <= c.n * EPS if big.size else True
     assert float(G.abs().max()) <= 1.5 * c.n * EPS
-
-
-@pytest.mark.parametrize("cfg", ["C3", "C4", "C5b", "C5a"])
-def test_config_sampled_parity(torch_cuda, cfg):
-    c = mi.CONFIGS[cfg]
-    d, e = c.matrix()
-    g = gpu_solve(torch_cuda, d, e, c.il, c.iu)
-    dg = g["diag"]
-    side = int(dg.side[0])
-    tn = max(abs(g["W"][0]), abs(g["W"][-1])) if c.k == c.n else 2.5
-    width = 6 if c.n > 30000 else 8
-    for a, b in _windows(c.k, 3, width, 7):
-        r = oracle.mrrr(d, e, c.il + a - 1, c.il + b - 1, root_side=side)
-        cols = slice(a - 1, b)
-        pos = np.nonzero(~np.isnan(r.root_lo))[0]
-        # the window's leftmost computed index is a guard: its group start is 1 by convention (S6)
-        check_integers(g, r, cols=cols, positions=pos)
-        assert np.max(np.abs(g["W"][cols] - r.W)) <= 8 * c.n * EPS * tn
-        Zw = g["Zd"][:, cols].cpu().numpy()
-        res = oracle.residuals(d, e, g["W"][cols], Zw).max()
-        assert res <= c.n * EPS * tn
-        # same vectors as the oracle's up to the stated tolerance (singletons: entrywise close)
-        sing = r.depth == 0
-        if np.any(sing):
-            dz = np.abs(np.abs(Zw[:, sing]) - np.abs(r.Z[:, sing])).max()
-            assert dz <= 1e-6, dz
-    # properties at full size: Sturm-count invariant of every root interval, ascending W, unit norms
-    W = g["W"]
-    assert np.all(np.diff(W) >= 0)
-    Zt = g["Zd"]
-    nrm = (Zt * Zt).sum(0).sqrt().cpu().numpy()
-    assert np.max(np.abs(nrm - 1)) <= 4 * np.sqrt(c.n) * EPS
-    # sampled orthogonality block vs all columns (fp64 GEMM, re-check of flagged pairs in binary128)
-    rng = np.random.default_rng(1)
-    S = np.sort(rng.choice(c.k, min(256, c.k), replace=False))
-    G = Zt[:, S].T @ Zt
-    G[np.arange(S.size), S] -= 1.0
-    big = torch_cuda.nonzero(G.abs() > 0.25 * c.n * EPS).cpu().numpy()
-    if big.size:
-        big = big[:2000]
-        cols_needed = np.unique(np.concatenate([S[big[:, 0]], big[:, 1]]))
-        Zs = Zt[:, cols_needed].cpu().numpy()
-        rel = {cc: i for i, cc in enumerate(cols_needed)}
-        pi = np.array([rel[x] for x in S[big[:, 0]]])
-        pj = np.array([rel[x] for x in big[:, 1]])
-        assert oracle.ortho_pairs(Zs, pi, pj) <= c.n * EPS
-    assert float(G.abs().max()) <= 1.5 * c.n * EPS
-    # residuals of a sample of columns in binary128
-    cols = np.sort(rng.choice(c.k, min(64, c.k), replace=False))
-    assert oracle.residuals(d, e, W[cols], Zt[:, cols].cpu().numpy()).max() <= c.n * EPS * tn
+    # every vector (all singletons) vs the oracle's: Davis-Kahan, |z_gpu - z_oracle| <= 2 (rho_gpu + rho_or) / gap
+    rho_g = oracle.residuals(d, e, g["W"], g["Z"])
+    rho_o = oracle.residuals(d, e, r.W, r.Z)
+    gap = np.minimum(np.append(np.inf, np.diff(r.W)), np.append(np.diff(r.W), np.inf))
+    sgn = np.where(np.sum(g["Z"] * r.Z, axis=0) >= 0, 1.0, -1.0)
+    dz = np.max(np.abs(g["Z"] - r.Z * sgn), axis=0)
+    assert np.all(r.depth == 0)
+    assert np.all(dz <= 2 * (rho_g + rho_o) / gap + 8 * np.sqrt(c.n) * EPS)
 
 
 def test_division_fast_path_is_ieee(torch_cuda):

@@ -218,3 +218,37 @@ def test_auto_root_side_rule():
     r = oracle.mrrr(d, e, 291, 300)
     res = oracle.residuals(d, e, r.W, r.Z)
     assert res.max() <= 300 * EPS * spectral_norm(d, e)
+
+
+@pytest.mark.parametrize("s", [600, -600, 1000, -1000])
+def test_scaling_is_an_exact_power_of_two_image(s):
+    # inputs with max |entry| outside [2^-500, 2^500] are solved on 2^-e T (A-21); a power-of-two
+    # scale commutes with every fp operation away from over/underflow, so the result is the exact image
+    d, e = mi.random_tridiag(60, 8, -1.0)
+    r0 = oracle.mrrr(d, e)
+    r = oracle.mrrr(d * 2.0 ** s, e * 2.0 ** s)
+    assert r.info == 0
+    assert np.array_equal(r.W, r0.W * 2.0 ** s)
+    assert np.array_equal(r.Z, r0.Z)
+
+
+def test_scaling_extreme_inputs_vs_jacobi():
+    # entries near the overflow threshold (||T||_1 itself overflows) and deep in the subnormal range; the
+    # reference is binary128 Jacobi of the stored input brought back to O(1) by the exact inverse power of two
+    d, e = mi.random_tridiag(40, 9, -1.0)
+    for s in (1022, -1040):
+        ds, es = np.ldexp(d, s), np.ldexp(e, s)
+        r = oracle.mrrr(ds, es)
+        assert r.info == 0
+        d1, e1 = np.ldexp(ds, -s), np.ldexp(es, -s)     # exact (the input as stored, unscaled)
+        hi, _ = oracle.jacobi(d1, e1)
+        tn = max(abs(hi[0]), abs(hi[-1]))
+        # W is returned on the fp64 grid of the scaled-back values: subnormal outputs carry their own rounding
+        grid = 2.0 ** (-1074 - s) if s < 0 else 0.0
+        assert np.max(np.abs(np.ldexp(r.W, -s) - hi)) <= 8 * 40 * EPS * tn + grid
+        assert oracle.residuals(d1, e1, hi, r.Z).max() <= 40 * EPS * tn
+
+
+def test_zero_matrix():
+    r = oracle.mrrr(np.zeros(5), np.zeros(4))
+    assert r.info == 0 and np.array_equal(r.W, np.zeros(5)) and r.nblocks == 5

@@ -22,8 +22,12 @@ Recipes (DESIGN.md "Inputs"):
       glue e[201 b - 1] = 1e-10 for b = 1..127 (0-based e).
 * C5  random, n = 65536, seed 14014951: d ~ U[-1,1), e ~ U[0,1)
       (C5a all pairs, C5b indices 1..6553).
-* Small families (App. D), for property tests: Clement (Kac),
-  Hermite, Legendre, Laguerre (readings A-23 in DESIGN.md).
+* Families of App. D for the §8(f1) sweeps: 1-2-1, Clement (Kac), Wilkinson, Hermite, Legendre,
+  Laguerre (readings A-23 in DESIGN.md), and the two prescribed-spectrum families Uniform
+  (lambda_k = eps + (k-1)(1-eps)/(n-1)) and Geometric (lambda_k = eps^((n-k)/(n-1))), eps = 2^-53: T is the
+  Householder tridiagonal form (LAPACK dsytrd) of Q diag(lambda) Q^T with Q the orthogonal factor of a
+  seeded Gaussian matrix (the LAPACK test-matrix recipe the paper's Artificial set follows),
+  computed with one BLAS thread so that the bytes do not depend on the host.
 """
 from __future__ import annotations
 
@@ -106,6 +110,48 @@ def legendre(n: int):
 def laguerre(n: int):
     # diag (3,5,...,2n+1); off-diagonal (2,3,...,n) (A-23 extends the garbled n-2 list)
     return 2.0 * np.arange(1, n + 1, dtype=np.float64) + 1.0, np.arange(2, n + 1, dtype=np.float64)
+
+
+def _prescribed_spectrum(lam: np.ndarray, seed: int):
+    import scipy.linalg as sla
+    from threadpoolctl import threadpool_limits
+    n = lam.size
+    with threadpool_limits(limits=1):
+        g = np.random.default_rng(seed).standard_normal((n, n))
+        q, r = np.linalg.qr(g)
+        q = q * np.sign(np.diag(r))          # Haar-distributed orthogonal factor
+        a = (q * lam) @ q.T
+        a = (a + a.T) / 2
+        c, d, e, tau, info = sla.lapack.dsytrd(a, lower=1)
+    assert info == 0
+    return np.ascontiguousarray(d), np.ascontiguousarray(e)
+
+
+def uniform_spectrum(n: int, seed: int = 7239):
+    """Uniform family (App. D): eigenvalues eps + (k-1)(1-eps)/(n-1), k = 1..n."""
+    eps = 2.0 ** -53
+    k = np.arange(1, n + 1, dtype=np.float64)
+    return _prescribed_spectrum(eps + (k - 1) * (1 - eps) / (n - 1), seed)
+
+
+def geometric_spectrum(n: int, seed: int = 7242):
+    """Geometric family (App. D): eigenvalues eps^((n-k)/(n-1)), k = 1..n."""
+    eps = 2.0 ** -53
+    k = np.arange(1, n + 1, dtype=np.float64)
+    return _prescribed_spectrum(eps ** ((n - k) / (n - 1)), seed)
+
+
+# App. D families by name, each a function of n (Wilkinson: the odd size 2m+1 <= n+1)
+FAMILIES = {
+    "uniform": lambda n: uniform_spectrum(n),
+    "geometric": lambda n: geometric_spectrum(n),
+    "121": lambda n: one_two_one(n),
+    "clement": lambda n: clement(n),
+    "wilkinson": lambda n: wilkinson(n // 2),
+    "hermite": lambda n: hermite(n),
+    "legendre": lambda n: legendre(n),
+    "laguerre": lambda n: laguerre(n),
+}
 
 
 def sha256(d: np.ndarray, e: np.ndarray) -> str:

@@ -153,8 +153,14 @@ class Solver:
             W = torch.empty(k, dtype=torch.float64, device=d.device)
         if Z is None:
             Zt = torch.empty((k, n), dtype=torch.float64, device=d.device)
+        elif Z.dim() == 2 and tuple(Z.shape) == (n, k) and Z.stride() == (1, n):
+            Zt = Z.T  # a column-major (n, k) view (e.g. the Z returned by an earlier call)
+        elif Z.dim() == 2 and tuple(Z.shape) == (k, n) and Z.is_contiguous():
+            Zt = Z    # row j of the (k, n) buffer receives eigenvector j
         else:
-            Zt = Z.T if Z.shape == (n, k) else Z
+            raise MrrrError("Z must be a contiguous (k, n) buffer or a column-major (n, k) view")
+        if not (Zt.is_cuda and Zt.dtype == torch.float64) or (W is not None and W.numel() < k):
+            raise MrrrError("W, Z must be float64 CUDA buffers of k and k x n entries")
         ep = e.data_ptr() if (e is not None and e.numel()) else None
         rc = load().mrrr_eig(self._h, d.data_ptr(), ep, n, il, iu, W.data_ptr(), Zt.data_ptr(), n)
         _check(rc, "mrrr_eig")

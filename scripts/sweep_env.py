@@ -13,7 +13,12 @@ import torch  # noqa: E402
 import mrrr_inputs as mi  # noqa: E402
 import paper_1401_4950_b200 as m  # noqa: E402
 
-cfg = mi.CONFIGS[sys.argv[1]]
+if sys.argv[1].startswith("fam:"):  # fam:<family>:<n>, all pairs
+    _, fam, nn = sys.argv[1].split(":")
+    _d, _e = mi.FAMILIES[fam](int(nn))
+    cfg = mi.Config(f"{fam}{_d.size}", _d.size, 1, _d.size, lambda: (_d, _e), fam)
+else:
+    cfg = mi.CONFIGS[sys.argv[1]]
 reps = int(sys.argv[2])
 d, e = cfg.matrix()
 dt, et = torch.from_numpy(d).cuda(), torch.from_numpy(e).cuda()

@@ -131,6 +131,7 @@ struct mrrr_ctx {
   bool rqi_pair = true;
   bool l2_persist = true;
   long long rqi_seg_min = 2048; // root blocks up to this size skip the segmented RQI (MRRR_RQISEGMIN)
+  bool nonlocal = false;         // this solve's root rounds found non-contracting recurrences (see run_bisection)
   int fault = 0;               // MRRR_FAULT: fault injection for the GPU tests (k_rqi2: bit 0 fallback, bit 1 careful)
   long long l2_max_window = 0;
 
@@ -625,12 +626,12 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
   }
   Node *cur = h->nodesA.as<Node>(), *nxt = h->nodesB.as<Node>();
   bool first = true;
-  const bool seg_on = !Y && single_nb > 0 && h->neg_tma && seg_base_k(h, single_nb) > 1;
-  const long long target = seg_on ? h->target_chains
-                          : (Y && h->segy_k > 1) ? h->target_y
-                          : (rep0 >= 0) ? h->target_child
-                                        : h->target_unseg;
+  bool seg_on = !Y && single_nb > 0 && h->neg_tma && seg_base_k(h, single_nb) > 1 && !h->nonlocal;
   while (nnode > 0) {
+    const long long target = seg_on ? h->target_chains
+                            : (Y && h->segy_k > 1) ? h->target_y
+                            : (rep0 >= 0) ? h->target_child
+                                          : h->target_unseg;
     int m = 1;
     while (m < h->mmax && (long long)nnode * ((1LL << (m + 1)) - 1) <= target) m++;
     long long P = (1LL << m) - 1;
@@ -697,6 +698,14 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
     read_counters(h);
     h->host_rounds++;
     h->stats_h[Y ? ST_NEGY : ST_NEGX] += nch + nex;
+    if (seg_on && (long long)h->h_cnt[C_NFB] * 4 > nch + nex) {
+      // most segment junctions failed: the recurrence does not contract on this matrix (delocalised
+      // eigenvectors, e.g. the 1-2-1, Clement, Hermite and prescribed-spectrum families), so every chain fell
+      // back to its sequential tail; the remaining rounds run whole chains, and the singleton RQI skips its
+      // segmented passes (their twist search would hand every singleton over)
+      seg_on = false;
+      h->nonlocal = true;
+    }
     if (!Y) {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, h->nc0, h->nc1));
@@ -1137,6 +1146,7 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
   h->last_n = n;
   h->last_k = k;
   h->host_rounds = h->host_launches = 0;
+  h->nonlocal = false;
   h->rqi_ms = 0;
   h->rqi_launches = 0;
   h->neg_ms = 0;
@@ -1396,7 +1406,7 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
   // S9/S10 root singletons
   // short root blocks: the two-lane kernel directly (chains are short; oscillatory vectors such as C1's defeat the
   // segmented twist search, which would hand every singleton over after a wasted pass)
-  run_rqi(h, ns, nbmax, W, Z, ldz, nbmax > h->rqi_seg_min);
+  run_rqi(h, ns, nbmax, W, Z, ldz, nbmax > h->rqi_seg_min && !h->nonlocal);
   CK(cudaEventRecord(h->ev[4], st));
   // S8 clusters (depth-first, chunked)
   if (ncl > 0) {

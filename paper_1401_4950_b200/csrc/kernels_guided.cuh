@@ -16,27 +16,6 @@
 #pragma once
 #include "kernels.cuh"
 
-// split the node list into k-section nodes (K) and tube nodes (P); P nodes get their point budget in pad
-__global__ void k_node_split(const Node *__restrict__ nodes, int nnode, Node *K, int *nK, Node *P, int *nP,
-                             int bud_full, int bud_tube) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nnode) return;
-  Node nd = nodes[i];
-  if (node_isolated(nd)) {
-    nd.pad = (isinf(nd.u) || isnan(nd.est)) ? bud_full : bud_tube;
-    P[atomicAdd(nP, 1)] = nd;
-  } else {
-    K[atomicAdd(nK, 1)] = nd;
-  }
-}
-
-__global__ void k_tube_count(const Node *__restrict__ P, int nP, double rtol, int *offs) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nP) return;
-  const Node nd = P[i];
-  offs[i] = tube_enum(nd, rtol, nd.pad, -1, nullptr);
-}
-
 // exclusive scan of offs[0..n) in place, offs[n] = total; *total_out = total (one CTA)
 __global__ void __launch_bounds__(1024) k_scan_excl(int *offs, int n, int *total_out) {
   __shared__ int part[1024];
@@ -73,73 +52,6 @@ __device__ __forceinline__ double laguerre_est(double sig, double G, double H, d
   const double den = (G >= 0.0) ? G + disc : G - disc;
   if (den == 0.0) return NAN;
   return sig - N / den;
-}
-
-// Walk every tube node along its index's path through the evaluated midpoints; emit the finished
-// interval or the node where the path left the tube, with a new estimate from the two deepest points.
-__global__ void k_tube_update(const Node *__restrict__ P, int nP, const int *__restrict__ offs,
-                              const int *__restrict__ counts, const double *__restrict__ dS,
-                              const double *__restrict__ dG, const double *__restrict__ dH,
-                              const RepDesc *__restrict__ reps, Node *next, int *nnext, double *out_lo,
-                              double *out_hi, double rtol, unsigned long long *alg) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nP) return;
-  const Node nd = P[i];
-  const int j = nd.b;
-  const int base = offs[i];
-  const bool full = isinf(nd.u) || isnan(nd.est);
-  const double x1 = full ? -INFINITY : __dsub_rn(nd.est, nd.u), x2 = full ? INFINITY : __dadd_rn(nd.est, nd.u);
-  double L1 = nd.lo, H1 = nd.hi, L2 = nd.lo, H2 = nd.hi;
-  double wl = nd.lo, wu = nd.hi;
-  int cum = 0;
-  unsigned used = 0;
-  double s1 = NAN, G1 = NAN, H1v = NAN, s2 = NAN, G2 = NAN, H2v = NAN;
-  for (int l = 0; l < 1100; l++) {
-    if (!bis_continue(wl, wu, rtol)) {
-      out_lo[nd.obase + j] = wl;
-      out_hi[nd.obase + j] = wu;
-      if (used) atomicAdd(alg, (unsigned long long)used);
-      return;
-    }
-    if (!bis_continue(L1, H1, rtol) || !bis_continue(L2, H2, rtol)) break;
-    const double W = __dsub_rn(H1, L1);
-    const double q = __ddiv_rn(__dsub_rn(L2, L1), W);
-    if (!(q >= 0.0) || q > (double)nd.pad) break;
-    const int cnt = (int)q + 1;
-    if (cum + cnt > nd.pad) break;
-    if (wl < L1 || wl > L2) break;  // the path left the tube
-    const double o = __ddiv_rn(__dsub_rn(wl, L1), W);
-    const int idx = cum + (int)o;
-    const double w = bis_mid(wl, wu);
-    const int c = base + idx;
-    if (!(o >= 0.0) || idx >= cum + cnt || __double_as_longlong(dS[c]) != __double_as_longlong(w)) break;
-    used++;
-    s2 = s1; G2 = G1; H2v = H1v;
-    s1 = w; G1 = dG[c]; H1v = dH[c];
-    if (counts[c] < j) wl = w;
-    else wu = w;
-    cum += cnt;
-    const double w1 = bis_mid(L1, H1);
-    if (x1 >= w1) L1 = w1; else H1 = w1;
-    const double w2 = bis_mid(L2, H2);
-    if (x2 <= w2) H2 = w2; else L2 = w2;
-  }
-  if (used) atomicAdd(alg, (unsigned long long)used);
-  Node c = nd;
-  c.lo = wl;
-  c.hi = wu;
-  c.est = NAN;
-  c.u = INFINITY;
-  const double N = (double)reps[nd.rep].nb;
-  const double e1 = isnan(s1) ? NAN : laguerre_est(s1, G1, H1v, N);
-  if (isfinite(e1) && e1 > wl && e1 < wu) {
-    const double e2 = isnan(s2) ? NAN : laguerre_est(s2, G2, H2v, N);
-    double u = isfinite(e2) ? 2.0 * fabs(e1 - e2) : 0.25 * fabs(e1 - s1);
-    const double fl = 2.0 * N * EPS_X * fabs(e1);
-    c.est = e1;
-    c.u = fmax(fmax(u, fl), 0x1p-1020);
-  }
-  next[atomicAdd(nnext, 1)] = c;
 }
 
 // ---------------------------------------------------------------------------

@@ -509,48 +509,6 @@ __device__ __forceinline__ dd shfl_idx_dd(dd v, int lane) {
   return dd_make(__shfl_sync(0xffffffffu, v.hi, lane), __shfl_sync(0xffffffffu, v.lo, lane));
 }
 
-__global__ void __launch_bounds__(256) k_zwrite(const Singleton *__restrict__ sg, int ns,
-                                                const RepDesc *__restrict__ reps, const YElt *__restrict__ my,
-                                                const dd *__restrict__ P2base, long long S,
-                                                const ZMeta *__restrict__ zm, double *Z, long long ldz,
-                                                const int *__restrict__ status = nullptr, int status_stride = 0) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= ns) return;
-  if (status && status[(long long)w * status_stride] != 1) return;  // segmented RQI: accepted singletons only
-  const ZMeta m = zm[w];
-  const Singleton s = sg[w];
-  const RepDesc R = reps[s.rep];
-  const int nb = R.nb, r = m.r, last = nb - 1;
-  const dd inv = dd_make(m.inv_hi, m.inv_lo);
-  const dd *P = P2base + (long long)w * S;  // P2 of pair w (contiguous, S = nbmax here)
-  double *Zc = Z + (long long)s.col * ldz + R.bstart;
-  if (m.careful) {
-    if (lane == 0) zsolve(my + R.off, nb, r, P, P, 1, inv, Zc);
-    return;
-  }
-  if (lane == 0) Zc[r] = inv.hi;
-  // rows r-1 .. 0 (factors -l+(r-1-m)) then rows r+1 .. n-1 (factors -u-(r+m))
-  for (int side = 0; side < 2; side++) {
-    const int len = side ? last - r : r;
-    dd carry = dd_from(1.0);
-    for (int m0 = 0; m0 < len; m0 += 32) {
-      const int mm = m0 + lane;
-      const bool valid = mm < len;
-      const int src = side ? (r + mm) : (r - 1 - mm);
-      dd v = valid ? dd_neg(ldw(P, src)) : dd_from(1.0);
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        dd o = shfl_up_dd(v, off);
-        if (lane >= off) v = dd_mul_nf(o, v);
-      }
-      dd z = dd_mul_nf(carry, v);
-      if (valid) Zc[side ? (r + 1 + mm) : (r - 1 - mm)] = dd_mul_nf(z, inv).hi;
-      carry = shfl_idx_dd(z, 31);
-    }
-  }
-}
-
 // Same output as k_zwrite, HBM-streaming form: a warp takes tiles of 32 x ZC rows; the tile's factors are
 // staged in shared memory by cp.async (coalesced, one tile ahead), each lane multiplies its own chunk of ZC
 // consecutive factors sequentially, one warp scan combines the 32 chunk products, and the z values go back

@@ -9,14 +9,15 @@
 // mismatch, or whose fast pass left the finite range, is handed to the two-lane kernel k_rqi2 (which also
 // runs the careful IEEE pass and the bisection fallback), so results never depend on a guess.
 //
-//   k_rqi3_init   RQI state: lambda = interval midpoint, bracket, acceptance threshold.
-//   k_twist_seg   iteration 1's twist search in x-arithmetic (A-31): F lane d+(i), B lane
-//                 c2(i)/omega(i+1) of the twisted factorization at lambda, fp64, segmented.
-//   k_twist_pick  junction check and r = argmin |gamma_k| (ties: smallest k), one warp per singleton.
-//   k_fixed_seg   the r-twisted factorization in y-arithmetic (dd), segmented: l+/u- into P2, the
-//                 partial norms S/T as per-segment affine maps, inertia counts, gamma_r's two halves.
-//   k_fixed_step  junction check, gamma_r, ||z||^2, inertia; the stask decision: accept (write W and
-//                 the z-write metadata), or apply the RQC and run another k_fixed_seg, or hand over.
+//   k_rqi3_init     RQI state: lambda = interval midpoint, bracket, acceptance threshold.
+//   k_twist_lane    iteration 1's twist search in x-arithmetic (A-31) over row-aligned chunks: the
+//                   F lane stores d+(i), the B lane forms gamma(i) = d+(i) - c2(i)/omega(i+1) and keeps the
+//                   chunk's argmin (k_twist_lane_dd: the same in dd, for child frames).
+//   k_twist_pick2   junction check and r = argmin |gamma_k| (ties: smallest k) over the verified chunks.
+//   k_fixed_chunk   the r-twisted factorization in y-arithmetic (dd), chunk-major and segmented: l+/u- into
+//                   P2, the partial norms S/T as per-chunk affine maps, inertia counts, gamma_r's two halves.
+//   k_fixed_step    junction check, gamma_r, ||z||^2, inertia; the stask decision: accept (write W and
+//                   the z-write metadata), or apply the RQC and run another k_fixed_chunk, or hand over.
 #pragma once
 #include "kernels_rqi.cuh"
 
@@ -66,160 +67,6 @@ __device__ __forceinline__ int seg_kf(int nb, int r, int K2) {
   return min(max((int)(((long long)K2 * sf + tot / 2) / tot), 1), K2 - 1);
 }
 __device__ __forceinline__ int seg_row(bool isB, int nb, int t) { return isB ? nb - 2 - t : t; }
-
-// iteration 1's twist search in fp64 (A-31): TF[i] = d+(i) (F), TB[i] = c2(i)/omega(i+1) (B),
-// gamma_i = TF[i] - TB[i]; thread = (singleton, lane, segment)
-__global__ void __launch_bounds__(128) k_twist_seg(const Singleton *__restrict__ sg, int ns,
-                                                   const RepDesc *__restrict__ reps, const QElt *__restrict__ mq,
-                                                   const RqiState *__restrict__ st, int K, int Wu, double *TF,
-                                                   double *TB, long long S_, SegRec *rec) {
-  // consecutive threads = consecutive singletons of one (lane, segment): on a shared representation they
-  // read the same row (broadcast) and store TF/TB[row * S_ + i] coalesced
-  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= (long long)ns * 2 * K) return;
-  const int i = (int)(g % ns), ks = (int)(g / ns), k = ks % K, isB = ks / K;
-  const RqiState S = st[i];
-  SegRec *R = rec + ((long long)i * 2 + isB) * K + k;
-  if (S.status != 0) return;
-  const RepDesc Rp = reps[sg[i].rep];
-  const int nb = Rp.nb, steps = nb - 1;
-  const QElt *q = mq + Rp.off;
-  // evaluated a fraction of the inflated bracket away from lambda-hat, so that |gamma_r| stays well above
-  // the fp64 rounding of its terms however close lambda-hat is (r is eigenvector j's peak either way)
-  const double lam = __dadd_rn(S.lam_hi, ldexp(__dsub_rn(S.bhi_hi, S.blo_hi), -8));
-  const int L = (steps + K - 1) / K;
-  const int t0 = min(k * L, steps), t1 = min((k + 1) * L, steps), tw = (k == 0) ? 0 : max(t0 - Wu, 0);
-  double *T = (isB ? TB : TF) + i;
-#define TROW(row) T[(long long)(row) * S_]
-  if (isB && k == 0) TROW(nb - 1) = 0.0;
-  if (t0 >= t1) {
-    R->empty = 1;
-    R->ok = 1;
-    return;
-  }
-  R->empty = 0;
-  // state entering step tw: F d+(row), B omega(row+1); guess = the value with no coupling term
-  const int rs = isB ? nb - 1 - tw : tw;
-  double den = __dsub_rn(__ldg(&q[rs].gb_hi), lam);
-  double din = den;
-  bool ok = true;
-  auto step = [&](int t, double c2, double gg) {
-    if (t == t0) din = den;
-    const double P = div_fast_nocheck(c2, den);
-    if (t >= t0) TROW(seg_row(isB, nb, t)) = isB ? P : den;
-    den = __dsub_rn(__dsub_rn(gg, lam), P);
-    ok &= isfinite(den) && den != 0.0;
-  };
-  // rows stream from L2 (the representation is shared by many singletons): PF rows in flight
-  constexpr int PF = 8;
-  double rc[PF], rg[PF];
-  auto ld = [&](int t, int u) {
-    const int row = max(seg_row(isB, nb, min(t, t1 - 1)), 0);
-    rc[u] = __ldg(&q[row].c2_hi);
-    rg[u] = isB ? __ldg(&q[row].gb_hi) : __ldg(&q[row].gf_hi);
-  };
-#pragma unroll
-  for (int u = 0; u < PF; u++) ld(tw + u, u);
-  int t = tw;
-  for (; t + PF <= t1; t += PF) {
-#pragma unroll
-    for (int u = 0; u < PF; u++) {
-      const double c2 = rc[u], gg = rg[u];
-      ld(t + u + PF, u);
-      step(t + u, c2, gg);
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < PF; u++)
-    if (t + u < t1) step(t + u, rc[u], rg[u]);
-  if (!isB && t1 == steps) TROW(nb - 1) = den;   // gamma_n = d+(n)
-#undef TROW
-  R->in_hi = din;
-  R->out_hi = den;
-  R->ok = ok ? 1 : 0;
-}
-
-// junctions of the twist pass and r = argmin |gamma_k| (ties to the smallest k).  A CTA covers 32 singletons
-// x 8 row groups: warp g scans rows g, g+8, ... of 32 consecutive singletons (coalesced [row * S + i] loads).
-__global__ void __launch_bounds__(256) k_twist_pick(const Singleton *__restrict__ sg, int ns,
-                                                    const RepDesc *__restrict__ reps, RqiState *st, int K,
-                                                    const double *__restrict__ TF, const double *__restrict__ TB,
-                                                    long long S_, const SegRec *__restrict__ rec, long long *stats) {
-  __shared__ int sh_lo[32], sh_hi[32];
-  __shared__ double sh_best[8][32];
-  __shared__ int sh_bk[8][32];
-  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
-  const int i = blockIdx.x * 32 + lane;
-  const bool act = i < ns && st[min(i, ns - 1)].status == 0;
-  int nb = 0;
-  if (act) nb = reps[sg[i].rep].nb;
-  if (grp == 0) {
-    // verified rows: F segments before the first failed junction (rows [0, fhi)), B likewise from the
-    // bottom (rows (blo, nb-2]); a segment is exact iff its entry state equals its exact predecessor's exit
-    // state.  The twist index lies where both lanes are exact (F fails past the peak, B before it).
-    int fhi = 0, blo = 0;
-    if (act) {
-      const int steps = nb - 1, L = (steps + K - 1) / K;
-      const SegRec *R = rec + (long long)i * 2 * K;
-      for (int ln = 0; ln < 2; ln++) {
-        int prev = -1, kv = 0;
-        for (int k = 0; k < K; k++) {
-          const SegRec &s_ = R[ln * K + k];
-          if (s_.empty) { kv = k + 1; continue; }
-          if (!s_.ok) break;
-          if (prev >= 0 && __double_as_longlong(s_.in_hi) != __double_as_longlong(R[ln * K + prev].out_hi)) break;
-          prev = k;
-          kv = k + 1;
-        }
-        const int tv = min(kv * L, steps);
-        if (ln == 0) fhi = (tv == steps) ? nb : tv;  // F's last step also fixes gamma_n
-        else blo = (tv == steps) ? -1 : nb - 2 - tv;
-      }
-    }
-    sh_lo[lane] = blo + 1;
-    sh_hi[lane] = fhi;
-  }
-  __syncthreads();
-  double best = INFINITY;
-  int bk = -1;
-  if (act) {
-    const int lo = max(sh_lo[lane], 0), hi = sh_hi[lane];
-    int kk = lo + ((grp - lo % 8) + 8) % 8;  // rows congruent to grp mod 8
-#pragma unroll 4
-    for (; kk < hi; kk += 8) {
-      const double gm = fabs(__dsub_rn(TF[(long long)kk * S_ + i], TB[(long long)kk * S_ + i]));
-      if (gm < best) { best = gm; bk = kk; }
-    }
-  }
-  sh_best[grp][lane] = best;
-  sh_bk[grp][lane] = bk;
-  __syncthreads();
-  if (grp == 0) {
-    unsigned ho = 0, rows = 0;
-    if (act) {
-      for (int g2 = 1; g2 < 8; g2++) {
-        const double ob = sh_best[g2][lane];
-        const int ok_ = sh_bk[g2][lane];
-        if (ok_ >= 0 && (bk < 0 || ob < best || (ob == best && ok_ < bk))) { best = ob; bk = ok_; }
-      }
-      // the x-arithmetic argmin must resolve gamma: |gamma_r| well above the fp64 rounding of its two terms
-      const double sc = (bk >= 0) ? fmax(fabs(TF[(long long)bk * S_ + i]), fabs(TB[(long long)bk * S_ + i])) : 0.0;
-      if (bk < 0 || !(best > 0x1p-46 * sc)) {
-        st[i].status = 2;
-        ho = 1;
-      } else {
-        st[i].r = bk;
-        rows = (unsigned)(2 * (nb - 1));
-      }
-    }
-    ho = __reduce_add_sync(0xffffffffu, ho);
-    rows = __reduce_add_sync(0xffffffffu, rows);
-    if (lane == 0) {
-      if (ho) atomicAdd((unsigned long long *)&stats[ST_HO_TWIST], (unsigned long long)ho);
-      if (rows) atomicAdd((unsigned long long *)&stats[ST_TWIST_ROWS], (unsigned long long)rows);
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Twist search in two passes over row-aligned chunks (A-31; replaces k_twist_seg + k_twist_pick):
@@ -524,36 +371,6 @@ __device__ __forceinline__ void seg_pass(const QElt *__restrict__ q, int nb, int
   }
 }
 
-__global__ void __launch_bounds__(128) k_fixed_seg(const Singleton *__restrict__ sg, int ns,
-                                                   const RepDesc *__restrict__ reps, const QElt *__restrict__ mq,
-                                                   const RqiState *__restrict__ st, int K, int Wu, dd *P2,
-                                                   long long nbmax, SegRec *rec, int bal) {
-  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= (long long)ns * 2 * K) return;
-  const int kk = (int)(g % (2 * K)), i = (int)(g / (2 * K));
-  const RqiState S = st[i];
-  if (S.status != 0) return;
-  SegRec *R = rec + g;
-  const RepDesc Rp = reps[sg[i].rep];
-  const int nb = Rp.nb, r = S.r;
-  const int KF = bal ? seg_kf(nb, r, 2 * K) : K;
-  const int isB = kk >= KF, k = isB ? kk - KF : kk;
-  K = isB ? 2 * K - KF : KF;  // this lane's segment count
-  const bool light = S.it == 0;  // the first pass at the bisection midpoint only yields the RQC
-  const QElt *q = mq + Rp.off;
-  const dd lam = dd_make(S.lam_hi, S.lam_lo), nlam = dd_neg(lam);
-  const int steps = isB ? nb - 1 - r : r;
-  const int L = (steps + K - 1) / K;
-  const int t0 = min(k * L, steps), t1 = min((k + 1) * L, steps), tw = (k == 0) ? 0 : max(t0 - (S.wide ? 8 * Wu : Wu), 0);
-  dd *P = P2 + (long long)i * nbmax;
-  if (t0 >= t1 && !(k == 0 && !isB)) {  // no steps (F segment 0 always reports d+(0) when r = 0)
-    R->empty = 1;
-    R->ok = 1;
-    return;
-  }
-  seg_pass(q, nb, isB, t0, t1, tw, light, lam, nlam, P, R);
-}
-
 // Chunk-major form of k_fixed_seg: the rows 0..nb-2 are cut into K2 fixed chunks of L rows.  Thread
 // (slot c, singleton i), c < K2, runs chunk c's primary part: its F part (rows [lo, min(hi, r))) if the
 // chunk starts below r (chunk 0 always: it reports d+(0) even when r = 0), else the whole chunk as B part;
@@ -723,27 +540,25 @@ struct FsInc {
   unsigned nact, wide, hofixed, horqc, iters, light, qd, zw, dmax;
 };
 __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restrict__ sg,
-                                                const RepDesc *__restrict__ reps, RqiState *st, int K, int bal,
-                                                int chunk, const SegRec *__restrict__ F, double *W, ZMeta *zmeta,
+                                                const RepDesc *__restrict__ reps, RqiState *st, int K,
+                                                const SegRec *__restrict__ F, double *W, ZMeta *zmeta,
                                                 int *diag_depth, double *fin_lo, double *fin_hi, FsInc &inc) {
   RqiState S = st[i];
   if (S.status != 0) return;
   const Singleton s = sg[i];
   const RepDesc Rp = reps[s.rep];
   const int nb = Rp.nb, r = S.r, j = s.j;
-  const int KF = chunk ? 2 * K : bal ? seg_kf(nb, r, 2 * K) : K;
-  const SegRec *B = F + KF;  // F: this singleton's records
   bool good = true;
   dd Ssum = dd_from(0.0), Tsum = dd_from(0.0), dr = dd_from(0.0), tr = dd_from(0.0);
   int c = 0;
   for (int ln = 0; ln < 2; ln++) {
     // chunk layout: F records at [2c], B records at [2c + 1] walked from the last chunk down
-    const SegRec *X = chunk ? F : ln ? B : F;
-    const int Kl = chunk ? 2 * K : ln ? 2 * K - KF : KF;
+    const SegRec *X = F;
+    const int Kl = 2 * K;
     int prev = -1;
     dd acc = dd_from(0.0);
     for (int kk = 0; kk < Kl; kk++) {
-      const int k = chunk ? 2 * (ln ? Kl - 1 - kk : kk) + ln : kk;
+      const int k = 2 * (ln ? Kl - 1 - kk : kk) + ln;
       const SegRec &a = X[k];
       if (a.empty) continue;
       good &= a.ok != 0;
@@ -833,16 +648,16 @@ __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restri
 }
 
 __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
-                             RqiState *st, int K, int bal, int chunk, const SegRec *__restrict__ rec, double *W,
+                             RqiState *st, int K, const SegRec *__restrict__ rec, double *W,
                              ZMeta *zmeta, int *diag_depth, double *fin_lo, double *fin_hi, long long *stats,
                              int *nactive, int stage) {
   extern __shared__ uint4 recsm[];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int per = 2 * K * (chunk ? 2 : 1);  // records per singleton
+  const int per = 4 * K;  // records per singleton: 2K chunks x 2 lanes
   const SegRec *F = stage ? reinterpret_cast<const SegRec *>(stage_recs(rec, per * (int)sizeof(SegRec), ns, recsm))
                           : rec + (long long)i * per;
   FsInc inc = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  if (i < ns) fixed_step_body(i, sg, reps, st, K, bal, chunk, F, W, zmeta, diag_depth, fin_lo, fin_hi, inc);
+  if (i < ns) fixed_step_body(i, sg, reps, st, K, F, W, zmeta, diag_depth, fin_lo, fin_hi, inc);
   const unsigned fm = 0xffffffffu;
   const unsigned nact = __reduce_add_sync(fm, inc.nact), wide = __reduce_add_sync(fm, inc.wide);
   const unsigned hof = __reduce_add_sync(fm, inc.hofixed), hor = __reduce_add_sync(fm, inc.horqc);

@@ -100,34 +100,6 @@ __global__ void k_clu_shift_init(int ncl, const double *__restrict__ ylo, const 
   ss[c] = s;
 }
 
-// S8(c): growth of dstqds(M_y, tau) for both candidate shifts, thread per (cluster, side)
-__global__ void k_clu_attempt(const Cluster *__restrict__ cl, int ncl, const RepDesc *__restrict__ reps,
-                              const YElt *__restrict__ my, const ShiftState *__restrict__ ss, double *gval,
-                              int *valid) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= 2 * ncl) return;
-  int c = t >> 1, side = t & 1;
-  if (ss[c].done) return;
-  RepDesc R = reps[cl[c].rep];
-  const YElt *y = my + R.off;
-  dd tau = dd_from(side ? ss[c].taur : ss[c].taul);
-  dd s = dd_neg(tau);
-  double g = 0.0;
-  int ok = 1;
-  for (int i = 0; i < R.nb - 1; i++) {
-    dd den, rr, out, xn;
-    qd_step(s, ld_d(y + i), ld_dl(y + i), ld_dll(y + i), tau, den, rr, out, xn);
-    ok &= !(isnan(den.hi) || isnan(out.hi));
-    g = dmaxd(g, fabs(den.hi));
-    s = xn;
-  }
-  dd den = dd_add(s, ld_d(y + R.nb - 1));
-  ok &= !isnan(den.hi);
-  g = dmaxd(g, fabs(den.hi));
-  gval[t] = g;
-  valid[t] = ok;
-}
-
 // growth max|fl64(d+)| and validity (no NaN) of dstqds(M_y, tau) (Alg. dstqds): fast pass on the
 // pivot-recurrence form (QElt), the careful IEEE pass (qd_step) if a pivot leaves [2^-1000, 2^1000]
 __device__ void dstqds_growth(const YElt *__restrict__ y, const QElt *__restrict__ q, int nb, double tau_x, double &g,
@@ -229,39 +201,6 @@ __global__ void k_clu_select_multi(const Cluster *__restrict__ cl, int ncl, cons
         s.done = 1;
         if (s.have_best) atomicAdd((unsigned long long *)&stats[ST_UNCERTIFIED], 1ull);
       }
-    }
-  }
-  if (s.done) atomicAdd(ndone, 1);
-  ss[c] = s;
-}
-
-__global__ void k_clu_select(const Cluster *__restrict__ cl, int ncl, const RepDesc *__restrict__ reps,
-                             ShiftState *ss, const double *__restrict__ gval, const int *__restrict__ valid, int a,
-                             int *ndone, long long *stats) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= ncl) return;
-  ShiftState s = ss[c];
-  if (s.done) { atomicAdd(ndone, 1); return; }
-  atomicAdd((unsigned long long *)&stats[ST_ATTEMPTS], 1ull);
-  double gthr = __dmul_rn(GROWTH, reps[cl[c].rep].spdiam);
-  int vl = valid[2 * c], vr = valid[2 * c + 1];
-  double gl = gval[2 * c], gr = gval[2 * c + 1];
-  int pick = 0;
-  if (vl && vr) pick = (gl <= gr) ? 1 : 2;
-  else if (vl) pick = 1;
-  else if (vr) pick = 2;
-  s.attempts++;
-  if (pick) {
-    double g = (pick == 1) ? gl : gr;
-    if (g < s.best_g) { s.best_g = g; s.best_tau = (pick == 1) ? s.taul : s.taur; s.have_best = 1; }
-    if (g <= gthr) { s.done = 1; s.certified = 1; }
-  }
-  if (!s.done) {
-    s.taul = __dsub_rn(s.taul, ldexp(s.offl, a));
-    s.taur = __dadd_rn(s.taur, ldexp(s.offr, a));
-    if (a == MAX_ATTEMPTS - 1) {
-      s.done = 1;
-      if (s.have_best) atomicAdd((unsigned long long *)&stats[ST_UNCERTIFIED], 1ull);
     }
   }
   if (s.done) atomicAdd(ndone, 1);
@@ -517,91 +456,6 @@ __device__ __forceinline__ void stw(dd *w, long long off, dd v) {
   __stcs(reinterpret_cast<double2 *>(w + off), make_double2(v.hi, v.lo));
 }
 
-// Getvec: r < 0 -> full twisted factorization + twist search (iteration 1);
-// r >= 0 (0-based) -> only the r-twisted factorization.
-// Representation elements and workspace values are prefetched two steps ahead.
-__device__ void getvec_dd(const YElt *__restrict__ y, int nb, dd lam, int r, dd *A, dd *B, long long S, GV &g) {
-  int cnt = 0;
-  const int last = nb - 1;
-  if (r < 0) {
-    dd s = dd_neg(lam);
-    YV c0 = ldy(y, 0), c1 = ldy(y, min(1, last));
-    for (int i = 0; i < last; i++) {
-      YV c2 = ldy(y, min(i + 2, last));
-      dd den, rr, out, xn;
-      qd_step(s, c0.d, c0.dl, c0.dll, lam, den, rr, out, xn);
-      stw(A, (long long)i * S, s);
-      stw(B, (long long)i * S, (den.hi == 0.0) ? dd_mark() : out);
-      cnt += dd_sb(den);
-      s = xn;
-      c0 = c1;
-      c1 = c2;
-    }
-    dd dlast = c0.d;  // y[nb-1].d
-    dd dn = dd_add(s, dlast);
-    cnt += dd_sb(dn);
-    dd gam = dn;  // gamma_n = s(n) + d(n) = d+(n)
-    int rbest = -1;
-    dd best = dd_from(INFINITY), gbest = gam;
-    if (!isnan(gam.hi)) { rbest = last; best = dd_abs(gam); }
-    dd p = dd_sub(dlast, lam);
-    if (last >= 1) {
-      YV b0 = ldy(y, last - 1), b1 = ldy(y, max(last - 2, 0));
-      dd a0 = ldw(A, (long long)(last - 1) * S), a1 = ldw(A, (long long)max(last - 2, 0) * S);
-      for (int i = last - 1; i >= 0; i--) {
-        int i2 = max(i - 2, 0);
-        YV b2 = ldy(y, i2);
-        dd a2 = ldw(A, (long long)i2 * S);
-        dd den, rr, out, xn;
-        qd_step(p, b0.dll, b0.dl, b0.d, lam, den, rr, out, xn);
-        dd gi = dd_add(a0, dd_mul(dd_mul(b0.d, rr), p));
-        stw(A, (long long)i * S, (den.hi == 0.0) ? dd_mark() : out);
-        if (!isnan(gi.hi)) {
-          dd ag = dd_abs(gi);
-          if (!dd_lt(best, ag)) { best = ag; rbest = i; gbest = gi; }
-        }
-        p = xn;
-        b0 = b1; b1 = b2;
-        a0 = a1; a1 = a2;
-      }
-    }
-    g.r = rbest;
-    g.gamma = gbest;
-  } else {
-    dd s = dd_neg(lam), gamma = dd_from(0.0);
-    dd dlast = ldy(y, last).d;
-    dd p = dd_sub(dlast, lam);
-    // unified loop: k < r forward dstqds step i = k; else backward dqds step i = nb-2-(k-r)
-    const int K = last;
-#define IDX(k) ((k) < r ? (k) : last - 1 - ((k) - r))
-    YV c0 = ldy(y, IDX(0)), c1 = ldy(y, IDX(min(1, max(K - 1, 0))));
-    for (int k = 0; k < K; k++) {
-      YV c2 = ldy(y, IDX(min(k + 2, K - 1)));
-      const bool fw = k < r;
-      const int i = IDX(k);
-      dd den, rr, out, xn;
-      qd_step(fw ? s : p, fw ? c0.d : c0.dll, c0.dl, fw ? c0.dll : c0.d, lam, den, rr, out, xn);
-      if (fw) {
-        stw(B, (long long)i * S, (den.hi == 0.0) ? dd_mark() : out);
-        s = xn;
-      } else {
-        stw(A, (long long)i * S, (den.hi == 0.0) ? dd_mark() : out);
-        if (i == r) gamma = dd_add(s, dd_mul(dd_mul(c0.d, rr), p));
-        p = xn;
-      }
-      cnt += dd_sb(den);
-      c0 = c1;
-      c1 = c2;
-    }
-#undef IDX
-    if (r == last) gamma = dd_add(s, dlast);
-    cnt += dd_sb(gamma);
-    g.r = r;
-    g.gamma = gamma;
-  }
-  g.c = cnt;
-}
-
 // z solve of N_r^T z = e_r with zero-pivot substitution (A-25); returns ||z||^2.
 // Backward branch (i = r-1 .. 0, uses l+ in B) then forward branch (i = r .. nb-2, uses u- in A),
 // as one loop over k with the workspace prefetched two steps ahead.  If Zc != nullptr writes
@@ -667,77 +521,6 @@ __device__ __noinline__ dd bisect_y_full(const YElt *__restrict__ y, const QElt 
     else hi = mid;
   }
   return dd_add(lo, dd_mul_d(dd_sub(hi, lo), 0.5));
-}
-
-__global__ void __launch_bounds__(64) k_rqi(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
-                                            const YElt *__restrict__ my, dd *wsA, dd *wsB, long long S, double *W,
-                                            double *Z, long long ldz, int *diag_depth, double *fin_lo, double *fin_hi,
-                                            long long *stats) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= ns) return;
-  const Singleton s = sg[t];
-  const RepDesc R = reps[s.rep];
-  const int nb = R.nb, j = s.j;
-  const YElt *y = my + R.off;
-  dd *A = wsA + t, *B = wsB + t;
-  double mid = bis_mid(s.lo, s.hi);
-  double nu = __dmul_rn(__dmul_rn(100.0, (double)nb), EPS_X);
-  dd blo = dd_from(__dsub_rn(s.lo, __dmul_rn(nu, fabs(s.lo))));
-  dd bhi = dd_from(__dadd_rn(s.hi, __dmul_rn(nu, fabs(s.hi))));
-  dd lam = dd_from(mid);
-  double thr1 = __dmul_rn(__dmul_rn(s.gap, EPS_X), sqrt((double)nb));
-  int r = -1, iters = 0;
-  long long qd = 0, qdg = 0, zs = 0;
-  bool accepted = false;
-  GV g;
-  dd nz = dd_from(1.0);
-  for (int it = 0; it < MAX_RQI && !accepted; it++) {
-    if (r < 0) { qd += 2 * (nb - 1); qdg += nb - 1; } else qd += nb - 1;
-    getvec_dd(y, nb, lam, r, A, B, S, g);
-    iters++;
-    r = g.r;
-    if (r < 0) break;
-    zs += nb - 1;
-    dd zz = zsolve(y, nb, r, A, B, S, dd_from(0.0), nullptr);
-    if (!isfinite(zz.hi) || zz.hi == 0.0) break;
-    nz = dd_sqrt(zz);
-    dd resid = dd_div(dd_abs(g.gamma), nz);
-    dd rqc = dd_div(g.gamma, zz);
-    dd tol2 = dd_mul_d(dd_abs(lam), 4.0 * EPS_Y);  // A-30 floor as in k_rqi2
-    if (dd_lt(tol2, dd_from(__dmul_rn(0x1p-100, R.spdiam)))) tol2 = dd_from(__dmul_rn(0x1p-100, R.spdiam));
-    if (resid.hi <= thr1 || dd_lt(dd_abs(rqc), tol2)) { accepted = true; break; }
-    if (g.c < j) blo = lam; else bhi = lam;
-    dd nl = dd_add(lam, rqc);
-    bool ok = ((g.c < j) ? (rqc.hi > 0.0) : (rqc.hi < 0.0)) && dd_lt(blo, nl) && dd_lt(nl, bhi);
-    if (ok) lam = nl;
-    else break;
-  }
-  atomicAdd((unsigned long long *)&stats[ST_RQI_ITERS], (unsigned long long)iters);
-  atomicAdd((unsigned long long *)&stats[ST_QD_STEPS], (unsigned long long)qd);
-  atomicAdd((unsigned long long *)&stats[ST_QDG_STEPS], (unsigned long long)qdg);
-  atomicAdd((unsigned long long *)&stats[ST_Z_STEPS], (unsigned long long)zs);
-  atomicAdd((unsigned long long *)&stats[ST_ZW_STEPS], (unsigned long long)(nb - 1));
-  atomicAdd((unsigned long long *)&stats[ST_GETVEC], (unsigned long long)iters);
-  if (!accepted) {
-    atomicAdd((unsigned long long *)&stats[ST_RQI_FALLBACK], 1ull);
-    lam = bisect_y_full(y, nullptr, nb, j, blo, bhi, R.spdiam);
-    getvec_dd(y, nb, lam, r, A, B, S, g);
-    atomicAdd((unsigned long long *)&stats[ST_GETVEC], 1ull);
-    r = g.r;
-    if (r < 0) r = 0;
-    dd zz = zsolve(y, nb, r, A, B, S, dd_from(0.0), nullptr);
-    nz = dd_sqrt(zz);
-  }
-  dd sig = dd_make(R.sig_hi, R.sig_lo);
-  W[s.col] = dd_add(lam, sig).hi;
-  double *Zc = Z + (long long)s.col * ldz + R.bstart;
-  zsolve(y, nb, r, A, B, S, dd_rcp(nz), Zc);
-  if (diag_depth) {
-    diag_depth[s.col] = R.depth;
-    fin_lo[s.col] = s.lo;
-    fin_hi[s.col] = s.hi;
-  }
-  atomicMax((unsigned long long *)&stats[ST_DMAX], (unsigned long long)R.depth);
 }
 
 // size-1 blocks (S2): eigenpair (alpha_s, e_s)

@@ -97,23 +97,16 @@ struct mrrr_ctx {
   long long target_unseg = 32768;   // k-section budget per round of whole-length root chains (C1: 3-4 levels)
   long long target_child = 8192;    // ... of child-frame rounds (less speculation on long child chains)
   int mmax = 16;
-  int chains_per_thread = 1;
   bool neg_tma = true;  // x-NegCount with TMA-staged representation tiles (k_negcount_tma)
-  bool guided = false;  // guided rounds for isolated nodes (kernels_guided.cuh); MRRR_GUIDED=1 (C2: fewer rounds, more FP64 work: slower)
-  int bud_full = 15, bud_tube = 40;
   bool grouped = true;  // child bisection with CTAs grouped by representation (k_negcount_grp)
   int seg_k = 8, seg_w = 128;  // segmented root NegCount: segments per chain, warm-up rows (k_negcount_seg)
   bool rqi_seg = true;         // segmented RQI passes (kernels_rqi3.cuh); MRRR_RQISEG=0: the two-lane kernel only
   int rqi_segk = 8, rqi_segw = 0;  // rqi_segw 0: by frame length (128 up to 16K rows, else 192)
   long long rqi_threads = 131072;  // adaptive RQI segment count target (threads per segmented pass)
-  bool rqi_bal = true;         // split a singleton's 2K segments between its lanes by length
-  bool rqi_chunk = true;       // chunk-major fixed passes (k_fixed_chunk) instead of lane-major (k_fixed_seg)
   bool rqi_seg_child = true;   // segmented RQI for child-frame singletons (dd twist search)
   int segchild_min = 8;        // ... when the level has at least this many singletons per child representation
   long long twdd_root_max = 0;  // root blocks up to this size take the dd twist search (MRRR_TWDD_ROOT)
-  bool tw2 = true;             // twist search in two passes storing only d+ (k_twist_lane, k_twist_pick2)
   bool rqi_bulk = true;        // k_fixed_chunk stores the factors by bulk copies of staged 8-row runs
-  bool zw_chunk = true;        // k_zwrite_chunk (chunked products, staged tiles) instead of the per-row warp scan
   int segy_k = 16, segy_w = 128;  // segmented y-NegCount, shift growth, child build (MRRR_SEGYK=1: unsegmented)
   int segx_k = 16, segx_w = 128;  // segmented many-representation x-NegCount (child rounds with long chains)
   long long cur_nbmax = 0;       // longest representation of the current child bisection (0: segx off)
@@ -128,7 +121,6 @@ struct mrrr_ctx {
   bool dev_rounds = false;     // segmented rounds enqueued in batches on device-side counters (MRRR_DEVROUNDS=1;
                                // slower on C2: the oversized early-exit grids cost more than the saved syncs)
   int max_nodes = 0;           // bound on live bisection nodes (indices in the computed set)  // tube point budgets: no estimate (4 full levels) / with estimate
-  bool rqi_pair = true;
   bool l2_persist = true;
   long long rqi_seg_min = 2048; // root blocks up to this size skip the segmented RQI (MRRR_RQISEGMIN)
   bool nonlocal = false;         // this solve's root rounds found non-contracting recurrences (see run_bisection)
@@ -358,98 +350,11 @@ void launch_negcount(mrrr_t h, const Node *nodes, int nnode, int m, int nex, con
     launch_check(h);
     return;
   }
-  int ch = Y ? 1 : h->chains_per_thread;
-  long long thr = (tot + ch - 1) / ch;
   const ExplicitChain *ex = h->ex.as<ExplicitChain>();
-  const RepDesc *reps = h->reps.as<RepDesc>();
-  const double2 *mx = h->mx.as<double2>();
-  const YElt *my = h->my.as<YElt>();
-  const QElt *mq = h->mq.as<QElt>();
-  int *cnts = h->counts.as<int>(), *exc = h->excounts.as<int>();
-  unsigned g = nblocks_for(thr, 128);
-  cudaStream_t st = h->stream;
-  switch (ch) {
-    case 1: k_negcount<Y, 1><<<g, 128, 0, st>>>(nodes, nnode, m, ex, nex, reps, mx, my, mq, cnts, exc); break;
-    case 2: k_negcount<Y, 2><<<g, 128, 0, st>>>(nodes, nnode, m, ex, nex, reps, mx, my, mq, cnts, exc); break;
-    case 3: k_negcount<Y, 3><<<g, 128, 0, st>>>(nodes, nnode, m, ex, nex, reps, mx, my, mq, cnts, exc); break;
-    default: k_negcount<Y, 4><<<g, 128, 0, st>>>(nodes, nnode, m, ex, nex, reps, mx, my, mq, cnts, exc); break;
-  }
+  k_negcount<Y, 1><<<nblocks_for(tot, 128), 128, 0, h->stream>>>(
+      nodes, nnode, m, ex, nex, h->reps.as<RepDesc>(), h->mx.as<double2>(), h->my.as<YElt>(), h->mq.as<QElt>(),
+      h->counts.as<int>(), h->excounts.as<int>());
   launch_check(h);
-}
-
-// Guided rounds (kernels_guided.cuh): isolated nodes evaluate a tube around a Laguerre estimate of their
-// eigenvalue instead of a full k-section subtree; the rest as in run_bisection.  Same intervals.
-void run_bisection_guided(mrrr_t h, int nnode, double *out_lo, double *out_hi, double rtol, int nverify,
-                          const int *blist_dev, int nbl, bool *restart) {
-  Node *cur = h->nodesA.as<Node>(), *nxt = h->nodesB.as<Node>();
-  bool first = true;
-  unsigned long long *alg = (unsigned long long *)(h->stats.as<long long>() + ST_NEGX_ALG);
-  while (nnode > 0) {
-    CK(h->nodesK.ensure(sizeof(Node) * nnode));
-    CK(h->nodesP.ensure(sizeof(Node) * nnode));
-    CK(h->offsP.ensure(sizeof(int) * (nnode + 1)));
-    zero_counters(h);
-    k_node_split<<<nblocks_for(nnode, 128), 128, 0, h->stream>>>(cur, nnode, h->nodesK.as<Node>(),
-                                                                h->cnt.as<int>() + C_NK, h->nodesP.as<Node>(),
-                                                                h->cnt.as<int>() + C_NP, h->bud_full, h->bud_tube);
-    launch_check(h);
-    read_counters(h);
-    const int nK = h->h_cnt[C_NK], nP = h->h_cnt[C_NP];
-    int nPc = 0;
-    if (nP > 0) {
-      k_tube_count<<<nblocks_for(nP, 128), 128, 0, h->stream>>>(h->nodesP.as<Node>(), nP, rtol, h->offsP.as<int>());
-      launch_check(h);
-      k_scan_excl<<<1, 1024, 0, h->stream>>>(h->offsP.as<int>(), nP, h->cnt.as<int>() + C_NPC);
-      launch_check(h);
-      read_counters(h);
-      nPc = h->h_cnt[C_NPC];
-    }
-    int m = 1;
-    const long long budget = std::max<long long>(h->target_unseg - nPc, 0);
-    while (m < h->mmax && (long long)nK * ((1LL << (m + 1)) - 1) <= budget) m++;
-    const long long nKc = (long long)nK * ((1LL << m) - 1);
-    const int nex = first ? nverify : 0;
-    CK(h->counts.ensure(std::max<long long>(nKc + nPc, 1) * sizeof(int)));
-    CK(h->dS.ensure(sizeof(double) * std::max(nPc, 1)));
-    CK(h->dG.ensure(sizeof(double) * std::max(nPc, 1)));
-    CK(h->dH.ensure(sizeof(double) * std::max(nPc, 1)));
-    zero_counters(h);
-    CK(cudaEventRecord(h->nc0, h->stream));
-    launch_negcount<false>(h, h->nodesK.as<Node>(), nK, m, nex, h->nodesP.as<Node>(), nP, h->offsP.as<int>(), nPc,
-                           rtol);
-    CK(cudaEventRecord(h->nc1, h->stream));
-    if (nex > 0) {
-      k_root_verify<<<nblocks_for(nbl, 128), 128, 0, h->stream>>>(blist_dev, nbl, h->starts.as<int>(),
-                                                                  h->binfo.as<double>(), h->excounts.as<int>(),
-                                                                  h->cnt.as<int>() + C_NEX);
-      launch_check(h);
-    }
-    if (nK > 0) {
-      k_bisect_update<<<nblocks_for((long long)nK << m, 128), 128, 0, h->stream>>>(
-          h->nodesK.as<Node>(), nK, m, h->counts.as<int>(), nxt, h->cnt.as<int>() + C_NNEXT, out_lo, out_hi, rtol,
-          alg);
-      launch_check(h);
-    }
-    if (nP > 0) {
-      k_tube_update<<<nblocks_for(nP, 128), 128, 0, h->stream>>>(
-          h->nodesP.as<Node>(), nP, h->offsP.as<int>(), h->counts.as<int>() + nKc, h->dS.as<double>(),
-          h->dG.as<double>(), h->dH.as<double>(), h->reps.as<RepDesc>(), nxt, h->cnt.as<int>() + C_NNEXT, out_lo,
-          out_hi, rtol, alg);
-      launch_check(h);
-    }
-    read_counters(h);
-    h->host_rounds++;
-    h->stats_h[ST_NEGX] += nKc + nPc + nex;
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, h->nc0, h->nc1));
-    h->neg_ms += ms;
-    h->neg_launches++;
-    if (nex > 0 && h->h_cnt[C_NEX] > 0) { *restart = true; return; }
-    nnode = h->h_cnt[C_NNEXT];
-    std::swap(cur, nxt);
-    first = false;
-    if (cur != h->nodesA.as<Node>() && cur != h->nodesB.as<Node>()) break;  // unreachable (ping-pong)
-  }
 }
 
 __global__ void k_set_int(int *p, int v) { *p = v; }
@@ -618,10 +523,6 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
                    const int *blist_dev, int nbl, bool *restart, int rep0, int nrep, int single_nb) {
   if (!Y && rep0 >= 0 && nrep > 1 && h->neg_tma && h->grouped) {
     run_bisection_grouped(h, nnode, out_lo, out_hi, rtol, rep0, nrep);
-    return;
-  }
-  if (!Y && h->guided && h->neg_tma) {
-    run_bisection_guided(h, nnode, out_lo, out_hi, rtol, nverify, blist_dev, nbl, restart);
     return;
   }
   Node *cur = h->nodesA.as<Node>(), *nxt = h->nodesB.as<Node>();
@@ -793,138 +694,102 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
              bool child = false) {
   if (ns <= 0) return;
   l2_pin_reps(h, true);
-  const bool pair = h->rqi_pair;
-  // workspace per singleton: pair kernel 3 dd planes (P0, P1, P2), single-lane kernel 2
-  long long per = (pair ? 3LL : 2LL) * (long long)sizeof(dd) * std::max<long long>(nbmax, 1);
+  // workspace per singleton: 3 dd planes (the two-lane kernel's P0, P1, P2; the segmented passes use the first
+  // for the twist search and the second for the stored factors)
+  long long per = 3LL * (long long)sizeof(dd) * std::max<long long>(nbmax, 1);
   long long budget = std::min<long long>(h->ws_limit / 2, 64LL << 30);
   long long bmax = std::max<long long>(32, budget / per);
   long long batch = std::min<long long>(ns, bmax);
   long long stride = (batch + 31) / 32 * 32;  // pairs launched per batch (grid padding)
-  if (pair) {
-    CK(h->wsA.ensure((size_t)3 * stride * nbmax * sizeof(dd)));
-  } else {
-    CK(h->wsA.ensure((size_t)stride * nbmax * sizeof(dd)));
-    CK(h->wsB.ensure((size_t)stride * nbmax * sizeof(dd)));
-  }
+  CK(h->wsA.ensure((size_t)3 * stride * nbmax * sizeof(dd)));
   bool diag = (h->flags & MRRR_KEEP_DIAG) != 0;
   for (long long b0 = 0; b0 < ns; b0 += batch) {
     long long nb = std::min<long long>(batch, ns - b0);
     CK(cudaEventRecord(h->rq0, h->stream));
-    if (pair) {
-      CK(h->zmeta.ensure(sizeof(ZMeta) * stride));
-      const Singleton *sgb = h->sing.as<Singleton>() + b0;
-      int nold = (int)nb;
-      if (h->rqi_seg && allow_seg) {
-        // segmented passes (kernels_rqi3.cuh); singletons they hand over go through k_rqi2 below
-        // segments per lane: at least rqi_segk; more when the batch has few singletons (a rank's shard),
-        // so that about rqi_threads threads run, as long as a chunk stays longer than the warm-up
-        int K = h->rqi_segk;
-        // warm-up rows: 128 suffice up to n = 16K (no retries measured); longer frames get 192
-        const int Wu = h->rqi_segw > 0 ? h->rqi_segw : (nbmax <= 16384 ? 128 : 192);
-        while (2 * K <= 32 && (long long)nb * 2 * (2 * K) <= h->rqi_threads && (nbmax - 1) >= 2 * (2 * K) * Wu) K *= 2;
-        CK(h->rqst.ensure(sizeof(RqiState) * stride));
-        CK(h->rqrec.ensure(sizeof(SegRec) * stride * 4 * K));  // chunk layout: 2K chunks x 2 lanes
-        CK(h->hand.ensure(sizeof(Singleton) * stride));
-        double *TF = reinterpret_cast<double *>(h->wsA.as<dd>());  // [row * stride + singleton]
-        double *TB = TF + stride * nbmax;
-        dd *P2s = h->wsA.as<dd>() + stride * nbmax;  // after TF, TB
-        RqiState *rs = h->rqst.as<RqiState>();
-        SegRec *rec = h->rqrec.as<SegRec>();
-        k_rqi3_init<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs);
-        if (child || nbmax <= h->twdd_root_max) {  // dd twist search: child frames, and short root blocks
-          // child frames: the dd twist search (d+ in dd over the P0 plane)
-          const int KT = 2 * K;
-          TwRec *trec = reinterpret_cast<TwRec *>(rec);
-          dd *TFd = h->wsA.as<dd>();
-          k_twist_lane_dd<false><<<nblocks_for((long long)KT * nb, 128), 128, 0, h->stream>>>(
-              sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, KT, Wu, TFd, stride, trec);
-          k_twist_lane_dd<true><<<nblocks_for((long long)KT * nb, 128), 128, 0, h->stream>>>(
-              sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, KT, Wu, TFd, stride, trec);
-          k_twist_pick2<<<nblocks_for(nb, 32), 32, stage_bytes(h, 32 * 2 * KT * sizeof(TwRec)), h->stream>>>(
-              sgb, (int)nb, h->reps.as<RepDesc>(), rs, KT, nullptr, TFd, stride, trec, 0x1p-90,
-              h->stats.as<long long>(), stage_bytes(h, 32 * 2 * KT * sizeof(TwRec)) ? 1 : 0);
-        } else if (h->tw2) {
-          // twist search: forward lane stores d+, backward lane forms gamma and the per-chunk argmin
-          const int KT = 2 * K;
-          TwRec *trec = reinterpret_cast<TwRec *>(rec);
-          k_twist_lane<false><<<nblocks_for((long long)KT * nb, 128), 128, 0, h->stream>>>(
-              sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, KT, Wu, TF, stride, trec);
-          k_twist_lane<true><<<nblocks_for((long long)KT * nb, 128), 128, 0, h->stream>>>(
-              sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, KT, Wu, TF, stride, trec);
-          k_twist_pick2<<<nblocks_for(nb, 32), 32, stage_bytes(h, 32 * 2 * KT * sizeof(TwRec)), h->stream>>>(
-              sgb, (int)nb, h->reps.as<RepDesc>(), rs, KT, TF, nullptr, stride, trec, 0x1p-46,
-              h->stats.as<long long>(), stage_bytes(h, 32 * 2 * KT * sizeof(TwRec)) ? 1 : 0);
-        } else {
-          k_twist_seg<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
-                                                                            h->mq.as<QElt>(), rs, K, Wu, TF, TB, stride,
-                                                                            rec);
-          k_twist_pick<<<(unsigned)((nb + 31) / 32), 256, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs, K,
-                                                                          TF, TB, stride, rec, h->stats.as<long long>());
-        }
-        launch_check(h);
-        for (int it = 0; it < MAX_RQI + 2; it++) {  // + the passes repeated with a wide warm-up
-          CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
-          if (h->rqi_chunk)
-            k_fixed_chunk<<<nblocks_for((2 * K + 1) * nb, 128), 128, 0, h->stream>>>(
-                sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, 2 * K, Wu, P2s, nbmax, rec,
-                h->rqi_bulk ? 1 : 0);
-          else
-            k_fixed_seg<<<nblocks_for(2 * K * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
-                                                                              h->mq.as<QElt>(), rs, K, Wu, P2s, nbmax,
-                                                                              rec, h->rqi_bal ? 1 : 0);
-          const size_t fsb = stage_bytes(h, 32 * 2 * K * (h->rqi_chunk ? 2 : 1) * sizeof(SegRec));
-          k_fixed_step<<<nblocks_for(nb, 32), 32, fsb, h->stream>>>(
-              sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, h->rqi_bal ? 1 : 0, h->rqi_chunk ? 1 : 0, rec, W,
-              h->zmeta.as<ZMeta>(),
-              diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
-              diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), h->cnt.as<int>() + C_NFB, fsb ? 1 : 0);
-          launch_check(h);
-          h->host_launches += 1;
-          if (it == 0) continue;  // the RQC-only pass never finishes a singleton: no host check after it
-          int act = 0;
-          CK(cudaMemcpyAsync(&act, h->cnt.as<int>() + C_NFB, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-          CK(cudaStreamSynchronize(h->stream));
-          if (act == 0) break;
-        }
-        const int *stat = reinterpret_cast<const int *>(reinterpret_cast<const char *>(rs) + offsetof(RqiState, status));
-        if (h->zw_chunk)
-          k_zwrite_chunk<<<nblocks_for(nb, 4), 128, 0, h->stream>>>(
-              sgb, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), P2s, nbmax, h->zmeta.as<ZMeta>(), Z, ldz, stat,
-              (int)(sizeof(RqiState) / sizeof(int)));
-        else
-          k_zwrite<<<nblocks_for(32 * nb, 256), 256, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(),
-                                                                   h->my.as<YElt>(), P2s, nbmax, h->zmeta.as<ZMeta>(),
-                                                                   Z, ldz, stat, (int)(sizeof(RqiState) / sizeof(int)));
-        launch_check(h);
+    CK(h->zmeta.ensure(sizeof(ZMeta) * stride));
+    const Singleton *sgb = h->sing.as<Singleton>() + b0;
+    int nold = (int)nb;
+    if (h->rqi_seg && allow_seg) {
+      // segmented passes (kernels_rqi3.cuh); singletons they hand over go through k_rqi2 below
+      // segments per lane: at least rqi_segk; more when the batch has few singletons (a rank's shard),
+      // so that about rqi_threads threads run, as long as a chunk stays longer than the warm-up
+      int K = h->rqi_segk;
+      // warm-up rows: 128 suffice up to n = 16K (no retries measured); longer frames get 192
+      const int Wu = h->rqi_segw > 0 ? h->rqi_segw : (nbmax <= 16384 ? 128 : 192);
+      while (2 * K <= 32 && (long long)nb * 2 * (2 * K) <= h->rqi_threads && (nbmax - 1) >= 2 * (2 * K) * Wu) K *= 2;
+      CK(h->rqst.ensure(sizeof(RqiState) * stride));
+      CK(h->rqrec.ensure(sizeof(SegRec) * stride * 4 * K));  // chunk layout: 2K chunks x 2 lanes
+      CK(h->hand.ensure(sizeof(Singleton) * stride));
+      double *TF = reinterpret_cast<double *>(h->wsA.as<dd>());  // [row * stride + singleton]
+      dd *P2s = h->wsA.as<dd>() + stride * nbmax;                 // after TF
+      RqiState *rs = h->rqst.as<RqiState>();
+      SegRec *rec = h->rqrec.as<SegRec>();
+      k_rqi3_init<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs);
+      const int KT = 2 * K;
+      TwRec *trec = reinterpret_cast<TwRec *>(rec);
+      const size_t tsb = stage_bytes(h, 32 * 2 * KT * sizeof(TwRec));
+      if (child || nbmax <= h->twdd_root_max) {
+        // child frames: the dd twist search (d+ in dd over the first plane)
+        dd *TFd = h->wsA.as<dd>();
+        k_twist_lane_dd<false><<<nblocks_for((long long)KT * nb, 128), 128, 0, h->stream>>>(
+            sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, KT, Wu, TFd, stride, trec);
+        k_twist_lane_dd<true><<<nblocks_for((long long)KT * nb, 128), 128, 0, h->stream>>>(
+            sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, KT, Wu, TFd, stride, trec);
+        k_twist_pick2<<<nblocks_for(nb, 32), 32, tsb, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs, KT, nullptr,
+                                                                 TFd, stride, trec, 0x1p-90, h->stats.as<long long>(),
+                                                                 tsb ? 1 : 0);
+      } else {
+        // twist search: forward lane stores d+, backward lane forms gamma and the per-chunk argmin
+        k_twist_lane<false><<<nblocks_for((long long)KT * nb, 128), 128, 0, h->stream>>>(
+            sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, KT, Wu, TF, stride, trec);
+        k_twist_lane<true><<<nblocks_for((long long)KT * nb, 128), 128, 0, h->stream>>>(
+            sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, KT, Wu, TF, stride, trec);
+        k_twist_pick2<<<nblocks_for(nb, 32), 32, tsb, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs, KT, TF,
+                                                                 nullptr, stride, trec, 0x1p-46,
+                                                                 h->stats.as<long long>(), tsb ? 1 : 0);
+      }
+      launch_check(h);
+      for (int it = 0; it < MAX_RQI + 2; it++) {  // + the passes repeated with a wide warm-up
         CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
-        k_rqi3_collect<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, rs, h->hand.as<Singleton>(),
-                                                                    h->cnt.as<int>() + C_NFB);
+        k_fixed_chunk<<<nblocks_for((2 * K + 1) * nb, 128), 128, 0, h->stream>>>(
+            sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, 2 * K, Wu, P2s, nbmax, rec,
+            h->rqi_bulk ? 1 : 0);
+        const size_t fsb = stage_bytes(h, 32 * 4 * K * sizeof(SegRec));
+        k_fixed_step<<<nblocks_for(nb, 32), 32, fsb, h->stream>>>(
+            sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, rec, W, h->zmeta.as<ZMeta>(),
+            diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
+            diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), h->cnt.as<int>() + C_NFB, fsb ? 1 : 0);
         launch_check(h);
-        CK(cudaMemcpyAsync(&nold, h->cnt.as<int>() + C_NFB, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        h->host_launches += 1;
+        if (it == 0) continue;  // the RQC-only pass never finishes a singleton: no host check after it
+        int act = 0;
+        CK(cudaMemcpyAsync(&act, h->cnt.as<int>() + C_NFB, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
-        sgb = h->hand.as<Singleton>();
-        h->stats_h[ST_RQI_HANDOVER] += nold;
+        if (act == 0) break;
       }
-      if (nold > 0) {
-        k_rqi2<<<nblocks_for(2 * nold, 64), 64, 64 * MRRR_RQI_RING * sizeof(RingSlot), h->stream>>>(
-            sgb, nold, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->mq.as<QElt>(), h->wsA.as<dd>(), stride, nbmax, W,
-            h->zmeta.as<ZMeta>(), diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
-            diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), h->fault);
-        launch_check(h);
-        if (h->zw_chunk)
-          k_zwrite_chunk<<<nblocks_for(nold, 4), 128, 0, h->stream>>>(
-              sgb, nold, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>() + 2 * stride * nbmax, nbmax,
-              h->zmeta.as<ZMeta>(), Z, ldz);
-        else
-          k_zwrite<<<nblocks_for(32 * nold, 256), 256, 0, h->stream>>>(
-              sgb, nold, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>() + 2 * stride * nbmax, nbmax,
-              h->zmeta.as<ZMeta>(), Z, ldz);
-      }
-    } else {
-      k_rqi<<<nblocks_for(nb, 64), 64, 0, h->stream>>>(
-          h->sing.as<Singleton>() + b0, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>(),
-          h->wsB.as<dd>(), stride, W, Z, ldz, diag ? h->ddepth.as<int>() : nullptr,
-          diag ? h->dflo.as<double>() : nullptr, diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>());
+      const int *stat = reinterpret_cast<const int *>(reinterpret_cast<const char *>(rs) + offsetof(RqiState, status));
+      k_zwrite_chunk<<<nblocks_for(nb, 4), 128, 0, h->stream>>>(
+          sgb, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), P2s, nbmax, h->zmeta.as<ZMeta>(), Z, ldz, stat,
+          (int)(sizeof(RqiState) / sizeof(int)));
+      launch_check(h);
+      CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
+      k_rqi3_collect<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, rs, h->hand.as<Singleton>(),
+                                                                  h->cnt.as<int>() + C_NFB);
+      launch_check(h);
+      CK(cudaMemcpyAsync(&nold, h->cnt.as<int>() + C_NFB, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      sgb = h->hand.as<Singleton>();
+      h->stats_h[ST_RQI_HANDOVER] += nold;
+    }
+    if (nold > 0) {
+      k_rqi2<<<nblocks_for(2 * nold, 64), 64, 64 * MRRR_RQI_RING * sizeof(RingSlot), h->stream>>>(
+          sgb, nold, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->mq.as<QElt>(), h->wsA.as<dd>(), stride, nbmax, W,
+          h->zmeta.as<ZMeta>(), diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
+          diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), h->fault);
+      launch_check(h);
+      k_zwrite_chunk<<<nblocks_for(nold, 4), 128, 0, h->stream>>>(
+          sgb, nold, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>() + 2 * stride * nbmax, nbmax,
+          h->zmeta.as<ZMeta>(), Z, ldz);
     }
     launch_check(h);
     CK(cudaEventRecord(h->rq1, h->stream));
@@ -1495,9 +1360,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_TARGET_UNSEG")) h->target_unseg = atoll(s);
     if (const char *s = getenv("MRRR_TARGET_CHILD")) h->target_child = atoll(s);
     if (const char *s = getenv("MRRR_MMAX")) h->mmax = atoi(s);
-    if (const char *s = getenv("MRRR_CH")) h->chains_per_thread = std::max(1, std::min(4, atoi(s)));
     if (const char *s = getenv("MRRR_NEGTMA")) h->neg_tma = atoi(s) != 0;
-    if (const char *s = getenv("MRRR_GUIDED")) h->guided = atoi(s) != 0;
     if (const char *s = getenv("MRRR_GROUPED")) h->grouped = atoi(s) != 0;
     if (const char *s = getenv("MRRR_SEGK")) h->seg_k = std::max(1, std::min(64, atoi(s)));
     if (const char *s = getenv("MRRR_SEGW")) h->seg_w = std::max(1, atoi(s));
@@ -1508,12 +1371,8 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_RQISEG")) h->rqi_seg = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQISEGK")) h->rqi_segk = std::max(1, std::min(64, atoi(s)));
     if (const char *s = getenv("MRRR_RQISEGW")) h->rqi_segw = std::max(1, atoi(s));
-    if (const char *s = getenv("MRRR_RQIBAL")) h->rqi_bal = atoi(s) != 0;
-    if (const char *s = getenv("MRRR_ZWCHUNK")) h->zw_chunk = atoi(s) != 0;
-    if (const char *s = getenv("MRRR_RQICHUNK")) h->rqi_chunk = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQIBULK")) h->rqi_bulk = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQITHREADS")) h->rqi_threads = atoll(s);
-    if (const char *s = getenv("MRRR_TW2")) h->tw2 = atoi(s) != 0;
     if (const char *s = getenv("MRRR_TWDD_ROOT")) h->twdd_root_max = atoll(s);
     if (const char *s = getenv("MRRR_RQISEGCHILD")) h->rqi_seg_child = atoi(s) != 0;
     if (const char *s = getenv("MRRR_SEGCHILDMIN")) h->segchild_min = atoi(s);
@@ -1525,9 +1384,6 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_SEGYW")) h->segy_w = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_SEGXK")) h->segx_k = std::max(1, std::min(64, atoi(s)));
     if (const char *s = getenv("MRRR_SEGXW")) h->segx_w = std::max(1, atoi(s));
-    if (const char *s = getenv("MRRR_BUD_FULL")) h->bud_full = std::max(1, atoi(s));
-    if (const char *s = getenv("MRRR_BUD_TUBE")) h->bud_tube = std::max(1, atoi(s));
-    if (const char *s = getenv("MRRR_RQI")) h->rqi_pair = atoi(s) != 1;
     if (const char *s = getenv("MRRR_L2PIN")) h->l2_persist = atoi(s) != 0;
     if (const char *s = getenv("MRRR_FAULT")) h->fault = atoi(s);
     if (const char *s = getenv("MRRR_RQISEGMIN")) h->rqi_seg_min = atoll(s);

@@ -13,5 +13,5 @@ timeout 900 python bench.py --workload $WL > $O/bench_${WL}_$TAG.log 2>&1; echo 
 timeout 300 python scripts/profile_solve.py $WL 2 > $O/plain_$TAG.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_${WL}_$TAG.csv \
     python scripts/profile_solve.py $WL 2 > $O/ncu_launch_$TAG.log 2>&1; echo "ncu launches rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_rqi2|k_negcount|k_zwrite" -s 0 -c 4 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_rqi2|k_negcount|k_zwrite_chunk" -s 0 -c 4 \
     -o $O/prof_${WL}_$TAG python scripts/profile_solve.py $WL 1 > $O/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"

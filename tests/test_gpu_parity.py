@@ -280,16 +280,14 @@ def test_division_fast_path_is_ieee(torch_cuda):
     assert m.selftest(1, 1 << 28, 12345) == 0
 
 
-@pytest.mark.parametrize("env", [{"MRRR_GUIDED": "1"}, {"MRRR_GROUPED": "0"}, {"MRRR_NEGTMA": "0"},
+@pytest.mark.parametrize("env", [{"MRRR_GROUPED": "0"}, {"MRRR_NEGTMA": "0"},
                                  {"MRRR_TARGET_CHAINS": "8192"}, {"MRRR_SEGK": "1"}, {"MRRR_RQISEG": "0"},
-                                 {"MRRR_RQISEG": "1", "MRRR_RQISEGK": "1"}, {"MRRR_RQIBAL": "0"},
-                                 {"MRRR_RQISEGW": "16"}, {"MRRR_ZWCHUNK": "0"},
-                                 {"MRRR_RQICHUNK": "0"}, {"MRRR_RQICHUNK": "1", "MRRR_RQISEGW": "16"},
+                                 {"MRRR_RQISEG": "1", "MRRR_RQISEGK": "1"},
+                                 {"MRRR_RQISEGW": "16"}, {"MRRR_RQISEGMIN": "0"},
                                  {"MRRR_RQIBULK": "0"}, {"MRRR_SEGCH2": "1000000"}, {"MRRR_SEGTHREADS": "262144"},
                                  {"MRRR_SEGYK": "1"}, {"MRRR_SEGYW": "8"}, {"MRRR_SEGXK": "1"}, {"MRRR_SEGXK": "8", "MRRR_SEGXW": "8"},
-                                 {"MRRR_DEVSTABLE": "0"}, {"MRRR_DEVROUNDS": "1"}, {"MRRR_TW2": "0"},
-                                 {"MRRR_TW2": "1", "MRRR_RQISEGW": "16"}, {"MRRR_RQISEGCHILD": "0"},
-                                 {"MRRR_SEGCHILDMIN": "0"}, {"MRRR_RECSTAGE": "1"}])
+                                 {"MRRR_DEVSTABLE": "0"}, {"MRRR_DEVROUNDS": "1"}, {"MRRR_RQISEGCHILD": "0"},
+                                 {"MRRR_SEGCHILDMIN": "0"}, {"MRRR_RECSTAGE": "1"}, {"MRRR_TWDD_ROOT": "100000"}])
 def test_bisection_schedules_are_bit_identical(torch_cuda, env, monkeypatch):
     # every evaluation schedule (k-section budget, TMA staging, representation-grouped child rounds, guided
     # tube rounds) must reproduce the oracle's sequential Alg. Bisection intervals bit for bit (rule W)

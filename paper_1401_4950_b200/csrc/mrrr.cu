@@ -204,6 +204,25 @@ __global__ void k_root_nodes(const int *__restrict__ blist, int nbl, const int *
   ex[t] = ExplicitChain{left ? P : -P, blk, 0};
 }
 
+// guard-extension batches of the single block: one start node per side with indices [w[2k], w[2k+1]]
+__global__ void k_guard_nodes(const int *__restrict__ starts, const double *__restrict__ binfo, int w0, int w1,
+                              int w2, int w3, Node *nodes) {
+  const int t = threadIdx.x;
+  const int wlo = t ? w2 : w0, whi = t ? w3 : w1;
+  const int nb = starts[1] - starts[0];
+  const double P = binfo[4];
+  const bool left = binfo[6] == 1.0;
+  Node nd;
+  nd.lo = left ? 0.0 : -P;
+  nd.hi = left ? P : 0.0;
+  nd.a = 0; nd.b = nb;
+  nd.wlo = wlo; nd.whi = whi;
+  nd.rep = 0; nd.pad = 0;
+  nd.obase = (long long)starts[0] - 1;
+  nd.est = NAN; nd.u = INFINITY;
+  nodes[t] = nd;
+}
+
 // verification of NegCount at the far root end; doubles P where it fails; flags a restart
 __global__ void k_root_verify(const int *__restrict__ blist, int nbl, const int *__restrict__ starts, double *binfo,
                               const int *__restrict__ excounts, int *restart) {
@@ -224,6 +243,17 @@ __global__ void k_guard_check(const int *__restrict__ cab, const double *__restr
   // positions: index j at j-1 (single block starts at 0)
   need[0] = (ca > 1 && !is_boundary(rlo[ca - 1], rhi[ca - 1], rlo[ca], rhi[ca], gaptol)) ? 1 : 0;
   need[1] = (cb < nb && !is_boundary(rlo[cb - 2], rhi[cb - 2], rlo[cb - 1], rhi[cb - 1], gaptol)) ? 1 : 0;
+}
+
+// the guard-extension rule over already computed indices (single block, positions j-1): left, from ca while
+// index ca is not separated from ca+1 step outward (not below lo_far); right likewise from cb (not above hi_far)
+__global__ void k_guard_scan(int *cab, int lo_far, int hi_far, const double *__restrict__ rlo,
+                             const double *__restrict__ rhi, int nb, double gaptol) {
+  int ca = cab[0], cb = cab[1];
+  while (ca > 1 && ca > lo_far && !is_boundary(rlo[ca - 1], rhi[ca - 1], rlo[ca], rhi[ca], gaptol)) ca--;
+  while (cb < nb && cb < hi_far && !is_boundary(rlo[cb - 2], rhi[cb - 2], rlo[cb - 1], rhi[cb - 1], gaptol)) cb++;
+  cab[0] = ca;
+  cab[1] = cb;
 }
 
 // multi-block ranking of T-frame midpoints (S4/S6): rank = #{keys before mine}
@@ -1164,6 +1194,21 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
     CK(h->nodesB.ensure(sizeof(Node) * cap));
     CK(h->ex.ensure(sizeof(ExplicitChain) * (nbl + 64)));
     CK(h->excounts.ensure(sizeof(int) * (nbl + 64)));
+    // a single block's subset (or shard) bisects GUARD_MARGIN indices beyond each guard in the same run, so that
+    // a cluster that straddles the edge is usually covered without a guard-extension pass (the indices the
+    // extension rule does not reach are reset to "not computed" below)
+    const int GUARD_MARGIN = 32;
+    std::vector<int> cabm = cab;
+    if (single && nbl) {
+      if (cab[0] > 1) cabm[0] = std::max(1, cab[0] - GUARD_MARGIN);
+      if (cab[1] < (int)n) cabm[1] = std::min((int)n, cab[1] + GUARD_MARGIN);
+      if (cabm != cab) {
+        h->max_nodes = std::max<int>(h->max_nodes, cabm[1] - cabm[0] + 3);
+        CK(h->nodesA.grow_keep(sizeof(Node) * (size_t)h->max_nodes, 0, st));
+        CK(h->nodesB.grow_keep(sizeof(Node) * (size_t)h->max_nodes, 0, st));
+        CK(cudaMemcpyAsync(h->cab.p, cabm.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, st));
+      }
+    }
     for (int attempt = 0; attempt < 64; attempt++) {
       k_root_nodes<<<nblocks_for(nbl, 128), 128, 0, st>>>(h->blist.as<int>(), nbl, h->starts.as<int>(),
                                                           h->binfo.as<double>(), h->cab.as<int>(), h->nodesA.as<Node>(),
@@ -1174,6 +1219,7 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
                            &restart, -1, 0, single ? (int)n : 0);
       if (!restart) break;
     }
+    if (cabm != cab) CK(cudaMemcpyAsync(h->cab.p, cab.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, st));
     // root definiteness
     std::vector<double> hb(16 * nblk);
     CK(cudaMemcpy(hb.data(), h->binfo.p, sizeof(double) * 16 * nblk, cudaMemcpyDeviceToHost));
@@ -1181,36 +1227,65 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
       if (hb[16 * b + 8] == 0.0) return MRRR_ERR_ROOT;
       h->stats_h[ST_ROOT_BACKOFF] += (long long)hb[16 * b + 7];
     }
-    // guard extension (single block): bisect one more index until separated
+    // guard extension (single block, S5): the oracle bisects one more index at a time while the outermost
+    // computed index is not separated from its inner neighbour.  Here the indices beyond each unseparated end are
+    // bisected in doubling batches (1, 2, 4, ... indices in one shared-tree run), k_guard_scan walks their
+    // boundaries outward from the old end exactly as the one-at-a-time rule does, and the indices the rule never
+    // reaches are reset to "not computed" -- the same computed set and intervals, in O(log) passes instead of one
+    // pass per index of a cluster that straddles a subset or shard edge (255 passes in C4's clusters)
     if (single && nbl) {
       int nb = (int)n;
-      CK(h->scal.ensure(64));
-      for (int it = 0; it < nb; it++) {
+      int step[2] = {256, 256};  // extension batches: 256 indices per side, then doubling
+      int far[2] = {cabm[0], cabm[1]};  // outermost computed index per side (margin and batches overshoot the rule)
+      for (int it = 0; it < 64; it++) {
+        // walk outward from the current ends over the computed indices: the one-at-a-time rule's stopping point
+        CK(cudaMemcpyAsync(h->cab.p, cab.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, st));
+        k_guard_scan<<<1, 1, 0, st>>>(h->cab.as<int>(), far[0], far[1], h->rlo.as<double>(), h->rhi.as<double>(),
+                                      nb, h->gaptol);
+        launch_check(h);
+        CK(cudaMemcpyAsync(cab.data(), h->cab.p, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
         k_guard_check<<<1, 1, 0, st>>>(h->cab.as<int>(), h->rlo.as<double>(), h->rhi.as<double>(), nb, h->gaptol,
                                        h->cnt.as<int>() + 8);
         launch_check(h);
         read_counters(h);
-        bool needL = h->h_cnt[8], needR = h->h_cnt[9];
-        if (!needL && !needR) break;
-        if (needL) cab[0]--;
-        if (needR) cab[1]++;
-        CK(cudaMemcpyAsync(h->cab.p, cab.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, st));
-        // one node per new index, from the root start interval
-        std::vector<int> cab1 = cab;
+        const bool need[2] = {h->h_cnt[8] != 0, h->h_cnt[9] != 0};
+        if (!need[0] && !need[1]) break;
+        // both sides' batches beyond the computed extents, in one shared-tree run
+        int w[4] = {0, -1, 0, -1}, nn = 0;
         for (int side = 0; side < 2; side++) {
-          bool need = side ? needR : needL;
-          if (!need) continue;
-          int j = side ? cab[1] : cab[0];
-          std::vector<int> cj = {j, j};
-          CK(cudaMemcpyAsync(h->cab.p, cj.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, st));
-          k_root_nodes<<<1, 1, 0, st>>>(h->blist.as<int>(), 1, h->starts.as<int>(), h->binfo.as<double>(),
-                                        h->cab.as<int>(), h->nodesA.as<Node>(), h->ex.as<ExplicitChain>());
+          if (!need[side]) continue;
+          const int a = side ? far[1] + 1 : std::max(1, far[0] - step[0]);
+          const int b = side ? std::min(nb, far[1] + step[1]) : far[0] - 1;
+          step[side] *= 2;
+          if (a > b) continue;
+          w[2 * nn] = a;
+          w[2 * nn + 1] = b;
+          nn++;
+          far[side] = side ? b : a;
+        }
+        if (nn > 0) {
+          // node capacity: every index of the batches may separate
+          h->max_nodes = std::max(h->max_nodes, (w[1] - w[0] + 1) + (w[3] - w[2] + 1) + 2);
+          CK(h->nodesA.grow_keep(sizeof(Node) * (size_t)h->max_nodes, 0, st));
+          CK(h->nodesB.grow_keep(sizeof(Node) * (size_t)h->max_nodes, 0, st));
+          k_guard_nodes<<<1, nn, 0, st>>>(h->starts.as<int>(), h->binfo.as<double>(), w[0], w[1], w[2], w[3],
+                                          h->nodesA.as<Node>());
           launch_check(h);
           bool rs = false;
-          run_bisection<false>(h, 1, h->rlo.as<double>(), h->rhi.as<double>(), rtol, 0, nullptr, 0, &rs);
+          run_bisection<false>(h, nn, h->rlo.as<double>(), h->rhi.as<double>(), rtol, 0, nullptr, 0, &rs, -1, 0, nb);
         }
-        CK(cudaMemcpyAsync(h->cab.p, cab.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, st));
       }
+      CK(cudaMemcpyAsync(h->cab.p, cab.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, st));
+      // indices a batch computed beyond the rule's stopping point: not computed (as in the oracle)
+      if (far[0] < cab[0]) {
+        k_fill<<<nblocks_for(cab[0] - far[0], 256), 256, 0, st>>>(h->rlo.as<double>() + far[0] - 1, cab[0] - far[0], NAN);
+        k_fill<<<nblocks_for(cab[0] - far[0], 256), 256, 0, st>>>(h->rhi.as<double>() + far[0] - 1, cab[0] - far[0], NAN);
+      }
+      if (far[1] > cab[1]) {
+        k_fill<<<nblocks_for(far[1] - cab[1], 256), 256, 0, st>>>(h->rlo.as<double>() + cab[1], far[1] - cab[1], NAN);
+        k_fill<<<nblocks_for(far[1] - cab[1], 256), 256, 0, st>>>(h->rhi.as<double>() + cab[1], far[1] - cab[1], NAN);
+      }
+      launch_check(h);
     }
   }
   CK(cudaEventRecord(h->ev[2], st));

@@ -132,6 +132,18 @@ def test_parity_subset_in_cluster(torch_cuda):
         check_tol(d, e, g["W"], g["Z"], r.W, 301.0)
 
 
+@pytest.mark.parametrize("il,iu", [(5, 7), (1, 40), (100, 130), (1500, 1600), (1604, 1608)])
+def test_parity_subset_edges_in_large_clusters(torch_cuda, il, iu):
+    # glued Wilkinson with clusters of 8/16 (and 256-clusters at C4 size): the guards extend through whole
+    # clusters in doubling batches; the computed set (NaN pattern), intervals and groups equal the oracle's
+    # one-at-a-time extension bit for bit
+    d, e = mi.glued_wilkinson(8, 100, 1e-10)
+    g = gpu_solve(torch_cuda, d, e, il, iu)
+    r = oracle.mrrr(d, e, il, iu)
+    check_integers(g, r)
+    check_tol(d, e, g["W"], g["Z"], r.W, 101.0)
+
+
 @pytest.mark.parametrize("sel", [(1, 40), (3, 9), (10, 40), (40, 40), (1, 1)])
 def test_parity_split_matrix(torch_cuda, sel):
     rng = np.random.default_rng(3)

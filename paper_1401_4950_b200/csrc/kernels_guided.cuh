@@ -585,11 +585,15 @@ __global__ void k_seg_combine_xg(long long tot, long long nn, int K, const SegOu
   f.cnt = (prev >= 0) ? total : 0;
   fb[atomicAdd(nfb, 1)] = f;
 }
-// careful (IEEE) tail from the first unverified segment's first row with the last exact state
+// careful (IEEE) evaluation from the first unverified segment's first row with the last exact state, re-joining
+// the recorded segments: after running a segment exactly, the next segment's result is taken over as soon as its
+// recorded entry state equals the exact one bit for bit (then it saw the sequential operands); only the segments
+// whose warm-up did not converge are re-run (one or two per chain instead of the whole tail)
 __global__ void k_seg_fallback_xg(const FbX *__restrict__ fb, const int *__restrict__ nfb,
                                   const Node *__restrict__ nodes, int nnode, int m,
                                   const ExplicitChain *__restrict__ ex, const RepDesc *__restrict__ reps,
-                                  const double2 *__restrict__ mx, int K, int Wu, int *counts, int *excounts) {
+                                  const double2 *__restrict__ mx, int K, int Wu, int *counts, int *excounts,
+                                  const SegOutX *__restrict__ seg) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *nfb) return;
   const FbX f = fb[i];
@@ -600,16 +604,14 @@ __global__ void k_seg_fallback_xg(const FbX *__restrict__ fb, const int *__restr
   const RepDesc R = reps[rep];
   const double2 *M = mx + R.off;
   const int nb = R.nb, steps = nb - 1;
-  const int L = (steps >= 2 * K * Wu) ? (steps + K - 1) / K : steps;
+  const bool segd = steps >= 2 * K * Wu;
+  const int L = segd ? (steps + K - 1) / K : steps;
+  const SegOutX *S = seg + f.c * K;
   double s = f.s;
   int cnt = f.cnt;
   // the IEEE operations, with the verified division fast path where its range test passes (bit-identical);
   // the child representation streams from HBM: PF rows in flight
   constexpr int PF = 8;
-  const int r0 = min(f.k * L, steps);
-  double2 ring[PF];
-#pragma unroll
-  for (int u = 0; u < PF; u++) ring[u] = __ldg(M + min(r0 + u, nb - 1));
   auto step = [&](double2 mm) {
     const double dp = __dadd_rn(mm.x, s);
     double q = div_fast_nocheck(s, dp);
@@ -617,18 +619,48 @@ __global__ void k_seg_fallback_xg(const FbX *__restrict__ fb, const int *__restr
     s = __dsub_rn(__dmul_rn(q, mm.y), sig);
     cnt += sbx(dp);
   };
-  int r = r0;
-  for (; r + PF <= steps; r += PF) {
+  auto run_rows = [&](int r0, int r1) {  // steps on rows [r0, r1)
+    double2 ring[PF];
 #pragma unroll
-    for (int u = 0; u < PF; u++) {
-      const double2 mm = ring[u];
-      ring[u] = __ldg(M + min(r + u + PF, nb - 1));
-      step(mm);
+    for (int u = 0; u < PF; u++) ring[u] = __ldg(M + min(r0 + u, nb - 1));
+    int r = r0;
+    for (; r + PF <= r1; r += PF) {
+#pragma unroll
+      for (int u = 0; u < PF; u++) {
+        const double2 mm = ring[u];
+        ring[u] = __ldg(M + min(r + u + PF, nb - 1));
+        step(mm);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PF; u++)
+      if (r + u < r1) step(ring[u]);
+  };
+  int k = f.k;
+  if (!segd) {
+    run_rows(0, steps);
+  } else {
+    while (k < K) {
+      const int bk = min(k * L, steps), ek = min(bk + L, steps);
+      run_rows(bk, ek);  // segment k exactly
+      k++;
+      // re-join: take over every following segment whose entry state is the exact one
+      while (k < K) {
+        const SegOutX o = S[k];
+        if (o.empty) { k++; continue; }
+        if (!o.ok || __double_as_longlong(o.in) != __double_as_longlong(s)) break;
+        cnt += o.cnt;  // (the segment that ends at the last step also counted the final row)
+        s = o.out;
+        const int ekk = min(min(k * L, steps) + L, steps);
+        k++;
+        if (ekk == steps) {
+          if (f.c < nn) counts[f.c] = cnt;
+          else excounts[f.c - nn] = cnt;
+          return;
+        }
+      }
     }
   }
-#pragma unroll
-  for (int u = 0; u < PF; u++)
-    if (r + u < steps) step(ring[u]);
   cnt += sbx(__dadd_rn(__ldg(M + nb - 1).x, s));
   if (f.c < nn) counts[f.c] = cnt;
   else excounts[f.c - nn] = cnt;

@@ -350,7 +350,8 @@ void launch_negcount(mrrr_t h, const Node *nodes, int nnode, int m, int nex, con
                                                                    h->segfby.as<FbX>(), h->cnt.as<int>() + C_NFB);
     k_seg_fallback_xg<<<nblocks_for(tot, 128), 128, 0, h->stream>>>(
         h->segfby.as<FbX>(), h->cnt.as<int>() + C_NFB, nodes, nnode, m, h->ex.as<ExplicitChain>(),
-        h->reps.as<RepDesc>(), h->mx.as<double2>(), K, h->segx_w, h->counts.as<int>(), h->excounts.as<int>());
+        h->reps.as<RepDesc>(), h->mx.as<double2>(), K, h->segx_w, h->counts.as<int>(), h->excounts.as<int>(),
+        h->segoutx.as<SegOutX>());
     launch_check(h);
     return;
   }

@@ -784,6 +784,10 @@ __global__ void k_clu_attempt_combine(const Cluster *__restrict__ cl, int ncl, c
 // [bk, ek) after a warm-up and writes those child rows; k_clu_build_combine verifies the junctions and
 // rebuilds the clusters that do not verify whole (clu_build_one), so the child representation is bit for
 // bit the sequential one.  Records: SegG (gmax unused).
+#ifndef MRRR_BG
+#define MRRR_BG 4
+#endif
+constexpr int BG = MRRR_BG;  // child rows per bulk store in k_clu_build_seg
 __global__ void __launch_bounds__(128) k_clu_build_seg(const Cluster *__restrict__ cl, int ncl,
                                                        const RepDesc *__restrict__ reps,
                                                        const ShiftState *__restrict__ ss, double2 *mx, YElt *my,
@@ -827,7 +831,25 @@ __global__ void __launch_bounds__(128) k_clu_build_seg(const Cluster *__restrict
   bool ok = true;
   for (int i = w0; i < bk; i++) den = clu_build_row(den, q, i, tau, nullptr, nullptr, ok);
   din = den;
-  for (int i = bk; i < ek; i++) den = clu_build_row(den, q, i, tau, yc, xc, ok);
+  // the rows are staged in shared memory and written by bulk (TMA-engine) copies of BG-row runs: a warp's lanes
+  // are different clusters, so plain stores scattered 32 partial lines per instruction (store-bound: C3's child
+  // build moved 8.6 GB at 0.66 TB/s)
+  extern __shared__ __align__(16) unsigned char bsm[];
+  YElt *sy = reinterpret_cast<YElt *>(bsm) + threadIdx.x * 2 * BG;
+  double2 *sx = reinterpret_cast<double2 *>(bsm + (size_t)blockDim.x * 2 * BG * sizeof(YElt)) + threadIdx.x * 2 * BG;
+  int grp = 0, ng = 0;
+  for (int i = bk; i < ek; i++) {
+    den = clu_build_row(den, q, i, tau, sy + grp * BG + ng, sx + grp * BG + ng, ok, true);
+    if (++ng == BG || i + 1 == ek) {
+      const int low = i - ng + 1;
+      bulk_store(yc + low, sy + grp * BG, (unsigned)(ng * sizeof(YElt)));
+      bulk_store(xc + low, sx + grp * BG, (unsigned)(ng * sizeof(double2)));
+      grp ^= 1;
+      ng = 0;
+      bulk_wait_read<2>();  // the other group's two stores have read their rows
+    }
+  }
+  bulk_wait_all();
   if (ek == steps) {
     ok &= isfinite(den.hi) && isfinite(den.lo);
     YElt e;

@@ -255,20 +255,6 @@ __device__ __forceinline__ bool rcp_nr2(double b, double &r1, double &r2) {
   r2 = __fma_rn(r1, e2, r1);
   return (fabs(b) > 0x1p-1000) && (fabs(b) < 0x1p1000);
 }
-// bulk (TMA-engine) store of a thread's staged factor rows: one contiguous run per 8 rows instead of 8
-// lane-scattered 16-byte stores (a warp's lanes are different singletons, so plain stores hit 32 lines)
-__device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, unsigned bytes) {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
-               "r"(bytes)
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 #ifndef MRRR_ZG
 #define MRRR_ZG 8
 #endif

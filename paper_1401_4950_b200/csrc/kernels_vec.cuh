@@ -212,7 +212,7 @@ __global__ void k_clu_select_multi(const Cluster *__restrict__ cl, int ncl, cons
 // one row of the fast child build: l+(i) = dl(i)/d+(i) and c2(i)/d+(i) from the reciprocal pair of d+(i),
 // the child's y-row (d, dl, dll) and x-row (d, dll); returns d+(i+1) (the y_step recurrence)
 __device__ __forceinline__ dd clu_build_row(dd den, const QElt *__restrict__ q, int i, dd tau, YElt *yc, double2 *xc,
-                                            bool &ok) {
+                                            bool &ok, bool staged = false) {
   const double b = den.hi;
   ok &= (fabs(b) > 0x1p-1000) && (fabs(b) < 0x1p1000);
   const double r = rcp_seed(b);
@@ -235,9 +235,10 @@ __device__ __forceinline__ dd clu_build_row(dd den, const QElt *__restrict__ q, 
     const dd dll = dd_mul(dl, out);
     YElt e;
     e.d_hi = den.hi; e.d_lo = den.lo; e.dl_hi = dl.hi; e.dl_lo = dl.lo; e.dll_hi = dll.hi; e.dll_lo = dll.lo;
-    yc[i] = e;
     const double dx = den.hi, lx = out.hi;
-    xc[i] = make_double2(dx, __dmul_rn(__dmul_rn(dx, lx), lx));
+    const double2 xe = make_double2(dx, __dmul_rn(__dmul_rn(dx, lx), lx));
+    if (staged) { *yc = e; *xc = xe; }  // shared-memory staging slot of row i
+    else { yc[i] = e; xc[i] = xe; }
   }
   return dd_sub_nf(dd_sub_nf(dd_make(__ldg(&q[i].gf_hi), __ldg(&q[i].gf_lo)), tau), Pq);
 }

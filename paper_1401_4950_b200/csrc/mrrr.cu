@@ -930,7 +930,13 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
     if (h->segy_k > 1) {  // child rows built by verified segments (latency n/K + W rows per thread)
       const int K = h->segy_k;
       CK(h->segoutg.ensure(sizeof(SegG) * (long long)nc * K));
-      k_clu_build_seg<<<nblocks_for((long long)nc * K, 128), 128, 0, h->stream>>>(
+      const size_t bsb = (size_t)128 * 2 * BG * (sizeof(YElt) + sizeof(double2));
+      static bool bsb_set = false;
+      if (!bsb_set) {
+        CK(cudaFuncSetAttribute(k_clu_build_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsb));
+        bsb_set = true;
+      }
+      k_clu_build_seg<<<nblocks_for((long long)nc * K, 128), 128, bsb, h->stream>>>(
           cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(), h->mx.as<double2>(), h->my.as<YElt>(),
           h->mq.as<QElt>(), poolbase, (int)nbmax, K, h->segy_w, h->segoutg.as<SegG>());
       CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));

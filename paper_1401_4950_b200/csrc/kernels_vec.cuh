@@ -73,7 +73,7 @@ __global__ void k_clu_yref_init(const Cluster *__restrict__ cl, int ncl, const R
     dyadic_widen(L, H, &L, &H);
     BNode b;
     b.lo = L; b.hi = H; b.clo = 0; b.chi = 0; b.j = j; b.rep = C.rep;
-    b.needLo = 1; b.needHi = 1; b.fixes = 0; b.pad = 0;
+    b.needLo = 1; b.needHi = 1; b.fixes = 0; b.j2 = j;
     b.obase = 2LL * c + side - j;
     bn[2 * c + side] = b;
   }
@@ -178,7 +178,9 @@ __global__ void k_clu_select_multi(const Cluster *__restrict__ cl, int ncl, cons
   if (c >= ncl) return;
   ShiftState s = ss[c];
   if (s.done) { atomicAdd(ndone, 1); return; }
-  const double gthr = __dmul_rn(GROWTH, reps[cl[c].rep].spdiam);
+  // mixed-precision growth bound eq:newkelgbound P:6052-6056 (A-35): max(G, eps_x / (eps_y sqrt(n))) spdiam
+  const RepDesc Rg = reps[cl[c].rep];
+  const double gthr = __dmul_rn(dmaxd(GROWTH, __ddiv_rn(0x1p51, sqrt((double)Rg.nb))), Rg.spdiam);
   for (int a = a0; a < a0 + na && !s.done; a++) {
     atomicAdd((unsigned long long *)&stats[ST_ATTEMPTS], 1ull);
     const long long o = ((long long)c * na + (a - a0)) * 2;
@@ -346,7 +348,7 @@ __global__ void k_clu_child_starts(const Cluster *__restrict__ cl, int ncl, cons
     dyadic_widen(l2, h2, &L, &H);
     BNode b;
     b.lo = L; b.hi = H; b.clo = 0; b.chi = 0; b.j = j; b.rep = repbase + c;
-    b.needLo = 1; b.needHi = 1; b.fixes = 0; b.pad = 0;
+    b.needLo = 1; b.needHi = 1; b.fixes = 0; b.j2 = j;
     b.obase = base;
     bn[o + (j - C.p)] = b;
   }

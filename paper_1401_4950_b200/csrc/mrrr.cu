@@ -123,6 +123,7 @@ struct mrrr_ctx {
   int max_nodes = 0;           // bound on live bisection nodes (indices in the computed set)  // tube point budgets: no estimate (4 full levels) / with estimate
   bool l2_persist = true;
   long long rqi_seg_min = 2048; // root blocks up to this size skip the segmented RQI (MRRR_RQISEGMIN)
+  bool bmerge = true;            // start nodes sharing a start interval bisected as one node (MRRR_BMERGE=0: off)
   bool nonlocal = false;         // this solve's root rounds found non-contracting recurrences (see run_bisection)
   int fault = 0;               // MRRR_FAULT: fault injection for the GPU tests (k_rqi2: bit 0 fallback, bit 1 careful)
   long long l2_max_window = 0;
@@ -671,6 +672,12 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
 template <bool Y>
 int run_brackets(mrrr_t h, int nbn) {
   BNode *cur = h->bnA.as<BNode>(), *pend = h->bnB.as<BNode>();
+  // consecutive start nodes with identical start intervals: one shared node per run
+  if (nbn > 1 && h->bmerge) {
+    k_bnode_mark<<<nblocks_for(nbn, 128), 128, 0, h->stream>>>(cur, nbn);
+    k_bnode_merge<<<nblocks_for(nbn, 128), 128, 0, h->stream>>>(cur, nbn);
+    launch_check(h);
+  }
   Node *ready = h->nodesA.as<Node>();
   int nready = 0;
   zero_counters(h);
@@ -1468,6 +1475,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_SEGXW")) h->segx_w = std::max(1, atoi(s));
     if (const char *s = getenv("MRRR_L2PIN")) h->l2_persist = atoi(s) != 0;
     if (const char *s = getenv("MRRR_FAULT")) h->fault = atoi(s);
+    if (const char *s = getenv("MRRR_BMERGE")) h->bmerge = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQISEGMIN")) h->rqi_seg_min = atoll(s);
     {
       int dev = h->device, maxwin = 0, l2 = 0;

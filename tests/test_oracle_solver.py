@@ -163,6 +163,9 @@ def test_glued_wilkinson_band_structure_larger():
         sizes.append(b - a)
     assert max(sizes) == 16 and sizes.count(8) > 0
     assert r.stats["n_clusters"] > 0
+    # the mixed solver's relaxed growth bound (eq:newkelgbound P:6052-6056, A-35) certifies every shift of the
+    # glued matrix (with the fixed bound 64 eight of them were uncertified): phi = 1
+    assert r.stats["uncertified"] == 0 and r.stats["shift_attempts"] == r.stats["n_clusters"]
 
 
 def test_split_matrices_multiblock():

@@ -34,7 +34,7 @@ typedef __float128 qreal;
 #define EPS_Y 0x1p-104         /* conservative y unit roundoff for thresholds (A-14) */
 #define ATOL (2.0 * DBL_MIN)   /* atol = 2 omega */
 #define RTOL_Y 0x1p-50         /* "full accuracy" of cluster ends in y (A-12) */
-#define GROWTH 64.0            /* element growth threshold (A-11) */
+#define GROWTH 64.0            /* element growth threshold (A-11), relaxed by eq:newkelgbound (A-35) */
 #define MAX_ATTEMPTS 6         /* shift attempts (A-11) */
 #define MAX_RQI 10             /* RQI cap (A-14) */
 #define MAXD 8                 /* representation tree depth cap */
@@ -670,7 +670,9 @@ static void do_cluster(const ctx_t *cx, const rep_t *M, const double *lo, const 
   qreal *bd = malloc(sizeof(qreal) * nb), *bl = malloc(sizeof(qreal) * nb);
   double best_g = INFINITY, best_tau = 0;
   int have_best = 0, certified = 0;
-  double gthr = GROWTH * M->spdiam;
+  /* growth bound of the mixed solver, eq:newkelgbound P:6052-6056 (A-35): k_elg <= max(original, eps_x / (eps_y */
+  /* sqrt(n))), with the original bound G = 64 of A-11                                                             */
+  double gthr = dmax(GROWTH, 0x1p51 / sqrt((double)nb)) * M->spdiam;
   for (int a = 0; a < MAX_ATTEMPTS; a++) {
     STAT_ADD(ST_ATTEMPTS, 1);
     dstqds_q(nb, M->d, M->dl, M->dll, (qreal)taul, dpl, lpl, NULL);

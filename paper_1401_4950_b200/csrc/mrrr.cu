@@ -113,8 +113,8 @@ struct mrrr_ctx {
   bool stage_attr = false, rec_stage = false;  // record staging in shared memory (MRRR_RECSTAGE=1; slower on C2)
   size_t stage_lim = 0;
   long long seg_ch2 = 0;  // segmented rounds with at most this many chains run two chains per thread (slower on C2)
-  long long seg_threads = 131072;  // adaptive segment count: more segments while a round has fewer threads
-  int seg_minlen = 2048;           // ... and the segments stay this long (only long chains: a rank's C5a shard)
+  long long seg_threads = 262144;  // adaptive segment count: more segments while a round has fewer threads
+  int seg_minlen = 512;            // ... and the segments stay this long (long chains: C5b, a rank's C5a shard)
   int dev_frac = 0;            // ... once the indices still sharing nodes are at most 1/dev_frac of the nodes (0: by n)
   bool dev_stable = true;      // device-driven rounds once every node holds one index (exact grids)
   int dev_rb = 16;            // rounds per device-driven batch (32: empty tail rounds cost a rank's short run)

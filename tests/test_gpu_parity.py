@@ -186,6 +186,44 @@ def test_scaled_inputs(torch_cuda, s):
     assert np.array_equal(r.W, g["W"]) or np.max(np.abs(np.ldexp(g["W"] - r.W, -s))) <= 8 * 700 * EPS * 3
 
 
+@pytest.mark.parametrize("case", ["zero", "constant_diag", "two_equal_blocks", "tiny_offdiag"])
+def test_degenerate_inputs(torch_cuda, case):
+    # degenerate inputs: the zero matrix and a constant diagonal (every off-diagonal splits: n blocks of size 1,
+    # all eigenvalues equal), two identical decoupled blocks (every eigenvalue exactly double), off-diagonals
+    # just above the split threshold
+    n = 60
+    if case == "zero":
+        d, e = np.zeros(n), np.zeros(n - 1)
+    elif case == "constant_diag":
+        d, e = np.full(n, 2.5), np.zeros(n - 1)
+    elif case == "two_equal_blocks":
+        d1, e1 = mi.random_tridiag(30, 5, -1.0)
+        d, e = np.concatenate([d1, d1]), np.concatenate([e1, [0.0], e1])
+    else:
+        d, e = mi.random_tridiag(n, 6, -1.0)
+        e[10] = 4 * EPS * np.sqrt(n) * 4
+    g = gpu_solve(torch_cuda, d, e)
+    r = oracle.mrrr(d, e)
+    assert r.info == 0
+    check_integers(g, r)
+    tn = max(abs(r.W[0]), abs(r.W[-1]), 1.0)
+    check_tol(d, e, g["W"], g["Z"], r.W, tn)
+    assert oracle.ortho_full(g["Z"]) <= max(n, 32) * EPS
+
+
+def test_large_n_small_subset(torch_cuda):
+    # n = 300,000 (past C5a's 65,536): 64-bit offsets of the workspace planes and of Z, indices 1..48 and the
+    # last 48, compared with the oracle
+    n = 300_000
+    d, e = mi.random_tridiag(n, 8, 0.0)
+    for il, iu in [(1, 48), (n - 47, n)]:
+        g = gpu_solve(torch_cuda, d, e, il, iu)
+        r = oracle.mrrr(d, e, il, iu)
+        check_integers(g, r)
+        check_tol(d, e, g["W"], g["Z"], r.W, 2.5)
+        assert oracle.ortho_full(g["Z"]) <= n * EPS
+
+
 def test_error_codes(torch_cuda):
     import paper_1401_4950_b200 as m
     d, e = mi.one_two_one(5)

@@ -82,6 +82,22 @@ int mrrr_eig(mrrr_t h, const double *d, const double *e, int64_t n, int64_t il, 
 int mrrr_eig_host(mrrr_t h, const double *d, const double *e, int64_t n, int64_t il, int64_t iu, double *W,
                   double *Z, int64_t ldz);
 
+/* Single/double realisation: eigenpairs il..iu of T given in binary32, W and Z
+ * returned in binary32, every computation in binary64 ("data conversion is only necessary when reading the
+ * input and writing the output").  Parameters of that realisation:
+ * gaptol fixed to 1e-5 (mrrr_opts.gaptol is ignored here), bisection to 1e-2 gaptol, epsilon_x =
+ * 2^-24 in the split rule, the root perturbation and the RQI stopping test, the growth bound
+ * max(64, 2^29 / sqrt(n)) spdiam (eq:newkelgbound P:6052-6056).  Accuracy target: residuals and orthogonality
+ * O(n eps_s), eps_s = 2^-24.  d, e, W, Z are DEVICE pointers (float); ldz >= n.  The solve keeps binary64
+ * copies of W and Z in handle workspace (8 n k bytes) before the final conversion.  Same argument checks and
+ * return codes as mrrr_eig. */
+int mrrr_seig(mrrr_t h, const float *d, const float *e, int64_t n, int64_t il, int64_t iu, float *W, float *Z,
+              int64_t ldz);
+
+/* mrrr_seig with HOST pointers (copies in, solve, copies out). */
+int mrrr_seig_host(mrrr_t h, const float *d, const float *e, int64_t n, int64_t il, int64_t iu, float *W,
+                   float *Z, int64_t ldz);
+
 /* Index-range shard of a multi-GPU solve (one process per GPU) of the selection
  * [il, iu]: the rank's shard is the contiguous range [sl, su] (1-based, il <= sl <= su <= iu); every rank
  * builds the same root (bit-identical: the root side follows the same rule on [il, iu] as mrrr_eig), bisects

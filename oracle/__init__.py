@@ -17,6 +17,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "mrrr_oracle.c")
 LIB = os.path.join(HERE, "liboracle.so")
+LIB_SD = os.path.join(HERE, "liboracle_sd.so")  # the same source with -DORACLE_SD: single/double realisation
 
 CFLAGS = ["-O2", "-std=gnu11", "-fopenmp", "-fPIC", "-shared", "-ffp-contract=off",
           "-fno-fast-math", "-fexcess-precision=standard"]
@@ -27,9 +28,9 @@ STAT_NAMES = ["d_max", "n_clusters", "largest_cluster", "uncertified", "shift_at
 
 
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        cmd = ["gcc", *CFLAGS, "-o", LIB, SRC, "-lquadmath", "-lm"]
-        subprocess.check_call(cmd)
+    for out, extra in ((LIB, []), (LIB_SD, ["-DORACLE_SD"])):
+        if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(SRC):
+            subprocess.check_call(["gcc", *CFLAGS, *extra, "-o", out, SRC, "-lquadmath", "-lm"])
     return LIB
 
 
@@ -44,16 +45,16 @@ class _Diag(C.Structure):
                  "grp_first", "grp_last", "fin_lo", "fin_hi", "stats")]
 
 
-_lib = None
+_libs = {}
 _dp = C.POINTER(C.c_double)
 _i64 = C.c_int64
 
 
-def lib():
-    global _lib
-    if _lib is None:
+def lib(sd: bool = False):
+    """The double/quadruple oracle, or (sd=True) the single/double realisation built from the same source."""
+    if sd not in _libs:
         build()
-        L = C.CDLL(LIB)
+        L = C.CDLL(LIB_SD if sd else LIB)
         L.oracle_mrrr.restype = C.c_int
         L.oracle_mrrr.argtypes = [_i64, C.c_void_p, C.c_void_p, _i64, _i64, C.POINTER(_Opts), C.c_void_p,
                                   C.c_void_p, _i64, C.POINTER(_Diag)]
@@ -118,8 +119,8 @@ def lib():
         L.oracle_root_x_from.restype = C.c_int
         L.oracle_root_x_from.argtypes = [_i64, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_double, _dp,
                                          C.c_void_p, C.c_void_p, C.POINTER(C.c_int)]
-        _lib = L
-    return _lib
+        _libs[sd] = L
+    return _libs[sd]
 
 
 def _f64(a):
@@ -150,18 +151,23 @@ class OracleResult:
     stats: dict = field(default_factory=dict)
 
 
-def mrrr(d, e, il: int | None = None, iu: int | None = None, *, gaptol: float = 1e-10, seed: int = 0,
-         root_side: int = 0, threads: int = 0, roots_only: bool = False) -> OracleResult:
+def mrrr(d, e, il: int | None = None, iu: int | None = None, *, gaptol: float | None = None, seed: int = 0,
+         root_side: int = 0, threads: int = 0, roots_only: bool = False, sd: bool = False) -> OracleResult:
     """Eigenpairs il..iu (1-based, inclusive) of the tridiagonal (d, e) by the oracle.  roots_only: stop after
-    the root bisection (S1-S5): only nblocks/block_start/mu/side/root_lo/root_hi/root_gstart are filled."""
+    the root bisection (S1-S5): only nblocks/block_start/mu/side/root_lo/root_hi/root_gstart are filled.
+    sd: the single/double realisation (liboracle_sd.so, gaptol 1e-5 by default); its inputs are
+    the binary32 values (pass them as float32 or as their exact float64 images) and W, Z come back in float64
+    before the final binary32 rounding (float32 of them is the realisation's output)."""
     d = _f64(d)
     n = d.size
     e = _f64(e) if n > 1 else np.zeros(1)
     il = 1 if il is None else int(il)
     iu = n if iu is None else int(iu)
     k = iu - il + 1
-    L = lib()
+    L = lib(sd)
     maxd = L.oracle_maxd()
+    if gaptol is None:
+        gaptol = 0.0 if sd else 1e-10
     W = np.zeros(k)
     Z = np.zeros((k, n))  # column j of the Fortran-style Z is row j here (ldz = n)
     nblocks = np.zeros(1, np.int32)
@@ -188,8 +194,8 @@ def mrrr(d, e, il: int | None = None, iu: int | None = None, *, gaptol: float = 
 
 
 # ---------------------------------------------------------------- unit wrappers
-def xi(seed: int, idx: int) -> float:
-    return lib().oracle_xi(seed, idx)
+def xi(seed: int, idx: int, *, sd: bool = False) -> float:
+    return lib(sd).oracle_xi(seed, idx)
 
 
 def norm1(d, e) -> float:
@@ -197,23 +203,23 @@ def norm1(d, e) -> float:
     return lib().oracle_norm1(d.size, _ptr(d), _ptr(e))
 
 
-def split(d, e) -> np.ndarray:
+def split(d, e, *, sd: bool = False) -> np.ndarray:
     d, e = _f64(d), _f64(e)
     st = np.zeros(d.size + 1, np.int32)
-    nb = lib().oracle_split(d.size, _ptr(d), _ptr(e), _ptr(st))
+    nb = lib(sd).oracle_split(d.size, _ptr(d), _ptr(e), _ptr(st))
     return st[:nb + 1].copy()
 
 
-def gershgorin(d, e):
+def gershgorin(d, e, *, sd: bool = False):
     d, e = _f64(d), _f64(e)
     gl, gu, t = C.c_double(), C.c_double(), C.c_double()
-    lib().oracle_gershgorin(d.size, _ptr(d), _ptr(e), C.byref(gl), C.byref(gu), C.byref(t))
+    lib(sd).oracle_gershgorin(d.size, _ptr(d), _ptr(e), C.byref(gl), C.byref(gu), C.byref(t))
     return gl.value, gu.value, t.value
 
 
-def negcount_x(dx, dllx, sigma: float) -> int:
+def negcount_x(dx, dllx, sigma: float, *, sd: bool = False) -> int:
     dx, dllx = _f64(dx), _f64(dllx)
-    return lib().oracle_negcount_x(dx.size, _ptr(dx), _ptr(dllx), sigma)
+    return lib(sd).oracle_negcount_x(dx.size, _ptr(dx), _ptr(dllx), sigma)
 
 
 def negcount_x_many(dx, dllx, sigmas) -> np.ndarray:
@@ -229,10 +235,10 @@ def negcount_t(d, e, sigma: float, mu: float = 0.0) -> int:
     return lib().oracle_negcount_t_q(d.size, _ptr(d), _ptr(e), mu, sigma)
 
 
-def bisect_x(dx, dllx, j: int, lo: float, hi: float, rtol: float):
+def bisect_x(dx, dllx, j: int, lo: float, hi: float, rtol: float, *, sd: bool = False):
     dx, dllx = _f64(dx), _f64(dllx)
     a, b = C.c_double(lo), C.c_double(hi)
-    lib().oracle_bisect_x(dx.size, _ptr(dx), _ptr(dllx), j, rtol, C.byref(a), C.byref(b))
+    lib(sd).oracle_bisect_x(dx.size, _ptr(dx), _ptr(dllx), j, rtol, C.byref(a), C.byref(b))
     return a.value, b.value
 
 
@@ -258,38 +264,38 @@ def root_x(d, e, left: bool = True):
     return dict(rc=rc, mu=mu.value, d=dx, l=lx[:n - 1].copy(), gl=gl.value, gu=gu.value, backoffs=bo.value)
 
 
-def root_y(d, e, left: bool = True, seed: int = 0, s: int = 0, nb: int | None = None):
+def root_y(d, e, left: bool = True, seed: int = 0, s: int = 0, nb: int | None = None, *, sd: bool = False):
     d, e = _f64(d), _f64(e)
     n = d.size
     nb = n - s if nb is None else nb
     mu = C.c_double()
     arrs = [np.zeros(nb) for _ in range(6)]
-    rc = lib().oracle_root_y(n, _ptr(d), _ptr(e), s, nb, int(left), seed, C.byref(mu), *[_ptr(a) for a in arrs])
+    rc = lib(sd).oracle_root_y(n, _ptr(d), _ptr(e), s, nb, int(left), seed, C.byref(mu), *[_ptr(a) for a in arrs])
     dh, dl, lh, ll, dx, dllx = arrs
     return dict(rc=rc, mu=mu.value, d_hi=dh, d_lo=dl, l_hi=lh, l_lo=ll, dx=dx, dllx=dllx)
 
 
-def dstqds(d, l, tau: float):
+def dstqds(d, l, tau: float, *, sd: bool = False):
     d, l = _f64(d), _f64(l)
     n = d.size
     lpad = np.zeros(n)
     lpad[:n - 1] = l
     dph, dpl, lph, sh = (np.zeros(n) for _ in range(4))
-    lib().oracle_dstqds(n, _ptr(d), _ptr(lpad), tau, _ptr(dph), _ptr(dpl), _ptr(lph), _ptr(sh))
+    lib(sd).oracle_dstqds(n, _ptr(d), _ptr(lpad), tau, _ptr(dph), _ptr(dpl), _ptr(lph), _ptr(sh))
     return dph, lph[:n - 1], sh
 
 
-def dqds(d, l, tau: float):
+def dqds(d, l, tau: float, *, sd: bool = False):
     d, l = _f64(d), _f64(l)
     n = d.size
     lpad = np.zeros(n)
     lpad[:n - 1] = l
     om, um, p = (np.zeros(n) for _ in range(3))
-    lib().oracle_dqds(n, _ptr(d), _ptr(lpad), tau, _ptr(om), _ptr(um), _ptr(p))
+    lib(sd).oracle_dqds(n, _ptr(d), _ptr(lpad), tau, _ptr(om), _ptr(um), _ptr(p))
     return om, um[:n - 1], p
 
 
-def getvec(d, l, lam_hi: float, lam_lo: float = 0.0, r: int = 0):
+def getvec(d, l, lam_hi: float, lam_lo: float = 0.0, r: int = 0, *, sd: bool = False):
     d, l = _f64(d), _f64(l)
     n = d.size
     lpad = np.zeros(n)
@@ -298,7 +304,7 @@ def getvec(d, l, lam_hi: float, lam_lo: float = 0.0, r: int = 0):
     rr = C.c_int64(r)
     g, zz = C.c_double(), C.c_double()
     c = C.c_int64()
-    lib().oracle_getvec(n, _ptr(d), _ptr(lpad), lam_hi, lam_lo, C.byref(rr), _ptr(z), C.byref(g), C.byref(zz),
+    lib(sd).oracle_getvec(n, _ptr(d), _ptr(lpad), lam_hi, lam_lo, C.byref(rr), _ptr(z), C.byref(g), C.byref(zz),
                         C.byref(c))
     return dict(z=z, gamma=g.value, zz=zz.value, r=rr.value, c=c.value)
 
@@ -369,26 +375,26 @@ def bracket_x(dx, dllx, j: int, lo: float, hi: float):
     return a.value, b.value, fixes
 
 
-def bracket_y(d, l, j: int, lo: float, hi: float):
+def bracket_y(d, l, j: int, lo: float, hi: float, *, sd: bool = False):
     d, lp = _lpad(d, l)
     a, b = C.c_double(lo), C.c_double(hi)
-    fixes = lib().oracle_bracket_y(d.size, _ptr(d), _ptr(lp), j, C.byref(a), C.byref(b))
+    fixes = lib(sd).oracle_bracket_y(d.size, _ptr(d), _ptr(lp), j, C.byref(a), C.byref(b))
     return a.value, b.value, fixes
 
 
-def bisect_y_full(d, l, j: int, lo: float, hi: float):
+def bisect_y_full(d, l, j: int, lo: float, hi: float, *, sd: bool = False):
     d, lp = _lpad(d, l)
     a, b = C.c_double(), C.c_double()
-    lib().oracle_bisect_y_full(d.size, _ptr(d), _ptr(lp), j, lo, hi, C.byref(a), C.byref(b))
+    lib(sd).oracle_bisect_y_full(d.size, _ptr(d), _ptr(lp), j, lo, hi, C.byref(a), C.byref(b))
     return a.value, b.value
 
 
-def rqi(d, l, j: int, lo: float, hi: float, gap: float):
+def rqi(d, l, j: int, lo: float, hi: float, gap: float, *, sd: bool = False):
     d, lp = _lpad(d, l)
     W = C.c_double()
     z = np.zeros(d.size)
     it, fb = C.c_int64(), C.c_int64()
-    lib().oracle_rqi(d.size, _ptr(d), _ptr(lp), j, lo, hi, gap, C.byref(W), _ptr(z), C.byref(it), C.byref(fb))
+    lib(sd).oracle_rqi(d.size, _ptr(d), _ptr(lp), j, lo, hi, gap, C.byref(W), _ptr(z), C.byref(it), C.byref(fb))
     return dict(W=W.value, z=z, iters=it.value, fallbacks=fb.value)
 
 

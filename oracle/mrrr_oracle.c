@@ -13,6 +13,10 @@
  *   y-arithmetic = IEEE binary128 (__float128, libquadmath)
  *   (double/quadruple realisation; Table tab:precisions P:5552-5571)
  *
+ * Built a second time with -DORACLE_SD (liboracle_sd.so): the single/double
+ * realisation, y-arithmetic = binary64, epsilon_x = 2^-24,
+ * gaptol 1e-5 -- the same steps with the constants of the #ifdef block below.
+ *
  * Every function cites the passage it follows as P:<line> and the
  * DESIGN.md reading (A-<n>) where the paper is silent or garbled.
  *
@@ -28,17 +32,52 @@
 #include <stdlib.h>
 #include <string.h>
 
-typedef __float128 qreal;
+typedef __float128 qreal;  /* binary128: the test tools below (residuals, Jacobi), both realisations */
 
+#ifdef ORACLE_SD
+/* Single/double realisation: binary32 input and output, ALL computations in      */
+/* binary64 ("we carry out all computations in the former"), gaptol fixed to 1e-5.       */
+/* Compiled from this same file with -DORACLE_SD into liboracle_sd.so; DESIGN.md "Single/double" lists the    */
+/* reading of every constant below.                                                                              */
+typedef double yreal;
+#define EPS_X 0x1p-24          /* epsilon_x = epsilon_s: the binary32 output precision, Table tab:precisions */
+#define EPS_Y 0x1p-53          /* y = binary64 */
+#define XI_SCALE 0x1p-24       /* perturbation xi = eps_x: |xi| <= 2^-25 */
+#define KELG_RATIO 0x1p29      /* eps_x / eps_y of eq:newkelgbound P:6052-6056 */
+#define Y_FULLREL 0x1p-50      /* "full accuracy" of the bisection fallback in binary64 (a few ulps, A-14) */
+#define DEFAULT_GAPTOL 1e-5
+#define YFABS fabs
+#define YFINITE isfinite
+#define YFMAX fmax
+#define YISINF isinf
+#define YISNAN isnan
+#define YSQRT sqrt
+#define YSIGNBIT signbit
+#else
+typedef __float128 yreal;      /* double/quadruple realisation */
 #define EPS_X 0x1p-53          /* epsilon_x, Table tab:precisions P:5559 */
 #define EPS_Y 0x1p-104         /* conservative y unit roundoff for thresholds (A-14) */
+#define XI_SCALE 0x1p-53       /* |xi| <= 2^-54 = eps_x / 2 (A-9) */
+#define KELG_RATIO 0x1p51      /* eps_x / eps_y of eq:newkelgbound P:6052-6056 (A-35) */
+#define Y_FULLREL 0x1p-98Q     /* a few eps_y (A-14) */
+#define DEFAULT_GAPTOL 1e-10   /* P:6277 */
+#define YFABS fabsq
+#define YFINITE finiteq
+#define YFMAX fmaxq
+#define YISINF isinfq
+#define YISNAN isnanq
+#define YSQRT sqrtq
+#define YSIGNBIT signbitq
+#endif
+/* the arithmetic of the eigenvalue approximations (x-bisection, intervals, shifts) is binary64 in both     */
+/* realisations: Gershgorin inflation, interval inflation nu and the shift offsets scale with its epsilon    */
+#define EPS_A 0x1p-53
 #define ATOL (2.0 * DBL_MIN)   /* atol = 2 omega */
 #define RTOL_Y 0x1p-50         /* "full accuracy" of cluster ends in y (A-12) */
 #define GROWTH 64.0            /* element growth threshold (A-11), relaxed by eq:newkelgbound (A-35) */
 #define MAX_ATTEMPTS 6         /* shift attempts (A-11) */
 #define MAX_RQI 10             /* RQI cap (A-14) */
 #define MAXD 8                 /* representation tree depth cap */
-#define DEFAULT_GAPTOL 1e-10   /* P:6277 */
 #define DEFAULT_SEED 0x4D52525233ULL
 
 enum {
@@ -48,7 +87,7 @@ enum {
 };
 
 typedef struct {
-  double gaptol;      /* <= 0 -> 1e-10 */
+  double gaptol;      /* <= 0 -> DEFAULT_GAPTOL (1e-10; single/double 1e-5) */
   uint64_t seed;      /* perturbation key, 0 -> DEFAULT_SEED */
   int32_t root_side;  /* 0 auto (S3 rule), 1 left, 2 right */
   int32_t threads;    /* 0 -> OpenMP default */
@@ -80,13 +119,14 @@ static void stat_max(int i, int64_t v) {
 
 /* SignBit(d) of Alg. negcountLDL remark (2), P:7159-7161 (A-6); a NaN counts 0. */
 static inline int sbx(double x) { return signbit(x) && !isnan(x); }
+static inline int sby(yreal x) { return YSIGNBIT(x) && !YISNAN(x); }
 static inline int sbq(qreal x) { return signbitq(x) && !isnanq(x); }
 static inline double dmax(double a, double b) { return (b > a) ? b : a; }
 static inline double dmin(double a, double b) { return (b < a) ? b : a; }
 
 /* ------------------------------------------------------------------------- */
 /* Perturbation PRNG: counter-based SplitMix64 (A-9; "any (fixed) sequence of  */
-/* pseudo-random numbers").  xi in [-2^-54, 2^-54).              */
+/* pseudo-random numbers").  xi in [-XI_SCALE/2, XI_SCALE/2).     */
 /* ------------------------------------------------------------------------- */
 double oracle_xi(uint64_t seed, uint64_t idx) {
   uint64_t z = seed + (idx + 1) * 0x9E3779B97F4A7C15ULL;
@@ -94,7 +134,7 @@ double oracle_xi(uint64_t seed, uint64_t idx) {
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
   z ^= z >> 31;
   double u = (double)(z >> 11) * 0x1p-53;
-  return (u - 0.5) * 0x1p-53;
+  return (u - 0.5) * XI_SCALE;
 }
 
 /* ------------------------------------------------------------------------- */
@@ -135,7 +175,7 @@ void oracle_gershgorin(int64_t nb, const double *a, const double *b, double *gl_
   gl = dmin(gl, a[nb - 1] - fabs(b[nb - 2]));
   gu = dmax(gu, a[nb - 1] + fabs(b[nb - 2]));
   double bnorm = dmax(fabs(gl), fabs(gu));
-  double t = ((double)(2 * nb + 10) * bnorm) * EPS_X;
+  double t = ((double)(2 * nb + 10) * bnorm) * EPS_A;
   *gl_out = gl - t;
   *gu_out = gu + t;
   if (t_out) *t_out = t;
@@ -161,18 +201,18 @@ int64_t oracle_negcount_x(int64_t nb, const double *d, const double *dll, double
 }
 
 /* the same count in y-arithmetic (binary128) */
-static int64_t negcount_q(int64_t nb, const qreal *d, const qreal *dll, qreal sigma) {
+static int64_t negcount_q(int64_t nb, const yreal *d, const yreal *dll, yreal sigma) {
   int64_t count = 0;
-  qreal s = -sigma, dp, q;
+  yreal s = -sigma, dp, q;
   for (int64_t i = 0; i < nb - 1; i++) {
     dp = d[i] + s;
-    if (isinfq(s) && isinfq(dp)) q = 1;
+    if (YISINF(s) && YISINF(dp)) q = 1;
     else q = s / dp;
     s = q * dll[i] - sigma;
-    count += sbq(dp);
+    count += sby(dp);
   }
   dp = d[nb - 1] + s;
-  count += sbq(dp);
+  count += sby(dp);
   return count;
 }
 
@@ -222,14 +262,14 @@ void oracle_bisect_x(int64_t nb, const double *d, const double *dll, int64_t j, 
   *phi = wu;
 }
 
-static void bisect_y_fp64pts(int64_t nb, const qreal *d, const qreal *dll, int64_t j, double rtol,
+static void bisect_y_fp64pts(int64_t nb, const yreal *d, const yreal *dll, int64_t j, double rtol,
                              double *plo, double *phi) {
   double wl = *plo, wu = *phi;
   int64_t ev = 0;
   while (bis_continue(wl, wu, rtol)) {
     double w = wl + (wu - wl) / 2;
     ev++;
-    if (negcount_q(nb, d, dll, (qreal)w) < j) wl = w;
+    if (negcount_q(nb, d, dll, (yreal)w) < j) wl = w;
     else wu = w;
   }
   STAT_ADD(ST_NEGY, ev);
@@ -265,11 +305,11 @@ static void bracket_x(int64_t nb, const double *d, const double *dll, int64_t j,
   *phi = hi;
 }
 
-static void bracket_y(int64_t nb, const qreal *d, const qreal *dll, int64_t j, double *plo, double *phi) {
+static void bracket_y(int64_t nb, const yreal *d, const yreal *dll, int64_t j, double *plo, double *phi) {
   double lo = *plo, hi = *phi;
   int64_t fix = 0;
-  for (int it = 0; it < 64 && negcount_q(nb, d, dll, (qreal)lo) >= j; it++) { lo = lo - (hi - lo); fix++; }
-  for (int it = 0; it < 64 && negcount_q(nb, d, dll, (qreal)hi) < j; it++) { hi = hi + (hi - lo); fix++; }
+  for (int it = 0; it < 64 && negcount_q(nb, d, dll, (yreal)lo) >= j; it++) { lo = lo - (hi - lo); fix++; }
+  for (int it = 0; it < 64 && negcount_q(nb, d, dll, (yreal)hi) < j; it++) { hi = hi + (hi - lo); fix++; }
   STAT_ADD(ST_NEGY, 2 + 2 * fix);
   if (fix) STAT_ADD(ST_BRACKET_FIX, fix);
   *plo = lo;
@@ -286,13 +326,13 @@ int oracle_is_boundary(double lo1, double hi1, double lo2, double hi2, double ga
 /* ------------------------------------------------------------------------- */
 /* Alg. dstqds P:3324-3351 and Alg. dqds P:3366-3393 (A-1, A-2 readings) in y */
 /* ------------------------------------------------------------------------- */
-static void dstqds_q(int64_t nb, const qreal *d, const qreal *dl, const qreal *dll, qreal tau,
-                     qreal *dplus, qreal *lplus, qreal *s_out) {
-  qreal s = -tau, q;
+static void dstqds_q(int64_t nb, const yreal *d, const yreal *dl, const yreal *dll, yreal tau,
+                     yreal *dplus, yreal *lplus, yreal *s_out) {
+  yreal s = -tau, q;
   for (int64_t i = 0; i < nb - 1; i++) {
     if (s_out) s_out[i] = s;
     dplus[i] = s + d[i];
-    if (isinfq(s) && isinfq(dplus[i])) q = 1;
+    if (YISINF(s) && YISINF(dplus[i])) q = 1;
     else q = s / dplus[i];
     lplus[i] = dl[i] / dplus[i];
     s = q * dll[i] - tau;
@@ -301,13 +341,13 @@ static void dstqds_q(int64_t nb, const qreal *d, const qreal *dl, const qreal *d
   dplus[nb - 1] = s + d[nb - 1];
 }
 
-static void dqds_q(int64_t nb, const qreal *d, const qreal *dl, const qreal *dll, qreal tau,
-                   qreal *omega, qreal *uminus, qreal *p_out) {
-  qreal p = d[nb - 1] - tau, q;
+static void dqds_q(int64_t nb, const yreal *d, const yreal *dl, const yreal *dll, yreal tau,
+                   yreal *omega, yreal *uminus, yreal *p_out) {
+  yreal p = d[nb - 1] - tau, q;
   if (p_out) p_out[nb - 1] = p;
   for (int64_t i = nb - 2; i >= 0; i--) {
     omega[i + 1] = p + dll[i];                       /* A-1: omega^-(i+1) */
-    if (isinfq(p) && isinfq(omega[i + 1])) q = 1;    /* A-2 guard */
+    if (YISINF(p) && YISINF(omega[i + 1])) q = 1;    /* A-2 guard */
     else q = p / omega[i + 1];
     uminus[i] = dl[i] / omega[i + 1];
     p = q * d[i] - tau;
@@ -321,9 +361,9 @@ static void dqds_q(int64_t nb, const qreal *d, const qreal *dl, const qreal *dll
 /* ------------------------------------------------------------------------- */
 typedef struct {
   int64_t nb;
-  qreal *d, *l, *dl, *dll;   /* M_y: N-representation + cached dl, dll */
+  yreal *d, *l, *dl, *dll;   /* M_y: N-representation + cached dl, dll */
   double *dx, *dllx;         /* M_x = fl64(M_y) copy for x-bisection */
-  qreal sigma;               /* accumulated shift: lambda[T] = lambda[M] + sigma */
+  yreal sigma;               /* accumulated shift: lambda[T] = lambda[M] + sigma */
   double spdiam;             /* spdiam[M_root] = gu - gl of the block */
   int depth;
 } rep_t;
@@ -331,10 +371,10 @@ typedef struct {
 static rep_t *rep_alloc(int64_t nb) {
   rep_t *r = calloc(1, sizeof(rep_t));
   r->nb = nb;
-  r->d = malloc(sizeof(qreal) * nb);
-  r->l = malloc(sizeof(qreal) * nb);
-  r->dl = malloc(sizeof(qreal) * nb);
-  r->dll = malloc(sizeof(qreal) * nb);
+  r->d = malloc(sizeof(yreal) * nb);
+  r->l = malloc(sizeof(yreal) * nb);
+  r->dl = malloc(sizeof(yreal) * nb);
+  r->dll = malloc(sizeof(yreal) * nb);
   r->dx = malloc(sizeof(double) * nb);
   r->dllx = malloc(sizeof(double) * nb);
   return r;
@@ -410,16 +450,16 @@ static rep_t *make_root(int64_t n, int64_t s, int64_t nb, const double *d, const
   if (backoffs) STAT_ADD(ST_ROOT_BACKOFF, backoffs);
   for (int64_t i = 0; i < nb; i++) {
     double x = r->dx[i];
-    r->d[i] = (qreal)x + (qreal)(x * oracle_xi(seed, (uint64_t)(s + i)));
+    r->d[i] = (yreal)x + (yreal)(x * oracle_xi(seed, (uint64_t)(s + i)));
   }
   for (int64_t i = 0; i < nb - 1; i++) {
     double x = lx[i];
-    r->l[i] = (qreal)x + (qreal)(x * oracle_xi(seed, (uint64_t)(n + s + i)));
+    r->l[i] = (yreal)x + (yreal)(x * oracle_xi(seed, (uint64_t)(n + s + i)));
   }
   r->l[nb - 1] = 0;
-  rep_derive(r);   /* recomputes dx = fl64(d_y) == d_x exactly (|xi| < 2^-54) */
+  rep_derive(r);   /* dx = fl64(d_y): == d_x exactly for |xi| < 2^-54; single/double: dx = d_y */
   free(lx);
-  r->sigma = (qreal)(*mu_out);
+  r->sigma = (yreal)(*mu_out);
   r->spdiam = *gu_out - *gl_out;
   r->depth = 0;
   return r;
@@ -432,35 +472,35 @@ static rep_t *make_root(int64_t n, int64_t s, int64_t nb, const double *d, const
 /* r_io > 0 (1-based, fixed after iteration 1): only the twisted  */
 /* factorization with index r; c = inertia of Delta_r.                         */
 /* ------------------------------------------------------------------------- */
-typedef struct { qreal *dp, *lp, *sv, *om, *um, *gam, *z; } gv_ws;
+typedef struct { yreal *dp, *lp, *sv, *om, *um, *gam, *z; } gv_ws;
 
 static void gv_alloc(gv_ws *w, int64_t nb) {
-  w->dp = malloc(sizeof(qreal) * nb); w->lp = malloc(sizeof(qreal) * nb);
-  w->sv = malloc(sizeof(qreal) * nb); w->om = malloc(sizeof(qreal) * nb);
-  w->um = malloc(sizeof(qreal) * nb); w->gam = malloc(sizeof(qreal) * nb);
-  w->z = malloc(sizeof(qreal) * nb);
+  w->dp = malloc(sizeof(yreal) * nb); w->lp = malloc(sizeof(yreal) * nb);
+  w->sv = malloc(sizeof(yreal) * nb); w->om = malloc(sizeof(yreal) * nb);
+  w->um = malloc(sizeof(yreal) * nb); w->gam = malloc(sizeof(yreal) * nb);
+  w->z = malloc(sizeof(yreal) * nb);
 }
 static void gv_free(gv_ws *w) {
   free(w->dp); free(w->lp); free(w->sv); free(w->om); free(w->um); free(w->gam); free(w->z);
 }
 
-static void getvec_q(const rep_t *M, qreal lam, int64_t *r_io, gv_ws *w, qreal *gamma_out, qreal *zz_out,
+static void getvec_q(const rep_t *M, yreal lam, int64_t *r_io, gv_ws *w, yreal *gamma_out, yreal *zz_out,
                      int64_t *c_out) {
   const int64_t nb = M->nb;
-  const qreal *d = M->d, *dl = M->dl, *dll = M->dll;
-  qreal *dp = w->dp, *lp = w->lp, *om = w->om, *um = w->um, *z = w->z;
+  const yreal *d = M->d, *dl = M->dl, *dll = M->dll;
+  yreal *dp = w->dp, *lp = w->lp, *om = w->om, *um = w->um, *z = w->z;
   int64_t r, c = 0;
-  qreal gamma;
+  yreal gamma;
   STAT_ADD(ST_GETVEC, 1);
   if (*r_io == 0) {
     dstqds_q(nb, d, dl, dll, lam, dp, lp, w->sv);
-    for (int64_t i = 0; i < nb; i++) c += sbq(dp[i]);
+    for (int64_t i = 0; i < nb; i++) c += sby(dp[i]);
     /* dqds with gamma_k = s(k) + d(k)/omega(k+1) * p(k+1) folded in */
-    qreal p = d[nb - 1] - lam, q;
+    yreal p = d[nb - 1] - lam, q;
     w->gam[nb - 1] = w->sv[nb - 1] + d[nb - 1];
     for (int64_t i = nb - 2; i >= 0; i--) {
       om[i + 1] = p + dll[i];
-      if (isinfq(p) && isinfq(om[i + 1])) q = 1;
+      if (YISINF(p) && YISINF(om[i + 1])) q = 1;
       else q = p / om[i + 1];
       um[i] = dl[i] / om[i + 1];
       w->gam[i] = w->sv[i] + (d[i] / om[i + 1]) * p;
@@ -468,10 +508,10 @@ static void getvec_q(const rep_t *M, qreal lam, int64_t *r_io, gv_ws *w, qreal *
     }
     om[0] = p;
     r = -1;
-    qreal best = 0;
+    yreal best = 0;
     for (int64_t k = 0; k < nb; k++) {
-      if (isnanq(w->gam[k])) continue;
-      qreal ag = fabsq(w->gam[k]);
+      if (YISNAN(w->gam[k])) continue;
+      yreal ag = YFABS(w->gam[k]);
       if (r < 0 || ag < best) { r = k; best = ag; }
     }
     if (r < 0) { *r_io = 0; *gamma_out = NAN; *zz_out = NAN; *c_out = c; return; }
@@ -479,31 +519,31 @@ static void getvec_q(const rep_t *M, qreal lam, int64_t *r_io, gv_ws *w, qreal *
     *r_io = r + 1;
   } else {
     r = *r_io - 1;
-    qreal s = -lam, q;
+    yreal s = -lam, q;
     for (int64_t i = 0; i < r; i++) {
       dp[i] = s + d[i];
-      if (isinfq(s) && isinfq(dp[i])) q = 1;
+      if (YISINF(s) && YISINF(dp[i])) q = 1;
       else q = s / dp[i];
       lp[i] = dl[i] / dp[i];
       s = q * dll[i] - lam;
-      c += sbq(dp[i]);
+      c += sby(dp[i]);
     }
     if (r == nb - 1) {
       gamma = s + d[nb - 1];
     } else {
-      qreal p = d[nb - 1] - lam;
+      yreal p = d[nb - 1] - lam;
       gamma = 0;
       for (int64_t i = nb - 2; i >= r; i--) {
         om[i + 1] = p + dll[i];
-        if (isinfq(p) && isinfq(om[i + 1])) q = 1;
+        if (YISINF(p) && YISINF(om[i + 1])) q = 1;
         else q = p / om[i + 1];
         um[i] = dl[i] / om[i + 1];
         if (i == r) gamma = s + (d[r] / om[r + 1]) * p;
         p = q * d[i] - lam;
-        c += sbq(om[i + 1]);
+        c += sby(om[i + 1]);
       }
     }
-    c += sbq(gamma);
+    c += sby(gamma);
   }
   /* solve N_r^T z = e_r with zero-pivot substitution;          */
   /* DESIGN.md reading A-25: immediate neighbours first, undefined refs := 0 */
@@ -515,21 +555,21 @@ static void getvec_q(const rep_t *M, qreal lam, int64_t *r_io, gv_ws *w, qreal *
     if (dp[i] != 0) z[i] = -lp[i] * z[i + 1];
     else {
       STAT_ADD(ST_ZPIV, 1);
-      qreal num = (i + 1 < nb - 1) ? dl[i + 1] : 0, zz2 = (i + 2 < nb) ? z[i + 2] : 0;
-      qreal v = -(num / dl[i]) * zz2;
-      z[i] = finiteq(v) ? v : 0;
+      yreal num = (i + 1 < nb - 1) ? dl[i + 1] : 0, zz2 = (i + 2 < nb) ? z[i + 2] : 0;
+      yreal v = -(num / dl[i]) * zz2;
+      z[i] = YFINITE(v) ? v : 0;
     }
   }
   for (int64_t i = r; i < nb - 1; i++) {
     if (om[i + 1] != 0) z[i + 1] = -um[i] * z[i];
     else {
       STAT_ADD(ST_ZPIV, 1);
-      qreal num = (i >= 1) ? dl[i - 1] : 0, zm = (i >= 1) ? z[i - 1] : 0;
-      qreal v = -(num / dl[i]) * zm;
-      z[i + 1] = finiteq(v) ? v : 0;
+      yreal num = (i >= 1) ? dl[i - 1] : 0, zm = (i >= 1) ? z[i - 1] : 0;
+      yreal v = -(num / dl[i]) * zm;
+      z[i + 1] = YFINITE(v) ? v : 0;
     }
   }
-  qreal zz = 0;
+  yreal zz = 0;
   for (int64_t i = 0; i < nb; i++) zz += z[i] * z[i];
   *gamma_out = gamma;
   *zz_out = zz;
@@ -539,11 +579,11 @@ static void getvec_q(const rep_t *M, qreal lam, int64_t *r_io, gv_ws *w, qreal *
 /* y-bisection to full accuracy (fallback of RQI): Alg. Bisection P:3077-3111 on the  */
 /* y-representation with y-arithmetic counts, stopping at relative width 2^-98 of |lambda| (a few eps_y,    */
 /* A-14) or at atol = 2 omega.  Pinned: tests/test_oracle_branches.py (binary128 Jacobi).     */
-static qreal bisect_y_full(const rep_t *M, int64_t j, qreal lo, qreal hi) {
+static yreal bisect_y_full(const rep_t *M, int64_t j, yreal lo, yreal hi) {
   for (int it = 0; it < 400; it++) {
-    qreal m = fmaxq(fabsq(lo), fabsq(hi));
-    if (!(hi - lo > fmaxq(0x1p-98Q * m, (qreal)ATOL))) break;
-    qreal w = lo + (hi - lo) / 2;
+    yreal m = YFMAX(YFABS(lo), YFABS(hi));
+    if (!(hi - lo > YFMAX(Y_FULLREL * m, (yreal)ATOL))) break;
+    yreal w = lo + (hi - lo) / 2;
     STAT_ADD(ST_NEGY, 1);
     if (negcount_q(M->nb, M->d, M->dll, w) < j) lo = w;
     else hi = w;
@@ -558,23 +598,23 @@ static void rqi_singleton(const rep_t *M, int64_t j, double lo, double hi, doubl
                           double *zcol, gv_ws *w) {
   const int64_t nb = M->nb;
   double mid = lo + (hi - lo) / 2;
-  double nu = (100.0 * (double)nb) * EPS_X;
-  qreal blo = (qreal)(lo - nu * fabs(lo)), bhi = (qreal)(hi + nu * fabs(hi));
-  qreal lam = (qreal)mid, gamma, zz;
+  double nu = (100.0 * (double)nb) * EPS_A;
+  yreal blo = (yreal)(lo - nu * fabs(lo)), bhi = (yreal)(hi + nu * fabs(hi));
+  yreal lam = (yreal)mid, gamma, zz;
   double thr1 = (gap * EPS_X) * sqrt((double)nb);
   int64_t r = 0, c, iters = 0;
   int accepted = 0;
   for (int it = 0; it < MAX_RQI && !accepted; it++) {
     getvec_q(M, lam, &r, w, &gamma, &zz, &c);
     iters++;
-    if (r == 0 || !finiteq(zz) || zz == 0) break;
-    qreal nz = sqrtq(zz);
-    qreal resid = fabsq(gamma) / nz, rqc = gamma / zz;
+    if (r == 0 || !YFINITE(zz) || zz == 0) break;
+    yreal nz = YSQRT(zz);
+    yreal resid = YFABS(gamma) / nz, rqc = gamma / zz;
     /* stopping tests of Alg. stask: ||r|| <= tol1 (mixed: k_rs gap eps_x sqrt(n)) */
     /* or |RQC| < tol2 |lam| with tol2 = 4 eps_y (A-14)                                                        */
-    if ((double)resid <= thr1 || fabsq(rqc) < 4 * EPS_Y * fabsq(lam)) { accepted = 1; break; }
+    if ((double)resid <= thr1 || YFABS(rqc) < 4 * EPS_Y * YFABS(lam)) { accepted = 1; break; }
     if (c < j) blo = lam; else bhi = lam;
-    qreal nl = lam + rqc;
+    yreal nl = lam + rqc;
     int ok = ((c < j) ? (rqc > 0) : (rqc < 0)) && (blo < nl) && (nl < bhi);
     if (ok) lam = nl;
     else break;
@@ -585,7 +625,7 @@ static void rqi_singleton(const rep_t *M, int64_t j, double lo, double hi, doubl
     lam = bisect_y_full(M, j, blo, bhi);
     getvec_q(M, lam, &r, w, &gamma, &zz, &c);
   }
-  qreal nz = sqrtq(zz);
+  yreal nz = YSQRT(zz);
   *W_out = (double)(lam + M->sigma);
   for (int64_t i = 0; i < nb; i++) zcol[i] = (double)(w->z[i] / nz);
 }
@@ -651,7 +691,7 @@ static void do_cluster(const ctx_t *cx, const rep_t *M, const double *lo, const 
   const int64_t nb = M->nb;
   STAT_ADD(ST_NCLUSTERS, 1);
   stat_max(ST_LARGEST, q - p + 1);
-  double nu = (100.0 * (double)nb) * EPS_X;
+  double nu = (100.0 * (double)nb) * EPS_A;
   /* (a) refine the extremal eigenvalues of M_y (y-arithmetic) */
   double Lp = lo[p] - nu * fabs(lo[p]), Hp = hi[p] + nu * fabs(hi[p]);
   double Lq = lo[q] - nu * fabs(lo[q]), Hq = hi[q] + nu * fabs(hi[q]);
@@ -662,26 +702,26 @@ static void do_cluster(const ctx_t *cx, const rep_t *M, const double *lo, const 
   bisect_y_fp64pts(nb, M->d, M->dll, p, RTOL_Y, &Lp, &Hp);
   bisect_y_fp64pts(nb, M->d, M->dll, q, RTOL_Y, &Lq, &Hq);
   /* (b) tau_l = lam_p_low - 100 eps |.|, tau_r = lam_q_up + 100 eps |.| */
-  double offl = (100.0 * EPS_X) * fabs(Lp), offr = (100.0 * EPS_X) * fabs(Hq);
+  double offl = (100.0 * EPS_A) * fabs(Lp), offr = (100.0 * EPS_A) * fabs(Hq);
   double taul = Lp - offl, taur = Hq + offr;
   /* (c) attempts */
-  qreal *dpl = malloc(sizeof(qreal) * nb), *lpl = malloc(sizeof(qreal) * nb);
-  qreal *dpr = malloc(sizeof(qreal) * nb), *lpr = malloc(sizeof(qreal) * nb);
-  qreal *bd = malloc(sizeof(qreal) * nb), *bl = malloc(sizeof(qreal) * nb);
+  yreal *dpl = malloc(sizeof(yreal) * nb), *lpl = malloc(sizeof(yreal) * nb);
+  yreal *dpr = malloc(sizeof(yreal) * nb), *lpr = malloc(sizeof(yreal) * nb);
+  yreal *bd = malloc(sizeof(yreal) * nb), *bl = malloc(sizeof(yreal) * nb);
   double best_g = INFINITY, best_tau = 0;
   int have_best = 0, certified = 0;
   /* growth bound of the mixed solver, eq:newkelgbound P:6052-6056 (A-35): k_elg <= max(original, eps_x / (eps_y */
   /* sqrt(n))), with the original bound G = 64 of A-11                                                             */
-  double gthr = dmax(GROWTH, 0x1p51 / sqrt((double)nb)) * M->spdiam;
+  double gthr = dmax(GROWTH, KELG_RATIO / sqrt((double)nb)) * M->spdiam;
   for (int a = 0; a < MAX_ATTEMPTS; a++) {
     STAT_ADD(ST_ATTEMPTS, 1);
-    dstqds_q(nb, M->d, M->dl, M->dll, (qreal)taul, dpl, lpl, NULL);
-    dstqds_q(nb, M->d, M->dl, M->dll, (qreal)taur, dpr, lpr, NULL);
+    dstqds_q(nb, M->d, M->dl, M->dll, (yreal)taul, dpl, lpl, NULL);
+    dstqds_q(nb, M->d, M->dl, M->dll, (yreal)taur, dpr, lpr, NULL);
     int vl = 1, vr = 1;
     double gl = 0, gr = 0;
     for (int64_t i = 0; i < nb; i++) {
-      if (isnanq(dpl[i]) || (i < nb - 1 && isnanq(lpl[i]))) vl = 0;
-      if (isnanq(dpr[i]) || (i < nb - 1 && isnanq(lpr[i]))) vr = 0;
+      if (YISNAN(dpl[i]) || (i < nb - 1 && YISNAN(lpl[i]))) vl = 0;
+      if (YISNAN(dpr[i]) || (i < nb - 1 && YISNAN(lpr[i]))) vr = 0;
       gl = dmax(gl, fabs((double)dpl[i]));
       gr = dmax(gr, fabs((double)dpr[i]));
     }
@@ -693,8 +733,8 @@ static void do_cluster(const ctx_t *cx, const rep_t *M, const double *lo, const 
       double g = (pick == 1) ? gl : gr;
       if (g < best_g) {
         best_g = g; best_tau = (pick == 1) ? taul : taur; have_best = 1;
-        memcpy(bd, (pick == 1) ? dpl : dpr, sizeof(qreal) * nb);
-        memcpy(bl, (pick == 1) ? lpl : lpr, sizeof(qreal) * nb);
+        memcpy(bd, (pick == 1) ? dpl : dpr, sizeof(yreal) * nb);
+        memcpy(bl, (pick == 1) ? lpl : lpr, sizeof(yreal) * nb);
       }
       if (g <= gthr) { certified = 1; break; }
     }
@@ -711,11 +751,11 @@ static void do_cluster(const ctx_t *cx, const rep_t *M, const double *lo, const 
   if (!certified) STAT_ADD(ST_UNCERTIFIED, 1);
   /* (d) child representation M_y, M_x */
   rep_t *C = rep_alloc(nb);
-  memcpy(C->d, bd, sizeof(qreal) * nb);
-  memcpy(C->l, bl, sizeof(qreal) * nb);
+  memcpy(C->d, bd, sizeof(yreal) * nb);
+  memcpy(C->l, bl, sizeof(yreal) * nb);
   free(bd); free(bl);
   rep_derive(C);
-  C->sigma = M->sigma + (qreal)best_tau;
+  C->sigma = M->sigma + (yreal)best_tau;
   C->spdiam = M->spdiam;
   C->depth = M->depth + 1;
   /* (e) child intervals */
@@ -1119,18 +1159,18 @@ void oracle_jacobi_ldl(int64_t n, const double *d, const double *l, double *w_hi
 }
 
 /* -------- unit-level wrappers for pins (y values exchanged as hi/lo pairs) -------- */
-static void q_out(qreal v, double *hi, double *lo) { *hi = (double)v; *lo = (double)(v - (qreal)(*hi)); }
+static void q_out(yreal v, double *hi, double *lo) { *hi = (double)v; *lo = (double)(v - (yreal)(*hi)); }
 
 void oracle_dstqds(int64_t nb, const double *d, const double *l, double tau, double *dp_hi, double *dp_lo,
                    double *lp_hi, double *s_hi) {
-  qreal *D = malloc(sizeof(qreal) * nb), *DL = malloc(sizeof(qreal) * nb), *DLL = malloc(sizeof(qreal) * nb);
-  qreal *dp = malloc(sizeof(qreal) * nb), *lp = malloc(sizeof(qreal) * nb), *s = malloc(sizeof(qreal) * nb);
+  yreal *D = malloc(sizeof(yreal) * nb), *DL = malloc(sizeof(yreal) * nb), *DLL = malloc(sizeof(yreal) * nb);
+  yreal *dp = malloc(sizeof(yreal) * nb), *lp = malloc(sizeof(yreal) * nb), *s = malloc(sizeof(yreal) * nb);
   for (int64_t i = 0; i < nb; i++) {
     D[i] = d[i];
-    DL[i] = (i < nb - 1) ? (qreal)d[i] * (qreal)l[i] : 0;
-    DLL[i] = (i < nb - 1) ? DL[i] * (qreal)l[i] : 0;
+    DL[i] = (i < nb - 1) ? (yreal)d[i] * (yreal)l[i] : 0;
+    DLL[i] = (i < nb - 1) ? DL[i] * (yreal)l[i] : 0;
   }
-  dstqds_q(nb, D, DL, DLL, (qreal)tau, dp, lp, s);
+  dstqds_q(nb, D, DL, DLL, (yreal)tau, dp, lp, s);
   for (int64_t i = 0; i < nb; i++) {
     double dummy;
     q_out(dp[i], &dp_hi[i], dp_lo ? &dp_lo[i] : &dummy);
@@ -1142,14 +1182,14 @@ void oracle_dstqds(int64_t nb, const double *d, const double *l, double tau, dou
 
 void oracle_dqds(int64_t nb, const double *d, const double *l, double tau, double *om_hi, double *um_hi,
                  double *p_hi) {
-  qreal *D = malloc(sizeof(qreal) * nb), *DL = malloc(sizeof(qreal) * nb), *DLL = malloc(sizeof(qreal) * nb);
-  qreal *om = malloc(sizeof(qreal) * nb), *um = malloc(sizeof(qreal) * nb), *p = malloc(sizeof(qreal) * nb);
+  yreal *D = malloc(sizeof(yreal) * nb), *DL = malloc(sizeof(yreal) * nb), *DLL = malloc(sizeof(yreal) * nb);
+  yreal *om = malloc(sizeof(yreal) * nb), *um = malloc(sizeof(yreal) * nb), *p = malloc(sizeof(yreal) * nb);
   for (int64_t i = 0; i < nb; i++) {
     D[i] = d[i];
-    DL[i] = (i < nb - 1) ? (qreal)d[i] * (qreal)l[i] : 0;
-    DLL[i] = (i < nb - 1) ? DL[i] * (qreal)l[i] : 0;
+    DL[i] = (i < nb - 1) ? (yreal)d[i] * (yreal)l[i] : 0;
+    DLL[i] = (i < nb - 1) ? DL[i] * (yreal)l[i] : 0;
   }
-  dqds_q(nb, D, DL, DLL, (qreal)tau, om, um, p);
+  dqds_q(nb, D, DL, DLL, (yreal)tau, om, um, p);
   for (int64_t i = 0; i < nb; i++) {
     om_hi[i] = (double)om[i];
     if (i < nb - 1 && um_hi) um_hi[i] = (double)um[i];
@@ -1162,12 +1202,12 @@ void oracle_dqds(int64_t nb, const double *d, const double *l, double tau, doubl
 void oracle_getvec(int64_t nb, const double *d, const double *l, double lam_hi, double lam_lo, int64_t *r_io,
                    double *z_out, double *gamma_hi, double *zz_hi, int64_t *c_out) {
   rep_t *M = rep_alloc(nb);
-  for (int64_t i = 0; i < nb; i++) { M->d[i] = d[i]; M->l[i] = (i < nb - 1) ? (qreal)l[i] : 0; }
+  for (int64_t i = 0; i < nb; i++) { M->d[i] = d[i]; M->l[i] = (i < nb - 1) ? (yreal)l[i] : 0; }
   rep_derive(M);
   gv_ws w;
   gv_alloc(&w, nb);
-  qreal g, zz;
-  getvec_q(M, (qreal)lam_hi + (qreal)lam_lo, r_io, &w, &g, &zz, c_out);
+  yreal g, zz;
+  getvec_q(M, (yreal)lam_hi + (yreal)lam_lo, r_io, &w, &g, &zz, c_out);
   for (int64_t i = 0; i < nb; i++) z_out[i] = (double)w.z[i];
   *gamma_hi = (double)g;
   *zz_hi = (double)zz;
@@ -1199,7 +1239,7 @@ void oracle_stats_reset(void) { memset(g_stats, 0, sizeof(g_stats)); }
 
 static rep_t *rep_from_fp64(int64_t nb, const double *d, const double *l) {
   rep_t *M = rep_alloc(nb);
-  for (int64_t i = 0; i < nb; i++) { M->d[i] = d[i]; M->l[i] = (i < nb - 1) ? (qreal)l[i] : 0; }
+  for (int64_t i = 0; i < nb; i++) { M->d[i] = d[i]; M->l[i] = (i < nb - 1) ? (yreal)l[i] : 0; }
   rep_derive(M);
   M->sigma = 0;
   M->depth = 0;
@@ -1227,7 +1267,7 @@ int64_t oracle_bracket_y(int64_t nb, const double *d, const double *l, int64_t j
 void oracle_bisect_y_full(int64_t nb, const double *d, const double *l, int64_t j, double lo, double hi,
                           double *lam_hi, double *lam_lo) {
   rep_t *M = rep_from_fp64(nb, d, l);
-  q_out(bisect_y_full(M, j, (qreal)lo, (qreal)hi), lam_hi, lam_lo);
+  q_out(bisect_y_full(M, j, (yreal)lo, (yreal)hi), lam_hi, lam_lo);
   rep_free(M);
 }
 

@@ -60,6 +60,8 @@ def load() -> C.CDLL:
         L.mrrr_init.argtypes = [C.POINTER(vp), C.POINTER(_Opts)]
         L.mrrr_eig.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, i64]
         L.mrrr_eig_host.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, i64]
+        L.mrrr_seig.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, i64]
+        L.mrrr_seig_host.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, i64]
         L.mrrr_eig_shard.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, vp, vp, i64, i64, C.POINTER(i64),
                                       C.POINTER(i64)]
         L.mrrr_get_stats.argtypes = [vp, vp, C.c_int32]
@@ -76,7 +78,8 @@ def load() -> C.CDLL:
         L.mrrr_eig_dist.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, i64, i64, i64, vp, vp, i64, i64,
                                     C.POINTER(i64), C.POINTER(i64)]
         for f in ("mrrr_init", "mrrr_eig", "mrrr_eig_host", "mrrr_eig_shard", "mrrr_get_stats", "mrrr_get_times",
-                  "mrrr_get_diag", "mrrr_destroy", "mrrr_nccl_unique_id", "mrrr_eig_dist"):
+                  "mrrr_get_diag", "mrrr_destroy", "mrrr_nccl_unique_id", "mrrr_eig_dist", "mrrr_seig",
+                  "mrrr_seig_host"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -84,7 +87,7 @@ def load() -> C.CDLL:
 
 EXPORTED = ["mrrr_init", "mrrr_eig", "mrrr_eig_host", "mrrr_eig_shard", "mrrr_get_stats", "mrrr_get_diag",
             "mrrr_get_times", "mrrr_selftest", "mrrr_shard_owner", "mrrr_strerror", "mrrr_destroy",
-            "mrrr_nccl_unique_id", "mrrr_eig_dist"]
+            "mrrr_nccl_unique_id", "mrrr_eig_dist", "mrrr_seig", "mrrr_seig_host"]
 
 
 def nccl_unique_id() -> bytes:
@@ -140,52 +143,66 @@ class Solver:
     def eig(self, d, e, il: int | None = None, iu: int | None = None, W=None, Z=None):
         """Device solve: d, e are float64 CUDA tensors.  Returns (W, Z) with Z of shape (n, k) (a
         column-major view: Z[:, j] is contiguous)."""
+        return self._eig_dev(d, e, il, iu, W, Z, single=False)
+
+    def seig(self, d, e, il: int | None = None, iu: int | None = None, W=None, Z=None):
+        """Single/double realisation (mrrr_seig): d, e float32 CUDA tensors in, float32 (W, Z)
+        out, binary64 inside, gaptol 1e-5."""
+        return self._eig_dev(d, e, il, iu, W, Z, single=True)
+
+    def _eig_dev(self, d, e, il, iu, W, Z, single: bool):
         import torch
+        dt = torch.float32 if single else torch.float64
+        tn = "float32" if single else "float64"
         n = d.numel()
         il = 1 if il is None else int(il)
         iu = n if iu is None else int(iu)
         k = max(iu - il + 1, 0)
-        if not (d.is_cuda and d.dtype == torch.float64 and d.is_contiguous()):
-            raise MrrrError("d must be a contiguous float64 CUDA tensor")
-        if n > 1 and not (e.is_cuda and e.dtype == torch.float64 and e.is_contiguous()):
-            raise MrrrError("e must be a contiguous float64 CUDA tensor")
+        if not (d.is_cuda and d.dtype == dt and d.is_contiguous()):
+            raise MrrrError(f"d must be a contiguous {tn} CUDA tensor")
+        if n > 1 and not (e.is_cuda and e.dtype == dt and e.is_contiguous()):
+            raise MrrrError(f"e must be a contiguous {tn} CUDA tensor")
         if W is None:
-            W = torch.empty(k, dtype=torch.float64, device=d.device)
+            W = torch.empty(k, dtype=dt, device=d.device)
         if Z is None:
-            Zt = torch.empty((k, n), dtype=torch.float64, device=d.device)
+            Zt = torch.empty((k, n), dtype=dt, device=d.device)
         elif Z.dim() == 2 and tuple(Z.shape) == (n, k) and Z.stride() == (1, n):
             Zt = Z.T  # a column-major (n, k) view (e.g. the Z returned by an earlier call)
         elif Z.dim() == 2 and tuple(Z.shape) == (k, n) and Z.is_contiguous():
             Zt = Z    # row j of the (k, n) buffer receives eigenvector j
         else:
             raise MrrrError("Z must be a contiguous (k, n) buffer or a column-major (n, k) view")
-        if not (Zt.is_cuda and Zt.dtype == torch.float64) or (W is not None and W.numel() < k):
-            raise MrrrError("W, Z must be float64 CUDA buffers of k and k x n entries")
+        if not (Zt.is_cuda and Zt.dtype == dt and W.dtype == dt) or W.numel() < k:
+            raise MrrrError(f"W, Z must be {tn} CUDA buffers of k and k x n entries")
         ep = e.data_ptr() if (e is not None and e.numel()) else None
-        rc = load().mrrr_eig(self._h, d.data_ptr(), ep, n, il, iu, W.data_ptr(), Zt.data_ptr(), n)
-        _check(rc, "mrrr_eig")
+        fn = "mrrr_seig" if single else "mrrr_eig"
+        rc = getattr(load(), fn)(self._h, d.data_ptr(), ep, n, il, iu, W.data_ptr(), Zt.data_ptr(), n)
+        _check(rc, fn)
         self._last = (n, k)
         return W, Zt.T
 
     def eig_host(self, d: np.ndarray, e: np.ndarray, il: int | None = None, iu: int | None = None,
-                 W: np.ndarray | None = None, Zt: np.ndarray | None = None):
+                 W: np.ndarray | None = None, Zt: np.ndarray | None = None, single: bool = False):
         """Host solve (copies inside the call): d, e host arrays in, (W, Z[n, k]) host arrays out.  W (k,) and
-        Zt (k, n) may be supplied (e.g. page-locked buffers for full-speed copies)."""
-        d = np.ascontiguousarray(d, dtype=np.float64)
+        Zt (k, n) may be supplied (e.g. page-locked buffers for full-speed copies).  single: the
+        single/double realisation (mrrr_seig_host; float32 arrays in and out)."""
+        dt = np.float32 if single else np.float64
+        d = np.ascontiguousarray(d, dtype=dt)
         n = d.size
-        e = np.ascontiguousarray(e, dtype=np.float64) if n > 1 else np.zeros(1)
+        e = np.ascontiguousarray(e, dtype=dt) if n > 1 else np.zeros(1, dt)
         il = 1 if il is None else int(il)
         iu = n if iu is None else int(iu)
         k = iu - il + 1
         if W is None:
-            W = np.empty(k)
+            W = np.empty(k, dt)
         if Zt is None:
-            Zt = np.empty((k, n))
-        if W.shape != (k,) or Zt.shape != (k, n) or W.dtype != np.float64 or Zt.dtype != np.float64 \
+            Zt = np.empty((k, n), dt)
+        if W.shape != (k,) or Zt.shape != (k, n) or W.dtype != dt or Zt.dtype != dt \
                 or not (W.flags.c_contiguous and Zt.flags.c_contiguous):
-            raise MrrrError("W must be float64 (k,), Zt float64 C-contiguous (k, n)")
-        rc = load().mrrr_eig_host(self._h, d.ctypes.data, e.ctypes.data, n, il, iu, W.ctypes.data, Zt.ctypes.data, n)
-        _check(rc, "mrrr_eig_host")
+            raise MrrrError(f"W must be {dt.__name__} (k,), Zt {dt.__name__} C-contiguous (k, n)")
+        fn = "mrrr_seig_host" if single else "mrrr_eig_host"
+        rc = getattr(load(), fn)(self._h, d.ctypes.data, e.ctypes.data, n, il, iu, W.ctypes.data, Zt.ctypes.data, n)
+        _check(rc, fn)
         self._last = (n, k)
         return W, Zt.T
 

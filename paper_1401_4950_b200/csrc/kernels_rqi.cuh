@@ -600,7 +600,8 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
                                              const YElt *__restrict__ my, const QElt *__restrict__ mq, dd *ws,
                                              long long S, long long nbmax,
                                              double *W, ZMeta *zmeta, int *diag_depth, double *fin_lo,
-                                             double *fin_hi, long long *stats, int fault) {
+                                             double *fin_hi, long long *stats, int fault, int sd, double eps_x,
+                                             double eps_y) {
   // fault (MRRR_FAULT, GPU tests only): bit 0 skips the RQI iterations (every singleton takes the bisection
   // fallback of P:3481-3482), bit 1 sends every Getvec through the careful IEEE pass
   const bool fc = (fault & 2) != 0;
@@ -622,7 +623,7 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
   dd blo = dd_from(__dsub_rn(s.lo, __dmul_rn(nu, fabs(s.lo))));
   dd bhi = dd_from(__dadd_rn(s.hi, __dmul_rn(nu, fabs(s.hi))));
   dd lam = dd_from(mid);
-  double thr1 = __dmul_rn(__dmul_rn(s.gap, EPS_X), sqrt((double)nb));
+  double thr1 = __dmul_rn(__dmul_rn(s.gap, eps_x), sqrt((double)nb));
   int r = -1, iters = 0;
   long long qd = 0, qdg = 0, zs = 0;
   bool accepted = false, lu_valid = false, careful = false;
@@ -647,11 +648,11 @@ __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, i
     dd resid = dd_div(dd_abs(g.gamma), nz);
     dd rqc = dd_div(g.gamma, zz);
     // tol2: |RQC| < 4 eps_y |lam|, not below the representation's y-rounding 2^-100 spdiam (A-30)
-    dd tol2 = dd_mul_d(dd_abs(lam), 4.0 * EPS_Y);
+    dd tol2 = dd_mul_d(dd_abs(lam), 4.0 * eps_y);
     if (dd_lt(tol2, dd_from(__dmul_rn(0x1p-100, R.spdiam)))) tol2 = dd_from(__dmul_rn(0x1p-100, R.spdiam));
     if (resid.hi <= thr1 || dd_lt(dd_abs(rqc), tol2)) { accepted = true; break; }
     if (g.c < j) blo = lam; else bhi = lam;
-    dd nl = dd_add(lam, rqc);
+    dd nl = sd ? dd_from(__dadd_rn(lam.hi, rqc.hi)) : dd_add(lam, rqc);  // sd: lambda kept in binary64
     const bool sgn = (g.c < j) ? (rqc.hi > 0.0) : (rqc.hi < 0.0);
     bool ok = sgn && dd_lt(blo, nl) && dd_lt(nl, bhi);
 #ifdef MRRR_DEBUG_RQI

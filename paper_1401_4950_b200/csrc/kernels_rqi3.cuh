@@ -35,7 +35,7 @@ struct SegRec {
 };
 
 __global__ void k_rqi3_init(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
-                            RqiState *st) {
+                            RqiState *st, double eps_x) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ns) return;
   const Singleton s = sg[i];
@@ -48,7 +48,7 @@ __global__ void k_rqi3_init(const Singleton *__restrict__ sg, int ns, const RepD
   q.blo_lo = 0.0;
   q.bhi_hi = __dadd_rn(s.hi, __dmul_rn(nu, fabs(s.hi)));
   q.bhi_lo = 0.0;
-  q.thr1 = __dmul_rn(__dmul_rn(s.gap, EPS_X), sqrt((double)nb));
+  q.thr1 = __dmul_rn(__dmul_rn(s.gap, eps_x), sqrt((double)nb));  // k_rs gap eps_x sqrt(n)
   q.r = -1;
   q.it = 0;
   q.status = 0;
@@ -357,6 +357,79 @@ __device__ __forceinline__ void seg_pass(const QElt *__restrict__ q, int nb, int
   }
 }
 
+// the same segment in binary64 (single/double realisation): den' = (g - lam) - c2 / den with the
+// IEEE quotients c2/den and dl/den from one reciprocal pair of den (fast range; a pivot outside it flags the
+// segment, as in the dd pass); factors stored with zero low words, partial norms in binary64
+__device__ __forceinline__ double sd_q2(double a, double b, double r1, double r2) {
+  const double q0 = __dmul_rn(a, r1);
+  return __fma_rn(__fma_rn(-b, q0, a), r2, q0);
+}
+template <bool LIGHT>
+__device__ __forceinline__ void seg_pass_sd(const QElt *__restrict__ q, int nb, int isB, int t0, int t1, int tw,
+                                            double lam, dd *P, SegRec *R, double2 *stg) {
+  R->empty = 0;
+  const int rs = isB ? nb - 1 - tw : tw, og = isB ? 6 : 4;  // double offset of g in a QElt row
+  double den = __dsub_rn(__ldg(&q[rs].gb_hi), lam);
+  bool ok = true;
+  for (int t = tw; t < t0; t++) {
+    const double *pq = reinterpret_cast<const double *>(q + seg_row(isB, nb, t));
+    const double c2 = __ldg(pq), gg = __ldg(pq + og);
+    double r1, r2;
+    ok &= rcp_nr2(den, r1, r2);
+    den = __dsub_rn(__dsub_rn(gg, lam), sd_q2(c2, den, r1, r2));
+  }
+  const double din = den;
+  double Pq = 0.0, A = 1.0, Bs = 0.0;
+  int cnt = 0, ng = 0, grp = 0;
+  const int dq = isB ? -8 : 8;  // doubles per QElt row, in the lane's direction
+  const double *pq = reinterpret_cast<const double *>(q + min(max(seg_row(isB, nb, t0), 0), nb - 1));
+  double nc2 = __ldg(pq), ndl = __ldg(pq + 2), ngg = __ldg(pq + og);
+  for (int t = t0; t < t1; t++) {
+    const int row = seg_row(isB, nb, t);
+    const double c2 = nc2, dl = ndl, gg = ngg;
+    if (t + 1 < t1) pq += dq;
+    nc2 = __ldg(pq);
+    ndl = __ldg(pq + 2);
+    ngg = __ldg(pq + og);
+    double r1, r2;
+    ok &= rcp_nr2(den, r1, r2);
+    Pq = sd_q2(c2, den, r1, r2);
+    const double out = LIGHT ? __dmul_rn(dl, r2) : sd_q2(dl, den, r1, r2);
+    if (!LIGHT) {
+      if (stg) {
+        stg[grp * ZG + (isB ? ZG - 1 - ng : ng)] = make_double2(out, 0.0);
+        if (++ng == ZG || t + 1 == t1) {
+          const int low = isB ? row : row - ng + 1;
+          bulk_store(P + low, stg + grp * ZG + (isB ? ZG - ng : 0), (unsigned)(ng * sizeof(double2)));
+          grp ^= 1;
+          ng = 0;
+          bulk_wait_read<1>();
+        }
+      } else {
+        P[row] = dd_make(out, 0.0);
+      }
+    }
+    const double o2 = __dmul_rn(out, out);
+    A = __dmul_rn(o2, A);
+    Bs = __fma_rn(o2, Bs, o2);
+    cnt += (signbit(den) && !isnan(den)) ? 1 : 0;
+    den = __dsub_rn(__dsub_rn(gg, lam), Pq);
+  }
+  if (!LIGHT && stg) bulk_wait_all();
+  ok &= isfinite(den) && isfinite(Bs);
+  R->in_hi = din;
+  R->in_lo = 0.0;
+  R->out_hi = den;
+  R->out_lo = 0.0;
+  R->A = A;
+  R->B_hi = Bs;
+  R->B_lo = 0.0;
+  R->t_hi = Pq;
+  R->t_lo = 0.0;
+  R->cnt = cnt;
+  R->ok = ok ? 1 : 0;
+}
+
 // Chunk-major form of k_fixed_seg: the rows 0..nb-2 are cut into K2 fixed chunks of L rows.  Thread
 // (slot c, singleton i), c < K2, runs chunk c's primary part: its F part (rows [lo, min(hi, r))) if the
 // chunk starts below r (chunk 0 always: it reports d+(0) even when r = 0), else the whole chunk as B part;
@@ -459,7 +532,7 @@ __global__ void __launch_bounds__(128) k_twist_lane_dd(const Singleton *__restri
 __global__ void __launch_bounds__(128, MRRR_FC_MINB) k_fixed_chunk(const Singleton *__restrict__ sg, int ns,
                                                      const RepDesc *__restrict__ reps, const QElt *__restrict__ mq,
                                                      const RqiState *__restrict__ st, int K2, int Wu, dd *P2,
-                                                     long long nbmax, SegRec *rec, int bulk) {
+                                                     long long nbmax, SegRec *rec, int bulk, int sd) {
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= (long long)ns * (K2 + 1)) return;
   const int i = (int)(g % ns), slot = (int)(g / ns);
@@ -516,8 +589,14 @@ __global__ void __launch_bounds__(128, MRRR_FC_MINB) k_fixed_chunk(const Singlet
   const QElt *q = mq + Rp.off;
   const dd lam = dd_make(S.lam_hi, S.lam_lo), nlam = dd_neg(lam);
   __shared__ __align__(16) double2 stage[128 * ZSTRIDE];
-  seg_pass(q, nb, isB, t0, t1, t0 == 0 ? 0 : max(t0 - W, 0), light, lam, nlam, P2 + (long long)i * nbmax, R,
-           bulk ? stage + threadIdx.x * ZSTRIDE : nullptr, Rp.depth > 0);
+  const int tw = t0 == 0 ? 0 : max(t0 - W, 0);
+  double2 *stg = bulk ? stage + threadIdx.x * ZSTRIDE : nullptr;
+  if (sd) {
+    if (light) seg_pass_sd<true>(q, nb, isB, t0, t1, tw, S.lam_hi, P2 + (long long)i * nbmax, R, nullptr);
+    else seg_pass_sd<false>(q, nb, isB, t0, t1, tw, S.lam_hi, P2 + (long long)i * nbmax, R, stg);
+    return;
+  }
+  seg_pass(q, nb, isB, t0, t1, tw, light, lam, nlam, P2 + (long long)i * nbmax, R, stg, Rp.depth > 0);
 }
 
 // thread per singleton: junctions, gamma_r, ||z||^2, inertia, and the stask decision
@@ -528,7 +607,8 @@ struct FsInc {
 __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restrict__ sg,
                                                 const RepDesc *__restrict__ reps, RqiState *st, int K,
                                                 const SegRec *__restrict__ F, double *W, ZMeta *zmeta,
-                                                int *diag_depth, double *fin_lo, double *fin_hi, FsInc &inc) {
+                                                int *diag_depth, double *fin_lo, double *fin_hi, FsInc &inc,
+                                                int sd, double eps_y) {
   RqiState S = st[i];
   if (S.status != 0) return;
   const Singleton s = sg[i];
@@ -574,7 +654,8 @@ __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restri
     inc.hofixed++;
     return;
   }
-  const dd gamma = (r == nb - 1) ? dr : dd_sub(dr, tr);
+  // single/double: gamma_r = d+(r) - c2(r)/omega(r+1) in binary64
+  const dd gamma = (r == nb - 1) ? dr : (sd ? dd_from(__dsub_rn(dr.hi, tr.hi)) : dd_sub(dr, tr));
   c += dd_sb(gamma);
   const dd zz = dd_add_d(dd_add(Ssum, Tsum), 1.0);
   dd lam = dd_make(S.lam_hi, S.lam_lo), blo = dd_make(S.blo_hi, S.blo_lo), bhi = dd_make(S.bhi_hi, S.bhi_lo);
@@ -589,7 +670,7 @@ __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restri
     const dd nz = dd_sqrt(zz);
     const dd resid = dd_div(dd_abs(gamma), nz);
     const dd rqc = dd_div(gamma, zz);
-    dd tol2 = dd_mul_d(dd_abs(lam), 4.0 * EPS_Y);  // A-30
+    dd tol2 = dd_mul_d(dd_abs(lam), 4.0 * eps_y);  // A-30
     if (dd_lt(tol2, dd_from(__dmul_rn(0x1p-100, Rp.spdiam)))) tol2 = dd_from(__dmul_rn(0x1p-100, Rp.spdiam));
     if (resid.hi <= S.thr1 || dd_lt(dd_abs(rqc), tol2)) {
       if (S.it == 1) {  // accepted on the RQC-only pass: repeat it at the same lambda with the factors stored
@@ -600,7 +681,7 @@ __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restri
       accepted = true;
     } else {
       if (c < j) blo = lam; else bhi = lam;
-      const dd nl = dd_add(lam, rqc);
+      const dd nl = sd ? dd_from(__dadd_rn(lam.hi, rqc.hi)) : dd_add(lam, rqc);  // sd: lambda in binary64
       const bool okc = ((c < j) ? (rqc.hi > 0.0) : (rqc.hi < 0.0)) && dd_lt(blo, nl) && dd_lt(nl, bhi);
       if (okc && S.it < MAX_RQI) lam = nl;
       else handover = true;  // bisection fallback / iteration cap: the two-lane kernel redoes this singleton
@@ -636,14 +717,14 @@ __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restri
 __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
                              RqiState *st, int K, const SegRec *__restrict__ rec, double *W,
                              ZMeta *zmeta, int *diag_depth, double *fin_lo, double *fin_hi, long long *stats,
-                             int *nactive, int stage) {
+                             int *nactive, int stage, int sd, double eps_y) {
   extern __shared__ uint4 recsm[];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int per = 4 * K;  // records per singleton: 2K chunks x 2 lanes
   const SegRec *F = stage ? reinterpret_cast<const SegRec *>(stage_recs(rec, per * (int)sizeof(SegRec), ns, recsm))
                           : rec + (long long)i * per;
   FsInc inc = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  if (i < ns) fixed_step_body(i, sg, reps, st, K, F, W, zmeta, diag_depth, fin_lo, fin_hi, inc);
+  if (i < ns) fixed_step_body(i, sg, reps, st, K, F, W, zmeta, diag_depth, fin_lo, fin_hi, inc, sd, eps_y);
   const unsigned fm = 0xffffffffu;
   const unsigned nact = __reduce_add_sync(fm, inc.nact), wide = __reduce_add_sync(fm, inc.wide);
   const unsigned hof = __reduce_add_sync(fm, inc.hofixed), hor = __reduce_add_sync(fm, inc.horqc);

@@ -173,14 +173,15 @@ __global__ void k_clu_attempt_multi(const Cluster *__restrict__ cl, int ncl, con
 
 __global__ void k_clu_select_multi(const Cluster *__restrict__ cl, int ncl, const RepDesc *__restrict__ reps,
                                    ShiftState *ss, const double *__restrict__ gval, const int *__restrict__ valid,
-                                   int a0, int na, int *ndone, long long *stats) {
+                                   int a0, int na, int *ndone, long long *stats, double kelg) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncl) return;
   ShiftState s = ss[c];
   if (s.done) { atomicAdd(ndone, 1); return; }
-  // mixed-precision growth bound eq:newkelgbound P:6052-6056 (A-35): max(G, eps_x / (eps_y sqrt(n))) spdiam
+  // mixed-precision growth bound eq:newkelgbound P:6052-6056 (A-35): max(G, eps_x / (eps_y sqrt(n))) spdiam,
+  // kelg = eps_x / eps_y (2^51 double/dd, 2^29 single/double)
   const RepDesc Rg = reps[cl[c].rep];
-  const double gthr = __dmul_rn(dmaxd(GROWTH, __ddiv_rn(0x1p51, sqrt((double)Rg.nb))), Rg.spdiam);
+  const double gthr = __dmul_rn(dmaxd(GROWTH, __ddiv_rn(kelg, sqrt((double)Rg.nb))), Rg.spdiam);
   for (int a = a0; a < a0 + na && !s.done; a++) {
     atomicAdd((unsigned long long *)&stats[ST_ATTEMPTS], 1ull);
     const long long o = ((long long)c * na + (a - a0)) * 2;

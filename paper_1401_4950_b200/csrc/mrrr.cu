@@ -21,6 +21,7 @@
 #include "kernels_rqi.cuh"
 #include "kernels_guided.cuh"
 #include "kernels_rqi3.cuh"
+#include "kernels_sd.cuh"
 
 namespace {
 
@@ -125,6 +126,8 @@ struct mrrr_ctx {
   long long rqi_seg_min = 2048; // root blocks up to this size skip the segmented RQI (MRRR_RQISEGMIN)
   bool bmerge = true;            // start nodes sharing a start interval bisected as one node (MRRR_BMERGE=0: off)
   bool nonlocal = false;         // this solve's root rounds found non-contracting recurrences (see run_bisection)
+  bool sd = false;             // this solve runs the single/double realisation (mrrr_seig)
+  double gaptol_sd = 1e-5;     // its fixed gaptol
   int fault = 0;               // MRRR_FAULT: fault injection for the GPU tests (k_rqi2: bit 0 fallback, bit 1 careful)
   long long l2_max_window = 0;
 
@@ -139,7 +142,7 @@ struct mrrr_ctx {
   std::vector<cudaEvent_t> rev;           // events around device-driven rounds
   Buf nodesA, nodesB, counts, ex, excounts, exmap, bnA, bnB, sing, clusA, clusB, ss, gval, valid, cseg, bnoff,
       ipool_lo, ipool_hi, yref_lo, yref_hi, wsA, wsB, stats, cnt, ddepth, dgf, dgl, dflo, dfhi, hd, he, hW, hZ, zmeta,
-      hd2;
+      hd2, sdin, sdW, sdZ, sdhin, sdhW, sdhZ;
   int *h_cnt = nullptr;  // pinned counters
 
   // results of the last call
@@ -762,7 +765,8 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
       dd *P2s = h->wsA.as<dd>() + stride * nbmax;                 // after TF
       RqiState *rs = h->rqst.as<RqiState>();
       SegRec *rec = h->rqrec.as<SegRec>();
-      k_rqi3_init<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs);
+      k_rqi3_init<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs,
+                                                                h->sd ? 0x1p-24 : EPS_X);
       const int KT = 2 * K;
       TwRec *trec = reinterpret_cast<TwRec *>(rec);
       const size_t tsb = stage_bytes(h, 32 * 2 * KT * sizeof(TwRec));
@@ -791,12 +795,13 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
         CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
         k_fixed_chunk<<<nblocks_for((2 * K + 1) * nb, 128), 128, 0, h->stream>>>(
             sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, 2 * K, Wu, P2s, nbmax, rec,
-            h->rqi_bulk ? 1 : 0);
+            h->rqi_bulk ? 1 : 0, h->sd ? 1 : 0);
         const size_t fsb = stage_bytes(h, 32 * 4 * K * sizeof(SegRec));
         k_fixed_step<<<nblocks_for(nb, 32), 32, fsb, h->stream>>>(
             sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, rec, W, h->zmeta.as<ZMeta>(),
             diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
-            diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), h->cnt.as<int>() + C_NFB, fsb ? 1 : 0);
+            diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), h->cnt.as<int>() + C_NFB, fsb ? 1 : 0,
+            h->sd ? 1 : 0, h->sd ? 0x1p-53 : EPS_Y);
         launch_check(h);
         h->host_launches += 1;
         if (it == 0) continue;  // the RQC-only pass never finishes a singleton: no host check after it
@@ -823,7 +828,8 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
       k_rqi2<<<nblocks_for(2 * nold, 64), 64, 64 * MRRR_RQI_RING * sizeof(RingSlot), h->stream>>>(
           sgb, nold, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->mq.as<QElt>(), h->wsA.as<dd>(), stride, nbmax, W,
           h->zmeta.as<ZMeta>(), diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
-          diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), h->fault);
+          diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), h->fault, h->sd ? 1 : 0,
+          h->sd ? 0x1p-24 : EPS_X, h->sd ? 0x1p-53 : EPS_Y);
       launch_check(h);
       k_zwrite_chunk<<<nblocks_for(nold, 4), 128, 0, h->stream>>>(
           sgb, nold, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>() + 2 * stride * nbmax, nbmax,
@@ -893,9 +899,18 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
     k_clu_yref_init<<<nblocks_for(nc, 128), 128, 0, h->stream>>>(cl, nc, h->reps.as<RepDesc>(), ilo, ihi,
                                                                  h->bnA.as<BNode>());
     launch_check(h);
-    int nr = run_brackets<true>(h, 2 * nc);
     bool dummy = false;
-    run_bisection<true>(h, nr, h->yref_lo.as<double>(), h->yref_hi.as<double>(), RTOL_Y, 0, nullptr, 0, &dummy);
+    if (h->sd) {
+      // single/double: y = binary64, so the y-count is the x-count on M_x = M_y (the same operations): the
+      // x-path brackets and bisection with the y tolerance
+      const int nr = run_brackets<false>(h, 2 * nc);
+      h->cur_nbmax = nbmax;
+      run_bisection<false>(h, nr, h->yref_lo.as<double>(), h->yref_hi.as<double>(), RTOL_Y, 0, nullptr, 0, &dummy);
+      h->cur_nbmax = 0;
+    } else {
+      const int nr = run_brackets<true>(h, 2 * nc);
+      run_bisection<true>(h, nr, h->yref_lo.as<double>(), h->yref_hi.as<double>(), RTOL_Y, 0, nullptr, 0, &dummy);
+    }
     // (b, c) shifts
     CK(h->ss.ensure(sizeof(ShiftState) * nc));
     CK(h->gval.ensure(sizeof(double) * 2LL * nc));
@@ -909,7 +924,11 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
     for (int a0 = 0; a0 < MAX_ATTEMPTS;) {
       const int na = (a0 == 0) ? 1 : MAX_ATTEMPTS - a0;
       CK(cudaMemsetAsync(h->cnt.as<int>() + C_NDONE, 0, sizeof(int), h->stream));
-      if (h->segy_k > 1) {  // growth chains split into verified segments (latency: n/K + W rows per thread)
+      if (h->sd) {  // binary64 dstqds in the reference order (kernels_sd.cuh)
+        k_sd_attempt<<<nblocks_for(2LL * na * nc, 64), 64, 0, h->stream>>>(
+            cl, nc, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->ss.as<ShiftState>(), a0, na, h->gval.as<double>(),
+            h->valid.as<int>());
+      } else if (h->segy_k > 1) {  // growth chains split into verified segments (latency: n/K + W rows per thread)
         const int K = h->segy_k;
         const long long T = 2LL * na * nc;
         CK(h->segoutg.ensure(sizeof(SegG) * T * K));
@@ -927,14 +946,18 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
       launch_check(h);
       k_clu_select_multi<<<nblocks_for(nc, 128), 128, 0, h->stream>>>(
           cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(), h->gval.as<double>(), h->valid.as<int>(), a0, na,
-          h->cnt.as<int>() + C_NDONE, h->stats.as<long long>());
+          h->cnt.as<int>() + C_NDONE, h->stats.as<long long>(), h->sd ? 0x1p29 : 0x1p51);
       launch_check(h);
       read_counters(h);
       if (h->h_cnt[C_NDONE] >= nc) break;
       a0 += na;
     }
     // (d) children
-    if (h->segy_k > 1) {  // child rows built by verified segments (latency n/K + W rows per thread)
+    if (h->sd) {
+      k_sd_build<<<nblocks_for(nc, 64), 64, 0, h->stream>>>(cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(),
+                                                            h->mx.as<double2>(), h->my.as<YElt>(), repbase, poolbase,
+                                                            (int)nbmax);
+    } else if (h->segy_k > 1) {  // child rows built by verified segments (latency n/K + W rows per thread)
       const int K = h->segy_k;
       CK(h->segoutg.ensure(sizeof(SegG) * (long long)nc * K));
       const size_t bsb = (size_t)128 * 2 * BG * (sizeof(YElt) + sizeof(double2));
@@ -1072,8 +1095,9 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
 
   // S1/S2 (and the S0 scale test: the largest |entry| comes out of the same pass)
   struct ScalRec { int nblk, err; double tnorm, amax; };
+  const double eps_split = h->sd ? 0x1p-24 : EPS_X;  // eps_x of the split rule
   k_split<1024><<<1, 1024, 0, st>>>(d, e, n, h->starts.as<int>(), h->scal.as<int>(), (double *)(h->scal.as<char>() + 8),
-                                    h->scal.as<int>() + 1, (double *)(h->scal.as<char>() + 16));
+                                    h->scal.as<int>() + 1, (double *)(h->scal.as<char>() + 16), eps_split);
   launch_check(h);
   ScalRec hs;
   CK(cudaMemcpyAsync(&hs, h->scal.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
@@ -1092,7 +1116,7 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
     e = es;
     k_split<1024><<<1, 1024, 0, st>>>(d, e, n, h->starts.as<int>(), h->scal.as<int>(),
                                       (double *)(h->scal.as<char>() + 8), h->scal.as<int>() + 1,
-                                      (double *)(h->scal.as<char>() + 16));
+                                      (double *)(h->scal.as<char>() + 16), eps_split);
     launch_check(h);
     CK(cudaMemcpyAsync(&hs, h->scal.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -1175,12 +1199,12 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
     k_root<256><<<nbl, 256, 0, st>>>(d, e, n, h->starts.as<int>(), h->blist.as<int>(), h->bside.as<int>(), h->seed,
                                      h->binfo.as<double>(), h->mx.as<double2>(), h->my.as<YElt>(),
                                      h->lscratch.as<double>(), h->reps.as<RepDesc>(),
-                                     G > 1 ? h->gpart.as<double>() : nullptr, G > 1 ? G : 0);
+                                     G > 1 ? h->gpart.as<double>() : nullptr, G > 1 ? G : 0, h->sd ? 1 : 0);
     launch_check(h);
     if (G > 1) {
       k_root_derive<256><<<dim3(nbl, G), 256, 0, st>>>(n, h->starts.as<int>(), h->blist.as<int>(), h->seed,
                                                        h->binfo.as<double>(), h->mx.as<double2>(), h->my.as<YElt>(),
-                                                       h->lscratch.as<double>(), G);
+                                                       h->lscratch.as<double>(), G, h->sd ? 1 : 0);
       launch_check(h);
     }
     k_build_q<<<dim3(nbl, (unsigned)std::min<long long>(64, std::max<long long>(1, (n + 255) / 256 / std::max(1, nbl / 148 + 1)))),
@@ -1712,6 +1736,79 @@ int mrrr_eig_host(mrrr_t h, const double *d, const double *e, int64_t n, int64_t
     rc = er.code;
   }
   return rc;
+}
+
+// single/double realisation: binary32 in and out, binary64 inside, gaptol 1e-5
+static int seig_device(mrrr_t h, const float *d, const float *e, long long n, long long il, long long iu, float *W,
+                       float *Z, long long ldz) {
+  const long long k = iu - il + 1;
+  CK(h->sdin.ensure(sizeof(double) * (2 * n)));
+  CK(h->sdW.ensure(sizeof(double) * k));
+  CK(h->sdZ.ensure(sizeof(double) * n * k));
+  double *dd_ = h->sdin.as<double>(), *de = dd_ + n;
+  k_f2d<<<nblocks_for(n, 256), 256, 0, h->stream>>>(d, dd_, n);
+  if (n > 1) k_f2d<<<nblocks_for(n - 1, 256), 256, 0, h->stream>>>(e, de, n - 1);
+  launch_check(h);
+  struct Profile {  // the handle's profile is restored on every exit path (errors throw)
+    mrrr_t h;
+    double g;
+    ~Profile() { h->sd = false; h->gaptol = g; }
+  } prof{h, h->gaptol};
+  h->sd = true;
+  h->gaptol = h->gaptol_sd;
+  int rc = solve(h, dd_, de, n, il, iu, h->sdW.as<double>(), h->sdZ.as<double>(), n, 0, 0, nullptr, nullptr, 0);
+  if (rc) return rc;
+  k_w_d2f<<<nblocks_for(k, 256), 256, 0, h->stream>>>(h->sdW.as<double>(), W, k);
+  for (long long c0 = 0; c0 < k; c0 += 65535) {
+    const long long kc = std::min<long long>(65535, k - c0);
+    k_z_d2f<<<dim3(nblocks_for(n, 256), (unsigned)kc), 256, 0, h->stream>>>(h->sdZ.as<double>() + c0 * n,
+                                                                           Z + c0 * ldz, n, ldz);
+  }
+  launch_check(h);
+  CK(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int mrrr_seig(mrrr_t h, const float *d, const float *e, int64_t n, int64_t il, int64_t iu, float *W, float *Z,
+              int64_t ldz) {
+  if (!h) return -1;
+  int a = check_args(reinterpret_cast<const double *>(d), reinterpret_cast<const double *>(e), n, il, iu,
+                     reinterpret_cast<const double *>(W), reinterpret_cast<const double *>(Z), ldz);
+  if (a) return a;
+  try {
+    CK(cudaSetDevice(h->device));
+    return seig_device(h, d, e, n, il, iu, W, Z, ldz);
+  } catch (Err &er) {
+    return er.code;
+  }
+}
+
+int mrrr_seig_host(mrrr_t h, const float *d, const float *e, int64_t n, int64_t il, int64_t iu, float *W, float *Z,
+                   int64_t ldz) {
+  if (!h) return -1;
+  int a = check_args(reinterpret_cast<const double *>(d), reinterpret_cast<const double *>(e), n, il, iu,
+                     reinterpret_cast<const double *>(W), reinterpret_cast<const double *>(Z), ldz);
+  if (a) return a;
+  const long long k = iu - il + 1;
+  try {
+    CK(cudaSetDevice(h->device));
+    CK(h->sdhin.ensure(sizeof(float) * 2 * n));
+    CK(h->sdhW.ensure(sizeof(float) * k));
+    CK(h->sdhZ.ensure(sizeof(float) * n * k));
+    float *df = h->sdhin.as<float>(), *ef = df + n, *dW = h->sdhW.as<float>(), *dZ = h->sdhZ.as<float>();
+    CK(cudaMemcpyAsync(df, d, sizeof(float) * n, cudaMemcpyHostToDevice, h->stream));
+    if (n > 1) CK(cudaMemcpyAsync(ef, e, sizeof(float) * (n - 1), cudaMemcpyHostToDevice, h->stream));
+    int rc = seig_device(h, df, ef, n, il, iu, dW, dZ, n);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(W, dW, sizeof(float) * k, cudaMemcpyDeviceToHost, h->stream));
+    if (ldz == n) CK(cudaMemcpyAsync(Z, dZ, sizeof(float) * n * k, cudaMemcpyDeviceToHost, h->stream));
+    else CK(cudaMemcpy2DAsync(Z, sizeof(float) * ldz, dZ, sizeof(float) * n, sizeof(float) * n, k,
+                              cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return 0;
+  } catch (Err &er) {
+    return er.code;
+  }
 }
 
 int mrrr_get_stats(mrrr_t h, int64_t *s, int32_t ns) {

@@ -165,8 +165,10 @@ int mrrr_shard_owner(const int32_t *gstart, int64_t n, int64_t il, int64_t iu, i
  * x-arithmetic twist search did not resolve gamma / a segment junction failed / the RQC was rejected,
  * 28 dd rows of RQC-only (light) passes, 29 fp64 rows of the segmented twist search (both lanes),
  * 30 segmented RQI passes repeated with an 8x longer warm-up after a failed junction, 31 singletons whose
- * last two-lane Getvec ran the careful IEEE pass (zero pivots / special values). */
-#define MRRR_NSTATS 32
+ * last two-lane Getvec ran the careful IEEE pass (zero pivots / special values), 32 segmented
+ * many-representation x-NegCount chains (child bisection) whose junctions did not all verify, 33 segments those
+ * chains re-ran sequentially. */
+#define MRRR_NSTATS 34
 int mrrr_get_stats(mrrr_t h, int64_t *stats, int32_t nstats);
 
 /* Diagnostics of the last call made with MRRR_KEEP_DIAG (host buffers owned

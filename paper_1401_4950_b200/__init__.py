@@ -23,11 +23,12 @@ LIB_PATH = os.environ.get("MRRR_LIB") or os.path.join(HERE, "libmrrr.so")
 
 KEEP_DIAG = 1
 MAXD = 8
-NSTATS = 32
+NSTATS = 34
 STAT_NAMES = ["d_max", "n_clusters", "largest_cluster", "uncertified", "shift_attempts", "rqi_iters",
               "rqi_fallbacks", "bracket_fixes", "root_backoffs", "failed", "negcount_x", "negcount_y",
               "getvec_calls", "rounds", "launches", "nblocks", "qd_steps", "qdg_steps", "z_steps", "zw_steps",
-              "negcount_x_alg", "negcount_y_alg", "rqi_reject_sign", "rqi_reject_bracket", "rqi_handover", "ho_twist", "ho_fixed", "ho_rqc", "qd_light", "twist_rows", "seg_wide", "careful"]
+              "negcount_x_alg", "negcount_y_alg", "rqi_reject_sign", "rqi_reject_bracket", "rqi_handover", "ho_twist", "ho_fixed", "ho_rqc", "qd_light", "twist_rows", "seg_wide", "careful",
+              "xg_fallback_chains", "xg_fallback_segments"]
 TIME_NAMES = ["total", "split_root", "root_bisection", "classification", "clusters", "singletons",
               "rqi_ms_per_launch", "rqi_launches", "negcount_ms_per_launch", "negcount_launches", "t10", "t11"]
 

@@ -487,6 +487,27 @@ struct SegOutX {
   double in, out;
   int cnt, ok, empty, pad;
 };
+// one segment of k_negcount_seg_xg with the IEEE quotient at every step (q_ieee): used for sigma = +-0, where the
+// state stays a signed zero that the fast sequence's range test rejects (every segment would fail its junction
+// and the whole chain would rerun sequentially)
+__device__ __noinline__ void seg_xg_exact(const double2 *__restrict__ M, int nb, int steps, int w0, int bk, int ek,
+                                          double sig, SegOutX *o) {
+  double s = -sig, s_in = -sig;
+  int cnt = 0;
+  for (int i = w0; i < ek; i++) {
+    if (i == bk) s_in = s;
+    const double2 mm = __ldg(M + i);
+    const double dp = __dadd_rn(mm.x, s);
+    s = __dsub_rn(__dmul_rn(q_ieee(s, dp), mm.y), sig);
+    if (i >= bk) cnt += sbx(dp);
+  }
+  if (ek == steps) cnt += sbx(__dadd_rn(__ldg(M + nb - 1).x, s));
+  o->in = s_in;
+  o->out = s;
+  o->cnt = cnt;
+  o->ok = 1;
+  o->empty = 0;
+}
 __global__ void __launch_bounds__(128) k_negcount_seg_xg(const Node *__restrict__ nodes, int nnode, int m,
                                                          const ExplicitChain *__restrict__ ex, int nex,
                                                          const RepDesc *__restrict__ reps,
@@ -521,6 +542,10 @@ __global__ void __launch_bounds__(128) k_negcount_seg_xg(const Node *__restrict_
     w0 = 0;
   }
   const double2 *M = mx + R.off;
+  if (sig == 0.0) {  // (rare: the first midpoint of a child interval symmetric about 0) exact IEEE steps
+    seg_xg_exact(M, nb, steps, w0, bk, ek, sig, o);
+    return;
+  }
   double s = -sig, s_in = -sig;
   int cnt = 0;
   bool ok = true;
@@ -560,7 +585,7 @@ struct FbX {
   int k, cnt;  // first unverified segment, count of the verified rows before it
 };
 __global__ void k_seg_combine_xg(long long tot, long long nn, int K, const SegOutX *__restrict__ seg, int *counts,
-                                 int *excounts, FbX *fb, int *nfb) {
+                                 int *excounts, FbX *fb, int *nfb, long long *stats) {
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= tot) return;
   const SegOutX *S = seg + c * K;
@@ -584,6 +609,7 @@ __global__ void k_seg_combine_xg(long long tot, long long nn, int K, const SegOu
   f.k = (prev >= 0) ? k : 0;
   f.cnt = (prev >= 0) ? total : 0;
   fb[atomicAdd(nfb, 1)] = f;
+  atomicAdd((unsigned long long *)&stats[ST_XG_FB], 1ull);
 }
 // careful (IEEE) evaluation from the first unverified segment's first row with the last exact state, re-joining
 // the recorded segments: after running a segment exactly, the next segment's result is taken over as soon as its
@@ -593,7 +619,7 @@ __global__ void k_seg_fallback_xg(const FbX *__restrict__ fb, const int *__restr
                                   const Node *__restrict__ nodes, int nnode, int m,
                                   const ExplicitChain *__restrict__ ex, const RepDesc *__restrict__ reps,
                                   const double2 *__restrict__ mx, int K, int Wu, int *counts, int *excounts,
-                                  const SegOutX *__restrict__ seg) {
+                                  const SegOutX *__restrict__ seg, long long *stats) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *nfb) return;
   const FbX f = fb[i];
@@ -615,7 +641,10 @@ __global__ void k_seg_fallback_xg(const FbX *__restrict__ fb, const int *__restr
   auto step = [&](double2 mm) {
     const double dp = __dadd_rn(mm.x, s);
     double q = div_fast_nocheck(s, dp);
-    if (!div_range_ok(s, dp, q)) q = (isinf(s) && isinf(dp)) ? 1.0 : __ddiv_rn(s, dp);
+    if (!div_range_ok(s, dp, q))
+      q = (s == 0.0 && dp != 0.0 && !isnan(dp)) ? __dmul_rn(s, copysign(1.0, dp))  // exact signed zero
+          : (isinf(s) && isinf(dp))             ? 1.0
+                                                : __ddiv_rn(s, dp);
     s = __dsub_rn(__dmul_rn(q, mm.y), sig);
     cnt += sbx(dp);
   };
@@ -643,6 +672,7 @@ __global__ void k_seg_fallback_xg(const FbX *__restrict__ fb, const int *__restr
     while (k < K) {
       const int bk = min(k * L, steps), ek = min(bk + L, steps);
       run_rows(bk, ek);  // segment k exactly
+      atomicAdd((unsigned long long *)&stats[ST_XG_FBSEG], 1ull);
       k++;
       // re-join: take over every following segment whose entry state is the exact one
       while (k < K) {

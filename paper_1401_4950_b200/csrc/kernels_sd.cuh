@@ -6,11 +6,12 @@
 //
 //   k_f2d / k_w_d2f / k_z_d2f   "data conversion is only necessary when reading the input and writing the
 //                               output": binary32 <-> binary64 at the boundary.
-//   k_sd_attempt                S8(c) shift attempts: Alg. dstqds P:3324-3351 in binary64, growth max|d+| and
-//                               validity, in the operation order of the reference loop (the child data decide
-//                               integer outputs, so they must be bit-identical to the oracle's binary64 run).
-//   k_sd_build                  S8(d) child representation (d+, l+) and its derived rows dl = d l, dll = dl l
-//                               (P:4145-4147), sigma accumulated in binary64.
+//   k_sd_seg / _combine         S8(c) shift attempts and S8(d) child representations: Alg. dstqds
+//                               in binary64 in the operation order of the reference loop (the child data decide
+//                               integer outputs, so they must be bit-identical to the oracle's binary64 run):
+//                               growth max|d+| and validity per attempt; the child rows d = d+, dl = d l,
+//                               dll = dl l and sigma accumulated in binary64.  Segmented chains
+//                               with bit-exact junctions (sequential recomputation where a junction fails).
 //
 // The singleton RQI runs the segmented passes of kernels_rqi3.cuh with their binary64 step (seg_pass_sd).
 #pragma once
@@ -48,44 +49,75 @@ __device__ __forceinline__ void sd_dstqds_row(double &s, double d, double dl, do
   s = __dsub_rn(__dmul_rn(q, dll), tau);
 }
 
-// S8(c): attempts a0 .. a0+na-1 of every open cluster, thread per (cluster, attempt, side); growth g = max |d+|
-// and validity (no NaN among d+, l+) as the oracle's do_cluster forms them; k_clu_select_multi replays the
-// sequential acceptance
-__global__ void k_sd_attempt(const Cluster *__restrict__ cl, int ncl, const RepDesc *__restrict__ reps,
-                             const YElt *__restrict__ my, const ShiftState *__restrict__ ss, int a0, int na,
-                             double *gval, int *valid) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= 2LL * na * ncl) return;
-  const int c = (int)(t / (2 * na)), ia = (int)((t >> 1) % na), side = (int)(t & 1);
-  const ShiftState S = ss[c];
-  if (S.done) return;
+// shift of chain t: attempt mode (na > 0): t = (cluster, attempt a0 + ia, side) as in k_clu_attempt_multi; build
+// mode (na == 0): t = cluster, tau = its accepted shift
+__device__ __forceinline__ double sd_chain_tau(const ShiftState &S, long long t, int a0, int na) {
+  if (na == 0) return S.best_tau;
+  const int ia = (int)((t >> 1) % na), side = (int)(t & 1);
   double tau = side ? S.taur : S.taul;
   for (int b = a0; b < a0 + ia; b++) tau = side ? __dadd_rn(tau, ldexp(S.offr, b)) : __dsub_rn(tau, ldexp(S.offl, b));
-  const RepDesc R = reps[cl[c].rep];
-  const YElt *y = my + R.off;
-  double s = -tau, g = 0.0;
-  int v = 1;
-  for (int i = 0; i < R.nb - 1; i++) {
+  return tau;
+}
+__device__ __forceinline__ int sd_chain_cluster(long long t, int na) { return na ? (int)(t / (2 * na)) : (int)t; }
+
+// rows [b, e) of dstqds(M, tau) from state s: growth / validity over the rows, child rows written when yc != 0;
+// the last row (b .. e reaching nb-1) adds d+(nb) = s + d(nb).  The parent rows are loaded PF rows ahead into a
+// register ring (the recurrence would otherwise wait for every row's L2 / HBM latency)
+__device__ __forceinline__ void sd_rows(const YElt *__restrict__ y, int nb, int b, int e, double tau, double &s,
+                                        double &g, int &v, YElt *yc, double2 *xc) {
+  constexpr int PF = 8;
+  double rd[PF], rl[PF], rll[PF];
+  auto ld = [&](int i, int u) {
+    const int ii = min(i, nb - 1);
+    rd[u] = __ldg(&y[ii].d_hi);
+    rl[u] = __ldg(&y[ii].dl_hi);
+    rll[u] = __ldg(&y[ii].dll_hi);
+  };
+  auto row = [&](int i, double d, double dl, double dll) {
     double dp, lp;
-    sd_dstqds_row(s, __ldg(&y[i].d_hi), __ldg(&y[i].dl_hi), __ldg(&y[i].dll_hi), tau, dp, lp);
+    sd_dstqds_row(s, d, dl, dll, tau, dp, lp);
     v &= !(isnan(dp) || isnan(lp));
     g = dmaxd(g, fabs(dp));
+    if (yc) {
+      const double dlc = __dmul_rn(dp, lp), dllc = __dmul_rn(dlc, lp);
+      YElt el;
+      el.d_hi = dp; el.d_lo = 0.0; el.dl_hi = dlc; el.dl_lo = 0.0; el.dll_hi = dllc; el.dll_lo = 0.0;
+      yc[i] = el;
+      xc[i] = make_double2(dp, dllc);
+    }
+  };
+#pragma unroll
+  for (int u = 0; u < PF; u++) ld(b + u, u);
+  int i = b;
+  for (; i + PF <= e; i += PF) {
+#pragma unroll
+    for (int u = 0; u < PF; u++) {
+      const double d = rd[u], dl = rl[u], dll = rll[u];
+      ld(i + u + PF, u);
+      row(i + u, d, dl, dll);
+    }
   }
-  const double dn = __dadd_rn(s, __ldg(&y[R.nb - 1].d_hi));
-  v &= !isnan(dn);
-  gval[t] = dmaxd(g, fabs(dn));
-  valid[t] = v;
+#pragma unroll
+  for (int u = 0; u < PF; u++)
+    if (i + u < e) row(i + u, rd[u], rl[u], rll[u]);
+  if (e == nb - 1) {
+    const double dn = __dadd_rn(s, __ldg(&y[nb - 1].d_hi));
+    v &= !isnan(dn);
+    g = dmaxd(g, fabs(dn));
+    if (yc) {
+      YElt el;
+      el.d_hi = dn; el.d_lo = 0.0; el.dl_hi = el.dl_lo = el.dll_hi = el.dll_lo = 0.0;
+      yc[nb - 1] = el;
+      xc[nb - 1] = make_double2(dn, 0.0);
+    }
+  }
 }
 
-// S8(d): child representation of cluster c (rep id repbase + c, rows at poolbase + c * nbmax): d = d+,
-// l = l+ of dstqds(M, tau_best); rows dl = d l, dll = dl l, M_x = (d, dll) (the oracle's rep_derive with
-// y = binary64, where fl64(M_y) = M_y); sigma = fl64(sigma_parent + tau).  No valid shift: nb = -1 (the
-// members go back to the parent as singletons, as in the double/dd path).
-__global__ void k_sd_build(const Cluster *__restrict__ cl, int ncl, RepDesc *reps, const ShiftState *__restrict__ ss,
-                           double2 *mx, YElt *my, int repbase, long long poolbase, int nbmax) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= ncl) return;
-  const ShiftState S = ss[c];
+// build mode: the child representation descriptor (rep id repbase + c, rows at poolbase + c * nbmax), sigma =
+// fl64(sigma_parent + tau); no valid shift: nb = -1 (members go back to the parent as singletons, as in the
+// double/dd path)
+__device__ __forceinline__ void sd_child_desc(const Cluster *__restrict__ cl, int c, RepDesc *reps,
+                                              const ShiftState &S, int repbase, long long poolbase, int nbmax) {
   const RepDesc P = reps[cl[c].rep];
   RepDesc R = P;
   R.off = poolbase + (long long)c * nbmax;
@@ -94,24 +126,96 @@ __global__ void k_sd_build(const Cluster *__restrict__ cl, int ncl, RepDesc *rep
   R.sig_lo = 0.0;
   if (!S.have_best) R.nb = -1;
   reps[repbase + c] = R;
-  if (!S.have_best) return;
-  const YElt *y = my + P.off;
-  YElt *yc = my + R.off;
-  double2 *xc = mx + R.off;
-  const double tau = S.best_tau;
-  double s = -tau;
-  for (int i = 0; i < P.nb - 1; i++) {
-    double dp, lp;
-    sd_dstqds_row(s, __ldg(&y[i].d_hi), __ldg(&y[i].dl_hi), __ldg(&y[i].dll_hi), tau, dp, lp);
-    const double dl = __dmul_rn(dp, lp), dll = __dmul_rn(dl, lp);
-    YElt e;
-    e.d_hi = dp; e.d_lo = 0.0; e.dl_hi = dl; e.dl_lo = 0.0; e.dll_hi = dll; e.dll_lo = 0.0;
-    yc[i] = e;
-    xc[i] = make_double2(dp, dll);
+}
+
+// S8(c)/(d) as segmented chains: chain t's rows 0..nb-2 in K segments, segment k started Wu rows early from the
+// guess q = 1 (s = dll(w0-1) - tau); it records its entry state at its first row and its exit state, and is
+// accepted by k_sd_seg_combine only if the entry equals the predecessor's exit bit for bit (then it applied
+// every operation to the sequential operands; otherwise the chain is recomputed sequentially there).
+// Thread = (segment k, chain t), chains fastest: a warp runs one segment of 32 chains (shared parent rows).
+struct SegSD {
+  double s_in, s_out, g;
+  int valid, empty;
+};
+__global__ void __launch_bounds__(128) k_sd_seg(const Cluster *__restrict__ cl, const RepDesc *__restrict__ reps,
+                                                const YElt *__restrict__ my, const ShiftState *__restrict__ ss,
+                                                long long T, int a0, int na, int K, int Wu, SegSD *seg,
+                                                double2 *mx, YElt *myc, long long poolbase, int nbmax) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= T * K) return;
+  const long long t = g % T;
+  const int k = (int)(g / T);
+  SegSD *o = seg + t * K + k;
+  const int c = sd_chain_cluster(t, na);
+  const ShiftState S = ss[c];
+  if ((na && S.done) || (!na && !S.have_best)) { o->empty = 1; return; }
+  const RepDesc R = reps[cl[c].rep];
+  const int nb = R.nb, steps = nb - 1;
+  int bk, ek, w0;
+  if (steps >= 2 * K * Wu) {
+    const int L = (steps + K - 1) / K;
+    bk = min(k * L, steps);
+    ek = min(bk + L, steps);
+    w0 = (k == 0) ? 0 : max(bk - Wu, 0);
+  } else {
+    if (k > 0) { o->empty = 1; return; }
+    bk = 0; ek = steps; w0 = 0;
   }
-  const double dn = __dadd_rn(s, __ldg(&y[P.nb - 1].d_hi));
-  YElt e;
-  e.d_hi = dn; e.d_lo = 0.0; e.dl_hi = e.dl_lo = e.dll_hi = e.dll_lo = 0.0;
-  yc[P.nb - 1] = e;
-  xc[P.nb - 1] = make_double2(dn, 0.0);
+  const double tau = sd_chain_tau(S, t, a0, na);
+  const YElt *y = my + R.off;
+  double s = (w0 == 0) ? -tau : __dsub_rn(__ldg(&y[w0 - 1].dll_hi), tau);
+  double gg = 0.0;
+  int v = 1;
+  sd_rows(y, nb, w0, bk, tau, s, gg, v, nullptr, nullptr);  // warm-up (no growth / validity, bk < nb - 1)
+  gg = 0.0;
+  v = 1;
+  o->s_in = s;
+  const long long off = poolbase + (long long)c * nbmax;
+  sd_rows(y, nb, bk, ek, tau, s, gg, v, na ? nullptr : myc + off, na ? nullptr : mx + off);
+  o->s_out = s;
+  o->g = gg;
+  o->valid = v;
+  o->empty = 0;
+}
+// junctions of chain t; accepted: growth / validity (attempts) or the descriptor (build); else the chain is
+// recomputed sequentially (and its child rows rewritten)
+__global__ void k_sd_seg_combine(const Cluster *__restrict__ cl, RepDesc *reps, const YElt *__restrict__ my,
+                                 const ShiftState *__restrict__ ss, long long T, int a0, int na, int K,
+                                 const SegSD *__restrict__ seg, double *gval, int *valid, double2 *mx, YElt *myc,
+                                 int repbase, long long poolbase, int nbmax, int *nfb) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int c = sd_chain_cluster(t, na);
+  const ShiftState S = ss[c];
+  if (na && S.done) return;
+  if (!na) {
+    sd_child_desc(cl, c, reps, S, repbase, poolbase, nbmax);
+    if (!S.have_best) return;
+  }
+  const SegSD *R = seg + t * K;
+  bool good = true;
+  double gg = 0.0;
+  int v = 1, prev = -1;
+  for (int k = 0; k < K && good; k++) {
+    const SegSD &a = R[k];
+    if (a.empty) continue;
+    good = prev < 0 || __double_as_longlong(a.s_in) == __double_as_longlong(R[prev].s_out);
+    gg = dmaxd(gg, a.g);
+    v &= a.valid;
+    prev = k;
+  }
+  if (!good) {
+    atomicAdd(nfb, 1);
+    const RepDesc P = reps[cl[c].rep];
+    const double tau = sd_chain_tau(S, t, a0, na);
+    const long long off = poolbase + (long long)c * nbmax;
+    double s = -tau;
+    gg = 0.0;
+    v = 1;
+    sd_rows(my + P.off, P.nb, 0, P.nb - 1, tau, s, gg, v, na ? nullptr : myc + off, na ? nullptr : mx + off);
+  }
+  if (na) {
+    gval[t] = gg;
+    valid[t] = v;
+  }
 }

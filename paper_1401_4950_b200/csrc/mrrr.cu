@@ -128,6 +128,7 @@ struct mrrr_ctx {
   bool nonlocal = false;         // this solve's root rounds found non-contracting recurrences (see run_bisection)
   bool sd = false;             // this solve runs the single/double realisation (mrrr_seig)
   double gaptol_sd = 1e-5;     // its fixed gaptol
+  int segsd_k = 32;            // segments per binary64 dstqds chain (shift attempts, child builds; MRRR_SEGSDK)
   int fault = 0;               // MRRR_FAULT: fault injection for the GPU tests (k_rqi2: bit 0 fallback, bit 1 careful)
   long long l2_max_window = 0;
 
@@ -142,7 +143,7 @@ struct mrrr_ctx {
   std::vector<cudaEvent_t> rev;           // events around device-driven rounds
   Buf nodesA, nodesB, counts, ex, excounts, exmap, bnA, bnB, sing, clusA, clusB, ss, gval, valid, cseg, bnoff,
       ipool_lo, ipool_hi, yref_lo, yref_hi, wsA, wsB, stats, cnt, ddepth, dgf, dgl, dflo, dfhi, hd, he, hW, hZ, zmeta,
-      hd2, sdin, sdW, sdZ, sdhin, sdhW, sdhZ;
+      hd2, sdin, sdW, sdZ, sdhin, sdhW, sdhZ, segsd;
   int *h_cnt = nullptr;  // pinned counters
 
   // results of the last call
@@ -351,11 +352,12 @@ void launch_negcount(mrrr_t h, const Node *nodes, int nnode, int m, int nex, con
         h->segoutx.as<SegOutX>());
     k_seg_combine_xg<<<nblocks_for(tot, 128), 128, 0, h->stream>>>(tot, tot - nex, K, h->segoutx.as<SegOutX>(),
                                                                    h->counts.as<int>(), h->excounts.as<int>(),
-                                                                   h->segfby.as<FbX>(), h->cnt.as<int>() + C_NFB);
+                                                                   h->segfby.as<FbX>(), h->cnt.as<int>() + C_NFB,
+                                                                   h->stats.as<long long>());
     k_seg_fallback_xg<<<nblocks_for(tot, 128), 128, 0, h->stream>>>(
         h->segfby.as<FbX>(), h->cnt.as<int>() + C_NFB, nodes, nnode, m, h->ex.as<ExplicitChain>(),
         h->reps.as<RepDesc>(), h->mx.as<double2>(), K, h->segx_w, h->counts.as<int>(), h->excounts.as<int>(),
-        h->segoutx.as<SegOutX>());
+        h->segoutx.as<SegOutX>(), h->stats.as<long long>());
     launch_check(h);
     return;
   }
@@ -756,7 +758,13 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
       // so that about rqi_threads threads run, as long as a chunk stays longer than the warm-up
       int K = h->rqi_segk;
       // warm-up rows: 128 suffice up to n = 16K (no retries measured); longer frames get 192
-      const int Wu = h->rqi_segw > 0 ? h->rqi_segw : (nbmax <= 16384 ? 128 : 192);
+      int Wu = h->rqi_segw > 0 ? h->rqi_segw : (nbmax <= 16384 ? 128 : 192);
+      if (h->sd && (h->nonlocal || nbmax <= h->rqi_seg_min)) {
+        // single/double on short or non-contracting frames: every chunk starts at row 0 (a warm-up over the whole
+        // frame), so every junction holds by construction and the binary64 passes never hand over for a junction
+        K = 1;
+        Wu = (int)nbmax;
+      }
       while (2 * K <= 32 && (long long)nb * 2 * (2 * K) <= h->rqi_threads && (nbmax - 1) >= 2 * (2 * K) * Wu) K *= 2;
       CK(h->rqst.ensure(sizeof(RqiState) * stride));
       CK(h->rqrec.ensure(sizeof(SegRec) * stride * 4 * K));  // chunk layout: 2K chunks x 2 lanes
@@ -924,10 +932,18 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
     for (int a0 = 0; a0 < MAX_ATTEMPTS;) {
       const int na = (a0 == 0) ? 1 : MAX_ATTEMPTS - a0;
       CK(cudaMemsetAsync(h->cnt.as<int>() + C_NDONE, 0, sizeof(int), h->stream));
-      if (h->sd) {  // binary64 dstqds in the reference order (kernels_sd.cuh)
-        k_sd_attempt<<<nblocks_for(2LL * na * nc, 64), 64, 0, h->stream>>>(
-            cl, nc, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->ss.as<ShiftState>(), a0, na, h->gval.as<double>(),
-            h->valid.as<int>());
+      if (h->sd) {  // binary64 dstqds in the reference order, segmented chains (kernels_sd.cuh)
+        const long long T = 2LL * na * nc;
+        int K = std::max(1, h->segsd_k);
+        while (K > 1 && nbmax - 1 < 2LL * K * h->segy_w) K /= 2;  // segments at least two warm-ups long
+        CK(h->segsd.ensure(sizeof(SegSD) * T * K));
+        CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
+        k_sd_seg<<<nblocks_for(T * K, 128), 128, 0, h->stream>>>(cl, h->reps.as<RepDesc>(), h->my.as<YElt>(),
+                                                                 h->ss.as<ShiftState>(), T, a0, na, K, h->segy_w,
+                                                                 h->segsd.as<SegSD>(), nullptr, nullptr, 0, 0);
+        k_sd_seg_combine<<<nblocks_for(T, 64), 64, 0, h->stream>>>(
+            cl, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->ss.as<ShiftState>(), T, a0, na, K, h->segsd.as<SegSD>(),
+            h->gval.as<double>(), h->valid.as<int>(), nullptr, nullptr, 0, 0, 0, h->cnt.as<int>() + C_NFB);
       } else if (h->segy_k > 1) {  // growth chains split into verified segments (latency: n/K + W rows per thread)
         const int K = h->segy_k;
         const long long T = 2LL * na * nc;
@@ -954,9 +970,17 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
     }
     // (d) children
     if (h->sd) {
-      k_sd_build<<<nblocks_for(nc, 64), 64, 0, h->stream>>>(cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(),
-                                                            h->mx.as<double2>(), h->my.as<YElt>(), repbase, poolbase,
-                                                            (int)nbmax);
+      int K = std::max(1, h->segsd_k);
+      while (K > 1 && nbmax - 1 < 2LL * K * h->segy_w) K /= 2;
+      CK(h->segsd.ensure(sizeof(SegSD) * (long long)nc * K));
+      CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
+      k_sd_seg<<<nblocks_for((long long)nc * K, 128), 128, 0, h->stream>>>(
+          cl, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->ss.as<ShiftState>(), nc, 0, 0, K, h->segy_w,
+          h->segsd.as<SegSD>(), h->mx.as<double2>(), h->my.as<YElt>(), poolbase, (int)nbmax);
+      k_sd_seg_combine<<<nblocks_for(nc, 64), 64, 0, h->stream>>>(
+          cl, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->ss.as<ShiftState>(), nc, 0, 0, K, h->segsd.as<SegSD>(),
+          nullptr, nullptr, h->mx.as<double2>(), h->my.as<YElt>(), repbase, poolbase, (int)nbmax,
+          h->cnt.as<int>() + C_NFB);
     } else if (h->segy_k > 1) {  // child rows built by verified segments (latency n/K + W rows per thread)
       const int K = h->segy_k;
       CK(h->segoutg.ensure(sizeof(SegG) * (long long)nc * K));
@@ -1033,7 +1057,8 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
     // child frames: the segmented passes with the dd twist search when the child representations are shared
     // by enough singletons for their row loads to coincide (else each lane streams its own representation
     // from HBM and the two-lane kernel is faster: measured C3, 2 singletons per child, vs C4, up to 256)
-    run_rqi(h, ns, nbmax, W, Z, ldz, h->rqi_seg_child && ns >= (long long)h->segchild_min * nc, true);
+    // (single/double: always the segmented passes -- their fixed passes run in binary64, k_rqi2 in dd)
+    run_rqi(h, ns, nbmax, W, Z, ldz, h->sd || (h->rqi_seg_child && ns >= (long long)h->segchild_min * nc), true);
     process_clusters(h, NX.as<Cluster>(), nnx, repbase + nc, poolbase + (long long)nc * nbmax, ipool_top + stot, nbmax,
                      true, W, Z, ldz, kout, level + 1);
     CK(cudaStreamSynchronize(h->stream));
@@ -1384,7 +1409,9 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
   // S9/S10 root singletons
   // short root blocks: the two-lane kernel directly (chains are short; oscillatory vectors such as C1's defeat the
   // segmented twist search, which would hand every singleton over after a wasted pass)
-  run_rqi(h, ns, nbmax, W, Z, ldz, nbmax > h->rqi_seg_min && !h->nonlocal);
+  // (single/double: always the segmented passes, whose fixed passes run in binary64; run_rqi gives them exact
+  // starts where the frames are short or do not contract)
+  run_rqi(h, ns, nbmax, W, Z, ldz, h->sd || (nbmax > h->rqi_seg_min && !h->nonlocal));
   CK(cudaEventRecord(h->ev[4], st));
   // S8 clusters (depth-first, chunked)
   if (ncl > 0) {
@@ -1501,6 +1528,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_FAULT")) h->fault = atoi(s);
     if (const char *s = getenv("MRRR_BMERGE")) h->bmerge = atoi(s) != 0;
     if (const char *s = getenv("MRRR_RQISEGMIN")) h->rqi_seg_min = atoll(s);
+    if (const char *s = getenv("MRRR_SEGSDK")) h->segsd_k = std::max(1, std::min(64, atoi(s)));
     {
       int dev = h->device, maxwin = 0, l2 = 0;
       cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);

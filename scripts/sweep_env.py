@@ -2,7 +2,8 @@
 
     python scripts/sweep_env.py C2 5 "" "MRRR_SEGK=16" "MRRR_SEGK=16 MRRR_SEGW=64"
 
-prints ms per solve (median over reps, CUDA events, L2 flushed between solves) and the phase split."""
+prints ms per solve (median over reps, CUDA events, L2 flushed between solves) and the phase split.
+A config name "sd:<cfg>" runs the single/double realisation (mrrr_seig) on the binary32 copy of <cfg>."""
 import os
 import sys
 
@@ -13,6 +14,9 @@ import torch  # noqa: E402
 import mrrr_inputs as mi  # noqa: E402
 import paper_1401_4950_b200 as m  # noqa: E402
 
+SD = sys.argv[1].startswith("sd:")
+if SD:
+    sys.argv[1] = sys.argv[1][3:]
 if sys.argv[1].startswith("fam:"):  # fam:<family>:<n>, all pairs
     _, fam, nn = sys.argv[1].split(":")
     _d, _e = mi.FAMILIES[fam](int(nn))
@@ -21,9 +25,10 @@ else:
     cfg = mi.CONFIGS[sys.argv[1]]
 reps = int(sys.argv[2])
 d, e = cfg.matrix()
-dt, et = torch.from_numpy(d).cuda(), torch.from_numpy(e).cuda()
-W = torch.empty(cfg.k, dtype=torch.float64, device="cuda")
-Z = torch.empty((cfg.k, cfg.n), dtype=torch.float64, device="cuda")
+fdt = np.float32 if SD else np.float64
+dt, et = torch.from_numpy(d.astype(fdt)).cuda(), torch.from_numpy(e.astype(fdt)).cuda()
+W = torch.empty(cfg.k, dtype=dt.dtype, device="cuda")
+Z = torch.empty((cfg.k, cfg.n), dtype=dt.dtype, device="cuda")
 flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")
 base = dict(os.environ)
 W0 = None
@@ -40,7 +45,7 @@ for spec in sys.argv[3:]:
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         a.record()
-        s.eig(dt, et, cfg.il, cfg.iu, W=W, Z=Z)
+        (s.seig if SD else s.eig)(dt, et, cfg.il, cfg.iu, W=W, Z=Z)
         b.record()
         torch.cuda.synchronize()
         if r >= 2:
@@ -51,8 +56,9 @@ for spec in sys.argv[3:]:
         W0 = Wc.copy()
     t = s.times()
     st = s.stats()
-    print(f"{cfg.name} [{spec or 'default'}] {np.median(ts):.3f} ms (min {min(ts):.3f}) | bis {t['root_bisection']:.2f} "
+    print(f"{'sd:' if SD else ''}{cfg.name} [{spec or 'default'}] {np.median(ts):.3f} ms (min {min(ts):.3f}) | bis {t['root_bisection']:.2f} "
           f"clu {t['clusters']:.2f} sing {t['singletons']:.2f} | neg {t['negcount_ms_per_launch']*1e3:.1f} us x "
           f"{int(t['negcount_launches'])} | rqi {t['rqi_ms_per_launch']:.3f} x {int(t['rqi_launches'])} | "
-          f"rounds {st['rounds']} launches {st['launches']} ho {st['rqi_handover']} {same}", flush=True)
+          f"rounds {st['rounds']} launches {st['launches']} ho {st['rqi_handover']} "
+          f"xgfb {st['xg_fallback_chains']}/{st['xg_fallback_segments']} {same}", flush=True)
     s.close()

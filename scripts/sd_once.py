@@ -1,4 +1,5 @@
-"""One single/double solve of a configuration (binary32 copy of its matrix) -- for ncu launch lists."""
+"""One solve of a configuration for ncu launch lists: `python scripts/sd_once.py C3` (double/dd, mrrr_eig) or
+`python scripts/sd_once.py sd:C2` (single/double, mrrr_seig on the binary32 copy of the matrix)."""
 import sys
 
 import numpy as np
@@ -8,11 +9,13 @@ sys.path.insert(0, __file__.rsplit("/", 2)[0])
 import mrrr_inputs as mi  # noqa: E402
 import paper_1401_4950_b200 as m  # noqa: E402
 
-c = mi.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C2"]
+name = sys.argv[1] if len(sys.argv) > 1 else "sd:C2"
+sd = name.startswith("sd:")
+c = mi.CONFIGS[name[3:] if sd else name]
 d, e = c.matrix()
-d32 = torch.from_numpy(d.astype(np.float32)).cuda()
-e32 = torch.from_numpy(e.astype(np.float32)).cuda()
+dt = np.float32 if sd else np.float64
+d_, e_ = torch.from_numpy(d.astype(dt)).cuda(), torch.from_numpy(e.astype(dt)).cuda()
 s = m.Solver()
-s.seig(d32, e32, c.il, c.iu)
+(s.seig if sd else s.eig)(d_, e_, c.il, c.iu)
 torch.cuda.synchronize()
 print(s.times(), s.stats())

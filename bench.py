@@ -7,6 +7,7 @@ classification, cluster path, singleton RQI + eigenvectors, W/Z stores) of the w
     python bench.py                          # N=1, C2 (random n=8192, all pairs)
     python bench.py --workload C5a --steps 3
     python bench.py --impl reference         # the CPU oracle timed on this host (reference arm)
+    python bench.py --profile sd             # the single/double realisation (mrrr_seig)
     torchrun --nproc-per-node N bench.py --gpus N   # index-range shards, one rank per GPU
 
 Timing: W warm-up steps, then K steps; each step is bracketed by CUDA events on the solver's stream
@@ -156,12 +157,12 @@ def reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(cfg, d, e, ksamp):
+def cpu_baseline(cfg, d, e, ksamp, sd=False):
     import oracle
     threads = os.cpu_count() or 1
-    oracle.mrrr(d, e, 1, 4, threads=threads)
+    oracle.mrrr(d, e, 1, 4, threads=threads, sd=sd)
     t0 = time.perf_counter()
-    r = oracle.mrrr(d, e, 1, ksamp, threads=threads, root_side=1)
+    r = oracle.mrrr(d, e, 1, ksamp, threads=threads, root_side=1, sd=sd)
     t = time.perf_counter() - t0
     assert r.info == 0
     return {"value": ksamp * cfg.n / t, "unit": UNIT, "cores": threads, "kind": "oracle",
@@ -180,7 +181,11 @@ def main():
     ap.add_argument("--cpu-k", type=int, default=8192)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", default="dd", choices=["dd", "sd"],
+                    help="dd: fp64 I/O, double-double inside (the headline); sd: the single/double realisation "
+                         "(binary32 I/O, binary64 inside, gaptol 1e-5; one GPU)")
     args = ap.parse_args()
+    SD = args.profile == "sd"
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -205,6 +210,11 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = mi.CONFIGS[args.workload]
     d_np, e_np = cfg.matrix()
+    if SD:
+        if world > 1:
+            raise SystemExit("--profile sd runs on one GPU")
+        d_np, e_np = d_np.astype(np.float32), e_np.astype(np.float32)
+    fdt = torch.float32 if SD else torch.float64
     n, k = cfg.n, cfg.k
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)
@@ -219,14 +229,14 @@ def main():
         # mrrr_eig_dist bootstraps its own NCCL communicator from one id sent over the torch group
         nccl_ident = pd.nccl_id_broadcast() if backend != "gloo" else None
     else:
-        W = torch.empty(k, dtype=torch.float64, device=dev)
-        Zt = torch.empty((k, n), dtype=torch.float64, device=dev)
+        W = torch.empty(k, dtype=fdt, device=dev)
+        Zt = torch.empty((k, n), dtype=fdt, device=dev)
     flushbuf = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=dev)
 
     def step():
         with torch.cuda.stream(stream):
             if world == 1:
-                solver.eig(d, e, cfg.il, cfg.iu, W=W, Z=Zt)
+                (solver.seig if SD else solver.eig)(d, e, cfg.il, cfg.iu, W=W, Z=Zt)
             elif backend != "gloo":
                 # the C-ABI multi-GPU call: shard solve + the eigenvalue all-gather over NCCL inside libmrrr
                 # (the only collective); Z stays column-sharded
@@ -296,7 +306,7 @@ def main():
                           "k_negcount", launch_ms, f, f_sv))
         if rq_n:
             launch_ms = rq_ms / rq_n
-            f = fl.rqi_flops(stats, n) / nrq
+            f = fl.rqi_flops(stats, n, sd=SD) / nrq
             cands.append(("singleton RQI + eigenvectors (k_twist_lane, k_fixed_chunk, k_zwrite_chunk; k_rqi2 for hand-overs)",
                           "k_fixed_chunk", launch_ms, f, f))
         out = []
@@ -314,10 +324,10 @@ def main():
         roof_other = out[1:] if len(out) > 1 else None
         # whole-solve roofline as the north_star defines it: the slower of (counted FP64 operations, divisions
         # weighted by their issue cost, at peak) and (the Z bytes at HBM bandwidth), against the step time
-        ftot = fl.negcount_flops(stats, n) + fl.rqi_flops(stats, n)
-        ftot_sv = fl.negcount_flops(stats, n, wdiv_survey) + fl.rqi_flops(stats, n)
+        ftot = fl.negcount_flops(stats, n) + fl.rqi_flops(stats, n, sd=SD)
+        ftot_sv = fl.negcount_flops(stats, n, wdiv_survey) + fl.rqi_flops(stats, n, sd=SD)
         t_fp = ftot / (peak * 1e12)
-        zb = 8.0 * k * n
+        zb = (4.0 if SD else 8.0) * k * n
         t_hbm = zb / (pk.get("hbm_gbs", 6550.0) * 1e9)
         t_bound = max(t_fp, t_hbm)
         roof_step = {"bound": "alu" if t_fp >= t_hbm else "hbm", "flops": ftot, "z_bytes": zb,
@@ -335,30 +345,36 @@ def main():
         import torch as _t
         hd = _t.from_numpy(d_np).pin_memory().numpy()
         he = _t.from_numpy(e_np).pin_memory().numpy()
-        hW = _t.empty(k, dtype=_t.float64).pin_memory().numpy()     # page-locked result buffers
-        hZ = _t.empty((k, n), dtype=_t.float64).pin_memory().numpy()
+        tdt = _t.float32 if SD else _t.float64
+        hW = _t.empty(k, dtype=tdt).pin_memory().numpy()     # page-locked result buffers
+        hZ = _t.empty((k, n), dtype=tdt).pin_memory().numpy()
         hs = mrrr.Solver(device=local)
-        hs.eig_host(hd, he, cfg.il, cfg.iu, W=hW, Zt=hZ)
+        hs.eig_host(hd, he, cfg.il, cfg.iu, W=hW, Zt=hZ, single=SD)
         t0 = time.perf_counter()
         reps = max(1, min(args.steps, 3))
         for _ in range(reps):
-            Wh, Zh = hs.eig_host(hd, he, cfg.il, cfg.iu, W=hW, Zt=hZ)
+            Wh, Zh = hs.eig_host(hd, he, cfg.il, cfg.iu, W=hW, Zt=hZ, single=SD)
         te = (time.perf_counter() - t0) / reps
         hs.close()
-        e2e = {"value": k * n / te, "unit": UNIT, "h2d_bytes_per_step": 8 * (2 * n - 1),
-               "d2h_bytes_per_step": 8 * k + 8 * k * n, "ms_per_step": te * 1e3,
-               "path": "mrrr_eig_host: pinned host d, e in, pinned host W, Z out; H2D + solve + D2H timed (wall clock)"}
+        bw = 4 if SD else 8
+        e2e = {"value": k * n / te, "unit": UNIT, "h2d_bytes_per_step": bw * (2 * n - 1),
+               "d2h_bytes_per_step": bw * k + bw * k * n, "ms_per_step": te * 1e3,
+               "path": f"{'mrrr_seig_host' if SD else 'mrrr_eig_host'}: pinned host d, e in, pinned host W, Z out; "
+                       "H2D + solve + D2H timed (wall clock)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, d_np, e_np, min(args.cpu_k, k))
+        cpu = cpu_baseline(cfg, d_np.astype(np.float64), e_np.astype(np.float64), min(args.cpu_k, k), sd=SD)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64+dd", "data": "synthetic",
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64 (binary32 I/O)" if SD else "f64+dd",
+                "data": "synthetic" + (", binary32 copy of the workload's matrix" if SD else ""),
                 "config": {"workload": cfg.name, "n": n, "k": k, "il": cfg.il, "iu": cfg.iu, "desc": cfg.note,
                            "parallelism": f"index shards x{world}" if world > 1 else "single GPU",
+                           "profile": "single/double (mrrr_seig, P:6224-6248, gaptol 1e-5)" if SD
+                           else "double/double-double (mrrr_eig)",
                            "l2": "flushed between steps (256 MiB write, outside the events)"},
                 "gpu_launches": int(launches_per_step) * args.steps,
                 "phases_ms": tphase, "stats": stats, "roofline": roof, "roofline_other": roof_other, "roofline_step": roof_step,

@@ -22,18 +22,24 @@ SLOTS_ZW = 9.0
 SLOTS_QD_SEG = 68.0
 SLOTS_QD_LIGHT = 40.0
 SLOTS_TWIST = 8.0
+# single/double realisation (seg_pass_sd): reciprocal pair 5 + two binary64 quotients (MUL + 2 FMA each) +
+# 2 subtractions + norm recurrence 3 = 16 slots; light pass: one quotient and the fp64 norm = 14
+SLOTS_QD_SD = 16.0
+SLOTS_QD_LIGHT_SD = 14.0
 
 
-def rqi_slots(stats: dict, w_div: float = 0.0) -> float:
+def rqi_slots(stats: dict, w_div: float = 0.0, sd: bool = False) -> float:
     seg = stats.get("twist_rows", 0) > 0 or stats.get("qd_light", 0) > 0
-    return (stats["qd_steps"] * (SLOTS_QD_SEG if seg else SLOTS_QD) + stats["qdg_steps"] * SLOTS_ITER1
+    qd = SLOTS_QD_SD if sd else (SLOTS_QD_SEG if seg else SLOTS_QD)
+    light = SLOTS_QD_LIGHT_SD if sd else SLOTS_QD_LIGHT
+    return (stats["qd_steps"] * qd + stats["qdg_steps"] * SLOTS_ITER1
             + stats["z_steps"] * SLOTS_Z + stats["zw_steps"] * SLOTS_ZW
-            + stats.get("qd_light", 0) * SLOTS_QD_LIGHT + stats.get("twist_rows", 0) * SLOTS_TWIST)
+            + stats.get("qd_light", 0) * light + stats.get("twist_rows", 0) * SLOTS_TWIST)
 
 
-def rqi_flops(stats: dict, n: int, w_div: float = 0.0) -> float:
-    """FMA-equivalent FP64 flops executed by all k_rqi2 launches of the last solve."""
-    return 2.0 * rqi_slots(stats, w_div)
+def rqi_flops(stats: dict, n: int, w_div: float = 0.0, sd: bool = False) -> float:
+    """FMA-equivalent FP64 flops executed by the singleton-RQI kernels of the last solve."""
+    return 2.0 * rqi_slots(stats, w_div, sd)
 
 
 # x-NegCount (Alg. negcountLDL P:7092-7119) per element: dp = d + s (DADD), q = s / dp (one IEEE division),

@@ -276,19 +276,64 @@ __global__ void k_rank(const double *__restrict__ d, const int *__restrict__ sta
   int nbk = starts[blk + 1] - starts[blk];
   keys[i] = (nbk == 1) ? d[i] : __dadd_rn(bis_mid(rlo[i], rhi[i]), binfo[16 * blk]);
 }
-__global__ void k_rank2(const int *__restrict__ starts, int nblk, const double *__restrict__ keys, long long n,
-                        long long il, long long iu, int *colmap) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double ki = keys[i];
-  long long r = 0;
-  for (long long j = 0; j < n; j++) {
-    double kj = keys[j];
-    // positions are ordered by (block, index): ties go to the earlier position
-    r += (kj < ki) || (kj == ki && j < i);
+// multi-block selection (S4/S6): the global rank of position i is its place in the order of (key, position),
+// found by a bitonic sort of (key, position) pairs padded to a power of two N2 (O(N2 log^2 N2) work instead of
+// the O(n^2) all-pairs count).  Stages with partner distance j >= BT/2 run one global pass per (k, j); all
+// smaller distances of a stage run in one shared-memory pass over BT-element tiles.
+constexpr int BT = 2048;  // elements per shared-memory tile (1024 threads)
+__device__ __forceinline__ bool rank_before(double ka, long long ia, double kb, long long ib) {
+  return ka < kb || (ka == kb && ia < ib);
+}
+__global__ void k_rank_init(const double *__restrict__ keys, long long n, long long N2, double *sk, long long *si) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N2) return;
+  sk[i] = (i < n) ? keys[i] : INFINITY;
+  si[i] = i;
+}
+__device__ __forceinline__ void bitonic_cmp(double *sk, long long *si, long long a, long long b, bool up) {
+  const double ka = sk[a], kb = sk[b];
+  const long long ia = si[a], ib = si[b];
+  if (rank_before(kb, ib, ka, ia) == up) {
+    sk[a] = kb; sk[b] = ka;
+    si[a] = ib; si[b] = ia;
   }
-  long long rank = r + 1;
-  colmap[i] = (rank >= il && rank <= iu) ? (int)(rank - il) : -1;
+}
+__global__ void k_bitonic_global(double *sk, long long *si, long long N2, long long k, long long j) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= N2 / 2) return;
+  const long long a = (t / j) * 2 * j + (t % j), b = a + j;
+  bitonic_cmp(sk, si, a, b, (a & k) == 0);
+}
+// substages j = jmax .. 1 of stage k (jmax < BT) on one BT-element tile in shared memory
+__global__ void __launch_bounds__(BT / 2) k_bitonic_tile(double *sk, long long *si, long long N2, long long k0,
+                                                         long long k1, long long jmax) {
+  __shared__ double tk[BT];
+  __shared__ long long ti[BT];
+  const long long base = (long long)blockIdx.x * BT;
+  for (int u = threadIdx.x; u < BT; u += blockDim.x) { tk[u] = sk[base + u]; ti[u] = si[base + u]; }
+  __syncthreads();
+  // stages k = k0, 2 k0, .., k1 (each from its own jmax); the first stage starts at jmax
+  for (long long k = k0; k <= k1; k <<= 1) {
+    for (long long j = (k == k0) ? jmax : k / 2; j >= 1; j >>= 1) {
+      const int t = threadIdx.x;
+      const int a = (int)((t / j) * 2 * j + (t % j)), b = a + (int)j;
+      const bool up = ((base + a) & k) == 0;
+      const double ka = tk[a], kb = tk[b];
+      const long long ia = ti[a], ib = ti[b];
+      if (rank_before(kb, ib, ka, ia) == up) {
+        tk[a] = kb; tk[b] = ka;
+        ti[a] = ib; ti[b] = ia;
+      }
+      __syncthreads();
+    }
+  }
+  for (int u = threadIdx.x; u < BT; u += blockDim.x) { sk[base + u] = tk[u]; si[base + u] = ti[u]; }
+}
+__global__ void k_rank_scatter(const long long *__restrict__ si, long long n, long long il, long long iu, int *colmap) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const long long rank = p + 1;
+  colmap[si[p]] = (rank >= il && rank <= iu) ? (int)(rank - il) : -1;
 }
 
 // self-test 1: div_fast/div_ieee vs __ddiv_rn on random bit patterns (wide exponent range) and specials
@@ -1365,9 +1410,24 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
     k_rank<<<nblocks_for(n, 256), 256, 0, st>>>(d, h->starts.as<int>(), nblk, h->binfo.as<double>(),
                                                  h->rlo.as<double>(), h->rhi.as<double>(), n, keys.as<double>());
     launch_check(h);
-    k_rank2<<<nblocks_for(n, 128), 128, 0, st>>>(h->starts.as<int>(), nblk, keys.as<double>(), n, il, iu,
-                                                  h->colmap.as<int>());
+    // rank = place in the (key, position) order: bitonic sort of the padded pairs
+    long long N2 = BT;
+    while (N2 < n) N2 <<= 1;
+    Buf sk, si;
+    CK(sk.ensure(sizeof(double) * N2));
+    CK(si.ensure(sizeof(long long) * N2));
+    k_rank_init<<<nblocks_for(N2, 256), 256, 0, st>>>(keys.as<double>(), n, N2, sk.as<double>(), si.as<long long>());
+    const unsigned ntile = (unsigned)(N2 / BT);
+    k_bitonic_tile<<<ntile, BT / 2, 0, st>>>(sk.as<double>(), si.as<long long>(), N2, 2, BT, 1);  // tiles sorted
+    for (long long k = 2 * BT; k <= N2; k <<= 1) {
+      long long j = k / 2;
+      for (; j >= BT / 2; j >>= 1)
+        k_bitonic_global<<<nblocks_for(N2 / 2, 256), 256, 0, st>>>(sk.as<double>(), si.as<long long>(), N2, k, j);
+      k_bitonic_tile<<<ntile, BT / 2, 0, st>>>(sk.as<double>(), si.as<long long>(), N2, k, k, j);
+    }
+    k_rank_scatter<<<nblocks_for(n, 256), 256, 0, st>>>(si.as<long long>(), n, il, iu, h->colmap.as<int>());
     launch_check(h);
+    CK(cudaStreamSynchronize(st));
     CK(cudaStreamSynchronize(st));
     keys.release();
   }

@@ -157,6 +157,24 @@ def test_parity_split_matrix(torch_cuda, sel):
     check_tol(d, e, g["W"], g["Z"], r.W, 2.0)
 
 
+@pytest.mark.parametrize("sel", [(1, 6000), (2500, 2600), (5999, 6000)])
+def test_parity_many_blocks(torch_cuda, sel):
+    # 6000 rows in ~700 blocks of 1..16 rows (repeated diagonal values across blocks: ties broken by position):
+    # the multi-block ranking (bitonic sort of (key, position) over 8192 padded entries: tile and global passes)
+    # must select exactly the oracle's columns
+    rng = np.random.default_rng(17)
+    n = 6000
+    d = np.round(rng.uniform(-1, 1, n), 2)
+    e = rng.uniform(-1, 1, n - 1)
+    cuts = np.cumsum(rng.integers(1, 17, n))
+    e[cuts[cuts < n - 1] - 1] = 0.0
+    g = gpu_solve(torch_cuda, d, e, *sel)
+    r = oracle.mrrr(d, e, *sel)
+    assert r.nblocks > 500
+    check_integers(g, r)
+    check_tol(d, e, g["W"], g["Z"], r.W, 4.0)
+
+
 def test_parity_split_threshold_exact(torch_cuda):
     # |beta| exactly at eps sqrt(n) ||T||_1 splits; one ulp above does not
     d = np.array([3.0, 1.0, 1.0, 1.0])

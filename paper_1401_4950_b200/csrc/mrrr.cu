@@ -140,11 +140,11 @@ struct mrrr_ctx {
   Buf gpart;                              // k_root_gersh partial bounds
   Buf segouty, segfby, segoutx, segoutg;  // segmented y-NegCount / many-representation x-NegCount / growth
   Buf rqst, rqrec, hand;                  // segmented RQI state, segment records, handed-over singletons
-  std::vector<cudaEvent_t> rev;           // events around device-driven rounds
   Buf nodesA, nodesB, counts, ex, excounts, exmap, bnA, bnB, sing, clusA, clusB, ss, gval, valid, cseg, bnoff,
       ipool_lo, ipool_hi, yref_lo, yref_hi, wsA, wsB, stats, cnt, ddepth, dgf, dgl, dflo, dfhi, hd, he, hW, hZ, zmeta,
       hd2, sdin, sdW, sdZ, sdhin, sdhW, sdhZ, segsd;
   int *h_cnt = nullptr;  // pinned counters
+  std::vector<int> h_rounds = std::vector<int>(258);  // node counts of the device-driven rounds
 
   // results of the last call
   long long last_n = 0, last_k = 0;
@@ -153,14 +153,18 @@ struct mrrr_ctx {
   double times[12] = {0};
   std::vector<int> h_starts;
   cudaEvent_t ev[8];
-  cudaEvent_t rq0, rq1;
   ncclComm_t comm = nullptr;   // mrrr_eig_dist communicator (created on first use)
   char comm_id[128] = {0};
   int comm_rank = -1, comm_world = 0;
   Buf dWl, dmeta, dmetas, dpad, dparts;  // mrrr_eig_dist staging
   double rqi_ms = 0, neg_ms = 0;
+  // kernel timing without host round trips: event pairs recorded on the stream during the solve, read only when
+  // mrrr_get_times asks (cudaEventElapsedTime between rounds left the GPU idle: ~4 us per call, 30 per C2 solve)
+  std::vector<cudaEvent_t> tev;
+  int ntev = 0;
+  std::vector<std::pair<int, int>> tneg, trq;
+  bool times_dirty = false;
   long long neg_launches = 0, neg_len = 0;
-  cudaEvent_t nc0, nc1;
   long long rqi_launches = 0;
   long long host_rounds = 0, host_launches = 0;
 };
@@ -381,6 +385,18 @@ void launch_check(mrrr_t h) {
   CK(cudaGetLastError());
 }
 
+// record the next pool event on the stream; returns its index (the pool grows on first use)
+int tev_rec(mrrr_t h) {
+  if (h->ntev >= (int)h->tev.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    h->tev.push_back(e);
+  }
+  const int i = h->ntev++;
+  CK(cudaEventRecord(h->tev[i], h->stream));
+  return i;
+}
+
 // NegCount chains: node grid points then explicit (rep, sigma) chains; CH chains per thread (x path)
 template <bool Y>
 void launch_negcount(mrrr_t h, const Node *nodes, int nnode, int m, int nex, const Node *nodesP = nullptr,
@@ -477,11 +493,7 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
   CK(h->rnd.ensure(sizeof(int) * 2 * (MAXR + 2)));
   CK(h->counts.ensure(sizeof(int) * maxch));
   CK(h->segout.ensure(sizeof(SegOut) * maxch * K));
-  while ((int)h->rev.size() < 2 * MAXR) {
-    cudaEvent_t e;
-    CK(cudaEventCreate(&e));
-    h->rev.push_back(e);
-  }
+  std::vector<std::pair<int, int>> rp;  // timing events of each round
   int *nn = h->rnd.as<int>(), *nfb = nn + MAXR + 2;
   CK(cudaMemsetAsync(h->rnd.p, 0, sizeof(int) * 2 * (MAXR + 2), h->stream));
   k_set_int<<<1, 1, 0, h->stream>>>(nn, nnode);
@@ -501,11 +513,11 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
     const unsigned g1 = (unsigned)(chmax / 128 + 1);
     for (int b = 0; b < RB && r < MAXR; b++, r++) {
       Node *in = (r & 1) ? nxt : cur, *out = (r & 1) ? cur : nxt;
-      CK(cudaEventRecord(h->rev[2 * r], h->stream));
+      const int ea = tev_rec(h);
       k_negcount_seg<1><<<gseg, 128, 2 * SEG_TILE * sizeof(double2), h->stream>>>(
           in, 0, 0, nullptr, 0, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L, h->seg_w, h->segout.as<SegOut>(),
           nn + r, mmax, h->target_chains);
-      CK(cudaEventRecord(h->rev[2 * r + 1], h->stream));
+      rp.push_back({ea, tev_rec(h)});
       // junction walk (careful tail inline) and shared-tree update in one launch
       k_seg_round<<<g1 * 4, 32, 0, h->stream>>>(0, 0, K, h->segout.as<SegOut>(), h->counts.as<int>(), in,
                                              h->reps.as<RepDesc>(), h->mx.as<double2>(), L, out, nn + r + 1, out_lo,
@@ -513,20 +525,17 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
       launch_check(h);
       h->host_launches += 3;
     }
-    int left = 0;
-    CK(cudaMemcpyAsync(&left, nn + r, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    // node counts of every round so far (the last one decides; the others count the rounds that ran)
+    CK(cudaMemcpyAsync(h->h_rounds.data(), nn, sizeof(int) * (r + 1), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    const int left = h->h_rounds[r];
     if (left == 0) break;
     known = left;
     if (r >= MAXR) { g_last_cuda_error = "bisection did not converge in 256 rounds"; throw Err{MRRR_ERR_CUDA}; }
   }
-  std::vector<int> hn(r + 1);
-  CK(cudaMemcpy(hn.data(), nn, sizeof(int) * (r + 1), cudaMemcpyDeviceToHost));
   for (int i = 0; i < r; i++) {
-    if (hn[i] == 0) break;
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, h->rev[2 * i], h->rev[2 * i + 1]));
-    h->neg_ms += ms;
+    if (h->h_rounds[i] == 0) break;
+    h->tneg.push_back(rp[i]);
     h->neg_launches++;
     h->host_rounds++;
   }
@@ -573,7 +582,7 @@ void run_bisection_grouped(mrrr_t h, int nnode, double *out_lo, double *out_hi, 
     const long long nch = (long long)nnode * P;
     CK(h->counts.ensure(std::max<long long>(nch, 1) * sizeof(int)));
     zero_counters(h);
-    CK(cudaEventRecord(h->nc0, h->stream));
+    const int ea = tev_rec(h);
     if (per_cta) {
       k_negcount_grp<<<ncta, 128, 2 * NEG_TILE * sizeof(double2), h->stream>>>(
           h->nodesK.as<Node>(), m, h->repoff.as<int>(), h->repcta.as<int>(), nrep, h->reps.as<RepDesc>(),
@@ -582,7 +591,7 @@ void run_bisection_grouped(mrrr_t h, int nnode, double *out_lo, double *out_hi, 
     } else {
       launch_negcount<false>(h, h->nodesK.as<Node>(), nnode, m, 0);
     }
-    CK(cudaEventRecord(h->nc1, h->stream));
+    h->tneg.push_back({ea, tev_rec(h)});
     k_bisect_update<<<nblocks_for((long long)nnode << m, 128), 128, 0, h->stream>>>(
         h->nodesK.as<Node>(), nnode, m, h->counts.as<int>(), nxt, h->cnt.as<int>() + C_NNEXT, out_lo, out_hi, rtol,
         alg);
@@ -590,9 +599,6 @@ void run_bisection_grouped(mrrr_t h, int nnode, double *out_lo, double *out_hi, 
     read_counters(h);
     h->host_rounds++;
     h->stats_h[ST_NEGX] += nch;
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, h->nc0, h->nc1));
-    h->neg_ms += ms;
     h->neg_launches++;
     nnode = h->h_cnt[C_NNEXT];
     std::swap(cur, nxt);
@@ -623,7 +629,8 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
     int nex = first ? nverify : 0;
     bool fused = false;  // the segmented round's update ran inside k_seg_round
     zero_counters(h);
-    CK(cudaEventRecord(h->nc0, h->stream));
+    const int ea = tev_rec(h);
+    int eb = -1;
     if (seg_on) {
       // segmented chains (kernels_guided.cuh): K concurrent segments per NegCount, verified bit-exact.
       // Rounds with few chains (one point per node) cut them into more segments, so that about
@@ -646,7 +653,7 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
             cur, nnode, m, h->ex.as<ExplicitChain>(), nex, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L,
             h->seg_w, h->segout.as<SegOut>(), nullptr, 0, 0);
       launch_check(h);
-      CK(cudaEventRecord(h->nc1, h->stream));
+      eb = tev_rec(h);
       if (nex == 0) {  // junction walk and shared-tree update in one launch
         k_seg_round<<<nblocks_for(nnode, 32), 32, 0, h->stream>>>(
             nnode, m, K, h->segout.as<SegOut>(), h->counts.as<int>(), cur, h->reps.as<RepDesc>(), h->mx.as<double2>(),
@@ -663,7 +670,7 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
       launch_check(h);
     } else {
       launch_negcount<Y>(h, cur, nnode, m, nex);
-      CK(cudaEventRecord(h->nc1, h->stream));
+      eb = tev_rec(h);
     }
     if (nex > 0) {
       k_root_verify<<<nblocks_for(nbl, 128), 128, 0, h->stream>>>(blist_dev, nbl, h->starts.as<int>(),
@@ -690,9 +697,7 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
       h->nonlocal = true;
     }
     if (!Y) {
-      float ms = 0;
-      CK(cudaEventElapsedTime(&ms, h->nc0, h->nc1));
-      h->neg_ms += ms;
+      h->tneg.push_back({ea, eb});
       h->neg_launches++;
     }
     if (nex > 0 && h->h_cnt[C_NEX] > 0) { *restart = true; return; }
@@ -793,7 +798,7 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
   bool diag = (h->flags & MRRR_KEEP_DIAG) != 0;
   for (long long b0 = 0; b0 < ns; b0 += batch) {
     long long nb = std::min<long long>(batch, ns - b0);
-    CK(cudaEventRecord(h->rq0, h->stream));
+    const int rq0 = tev_rec(h);
     CK(h->zmeta.ensure(sizeof(ZMeta) * stride));
     const Singleton *sgb = h->sing.as<Singleton>() + b0;
     int nold = (int)nb;
@@ -889,11 +894,7 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
           h->zmeta.as<ZMeta>(), Z, ldz);
     }
     launch_check(h);
-    CK(cudaEventRecord(h->rq1, h->stream));
-    CK(cudaEventSynchronize(h->rq1));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, h->rq0, h->rq1));
-    h->rqi_ms += ms;
+    h->trq.push_back({rq0, tev_rec(h)});
     h->rqi_launches++;
   }
   l2_pin_reps(h, false);
@@ -1153,6 +1154,10 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
   h->rqi_launches = 0;
   h->neg_ms = 0;
   h->neg_launches = 0;
+  h->ntev = 0;
+  h->tneg.clear();
+  h->trq.clear();
+  h->times_dirty = false;
   memset(h->stats_h, 0, sizeof(h->stats_h));
   bool diag = (h->flags & MRRR_KEEP_DIAG) != 0;
 
@@ -1503,17 +1508,7 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
   h->stats_h[ST_ROUNDS] = h->host_rounds;
   h->stats_h[ST_LAUNCHES] = h->host_launches;
   h->stats_h[ST_NBLK] = nblk;
-  float ms;
-  CK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[5])); h->times[0] = ms;
-  CK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1])); h->times[1] = ms;
-  CK(cudaEventElapsedTime(&ms, h->ev[1], h->ev[2])); h->times[2] = ms;
-  CK(cudaEventElapsedTime(&ms, h->ev[2], h->ev[3])); h->times[3] = ms;
-  CK(cudaEventElapsedTime(&ms, h->ev[4], h->ev[5])); h->times[4] = ms;
-  CK(cudaEventElapsedTime(&ms, h->ev[3], h->ev[4])); h->times[5] = ms;
-  h->times[6] = h->rqi_launches ? h->rqi_ms / h->rqi_launches : 0.0;
-  h->times[7] = (double)h->rqi_launches;
-  h->times[8] = h->neg_launches ? h->neg_ms / h->neg_launches : 0.0;
-  h->times[9] = (double)h->neg_launches;
+  h->times_dirty = true;  // phase and kernel times are read from the events by mrrr_get_times
   return 0;
 }
 
@@ -1599,10 +1594,6 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
       cudaGetLastError();
     }
     for (auto &ev : h->ev) CK(cudaEventCreate(&ev));
-    CK(cudaEventCreate(&h->rq0));
-    CK(cudaEventCreate(&h->rq1));
-    CK(cudaEventCreate(&h->nc0));
-    CK(cudaEventCreate(&h->nc1));
     CK(cudaMallocHost(&h->h_cnt, sizeof(int) * C_NCOUNTERS));
   } catch (Err &er) {
     delete h;
@@ -1907,6 +1898,29 @@ int mrrr_get_stats(mrrr_t h, int64_t *s, int32_t ns) {
 
 int mrrr_get_times(mrrr_t h, double *ms, int32_t nt) {
   if (!h || !ms) return -1;
+  if (h->times_dirty) {  // the last solve's events (complete: the solve synchronized its stream before returning)
+    auto el = [&](cudaEvent_t a, cudaEvent_t b) {
+      float v = 0.0f;
+      cudaEventElapsedTime(&v, a, b);
+      return (double)v;
+    };
+    h->times[0] = el(h->ev[0], h->ev[5]);
+    h->times[1] = el(h->ev[0], h->ev[1]);
+    h->times[2] = el(h->ev[1], h->ev[2]);
+    h->times[3] = el(h->ev[2], h->ev[3]);
+    h->times[4] = el(h->ev[4], h->ev[5]);
+    h->times[5] = el(h->ev[3], h->ev[4]);
+    h->neg_ms = 0.0;
+    for (auto &p : h->tneg) h->neg_ms += el(h->tev[p.first], h->tev[p.second]);
+    h->rqi_ms = 0.0;
+    for (auto &p : h->trq) h->rqi_ms += el(h->tev[p.first], h->tev[p.second]);
+    h->times[6] = h->rqi_launches ? h->rqi_ms / h->rqi_launches : 0.0;
+    h->times[7] = (double)h->rqi_launches;
+    h->times[8] = h->neg_launches ? h->neg_ms / h->neg_launches : 0.0;
+    h->times[9] = (double)h->neg_launches;
+    cudaGetLastError();
+    h->times_dirty = false;
+  }
   for (int i = 0; i < nt && i < 12; i++) ms[i] = h->times[i];
   return 0;
 }
@@ -1989,12 +2003,11 @@ int mrrr_destroy(mrrr_t h) {
                  &h->excounts, &h->exmap, &h->bnA, &h->bnB, &h->sing, &h->clusA, &h->clusB, &h->ss, &h->gval,
                  &h->valid, &h->cseg, &h->bnoff, &h->ipool_lo, &h->ipool_hi, &h->yref_lo, &h->yref_hi, &h->wsA,
                  &h->wsB, &h->stats, &h->cnt, &h->ddepth, &h->dgf, &h->dgl, &h->dflo, &h->dfhi,
-                 &h->hd, &h->he, &h->hW, &h->hZ, &h->zmeta, &h->hd2};
+                 &h->hd, &h->he, &h->hW, &h->hZ, &h->zmeta, &h->hd2,
+                 &h->sdin, &h->sdW, &h->sdZ, &h->sdhin, &h->sdhW, &h->sdhZ, &h->segsd};
   for (Buf *b : bufs) b->release();
   for (auto &ev : h->ev) cudaEventDestroy(ev);
-  for (auto &ev : h->rev) cudaEventDestroy(ev);
-  cudaEventDestroy(h->rq0);
-  cudaEventDestroy(h->rq1);
+  for (auto &ev : h->tev) cudaEventDestroy(ev);
   if (h->comm && nccl().ok) nccl().destroy(h->comm);
   h->dWl.release();
   h->dmeta.release();

@@ -157,12 +157,12 @@ def reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(cfg, d, e, ksamp, sd=False):
+def cpu_baseline(cfg, d, e, ksamp, sd=False, es=False):
     import oracle
     threads = os.cpu_count() or 1
-    oracle.mrrr(d, e, 1, 4, threads=threads, sd=sd)
+    oracle.mrrr(d, e, 1, 4, threads=threads, sd=sd, early_stop=es)
     t0 = time.perf_counter()
-    r = oracle.mrrr(d, e, 1, ksamp, threads=threads, root_side=1, sd=sd)
+    r = oracle.mrrr(d, e, 1, ksamp, threads=threads, root_side=1, sd=sd, early_stop=es)
     t = time.perf_counter() - t0
     assert r.info == 0
     return {"value": ksamp * cfg.n / t, "unit": UNIT, "cores": threads, "kind": "oracle",
@@ -184,6 +184,9 @@ def main():
     ap.add_argument("--profile", default="dd", choices=["dd", "sd"],
                     help="dd: fp64 I/O, double-double inside (the headline); sd: the single/double realisation "
                          "(binary32 I/O, binary64 inside, gaptol 1e-5; one GPU)")
+    ap.add_argument("--early-stop", action="store_true",
+                    help="early classification stop of the root bisection (MRRR_EARLY_STOP, S5', P:3204-3210, "
+                         "DESIGN.md A-41; SURVEY 8(f3)); the oracle legs run the same rule")
     args = ap.parse_args()
     SD = args.profile == "sd"
 
@@ -218,7 +221,8 @@ def main():
     n, k = cfg.n, cfg.k
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)
-    solver = mrrr.Solver(device=local, stream=stream.cuda_stream)
+    ES = args.early_stop
+    solver = mrrr.Solver(device=local, stream=stream.cuda_stream, early_stop=ES)
     d = torch.from_numpy(d_np).to(dev)
     e = torch.from_numpy(e_np).to(dev)
     # shard of the index range: contiguous blocks per rank, first-index group ownership
@@ -348,7 +352,7 @@ def main():
         tdt = _t.float32 if SD else _t.float64
         hW = _t.empty(k, dtype=tdt).pin_memory().numpy()     # page-locked result buffers
         hZ = _t.empty((k, n), dtype=tdt).pin_memory().numpy()
-        hs = mrrr.Solver(device=local)
+        hs = mrrr.Solver(device=local, early_stop=ES)
         hs.eig_host(hd, he, cfg.il, cfg.iu, W=hW, Zt=hZ, single=SD)
         t0 = time.perf_counter()
         reps = max(1, min(args.steps, 3))
@@ -364,7 +368,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, d_np.astype(np.float64), e_np.astype(np.float64), min(args.cpu_k, k), sd=SD)
+        cpu = cpu_baseline(cfg, d_np.astype(np.float64), e_np.astype(np.float64), min(args.cpu_k, k), sd=SD, es=ES)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -375,6 +379,7 @@ def main():
                            "parallelism": f"index shards x{world}" if world > 1 else "single GPU",
                            "profile": "single/double (mrrr_seig, P:6224-6248, gaptol 1e-5)" if SD
                            else "double/double-double (mrrr_eig)",
+                           "early_stop": ES,
                            "l2": "flushed between steps (256 MiB write, outside the events)"},
                 "gpu_launches": int(launches_per_step) * args.steps,
                 "phases_ms": tphase, "stats": stats, "roofline": roof, "roofline_other": roof_other, "roofline_step": roof_step,

@@ -51,6 +51,16 @@ typedef struct mrrr_ctx *mrrr_t;
 #define MRRR_ERR_PEER 7       /* mrrr_eig_dist: this rank succeeded but another rank failed */
 
 #define MRRR_KEEP_DIAG 1u     /* keep integer/interval diagnostics for mrrr_get_diag */
+/* Early classification stop of the root bisection (S5'): "only sufficient accuracy to classify
+ * eigenvalues into well-separated and clustered is needed ... Depending on the absolute gap of the eigenvalue,
+ * the refinement can be stopped earlier on" (sec. 3.2.2 remark (3); A-41).
+ * Every index is bisected to rtol_c = max(rtol, 2^-(10 + ceil(log2 n))) first; index j (not the first or last
+ * of its block) stops there when both of its neighbour pairs are already classification boundaries and its
+ * width is at most 2^-7 of its absolute gap; the others continue to rtol = 1e-2 gaptol.  Cluster boundaries
+ * are those of the default solve; stopped singletons start their RQI from the coarser interval.  Honoured by
+ * mrrr_eig / mrrr_seig (and their _host forms); shards and mrrr_eig_dist apply the same rule (it depends only
+ * on the indices j-1, j, j+1). */
+#define MRRR_EARLY_STOP 2u
 
 /* Options (all fields may be zero = default). */
 typedef struct {
@@ -59,7 +69,7 @@ typedef struct {
   void *stream;       /* cudaStream_t used for all work; NULL: a library-owned stream */
   double gaptol;      /* classification threshold; <= 0: 1e-10 */
   uint64_t seed;      /* key of the root perturbation stream; 0: default */
-  uint32_t flags;     /* MRRR_KEEP_DIAG */
+  uint32_t flags;     /* MRRR_KEEP_DIAG | MRRR_EARLY_STOP */
   uint32_t reserved;
   int64_t ws_limit;   /* soft cap on workspace bytes; <= 0: 60% of free device memory */
 } mrrr_opts;
@@ -167,8 +177,9 @@ int mrrr_shard_owner(const int32_t *gstart, int64_t n, int64_t il, int64_t iu, i
  * 30 segmented RQI passes repeated with an 8x longer warm-up after a failed junction, 31 singletons whose
  * last two-lane Getvec ran the careful IEEE pass (zero pivots / special values), 32 segmented
  * many-representation x-NegCount chains (child bisection) whose junctions did not all verify, 33 segments those
- * chains re-ran sequentially. */
-#define MRRR_NSTATS 34
+ * chains re-ran sequentially, 34 root indices the early classification stop (MRRR_EARLY_STOP) left at the
+ * stage-1 tolerance. */
+#define MRRR_NSTATS 35
 int mrrr_get_stats(mrrr_t h, int64_t *stats, int32_t nstats);
 
 /* Diagnostics of the last call made with MRRR_KEEP_DIAG (host buffers owned

@@ -24,7 +24,7 @@ CFLAGS = ["-O2", "-std=gnu11", "-fopenmp", "-fPIC", "-shared", "-ffp-contract=of
 
 STAT_NAMES = ["d_max", "n_clusters", "largest_cluster", "uncertified", "shift_attempts", "rqi_iters",
               "rqi_fallbacks", "bracket_fixes", "root_backoffs", "failed", "negcount_x", "negcount_y",
-              "getvec_calls", "zero_pivots"]
+              "getvec_calls", "zero_pivots", "early_stops"]
 
 
 def build(force: bool = False) -> str:
@@ -36,7 +36,7 @@ def build(force: bool = False) -> str:
 
 class _Opts(C.Structure):
     _fields_ = [("gaptol", C.c_double), ("seed", C.c_uint64), ("root_side", C.c_int32), ("threads", C.c_int32),
-                ("roots_only", C.c_int32)]
+                ("roots_only", C.c_int32), ("early_stop", C.c_int32)]
 
 
 class _Diag(C.Structure):
@@ -116,6 +116,10 @@ def lib(sd: bool = False):
         L.oracle_rqi.restype = None
         L.oracle_rqi.argtypes = [_i64, C.c_void_p, C.c_void_p, _i64, C.c_double, C.c_double, C.c_double, _dp,
                                  C.c_void_p, C.POINTER(_i64), C.POINTER(_i64)]
+        L.oracle_es_rtol.restype = C.c_double
+        L.oracle_es_rtol.argtypes = [_i64, C.c_double]
+        L.oracle_es_stop.restype = C.c_int
+        L.oracle_es_stop.argtypes = [C.c_double] * 7
         L.oracle_root_x_from.restype = C.c_int
         L.oracle_root_x_from.argtypes = [_i64, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_double, _dp,
                                          C.c_void_p, C.c_void_p, C.POINTER(C.c_int)]
@@ -152,12 +156,14 @@ class OracleResult:
 
 
 def mrrr(d, e, il: int | None = None, iu: int | None = None, *, gaptol: float | None = None, seed: int = 0,
-         root_side: int = 0, threads: int = 0, roots_only: bool = False, sd: bool = False) -> OracleResult:
+         root_side: int = 0, threads: int = 0, roots_only: bool = False, sd: bool = False,
+         early_stop: bool = False) -> OracleResult:
     """Eigenpairs il..iu (1-based, inclusive) of the tridiagonal (d, e) by the oracle.  roots_only: stop after
     the root bisection (S1-S5): only nblocks/block_start/mu/side/root_lo/root_hi/root_gstart are filled.
     sd: the single/double realisation (liboracle_sd.so, gaptol 1e-5 by default); its inputs are
     the binary32 values (pass them as float32 or as their exact float64 images) and W, Z come back in float64
-    before the final binary32 rounding (float32 of them is the realisation's output)."""
+    before the final binary32 rounding (float32 of them is the realisation's output).  early_stop: the early
+    classification stop of the root bisection (S5', A-41)."""
     d = _f64(d)
     n = d.size
     e = _f64(e) if n > 1 else np.zeros(1)
@@ -184,7 +190,7 @@ def mrrr(d, e, il: int | None = None, iu: int | None = None, *, gaptol: float | 
     fhi = np.zeros(k)
     st = np.zeros(16, np.int64)
     dg = _Diag(*[_ptr(a) for a in (nblocks, bstart, mu, side, rlo, rhi, rgs, depth, gf, gl, flo, fhi, st)])
-    op = _Opts(gaptol, seed, root_side, threads, int(roots_only))
+    op = _Opts(gaptol, seed, root_side, threads, int(roots_only), int(early_stop))
     info = L.oracle_mrrr(n, _ptr(d), _ptr(e), il, iu, C.byref(op), _ptr(W), _ptr(Z), n, C.byref(dg))
     nbk = int(nblocks[0])
     return OracleResult(W=W, Z=Z.T, info=info, nblocks=nbk, block_start=bstart[:nbk + 1].copy(),
@@ -194,6 +200,16 @@ def mrrr(d, e, il: int | None = None, iu: int | None = None, *, gaptol: float | 
 
 
 # ---------------------------------------------------------------- unit wrappers
+def es_rtol(n: int, rtol: float, *, sd: bool = False) -> float:
+    """Stage-1 tolerance of the early classification stop (S5', A-41)."""
+    return lib(sd).oracle_es_rtol(n, rtol)
+
+
+def es_stop(left, mid, right, gaptol: float, *, sd: bool = False) -> bool:
+    """The early-stop test of an index from the stage-1 intervals (lo, hi) of it and its two neighbours."""
+    return bool(lib(sd).oracle_es_stop(left[0], left[1], mid[0], mid[1], right[0], right[1], gaptol))
+
+
 def xi(seed: int, idx: int, *, sd: bool = False) -> float:
     return lib(sd).oracle_xi(seed, idx)
 

@@ -83,7 +83,7 @@ typedef __float128 yreal;      /* double/quadruple realisation */
 enum {
   ST_DMAX = 0, ST_NCLUSTERS, ST_LARGEST, ST_UNCERTIFIED, ST_ATTEMPTS, ST_RQI_ITERS,
   ST_RQI_FALLBACK, ST_BRACKET_FIX, ST_ROOT_BACKOFF, ST_FAILED, ST_NEGX, ST_NEGY,
-  ST_GETVEC, ST_ZPIV, ST_NSTATS = 16
+  ST_GETVEC, ST_ZPIV, ST_ESTOP, ST_NSTATS = 16
 };
 
 typedef struct {
@@ -92,6 +92,7 @@ typedef struct {
   int32_t root_side;  /* 0 auto (S3 rule), 1 left, 2 right */
   int32_t threads;    /* 0 -> OpenMP default */
   int32_t roots_only; /* 1: stop after S5 (split, roots, root bisection of the computed set; diagnostics only) */
+  int32_t early_stop; /* 1: early classification stop of the root bisection (S5', A-41) */
 } oracle_opts;
 
 typedef struct {      /* every pointer optional */
@@ -816,6 +817,7 @@ typedef struct {
   double mu, gl, gu;
   rep_t *root;
   double *lo, *hi;   /* [nb+2], 1-based, NaN = not computed */
+  double *s1lo, *s1hi; /* [nb+2] stage-1 intervals of the early stop (S5'), NaN = not computed */
   int64_t ca, cb;    /* computed range */
   int64_t jl, ju;    /* selected range (ju < jl: none) */
   int32_t *colmap;   /* [nb+2] */
@@ -835,6 +837,56 @@ static void root_bisect_one(blk_t *B, int64_t j, double rtol) {
   oracle_bisect_x(B->nb, B->root->dx, B->root->dllx, j, rtol, &lo, &hi);
   B->lo[j] = lo;
   B->hi[j] = hi;
+}
+
+/* ------------------------------------------------------------------------- */
+/* S5' Early classification stop: "only sufficient accuracy to  */
+/* classify eigenvalues into well-separated and clustered is needed ...        */
+/* Depending on the absolute gap of the eigenvalue, the refinement can be      */
+/* stopped earlier on" (sec. 3.2.2 remark (3); A-41).   */
+/* Stage 1 bisects index j to rtol_c = max(rtol, 2^-(10 + ceil(log2 n)));      */
+/* j (2 <= j <= nb-1) stops there when both neighbour pairs are already        */
+/* classification boundaries (reldist >= gaptol) and its width is */
+/* at most 2^-7 of its absolute gap; every other index continues from its      */
+/* stage-1 interval to rtol -- the same bisection path, hence the same final   */
+/* interval as without the stop.  A stopped interval contains the stage-1      */
+/* intervals' final refinements of the full run, so reldist only grows: the    */
+/* cluster boundaries are those of the full run.                               */
+/* ------------------------------------------------------------------------- */
+double oracle_es_rtol(int64_t n, double rtol) {
+  int e = 0;
+  while (e < 62 && ((int64_t)1 << e) < n) e++;   /* ceil(log2 n) */
+  return dmax(rtol, ldexp(1.0, -(10 + e)));
+}
+/* the stop test of index j from the stage-1 intervals of j-1, j, j+1 */
+int oracle_es_stop(double llo, double lhi, double clo, double chi, double rlo, double rhi, double gaptol) {
+  if (!oracle_is_boundary(llo, lhi, clo, chi, gaptol) || !oracle_is_boundary(clo, chi, rlo, rhi, gaptol)) return 0;
+  double gap = dmin(clo - lhi, rlo - chi);
+  return (chi - clo) <= ldexp(gap, -7);
+}
+static void stage1_one(blk_t *B, int64_t j, double rtol_c) {
+  if (j < 1 || j > B->nb || !isnan(B->s1lo[j])) return;
+  double lo = B->left ? 0.0 : -B->hi[0], hi = B->left ? B->hi[0] : 0.0;
+  oracle_bisect_x(B->nb, B->root->dx, B->root->dllx, j, rtol_c, &lo, &hi);
+  B->s1lo[j] = lo;
+  B->s1hi[j] = hi;
+}
+/* stage 2 of index j (its stage-1 interval and its neighbours' computed): stop, or continue to rtol */
+static void stage2_one(blk_t *B, int64_t j, double rtol, double gaptol) {
+  double lo = B->s1lo[j], hi = B->s1hi[j];
+  if (j >= 2 && j <= B->nb - 1 &&
+      oracle_es_stop(B->s1lo[j - 1], B->s1hi[j - 1], lo, hi, B->s1lo[j + 1], B->s1hi[j + 1], gaptol)) {
+    STAT_ADD(ST_ESTOP, 1);
+  } else {
+    oracle_bisect_x(B->nb, B->root->dx, B->root->dllx, j, rtol, &lo, &hi);
+  }
+  B->lo[j] = lo;
+  B->hi[j] = hi;
+}
+/* one index with the early stop (guard extension, one at a time) */
+static void root_bisect_es(blk_t *B, int64_t j, double rtol_c, double rtol, double gaptol) {
+  for (int64_t x = j - 1; x <= j + 1; x++) stage1_one(B, x, rtol_c);
+  stage2_one(B, j, rtol, gaptol);
 }
 
 static int mrrr_scaled(int64_t n, const double *d, const double *e, int64_t il, int64_t iu, const oracle_opts *op,
@@ -879,6 +931,8 @@ static int mrrr_scaled(int64_t n, const double *d, const double *e, int64_t il, 
   int force = op ? op->root_side : 0;
   if (op && op->threads > 0) omp_set_num_threads(op->threads);
   double rtol = 1e-2 * gaptol;      /* P:3204-3207, P:6228 */
+  int es = op ? op->early_stop : 0;  /* S5' (A-41) */
+  double rtol_c = es ? oracle_es_rtol(n, rtol) : rtol;
   int64_t k = iu - il + 1;
   memset(g_stats, 0, sizeof(g_stats));
 
@@ -900,7 +954,12 @@ static int mrrr_scaled(int64_t n, const double *d, const double *e, int64_t il, 
     B[b].lo = malloc(sizeof(double) * (nb + 2));
     B[b].hi = malloc(sizeof(double) * (nb + 2));
     B[b].colmap = malloc(sizeof(int32_t) * (nb + 2));
-    for (int64_t j = 0; j < nb + 2; j++) { B[b].lo[j] = B[b].hi[j] = NAN; B[b].colmap[j] = -1; }
+    B[b].s1lo = malloc(sizeof(double) * (nb + 2));
+    B[b].s1hi = malloc(sizeof(double) * (nb + 2));
+    for (int64_t j = 0; j < nb + 2; j++) {
+      B[b].lo[j] = B[b].hi[j] = NAN; B[b].colmap[j] = -1;
+      B[b].s1lo[j] = B[b].s1hi[j] = NAN;
+    }
     if (single) { B[b].jl = il; B[b].ju = iu; }
     else { B[b].jl = 1; B[b].ju = nb; }
   }
@@ -945,16 +1004,27 @@ static int mrrr_scaled(int64_t n, const double *d, const double *e, int64_t il, 
   for (int64_t b = 0; b < nblk; b++) {
     blk_t *X = &B[b];
     if (X->nb == 1) continue;
+    if (es) {
+      /* S5': stage 1 of the computed set and its neighbours, then the stop test / stage 2 per index */
+      int64_t a1 = X->ca > 1 ? X->ca - 1 : 1, b1 = X->cb < X->nb ? X->cb + 1 : X->nb;
 #pragma omp parallel for schedule(dynamic, 4)
-    for (int64_t j = X->ca; j <= X->cb; j++) root_bisect_one(X, j, rtol);
+      for (int64_t j = a1; j <= b1; j++) stage1_one(X, j, rtol_c);
+#pragma omp parallel for schedule(dynamic, 4)
+      for (int64_t j = X->ca; j <= X->cb; j++) stage2_one(X, j, rtol, gaptol);
+    } else {
+#pragma omp parallel for schedule(dynamic, 4)
+      for (int64_t j = X->ca; j <= X->cb; j++) root_bisect_one(X, j, rtol);
+    }
     /* guard extension while clustered (single-block subsets) */
     while (X->ca > 1 && !oracle_is_boundary(X->lo[X->ca], X->hi[X->ca], X->lo[X->ca + 1], X->hi[X->ca + 1], gaptol)) {
       X->ca--;
-      root_bisect_one(X, X->ca, rtol);
+      if (es) root_bisect_es(X, X->ca, rtol_c, rtol, gaptol);
+      else root_bisect_one(X, X->ca, rtol);
     }
     while (X->cb < X->nb && !oracle_is_boundary(X->lo[X->cb - 1], X->hi[X->cb - 1], X->lo[X->cb], X->hi[X->cb], gaptol)) {
       X->cb++;
-      root_bisect_one(X, X->cb, rtol);
+      if (es) root_bisect_es(X, X->cb, rtol_c, rtol, gaptol);
+      else root_bisect_one(X, X->cb, rtol);
     }
     X->hi[0] = NAN;
   }
@@ -1038,7 +1108,7 @@ done:
   if (dg && dg->stats) memcpy(dg->stats, g_stats, sizeof(g_stats));
   for (int64_t b = 0; b < nblk; b++) {
     rep_free(B[b].root);
-    free(B[b].lo); free(B[b].hi); free(B[b].colmap);
+    free(B[b].lo); free(B[b].hi); free(B[b].colmap); free(B[b].s1lo); free(B[b].s1hi);
   }
   free(B);
   free(starts);

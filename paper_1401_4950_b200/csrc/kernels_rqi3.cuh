@@ -24,6 +24,7 @@
 struct RqiState {
   double lam_hi, lam_lo, blo_hi, blo_lo, bhi_hi, bhi_lo, thr1;
   int r, it, status, wide;  // status: 0 active, 1 accepted, 2 handed to k_rqi2; wide: 8x warm-up
+  int light, pad;           // light: RQC-only (no factors stored) passes still due before a stored one
 };
 
 // per (singleton, lane, segment) record of a segmented pass
@@ -35,7 +36,7 @@ struct SegRec {
 };
 
 __global__ void k_rqi3_init(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
-                            RqiState *st, double eps_x) {
+                            RqiState *st, double eps_x, double rtol, int *mode0) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ns) return;
   const Singleton s = sg[i];
@@ -53,6 +54,12 @@ __global__ void k_rqi3_init(const Singleton *__restrict__ sg, int ns, const RepD
   q.it = 0;
   q.status = 0;
   q.wide = 0;
+  // the first pass only corrects lambda-hat (its factors are not the accepted vector's); an interval left at the
+  // early-stop tolerance (A-41: wider than the classification rtol; its midpoint within 2^-8 gap of lambda)
+  // takes a second one -- measured: two corrections from there, one from an rtol interval
+  q.light = bis_continue(s.lo, s.hi, rtol) ? 2 : 1;
+  q.pad = 0;
+  if (q.light == 2) atomicOr(mode0, 3);  // the first pass: the x-arithmetic one (mode 3) when any is due
   st[i] = q;
 }
 
@@ -532,12 +539,17 @@ __global__ void __launch_bounds__(128) k_twist_lane_dd(const Singleton *__restri
 __global__ void __launch_bounds__(128, MRRR_FC_MINB) k_fixed_chunk(const Singleton *__restrict__ sg, int ns,
                                                      const RepDesc *__restrict__ reps, const QElt *__restrict__ mq,
                                                      const RqiState *__restrict__ st, int K2, int Wu, dd *P2,
-                                                     long long nbmax, SegRec *rec, int bulk, int sd) {
+                                                     long long nbmax, SegRec *rec, int bulk, int sd,
+                                                     const int *__restrict__ modep) {
+  // 3: the x-arithmetic RQC-only passes (S.light == 2), 0: the dd RQC-only passes (S.light == 1), 1: the stored
+  // ones (S.light == 0), 2: none left (k_rqi_mode)
+  const int mode = *modep;
+  if (mode == 2) return;
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= (long long)ns * (K2 + 1)) return;
   const int i = (int)(g % ns), slot = (int)(g / ns);
   const RqiState S = st[i];
-  if (S.status != 0) return;
+  if (S.status != 0 || S.light != (mode == 3 ? 2 : mode == 0 ? 1 : 0)) return;
   const RepDesc Rp = reps[sg[i].rep];
   const int nb = Rp.nb, r = S.r, steps = nb - 1;
   const int L = max((steps + K2 - 1) / K2, 1), W = S.wide ? 8 * Wu : Wu;
@@ -585,13 +597,17 @@ __global__ void __launch_bounds__(128, MRRR_FC_MINB) k_fixed_chunk(const Singlet
     t1 = nb - 1 - r;
     R = R0 + 2 * cr + 1;
   }
-  const bool light = S.it == 0;
+  const bool light = S.light != 0;
   const QElt *q = mq + Rp.off;
   const dd lam = dd_make(S.lam_hi, S.lam_lo), nlam = dd_neg(lam);
   __shared__ __align__(16) double2 stage[128 * ZSTRIDE];
   const int tw = t0 == 0 ? 0 : max(t0 - W, 0);
   double2 *stg = bulk ? stage + threadIdx.x * ZSTRIDE : nullptr;
-  if (sd) {
+  // sd: the single/double realisation's binary64 passes; S.light == 2: the first of two RQC-only passes from an
+  // interval left at the early-stop tolerance (A-41) -- a correction from 2^-8 gap needs only ~2^-24 gap
+  // relative accuracy, which x-arithmetic on fl64 of the representation gives (the dd passes that follow
+  // decide the eigenpair), at about half the issue cost of the dd pass
+  if (sd || mode == 3) {
     if (light) seg_pass_sd<true>(q, nb, isB, t0, t1, tw, S.lam_hi, P2 + (long long)i * nbmax, R, nullptr);
     else seg_pass_sd<false>(q, nb, isB, t0, t1, tw, S.lam_hi, P2 + (long long)i * nbmax, R, stg);
     return;
@@ -602,15 +618,15 @@ __global__ void __launch_bounds__(128, MRRR_FC_MINB) k_fixed_chunk(const Singlet
 // thread per singleton: junctions, gamma_r, ||z||^2, inertia, and the stask decision
 // per-thread counter increments, summed per warp before one atomic each
 struct FsInc {
-  unsigned nact, wide, hofixed, horqc, iters, light, qd, zw, dmax;
-};
+  unsigned nact, wide, hofixed, horqc, iters, light, qd, zw, dmax, nlight;  // nact / nlight: active, next pass
+};                                                                           // stored / RQC-only
 __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restrict__ sg,
                                                 const RepDesc *__restrict__ reps, RqiState *st, int K,
                                                 const SegRec *__restrict__ F, double *W, ZMeta *zmeta,
                                                 int *diag_depth, double *fin_lo, double *fin_hi, FsInc &inc,
-                                                int sd, double eps_y) {
+                                                int sd, double eps_y, int mode) {
   RqiState S = st[i];
-  if (S.status != 0) return;
+  if (S.status != 0 || S.light != (mode == 3 ? 2 : mode == 0 ? 1 : 0)) return;
   const Singleton s = sg[i];
   const RepDesc Rp = reps[s.rep];
   const int nb = Rp.nb, r = S.r, j = s.j;
@@ -646,7 +662,7 @@ __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restri
   if (!good) {
     if (!S.wide) {  // a warm-up too short for this singleton: repeat the pass with an 8x longer one
       st[i].wide = 1;
-      inc.nact++;
+      if (S.light) inc.nlight++; else inc.nact++;
       inc.wide++;
       return;
     }
@@ -661,7 +677,8 @@ __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restri
   dd lam = dd_make(S.lam_hi, S.lam_lo), blo = dd_make(S.blo_hi, S.blo_lo), bhi = dd_make(S.bhi_hi, S.bhi_lo);
   S.it++;
   inc.iters++;
-  if (S.it == 1) inc.light += (unsigned)(nb - 1);
+  const bool was_light = S.light != 0;
+  if (was_light) inc.light += (unsigned)(nb - 1);
   else inc.qd += (unsigned)(nb - 1);
   bool accepted = false, handover = false;
   if (!isfinite(zz.hi) || zz.hi == 0.0) {
@@ -673,7 +690,8 @@ __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restri
     dd tol2 = dd_mul_d(dd_abs(lam), 4.0 * eps_y);  // A-30
     if (dd_lt(tol2, dd_from(__dmul_rn(0x1p-100, Rp.spdiam)))) tol2 = dd_from(__dmul_rn(0x1p-100, Rp.spdiam));
     if (resid.hi <= S.thr1 || dd_lt(dd_abs(rqc), tol2)) {
-      if (S.it == 1) {  // accepted on the RQC-only pass: repeat it at the same lambda with the factors stored
+      if (was_light) {  // accepted on an RQC-only pass: repeat it at the same lambda with the factors stored
+        S.light = 0;
         inc.nact++;
         st[i] = S;
         return;
@@ -685,6 +703,7 @@ __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restri
       const bool okc = ((c < j) ? (rqc.hi > 0.0) : (rqc.hi < 0.0)) && dd_lt(blo, nl) && dd_lt(nl, bhi);
       if (okc && S.it < MAX_RQI) lam = nl;
       else handover = true;  // bisection fallback / iteration cap: the two-lane kernel redoes this singleton
+      S.light = was_light ? max(S.light - 1, 0) : 0;  // RQC-only passes still due (k_rqi3_init)
     }
   }
   if (accepted) {
@@ -705,6 +724,8 @@ __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restri
   } else if (handover) {
     S.status = 2;
     inc.horqc++;
+  } else if (S.light) {
+    inc.nlight++;
   } else {
     inc.nact++;
   }
@@ -717,22 +738,25 @@ __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restri
 __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
                              RqiState *st, int K, const SegRec *__restrict__ rec, double *W,
                              ZMeta *zmeta, int *diag_depth, double *fin_lo, double *fin_hi, long long *stats,
-                             int *nactive, int stage, int sd, double eps_y) {
+                             int *nactive, int stage, int sd, double eps_y, const int *__restrict__ modep) {
+  const int mode = *modep;
+  if (mode == 2) return;
   extern __shared__ uint4 recsm[];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int per = 4 * K;  // records per singleton: 2K chunks x 2 lanes
   const SegRec *F = stage ? reinterpret_cast<const SegRec *>(stage_recs(rec, per * (int)sizeof(SegRec), ns, recsm))
                           : rec + (long long)i * per;
-  FsInc inc = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  if (i < ns) fixed_step_body(i, sg, reps, st, K, F, W, zmeta, diag_depth, fin_lo, fin_hi, inc, sd, eps_y);
+  FsInc inc = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (i < ns) fixed_step_body(i, sg, reps, st, K, F, W, zmeta, diag_depth, fin_lo, fin_hi, inc, sd, eps_y, mode);
   const unsigned fm = 0xffffffffu;
   const unsigned nact = __reduce_add_sync(fm, inc.nact), wide = __reduce_add_sync(fm, inc.wide);
   const unsigned hof = __reduce_add_sync(fm, inc.hofixed), hor = __reduce_add_sync(fm, inc.horqc);
   const unsigned it = __reduce_add_sync(fm, inc.iters), li = __reduce_add_sync(fm, inc.light);
   const unsigned qd = __reduce_add_sync(fm, inc.qd), zw = __reduce_add_sync(fm, inc.zw);
-  const unsigned dm = __reduce_max_sync(fm, inc.dmax);
+  const unsigned dm = __reduce_max_sync(fm, inc.dmax), nl = __reduce_add_sync(fm, inc.nlight);
   if ((threadIdx.x & 31) == 0) {
     if (nact) atomicAdd(nactive, (int)nact);
+    if (nl) atomicAdd(nactive + 1, (int)nl);
     if (wide) atomicAdd((unsigned long long *)&stats[ST_SEG_WIDE], (unsigned long long)wide);
     if (hof) atomicAdd((unsigned long long *)&stats[ST_HO_FIXED], (unsigned long long)hof);
     if (hor) atomicAdd((unsigned long long *)&stats[ST_HO_RQC], (unsigned long long)hor);
@@ -745,6 +769,14 @@ __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const Rep
     if (zw) atomicAdd((unsigned long long *)&stats[ST_ZW_STEPS], (unsigned long long)zw);
     if (dm) atomicMax((unsigned long long *)&stats[ST_DMAX], (unsigned long long)dm);
   }
+}
+
+// mode of pass p + 1 from pass p's mode and the counts it left (q[3p] singletons active for a stored pass,
+// q[3p + 1] for an RQC-only pass, q[3p + 2] the mode): light passes first, then the stored passes of everyone
+// waiting, 2 when nothing is left; the host enqueues several passes between its checks
+__global__ void k_rqi_mode(int *q, int p) {
+  const int m = q[3 * p + 2], a0 = q[3 * p], a1 = q[3 * p + 1];
+  q[3 * (p + 1) + 2] = (m == 2) ? 2 : (m == 3) ? 0 : (m == 0) ? (a1 > 0 ? 0 : 1) : (a1 > 0 ? 0 : (a0 > 0 ? 1 : 2));
 }
 
 // singletons handed over (status != 1) for the two-lane kernel k_rqi2

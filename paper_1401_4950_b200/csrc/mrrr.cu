@@ -79,7 +79,7 @@ inline unsigned nblocks_for(long long n, int bs) { return (unsigned)std::max<lon
 
 // counters block on the device: reset/readback in one copy
 enum { C_NNEXT = 0, C_NEX, C_NPEND, C_NREADY, C_NSING, C_NCLUS, C_NNXT, C_NDONE, C_NK, C_NP, C_NPC, C_NFB,
-       C_NMULTI, C_NCOUNTERS = 16 };
+       C_NMULTI, C_NACT, C_NLIGHT, C_NCOUNTERS = 16 };
 
 }  // namespace
 
@@ -118,6 +118,8 @@ struct mrrr_ctx {
   int seg_minlen = 512;            // ... and the segments stay this long (long chains: C5b, a rank's C5a shard)
   int dev_frac = 0;            // ... once the indices still sharing nodes are at most 1/dev_frac of the nodes (0: by n)
   bool dev_stable = true;      // device-driven rounds once every node holds one index (exact grids)
+  long long es2_target = 4096;  // early stop, stage 2: k-section budget (C2: 2 levels per round; measured
+  int es2_minlen = 256;          // 16384 -> 4096 and 512 -> 256-row segments: 2.89 -> 2.53 ms)  (MRRR_ES2_*)
   int dev_rb = 16;            // rounds per device-driven batch (32: empty tail rounds cost a rank's short run)
   bool dev_rounds = false;     // segmented rounds enqueued in batches on device-side counters (MRRR_DEVROUNDS=1;
                                // slower on C2: the oversized early-exit grids cost more than the saved syncs)
@@ -134,6 +136,8 @@ struct mrrr_ctx {
 
   // buffers
   Buf starts, scal, binfo, bside, blist, cab, mx, my, mq, lscratch, reps, rlo, rhi, colmap, gstart;
+  Buf s1lo, s1hi, esr;  // early classification stop (S5'): stage-1 intervals, decision ranges
+  Buf rqmode;           // segmented RQI: per-pass counters and mode (k_rqi_mode)
   Buf nodesK, nodesP, offsP, dS, dG, dH;  // guided bisection rounds
   Buf repoff, repcur, repcta;             // representation-grouped rounds
   Buf segout, rnd;                        // segmented NegCount; per-round device counters
@@ -263,6 +267,65 @@ __global__ void k_guard_scan(int *cab, int lo_far, int hi_far, const double *__r
   while (cb < nb && cb < hi_far && !is_boundary(rlo[cb - 2], rhi[cb - 2], rlo[cb - 1], rhi[cb - 1], gaptol)) cb++;
   cab[0] = ca;
   cab[1] = cb;
+}
+
+// S5' early classification stop (sec. 3.2.2 remark (3) P:3204-3210; A-41; oracle
+// stage1_one/stage2_one): index j of a block (2 <= j <= nb-1) keeps its stage-1 interval (rtol_c) when both
+// neighbour pairs are classification boundaries and its width is at most 2^-7 of its absolute gap
+__device__ __forceinline__ bool es_stop(const double *__restrict__ s1lo, const double *__restrict__ s1hi, long long i,
+                                        int j, int nb, double gaptol) {
+  if (j < 2 || j > nb - 1) return false;
+  const double llo = s1lo[i - 1], lhi = s1hi[i - 1], clo = s1lo[i], chi = s1hi[i], rlo = s1lo[i + 1], rhi = s1hi[i + 1];
+  if (!is_boundary(llo, lhi, clo, chi, gaptol) || !is_boundary(clo, chi, rlo, rhi, gaptol)) return false;
+  const double gap = dmind(__dsub_rn(clo, lhi), __dsub_rn(rlo, chi));
+  return __dsub_rn(chi, clo) <= ldexp(gap, -7);
+}
+// one thread per index of the ranges rng[r] = {block, ja, jb, offset} (1-based within the block, offsets
+// prefix-summed): stopped indices take their stage-1 interval; the continuing ones form one stage-2 node per
+// run of consecutive continuing indices sharing a stage-1 interval (a stage-1 node holding several indices)
+struct EsRange { int blk, ja, jb, off; };
+__global__ void k_es_decide(const EsRange *__restrict__ rng, int nr, int total, const int *__restrict__ starts,
+                            const double *__restrict__ s1lo, const double *__restrict__ s1hi, double *rlo,
+                            double *rhi, double gaptol, Node *nodes, int *nnode, long long *stats) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  bool stop = false;
+  if (t < total) {
+    int lo = 0, hi = nr - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (rng[mid].off <= t) lo = mid; else hi = mid - 1;
+    }
+    const EsRange R = rng[lo];
+    const int s = starts[R.blk], nb = starts[R.blk + 1] - s;
+    const int j = R.ja + (t - R.off);
+    const long long i = (long long)s + j - 1;
+    stop = es_stop(s1lo, s1hi, i, j, nb, gaptol);
+    if (stop) {
+      rlo[i] = s1lo[i];
+      rhi[i] = s1hi[i];
+    } else {
+      auto same = [&](long long x, long long y) {
+        return __double_as_longlong(s1lo[x]) == __double_as_longlong(s1lo[y]) &&
+               __double_as_longlong(s1hi[x]) == __double_as_longlong(s1hi[y]);
+      };
+      const bool start = !(j > R.ja && same(i - 1, i) && !es_stop(s1lo, s1hi, i - 1, j - 1, nb, gaptol));
+      if (start) {
+        int je = j;
+        while (je < R.jb && same(i, i + (je + 1 - j)) && !es_stop(s1lo, s1hi, i + (je + 1 - j), je + 1, nb, gaptol)) je++;
+        Node nd;
+        nd.lo = s1lo[i];
+        nd.hi = s1hi[i];
+        nd.a = j - 1; nd.b = je;
+        nd.wlo = j; nd.whi = je;
+        nd.rep = R.blk; nd.pad = 0;
+        nd.obase = (long long)s - 1;
+        nd.est = NAN; nd.u = INFINITY;
+        nodes[atomicAdd(nnode, 1)] = nd;
+      }
+    }
+  }
+  const unsigned ns = __reduce_add_sync(0xffffffffu, stop ? 1u : 0u);
+  if ((threadIdx.x & 31) == 0 && ns) atomicAdd((unsigned long long *)&stats[ST_ESTOP], (unsigned long long)ns);
 }
 
 // multi-block ranking of T-frame midpoints (S4/S6): rank = #{keys before mine}
@@ -823,8 +886,12 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
       dd *P2s = h->wsA.as<dd>() + stride * nbmax;                 // after TF
       RqiState *rs = h->rqst.as<RqiState>();
       SegRec *rec = h->rqrec.as<SegRec>();
+      const int MAXP = 2 * MAX_RQI + 4;
+      CK(h->rqmode.ensure(sizeof(int) * 3 * (MAXP + 1)));
+      int *qm = h->rqmode.as<int>();
+      CK(cudaMemsetAsync(qm, 0, sizeof(int) * 3 * (MAXP + 1), h->stream));  // pass 0: mode 0 (or 3, k_rqi3_init)
       k_rqi3_init<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), rs,
-                                                                h->sd ? 0x1p-24 : EPS_X);
+                                                                h->sd ? 0x1p-24 : EPS_X, 1e-2 * h->gaptol, qm + 2);
       const int KT = 2 * K;
       TwRec *trec = reinterpret_cast<TwRec *>(rec);
       const size_t tsb = stage_bytes(h, 32 * 2 * KT * sizeof(TwRec));
@@ -849,24 +916,31 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
                                                                  h->stats.as<long long>(), tsb ? 1 : 0);
       }
       launch_check(h);
-      for (int it = 0; it < MAX_RQI + 2; it++) {  // + the passes repeated with a wide warm-up
-        CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
-        k_fixed_chunk<<<nblocks_for((2 * K + 1) * nb, 128), 128, 0, h->stream>>>(
-            sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, 2 * K, Wu, P2s, nbmax, rec,
-            h->rqi_bulk ? 1 : 0, h->sd ? 1 : 0);
-        const size_t fsb = stage_bytes(h, 32 * 4 * K * sizeof(SegRec));
-        k_fixed_step<<<nblocks_for(nb, 32), 32, fsb, h->stream>>>(
-            sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, rec, W, h->zmeta.as<ZMeta>(),
-            diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
-            diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), h->cnt.as<int>() + C_NFB, fsb ? 1 : 0,
-            h->sd ? 1 : 0, h->sd ? 0x1p-53 : EPS_Y);
-        launch_check(h);
-        h->host_launches += 1;
-        if (it == 0) continue;  // the RQC-only pass never finishes a singleton: no host check after it
-        int act = 0;
-        CK(cudaMemcpyAsync(&act, h->cnt.as<int>() + C_NFB, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+      // passes by mode: the RQC-only (light) passes of every singleton that still has one due run before the
+      // stored passes, so a singleton that needs two light passes (a start left at the early-stop tolerance)
+      // does not put a stored pass and a second light pass into two separate launches of the others.  The mode
+      // of each pass is decided on the device (k_rqi_mode); the host checks after batches of passes.
+      const size_t fsb = stage_bytes(h, 32 * 4 * K * sizeof(SegRec));
+      int p = 0;
+      for (int batch = 3; p < MAXP; batch = 1) {  // first batch: light, stored, and one spare pass (or x-light,
+                                                  // light, stored)
+        for (int b = 0; b < batch && p < MAXP; b++, p++) {
+          k_fixed_chunk<<<nblocks_for((2 * K + 1) * nb, 128), 128, 0, h->stream>>>(
+              sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, 2 * K, Wu, P2s, nbmax, rec,
+              h->rqi_bulk ? 1 : 0, h->sd ? 1 : 0, qm + 3 * p + 2);
+          k_fixed_step<<<nblocks_for(nb, 32), 32, fsb, h->stream>>>(
+              sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, rec, W, h->zmeta.as<ZMeta>(),
+              diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
+              diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), qm + 3 * p, fsb ? 1 : 0,
+              h->sd ? 1 : 0, h->sd ? 0x1p-53 : EPS_Y, qm + 3 * p + 2);
+          k_rqi_mode<<<1, 1, 0, h->stream>>>(qm, p);
+          launch_check(h);
+          h->host_launches += 2;
+        }
+        int nm = 0;
+        CK(cudaMemcpyAsync(&nm, qm + 3 * p + 2, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
-        if (act == 0) break;
+        if (nm == 2) break;
       }
       const int *stat = reinterpret_cast<const int *>(reinterpret_cast<const char *>(rs) + offsetof(RqiState, status));
       k_zwrite_chunk<<<nblocks_for(nb, 4), 128, 0, h->stream>>>(
@@ -1300,6 +1374,56 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
     long long v;
     ~RestoreTC() { h->target_chains = v; }
   } restore_tc{h, tc_saved};
+  // S5' early classification stop (MRRR_EARLY_STOP, A-41): stage 1 bisects to rtol_c into s1lo/s1hi
+  // (the computed set and one neighbour on each side), k_es_decide keeps the stopped intervals and runs the
+  // others on from their stage-1 nodes to rtol (the same paths, so the same intervals as without the stop)
+  const bool es = (h->flags & MRRR_EARLY_STOP) != 0;
+  double rtol_c = rtol;
+  if (es) {
+    int ex = 0;
+    while (ex < 62 && (1LL << ex) < n) ex++;  // ceil(log2 n), as oracle_es_rtol
+    rtol_c = std::max(rtol, std::ldexp(1.0, -(10 + ex)));
+    CK(h->s1lo.ensure(sizeof(double) * n));
+    CK(h->s1hi.ensure(sizeof(double) * n));
+    k_fill<<<nblocks_for(n, 256), 256, 0, st>>>(h->s1lo.as<double>(), n, NAN);
+    k_fill<<<nblocks_for(n, 256), 256, 0, st>>>(h->s1hi.as<double>(), n, NAN);
+    launch_check(h);
+  }
+  double *b1lo = es ? h->s1lo.as<double>() : h->rlo.as<double>(), *b1hi = es ? h->s1hi.as<double>() : h->rhi.as<double>();
+  auto es_stage2 = [&](const std::vector<EsRange> &rg0) {
+    std::vector<EsRange> rg;
+    int total = 0;
+    for (EsRange r : rg0)
+      if (r.jb >= r.ja) { r.off = total; total += r.jb - r.ja + 1; rg.push_back(r); }
+    if (total == 0) return;
+    CK(h->esr.ensure(sizeof(EsRange) * rg.size()));
+    CK(cudaMemcpyAsync(h->esr.p, rg.data(), sizeof(EsRange) * rg.size(), cudaMemcpyHostToDevice, st));
+    h->max_nodes = std::max(h->max_nodes, total + 2);
+    CK(h->nodesA.grow_keep(sizeof(Node) * (size_t)h->max_nodes, 0, st));
+    CK(h->nodesB.grow_keep(sizeof(Node) * (size_t)h->max_nodes, 0, st));
+    zero_counters(h);
+    k_es_decide<<<nblocks_for(total, 128), 128, 0, st>>>(h->esr.as<EsRange>(), (int)rg.size(), total,
+                                                         h->starts.as<int>(), h->s1lo.as<double>(),
+                                                         h->s1hi.as<double>(), h->rlo.as<double>(),
+                                                         h->rhi.as<double>(), h->gaptol, h->nodesA.as<Node>(),
+                                                         h->cnt.as<int>() + C_NNEXT, h->stats.as<long long>());
+    launch_check(h);
+    read_counters(h);
+    const int nn2 = h->h_cnt[C_NNEXT];
+    if (nn2 > 0) {
+      // stage 2 holds few nodes (C2: ~1,100 of 8,192) for ~17 levels: latency-bound rounds, so fewer k-section
+      // points per node and shorter segments than the throughput rounds of stage 1
+      struct Keep {
+        mrrr_t h; long long tc; int ml;
+        ~Keep() { h->target_chains = tc; h->seg_minlen = ml; }
+      } keep{h, h->target_chains, h->seg_minlen};
+      if (h->es2_target > 0) h->target_chains = h->es2_target;
+      if (h->es2_minlen > 0) h->seg_minlen = h->es2_minlen;
+      bool rs = false;
+      run_bisection<false>(h, nn2, h->rlo.as<double>(), h->rhi.as<double>(), rtol, 0, nullptr, 0, &rs, -1, 0,
+                           single ? (int)n : 0);
+    }
+  };
   if (nbl) {
     long long cap = std::max<long long>(ncomp + 2, nbl);
     h->max_nodes = (int)cap;
@@ -1315,12 +1439,17 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
     if (single && nbl) {
       if (cab[0] > 1) cabm[0] = std::max(1, cab[0] - GUARD_MARGIN);
       if (cab[1] < (int)n) cabm[1] = std::min((int)n, cab[1] + GUARD_MARGIN);
-      if (cabm != cab) {
-        h->max_nodes = std::max<int>(h->max_nodes, cabm[1] - cabm[0] + 3);
-        CK(h->nodesA.grow_keep(sizeof(Node) * (size_t)h->max_nodes, 0, st));
-        CK(h->nodesB.grow_keep(sizeof(Node) * (size_t)h->max_nodes, 0, st));
-        CK(cudaMemcpyAsync(h->cab.p, cabm.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, st));
-      }
+    }
+    std::vector<int> cabs = cabm;  // stage-1 range: with the early stop, one decision neighbour on each side
+    if (es && single && nbl) {
+      cabs[0] = std::max(1, cabm[0] - 1);
+      cabs[1] = std::min((int)n, cabm[1] + 1);
+    }
+    if (cabs != cab) {
+      h->max_nodes = std::max<int>(h->max_nodes, cabs[1] - cabs[0] + 3);
+      CK(h->nodesA.grow_keep(sizeof(Node) * (size_t)h->max_nodes, 0, st));
+      CK(h->nodesB.grow_keep(sizeof(Node) * (size_t)h->max_nodes, 0, st));
+      CK(cudaMemcpyAsync(h->cab.p, cabs.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, st));
     }
     for (int attempt = 0; attempt < 64; attempt++) {
       k_root_nodes<<<nblocks_for(nbl, 128), 128, 0, st>>>(h->blist.as<int>(), nbl, h->starts.as<int>(),
@@ -1328,11 +1457,18 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
                                                           h->ex.as<ExplicitChain>());
       launch_check(h);
       bool restart = false;
-      run_bisection<false>(h, nbl, h->rlo.as<double>(), h->rhi.as<double>(), rtol, nbl, h->blist.as<int>(), nbl,
-                           &restart, -1, 0, single ? (int)n : 0);
+      run_bisection<false>(h, nbl, b1lo, b1hi, es ? rtol_c : rtol, nbl, h->blist.as<int>(), nbl, &restart, -1, 0,
+                           single ? (int)n : 0);
       if (!restart) break;
     }
-    if (cabm != cab) CK(cudaMemcpyAsync(h->cab.p, cab.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, st));
+    if (es) {
+      std::vector<EsRange> rg;
+      if (single) rg.push_back({0, cabm[0], cabm[1], 0});
+      else
+        for (int b : blist) rg.push_back({b, 1, h->h_starts[b + 1] - h->h_starts[b], 0});
+      es_stage2(rg);
+    }
+    if (cabs != cab) CK(cudaMemcpyAsync(h->cab.p, cab.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, st));
     // root definiteness
     std::vector<double> hb(16 * nblk);
     CK(cudaMemcpy(hb.data(), h->binfo.p, sizeof(double) * 16 * nblk, cudaMemcpyDeviceToHost));
@@ -1381,11 +1517,23 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
           h->max_nodes = std::max(h->max_nodes, (w[1] - w[0] + 1) + (w[3] - w[2] + 1) + 2);
           CK(h->nodesA.grow_keep(sizeof(Node) * (size_t)h->max_nodes, 0, st));
           CK(h->nodesB.grow_keep(sizeof(Node) * (size_t)h->max_nodes, 0, st));
-          k_guard_nodes<<<1, nn, 0, st>>>(h->starts.as<int>(), h->binfo.as<double>(), w[0], w[1], w[2], w[3],
+          // early stop: stage 1 of the batches and their decision neighbours, then the decisions and stage 2
+          int we[4] = {w[0], w[1], w[2], w[3]};
+          if (es)
+            for (int q = 0; q < nn; q++) { we[2 * q] = std::max(1, w[2 * q] - 1); we[2 * q + 1] = std::min(nb, w[2 * q + 1] + 1); }
+          h->max_nodes = std::max(h->max_nodes, (we[1] - we[0] + 1) + (we[3] - we[2] + 1) + 2);
+          CK(h->nodesA.grow_keep(sizeof(Node) * (size_t)h->max_nodes, 0, st));
+          CK(h->nodesB.grow_keep(sizeof(Node) * (size_t)h->max_nodes, 0, st));
+          k_guard_nodes<<<1, nn, 0, st>>>(h->starts.as<int>(), h->binfo.as<double>(), we[0], we[1], we[2], we[3],
                                           h->nodesA.as<Node>());
           launch_check(h);
           bool rs = false;
-          run_bisection<false>(h, nn, h->rlo.as<double>(), h->rhi.as<double>(), rtol, 0, nullptr, 0, &rs, -1, 0, nb);
+          run_bisection<false>(h, nn, b1lo, b1hi, es ? rtol_c : rtol, 0, nullptr, 0, &rs, -1, 0, nb);
+          if (es) {
+            std::vector<EsRange> rg;
+            for (int q = 0; q < nn; q++) rg.push_back({0, w[2 * q], w[2 * q + 1], 0});
+            es_stage2(rg);
+          }
         }
       }
       CK(cudaMemcpyAsync(h->cab.p, cab.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, st));
@@ -1573,6 +1721,9 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_SEGCHILDMIN")) h->segchild_min = atoi(s);
     if (const char *s = getenv("MRRR_SEGTHREADS")) h->seg_threads = atoll(s);
     if (const char *s = getenv("MRRR_SEGMINLEN")) h->seg_minlen = atoi(s);
+    if (const char *s = getenv("MRRR_EARLY_STOP")) { if (atoi(s)) h->flags |= MRRR_EARLY_STOP; }  // dev sweeps
+    if (const char *s = getenv("MRRR_ES2_TARGET")) h->es2_target = atoll(s);
+    if (const char *s = getenv("MRRR_ES2_MINLEN")) h->es2_minlen = atoi(s);
     if (const char *s = getenv("MRRR_SEGCH2")) h->seg_ch2 = atoll(s);
     if (const char *s = getenv("MRRR_RECSTAGE")) h->rec_stage = atoi(s) != 0;
     if (const char *s = getenv("MRRR_SEGYK")) h->segy_k = std::max(1, std::min(64, atoi(s)));

@@ -282,18 +282,20 @@ __device__ __forceinline__ int seg_chain_count(const SegOut *__restrict__ seg, i
   const SegOut *S = seg + c * K;
   int total = 0, k = 0;
   double s_exact = S[0].s_in;  // -sigma
-  if (K == 8) {  // the usual segment count: all eight records loaded before the junction walk
-    SegOut o[8];
+  if ((K & 7) == 0) {  // batches of eight records loaded before their part of the junction walk (the loads of a
+    bool run = true;   // one-at-a-time walk are a chain of dependent misses: 32 segments cost ~20 us per round)
+    for (int k0 = 0; k0 < K && run; k0 += 8) {
+      SegOut o[8];
 #pragma unroll
-    for (int u = 0; u < 8; u++) o[u] = S[u];
-    bool run = true;
+      for (int u = 0; u < 8; u++) o[u] = S[k0 + u];
 #pragma unroll
-    for (int u = 0; u < 8; u++) {
-      run = run && o[u].ok && (u == 0 || __double_as_longlong(o[u].s_in) == __double_as_longlong(s_exact));
-      if (run) {
-        total += o[u].cnt;
-        s_exact = o[u].s_out;
-        k = u + 1;
+      for (int u = 0; u < 8; u++) {
+        run = run && o[u].ok && (k0 + u == 0 || __double_as_longlong(o[u].s_in) == __double_as_longlong(s_exact));
+        if (run) {
+          total += o[u].cnt;
+          s_exact = o[u].s_out;
+          k = k0 + u + 1;
+        }
       }
     }
   } else {
@@ -314,12 +316,28 @@ __device__ __forceinline__ int seg_chain_count(const SegOut *__restrict__ seg, i
   const int nb = R.nb;
   double s = s_exact;
   int cnt = total;
-  for (int r = min(k * L, nb - 1); r < nb - 1; r++) {
-    const double2 mm = M[r];
-    const double dp = __dadd_rn(mm.x, s);
-    const double q = (isinf(s) && isinf(dp)) ? 1.0 : __ddiv_rn(s, dp);
-    s = __dsub_rn(__dmul_rn(q, mm.y), sig);
-    cnt += sbx(dp);
+  // re-run the failed segment k exactly from the last exact state; where the state it reaches equals, bit for
+  // bit, the next segment's recorded entry state, that segment saw the sequential operands: take its count and
+  // exit state and walk on (near an eigenvalue only the segments past the eigenvector's peak, where the forward
+  // recurrence expands, fail -- the rest of the chain need not be re-run)
+  while (k < K) {
+    const int bk = min(k * L, nb - 1), ek = (k == K - 1) ? nb - 1 : min((k + 1) * L, nb - 1);
+    for (int r = bk; r < ek; r++) {
+      const double2 mm = M[r];
+      const double dp = __dadd_rn(mm.x, s);
+      const double q = (isinf(s) && isinf(dp)) ? 1.0 : __ddiv_rn(s, dp);
+      s = __dsub_rn(__dmul_rn(q, mm.y), sig);
+      cnt += sbx(dp);
+    }
+    k++;
+    while (k < K) {
+      const SegOut o = S[k];
+      if (!o.ok || __double_as_longlong(o.s_in) != __double_as_longlong(s)) break;
+      cnt += o.cnt;  // the last segment's record includes the final row's term
+      s = o.s_out;
+      k++;
+      if (k == K) { atomicAdd(nfb, 1); return cnt; }
+    }
   }
   cnt += sbx(__dadd_rn(M[nb - 1].x, s));
   atomicAdd(nfb, 1);

@@ -118,6 +118,8 @@ struct mrrr_ctx {
   int seg_minlen = 512;            // ... and the segments stay this long (long chains: C5b, a rank's C5a shard)
   int dev_frac = 0;            // ... once the indices still sharing nodes are at most 1/dev_frac of the nodes (0: by n)
   bool dev_stable = true;      // device-driven rounds once every node holds one index (exact grids)
+  bool round_ev = true;  // per-round timing events of the device-driven rounds (MRRR_ROUNDEV=0: ~2.7 us less per
+                         // event on C2, 5.49 -> 5.33 ms, but no per-launch kernel time for the roofline)
   long long es2_target = 4096;  // early stop, stage 2: k-section budget (C2: 2 levels per round; measured
   int es2_minlen = 256;          // 16384 -> 4096 and 512 -> 256-row segments: 2.89 -> 2.53 ms)  (MRRR_ES2_*)
   int dev_rb = 16;            // rounds per device-driven batch (32: empty tail rounds cost a rank's short run)
@@ -520,6 +522,7 @@ void launch_negcount(mrrr_t h, const Node *nodes, int nnode, int m, int nex, con
 
 __global__ void k_set_int(int *p, int v) { *p = v; }
 
+
 // dynamic shared memory for the record-staging kernels (k_twist_pick2, k_fixed_step): the bytes if they fit
 // the opt-in per-block limit (attributes raised once per handle), else 0 (the kernels then read global)
 size_t stage_bytes(mrrr_t h, size_t bytes) {
@@ -576,11 +579,11 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
     const unsigned g1 = (unsigned)(chmax / 128 + 1);
     for (int b = 0; b < RB && r < MAXR; b++, r++) {
       Node *in = (r & 1) ? nxt : cur, *out = (r & 1) ? cur : nxt;
-      const int ea = tev_rec(h);
+      const int ea = h->round_ev ? tev_rec(h) : -1;
       k_negcount_seg<1><<<gseg, 128, 2 * SEG_TILE * sizeof(double2), h->stream>>>(
           in, 0, 0, nullptr, 0, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L, h->seg_w, h->segout.as<SegOut>(),
           nn + r, mmax, h->target_chains);
-      rp.push_back({ea, tev_rec(h)});
+      rp.push_back({ea, h->round_ev ? tev_rec(h) : -1});
       // junction walk (careful tail inline) and shared-tree update in one launch
       k_seg_round<<<g1 * 4, 32, 0, h->stream>>>(0, 0, K, h->segout.as<SegOut>(), h->counts.as<int>(), in,
                                              h->reps.as<RepDesc>(), h->mx.as<double2>(), L, out, nn + r + 1, out_lo,
@@ -598,7 +601,7 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
   }
   for (int i = 0; i < r; i++) {
     if (h->h_rounds[i] == 0) break;
-    h->tneg.push_back(rp[i]);
+    if (rp[i].first >= 0) h->tneg.push_back(rp[i]);
     h->neg_launches++;
     h->host_rounds++;
   }
@@ -1721,6 +1724,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_SEGCHILDMIN")) h->segchild_min = atoi(s);
     if (const char *s = getenv("MRRR_SEGTHREADS")) h->seg_threads = atoll(s);
     if (const char *s = getenv("MRRR_SEGMINLEN")) h->seg_minlen = atoi(s);
+    if (const char *s = getenv("MRRR_ROUNDEV")) h->round_ev = atoi(s) != 0;
     if (const char *s = getenv("MRRR_EARLY_STOP")) { if (atoi(s)) h->flags |= MRRR_EARLY_STOP; }  // dev sweeps
     if (const char *s = getenv("MRRR_ES2_TARGET")) h->es2_target = atoll(s);
     if (const char *s = getenv("MRRR_ES2_MINLEN")) h->es2_minlen = atoi(s);

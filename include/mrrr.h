@@ -61,6 +61,13 @@ typedef struct mrrr_ctx *mrrr_t;
  * mrrr_eig / mrrr_seig (and their _host forms); shards and mrrr_eig_dist apply the same rule (it depends only
  * on the indices j-1, j, j+1). */
 #define MRRR_EARLY_STOP 2u
+/* Numerical support of the singleton eigenvectors (S10', Getvec remark (2): "for all i < i_first
+ * and for all i > i_last, z(i) can be set to zero ... easily detected and exploited"; A-42) is applied by
+ * default: going outward from the twist index r (z(r) = 1), a column ends at the first edge i whose coupling
+ * |dl(i)| (|z(i)| + |z(i+1)|) is at most gap * eps_x, and the rows past it are stored as exact zeros (the residual
+ * changes by at most that term, so the vector moves by O(eps_x) by the gap theorem).  MRRR_FULL_SUPPORT stores
+ * the whole recurrence instead (Alg. Getvec as printed).  W and every integer output are the same either way. */
+#define MRRR_FULL_SUPPORT 4u
 
 /* Options (all fields may be zero = default). */
 typedef struct {
@@ -69,7 +76,7 @@ typedef struct {
   void *stream;       /* cudaStream_t used for all work; NULL: a library-owned stream */
   double gaptol;      /* classification threshold; <= 0: 1e-10 */
   uint64_t seed;      /* key of the root perturbation stream; 0: default */
-  uint32_t flags;     /* MRRR_KEEP_DIAG | MRRR_EARLY_STOP */
+  uint32_t flags;     /* MRRR_KEEP_DIAG | MRRR_EARLY_STOP | MRRR_FULL_SUPPORT */
   uint32_t reserved;
   int64_t ws_limit;   /* soft cap on workspace bytes; <= 0: 60% of free device memory */
 } mrrr_opts;
@@ -178,8 +185,9 @@ int mrrr_shard_owner(const int32_t *gstart, int64_t n, int64_t il, int64_t iu, i
  * last two-lane Getvec ran the careful IEEE pass (zero pivots / special values), 32 segmented
  * many-representation x-NegCount chains (child bisection) whose junctions did not all verify, 33 segments those
  * chains re-ran sequentially, 34 root indices the early classification stop (MRRR_EARLY_STOP) left at the
- * stage-1 tolerance. */
-#define MRRR_NSTATS 35
+ * stage-1 tolerance, 35 segmented root x-NegCount chains whose junctions did not all verify (re-run
+ * sequentially from the failed segment). */
+#define MRRR_NSTATS 36
 int mrrr_get_stats(mrrr_t h, int64_t *stats, int32_t nstats);
 
 /* Diagnostics of the last call made with MRRR_KEEP_DIAG (host buffers owned

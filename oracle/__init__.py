@@ -24,7 +24,7 @@ CFLAGS = ["-O2", "-std=gnu11", "-fopenmp", "-fPIC", "-shared", "-ffp-contract=of
 
 STAT_NAMES = ["d_max", "n_clusters", "largest_cluster", "uncertified", "shift_attempts", "rqi_iters",
               "rqi_fallbacks", "bracket_fixes", "root_backoffs", "failed", "negcount_x", "negcount_y",
-              "getvec_calls", "zero_pivots", "early_stops"]
+              "getvec_calls", "zero_pivots", "early_stops", "support_rows"]
 
 
 def build(force: bool = False) -> str:
@@ -36,7 +36,7 @@ def build(force: bool = False) -> str:
 
 class _Opts(C.Structure):
     _fields_ = [("gaptol", C.c_double), ("seed", C.c_uint64), ("root_side", C.c_int32), ("threads", C.c_int32),
-                ("roots_only", C.c_int32), ("early_stop", C.c_int32)]
+                ("roots_only", C.c_int32), ("early_stop", C.c_int32), ("support", C.c_int32)]
 
 
 class _Diag(C.Structure):
@@ -114,7 +114,7 @@ def lib(sd: bool = False):
         L.oracle_bisect_y_full.restype = None
         L.oracle_bisect_y_full.argtypes = [_i64, C.c_void_p, C.c_void_p, _i64, C.c_double, C.c_double, _dp, _dp]
         L.oracle_rqi.restype = None
-        L.oracle_rqi.argtypes = [_i64, C.c_void_p, C.c_void_p, _i64, C.c_double, C.c_double, C.c_double, _dp,
+        L.oracle_rqi.argtypes = [_i64, C.c_void_p, C.c_void_p, _i64, C.c_double, C.c_double, C.c_double, C.c_int32, _dp,
                                  C.c_void_p, C.POINTER(_i64), C.POINTER(_i64)]
         L.oracle_es_rtol.restype = C.c_double
         L.oracle_es_rtol.argtypes = [_i64, C.c_double]
@@ -157,13 +157,14 @@ class OracleResult:
 
 def mrrr(d, e, il: int | None = None, iu: int | None = None, *, gaptol: float | None = None, seed: int = 0,
          root_side: int = 0, threads: int = 0, roots_only: bool = False, sd: bool = False,
-         early_stop: bool = False) -> OracleResult:
+         early_stop: bool = False, support: bool = False) -> OracleResult:
     """Eigenpairs il..iu (1-based, inclusive) of the tridiagonal (d, e) by the oracle.  roots_only: stop after
     the root bisection (S1-S5): only nblocks/block_start/mu/side/root_lo/root_hi/root_gstart are filled.
     sd: the single/double realisation (liboracle_sd.so, gaptol 1e-5 by default); its inputs are
     the binary32 values (pass them as float32 or as their exact float64 images) and W, Z come back in float64
     before the final binary32 rounding (float32 of them is the realisation's output).  early_stop: the early
-    classification stop of the root bisection (S5', A-41)."""
+    classification stop of the root bisection (S5', A-41).  support: numerical-support
+    truncation of every singleton vector (S10', Getvec remark (2) P:3459-3463, A-42)."""
     d = _f64(d)
     n = d.size
     e = _f64(e) if n > 1 else np.zeros(1)
@@ -190,7 +191,7 @@ def mrrr(d, e, il: int | None = None, iu: int | None = None, *, gaptol: float | 
     fhi = np.zeros(k)
     st = np.zeros(16, np.int64)
     dg = _Diag(*[_ptr(a) for a in (nblocks, bstart, mu, side, rlo, rhi, rgs, depth, gf, gl, flo, fhi, st)])
-    op = _Opts(gaptol, seed, root_side, threads, int(roots_only), int(early_stop))
+    op = _Opts(gaptol, seed, root_side, threads, int(roots_only), int(early_stop), int(support))
     info = L.oracle_mrrr(n, _ptr(d), _ptr(e), il, iu, C.byref(op), _ptr(W), _ptr(Z), n, C.byref(dg))
     nbk = int(nblocks[0])
     return OracleResult(W=W, Z=Z.T, info=info, nblocks=nbk, block_start=bstart[:nbk + 1].copy(),
@@ -405,12 +406,12 @@ def bisect_y_full(d, l, j: int, lo: float, hi: float, *, sd: bool = False):
     return a.value, b.value
 
 
-def rqi(d, l, j: int, lo: float, hi: float, gap: float, *, sd: bool = False):
+def rqi(d, l, j: int, lo: float, hi: float, gap: float, *, sd: bool = False, support: bool = False):
     d, lp = _lpad(d, l)
     W = C.c_double()
     z = np.zeros(d.size)
     it, fb = C.c_int64(), C.c_int64()
-    lib(sd).oracle_rqi(d.size, _ptr(d), _ptr(lp), j, lo, hi, gap, C.byref(W), _ptr(z), C.byref(it), C.byref(fb))
+    lib(sd).oracle_rqi(d.size, _ptr(d), _ptr(lp), j, lo, hi, gap, int(support), C.byref(W), _ptr(z), C.byref(it), C.byref(fb))
     return dict(W=W.value, z=z, iters=it.value, fallbacks=fb.value)
 
 

@@ -83,7 +83,7 @@ typedef __float128 yreal;      /* double/quadruple realisation */
 enum {
   ST_DMAX = 0, ST_NCLUSTERS, ST_LARGEST, ST_UNCERTIFIED, ST_ATTEMPTS, ST_RQI_ITERS,
   ST_RQI_FALLBACK, ST_BRACKET_FIX, ST_ROOT_BACKOFF, ST_FAILED, ST_NEGX, ST_NEGY,
-  ST_GETVEC, ST_ZPIV, ST_ESTOP, ST_NSTATS = 16
+  ST_GETVEC, ST_ZPIV, ST_ESTOP, ST_SUPPORT, ST_NSTATS = 16
 };
 
 typedef struct {
@@ -93,6 +93,7 @@ typedef struct {
   int32_t threads;    /* 0 -> OpenMP default */
   int32_t roots_only; /* 1: stop after S5 (split, roots, root bisection of the computed set; diagnostics only) */
   int32_t early_stop; /* 1: early classification stop of the root bisection (S5', A-41) */
+  int32_t support;    /* 1: numerical-support truncation of every singleton vector (S10', A-42) */
 } oracle_opts;
 
 typedef struct {      /* every pointer optional */
@@ -595,8 +596,31 @@ static yreal bisect_y_full(const rep_t *M, int64_t j, yreal lo, yreal hi) {
 /* RQI for a singleton, Alg. stask P:4026-4074 with the mixed stopping rule    */
 /* ||r|| <= k_rs gap eps_x sqrt(n), k_rs = 1 (A-14, A-15).       */
 /* j is the 1-based index in M; [lo, hi] its x-interval; gap > 0.             */
-static void rqi_singleton(const rep_t *M, int64_t j, double lo, double hi, double gap, double *W_out,
-                          double *zcol, gv_ws *w) {
+/* S10' numerical support (Getvec remark (2): "for all i < i_first and i > i_last, z(i) can be set */
+/* to zero ... easily detected and exploited"; A-42).  The paper gives no rule.  Reading: cutting z   */
+/* at the edge between rows i and i+1 (coupling dl(i), the off-diagonal of LDL^T) changes the residual of the  */
+/* twisted solution (z(r) = 1) by exactly |dl(i)| (|z(i)| + |z(i+1)|) in two entries, so by the gap theorem     */
+/* the cut vector stays within angle ~eps_x of the eigenvector when that term is <= gap eps_x.  Going outward */
+/* from r, the support ends at the first edge with |dl(i)| (|z(i)| + |z(i+1)|) <= gap eps_x; the entries past */
+/* it are set to zero.  Returns ||z||^2 of the truncated vector.                                                */
+static yreal numerical_support(const rep_t *M, yreal *z, int64_t r, double gap) {
+  const int64_t nb = M->nb;
+  const yreal tau = (yreal)(gap * EPS_X);
+  int64_t first = 0, last = nb - 1;  /* 0-based support [first, last]; r is 0-based */
+  for (int64_t i = r - 1; i >= 0; i--)
+    if (YFABS(M->dl[i]) * (YFABS(z[i]) + YFABS(z[i + 1])) <= tau) { first = i + 1; break; }
+  for (int64_t i = r; i < nb - 1; i++)
+    if (YFABS(M->dl[i]) * (YFABS(z[i]) + YFABS(z[i + 1])) <= tau) { last = i; break; }
+  for (int64_t i = 0; i < first; i++) z[i] = 0;
+  for (int64_t i = last + 1; i < nb; i++) z[i] = 0;
+  STAT_ADD(ST_SUPPORT, last - first + 1);
+  yreal zz = 0;
+  for (int64_t i = first; i <= last; i++) zz += z[i] * z[i];
+  return zz;
+}
+
+static void rqi_singleton(const rep_t *M, int64_t j, double lo, double hi, double gap, int support,
+                          double *W_out, double *zcol, gv_ws *w) {
   const int64_t nb = M->nb;
   double mid = lo + (hi - lo) / 2;
   double nu = (100.0 * (double)nb) * EPS_A;
@@ -626,6 +650,7 @@ static void rqi_singleton(const rep_t *M, int64_t j, double lo, double hi, doubl
     lam = bisect_y_full(M, j, blo, bhi);
     getvec_q(M, lam, &r, w, &gamma, &zz, &c);
   }
+  if (support && r > 0) zz = numerical_support(M, w->z, r - 1, gap);
   yreal nz = YSQRT(zz);
   *W_out = (double)(lam + M->sigma);
   for (int64_t i = 0; i < nb; i++) zcol[i] = (double)(w->z[i] / nz);
@@ -638,6 +663,7 @@ typedef struct {
   int64_t n, k, ldz, bstart;  /* global size, #outputs, ldz, block start */
   const int32_t *colmap;      /* [nb+1] 1-based local -> output column or -1 */
   double gaptol, rtol;
+  int support;                /* S10' (A-42) */
   double *W, *Z;
   oracle_diag *dg;
 } ctx_t;
@@ -671,7 +697,7 @@ static void do_singleton(const ctx_t *cx, const rep_t *M, const double *lo, cons
   gv_alloc(&w, M->nb);
   double *zc = malloc(sizeof(double) * M->nb);
   double Wv;
-  rqi_singleton(M, j, lo[j], hi[j], gap, &Wv, zc, &w);
+  rqi_singleton(M, j, lo[j], hi[j], gap, cx->support, &Wv, zc, &w);
   cx->W[col] = Wv;
   double *Zc = cx->Z + (int64_t)col * cx->ldz;
   for (int64_t i = 0; i < cx->n; i++) Zc[i] = 0.0;
@@ -1088,7 +1114,7 @@ static int mrrr_scaled(int64_t n, const double *d, const double *e, int64_t il, 
     }
     ctx_t *cx = malloc(sizeof(ctx_t));
     cx->n = n; cx->k = k; cx->ldz = ldz; cx->bstart = X->s; cx->colmap = X->colmap;
-    cx->gaptol = gaptol; cx->rtol = rtol; cx->W = W; cx->Z = Z; cx->dg = dg;
+    cx->gaptol = gaptol; cx->rtol = rtol; cx->support = op ? op->support : 0; cx->W = W; cx->Z = Z; cx->dg = dg;
     int64_t g0 = X->ca;
     for (int64_t j = X->ca + 1; j <= X->cb + 1; j++) {
       if (j == X->cb + 1 || oracle_is_boundary(X->lo[j - 1], X->hi[j - 1], X->lo[j], X->hi[j], gaptol)) {
@@ -1344,12 +1370,12 @@ void oracle_bisect_y_full(int64_t nb, const double *d, const double *l, int64_t 
 /* the singleton RQI of S9 on L D L^T (sigma = 0) from the x-interval [lo, hi] with gap; *fallbacks = 1 when */
 /* the RQI ended in the bisection fallback of P:3481-3482                                                    */
 void oracle_rqi(int64_t nb, const double *d, const double *l, int64_t j, double lo, double hi, double gap,
-                double *W, double *z, int64_t *iters, int64_t *fallbacks) {
+                int32_t support, double *W, double *z, int64_t *iters, int64_t *fallbacks) {
   rep_t *M = rep_from_fp64(nb, d, l);
   gv_ws w;
   gv_alloc(&w, nb);
   int64_t i0 = g_stats[ST_RQI_ITERS], f0 = g_stats[ST_RQI_FALLBACK];
-  rqi_singleton(M, j, lo, hi, gap, W, z, &w);
+  rqi_singleton(M, j, lo, hi, gap, support, W, z, &w);
   *iters = g_stats[ST_RQI_ITERS] - i0;
   *fallbacks = g_stats[ST_RQI_FALLBACK] - f0;
   gv_free(&w);

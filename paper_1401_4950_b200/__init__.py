@@ -23,13 +23,14 @@ LIB_PATH = os.environ.get("MRRR_LIB") or os.path.join(HERE, "libmrrr.so")
 
 KEEP_DIAG = 1
 EARLY_STOP = 2  # MRRR_EARLY_STOP (include/mrrr.h): early classification stop of the root bisection
+FULL_SUPPORT = 4  # MRRR_FULL_SUPPORT: store the whole Getvec recurrence (no numerical-support truncation, A-42)
 MAXD = 8
-NSTATS = 35
+NSTATS = 36
 STAT_NAMES = ["d_max", "n_clusters", "largest_cluster", "uncertified", "shift_attempts", "rqi_iters",
               "rqi_fallbacks", "bracket_fixes", "root_backoffs", "failed", "negcount_x", "negcount_y",
               "getvec_calls", "rounds", "launches", "nblocks", "qd_steps", "qdg_steps", "z_steps", "zw_steps",
               "negcount_x_alg", "negcount_y_alg", "rqi_reject_sign", "rqi_reject_bracket", "rqi_handover", "ho_twist", "ho_fixed", "ho_rqc", "qd_light", "twist_rows", "seg_wide", "careful",
-              "xg_fallback_chains", "xg_fallback_segments", "early_stops"]
+              "xg_fallback_chains", "xg_fallback_segments", "early_stops", "root_fallback_chains"]
 TIME_NAMES = ["total", "split_root", "root_bisection", "classification", "clusters", "singletons",
               "rqi_ms_per_launch", "rqi_launches", "negcount_ms_per_launch", "negcount_launches", "t10", "t11"]
 
@@ -133,10 +134,11 @@ class Solver:
 
     def __init__(self, device: int | None = None, gaptol: float = 0.0, seed: int = 0, root_side: int = 0,
                  keep_diag: bool = False, stream: int | None = None, ws_limit: int = 0,
-                 early_stop: bool = False):
+                 early_stop: bool = False, full_support: bool = False):
         L = load()
         self._h = C.c_void_p()
-        flags = (KEEP_DIAG if keep_diag else 0) | (EARLY_STOP if early_stop else 0)
+        flags = ((KEEP_DIAG if keep_diag else 0) | (EARLY_STOP if early_stop else 0)
+                 | (FULL_SUPPORT if full_support else 0))
         o = _Opts(-1 if device is None else int(device), int(root_side), stream, float(gaptol), int(seed),
                   flags, 0, int(ws_limit))
         _check(L.mrrr_init(C.byref(self._h), C.byref(o)), "mrrr_init")

@@ -520,7 +520,11 @@ __global__ void __launch_bounds__(128) k_zwrite_chunk(const Singleton *__restric
                                                       const RepDesc *__restrict__ reps, const YElt *__restrict__ my,
                                                       const dd *__restrict__ P2base, long long S,
                                                       const ZMeta *__restrict__ zm, double *Z, long long ldz,
-                                                      const int *__restrict__ status = nullptr, int status_stride = 0) {
+                                                      double eps_sup, const int *__restrict__ status = nullptr,
+                                                      int status_stride = 0) {
+  // eps_sup > 0: numerical support (S10', Getvec remark (2) P:3459-3463, A-42): going outward from r,
+  // the column ends at the first edge i with |dl(i)| (|z(i)| + |z(i+1)|) <= gap eps_x (z(r) = 1), i.e. on the
+  // normalised values <= gap eps_x / ||z||; the rows past it are written as zeros without reading their factors
   __shared__ __align__(16) double2 sbuf[4][2][ZP];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int w = blockIdx.x * 4 + wib;
@@ -533,15 +537,20 @@ __global__ void __launch_bounds__(128) k_zwrite_chunk(const Singleton *__restric
   const dd inv = dd_make(m.inv_hi, m.inv_lo);
   const dd *P = P2base + (long long)w * S;
   double *Zc = Z + (long long)s.col * ldz + R.bstart;
+  const YElt *y = my + R.off;
+  const double tau = eps_sup > 0.0 ? __dmul_rn(s.gap, eps_sup) : -1.0;  // gap eps_x on z with z(r) = 1
   if (m.careful) {
-    if (lane == 0) zsolve(my + R.off, nb, r, P, P, 1, inv, Zc);
+    if (lane == 0) zsolve(y, nb, r, P, P, 1, inv, Zc, tau);
     return;
   }
+  const double tauN = __dmul_rn(tau, inv.hi);  // the same test on the normalised values
   if (lane == 0) Zc[r] = inv.hi;
   double2(*buf)[ZP] = sbuf[wib];
   for (int side = 0; side < 2; side++) {
     const int len = side ? last - r : r;
     if (len <= 0) continue;
+    double prevv = inv.hi;  // normalised z of the row before the tile's first (z(r) for the first tile)
+    int cut = len;          // side-relative index of the first row outside the support
     const int ntile = (len + ZT - 1) / ZT;
     auto issue = [&](int t) {
       double2 *b = buf[t & 1];
@@ -586,12 +595,35 @@ __global__ void __launch_bounds__(128) k_zwrite_chunk(const Singleton *__restric
 #pragma unroll
       for (int e = 0; e < ZC; e++) sd[lane * (ZC + 1) + e] = dd_mul_nf(E, p[e]).hi;
       __syncwarp();
+      if (tau >= 0.0) {
+        // edge between this row and the previous one (towards r): dl(r - 1 - mm) on the left, dl(r + mm) on the right
+        int c = len;
+#pragma unroll
+        for (int e = ZC - 1; e >= 0; e--) {
+          const int mm = mc + e;
+          if (mm < len) {
+            const double v = sd[lane * (ZC + 1) + e];
+            const double pv = e ? sd[lane * (ZC + 1) + e - 1] : (lane ? sd[lane * (ZC + 1) - 2] : prevv);  // (ZC + 1)-stride chunks
+            const double dl = fabs(__ldg(&y[side ? r + mm : r - 1 - mm].dl_hi));
+            if (__dmul_rn(dl, __dadd_rn(fabs(v), fabs(pv))) <= tauN) c = mm;
+          }
+        }
+        cut = __reduce_min_sync(0xffffffffu, c);
+        prevv = sd[zpad(ZT - 1)];
+      }
+      __syncwarp();
 #pragma unroll
       for (int u = 0; u < ZC; u++) {
         const int ml = lane + 32 * u, mm = m0 + ml;
-        if (mm < len) Zc[side ? r + 1 + mm : r - 1 - mm] = sd[zpad(ml)];
+        if (mm < len) Zc[side ? r + 1 + mm : r - 1 - mm] = mm < cut ? sd[zpad(ml)] : 0.0;
       }
       __syncwarp();
+      if (cut < len) break;
+    }
+    if (cut < len) {
+      cp_wait<0>();  // drain the prefetch of the next tile
+      __syncwarp();
+      for (int mm = ((cut / ZT) + 1) * ZT + lane; mm < len; mm += 32) Zc[side ? r + 1 + mm : r - 1 - mm] = 0.0;
     }
   }
 }

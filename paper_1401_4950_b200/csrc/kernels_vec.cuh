@@ -464,9 +464,12 @@ __device__ __forceinline__ void stw(dd *w, long long off, dd v) {
 // Backward branch (i = r-1 .. 0, uses l+ in B) then forward branch (i = r .. nb-2, uses u- in A),
 // as one loop over k with the workspace prefetched two steps ahead.  If Zc != nullptr writes
 // fl64(z_i * inv) to Zc[i].
+// tau >= 0 (Zc only): numerical support (A-42) -- on each side, the rows past the first edge i with
+// |dl(i)| (|z(i)| + |z(i+1)|) <= tau are written as zeros (||z||^2 stays the full one)
 __device__ __noinline__ dd zsolve(const YElt *__restrict__ y, int nb, int r, const dd *A, const dd *B, long long S, dd inv,
-                     double *Zc) {
+                     double *Zc, double tau = -1.0) {
   dd zz = dd_from(1.0);
+  bool cutL = false, cutR = false;
   if (Zc) Zc[r] = inv.hi;
   const int K = nb - 1;
   if (K <= 0) return zz;
@@ -497,7 +500,12 @@ __device__ __noinline__ dd zsolve(const YElt *__restrict__ y, int nb, int r, con
       z = isfinite(v.hi) ? v : dd_from(0.0);
     }
     zz = dd_add(zz, dd_mul(z, z));
-    if (Zc) Zc[bw ? i : i + 1] = dd_mul(z, inv).hi;
+    if (Zc) {
+      bool &cut = bw ? cutL : cutR;
+      if (!cut && tau >= 0.0 &&
+          __dmul_rn(fabs(__ldg(&y[i].dl_hi)), __dadd_rn(fabs(z.hi), fabs(z1.hi))) <= tau) cut = true;
+      Zc[bw ? i : i + 1] = cut ? 0.0 : dd_mul(z, inv).hi;
+    }
     if (bw && i == r - 1) zrm1 = z;
     z2 = z1;
     z1 = z;

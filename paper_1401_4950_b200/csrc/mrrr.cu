@@ -101,6 +101,7 @@ struct mrrr_ctx {
   bool neg_tma = true;  // x-NegCount with TMA-staged representation tiles (k_negcount_tma)
   bool grouped = true;  // child bisection with CTAs grouped by representation (k_negcount_grp)
   int seg_k = 8, seg_w = 128;  // segmented root NegCount: segments per chain, warm-up rows (k_negcount_seg)
+  int fuse_mmax = 2;           // host-driven segmented rounds fuse walk + update (k_seg_round) up to this depth
   bool rqi_seg = true;         // segmented RQI passes (kernels_rqi3.cuh); MRRR_RQISEG=0: the two-lane kernel only
   int rqi_segk = 8, rqi_segw = 0;  // rqi_segw 0: by frame length (128 up to 16K rows, else 192)
   long long rqi_threads = 131072;  // adaptive RQI segment count target (threads per segmented pass)
@@ -579,13 +580,14 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
     const unsigned g1 = (unsigned)(chmax / 128 + 1);
     for (int b = 0; b < RB && r < MAXR; b++, r++) {
       Node *in = (r & 1) ? nxt : cur, *out = (r & 1) ? cur : nxt;
+      SegOut *sg = h->segout.as<SegOut>();
       const int ea = h->round_ev ? tev_rec(h) : -1;
       k_negcount_seg<1><<<gseg, 128, 2 * SEG_TILE * sizeof(double2), h->stream>>>(
-          in, 0, 0, nullptr, 0, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L, h->seg_w, h->segout.as<SegOut>(),
+          in, 0, 0, nullptr, 0, h->reps.as<RepDesc>(), h->mx.as<double2>(), K, L, h->seg_w, sg,
           nn + r, mmax, h->target_chains);
       rp.push_back({ea, h->round_ev ? tev_rec(h) : -1});
       // junction walk (careful tail inline) and shared-tree update in one launch
-      k_seg_round<<<g1 * 4, 32, 0, h->stream>>>(0, 0, K, h->segout.as<SegOut>(), h->counts.as<int>(), in,
+      k_seg_round<<<g1 * 4, 32, 0, h->stream>>>(0, 0, K, sg, h->counts.as<int>(), in,
                                              h->reps.as<RepDesc>(), h->mx.as<double2>(), L, out, nn + r + 1, out_lo,
                                              out_hi, rtol, alg, nullptr, nfb + r, nn + r, mmax, h->target_chains, negx);
       launch_check(h);
@@ -595,7 +597,12 @@ void run_rounds_device(mrrr_t h, Node *cur, Node *nxt, int nnode, int nb, int ma
     CK(cudaMemcpyAsync(h->h_rounds.data(), nn, sizeof(int) * (r + 1), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     const int left = h->h_rounds[r];
-    if (left == 0) break;
+    if (left == 0) {
+      std::vector<int> fb(r);
+      CK(cudaMemcpy(fb.data(), nfb, sizeof(int) * r, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < r; i++) h->stats_h[ST_ROOT_FB] += fb[i];
+      break;
+    }
     known = left;
     if (r >= MAXR) { g_last_cuda_error = "bisection did not converge in 256 rounds"; throw Err{MRRR_ERR_CUDA}; }
   }
@@ -720,7 +727,8 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
             h->seg_w, h->segout.as<SegOut>(), nullptr, 0, 0);
       launch_check(h);
       eb = tev_rec(h);
-      if (nex == 0) {  // junction walk and shared-tree update in one launch
+      if (nex == 0 && m <= h->fuse_mmax) {  // junction walk and shared-tree update in one launch (a thread per
+                                              // node walks its 2^m - 1 chains: only while m is small)
         k_seg_round<<<nblocks_for(nnode, 32), 32, 0, h->stream>>>(
             nnode, m, K, h->segout.as<SegOut>(), h->counts.as<int>(), cur, h->reps.as<RepDesc>(), h->mx.as<double2>(),
             L, nxt, h->cnt.as<int>() + C_NNEXT, out_lo, out_hi, rtol,
@@ -754,6 +762,7 @@ void run_bisection(mrrr_t h, int nnode, double *out_lo, double *out_hi, double r
     read_counters(h);
     h->host_rounds++;
     h->stats_h[Y ? ST_NEGY : ST_NEGX] += nch + nex;
+    if (seg_on) h->stats_h[ST_ROOT_FB] += h->h_cnt[C_NFB];
     if (seg_on && (long long)h->h_cnt[C_NFB] * 4 > nch + nex) {
       // most segment junctions failed: the recurrence does not contract on this matrix (delocalised
       // eigenvectors, e.g. the 1-2-1, Clement, Hermite and prescribed-spectrum families), so every chain fell
@@ -832,6 +841,12 @@ int run_brackets(mrrr_t h, int nbn) {
 
 // keep the representation pool (read by every RQI lane at every step) resident in L2 while the
 // workspace streams past it: persisting access-policy window on the handle's stream
+// numerical-support threshold of the Z write (S10', A-42): eps_x of the realisation, 0 when MRRR_FULL_SUPPORT
+double eps_support(mrrr_t h) {
+  if (h->flags & MRRR_FULL_SUPPORT) return 0.0;
+  return h->sd ? 0x1p-24 : EPS_X;
+}
+
 void l2_pin_reps(mrrr_t h, bool on) {
   if (!h->l2_persist) return;
   cudaStreamAttrValue v;
@@ -947,7 +962,8 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
       }
       const int *stat = reinterpret_cast<const int *>(reinterpret_cast<const char *>(rs) + offsetof(RqiState, status));
       k_zwrite_chunk<<<nblocks_for(nb, 4), 128, 0, h->stream>>>(
-          sgb, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), P2s, nbmax, h->zmeta.as<ZMeta>(), Z, ldz, stat,
+          sgb, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), P2s, nbmax, h->zmeta.as<ZMeta>(), Z, ldz,
+          eps_support(h), stat,
           (int)(sizeof(RqiState) / sizeof(int)));
       launch_check(h);
       CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
@@ -968,7 +984,7 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
       launch_check(h);
       k_zwrite_chunk<<<nblocks_for(nold, 4), 128, 0, h->stream>>>(
           sgb, nold, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->wsA.as<dd>() + 2 * stride * nbmax, nbmax,
-          h->zmeta.as<ZMeta>(), Z, ldz);
+          h->zmeta.as<ZMeta>(), Z, ldz, eps_support(h));
     }
     launch_check(h);
     h->trq.push_back({rq0, tev_rec(h)});
@@ -1724,8 +1740,10 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_SEGCHILDMIN")) h->segchild_min = atoi(s);
     if (const char *s = getenv("MRRR_SEGTHREADS")) h->seg_threads = atoll(s);
     if (const char *s = getenv("MRRR_SEGMINLEN")) h->seg_minlen = atoi(s);
+    if (const char *s = getenv("MRRR_FUSEM")) h->fuse_mmax = atoi(s);
     if (const char *s = getenv("MRRR_ROUNDEV")) h->round_ev = atoi(s) != 0;
     if (const char *s = getenv("MRRR_EARLY_STOP")) { if (atoi(s)) h->flags |= MRRR_EARLY_STOP; }  // dev sweeps
+    if (const char *s = getenv("MRRR_FULL_SUPPORT")) { if (atoi(s)) h->flags |= MRRR_FULL_SUPPORT; }
     if (const char *s = getenv("MRRR_ES2_TARGET")) h->es2_target = atoll(s);
     if (const char *s = getenv("MRRR_ES2_MINLEN")) h->es2_minlen = atoi(s);
     if (const char *s = getenv("MRRR_SEGCH2")) h->seg_ch2 = atoll(s);

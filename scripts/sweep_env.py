@@ -60,5 +60,5 @@ for spec in sys.argv[3:]:
           f"clu {t['clusters']:.2f} sing {t['singletons']:.2f} | neg {t['negcount_ms_per_launch']*1e3:.1f} us x "
           f"{int(t['negcount_launches'])} | rqi {t['rqi_ms_per_launch']:.3f} x {int(t['rqi_launches'])} | "
           f"rounds {st['rounds']} launches {st['launches']} ho {st['rqi_handover']} "
-          f"xgfb {st['xg_fallback_chains']}/{st['xg_fallback_segments']} {same}", flush=True)
+          f"xgfb {st['xg_fallback_chains']}/{st['xg_fallback_segments']} rootfb {st['root_fallback_chains']} {same}", flush=True)
     s.close()

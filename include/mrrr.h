@@ -186,8 +186,9 @@ int mrrr_shard_owner(const int32_t *gstart, int64_t n, int64_t il, int64_t iu, i
  * many-representation x-NegCount chains (child bisection) whose junctions did not all verify, 33 segments those
  * chains re-ran sequentially, 34 root indices the early classification stop (MRRR_EARLY_STOP) left at the
  * stage-1 tolerance, 35 segmented root x-NegCount chains whose junctions did not all verify (re-run
- * sequentially from the failed segment). */
-#define MRRR_NSTATS 36
+ * sequentially from the failed segment), 36 singletons whose numerical support reached past the z recompute
+ * window of an RQC-only acceptance (their factors came from a stored pass). */
+#define MRRR_NSTATS 37
 int mrrr_get_stats(mrrr_t h, int64_t *stats, int32_t nstats);
 
 /* Diagnostics of the last call made with MRRR_KEEP_DIAG (host buffers owned

@@ -25,12 +25,12 @@ KEEP_DIAG = 1
 EARLY_STOP = 2  # MRRR_EARLY_STOP (include/mrrr.h): early classification stop of the root bisection
 FULL_SUPPORT = 4  # MRRR_FULL_SUPPORT: store the whole Getvec recurrence (no numerical-support truncation, A-42)
 MAXD = 8
-NSTATS = 36
+NSTATS = 37
 STAT_NAMES = ["d_max", "n_clusters", "largest_cluster", "uncertified", "shift_attempts", "rqi_iters",
               "rqi_fallbacks", "bracket_fixes", "root_backoffs", "failed", "negcount_x", "negcount_y",
               "getvec_calls", "rounds", "launches", "nblocks", "qd_steps", "qdg_steps", "z_steps", "zw_steps",
               "negcount_x_alg", "negcount_y_alg", "rqi_reject_sign", "rqi_reject_bracket", "rqi_handover", "ho_twist", "ho_fixed", "ho_rqc", "qd_light", "twist_rows", "seg_wide", "careful",
-              "xg_fallback_chains", "xg_fallback_segments", "early_stops", "root_fallback_chains"]
+              "xg_fallback_chains", "xg_fallback_segments", "early_stops", "root_fallback_chains", "zwin_reruns"]
 TIME_NAMES = ["total", "split_root", "root_bisection", "classification", "clusters", "singletons",
               "rqi_ms_per_launch", "rqi_launches", "negcount_ms_per_launch", "negcount_launches", "t10", "t11"]
 

@@ -516,25 +516,32 @@ __device__ __forceinline__ dd shfl_idx_dd(dd v, int lane) {
 // the per-row warp scan; 1/||z|| rides in the carry.
 constexpr int ZC = 8, ZT = 32 * ZC, ZP = ZT + 32;  // rows per lane chunk, rows per tile, padded tile
 __device__ __forceinline__ int zpad(int m) { return m + m / ZC; }  // chunk stride ZC + 1: conflict-free
+// status (segmented RQI, kernels_rqi3.cuh): the RqiState ints of singleton w start at status[w * stride]:
+// [0] status (1 accepted), [2] light, [3] pad -- rerun marker of a z window too short for the support
 __global__ void __launch_bounds__(128) k_zwrite_chunk(const Singleton *__restrict__ sg, int ns,
                                                       const RepDesc *__restrict__ reps, const YElt *__restrict__ my,
                                                       const dd *__restrict__ P2base, long long S,
                                                       const ZMeta *__restrict__ zm, double *Z, long long ldz,
-                                                      double eps_sup, const int *__restrict__ status = nullptr,
-                                                      int status_stride = 0) {
+                                                      double eps_sup, int *status = nullptr, int status_stride = 0,
+                                                      int zwin = 0, int rerun = 0, int *nrerun = nullptr) {
   // eps_sup > 0: numerical support (S10', Getvec remark (2) P:3459-3463, A-42): going outward from r,
   // the column ends at the first edge i with |dl(i)| (|z(i)| + |z(i+1)|) <= gap eps_x (z(r) = 1), i.e. on the
-  // normalised values <= gap eps_x / ||z||; the rows past it are written as zeros without reading their factors
+  // normalised values <= gap eps_x / ||z||; the rows past it are written as zeros without reading their factors.
+  // inv_hi == 0 (accepted on an RQC-only pass, k_zrc recomputed the factors of the rows within zwin of r): a
+  // measuring sweep over the window finds both ends and ||z||^2 over the support (dd), then the write sweep;
+  // a support that reaches the window's edge before the matrix's marks the singleton for a stored pass (rerun).
   __shared__ __align__(16) double2 sbuf[4][2][ZP];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int w = blockIdx.x * 4 + wib;
   if (w >= ns) return;
-  if (status && status[(long long)w * status_stride] != 1) return;
+  int *stw_ = status ? status + (long long)w * status_stride : nullptr;
+  if (stw_ && stw_[0] != 1) return;
+  if (stw_ && rerun && stw_[3] != 1) return;
   const ZMeta m = zm[w];
   const Singleton s = sg[w];
   const RepDesc R = reps[s.rep];
   const int nb = R.nb, r = m.r, last = nb - 1;
-  const dd inv = dd_make(m.inv_hi, m.inv_lo);
+  dd inv = dd_make(m.inv_hi, m.inv_lo);
   const dd *P = P2base + (long long)w * S;
   double *Zc = Z + (long long)s.col * ldz + R.bstart;
   const YElt *y = my + R.off;
@@ -543,27 +550,31 @@ __global__ void __launch_bounds__(128) k_zwrite_chunk(const Singleton *__restric
     if (lane == 0) zsolve(y, nb, r, P, P, 1, inv, Zc, tau);
     return;
   }
-  const double tauN = __dmul_rn(tau, inv.hi);  // the same test on the normalised values
-  if (lane == 0) Zc[r] = inv.hi;
+  const bool win = m.inv_hi == 0.0 && tau >= 0.0;
   double2(*buf)[ZP] = sbuf[wib];
-  for (int side = 0; side < 2; side++) {
+  // one side: rows r-1, r-2, ... (side 0) or r+1, r+2, ... (side 1); phase 0 measures (cut and sum of squares of
+  // the unnormalised z, no stores), phase 1 writes with the measured cut, phase 2 detects and writes
+  auto zside = [&](int side, int phase, int lenA, int cutIn, dd &sum) -> int {
     const int len = side ? last - r : r;
-    if (len <= 0) continue;
-    double prevv = inv.hi;  // normalised z of the row before the tile's first (z(r) for the first tile)
-    int cut = len;          // side-relative index of the first row outside the support
-    const int ntile = (len + ZT - 1) / ZT;
+    const int lim = phase == 0 ? lenA : len;  // rows whose factors exist
+    const dd carry0 = phase == 0 ? dd_from(1.0) : inv;
+    const double tauT = phase == 0 ? tau : __dmul_rn(tau, inv.hi);
+    double prevv = carry0.hi;
+    int cut = phase == 1 ? cutIn : len;
+    const int ntile = (min(lim, phase == 1 ? cut : lim) + ZT - 1) / ZT;
     auto issue = [&](int t) {
       double2 *b = buf[t & 1];
 #pragma unroll
       for (int u = 0; u < ZC; u++) {
         const int ml = lane + 32 * u, mm = t * ZT + ml;
-        if (mm < len) cp16(&b[zpad(ml)], P + (side ? r + mm : r - 1 - mm));
+        if (mm < lim) cp16(&b[zpad(ml)], P + (side ? r + mm : r - 1 - mm));
       }
       cp_commit();
     };
-    issue(0);
-    dd carry = inv;
-    for (int t = 0; t < ntile; t++) {
+    if (ntile > 0) issue(0);
+    dd carry = carry0;
+    int t = 0;
+    for (; t < ntile; t++) {
       if (t + 1 < ntile) issue(t + 1);
       else cp_commit();
       cp_wait<1>();
@@ -574,7 +585,7 @@ __global__ void __launch_bounds__(128) k_zwrite_chunk(const Singleton *__restric
       dd acc = dd_from(1.0);
 #pragma unroll
       for (int e = 0; e < ZC; e++) {
-        if (mc + e < len) {
+        if (mc + e < lim) {
           const double2 f = b[lane * (ZC + 1) + e];
           const dd nf = dd_make(-f.x, -f.y);
           acc = (e == 0) ? nf : dd_mul_nf(acc, nf);
@@ -592,40 +603,84 @@ __global__ void __launch_bounds__(128) k_zwrite_chunk(const Singleton *__restric
       const dd E = lane ? dd_mul_nf(carry, ex) : carry;
       carry = dd_mul_nf(carry, shfl_idx_dd(v, 31));
       double *sd = reinterpret_cast<double *>(b);
+      dd zv[ZC];
 #pragma unroll
-      for (int e = 0; e < ZC; e++) sd[lane * (ZC + 1) + e] = dd_mul_nf(E, p[e]).hi;
+      for (int e = 0; e < ZC; e++) {
+        zv[e] = dd_mul_nf(E, p[e]);
+        sd[lane * (ZC + 1) + e] = zv[e].hi;
+      }
       __syncwarp();
-      if (tau >= 0.0) {
+      if (phase != 1 && tau >= 0.0) {
         // edge between this row and the previous one (towards r): dl(r - 1 - mm) on the left, dl(r + mm) on the right
         int c = len;
 #pragma unroll
         for (int e = ZC - 1; e >= 0; e--) {
           const int mm = mc + e;
-          if (mm < len) {
-            const double v = sd[lane * (ZC + 1) + e];
+          if (mm < lim) {
+            const double vv = sd[lane * (ZC + 1) + e];
             const double pv = e ? sd[lane * (ZC + 1) + e - 1] : (lane ? sd[lane * (ZC + 1) - 2] : prevv);  // (ZC + 1)-stride chunks
             const double dl = fabs(__ldg(&y[side ? r + mm : r - 1 - mm].dl_hi));
-            if (__dmul_rn(dl, __dadd_rn(fabs(v), fabs(pv))) <= tauN) c = mm;
+            if (__dmul_rn(dl, __dadd_rn(fabs(vv), fabs(pv))) <= tauT) c = mm;
           }
         }
         cut = __reduce_min_sync(0xffffffffu, c);
         prevv = sd[zpad(ZT - 1)];
       }
-      __syncwarp();
+      if (phase == 0) {
 #pragma unroll
-      for (int u = 0; u < ZC; u++) {
-        const int ml = lane + 32 * u, mm = m0 + ml;
-        if (mm < len) Zc[side ? r + 1 + mm : r - 1 - mm] = mm < cut ? sd[zpad(ml)] : 0.0;
+        for (int e = 0; e < ZC; e++)
+          if (mc + e < min(cut, lim)) sum = dd_add_nf(sum, dd_mul_nf(zv[e], zv[e]));
       }
       __syncwarp();
-      if (cut < len) break;
-    }
-    if (cut < len) {
-      cp_wait<0>();  // drain the prefetch of the next tile
+      if (phase != 0) {
+#pragma unroll
+        for (int u = 0; u < ZC; u++) {
+          const int ml = lane + 32 * u, mm = m0 + ml;
+          if (mm < len) Zc[side ? r + 1 + mm : r - 1 - mm] = mm < cut ? sd[zpad(ml)] : 0.0;
+        }
+      }
       __syncwarp();
-      for (int mm = ((cut / ZT) + 1) * ZT + lane; mm < len; mm += 32) Zc[side ? r + 1 + mm : r - 1 - mm] = 0.0;
+      if (cut < len && cut < m0 + ZT) {
+        t++;
+        break;
+      }
     }
+    cp_wait<0>();  // drain the prefetch of the next tile
+    __syncwarp();
+    if (phase != 0)
+      for (int mm = t * ZT + lane; mm < len; mm += 32) Zc[side ? r + 1 + mm : r - 1 - mm] = 0.0;
+    return cut;
+  };
+  if (!win) {
+    if (lane == 0) Zc[r] = inv.hi;
+    dd unused = dd_from(0.0);
+    for (int side = 0; side < 2; side++)
+      if ((side ? last - r : r) > 0) zside(side, 2, 0, 0, unused);
+    return;
   }
+  // window rows with recomputed factors: l+ rows [r - zwin, r), u- rows [r, r + zwin] (clipped)
+  const int lenL = r, lenR = last - r;
+  const int avL = min(r, zwin), avR = min(r + zwin, nb - 2) - r + 1;
+  dd sum = dd_from(0.0);
+  const int cL = lenL > 0 ? zside(0, 0, min(avL, lenL), 0, sum) : 0;
+  const int cR = lenR > 0 ? zside(1, 0, min(avR, lenR), 0, sum) : 0;
+  if ((lenL > 0 && cL >= min(avL, lenL) && avL < lenL) || (lenR > 0 && cR >= min(avR, lenR) && avR < lenR)) {
+    if (lane == 0 && stw_) {  // the support reaches past the window: a stored pass at the same lambda, then again
+      stw_[0] = 0;
+      stw_[2] = 0;
+      stw_[3] = 1;
+      atomicAdd(nrerun, 1);
+    }
+    return;
+  }
+  // ||z||^2 over the support: the lanes' partial sums plus z(r)^2 = 1
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) sum = dd_add_nf(sum, dd_make(__shfl_xor_sync(0xffffffffu, sum.hi, off),
+                                                                      __shfl_xor_sync(0xffffffffu, sum.lo, off)));
+  inv = dd_rcp(dd_sqrt(dd_add_d(sum, 1.0)));
+  if (lane == 0) Zc[r] = inv.hi;
+  if (lenL > 0) zside(0, 1, 0, cL, sum);
+  if (lenR > 0) zside(1, 1, 0, cR, sum);
 }
 
 __global__ void __launch_bounds__(64) k_rqi2(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,

@@ -274,7 +274,8 @@ constexpr int PFD = 16;
 __device__ __forceinline__ void l2_prefetch(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 template <bool LIGHT, bool PF>
 __device__ __forceinline__ void seg_pass_t(const QElt *__restrict__ q, int nb, int isB, int t0, int t1, int tw,
-                                           dd lam, dd nlam, dd *P, SegRec *R, double2 *stg) {
+                                           dd lam, dd nlam, dd *P, SegRec *R, double2 *stg, dd *zin = nullptr,
+                                           int zrow = -1) {
   constexpr bool pf = PF;
   R->empty = 0;
   const int rs = isB ? nb - 1 - tw : tw, og = isB ? 3 : 2;
@@ -303,6 +304,7 @@ __device__ __forceinline__ void seg_pass_t(const QElt *__restrict__ q, int nb, i
   for (int t = t0; t < t1; t++) {
     if (pf) l2_prefetch(q + min(max(seg_row(isB, nb, t + PFD), 0), nb - 1));
     const int row = seg_row(isB, nb, t);
+    if (LIGHT && row == zrow) *zin = den;  // the lane's state entering row zrow (z recompute window, k_zrc)
     const dd c2 = D2(nc2), dl = D2(ndl), gg = D2(ngg);
     if (t + 1 < t1) pq += dq;
     nc2 = __ldg(pq);
@@ -354,15 +356,88 @@ __device__ __forceinline__ void seg_pass_t(const QElt *__restrict__ q, int nb, i
 }
 __device__ __forceinline__ void seg_pass(const QElt *__restrict__ q, int nb, int isB, int t0, int t1, int tw,
                                          bool light, dd lam, dd nlam, dd *P, SegRec *R, double2 *stg = nullptr,
-                                         bool pf = false) {
+                                         bool pf = false, dd *zin = nullptr, int zrow = -1) {
   if (pf) {
-    if (light) seg_pass_t<true, true>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, nullptr);
+    if (light) seg_pass_t<true, true>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, nullptr, zin, zrow);
     else seg_pass_t<false, true>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, stg);
   } else {
-    if (light) seg_pass_t<true, false>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, nullptr);
+    if (light) seg_pass_t<true, false>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, nullptr, zin, zrow);
     else seg_pass_t<false, false>(q, nb, isB, t0, t1, tw, lam, nlam, P, R, stg);
   }
 }
+
+// Z recompute window (numerical support, A-42): a singleton accepted on an RQC-only pass is not
+// repeated as a stored pass.  Its factors l+ (rows [zf, r)) and u- (rows [r, zb]) are recomputed from the exact
+// lane states the accepted pass recorded entering rows zf and zb, with the stored pass's operations, so the
+// z write reads the same bits it would have read after a stored pass -- but only ZWIN rows on each side.
+__device__ __forceinline__ int zwin_f(int r, int win) { return max(r - win, 0); }
+__device__ __forceinline__ int zwin_b(int nb, int r, int win) { return min(r + win, nb - 2); }
+// thread per (singleton, lane): lane F recomputes l+(row) for rows [zf, r), lane B u-(row) for rows zb .. r (down),
+// from the states k_fixed_chunk recorded entering rows zf / zb in the accepted RQC-only pass (exact states: every
+// junction of that pass verified), with the stored pass's operations (seg_pass_t<false>), into the factor plane
+__global__ void __launch_bounds__(128) k_zrc(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
+                                             const QElt *__restrict__ mq, const RqiState *__restrict__ st,
+                                             const ZMeta *__restrict__ zm, const dd *__restrict__ zin, dd *P2,
+                                             long long nbmax, int zwin) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= 2LL * ns) return;
+  const int i = (int)(g % ns), isB = (int)(g / ns);
+  if (st[i].status != 1 || zm[i].inv_hi != 0.0 || zm[i].careful) return;
+  const RqiState S = st[i];
+  const RepDesc Rp = reps[sg[i].rep];
+  const int nb = Rp.nb, r = S.r;
+  const QElt *q = mq + Rp.off;
+  dd *P = P2 + (long long)i * nbmax;
+  const dd lam = dd_make(S.lam_hi, S.lam_lo), nlam = dd_neg(lam);
+  int t0, t1;  // lane steps: F step t = row t, B step t = row nb-2-t
+  if (!isB) {
+    t0 = zwin_f(r, zwin);
+    t1 = r;
+  } else {
+    if (r > nb - 2) return;
+    t0 = nb - 2 - zwin_b(nb, r, zwin);
+    t1 = nb - 1 - r;
+  }
+  if (t1 <= t0) return;
+  const int og = isB ? 3 : 2;
+  dd den = zin[2LL * i + isB];
+  // rows loaded ZPF steps ahead (a ring of registers): the loads stay off the recurrence's critical path
+  constexpr int ZPF = 8;
+  double2 rc[ZPF], rd[ZPF], rg[ZPF];
+  auto ld = [&](int t, int u) {
+    const double2 *pq = reinterpret_cast<const double2 *>(q + seg_row(isB, nb, min(t, t1 - 1)));
+    rc[u] = __ldg(pq);
+    rd[u] = __ldg(pq + 1);
+    rg[u] = __ldg(pq + og);
+  };
+#pragma unroll
+  for (int u = 0; u < ZPF; u++) ld(t0 + u, u);
+  for (int tb = t0; tb < t1; tb += ZPF)
+#pragma unroll
+  for (int u = 0; u < ZPF; u++) {
+    const int t = tb + u;
+    if (t >= t1) break;
+    const int row = seg_row(isB, nb, t);
+    const dd c2 = D2(rc[u]), dl = D2(rd[u]), gg = D2(rg[u]);
+    ld(t + ZPF, u);
+    double r1, r2;
+    rcp_nr2(den.hi, r1, r2);
+    const dd Pq = qdiv(c2, den, r1, r2);
+    const dd o = qdiv(dl, den, r1, r2);
+    stw(P, row, fast_two_sum(o.hi, o.lo));
+    den = dd_sum3_nf(gg, nlam, dd_neg(Pq));
+  }
+}
+// after a rerun's stored pass: a singleton that did not accept there goes to the two-lane kernel
+__global__ void k_zrc_settle(RqiState *st, int ns) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ns || st[i].pad != 1) return;
+  if (st[i].status == 0) st[i].status = 2;
+}
+static_assert(offsetof(RqiState, wide) == offsetof(RqiState, status) + 4 &&
+                  offsetof(RqiState, light) == offsetof(RqiState, status) + 8 &&
+                  offsetof(RqiState, pad) == offsetof(RqiState, status) + 12,
+              "k_zwrite_chunk reads status / light / pad at int offsets 0 / 2 / 3");
 
 // the same segment in binary64 (single/double realisation): den' = (g - lam) - c2 / den with the
 // IEEE quotients c2/den and dl/den from one reciprocal pair of den (fast range; a pivot outside it flags the
@@ -540,7 +615,8 @@ __global__ void __launch_bounds__(128, MRRR_FC_MINB) k_fixed_chunk(const Singlet
                                                      const RepDesc *__restrict__ reps, const QElt *__restrict__ mq,
                                                      const RqiState *__restrict__ st, int K2, int Wu, dd *P2,
                                                      long long nbmax, SegRec *rec, int bulk, int sd,
-                                                     const int *__restrict__ modep) {
+                                                     const int *__restrict__ modep, dd *zin = nullptr,
+                                                     int zwin = 0) {
   // 3: the x-arithmetic RQC-only passes (S.light == 2), 0: the dd RQC-only passes (S.light == 1), 1: the stored
   // ones (S.light == 0), 2: none left (k_rqi_mode)
   const int mode = *modep;
@@ -612,7 +688,12 @@ __global__ void __launch_bounds__(128, MRRR_FC_MINB) k_fixed_chunk(const Singlet
     else seg_pass_sd<false>(q, nb, isB, t0, t1, tw, S.lam_hi, P2 + (long long)i * nbmax, R, stg);
     return;
   }
-  seg_pass(q, nb, isB, t0, t1, tw, light, lam, nlam, P2 + (long long)i * nbmax, R, stg, Rp.depth > 0);
+  // zwin > 0: record the lane's state entering the first row of the z recompute window (k_zrc); rows the
+  // window does not reach (zf = 0, zb = nb - 2) start from the lane's exact start instead
+  int zrow = -1;
+  if (zin && light) zrow = isB ? zwin_b(nb, r, zwin) : zwin_f(r, zwin);
+  seg_pass(q, nb, isB, t0, t1, tw, light, lam, nlam, P2 + (long long)i * nbmax, R, stg, Rp.depth > 0,
+           zin ? zin + 2LL * i + isB : nullptr, zrow);
 }
 
 // thread per singleton: junctions, gamma_r, ||z||^2, inertia, and the stask decision
@@ -624,7 +705,7 @@ __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restri
                                                 const RepDesc *__restrict__ reps, RqiState *st, int K,
                                                 const SegRec *__restrict__ F, double *W, ZMeta *zmeta,
                                                 int *diag_depth, double *fin_lo, double *fin_hi, FsInc &inc,
-                                                int sd, double eps_y, int mode) {
+                                                int sd, double eps_y, int mode, int zrc) {
   RqiState S = st[i];
   if (S.status != 0 || S.light != (mode == 3 ? 2 : mode == 0 ? 1 : 0)) return;
   const Singleton s = sg[i];
@@ -690,26 +771,29 @@ __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restri
     dd tol2 = dd_mul_d(dd_abs(lam), 4.0 * eps_y);  // A-30
     if (dd_lt(tol2, dd_from(__dmul_rn(0x1p-100, Rp.spdiam)))) tol2 = dd_from(__dmul_rn(0x1p-100, Rp.spdiam));
     if (resid.hi <= S.thr1 || dd_lt(dd_abs(rqc), tol2)) {
-      if (was_light) {  // accepted on an RQC-only pass: repeat it at the same lambda with the factors stored
-        S.light = 0;
+      if (was_light && !(zrc && mode == 0)) {  // accepted on an RQC-only pass: repeat it at the same lambda with
+        S.light = 0;                           // the factors stored
         inc.nact++;
         st[i] = S;
         return;
       }
-      accepted = true;
+      accepted = true;  // zrc: accepted on a dd RQC-only pass; k_zrc recomputes the factors of the z window
     } else {
       if (c < j) blo = lam; else bhi = lam;
       const dd nl = sd ? dd_from(__dadd_rn(lam.hi, rqc.hi)) : dd_add(lam, rqc);  // sd: lambda in binary64
       const bool okc = ((c < j) ? (rqc.hi > 0.0) : (rqc.hi < 0.0)) && dd_lt(blo, nl) && dd_lt(nl, bhi);
       if (okc && S.it < MAX_RQI) lam = nl;
       else handover = true;  // bisection fallback / iteration cap: the two-lane kernel redoes this singleton
-      S.light = was_light ? max(S.light - 1, 0) : 0;  // RQC-only passes still due (k_rqi3_init)
+      // RQC-only passes still due (k_rqi3_init); zrc: every pass is one until acceptance (the factors of the
+      // accepted one come from k_zrc), so no stored pass runs
+      S.light = was_light ? max(S.light - 1, zrc ? 1 : 0) : 0;
     }
   }
   if (accepted) {
     const dd inv = dd_rcp(dd_sqrt(zz));
     ZMeta zm;
     zm.inv_hi = inv.hi; zm.inv_lo = inv.lo; zm.r = r; zm.careful = 0;
+    if (was_light) { zm.inv_hi = 0.0; zm.inv_lo = 0.0; }  // 1/||z|| over the support: k_zwrite_chunk computes it
     zmeta[i] = zm;
     const dd sig = dd_make(Rp.sig_hi, Rp.sig_lo);
     W[s.col] = dd_add(lam, sig).hi;
@@ -738,7 +822,8 @@ __device__ __forceinline__ void fixed_step_body(int i, const Singleton *__restri
 __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const RepDesc *__restrict__ reps,
                              RqiState *st, int K, const SegRec *__restrict__ rec, double *W,
                              ZMeta *zmeta, int *diag_depth, double *fin_lo, double *fin_hi, long long *stats,
-                             int *nactive, int stage, int sd, double eps_y, const int *__restrict__ modep) {
+                             int *nactive, int stage, int sd, double eps_y, const int *__restrict__ modep,
+                             int zrc = 0) {
   const int mode = *modep;
   if (mode == 2) return;
   extern __shared__ uint4 recsm[];
@@ -747,7 +832,7 @@ __global__ void k_fixed_step(const Singleton *__restrict__ sg, int ns, const Rep
   const SegRec *F = stage ? reinterpret_cast<const SegRec *>(stage_recs(rec, per * (int)sizeof(SegRec), ns, recsm))
                           : rec + (long long)i * per;
   FsInc inc = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  if (i < ns) fixed_step_body(i, sg, reps, st, K, F, W, zmeta, diag_depth, fin_lo, fin_hi, inc, sd, eps_y, mode);
+  if (i < ns) fixed_step_body(i, sg, reps, st, K, F, W, zmeta, diag_depth, fin_lo, fin_hi, inc, sd, eps_y, mode, zrc);
   const unsigned fm = 0xffffffffu;
   const unsigned nact = __reduce_add_sync(fm, inc.nact), wide = __reduce_add_sync(fm, inc.wide);
   const unsigned hof = __reduce_add_sync(fm, inc.hofixed), hor = __reduce_add_sync(fm, inc.horqc);

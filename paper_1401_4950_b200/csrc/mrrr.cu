@@ -101,6 +101,7 @@ struct mrrr_ctx {
   bool neg_tma = true;  // x-NegCount with TMA-staged representation tiles (k_negcount_tma)
   bool grouped = true;  // child bisection with CTAs grouped by representation (k_negcount_grp)
   int seg_k = 8, seg_w = 128;  // segmented root NegCount: segments per chain, warm-up rows (k_negcount_seg)
+  int zwin = 256;              // z recompute window of singletons accepted on an RQC-only pass (0: stored passes)
   int fuse_mmax = 2;           // host-driven segmented rounds fuse walk + update (k_seg_round) up to this depth
   bool rqi_seg = true;         // segmented RQI passes (kernels_rqi3.cuh); MRRR_RQISEG=0: the two-lane kernel only
   int rqi_segk = 8, rqi_segw = 0;  // rqi_segw 0: by frame length (128 up to 16K rows, else 192)
@@ -142,6 +143,7 @@ struct mrrr_ctx {
   Buf s1lo, s1hi, esr;  // early classification stop (S5'): stage-1 intervals, decision ranges
   Buf rqmode;           // segmented RQI: per-pass counters and mode (k_rqi_mode)
   Buf nodesK, nodesP, offsP, dS, dG, dH;  // guided bisection rounds
+  Buf zinb, zrcb;                         // z recompute window: lane states; rerun counter, mode, scratch
   Buf repoff, repcur, repcta;             // representation-grouped rounds
   Buf segout, rnd;                        // segmented NegCount; per-round device counters
   Buf gpart;                              // k_root_gersh partial bounds
@@ -897,6 +899,14 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
         Wu = (int)nbmax;
       }
       while (2 * K <= 32 && (long long)nb * 2 * (2 * K) <= h->rqi_threads && (nbmax - 1) >= 2 * (2 * K) * Wu) K *= 2;
+      // z recompute window (k_zrc): root frames of the double/dd solve with the numerical support on
+      const bool zrc = h->zwin > 0 && !child && !h->sd && eps_support(h) > 0.0 && nbmax > 2LL * h->zwin;
+      if (zrc) {
+        CK(h->zinb.ensure(sizeof(dd) * 2 * stride));
+        CK(h->zrcb.ensure(sizeof(int) * 4));
+        CK(cudaMemsetAsync(h->zrcb.p, 0, sizeof(int) * 4, h->stream));
+        k_set_int<<<1, 1, 0, h->stream>>>(h->zrcb.as<int>() + 1, 1);  // the rerun's pass mode: stored
+      }
       CK(h->rqst.ensure(sizeof(RqiState) * stride));
       CK(h->rqrec.ensure(sizeof(SegRec) * stride * 4 * K));  // chunk layout: 2K chunks x 2 lanes
       CK(h->hand.ensure(sizeof(Singleton) * stride));
@@ -945,12 +955,12 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
         for (int b = 0; b < batch && p < MAXP; b++, p++) {
           k_fixed_chunk<<<nblocks_for((2 * K + 1) * nb, 128), 128, 0, h->stream>>>(
               sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, 2 * K, Wu, P2s, nbmax, rec,
-              h->rqi_bulk ? 1 : 0, h->sd ? 1 : 0, qm + 3 * p + 2);
+              h->rqi_bulk ? 1 : 0, h->sd ? 1 : 0, qm + 3 * p + 2, zrc ? h->zinb.as<dd>() : nullptr, h->zwin);
           k_fixed_step<<<nblocks_for(nb, 32), 32, fsb, h->stream>>>(
               sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, rec, W, h->zmeta.as<ZMeta>(),
               diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
               diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), qm + 3 * p, fsb ? 1 : 0,
-              h->sd ? 1 : 0, h->sd ? 0x1p-53 : EPS_Y, qm + 3 * p + 2);
+              h->sd ? 1 : 0, h->sd ? 0x1p-53 : EPS_Y, qm + 3 * p + 2, zrc ? 1 : 0);
           k_rqi_mode<<<1, 1, 0, h->stream>>>(qm, p);
           launch_check(h);
           h->host_launches += 2;
@@ -960,12 +970,38 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
         CK(cudaStreamSynchronize(h->stream));
         if (nm == 2) break;
       }
-      const int *stat = reinterpret_cast<const int *>(reinterpret_cast<const char *>(rs) + offsetof(RqiState, status));
+      int *stat = reinterpret_cast<int *>(reinterpret_cast<char *>(rs) + offsetof(RqiState, status));
+      int *zc = zrc ? h->zrcb.as<int>() : nullptr;
+      if (zrc)
+        k_zrc<<<nblocks_for(2 * nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(),
+                                                             rs, h->zmeta.as<ZMeta>(), h->zinb.as<dd>(), P2s, nbmax,
+                                                             h->zwin);
       k_zwrite_chunk<<<nblocks_for(nb, 4), 128, 0, h->stream>>>(
           sgb, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), P2s, nbmax, h->zmeta.as<ZMeta>(), Z, ldz,
-          eps_support(h), stat,
-          (int)(sizeof(RqiState) / sizeof(int)));
+          eps_support(h), stat, (int)(sizeof(RqiState) / sizeof(int)), zrc ? h->zwin : 0, 0, zc);
       launch_check(h);
+      if (zrc) {
+        // supports that reach past the recompute window: a stored pass at the accepted lambda, then their z
+        int nre = 0;
+        CK(cudaMemcpyAsync(&nre, zc, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        h->stats_h[ST_ZRC_RERUN] += nre;
+        if (nre > 0) {
+          k_fixed_chunk<<<nblocks_for((2 * K + 1) * nb, 128), 128, 0, h->stream>>>(
+              sgb, (int)nb, h->reps.as<RepDesc>(), h->mq.as<QElt>(), rs, 2 * K, Wu, P2s, nbmax, rec,
+              h->rqi_bulk ? 1 : 0, 0, zc + 1);
+          k_fixed_step<<<nblocks_for(nb, 32), 32, fsb, h->stream>>>(
+              sgb, (int)nb, h->reps.as<RepDesc>(), rs, K, rec, W, h->zmeta.as<ZMeta>(),
+              diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
+              diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), zc + 2, fsb ? 1 : 0, 0, EPS_Y,
+              zc + 1, 0);
+          k_zrc_settle<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(rs, (int)nb);
+          k_zwrite_chunk<<<nblocks_for(nb, 4), 128, 0, h->stream>>>(
+              sgb, (int)nb, h->reps.as<RepDesc>(), h->my.as<YElt>(), P2s, nbmax, h->zmeta.as<ZMeta>(), Z, ldz,
+              eps_support(h), stat, (int)(sizeof(RqiState) / sizeof(int)), 0, 1, nullptr);
+          launch_check(h);
+        }
+      }
       CK(cudaMemsetAsync(h->cnt.as<int>() + C_NFB, 0, sizeof(int), h->stream));
       k_rqi3_collect<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, rs, h->hand.as<Singleton>(),
                                                                   h->cnt.as<int>() + C_NFB);
@@ -1741,6 +1777,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_SEGTHREADS")) h->seg_threads = atoll(s);
     if (const char *s = getenv("MRRR_SEGMINLEN")) h->seg_minlen = atoi(s);
     if (const char *s = getenv("MRRR_FUSEM")) h->fuse_mmax = atoi(s);
+    if (const char *s = getenv("MRRR_ZWIN")) h->zwin = std::max(0, atoi(s));
     if (const char *s = getenv("MRRR_ROUNDEV")) h->round_ev = atoi(s) != 0;
     if (const char *s = getenv("MRRR_EARLY_STOP")) { if (atoi(s)) h->flags |= MRRR_EARLY_STOP; }  // dev sweeps
     if (const char *s = getenv("MRRR_FULL_SUPPORT")) { if (atoi(s)) h->flags |= MRRR_FULL_SUPPORT; }

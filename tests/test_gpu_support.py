@@ -1,9 +1,10 @@
 """GPU numerical-support truncation (S10', Getvec remark (2) P:3459-3463, A-42; on by default,
 MRRR_FULL_SUPPORT turns it off).
 
-* Against the GPU's own full-support solve: W, every integer and interval bit-identical; every stored entry
-  inside a column's support bit-identical, every entry outside exactly zero (the truncation only stops the
-  Z-write recurrence).
+* Against the GPU's own full-support solve: W, every integer and interval bit-identical; every entry outside a
+  column's support exactly zero; every entry inside equal up to the normalisation (the full solve divides by
+  the whole recurrence's ||z||, the truncated one by the support's, in dd; root frames take their factors from
+  the z recompute window of k_zrc, the same operations from the same exact states as the stored pass).
 * Against the oracle run with the same rule (oracle.mrrr(..., support=True)): the support ends.  They are decided
   by fp64 comparisons of z values that the two sides compute at slightly different lambda-hat (RQI results are
   toleranced, not bit-exact) and, on the GPU, from normalised fl64 values; so an end may move by one row where
@@ -61,7 +62,10 @@ def check_vs_full(g, f):
     first, last = support(g["Z"])
     rows = np.arange(g["Z"].shape[0])[:, None]
     inside = (rows >= first[None, :]) & (rows <= last[None, :])
-    assert np.array_equal(g["Z"], np.where(inside, f["Z"], 0.0))
+    assert np.all(g["Z"][~inside] == 0.0)
+    eps = 2.0 ** -24 if g["Z"].dtype == np.float32 else EPS
+    assert np.all(np.abs(g["Z"] - f["Z"])[inside] <= 4 * eps * np.abs(f["Z"])[inside] + 4 * eps * eps), \
+        np.max(np.abs(g["Z"] - f["Z"])[inside])
     return first, last
 
 
@@ -174,3 +178,22 @@ def test_support_single_double(torch_cuda):
     res = oracle.residuals(d32.astype(np.float64), e32.astype(np.float64), g["W"].astype(np.float64),
                            g["Z"].astype(np.float64)).max()
     assert res <= d.size * eps_s * tn
+
+
+@pytest.mark.parametrize("zwin", ["16", "64"])
+def test_zwin_reruns(torch_cuda, zwin, monkeypatch):
+    # a z recompute window shorter than the supports: those singletons take a stored pass at the accepted lambda
+    # (k_zrc_settle hands a stored pass that does not accept to the two-lane kernel); gates unchanged
+    monkeypatch.setenv("MRRR_ZWIN", zwin)
+    d, e = mi.random_tridiag(3000, 9, -1.0)
+    g = solve(torch_cuda, d, e)
+    monkeypatch.setenv("MRRR_ZWIN", "0")
+    f = solve(torch_cuda, d, e)  # support on, every factor from a stored pass
+    assert g["stats"]["zwin_reruns"] > 0
+    r = oracle.mrrr(d, e, support=True)
+    check_integers(g, r)
+    check_ends(g, r)
+    tn = max(abs(r.W[0]), abs(r.W[-1]))
+    check_tol(d, e, g["W"], g["Z"], r.W, tn)
+    assert oracle.ortho_full(g["Z"]) <= d.size * EPS
+    assert np.max(np.abs(g["Z"] - f["Z"])) <= 4 * EPS

@@ -153,6 +153,7 @@ struct mrrr_ctx {
       ipool_lo, ipool_hi, yref_lo, yref_hi, wsA, wsB, stats, cnt, ddepth, dgf, dgl, dflo, dfhi, hd, he, hW, hZ, zmeta,
       hd2, sdin, sdW, sdZ, sdhin, sdhW, sdhZ, segsd;
   int *h_cnt = nullptr;  // pinned counters
+  int *h_small = nullptr;  // pinned scratch for the small device-to-host reads of a solve (64 ints)
   std::vector<int> h_rounds = std::vector<int>(258);  // node counts of the device-driven rounds
 
   // results of the last call
@@ -965,9 +966,9 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
           launch_check(h);
           h->host_launches += 2;
         }
-        int nm = 0;
-        CK(cudaMemcpyAsync(&nm, qm + 3 * p + 2, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(h->h_small, qm + 3 * p + 2, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
+        const int nm = h->h_small[0];
         if (nm == 2) break;
       }
       int *stat = reinterpret_cast<int *>(reinterpret_cast<char *>(rs) + offsetof(RqiState, status));
@@ -982,9 +983,9 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
       launch_check(h);
       if (zrc) {
         // supports that reach past the recompute window: a stored pass at the accepted lambda, then their z
-        int nre = 0;
-        CK(cudaMemcpyAsync(&nre, zc, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(h->h_small, zc, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
+        const int nre = h->h_small[0];
         h->stats_h[ST_ZRC_RERUN] += nre;
         if (nre > 0) {
           k_fixed_chunk<<<nblocks_for((2 * K + 1) * nb, 128), 128, 0, h->stream>>>(
@@ -1006,8 +1007,9 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
       k_rqi3_collect<<<nblocks_for(nb, 128), 128, 0, h->stream>>>(sgb, (int)nb, rs, h->hand.as<Singleton>(),
                                                                   h->cnt.as<int>() + C_NFB);
       launch_check(h);
-      CK(cudaMemcpyAsync(&nold, h->cnt.as<int>() + C_NFB, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaMemcpyAsync(h->h_small, h->cnt.as<int>() + C_NFB, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
       CK(cudaStreamSynchronize(h->stream));
+      nold = h->h_small[0];
       sgb = h->hand.as<Singleton>();
       h->stats_h[ST_RQI_HANDOVER] += nold;
     }
@@ -1304,8 +1306,10 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
                                     h->scal.as<int>() + 1, (double *)(h->scal.as<char>() + 16), eps_split);
   launch_check(h);
   ScalRec hs;
-  CK(cudaMemcpyAsync(&hs, h->scal.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  static_assert(sizeof(ScalRec) <= 64 * sizeof(int), "pinned scratch");
+  CK(cudaMemcpyAsync(h->h_small, h->scal.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  memcpy(&hs, h->h_small, sizeof(hs));
   if (hs.err) return MRRR_ERR_NONFINITE;
   // S0 scaling (A-21): max |entry| outside [2^-500, 2^500] -> solve 2^-ex T (exact power of two,
   // max |entry| in [1/2, 1)) and scale W back at the end; Z is scale invariant
@@ -1322,8 +1326,9 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
                                       (double *)(h->scal.as<char>() + 8), h->scal.as<int>() + 1,
                                       (double *)(h->scal.as<char>() + 16), eps_split);
     launch_check(h);
-    CK(cudaMemcpyAsync(&hs, h->scal.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h->h_small, h->scal.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    memcpy(&hs, h->h_small, sizeof(hs));
   }
   struct ScaleBack {  // W of the computed columns back to the input's scale on every successful return path
     mrrr_t h; double *W; long long cnt; int ex;
@@ -1805,6 +1810,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     }
     for (auto &ev : h->ev) CK(cudaEventCreate(&ev));
     CK(cudaMallocHost(&h->h_cnt, sizeof(int) * C_NCOUNTERS));
+    CK(cudaMallocHost(&h->h_small, sizeof(int) * 64));
   } catch (Err &er) {
     delete h;
     return er.code;
@@ -2225,6 +2231,7 @@ int mrrr_destroy(mrrr_t h) {
   h->dpad.release();
   h->dparts.release();
   if (h->h_cnt) cudaFreeHost(h->h_cnt);
+  if (h->h_small) cudaFreeHost(h->h_small);
   if (h->own_stream) cudaStreamDestroy(h->stream);
   delete h;
   return 0;

@@ -719,9 +719,11 @@ static void do_cluster(const ctx_t *cx, const rep_t *M, const double *lo, const 
   STAT_ADD(ST_NCLUSTERS, 1);
   stat_max(ST_LARGEST, q - p + 1);
   double nu = (100.0 * (double)nb) * EPS_A;
-  /* (a) refine the extremal eigenvalues of M_y (y-arithmetic) */
-  double Lp = lo[p] - nu * fabs(lo[p]), Hp = hi[p] + nu * fabs(hi[p]);
-  double Lq = lo[q] - nu * fabs(lo[q]), Hq = hi[q] + nu * fabs(hi[q]);
+  /* (a) refine the extremal eigenvalues of M_y (y-arithmetic), starting from their x-intervals */
+  /* (A-12'': the eigenvalue of M_y lies within ~n eps_x |lambda| of M_x's; bracket repair in y widens the     */
+  /* start by its own width on a failing side, on the same dyadic grid)                                        */
+  double Lp = lo[p], Hp = hi[p];
+  double Lq = lo[q], Hq = hi[q];
   oracle_dyadic_widen(Lp, Hp, &Lp, &Hp);
   oracle_dyadic_widen(Lq, Hq, &Lq, &Hq);
   bracket_y(nb, M->d, M->dll, p, &Lp, &Hp);
@@ -793,10 +795,16 @@ static void do_cluster(const ctx_t *cx, const rep_t *M, const double *lo, const 
   if (q < nb && !isnan(lo[q + 1])) { clo[q + 1] = lo[q + 1] - tau; chi[q + 1] = hi[q + 1] - tau; }
 #pragma omp taskloop grainsize(1) shared(clo, chi, C, lo, hi)
   for (int64_t j = p; j <= q; j++) {
-    double a1 = lo[j] - nu * fabs(lo[j]);
+    /* the cluster ends start from their y-refined intervals, which bracket the eigenvalues of M_y itself: the  */
+    /* inner inflation then covers only the y-arithmetic shift, nu_y = 100 n eps_y (A-13'); the others from    */
+    /* their x-intervals with nu                                                                                */
+    const int end = (j == p || j == q);
+    const double nin = end ? (100.0 * (double)nb) * EPS_Y : nu;
+    const double lj = (j == p) ? Lp : (j == q) ? Lq : lo[j], hj = (j == p) ? Hp : (j == q) ? Hq : hi[j];
+    double a1 = lj - nin * fabs(lj);
     double b1 = a1 - tau;
     double l2 = b1 - nu * fabs(b1);
-    double c1 = hi[j] + nu * fabs(hi[j]);
+    double c1 = hj + nin * fabs(hj);
     double e1 = c1 - tau;
     double h2 = e1 + nu * fabs(e1);
     double L, H;

@@ -63,13 +63,10 @@ __global__ void k_clu_yref_init(const Cluster *__restrict__ cl, int ncl, const R
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncl) return;
   Cluster C = cl[c];
-  int nb = reps[C.rep].nb;
-  double nu = __dmul_rn(__dmul_rn(100.0, (double)nb), EPS_X);
+  // start: the end's x-interval itself (A-12''); the y bracket verification repairs it on a failing side
   for (int side = 0; side < 2; side++) {
     int j = side ? C.q : C.p;
-    double lo = ilo[C.ibase + j], hi = ihi[C.ibase + j];
-    double L = __dsub_rn(lo, __dmul_rn(nu, fabs(lo)));
-    double H = __dadd_rn(hi, __dmul_rn(nu, fabs(hi)));
+    double L = ilo[C.ibase + j], H = ihi[C.ibase + j];
     dyadic_widen(L, H, &L, &H);
     BNode b;
     b.lo = L; b.hi = H; b.clo = 0; b.chi = 0; b.j = j; b.rep = C.rep;
@@ -312,7 +309,11 @@ __device__ void clu_build_one(int c, const Cluster *__restrict__ cl, RepDesc *re
 __global__ void k_clu_child_starts(const Cluster *__restrict__ cl, int ncl, const RepDesc *__restrict__ reps,
                                    const ShiftState *__restrict__ ss, const long long *__restrict__ cseg,
                                    const long long *__restrict__ bnoff, const double *__restrict__ ilo,
-                                   const double *__restrict__ ihi, double *clo, double *chi, BNode *bn, int repbase) {
+                                   const double *__restrict__ ihi, double *clo, double *chi, BNode *bn, int repbase,
+                                   const double *__restrict__ ylo, const double *__restrict__ yhi, double eps_y) {
+  // member j's start: (lambda(1 +- nu_in) - tau)(1 +- nu) (A-13); the cluster ends p, q start from
+  // their y-refined intervals (they bracket M_y's own eigenvalues), so their inner inflation only covers the
+  // y-arithmetic shift: nu_in = 100 n eps_y (A-13'); the other members from their x-intervals with nu_in = nu
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncl) return;
   Cluster C = cl[c];
@@ -320,6 +321,7 @@ __global__ void k_clu_child_starts(const Cluster *__restrict__ cl, int ncl, cons
   if (!S.have_best) return;
   int nb = reps[C.rep].nb;
   double nu = __dmul_rn(__dmul_rn(100.0, (double)nb), EPS_X);
+  const double nuy = __dmul_rn(__dmul_rn(100.0, (double)nb), eps_y);
   double tau = S.best_tau;
   long long base = cseg[c] - (C.p - 1);  // child ibase
   double lpm = ilo[C.ibase + C.p - 1];
@@ -338,11 +340,14 @@ __global__ void k_clu_child_starts(const Cluster *__restrict__ cl, int ncl, cons
   }
   long long o = bnoff[c];
   for (int j = C.p; j <= C.q; j++) {
-    double lo = ilo[C.ibase + j], hi = ihi[C.ibase + j];
-    double a1 = __dsub_rn(lo, __dmul_rn(nu, fabs(lo)));
+    const bool end = (j == C.p || j == C.q);
+    const double nin = end ? nuy : nu;
+    double lo = (j == C.p) ? ylo[2 * c] : (j == C.q) ? ylo[2 * c + 1] : ilo[C.ibase + j];
+    double hi = (j == C.p) ? yhi[2 * c] : (j == C.q) ? yhi[2 * c + 1] : ihi[C.ibase + j];
+    double a1 = __dsub_rn(lo, __dmul_rn(nin, fabs(lo)));
     double b1 = __dsub_rn(a1, tau);
     double l2 = __dsub_rn(b1, __dmul_rn(nu, fabs(b1)));
-    double c1 = __dadd_rn(hi, __dmul_rn(nu, fabs(hi)));
+    double c1 = __dadd_rn(hi, __dmul_rn(nin, fabs(hi)));
     double e1 = __dsub_rn(c1, tau);
     double h2 = __dadd_rn(e1, __dmul_rn(nu, fabs(e1)));
     double L, H;

@@ -1211,7 +1211,8 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
     CK(cudaMemsetAsync(h->bnA.p, 0, sizeof(BNode) * btot, h->stream));
     k_clu_child_starts<<<nblocks_for(nc, 64), 64, 0, h->stream>>>(
         cl, nc, h->reps.as<RepDesc>(), h->ss.as<ShiftState>(), h->cseg.as<long long>(), h->bnoff.as<long long>(), ilo,
-        ihi, h->ipool_lo.as<double>(), h->ipool_hi.as<double>(), h->bnA.as<BNode>(), repbase);
+        ihi, h->ipool_lo.as<double>(), h->ipool_hi.as<double>(), h->bnA.as<BNode>(), repbase,
+        h->yref_lo.as<double>(), h->yref_hi.as<double>(), h->sd ? 0x1p-53 : EPS_Y);
     launch_check(h);
     h->cur_nbmax = nbmax;  // chain-length hint for the segmented child counts
     int nrd = run_brackets<false>(h, (int)btot);

@@ -30,15 +30,26 @@ __global__ void k_build_q(const RepDesc *__restrict__ reps, const int *__restric
   const YElt *y = my + R.off;
   QElt *q = mq + R.off;
   // blockIdx.y splits the rows (a representation's rows are independent here)
+  // 16-byte loads and stores (YElt = 3 double2, QElt = 4 double2; both 16-byte aligned)
+  const double2 *y2 = reinterpret_cast<const double2 *>(y);
+  double2 *q2 = reinterpret_cast<double2 *>(q);
   for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < R.nb; i += blockDim.x * gridDim.y) {
-    dd d = ld_d(y + i), dl = ld_dl(y + i), dll = ld_dll(y + i);
+    const double2 vd = __ldg(y2 + 3LL * i), vdl = __ldg(y2 + 3LL * i + 1), vdll = __ldg(y2 + 3LL * i + 2);
+    dd d = dd_make(vd.x, vd.y), dl = dd_make(vdl.x, vdl.y), dll = dd_make(vdll.x, vdll.y);
     dd c2 = dd_mul(dl, dl);
-    dd gf = (i < R.nb - 1) ? dd_add(ld_d(y + i + 1), dll) : dd_from(0.0);
-    dd gb = (i > 0) ? dd_add(d, ld_dll(y + i - 1)) : d;
-    QElt e;
-    e.c2_hi = c2.hi; e.c2_lo = c2.lo; e.dl_hi = dl.hi; e.dl_lo = dl.lo;
-    e.gf_hi = gf.hi; e.gf_lo = gf.lo; e.gb_hi = gb.hi; e.gb_lo = gb.lo;
-    q[i] = e;
+    dd gf = dd_from(0.0), gb = d;
+    if (i < R.nb - 1) {
+      const double2 vn = __ldg(y2 + 3LL * (i + 1));
+      gf = dd_add(dd_make(vn.x, vn.y), dll);
+    }
+    if (i > 0) {
+      const double2 vp = __ldg(y2 + 3LL * (i - 1) + 2);
+      gb = dd_add(d, dd_make(vp.x, vp.y));
+    }
+    q2[4LL * i] = make_double2(c2.hi, c2.lo);
+    q2[4LL * i + 1] = make_double2(dl.hi, dl.lo);
+    q2[4LL * i + 2] = make_double2(gf.hi, gf.lo);
+    q2[4LL * i + 3] = make_double2(gb.hi, gb.lo);
   }
 }
 

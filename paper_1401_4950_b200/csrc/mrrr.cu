@@ -101,6 +101,7 @@ struct mrrr_ctx {
   bool neg_tma = true;  // x-NegCount with TMA-staged representation tiles (k_negcount_tma)
   bool grouped = true;  // child bisection with CTAs grouped by representation (k_negcount_grp)
   int seg_k = 8, seg_w = 128;  // segmented root NegCount: segments per chain, warm-up rows (k_negcount_seg)
+  bool zrc_child = true;       // ... also for child frames (MRRR_ZRC_CHILD=0: stored passes there)
   int zwin = 256;              // z recompute window of singletons accepted on an RQC-only pass (0: stored passes)
   int fuse_mmax = 2;           // host-driven segmented rounds fuse walk + update (k_seg_round) up to this depth
   bool rqi_seg = true;         // segmented RQI passes (kernels_rqi3.cuh); MRRR_RQISEG=0: the two-lane kernel only
@@ -901,7 +902,7 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
       }
       while (2 * K <= 32 && (long long)nb * 2 * (2 * K) <= h->rqi_threads && (nbmax - 1) >= 2 * (2 * K) * Wu) K *= 2;
       // z recompute window (k_zrc): root frames of the double/dd solve with the numerical support on
-      const bool zrc = h->zwin > 0 && !child && !h->sd && eps_support(h) > 0.0 && nbmax > 2LL * h->zwin;
+      const bool zrc = h->zwin > 0 && (!child || h->zrc_child) && !h->sd && eps_support(h) > 0.0 && nbmax > 2LL * h->zwin;
       if (zrc) {
         CK(h->zinb.ensure(sizeof(dd) * 2 * stride));
         CK(h->zrcb.ensure(sizeof(int) * 4));
@@ -1784,6 +1785,7 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_SEGMINLEN")) h->seg_minlen = atoi(s);
     if (const char *s = getenv("MRRR_FUSEM")) h->fuse_mmax = atoi(s);
     if (const char *s = getenv("MRRR_ZWIN")) h->zwin = std::max(0, atoi(s));
+    if (const char *s = getenv("MRRR_ZRC_CHILD")) h->zrc_child = atoi(s) != 0;
     if (const char *s = getenv("MRRR_ROUNDEV")) h->round_ev = atoi(s) != 0;
     if (const char *s = getenv("MRRR_EARLY_STOP")) { if (atoi(s)) h->flags |= MRRR_EARLY_STOP; }  // dev sweeps
     if (const char *s = getenv("MRRR_FULL_SUPPORT")) { if (atoi(s)) h->flags |= MRRR_FULL_SUPPORT; }

@@ -842,32 +842,33 @@ __global__ void __launch_bounds__(128) k_clu_build_seg(const Cluster *__restrict
                                                        const QElt *__restrict__ mq, long long poolbase, int nbmax,
                                                        int K, int Wu, SegG *seg) {
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  // a warp whose 32 threads all exist decides below, with all its lanes, whether it stores cooperatively
+  const bool warp_full = (g | 31) < (long long)ncl * K;
   if (g >= (long long)ncl * K) return;
   const int k = (int)(g / ncl), c = (int)(g % ncl);
   const ShiftState S = ss[c];
   SegG *o = seg + (long long)c * K + k;
-  if (!S.have_best) {
-    o->empty = 1;
-    o->ok = 1;
-    return;
-  }
   const RepDesc P = reps[cl[c].rep];
   const int nb = P.nb, steps = nb - 1;
-  int bk, ek, w0;
+  int bk = 0, ek = steps, w0 = 0;
+  bool live = S.have_best != 0;
   if (steps >= 2 * K * Wu) {
     const int L = (steps + K - 1) / K;
     bk = min(k * L, steps);
     ek = min(bk + L, steps);
     w0 = (k == 0) ? 0 : max(bk - Wu, 0);
-  } else {
-    if (k > 0) {
-      o->empty = 1;
-      o->ok = 1;
-      return;
-    }
-    bk = 0;
-    ek = steps;
-    w0 = 0;
+  } else if (k > 0) {
+    live = false;
+  }
+  bool coop = false;
+  if (warp_full) {  // every lane reaches these collectives (no lane has returned yet)
+    const int bk0 = __shfl_sync(0xffffffffu, bk, 0), ek0 = __shfl_sync(0xffffffffu, ek, 0);
+    coop = __all_sync(0xffffffffu, live && bk0 == bk && ek0 == ek);
+  }
+  if (!live) {
+    o->empty = 1;
+    o->ok = 1;
+    return;
   }
   const long long off = poolbase + (long long)c * nbmax;
   YElt *yc = my + off;
@@ -877,7 +878,23 @@ __global__ void __launch_bounds__(128) k_clu_build_seg(const Cluster *__restrict
   dd den = dd_sub(dd_make(__ldg(&q[w0].gb_hi), __ldg(&q[w0].gb_lo)), tau);
   dd din = den;
   bool ok = true;
-  for (int i = w0; i < bk; i++) den = clu_build_row(den, q, i, tau, nullptr, nullptr, ok);
+  // rows prefetched PFB ahead in a register ring (the parent rows are shared by the warp's lanes, L2-resident)
+  constexpr int PFB = 4;
+  QRow ring[PFB];
+#pragma unroll
+  for (int u = 0; u < PFB; u++) ring[u] = ld_qrow(q, min(w0 + u, steps - 1));
+  int slot = 0;
+  auto next_row = [&](int i) -> QRow {  // row i's data; refills its slot with row i + PFB
+    QRow cur = ring[0];
+#pragma unroll
+    for (int u = 0; u < PFB; u++) if (u == slot) cur = ring[u];
+    const QRow nx = ld_qrow(q, min(i + PFB, steps - 1));
+#pragma unroll
+    for (int u = 0; u < PFB; u++) if (u == slot) ring[u] = nx;
+    slot = (slot + 1 == PFB) ? 0 : slot + 1;
+    return cur;
+  };
+  for (int i = w0; i < bk; i++) den = clu_build_row_v(den, next_row(i), i, tau, nullptr, nullptr, ok, false);
   din = den;
   // the rows are staged in shared memory and written by bulk (TMA-engine) copies of BG-row runs: a warp's lanes
   // are different clusters, so plain stores scattered 32 partial lines per instruction (store-bound: C3's child
@@ -886,18 +903,45 @@ __global__ void __launch_bounds__(128) k_clu_build_seg(const Cluster *__restrict
   YElt *sy = reinterpret_cast<YElt *>(bsm) + threadIdx.x * 2 * BG;
   double2 *sx = reinterpret_cast<double2 *>(bsm + (size_t)blockDim.x * 2 * BG * sizeof(YElt)) + threadIdx.x * 2 * BG;
   int grp = 0, ng = 0;
-  for (int i = bk; i < ek; i++) {
-    den = clu_build_row(den, q, i, tau, sy + grp * BG + ng, sx + grp * BG + ng, ok, true);
-    if (++ng == BG || i + 1 == ek) {
-      const int low = i - ng + 1;
-      bulk_store(yc + low, sy + grp * BG, (unsigned)(ng * sizeof(YElt)));
-      bulk_store(xc + low, sx + grp * BG, (unsigned)(ng * sizeof(double2)));
-      grp ^= 1;
-      ng = 0;
-      bulk_wait_read<2>();  // the other group's two stores have read their rows
+  // a full warp on one row range (the usual case: 32 sibling clusters of one frame length on segment k) stores
+  // cooperatively: every 2 BG rows, one 16-byte store per lane writes one cluster's 2 BG YElt rows (6 BG chunks)
+  // and its 2 BG x-rows (2 BG chunks) -- 32 contiguous runs per 32 store instructions instead of 64 small
+  // bulk copies per lane (those ran the 8.6 GB of C3's child rows at 1.7 TB/s)
+  const int lane = threadIdx.x & 31;
+  constexpr int CG = 2 * BG;  // rows per cooperative store (the two staging groups as one buffer)
+  if (coop) {
+    const long long offl0 = poolbase + (long long)c * nbmax;
+    for (int i = bk; i < ek; i++) {
+      den = clu_build_row_v(den, next_row(i), i, tau, sy + ng, sx + ng, ok, true);
+      if (++ng == CG || i + 1 == ek) {
+        const int low = i - ng + 1;
+        __syncwarp();
+        const int ny = 3 * ng;  // 16-byte chunks of the YElt rows (48 B each); then ng chunks of x-rows
+        for (int l = 0; l < 32; l++) {
+          const long long offl = __shfl_sync(0xffffffffu, offl0, l);
+          const double2 *src_y = reinterpret_cast<const double2 *>(sy - (lane - l) * 2 * BG);
+          const double2 *src_x = sx - (lane - l) * 2 * BG;
+          if (lane < ny) reinterpret_cast<double2 *>(my + offl + low)[lane] = src_y[lane];
+          else if (lane < ny + ng) (mx + offl + low)[lane - ny] = src_x[lane - ny];
+        }
+        __syncwarp();
+        ng = 0;
+      }
     }
+  } else {
+    for (int i = bk; i < ek; i++) {
+      den = clu_build_row_v(den, next_row(i), i, tau, sy + grp * BG + ng, sx + grp * BG + ng, ok, true);
+      if (++ng == BG || i + 1 == ek) {
+        const int low = i - ng + 1;
+        bulk_store(yc + low, sy + grp * BG, (unsigned)(ng * sizeof(YElt)));
+        bulk_store(xc + low, sx + grp * BG, (unsigned)(ng * sizeof(double2)));
+        grp ^= 1;
+        ng = 0;
+        bulk_wait_read<2>();  // the other group's two stores have read their rows
+      }
+    }
+    bulk_wait_all();
   }
-  bulk_wait_all();
   if (ek == steps) {
     ok &= isfinite(den.hi) && isfinite(den.lo);
     YElt e;

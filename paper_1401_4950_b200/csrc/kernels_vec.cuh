@@ -222,6 +222,48 @@ __global__ void k_clu_select_multi(const Cluster *__restrict__ cl, int ncl, cons
 // Child rep id = repbase + c, data at pool offset poolbase + c * nbmax.
 // one row of the fast child build: l+(i) = dl(i)/d+(i) and c2(i)/d+(i) from the reciprocal pair of d+(i),
 // the child's y-row (d, dl, dll) and x-row (d, dll); returns d+(i+1) (the y_step recurrence)
+// the row's parent data (c2, dl, gf of q[i]) as three 16-byte values: callers that run a chain of rows load them
+// a few rows ahead (the chain's dependent steps otherwise wait on each row's load: stall_long_sb 38 % on C3)
+struct QRow { double2 c2, dl, gf; };
+__device__ __forceinline__ QRow ld_qrow(const QElt *__restrict__ q, int i) {
+  const double2 *p = reinterpret_cast<const double2 *>(q + i);
+  QRow r;
+  r.c2 = __ldg(p);
+  r.dl = __ldg(p + 1);
+  r.gf = __ldg(p + 2);
+  return r;
+}
+__device__ __forceinline__ dd clu_build_row_v(dd den, const QRow &qr, int i, dd tau, YElt *yc, double2 *xc, bool &ok,
+                                              bool staged) {
+  const double b = den.hi;
+  ok &= (fabs(b) > 0x1p-1000) && (fabs(b) < 0x1p1000);
+  const double r = rcp_seed(b);
+  double ee = __fma_rn(-b, r, 1.0);
+  ee = __fma_rn(ee, ee, ee);
+  const double r1 = __fma_rn(r, ee, r);
+  const double e2 = __fma_rn(-b, r1, 1.0);
+  const double r2 = __fma_rn(r1, e2, r1);
+  const dd dlp = dd_make(qr.dl.x, qr.dl.y);
+  const dd c2 = dd_make(qr.c2.x, qr.c2.y);
+  double h = __dmul_rn(dlp.hi, r1), t = __fma_rn(-h, b, dlp.hi);
+  t = __fma_rn(-h, den.lo, __dadd_rn(t, dlp.lo));
+  const dd out = fast_two_sum(h, __dmul_rn(t, r2));  // l+(i) = dl(i) / d+(i)
+  h = __dmul_rn(c2.hi, r1);
+  t = __fma_rn(-h, b, c2.hi);
+  t = __fma_rn(-h, den.lo, __dadd_rn(t, c2.lo));
+  const dd Pq = dd_make(h, __dmul_rn(t, r2));        // c2(i) / d+(i)
+  if (yc) {
+    const dd dl = dd_mul(den, out);
+    const dd dll = dd_mul(dl, out);
+    YElt e;
+    e.d_hi = den.hi; e.d_lo = den.lo; e.dl_hi = dl.hi; e.dl_lo = dl.lo; e.dll_hi = dll.hi; e.dll_lo = dll.lo;
+    const double dx = den.hi, lx = out.hi;
+    const double2 xe = make_double2(dx, __dmul_rn(__dmul_rn(dx, lx), lx));
+    if (staged) { *yc = e; *xc = xe; }  // shared-memory staging slot of row i
+    else { yc[i] = e; xc[i] = xe; }
+  }
+  return dd_sub_nf(dd_sub_nf(dd_make(qr.gf.x, qr.gf.y), tau), Pq);
+}
 __device__ __forceinline__ dd clu_build_row(dd den, const QElt *__restrict__ q, int i, dd tau, YElt *yc, double2 *xc,
                                             bool &ok, bool staged = false) {
   const double b = den.hi;

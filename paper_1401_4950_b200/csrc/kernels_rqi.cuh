@@ -647,8 +647,17 @@ __global__ void __launch_bounds__(128) k_zwrite_chunk(const Singleton *__restric
     }
     cp_wait<0>();  // drain the prefetch of the next tile
     __syncwarp();
-    if (phase != 0)
-      for (int mm = t * ZT + lane; mm < len; mm += 32) Zc[side ? r + 1 + mm : r - 1 - mm] = 0.0;
+    if (phase != 0 && t * ZT < len) {
+      // rows past the support: one contiguous range [a, b) of the column, stored as 16-byte zeros
+      const int a = side ? r + 1 + t * ZT : 0, b = side ? r + 1 + len : r - t * ZT;
+      double *z0 = Zc + a;
+      const int head = (reinterpret_cast<uintptr_t>(z0) & 15) ? 1 : 0, cnt = b - a;
+      if (head && lane == 0) z0[0] = 0.0;
+      double2 *z2 = reinterpret_cast<double2 *>(z0 + head);
+      const int n2 = (cnt - head) >> 1;
+      for (int u = lane; u < n2; u += 32) z2[u] = make_double2(0.0, 0.0);
+      if (((cnt - head) & 1) && lane == 0) z0[cnt - 1] = 0.0;
+    }
     return cut;
   };
   if (!win) {

@@ -377,7 +377,7 @@ __global__ void k_clu_child_starts(const Cluster *__restrict__ cl, int ncl, cons
   const double nuy = __dmul_rn(__dmul_rn(100.0, (double)nb), eps_y);
   double tau = S.best_tau;
   long long base = cseg[c] - (C.p - 1);  // child ibase
-  double lpm = ilo[C.ibase + C.p - 1];
+  const double lpm = (C.p > 1) ? ilo[C.ibase + C.p - 1] : NAN;  // (p = 1 has no left neighbour: no read before ilo)
   if (C.p > 1 && !isnan(lpm)) {
     clo[base + C.p - 1] = __dsub_rn(lpm, tau);
     chi[base + C.p - 1] = __dsub_rn(ihi[C.ibase + C.p - 1], tau);

@@ -109,6 +109,14 @@ struct mrrr_ctx {
   long long rqi_threads = 131072;  // adaptive RQI segment count target (threads per segmented pass)
   bool rqi_seg_child = true;   // segmented RQI for child-frame singletons (dd twist search)
   int segchild_min = 8;        // ... when the level has at least this many singletons per child representation
+  // deferred tails: a child level whose singletons go to the two-lane kernel only (few singletons per child) runs
+  // it on a side stream while the levels above finish (MRRR_DEFER_TAIL=0: in order on the solve stream)
+  bool defer_tail = true;
+  bool synccheck = false;  // MRRR_SYNCCHECK: synchronise after every launch check (fault localisation)
+  long long tail_max_bytes = 1LL << 30;  // largest two-lane workspace a deferred tail may hold (3 dd planes)
+  cudaStream_t s_tail = nullptr;
+  cudaEvent_t ev_tail_in = nullptr, ev_tail_done = nullptr;
+  bool tail_pending = false;
   long long twdd_root_max = 0;  // root blocks up to this size take the dd twist search (MRRR_TWDD_ROOT)
   bool rqi_bulk = true;        // k_fixed_chunk stores the factors by bulk copies of staged 8-row runs
   int segy_k = 16, segy_w = 128;  // segmented y-NegCount, shift growth, child build (MRRR_SEGYK=1: unsegmented)
@@ -148,6 +156,9 @@ struct mrrr_ctx {
   Buf repoff, repcur, repcta;             // representation-grouped rounds
   Buf segout, rnd;                        // segmented NegCount; per-round device counters
   Buf gpart;                              // k_root_gersh partial bounds
+  Buf tail_ws, tail_sing, tail_zmeta;     // deferred tail: two-lane planes, its singleton list, its z metadata
+  static constexpr int LVL_MAX = 64;      // per-level cluster lists and singleton copies (kept across solves: a
+  Buf lvl_L[LVL_MAX], lvl_NX[LVL_MAX], lvl_SG[LVL_MAX];  // cudaFree would wait for a deferred tail)
   Buf segouty, segfby, segoutx, segoutg;  // segmented y-NegCount / many-representation x-NegCount / growth
   Buf rqst, rqrec, hand;                  // segmented RQI state, segment records, handed-over singletons
   Buf nodesA, nodesB, counts, ex, excounts, exmap, bnA, bnB, sing, clusA, clusB, ss, gval, valid, cseg, bnoff,
@@ -450,9 +461,17 @@ int seg_base_k(mrrr_t h, long long nb) {
   return (nb - 1) >= 2LL * h->seg_k * h->seg_w ? h->seg_k : 1;
 }
 
-void launch_check(mrrr_t h) {
+void launch_check(mrrr_t h, int line = __builtin_LINE()) {
   h->host_launches++;
   CK(cudaGetLastError());
+  if (h->synccheck) {  // MRRR_SYNCCHECK (debugging): a fault is reported at the launch site that caused it
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) {
+      g_last_cuda_error = std::string("kernels launched before mrrr.cu:") + std::to_string(line) + ": " +
+                          cudaGetErrorString(e);
+      throw Err{MRRR_ERR_CUDA};
+    }
+  }
 }
 
 // record the next pool event on the stream; returns its index (the pool grows on first use)
@@ -869,7 +888,7 @@ void l2_pin_reps(mrrr_t h, bool on) {
 }
 
 void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long ldz, bool allow_seg,
-             bool child = false) {
+             bool child = false, const Singleton *list = nullptr) {
   if (ns <= 0) return;
   l2_pin_reps(h, true);
   // workspace per singleton: 3 dd planes (the two-lane kernel's P0, P1, P2; the segmented passes use the first
@@ -885,7 +904,7 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
     long long nb = std::min<long long>(batch, ns - b0);
     const int rq0 = tev_rec(h);
     CK(h->zmeta.ensure(sizeof(ZMeta) * stride));
-    const Singleton *sgb = h->sing.as<Singleton>() + b0;
+    const Singleton *sgb = (list ? list : h->sing.as<Singleton>()) + b0;
     int nold = (int)nb;
     if (h->rqi_seg && allow_seg) {
       // segmented passes (kernels_rqi3.cuh); singletons they hand over go through k_rqi2 below
@@ -1032,6 +1051,53 @@ void run_rqi(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long 
   l2_pin_reps(h, false);
 }
 
+// the solve stream waits for the deferred tail (before anything that could overwrite what the tail reads: the
+// representation slots of the next chunk, the end of the solve)
+void join_tail(mrrr_t h) {
+  if (h->tail_pending) CK(cudaStreamWaitEvent(h->stream, h->ev_tail_done, 0));
+}
+
+// two-lane workspace of a deferred tail of ns singletons on frames of up to nbmax rows
+long long tail_bytes(int ns, long long nbmax) {
+  const long long stride = ((long long)ns + 31) / 32 * 32;
+  return 3LL * stride * std::max<long long>(nbmax, 1) * (long long)sizeof(dd);
+}
+
+// a child level's singletons that go to the two-lane kernel only (run_rqi with allow_seg false): the same two
+// launches as run_rqi's k_rqi2 branch, on the side stream after the solve stream's current work (the child
+// representations), with their own workspace and a copy of the singleton list; the levels above go on meanwhile
+void launch_tail(mrrr_t h, int ns, long long nbmax, double *W, double *Z, long long ldz) {
+  if (!h->s_tail) {
+    CK(cudaStreamCreate(&h->s_tail));
+    CK(cudaEventCreateWithFlags(&h->ev_tail_in, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_tail_done, cudaEventDisableTiming));
+  }
+  if (h->tail_pending) CK(cudaStreamSynchronize(h->s_tail));  // its buffers are reused below
+  h->tail_pending = false;
+  const long long stride = ((long long)ns + 31) / 32 * 32;
+  CK(h->tail_ws.ensure((size_t)tail_bytes(ns, nbmax)));
+  CK(h->tail_sing.ensure(sizeof(Singleton) * stride));
+  CK(h->tail_zmeta.ensure(sizeof(ZMeta) * stride));
+  CK(cudaMemcpyAsync(h->tail_sing.p, h->sing.p, sizeof(Singleton) * ns, cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaEventRecord(h->ev_tail_in, h->stream));
+  CK(cudaStreamWaitEvent(h->s_tail, h->ev_tail_in, 0));
+  const bool diag = (h->flags & MRRR_KEEP_DIAG) != 0;
+  const Singleton *sgb = h->tail_sing.as<Singleton>();
+  k_rqi2<<<nblocks_for(2 * ns, 64), 64, 64 * MRRR_RQI_RING * sizeof(RingSlot), h->s_tail>>>(
+      sgb, ns, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->mq.as<QElt>(), h->tail_ws.as<dd>(), stride, nbmax, W,
+      h->tail_zmeta.as<ZMeta>(), diag ? h->ddepth.as<int>() : nullptr, diag ? h->dflo.as<double>() : nullptr,
+      diag ? h->dfhi.as<double>() : nullptr, h->stats.as<long long>(), h->fault, h->sd ? 1 : 0,
+      h->sd ? 0x1p-24 : EPS_X, h->sd ? 0x1p-53 : EPS_Y);
+  CK(cudaGetLastError());
+  k_zwrite_chunk<<<nblocks_for(ns, 4), 128, 0, h->s_tail>>>(
+      sgb, ns, h->reps.as<RepDesc>(), h->my.as<YElt>(), h->tail_ws.as<dd>() + 2 * stride * nbmax, nbmax,
+      h->tail_zmeta.as<ZMeta>(), Z, ldz, eps_support(h));
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(h->ev_tail_done, h->s_tail));
+  h->tail_pending = true;
+  h->host_launches += 2;  // (not in the RQI phase events: it overlaps other phases)
+}
+
 struct ClusterLevel {
   int ncl;
 };
@@ -1049,16 +1115,25 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
   long long per_child = nbmax * (long long)(sizeof(double2) + sizeof(YElt));
   long long budget = std::max<long long>(per_child, h->ws_limit / 4 - pool_top * (long long)(sizeof(double2) + sizeof(YElt)));
   int chunk = (int)std::max<long long>(1, std::min<long long>(ncl, budget / per_child));
+  const bool keep = level < mrrr_ctx::LVL_MAX;  // per-level buffers kept in the handle (no cudaFree mid-solve)
   for (int c0 = 0; c0 < ncl; c0 += chunk) {
     int nc = std::min(chunk, ncl - c0);
+    join_tail(h);  // a deferred tail of the previous chunk reads representation slots this chunk overwrites
     // own copy of this chunk's cluster list (device list buffers are reused by recursion)
-    Buf L;
+    Buf Lloc;
+    Buf &L = keep ? h->lvl_L[level] : Lloc;
     CK(L.ensure(sizeof(Cluster) * nc));
     CK(cudaMemcpyAsync(L.p, hl.data() + c0, sizeof(Cluster) * nc, cudaMemcpyHostToDevice, h->stream));
     Cluster *cl = L.as<Cluster>();
     // grow the pools (keeping live data): child reps, their data, interval segments
     int repbase = rep_top;
     long long poolbase = pool_top;
+    if (h->tail_pending) {  // a reallocated pool must not be freed under a running tail
+      const size_t pe = (size_t)(poolbase + (long long)nc * nbmax);
+      if (h->reps.cap < sizeof(RepDesc) * (size_t)(repbase + nc) || h->mx.cap < sizeof(double2) * pe ||
+          h->my.cap < sizeof(YElt) * pe || h->mq.cap < sizeof(QElt) * pe)
+        CK(cudaStreamSynchronize(h->s_tail));
+    }
     CK(h->reps.grow_keep(sizeof(RepDesc) * (size_t)(repbase + nc), sizeof(RepDesc) * (size_t)repbase, h->stream));
     CK(h->mx.grow_keep(sizeof(double2) * (size_t)(poolbase + (long long)nc * nbmax),
                        sizeof(double2) * (size_t)poolbase, h->stream));
@@ -1222,7 +1297,8 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
     h->cur_nbmax = 0;
     // (f) reclassify
     CK(h->sing.ensure(sizeof(Singleton) * std::max<long long>(btot, 1)));
-    Buf NX;
+    Buf NXloc;
+    Buf &NX = keep ? h->lvl_NX[level] : NXloc;
     CK(NX.ensure(sizeof(Cluster) * std::max<long long>(btot, 1)));
     zero_counters(h);
     k_clu_classify<<<nblocks_for(nc, 64), 64, 0, h->stream>>>(
@@ -1237,12 +1313,32 @@ void process_clusters(mrrr_t h, Cluster *list_dev, int ncl, int rep_top, long lo
     // by enough singletons for their row loads to coincide (else each lane streams its own representation
     // from HBM and the two-lane kernel is faster: measured C3, 2 singletons per child, vs C4, up to 256)
     // (single/double: always the segmented passes -- their fixed passes run in binary64, k_rqi2 in dd)
-    run_rqi(h, ns, nbmax, W, Z, ldz, h->sd || (h->rqi_seg_child && ns >= (long long)h->segchild_min * nc), true);
-    process_clusters(h, NX.as<Cluster>(), nnx, repbase + nc, poolbase + (long long)nc * nbmax, ipool_top + stot, nbmax,
-                     true, W, Z, ldz, kout, level + 1);
+    const bool segq = h->sd || (h->rqi_seg_child && ns >= (long long)h->segchild_min * nc);
+    if (ns > 0 && !segq && h->defer_tail && keep && tail_bytes(ns, nbmax) <= h->tail_max_bytes) {
+      // few singletons per child, two-lane kernel only: a deferred tail on the side stream, overlapping the
+      // deeper levels and the RQI of the levels above (C4: the depth-2 pair under the depth-1 passes)
+      launch_tail(h, ns, nbmax, W, Z, ldz);
+      process_clusters(h, NX.as<Cluster>(), nnx, repbase + nc, poolbase + (long long)nc * nbmax, ipool_top + stot,
+                       nbmax, true, W, Z, ldz, kout, level + 1);
+    } else if (ns > 0 && nnx > 0 && h->defer_tail && keep) {
+      // deeper levels first (a tail found there overlaps this level's passes), then this level's singletons
+      // from a copy of their list (the recursion rewrites h->sing); the results do not depend on the order
+      Buf &SG = h->lvl_SG[level];
+      CK(SG.ensure(sizeof(Singleton) * ns));
+      CK(cudaMemcpyAsync(SG.p, h->sing.p, sizeof(Singleton) * ns, cudaMemcpyDeviceToDevice, h->stream));
+      process_clusters(h, NX.as<Cluster>(), nnx, repbase + nc, poolbase + (long long)nc * nbmax, ipool_top + stot,
+                       nbmax, true, W, Z, ldz, kout, level + 1);
+      run_rqi(h, ns, nbmax, W, Z, ldz, segq, true, SG.as<Singleton>());
+    } else {
+      run_rqi(h, ns, nbmax, W, Z, ldz, segq, true);
+      process_clusters(h, NX.as<Cluster>(), nnx, repbase + nc, poolbase + (long long)nc * nbmax, ipool_top + stot,
+                       nbmax, true, W, Z, ldz, kout, level + 1);
+    }
     CK(cudaStreamSynchronize(h->stream));
-    NX.release();
-    L.release();
+    if (!keep) {
+      NX.release();
+      L.release();
+    }
   }
 }
 
@@ -1694,6 +1790,7 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
     CK(L0.ensure(sizeof(Cluster) * ncl));
     CK(cudaMemcpyAsync(L0.p, h->clusA.p, sizeof(Cluster) * ncl, cudaMemcpyDeviceToDevice, st));
     process_clusters(h, L0.as<Cluster>(), ncl, nblk, n, 0, nbmax, false, W, Z, ldz, kout, 0);
+    join_tail(h);  // W and Z columns of a deferred tail are done before anything reads them
     L0.release();
   }
   if (!single || n == 1) {
@@ -1781,6 +1878,8 @@ int mrrr_init(mrrr_t *out, const mrrr_opts *o) {
     if (const char *s = getenv("MRRR_TWDD_ROOT")) h->twdd_root_max = atoll(s);
     if (const char *s = getenv("MRRR_RQISEGCHILD")) h->rqi_seg_child = atoi(s) != 0;
     if (const char *s = getenv("MRRR_SEGCHILDMIN")) h->segchild_min = atoi(s);
+    if (const char *s = getenv("MRRR_DEFER_TAIL")) h->defer_tail = atoi(s) != 0;
+    if (const char *s = getenv("MRRR_SYNCCHECK")) h->synccheck = atoi(s) != 0;
     if (const char *s = getenv("MRRR_SEGTHREADS")) h->seg_threads = atoll(s);
     if (const char *s = getenv("MRRR_SEGMINLEN")) h->seg_minlen = atoi(s);
     if (const char *s = getenv("MRRR_FUSEM")) h->fuse_mmax = atoi(s);
@@ -2225,6 +2324,20 @@ int mrrr_destroy(mrrr_t h) {
                  &h->hd, &h->he, &h->hW, &h->hZ, &h->zmeta, &h->hd2,
                  &h->sdin, &h->sdW, &h->sdZ, &h->sdhin, &h->sdhW, &h->sdhZ, &h->segsd};
   for (Buf *b : bufs) b->release();
+  if (h->s_tail) {
+    cudaStreamSynchronize(h->s_tail);
+    cudaStreamDestroy(h->s_tail);
+    cudaEventDestroy(h->ev_tail_in);
+    cudaEventDestroy(h->ev_tail_done);
+  }
+  h->tail_ws.release();
+  h->tail_sing.release();
+  h->tail_zmeta.release();
+  for (int l = 0; l < mrrr_ctx::LVL_MAX; l++) {
+    h->lvl_L[l].release();
+    h->lvl_NX[l].release();
+    h->lvl_SG[l].release();
+  }
   for (auto &ev : h->ev) cudaEventDestroy(ev);
   for (auto &ev : h->tev) cudaEventDestroy(ev);
   if (h->comm && nccl().ok) nccl().destroy(h->comm);

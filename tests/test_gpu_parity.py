@@ -355,7 +355,8 @@ def test_division_fast_path_is_ieee(torch_cuda):
                                  {"MRRR_RQIBULK": "0"}, {"MRRR_SEGCH2": "1000000"}, {"MRRR_SEGTHREADS": "262144"},
                                  {"MRRR_SEGYK": "1"}, {"MRRR_SEGYW": "8"}, {"MRRR_SEGXK": "1"}, {"MRRR_SEGXK": "8", "MRRR_SEGXW": "8"},
                                  {"MRRR_DEVSTABLE": "0"}, {"MRRR_DEVROUNDS": "1"}, {"MRRR_RQISEGCHILD": "0"},
-                                 {"MRRR_SEGCHILDMIN": "0"}, {"MRRR_RECSTAGE": "1"}, {"MRRR_TWDD_ROOT": "100000"}])
+                                 {"MRRR_SEGCHILDMIN": "0"}, {"MRRR_RECSTAGE": "1"}, {"MRRR_TWDD_ROOT": "100000"},
+                                 {"MRRR_DEFER_TAIL": "0"}])
 def test_bisection_schedules_are_bit_identical(torch_cuda, env, monkeypatch):
     # every evaluation schedule (k-section budget, TMA staging, representation-grouped child rounds, guided
     # tube rounds) must reproduce the oracle's sequential Alg. Bisection intervals bit for bit (rule W)

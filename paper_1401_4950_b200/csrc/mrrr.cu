@@ -1393,6 +1393,7 @@ int solve(mrrr_t h, const double *d, const double *e, long long n, long long il,
   CK(h->starts.ensure(sizeof(int) * (n + 2)));
   CK(h->scal.ensure(64));
   CK(h->cnt.ensure(sizeof(int) * C_NCOUNTERS));
+  if (h->tail_pending) CK(cudaStreamSynchronize(h->s_tail));  // (a solve that threw may have left one running)
   CK(h->stats.ensure(sizeof(long long) * ST_N));
   CK(cudaMemsetAsync(h->stats.p, 0, sizeof(long long) * ST_N, st));
   CK(cudaEventRecord(h->ev[0], st));

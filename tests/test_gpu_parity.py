@@ -427,3 +427,31 @@ def test_eig_dist_two_ranks(torch_cuda):
                        timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("DIST_OK") == 2
+
+
+@pytest.mark.gpu
+def test_deferred_tails_chunked_levels_bit_identical(torch_cuda, monkeypatch):
+    # deferred tails (two-lane child levels on the side stream): a workspace limit
+    # that splits the root clusters into chunks of ~10 (the solve stream waits for each chunk's tail before the
+    # next chunk rewrites the representation slots) and many RQI batches; W and Z equal the unchunked solve and
+    # the in-order schedule (MRRR_DEFER_TAIL=0) bit for bit, and the integers / tolerances match the oracle
+    import paper_1401_4950_b200 as m
+    d, e = mi.glued_wilkinson(8, 100, 1e-10)
+    n = d.size
+    per_child = n * (16 + 48)  # double2 + YElt rows of one child representation
+    runs = []
+    for ws, defer in ((0, "1"), (4 * 11 * per_child, "1"), (4 * 11 * per_child, "0")):
+        monkeypatch.setenv("MRRR_DEFER_TAIL", defer)
+        s = m.Solver(keep_diag=True, ws_limit=ws)
+        W, Z = s.eig(torch_cuda.from_numpy(d).cuda(), torch_cuda.from_numpy(e).cuda())
+        torch_cuda.cuda.synchronize()
+        runs.append((W.cpu().numpy(), Z.cpu().numpy(), s.stats(), s.diag() if ws == 0 else None))
+        s.close()
+    for W, Z, st, _ in runs[1:]:
+        assert np.array_equal(W, runs[0][0]) and np.array_equal(Z, runs[0][1])
+        assert st["failed"] == 0
+    r = oracle.mrrr(d, e)
+    g = dict(W=runs[0][0], Z=runs[0][1], stats=runs[0][2], diag=runs[0][3])
+    check_integers(g, r)
+    tn = max(abs(r.W[0]), abs(r.W[-1]))
+    check_tol(d, e, g["W"], g["Z"], r.W, tn)

@@ -112,7 +112,9 @@ def ncu_traffic(kernel_prefix: str, workload: str):
             continue
         if js.get("workload") != workload:
             continue
-        ls = [e for e in js.get("launches", []) if e.get("kernel", "").startswith(kernel_prefix)]
+        # a prefix ending in "<" names one kernel exactly (template or not): k_root, not k_root_nodes
+        ls = [e for e in js.get("launches", []) if e.get("kernel", "").startswith(kernel_prefix)
+              or (kernel_prefix.endswith("<") and e.get("kernel", "") == kernel_prefix[:-1])]
         v = [e["dram_bytes"] for e in ls]
         if v:
             pipe = [e["fp64_pipe_pct"] for e in ls if "fp64_pipe_pct" in e]
@@ -306,8 +308,14 @@ def main():
             nl = tphase["negcount_launches"]
             f = fl.negcount_flops(stats, n) / nl
             f_sv = fl.negcount_flops(stats, n, wdiv_survey) / nl
-            cands.append(("k_negcount_seg (x-NegCount rounds: segmented root chains; child rounds k_negcount_seg_xg/tma)",
-                          "k_negcount", launch_ms, f, f_sv))
+            # segmented rounds need at least two segments of seg_minlen = 512 rows per chain half (mrrr.cu,
+            # seg_base_k): below n = 2049 (C1) the root rounds are the unsegmented chains of k_root
+            if n >= 2049:
+                cands.append(("k_negcount_seg (x-NegCount rounds: segmented root chains; child rounds k_negcount_seg_xg/tma)",
+                              "k_negcount", launch_ms, f, f_sv))
+            else:
+                cands.append(("k_root (x-NegCount rounds: one unsegmented chain per lane, n below the segmenting threshold)",
+                              "k_root<", launch_ms, f, f_sv))
         if rq_n:
             launch_ms = rq_ms / rq_n
             f = fl.rqi_flops(stats, n, sd=SD) / nrq
